@@ -1,0 +1,237 @@
+/*
+ * pgcp_b200.h -- C ABI of the B200-native PGCP hot path (libpgcp_b200.so).
+ *
+ * The reference (`/root/reference/pkg/src/pgcp`) is pure Python: its only
+ * "plugin seam" is the Python function surface re-exported in
+ * `pkg/src/pgcp/__init__.py:7-26` plus the per-subdomain batch seam
+ * `pipeline._run_tasks` (`pipeline.py:105-109`). This header is the native
+ * boundary under the drop-in Python package `paper_1903_12359_b200`, which
+ * binds it with ctypes. Every entry point names the
+ * reference code it replaces.
+ *
+ * Conventions
+ *   - every function returns an int status (PGCP_OK or a PGCP_E_* code);
+ *     pgcp_last_error() returns the thread-local message of the last failure;
+ *   - pointers documented "device" are CUDA device pointers, "host" are host;
+ *   - `stream` is a cudaStream_t passed as void*; all device work of a call is
+ *     enqueued on it. Calls that must report data-dependent sizes or errors
+ *     synchronise that stream before returning (documented per call);
+ *   - complex values are interleaved (re, im) doubles (numpy complex128);
+ *   - no PyTorch types cross this boundary.
+ */
+#ifndef PGCP_B200_H
+#define PGCP_B200_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define PGCP_API __attribute__((visibility("default")))
+#else
+#define PGCP_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PGCP_ABI_VERSION 1
+
+/* status codes -> Python exceptions (paper_1903_12359_b200/_native.py) */
+#define PGCP_OK 0
+#define PGCP_E_INVALID 1    /* bad argument                       -> ValueError      */
+#define PGCP_E_MESH 2       /* mesh.py:15 MeshError                                   */
+#define PGCP_E_PARTITION 3  /* partition.py:21 PartitionError                         */
+#define PGCP_E_SOLVE 4      /* flatten.py:24 SolveError (contract violation)          */
+#define PGCP_E_NOCONV 5     /* SolveError: PCG did not reach rtol within maxit         */
+#define PGCP_E_WELD 6       /* welding.py:35 WeldError                                */
+#define PGCP_E_CUDA 7       /* CUDA runtime failure                  -> RuntimeError    */
+#define PGCP_E_VALIDATION 8 /* pipeline.py:32 ValidationError                         */
+
+typedef struct pgcp_batch pgcp_batch;
+
+PGCP_API int pgcp_abi_version(void);
+PGCP_API const char* pgcp_last_error(void);
+
+/* -------------------------------------------------------------------------
+ * Batch of disk-type submeshes of one parent mesh, device resident.
+ *
+ * pgcp_batch_create replaces partition.py:94-137 (partition_mesh: face
+ * adjacency minus cut edges -> connected components ordered by minimum face,
+ * sorted vertex maps, disk-type check) and mesh.py:144-173 (boundary_loops:
+ * walk from the smallest boundary vertex, surface on the left). It also
+ * evaluates the parent mesh topology of mesh.py:206-223 (validate_topology).
+ *   V     device, n*3 float64     F     device, m*3 int32
+ *   cuts  device, ncuts*2 int64 parent vertex pairs (NULL iff ncuts == 0)
+ *   flags PGCP_BATCH_NO_CUTS: single domain = the whole mesh (pipeline.py:143-150)
+ * Synchronises `stream`. Errors: PGCP_E_MESH (bad indices, non-manifold or
+ * inconsistently oriented edges, pinched boundaries), PGCP_E_PARTITION
+ * (duplicate/non-edge cuts, non-disk component).
+ */
+#define PGCP_BATCH_NO_CUTS 1u
+PGCP_API int pgcp_batch_create(const double* V, const int32_t* F, int64_t n, int64_t m,
+                      const int64_t* cuts, int64_t ncuts, uint32_t flags,
+                      void* stream, pgcp_batch** out);
+PGCP_API int pgcp_batch_destroy(pgcp_batch* b);
+
+/* host int64 info[PGCP_INFO_COUNT] */
+#define PGCP_INFO_K 0            /* number of submeshes                          */
+#define PGCP_INFO_SUM_N 1        /* total local vertices (seam copies counted)   */
+#define PGCP_INFO_SUM_NB 2       /* total boundary-loop vertices                 */
+#define PGCP_INFO_NNZ_L 3        /* total nnz of the per-submesh Laplacians      */
+#define PGCP_INFO_PARENT_CHI 4   /* Euler characteristic of the parent mesh      */
+#define PGCP_INFO_PARENT_LOOPS 5 /* parent boundary loops (-2: "two or more")    */
+#define PGCP_INFO_N 6
+#define PGCP_INFO_M 7
+#define PGCP_INFO_BAD_COMP 8     /* first non-disk component (-1 if none)        */
+#define PGCP_INFO_COUNT 16
+PGCP_API int pgcp_batch_info(const pgcp_batch* b, int64_t* info, int ninfo);
+
+/* device pointer and element count of an internal array */
+#define PGCP_ARR_FACE_COMP 0   /* int32 [m]       parent face -> submesh            */
+#define PGCP_ARR_VERT_OFF 1    /* int64 [K+1]     local-vertex offsets              */
+#define PGCP_ARR_VMAP 2        /* int32 [sum_n]   local -> parent vertex (sorted)   */
+#define PGCP_ARR_LOOP_OFF 3    /* int64 [K+1]     boundary-loop offsets             */
+#define PGCP_ARR_LOOP 4        /* int32 [sum_nb]  loop, local indices               */
+#define PGCP_ARR_L_ROWPTR 5    /* int64 [sum_n+1] CSR rows (global, concatenated)   */
+#define PGCP_ARR_L_COL 6       /* int32 [nnz]     CSR columns, LOCAL indices        */
+#define PGCP_ARR_L_VAL 7       /* f64   [nnz]                                      */
+#define PGCP_ARR_W3 8          /* f64   [3m]      half-cotangent per face corner    */
+#define PGCP_ARR_PINS 9        /* int32 [2K]      default pins (local)              */
+PGCP_API int pgcp_batch_array(const pgcp_batch* b, int which, void** ptr, int64_t* count);
+
+/* Local faces of every submesh, faces in increasing parent-face order
+ * (partition.py:121-126 `remap[mesh.faces[fidx]]`).
+ *   face_off host int64 [K+1]; faces device int32 [m*3]. Synchronises. */
+PGCP_API int pgcp_batch_local_faces(pgcp_batch* b, int64_t* face_off, int32_t* faces, void* stream);
+
+/* K1 + K2: per-face cotangent weights (flatten.py:39-57) and the canonical
+ * CSR cotangent Laplacian of every submesh (flatten.py:61: rows sorted,
+ * duplicates summed, structural zeros kept). PGCP_E_MESH on a zero-area face.
+ * clamped (host, may be NULL) receives the number of |cot| > 1e8 clamps. */
+PGCP_API int pgcp_batch_laplacian(pgcp_batch* b, int64_t* clamped, void* stream);
+
+/* Default pins of every submesh (flatten.py:113-122, sequential arclength
+ * sum). Written to the PGCP_ARR_PINS array. */
+PGCP_API int pgcp_batch_default_pins(pgcp_batch* b, void* stream);
+
+/* Solver controls and per-submesh results */
+typedef struct {
+    double rtol;        /* stop when ||r|| <= rtol ||b|| (recurrence residual)   */
+    double contract_tol;/* residual contract of flatten.py:170-173 (1e-10)        */
+    int32_t maxit;      /* per-submesh iteration cap                             */
+    int32_t cluster;    /* CTAs per submesh (0 = auto)                           */
+} pgcp_solve_opts;
+
+typedef struct {
+    int32_t iters;      /* PCG iterations                                        */
+    int32_t status;     /* PGCP_OK / PGCP_E_NOCONV / PGCP_E_SOLVE                 */
+    double relres;      /* recurrence ||r||/||b||                                 */
+    double true_res;    /* ||A x - b|| recomputed                                 */
+    double bnorm;       /* ||b||                                                  */
+    double xnorm;       /* ||x||                                                  */
+} pgcp_solve_stat;
+
+/* DNCP free-boundary flattening of the listed submeshes (flatten.py:125-188):
+ * C_ff x = -C_f,fixed t solved as the equivalent complex Hermitian system
+ * (L + 2i M_xy) restricted to the non-pinned vertices, batched fp64 Jacobi
+ * PCG, one CTA cluster per submesh.
+ *   comps    host int32 [ncomp] submesh ids (NULL: all)
+ *   pins     host int32 [2*ncomp] local pins (NULL: default pins)
+ *   targets  host f64 [4] = (t0.re, t0.im, t1.re, t1.im)
+ *   z        device complex [sum_n] (written for the listed submeshes)
+ *   stats    host [ncomp]
+ * Synchronises. */
+PGCP_API int pgcp_batch_flatten(pgcp_batch* b, const int32_t* comps, int32_t ncomp,
+                       const int32_t* pins, const double* targets,
+                       const pgcp_solve_opts* opts, double* z,
+                       pgcp_solve_stat* stats, void* stream);
+
+/* Dirichlet harmonic extension (assemble.py:23-50) for the listed submeshes.
+ *   fixed_gid  device int32 [nfixed] global local-vertex ids held fixed
+ *   fixed_val  device complex [nfixed]
+ * Unknowns are the remaining local vertices of each listed submesh.
+ * Synchronises. */
+PGCP_API int pgcp_batch_harmonic(pgcp_batch* b, const int32_t* comps, int32_t ncomp,
+                        const int32_t* fixed_gid, const double* fixed_val, int64_t nfixed,
+                        const pgcp_solve_opts* opts, double* z,
+                        pgcp_solve_stat* stats, void* stream);
+
+/* Exported solver systems for pattern parity (flatten.py:160-166 C_ff and
+ * assemble.py:40 L_II), one submesh, CSR with int32 indptr/indices as scipy
+ * builds them. which = 0: C_ff of the last flatten (real 2n-4 form, exact
+ * zeros dropped as csr_binop does); 1: L_II of the last harmonic solve.
+ * Two-call protocol: pass NULL buffers to get (rows, nnz) in dims. */
+PGCP_API int pgcp_batch_export_system(pgcp_batch* b, int which, int32_t comp, int64_t* dims,
+                             int32_t* indptr, int32_t* indices, double* data,
+                             double* rhs, void* stream);
+
+/* Energy of embeddings: per submesh E_D - A (flatten.py:89-110).
+ * z device complex [sum_n]; energy host f64 [K]. Synchronises. */
+PGCP_API int pgcp_batch_conformal_energy(pgcp_batch* b, const double* z, double* energy, void* stream);
+
+/* -------------------------------------------------------------------------
+ * Boundary welding (welding.py:512-842), device resident, one CTA per weld.
+ * See paper_1903_12359_b200/welding.py for the record encoding.
+ */
+typedef struct {
+    int32_t kind;   /* 0 mob, 1 sqrt-ratio, 2 open, 3 close, 4 square-mobius */
+    int32_t flags;  /* bit0 axis, bits 8..15 npins, side/branch values        */
+    double p[16];   /* parameters (see welding.py)                            */
+} pgcp_rec;
+
+/* Replay records [rec0, rec0+nrec) on points (welding.py:512-526).
+ * pts device complex [npts] in/out; sides device int8 [npts] in/out.
+ * nan_flag device int32 (set to 1 on NaN). Asynchronous. */
+PGCP_API int pgcp_weld_replay(const pgcp_rec* recs, int32_t nrec, double* pts, int8_t* sides,
+                     int64_t npts, int32_t* nan_flag, void* stream);
+
+/* One partial (closed = 0) or closed (closed = 1) weld, welding.py:640-763:
+ *   a, b      device complex [na], [nb]   (input boundary samples)
+ *   out_a/b   device complex [na], [nb]
+ *   recs_a/b  device pgcp_rec [cap_rec]   (the two map logs)
+ *   meta      device f64 [8]: n_rec_a, n_rec_b, seam_error, scale, error code,
+ *             error index, aux
+ * One CTA; asynchronous. */
+PGCP_API int pgcp_weld_one(const double* a, int64_t na, const double* b, int64_t nb, int64_t k,
+                  int closed, double hard_tol, double* out_a, double* out_b,
+                  pgcp_rec* recs_a, pgcp_rec* recs_b, int32_t cap_rec, double* meta,
+                  void* stream);
+
+/* Geodesic map of a Jordan polygon to the unit circle (welding.py:803-842).
+ *   pts device complex [n] (ccw), interior: host complex or NULL
+ *   out device complex [n]; recs device [cap_rec]; meta as above. */
+PGCP_API int pgcp_weld_geodesic(const double* pts, int64_t n, const double* interior,
+                       double* out, pgcp_rec* recs, int32_t cap_rec, double* meta,
+                       void* stream);
+
+/* -------------------------------------------------------------------------
+ * Stitch and metrics
+ */
+/* stitch_global (assemble.py:286-337): average seam copies.
+ *   z       device complex [sum_n] per-submesh embeddings (local order)
+ *   coords  device complex [n]; stats host f64 [4]: seam_max, scale, -, -
+ * Synchronises. */
+PGCP_API int pgcp_batch_stitch(pgcp_batch* b, const double* z, double* coords, double* stats,
+                      void* stream);
+
+/* Angular distortion per corner (metrics.py:31-75) and flips
+ * (assemble.py:97-102, 259-263).
+ *   mode 0 planar (coords complex [n]), 1 sphere (coords f64 [n*3])
+ *   d device f64 [3m], valid device uint8 [3m], nflip host int64,
+ *   summary host f64 [PGCP_SUMMARY_COUNT]. Synchronises. */
+#define PGCP_SUMMARY_COUNT 16
+PGCP_API int pgcp_distortion(const double* V, const int32_t* F, int64_t n, int64_t m,
+                    const double* coords, int mode, double* d, uint8_t* valid,
+                    int64_t* nflip, double* summary, void* stream);
+
+/* host-side weld-schedule planner (partition.py:236-324): see planner.cpp */
+PGCP_API int pgcp_plan_weld_schedule(const int64_t* cyc, const int64_t* cyc_off, int32_t K,
+                            const int64_t* cuts, int64_t ncuts, int mode_sphere,
+                            const int32_t* pairs, int32_t npairs,
+                            int64_t* out_meta, int64_t* out_idx, int64_t out_cap,
+                            int64_t* out_len);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PGCP_B200_H */

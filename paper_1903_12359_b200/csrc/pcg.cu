@@ -1,0 +1,1078 @@
+// pcg.cu -- K3: batched fp64 Jacobi-preconditioned CG, one thread-block
+// cluster per subdomain, CG vectors resident in distributed shared memory.
+//
+// Replaces the two `spsolve` calls of the hot path:
+//   flatten.py:157-173  DNCP: C_ff x = -C_f,fixed t with C = blockdiag(L,L) - 2M
+//   assemble.py:34-48   harmonic: L_II u = -L_IB g (complex g, 2 RHS)
+// Both are solved in one complex-Hermitian form over the unknown vertices U:
+//     H = L_UU + 2i M_xy[U,U]      (flatten; M_xy[p,next]=+1/4, [p,prev]=-1/4)
+//     H = L_UU                      (harmonic; complex RHS)
+// which is exactly the real 2|U| system of the reference (pinned by
+// tests/test_oracle_pins.py::test_hermitian_form). CG on an HPD system with a
+// real diagonal preconditioner has real alpha/beta, so one recurrence serves
+// both halves and L is streamed once per iteration for both.
+//
+// Layout (per solve, over the listed subdomains = "slots"):
+//   rows      unknowns of slot j padded to 32*S_j rows (S_j slices); slot row
+//             base 32*sl_off[j]; padding rows are inert (D=1, b=0, val=0)
+//   matrix    sliced ELL, one 32-row slice per warp: entry k of row `lane` of
+//             slice s at sl_ptr[s] + 32k + lane, so every load of val/col is a
+//             coalesced 256 B / 128 B transaction; col = slot-local padded row
+//   coupling  flatten boundary rows carry (next, prev) rows in cpl[] and a bit
+//             in the slice mask: (H z)_u += i/2 (z_next - z_prev)
+//   vectors   z, p, q (complex) live in the shared memory of the cluster's
+//             CTAs (48 B/row); x and the diagonal stay in global memory
+//
+// Iteration (2 cluster barriers, both inside the reductions):
+//   A: s = A z; q = s + beta q; p = z + beta p; pq = Re<p,q>        [gathers z]
+//   B: alpha = rz/pq; x += alpha p; z -= alpha Dinv q;
+//      rz = sum D|z|^2, rr = sum D^2|z|^2   (residual r = D z)
+// using A p_new = A z + beta A p_old, so only z is ever gathered.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "batch.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace pgcp {
+
+struct SolveSystem {
+    bool dncp = false;
+    int32_t nslot = 0;
+    std::vector<int32_t> comps;      // slot -> comp
+    std::vector<int64_t> h_sl_off;   // slot -> first slice (nslot+1)
+    std::vector<int64_t> h_nu;       // slot -> unknowns
+    std::vector<int64_t> h_sv_off;   // slot -> compact vertex offset (nslot+1)
+    int64_t nslices = 0, rows = 0, nnz = 0, ne = 0;
+    int csize = 1;
+    DevBuf<int32_t> d_comps, slot_of_comp;
+    DevBuf<int64_t> sl_off, sv_off, sl_ptr;
+    DevBuf<uint32_t> sl_mask;
+    DevBuf<int32_t> col, urow, rowsrc, fixed_ref;
+    DevBuf<int2> cpl;
+    DevBuf<double> val, D, Dinv;
+    DevBuf<double2> b, x, fv;
+    DevBuf<int32_t> iters;
+    DevBuf<double> res;  // per slot: relres, bnorm^2, true_res^2, xnorm^2, pad
+};
+
+void free_system(void* p) { delete static_cast<SolveSystem*>(p); }
+
+namespace {
+
+constexpr int PCG_THREADS = 1024;
+constexpr int PCG_WARPS = PCG_THREADS / 32;
+constexpr int MAX_CLUSTER = 16;
+constexpr int SMEM_LIMIT = 227 * 1024;
+constexpr int RED_BYTES = 2 * MAX_CLUSTER * 2 * 8 + PCG_WARPS * 2 * 8 + 64;
+
+__device__ __forceinline__ int bsearch_off(const int64_t* __restrict__ off, int n, int64_t e) {
+    int lo = 0, hi = n - 1;  // largest j with off[j] <= e
+    while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if (off[mid] <= e) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+// ---------------------------------------------------------------------------
+// system build kernels
+
+__global__ void k_fixed_pins(int32_t nslot, const int32_t* __restrict__ pins, const int64_t* __restrict__ sv_off,
+                             int32_t* __restrict__ fixed_ref) {
+    GRID_STRIDE(j, nslot) {
+        fixed_ref[sv_off[j] + pins[2 * j]] = 2 * (int)j;
+        fixed_ref[sv_off[j] + pins[2 * j + 1]] = 2 * (int)j + 1;
+    }
+}
+
+__global__ void k_fixed_list(int64_t nfixed, const int32_t* __restrict__ gid, const int32_t* __restrict__ comp_of,
+                             const int32_t* __restrict__ slot_of_comp, const int64_t* __restrict__ vert_off,
+                             const int64_t* __restrict__ sv_off, int32_t* __restrict__ fixed_ref) {
+    GRID_STRIDE(i, nfixed) {
+        int g = gid[i];
+        int c = comp_of[g];
+        int j = slot_of_comp[c];
+        if (j < 0) continue;
+        fixed_ref[sv_off[j] + (g - vert_off[c])] = (int32_t)i;
+    }
+}
+
+__global__ void k_unknown_flag(int64_t ne, const int32_t* __restrict__ fixed_ref, int32_t* __restrict__ flag) {
+    GRID_STRIDE(e, ne) flag[e] = fixed_ref[e] < 0 ? 1 : 0;
+}
+
+__global__ void k_urow(int64_t ne, int32_t nslot, const int64_t* __restrict__ sv_off,
+                       const int64_t* __restrict__ sl_off, const int64_t* __restrict__ uscan,
+                       const int32_t* __restrict__ fixed_ref, int32_t* __restrict__ urow,
+                       int32_t* __restrict__ rowsrc) {
+    GRID_STRIDE(e, ne) {
+        if (fixed_ref[e] >= 0) {
+            urow[e] = -1;
+            continue;
+        }
+        int j = bsearch_off(sv_off, nslot + 1, e);
+        int64_t r = 32 * sl_off[j] + (uscan[e] - uscan[sv_off[j]]);
+        urow[e] = (int32_t)r;
+        rowsrc[r] = (int32_t)e;
+    }
+}
+
+struct BuildArgs {
+    int32_t nslot;
+    const int32_t* comps;
+    const int64_t* sv_off;
+    const int64_t* sl_off;
+    const int64_t* vert_off;
+    const int64_t* row_ptr;
+    const int32_t* col;
+    const double* val;
+    const int32_t* rowsrc;
+    const int32_t* urow;
+    const int32_t* fixed_ref;
+    const double2* fv;
+};
+
+__global__ void k_slice_len(BuildArgs a, int64_t nslices, int64_t* __restrict__ len) {
+    int lane = threadIdx.x & 31;
+    int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t s = warp; s < nslices; s += nwarp) {
+        int64_t r = 32 * s + lane;
+        int cnt = 0;
+        int e = a.rowsrc[r];
+        if (e >= 0) {
+            int j = bsearch_off(a.sv_off, a.nslot + 1, e);
+            int c = a.comps[j];
+            int self = (int)(e - a.sv_off[j]);
+            int64_t g = a.vert_off[c] + self;
+            for (int64_t q = a.row_ptr[g]; q < a.row_ptr[g + 1]; ++q) {
+                int lc = a.col[q];
+                if (lc != self && a.urow[a.sv_off[j] + lc] >= 0) ++cnt;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) cnt = max(cnt, __shfl_xor_sync(0xffffffffu, cnt, o));
+        if (lane == 0) len[s] = 32 * (int64_t)cnt;
+    }
+}
+
+__global__ void k_fill_rows(BuildArgs a, int64_t rows, const int64_t* __restrict__ sl_ptr,
+                            int32_t* __restrict__ ocol, double* __restrict__ oval, double* __restrict__ D,
+                            double* __restrict__ Dinv, double2* __restrict__ bvec, int2* __restrict__ cpl,
+                            double2* __restrict__ x) {
+    GRID_STRIDE(r, rows) {
+        int64_t s = r >> 5;
+        int lane = (int)(r & 31);
+        int64_t p0 = sl_ptr[s];
+        int w = (int)((sl_ptr[s + 1] - p0) >> 5);
+        int j = bsearch_off(a.sl_off, a.nslot + 1, s);
+        int64_t rbase = 32 * a.sl_off[j];
+        int selfrow = (int)(r - rbase);
+        int e = a.rowsrc[r];
+        int k = 0;
+        double d = 1.0;
+        double2 bb = make_double2(0.0, 0.0);
+        if (e >= 0) {
+            int c = a.comps[j];
+            int self = (int)(e - a.sv_off[j]);
+            int64_t g = a.vert_off[c] + self;
+            for (int64_t q = a.row_ptr[g]; q < a.row_ptr[g + 1]; ++q) {
+                int lc = a.col[q];
+                double v = a.val[q];
+                if (lc == self) {
+                    d = v;
+                    continue;
+                }
+                int64_t ee = a.sv_off[j] + lc;
+                int ur = a.urow[ee];
+                if (ur >= 0) {
+                    ocol[p0 + 32 * k + lane] = (int32_t)(ur - rbase);
+                    oval[p0 + 32 * k + lane] = v;
+                    ++k;
+                } else {
+                    double2 f = a.fv[a.fixed_ref[ee]];
+                    bb.x -= v * f.x;
+                    bb.y -= v * f.y;
+                }
+            }
+        }
+        for (; k < w; ++k) {
+            ocol[p0 + 32 * k + lane] = selfrow;
+            oval[p0 + 32 * k + lane] = 0.0;
+        }
+        D[r] = d;
+        Dinv[r] = 1.0 / d;
+        bvec[r] = bb;
+        cpl[r] = make_int2(-1, -1);
+        x[r] = make_double2(0.0, 0.0);
+    }
+}
+
+// DNCP boundary coupling (H = L + 2i M_xy) for every loop vertex of every slot
+__global__ void k_coupling(int32_t nslot, const int32_t* __restrict__ comps, const int64_t* __restrict__ loop_off,
+                           const int32_t* __restrict__ loop, const int64_t* __restrict__ sv_off,
+                           const int64_t* __restrict__ sl_off, const int32_t* __restrict__ urow,
+                           const int32_t* __restrict__ fixed_ref, const double2* __restrict__ fv,
+                           int2* __restrict__ cpl, uint32_t* __restrict__ mask, double2* __restrict__ bvec,
+                           int64_t total) {
+    // flattened over (slot, loop position)
+    GRID_STRIDE(t, total) {
+        // find slot by scanning cumulative loop lengths (nslot small)
+        int64_t acc = 0;
+        int j = 0;
+        for (; j < nslot; ++j) {
+            int c = comps[j];
+            int64_t nb = loop_off[c + 1] - loop_off[c];
+            if (t < acc + nb) break;
+            acc += nb;
+        }
+        if (j >= nslot) continue;
+        int c = comps[j];
+        int64_t lo = loop_off[c], nb = loop_off[c + 1] - lo;
+        int64_t pos = t - acc;
+        int u = loop[lo + pos];
+        int nx = loop[lo + (pos + 1) % nb];
+        int pv = loop[lo + (pos + nb - 1) % nb];
+        int64_t eu = sv_off[j] + u, en = sv_off[j] + nx, ep = sv_off[j] + pv;
+        int ru = urow[eu];
+        if (ru < 0) continue;
+        int64_t rbase = 32 * sl_off[j];
+        int rn = urow[en], rp = urow[ep];
+        cpl[ru] = make_int2(rn >= 0 ? (int)(rn - rbase) : -1, rp >= 0 ? (int)(rp - rbase) : -1);
+        atomicOr(&mask[ru >> 5], 1u << (ru & 31));
+        double2 bb = bvec[ru];
+        if (rn < 0) {  // -(i/2) t_next
+            double2 f = fv[fixed_ref[en]];
+            bb.x += 0.5 * f.y;
+            bb.y -= 0.5 * f.x;
+        }
+        if (rp < 0) {  // +(i/2) t_prev
+            double2 f = fv[fixed_ref[ep]];
+            bb.x -= 0.5 * f.y;
+            bb.y += 0.5 * f.x;
+        }
+        bvec[ru] = bb;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// the solver
+
+struct PcgArgs {
+    const int64_t* sl_off;   // slot -> first slice
+    const int64_t* sl_ptr;   // slice -> first entry
+    const uint32_t* sl_mask;
+    const int32_t* col;
+    const double* val;
+    const double* D;
+    const double* Dinv;
+    const int2* cpl;
+    const double2* b;
+    double2* x;
+    int32_t* iters;
+    double* res;             // per slot [8]
+    double tol2;             // rtol^2
+    int32_t maxit;
+    int32_t chunk_cap;       // slices per CTA the smem was sized for
+};
+
+struct Vec {
+    double2* z;
+    double2* p;
+    double2* q;
+};
+
+// deterministic cluster-wide sum of two doubles: warp -> CTA (fixed order) ->
+// every CTA receives every CTA's partial through DSMEM -> fixed-order sum
+__device__ __forceinline__ double2 cluster_sum2(cg::cluster_group& cl, int csize, int rank, double a, double b,
+                                                double2* s_warp, double2* s_slot, int parity) {
+    int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    a = warp_sum(a);
+    b = warp_sum(b);
+    if (lane == 0) s_warp[w] = make_double2(a, b);
+    __syncthreads();
+    if (w == 0) {
+        double2 v = (lane < PCG_WARPS) ? s_warp[lane] : make_double2(0.0, 0.0);
+        double ta = warp_sum(v.x), tb = warp_sum(v.y);
+        if (lane < csize) {
+            double2* dst = cl.map_shared_rank(s_slot + parity * MAX_CLUSTER, lane);
+            dst[rank] = make_double2(ta, tb);
+        }
+    }
+    cl.sync();
+    double2 t = make_double2(0.0, 0.0);
+    const double2* src = s_slot + parity * MAX_CLUSTER;
+    for (int r = 0; r < csize; ++r) {
+        t.x += src[r].x;
+        t.y += src[r].y;
+    }
+    return t;
+}
+
+__global__ void __launch_bounds__(PCG_THREADS, 1) k_pcg(PcgArgs A) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    cg::cluster_group cl = cg::this_cluster();
+    const int csize = (int)cl.num_blocks();
+    const int rank = (int)cl.block_rank();
+    const int slot = blockIdx.x / csize;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+
+    const int64_t s0 = A.sl_off[slot];
+    const int S = (int)(A.sl_off[slot + 1] - s0);
+    const int chunk = (S + csize - 1) / csize;
+    const int my_lo = min(S, rank * chunk);
+    const int nloc = min(S, my_lo + chunk) - my_lo;
+    const float inv_chunk = 1.0f / (float)chunk;
+
+    double2* s_warp = reinterpret_cast<double2*>(smem);
+    double2* s_slot = s_warp + PCG_WARPS;
+    double2* zl = s_slot + 2 * MAX_CLUSTER;
+    double2* pl = zl + 32 * A.chunk_cap;
+    double2* ql = pl + 32 * A.chunk_cap;
+
+    const int64_t row0 = 32 * (s0 + my_lo);  // first global row of this CTA
+    const int nrow = 32 * nloc;
+
+    // init: x = 0 (done by the builder), r = b, z = Dinv b
+    double l_rz = 0.0, l_bb = 0.0;
+    for (int i = threadIdx.x; i < nrow; i += PCG_THREADS) {
+        double2 bi = A.b[row0 + i];
+        double di = A.Dinv[row0 + i];
+        double2 zi = make_double2(di * bi.x, di * bi.y);
+        zl[i] = zi;
+        pl[i] = make_double2(0.0, 0.0);
+        ql[i] = make_double2(0.0, 0.0);
+        l_rz += bi.x * zi.x + bi.y * zi.y;
+        l_bb += bi.x * bi.x + bi.y * bi.y;
+    }
+    int parity = 0;
+    double2 t0 = cluster_sum2(cl, csize, rank, l_rz, l_bb, s_warp, s_slot, parity);
+    parity ^= 1;
+    double rz = t0.x;
+    const double bb = t0.y;
+    const double stop = A.tol2 * bb;
+    double beta = 0.0, rr = bb;
+    int it = 0;
+
+    if (bb > 0.0 && rr > stop) {
+        for (it = 0; it < A.maxit;) {
+            // ---- phase A: q = A z + beta q, p = z + beta p, pq
+            double l_pq = 0.0;
+            for (int ls = warp; ls < nloc; ls += PCG_WARPS) {
+                const int64_t gs = s0 + my_lo + ls;
+                const int64_t e0 = A.sl_ptr[gs];
+                const int wdt = (int)((A.sl_ptr[gs + 1] - e0) >> 5);
+                const int li = 32 * ls + lane;
+                const int64_t gr = row0 + li;
+                double2 zi = zl[li];
+                double di = A.D[gr];
+                double sx = di * zi.x, sy = di * zi.y;
+                const int32_t* cp = A.col + e0 + lane;
+                const double* vp = A.val + e0 + lane;
+#pragma unroll 4
+                for (int k = 0; k < wdt; ++k) {
+                    int c = __ldg(cp + 32 * k);
+                    double v = __ldg(vp + 32 * k);
+                    int sc = c >> 5;
+                    int own = __float2int_rz(((float)sc + 0.5f) * inv_chunk);
+                    int off = c - 32 * own * chunk;
+                    double2 zc = (own == rank) ? zl[off] : *cl.map_shared_rank(zl + off, own);
+                    sx = fma(v, zc.x, sx);
+                    sy = fma(v, zc.y, sy);
+                }
+                uint32_t msk = A.sl_mask[gs];
+                if (msk & (1u << lane)) {
+                    int2 nb = A.cpl[gr];
+                    double2 zn = make_double2(0.0, 0.0), zp = make_double2(0.0, 0.0);
+                    if (nb.x >= 0) {
+                        int o = __float2int_rz(((float)(nb.x >> 5) + 0.5f) * inv_chunk);
+                        zn = (o == rank) ? zl[nb.x - 32 * o * chunk] : *cl.map_shared_rank(zl + (nb.x - 32 * o * chunk), o);
+                    }
+                    if (nb.y >= 0) {
+                        int o = __float2int_rz(((float)(nb.y >> 5) + 0.5f) * inv_chunk);
+                        zp = (o == rank) ? zl[nb.y - 32 * o * chunk] : *cl.map_shared_rank(zl + (nb.y - 32 * o * chunk), o);
+                    }
+                    // + i/2 (zn - zp)
+                    sx -= 0.5 * (zn.y - zp.y);
+                    sy += 0.5 * (zn.x - zp.x);
+                }
+                double2 qi = ql[li], pi = pl[li];
+                qi.x = fma(beta, qi.x, sx);
+                qi.y = fma(beta, qi.y, sy);
+                pi.x = fma(beta, pi.x, zi.x);
+                pi.y = fma(beta, pi.y, zi.y);
+                ql[li] = qi;
+                pl[li] = pi;
+                l_pq += pi.x * qi.x + pi.y * qi.y;
+            }
+            double2 tq = cluster_sum2(cl, csize, rank, l_pq, 0.0, s_warp, s_slot, parity);
+            parity ^= 1;
+            const double alpha = rz / tq.x;
+            // ---- phase B
+            double l_rz2 = 0.0, l_rr = 0.0;
+            for (int i = threadIdx.x; i < nrow; i += PCG_THREADS) {
+                const int64_t gr = row0 + i;
+                double2 pi = pl[i], qi = ql[i], zi = zl[i];
+                double2 xi = A.x[gr];
+                xi.x = fma(alpha, pi.x, xi.x);
+                xi.y = fma(alpha, pi.y, xi.y);
+                A.x[gr] = xi;
+                double dv = A.Dinv[gr], di = A.D[gr];
+                double ad = alpha * dv;
+                zi.x = fma(-ad, qi.x, zi.x);
+                zi.y = fma(-ad, qi.y, zi.y);
+                zl[i] = zi;
+                double m2 = zi.x * zi.x + zi.y * zi.y;
+                l_rz2 += di * m2;
+                l_rr += di * di * m2;
+            }
+            double2 tr = cluster_sum2(cl, csize, rank, l_rz2, l_rr, s_warp, s_slot, parity);
+            parity ^= 1;
+            beta = tr.x / rz;
+            rz = tr.x;
+            rr = tr.y;
+            ++it;
+            if (rr <= stop || !(rr == rr)) break;
+        }
+    }
+    if (rank == 0 && threadIdx.x == 0) {
+        A.iters[slot] = it;
+        A.res[8 * slot + 0] = (bb > 0.0) ? sqrt(rr / bb) : 0.0;
+        A.res[8 * slot + 1] = bb;
+    }
+}
+
+// true residual ||b - H x||, ||x||, ||b|| per slot; one block per slot,
+// fixed-order reduction; x gathered from global memory
+__global__ void k_true_residual(PcgArgs A) {
+    __shared__ double red[3][32];
+    const int slot = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int64_t s0 = A.sl_off[slot];
+    const int S = (int)(A.sl_off[slot + 1] - s0);
+    const int64_t rbase = 32 * s0;
+    double a_r = 0.0, a_x = 0.0, a_b = 0.0;
+    for (int ls = warp; ls < S; ls += nw) {
+        const int64_t gs = s0 + ls;
+        const int64_t e0 = A.sl_ptr[gs];
+        const int wdt = (int)((A.sl_ptr[gs + 1] - e0) >> 5);
+        const int64_t gr = rbase + 32 * ls + lane;
+        double2 xi = A.x[gr];
+        double di = A.D[gr];
+        double sx = di * xi.x, sy = di * xi.y;
+        for (int k = 0; k < wdt; ++k) {
+            int c = A.col[e0 + 32 * k + lane];
+            double v = A.val[e0 + 32 * k + lane];
+            double2 xc = A.x[rbase + c];
+            sx = fma(v, xc.x, sx);
+            sy = fma(v, xc.y, sy);
+        }
+        if (A.sl_mask[gs] & (1u << lane)) {
+            int2 nb = A.cpl[gr];
+            double2 zn = nb.x >= 0 ? A.x[rbase + nb.x] : make_double2(0.0, 0.0);
+            double2 zp = nb.y >= 0 ? A.x[rbase + nb.y] : make_double2(0.0, 0.0);
+            sx -= 0.5 * (zn.y - zp.y);
+            sy += 0.5 * (zn.x - zp.x);
+        }
+        double2 bi = A.b[gr];
+        double rx = bi.x - sx, ry = bi.y - sy;
+        a_r += rx * rx + ry * ry;
+        a_x += xi.x * xi.x + xi.y * xi.y;
+        a_b += bi.x * bi.x + bi.y * bi.y;
+    }
+    a_r = warp_sum(a_r);
+    a_x = warp_sum(a_x);
+    a_b = warp_sum(a_b);
+    if (lane == 0) {
+        red[0][warp] = a_r;
+        red[1][warp] = a_x;
+        red[2][warp] = a_b;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        double r0 = lane < nw ? red[0][lane] : 0.0;
+        double r1 = lane < nw ? red[1][lane] : 0.0;
+        double r2 = lane < nw ? red[2][lane] : 0.0;
+        r0 = warp_sum(r0);
+        r1 = warp_sum(r1);
+        r2 = warp_sum(r2);
+        if (lane == 0) {
+            A.res[8 * slot + 2] = sqrt(r0);
+            A.res[8 * slot + 3] = sqrt(r1);
+            A.res[8 * slot + 4] = sqrt(r2);
+        }
+    }
+}
+
+// scatter the solution back to submesh-local vertices (fixed vertices get
+// their prescribed values)
+__global__ void k_scatter(int64_t ne, int32_t nslot, const int32_t* __restrict__ comps,
+                          const int64_t* __restrict__ sv_off, const int64_t* __restrict__ vert_off,
+                          const int32_t* __restrict__ urow, const int32_t* __restrict__ fixed_ref,
+                          const double2* __restrict__ fv, const double2* __restrict__ x, double2* __restrict__ z) {
+    GRID_STRIDE(e, ne) {
+        int j = bsearch_off(sv_off, nslot + 1, e);
+        int64_t g = vert_off[comps[j]] + (e - sv_off[j]);
+        int r = urow[e];
+        z[g] = (r >= 0) ? x[r] : fv[fixed_ref[e]];
+    }
+}
+
+// per slot: shoelace area of the loop, E_D - A, max |z| (flatten.py:176-187)
+__global__ void k_flat_checks(const int32_t* __restrict__ comps, const int64_t* __restrict__ vert_off,
+                              const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+                              const double* __restrict__ val, const int64_t* __restrict__ loop_off,
+                              const int32_t* __restrict__ loop, const double2* __restrict__ z,
+                              double* __restrict__ res) {
+    __shared__ double red[3][32];
+    int slot = blockIdx.x;
+    int c = comps[slot];
+    int64_t vb = vert_off[c], ve = vert_off[c + 1];
+    double ed = 0.0, mx = 0.0, ar = 0.0;
+    for (int64_t g = vb + threadIdx.x; g < ve; g += blockDim.x) {
+        double sx = 0.0, sy = 0.0;
+        for (int64_t q = row_ptr[g]; q < row_ptr[g + 1]; ++q) {
+            double2 zz = z[vb + col[q]];
+            sx += val[q] * zz.x;
+            sy += val[q] * zz.y;
+        }
+        double2 zi = z[g];
+        ed += 0.5 * (zi.x * sx + zi.y * sy);
+        mx = fmax(mx, zi.x * zi.x + zi.y * zi.y);
+    }
+    int64_t lo = loop_off[c], nb = loop_off[c + 1] - lo;
+    for (int64_t j = threadIdx.x; j < nb; j += blockDim.x) {
+        double2 w = z[vb + loop[lo + j]];
+        double2 u = z[vb + loop[lo + (j + 1) % nb]];
+        ar += 0.5 * (w.x * u.y - w.y * u.x);
+    }
+    int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    ed = warp_sum(ed);
+    ar = warp_sum(ar);
+    mx = warp_max(mx);
+    if (lane == 0) {
+        red[0][warp] = ed;
+        red[1][warp] = ar;
+        red[2][warp] = mx;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        double a = lane < nw ? red[0][lane] : 0.0;
+        double b = lane < nw ? red[1][lane] : 0.0;
+        double m = lane < nw ? red[2][lane] : 0.0;
+        a = warp_sum(a);
+        b = warp_sum(b);
+        m = warp_max(m);
+        if (lane == 0) {
+            res[8 * slot + 5] = b;       // signed area
+            res[8 * slot + 6] = a - b;   // E_C = E_D - A
+            res[8 * slot + 7] = m;       // max |z|^2
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+
+int pick_cluster(int64_t max_slices, int32_t nslot, int32_t forced, int* csize_out, int* chunk_out) {
+    const int max_chunk = (SMEM_LIMIT - RED_BYTES) / (48 * 32);
+    int cmin = 1;
+    while (cmin <= MAX_CLUSTER && (max_slices + cmin - 1) / cmin > max_chunk) cmin *= 2;
+    if (cmin > MAX_CLUSTER) {
+        set_error("subdomain with %lld unknown slices exceeds the on-chip capacity of a %d-CTA cluster",
+                  (long long)max_slices, MAX_CLUSTER);
+        return PGCP_E_INVALID;
+    }
+    int c = cmin;
+    if (forced > 0) {
+        c = std::max(cmin, forced);
+    } else {
+        // spread over the SMs when there are few subdomains, but keep >= 8
+        // slices (256 rows) per CTA so DSMEM halo traffic stays small
+        while (c < MAX_CLUSTER && (int64_t)(2 * c) * nslot <= 148 && (max_slices + 2 * c - 1) / (2 * c) >= 8) c *= 2;
+    }
+    *csize_out = c;
+    *chunk_out = (int)((max_slices + c - 1) / c);
+    return PGCP_OK;
+}
+
+int launch_pcg(SolveSystem* S, const PcgArgs& args, int csize, cudaStream_t s) {
+    int chunk = args.chunk_cap;
+    size_t smem = (size_t)RED_BYTES + (size_t)3 * 32 * chunk * sizeof(double2);
+    if (smem > SMEM_LIMIT) {
+        set_error("pcg: shared memory %zu exceeds limit", smem);
+        return PGCP_E_INVALID;
+    }
+    PGCP_TRY_CUDA(cudaFuncSetAttribute(k_pcg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (csize > 8) PGCP_TRY_CUDA(cudaFuncSetAttribute(k_pcg, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(S->nslot * csize), 1, 1);
+    cfg.blockDim = dim3(PCG_THREADS, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = csize;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int nclusters = 0;
+    cudaError_t oe = cudaOccupancyMaxActiveClusters(&nclusters, k_pcg, &cfg);
+    if (oe != cudaSuccess || nclusters < 1) {
+        set_error("pcg: cluster of %d CTAs with %zu B shared memory cannot be scheduled (%s)", csize, smem,
+                  cudaGetErrorString(oe));
+        cudaGetLastError();
+        return PGCP_E_CUDA;
+    }
+    PGCP_TRY_CUDA(cudaLaunchKernelEx(&cfg, k_pcg, args));
+    return PGCP_OK;
+}
+
+// Build the slot system. pins (device int32 [2*nslot]) for DNCP, or the fixed
+// list for harmonic. fv = fixed values (device complex).
+int build_system(pgcp_batch* b, SolveSystem* S, bool dncp, const int32_t* d_pins, const double2* targets_host,
+                 const int32_t* fixed_gid, const double* fixed_val, int64_t nfixed, cudaStream_t s) {
+    const int32_t nslot = S->nslot;
+    S->dncp = dncp;
+    // compact vertex enumeration over the slots
+    S->h_sv_off.assign(nslot + 1, 0);
+    for (int j = 0; j < nslot; ++j) {
+        int c = S->comps[j];
+        S->h_sv_off[j + 1] = S->h_sv_off[j] + (b->h_vert_off[c + 1] - b->h_vert_off[c]);
+    }
+    S->ne = S->h_sv_off[nslot];
+    PGCP_TRY(S->d_comps.alloc(nslot, s));
+    PGCP_TRY_CUDA(cudaMemcpyAsync(S->d_comps.p, S->comps.data(), nslot * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    PGCP_TRY(S->sv_off.alloc(nslot + 1, s));
+    PGCP_TRY_CUDA(cudaMemcpyAsync(S->sv_off.p, S->h_sv_off.data(), (nslot + 1) * sizeof(int64_t),
+                                  cudaMemcpyHostToDevice, s));
+    std::vector<int32_t> h_soc(b->K, -1);
+    for (int j = 0; j < nslot; ++j) h_soc[S->comps[j]] = j;
+    PGCP_TRY(S->slot_of_comp.alloc(b->K, s));
+    PGCP_TRY_CUDA(cudaMemcpyAsync(S->slot_of_comp.p, h_soc.data(), b->K * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+
+    // fixed vertices and their values
+    PGCP_TRY(S->fixed_ref.alloc(S->ne, s));
+    PGCP_TRY(S->fixed_ref.fill_bytes(0xff, s));  // -1
+    if (dncp) {
+        PGCP_TRY(S->fv.alloc(2 * (int64_t)nslot, s));
+        std::vector<double2> hfv(2 * nslot);
+        for (int j = 0; j < nslot; ++j) {
+            hfv[2 * j] = targets_host[0];
+            hfv[2 * j + 1] = targets_host[1];
+        }
+        PGCP_TRY_CUDA(cudaMemcpyAsync(S->fv.p, hfv.data(), hfv.size() * sizeof(double2), cudaMemcpyHostToDevice, s));
+        k_fixed_pins<<<grid_for(nslot, 64), 64, 0, s>>>(nslot, d_pins, S->sv_off.p, S->fixed_ref.p);
+        PGCP_LAUNCH_CHECK();
+        PGCP_TRY_CUDA(cudaStreamSynchronize(s));  // hfv is a local
+    } else {
+        PGCP_TRY(S->fv.alloc(nfixed, s));
+        if (nfixed > 0) {
+            PGCP_TRY_CUDA(cudaMemcpyAsync(S->fv.p, fixed_val, nfixed * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+            k_fixed_list<<<grid_for(nfixed, 256), 256, 0, s>>>(nfixed, fixed_gid, b->comp_of_gid.p,
+                                                              S->slot_of_comp.p, b->vert_off.p, S->sv_off.p,
+                                                              S->fixed_ref.p);
+            PGCP_LAUNCH_CHECK();
+        }
+    }
+    // unknown numbering
+    DevBuf<int32_t> flag;
+    DevBuf<int64_t> uscan;
+    PGCP_TRY(flag.alloc(S->ne, s));
+    PGCP_TRY(uscan.alloc(S->ne + 1, s));
+    k_unknown_flag<<<grid_for(S->ne, 256), 256, 0, s>>>(S->ne, S->fixed_ref.p, flag.p);
+    PGCP_LAUNCH_CHECK();
+    PGCP_TRY(exclusive_scan_i32_to_i64(flag.p, uscan.p, S->ne, s));
+    std::vector<int64_t> hus(nslot + 1);
+    for (int j = 0; j <= nslot; ++j)
+        PGCP_TRY_CUDA(cudaMemcpyAsync(&hus[j], uscan.p + S->h_sv_off[j], sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    PGCP_TRY_CUDA(cudaStreamSynchronize(s));
+    S->h_nu.resize(nslot);
+    S->h_sl_off.assign(nslot + 1, 0);
+    for (int j = 0; j < nslot; ++j) {
+        S->h_nu[j] = hus[j + 1] - hus[j];
+        int64_t sl = (S->h_nu[j] + 31) / 32;
+        if (sl == 0) sl = 1;  // keep every slot addressable (all-fixed submesh)
+        S->h_sl_off[j + 1] = S->h_sl_off[j] + sl;
+    }
+    S->nslices = S->h_sl_off[nslot];
+    S->rows = 32 * S->nslices;
+    PGCP_TRY(S->sl_off.alloc(nslot + 1, s));
+    PGCP_TRY_CUDA(cudaMemcpyAsync(S->sl_off.p, S->h_sl_off.data(), (nslot + 1) * sizeof(int64_t),
+                                  cudaMemcpyHostToDevice, s));
+    PGCP_TRY(S->urow.alloc(S->ne, s));
+    PGCP_TRY(S->rowsrc.alloc(S->rows, s));
+    PGCP_TRY(S->rowsrc.fill_bytes(0xff, s));
+    k_urow<<<grid_for(S->ne, 256), 256, 0, s>>>(S->ne, nslot, S->sv_off.p, S->sl_off.p, uscan.p, S->fixed_ref.p,
+                                              S->urow.p, S->rowsrc.p);
+    PGCP_LAUNCH_CHECK();
+
+    BuildArgs a;
+    a.nslot = nslot;
+    a.comps = S->d_comps.p;
+    a.sv_off = S->sv_off.p;
+    a.sl_off = S->sl_off.p;
+    a.vert_off = b->vert_off.p;
+    a.row_ptr = b->row_ptr.p;
+    a.col = b->col.p;
+    a.val = b->val.p;
+    a.rowsrc = S->rowsrc.p;
+    a.urow = S->urow.p;
+    a.fixed_ref = S->fixed_ref.p;
+    a.fv = S->fv.p;
+    DevBuf<int64_t> len;
+    PGCP_TRY(len.alloc(S->nslices, s));
+    k_slice_len<<<grid_for(S->nslices * 32, 256), 256, 0, s>>>(a, S->nslices, len.p);
+    PGCP_LAUNCH_CHECK();
+    PGCP_TRY(S->sl_ptr.alloc(S->nslices + 1, s));
+    PGCP_TRY(exclusive_scan_i64(len.p, S->sl_ptr.p, S->nslices, s));
+    PGCP_TRY(fetch_scalar(S->sl_ptr.p + S->nslices, &S->nnz, s));
+    PGCP_TRY(S->col.alloc(S->nnz, s));
+    PGCP_TRY(S->val.alloc(S->nnz, s));
+    PGCP_TRY(S->D.alloc(S->rows, s));
+    PGCP_TRY(S->Dinv.alloc(S->rows, s));
+    PGCP_TRY(S->b.alloc(S->rows, s));
+    PGCP_TRY(S->x.alloc(S->rows, s));
+    PGCP_TRY(S->cpl.alloc(S->rows, s));
+    PGCP_TRY(S->sl_mask.alloc(S->nslices, s));
+    PGCP_TRY(S->sl_mask.zero(s));
+    k_fill_rows<<<grid_for(S->rows, 256), 256, 0, s>>>(a, S->rows, S->sl_ptr.p, S->col.p, S->val.p, S->D.p,
+                                                     S->Dinv.p, S->b.p, S->cpl.p, S->x.p);
+    PGCP_LAUNCH_CHECK();
+    if (dncp) {
+        int64_t total = 0;
+        for (int j = 0; j < nslot; ++j) {
+            int c = S->comps[j];
+            total += b->h_loop_off[c + 1] - b->h_loop_off[c];
+        }
+        if (total > 0) {
+            k_coupling<<<grid_for(total, 256), 256, 0, s>>>(nslot, S->d_comps.p, b->loop_off.p, b->loop.p, S->sv_off.p,
+                                                          S->sl_off.p, S->urow.p, S->fixed_ref.p, S->fv.p, S->cpl.p,
+                                                          S->sl_mask.p, S->b.p, total);
+            PGCP_LAUNCH_CHECK();
+        }
+    }
+    return PGCP_OK;
+}
+
+int run_solve(pgcp_batch* b, SolveSystem* S, const pgcp_solve_opts* o, double* z, pgcp_solve_stat* st,
+              cudaStream_t s) {
+    const int32_t nslot = S->nslot;
+    int64_t max_sl = 0;
+    for (int j = 0; j < nslot; ++j) max_sl = std::max(max_sl, S->h_sl_off[j + 1] - S->h_sl_off[j]);
+    int csize = 1, chunk = 1;
+    PGCP_TRY(pick_cluster(max_sl, nslot, o ? o->cluster : 0, &csize, &chunk));
+    S->csize = csize;
+    PGCP_TRY(S->iters.alloc(nslot, s));
+    PGCP_TRY(S->res.alloc(8 * (int64_t)nslot, s));
+    PGCP_TRY(S->res.zero(s));
+    PcgArgs A;
+    A.sl_off = S->sl_off.p;
+    A.sl_ptr = S->sl_ptr.p;
+    A.sl_mask = S->sl_mask.p;
+    A.col = S->col.p;
+    A.val = S->val.p;
+    A.D = S->D.p;
+    A.Dinv = S->Dinv.p;
+    A.cpl = S->cpl.p;
+    A.b = S->b.p;
+    A.x = S->x.p;
+    A.iters = S->iters.p;
+    A.res = S->res.p;
+    double rtol = (o && o->rtol > 0) ? o->rtol : 1e-10;
+    A.tol2 = rtol * rtol;
+    A.maxit = (o && o->maxit > 0) ? o->maxit : 200000;
+    A.chunk_cap = chunk;
+    PGCP_TRY(launch_pcg(S, A, csize, s));
+    k_true_residual<<<nslot, 512, 0, s>>>(A);
+    PGCP_LAUNCH_CHECK();
+    k_scatter<<<grid_for(S->ne, 256), 256, 0, s>>>(S->ne, nslot, S->d_comps.p, S->sv_off.p, b->vert_off.p, S->urow.p,
+                                                 S->fixed_ref.p, S->fv.p, S->x.p, (double2*)z);
+    PGCP_LAUNCH_CHECK();
+    if (S->dncp) {
+        k_flat_checks<<<nslot, 256, 0, s>>>(S->d_comps.p, b->vert_off.p, b->row_ptr.p, b->col.p, b->val.p,
+                                            b->loop_off.p, b->loop.p, (const double2*)z, S->res.p);
+        PGCP_LAUNCH_CHECK();
+    }
+    std::vector<int32_t> hit(nslot);
+    std::vector<double> hres(8 * nslot);
+    PGCP_TRY_CUDA(cudaMemcpyAsync(hit.data(), S->iters.p, nslot * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    PGCP_TRY_CUDA(cudaMemcpyAsync(hres.data(), S->res.p, 8 * nslot * sizeof(double), cudaMemcpyDeviceToHost, s));
+    PGCP_TRY_CUDA(cudaStreamSynchronize(s));
+    const double ctol = (o && o->contract_tol > 0) ? o->contract_tol : 1e-10;
+    int worst = PGCP_OK;
+    for (int j = 0; j < nslot; ++j) {
+        pgcp_solve_stat t;
+        t.iters = hit[j];
+        t.relres = hres[8 * j + 0];
+        t.true_res = hres[8 * j + 2];
+        t.xnorm = hres[8 * j + 3];
+        t.bnorm = hres[8 * j + 4];
+        t.status = PGCP_OK;
+        bool finite = std::isfinite(t.true_res) && std::isfinite(t.xnorm);
+        if (!finite) {
+            t.status = PGCP_E_SOLVE;
+        } else if (t.relres > rtol && t.iters >= A.maxit) {
+            t.status = PGCP_E_NOCONV;
+        } else if (t.bnorm > 0 && t.true_res > std::max(ctol * t.bnorm, 1e3 * ctol * t.xnorm)) {
+            t.status = PGCP_E_SOLVE;
+        }
+        if (st) st[j] = t;
+        if (t.status != PGCP_OK && worst == PGCP_OK) {
+            worst = t.status;
+            if (t.status == PGCP_E_NOCONV)
+                set_error("submesh %d: PCG did not converge (%d iterations, relres %.3e)", S->comps[j], t.iters,
+                          t.relres);
+            else if (!finite)
+                set_error("submesh %d: singular or non-finite system", S->comps[j]);
+            else
+                set_error("submesh %d: %s residual %.3e above tolerance", S->comps[j],
+                          S->dncp ? "flattening" : "harmonic", t.true_res);
+        }
+        if (S->dncp && worst == PGCP_OK) {
+            double area = hres[8 * j + 5], ec = hres[8 * j + 6], sc2 = hres[8 * j + 7];
+            if (area <= 0) {
+                set_error("flattening produced nonpositive signed area (inconsistent input orientation)");
+                if (st) st[j].status = PGCP_E_MESH;
+                worst = PGCP_E_MESH;
+            } else if (ec < -1e-8 * sc2) {
+                set_error("conformal energy %.3e below lower bound", ec);
+                if (st) st[j].status = PGCP_E_SOLVE;
+                worst = PGCP_E_SOLVE;
+            }
+        }
+    }
+    return worst;
+}
+
+int prepare_slots(pgcp_batch* b, SolveSystem* S, const int32_t* comps, int32_t ncomp) {
+    if (!b->has_laplacian) {
+        set_error("laplacian not built");
+        return PGCP_E_INVALID;
+    }
+    if (comps == nullptr) {
+        S->comps.resize(b->K);
+        for (int c = 0; c < b->K; ++c) S->comps[c] = c;
+    } else {
+        S->comps.assign(comps, comps + ncomp);
+        for (int c : S->comps)
+            if (c < 0 || c >= b->K) {
+                set_error("submesh id %d out of range", c);
+                return PGCP_E_INVALID;
+            }
+    }
+    S->nslot = (int32_t)S->comps.size();
+    return PGCP_OK;
+}
+
+}  // namespace
+
+SolveSystem*& system_slot(pgcp_batch* b, int which) {
+    return reinterpret_cast<SolveSystem*&>(b->sys[which]);
+}
+
+int solve_flatten(pgcp_batch* b, const int32_t* comps, int32_t ncomp, const int32_t* pins, const double* targets,
+                  const pgcp_solve_opts* o, double* z, pgcp_solve_stat* st, cudaStream_t s) {
+    SolveSystem*& slot = system_slot(b, 0);
+    delete slot;
+    slot = new SolveSystem();
+    SolveSystem* S = slot;
+    PGCP_TRY(prepare_slots(b, S, comps, ncomp));
+    if (S->nslot == 0) return PGCP_OK;
+    double2 t[2] = {make_double2(0.0, 0.0), make_double2(1.0, 0.0)};
+    if (targets) {
+        t[0] = make_double2(targets[0], targets[1]);
+        t[1] = make_double2(targets[2], targets[3]);
+    }
+    if (t[0].x == t[1].x && t[0].y == t[1].y) {
+        set_error("pin targets must be distinct");
+        return PGCP_E_MESH;
+    }
+    // pins: given (host, local) or the default half-perimeter pins
+    DevBuf<int32_t> dp;
+    PGCP_TRY(dp.alloc(2 * (int64_t)S->nslot, s));
+    std::vector<int32_t> hp(2 * S->nslot);
+    if (pins) {
+        for (int j = 0; j < 2 * S->nslot; ++j) hp[j] = pins[j];
+    } else {
+        if (b->pins.p == nullptr) PGCP_TRY(default_pins(b, s));
+        std::vector<int32_t> all(2 * b->K);
+        PGCP_TRY_CUDA(cudaMemcpyAsync(all.data(), b->pins.p, all.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        PGCP_TRY_CUDA(cudaStreamSynchronize(s));
+        for (int j = 0; j < S->nslot; ++j) {
+            hp[2 * j] = all[2 * S->comps[j]];
+            hp[2 * j + 1] = all[2 * S->comps[j] + 1];
+        }
+    }
+    // pins must be two distinct boundary vertices (flatten.py:154-157)
+    for (int j = 0; j < S->nslot; ++j) {
+        int c = S->comps[j];
+        int64_t nc = b->h_vert_off[c + 1] - b->h_vert_off[c];
+        if (hp[2 * j] == hp[2 * j + 1] || hp[2 * j] < 0 || hp[2 * j + 1] < 0 || hp[2 * j] >= nc || hp[2 * j + 1] >= nc) {
+            set_error("pins must be two distinct boundary vertices");
+            return PGCP_E_MESH;
+        }
+    }
+    if (pins) {  // boundary membership of user pins
+        std::vector<int32_t> hl(b->sum_nb);
+        PGCP_TRY_CUDA(cudaMemcpyAsync(hl.data(), b->loop.p, b->sum_nb * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        PGCP_TRY_CUDA(cudaStreamSynchronize(s));
+        for (int j = 0; j < S->nslot; ++j) {
+            int c = S->comps[j];
+            bool f0 = false, f1 = false;
+            for (int64_t q = b->h_loop_off[c]; q < b->h_loop_off[c + 1]; ++q) {
+                f0 |= hl[q] == hp[2 * j];
+                f1 |= hl[q] == hp[2 * j + 1];
+            }
+            if (!f0 || !f1) {
+                set_error("pins must be two distinct boundary vertices");
+                return PGCP_E_MESH;
+            }
+        }
+    }
+    PGCP_TRY_CUDA(cudaMemcpyAsync(dp.p, hp.data(), hp.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    b->last_flat_pins = hp;
+    PGCP_TRY(build_system(b, S, true, dp.p, t, nullptr, nullptr, 0, s));
+    return run_solve(b, S, o, z, st, s);
+}
+
+int solve_harmonic(pgcp_batch* b, const int32_t* comps, int32_t ncomp, const int32_t* fixed_gid,
+                   const double* fixed_val, int64_t nfixed, const pgcp_solve_opts* o, double* z,
+                   pgcp_solve_stat* st, cudaStream_t s) {
+    SolveSystem*& slot = system_slot(b, 1);
+    delete slot;
+    slot = new SolveSystem();
+    SolveSystem* S = slot;
+    PGCP_TRY(prepare_slots(b, S, comps, ncomp));
+    if (S->nslot == 0) return PGCP_OK;
+    PGCP_TRY(build_system(b, S, false, nullptr, nullptr, fixed_gid, fixed_val, nfixed, s));
+    return run_solve(b, S, o, z, st, s);
+}
+
+int system_dims(pgcp_batch* b, int which, int32_t* nslot_out) {
+    SolveSystem* S = system_slot(b, which);
+    *nslot_out = S ? S->nslot : 0;
+    return PGCP_OK;
+}
+
+
+// Host-side export of the last solve's system in the reference's CSR form,
+// for pattern parity: which = 0 -> C_ff (flatten.py:160-166, real 2|U| rows,
+// exact zeros of L dropped as csr_binop does), which = 1 -> L_II
+// (assemble.py:40, explicit zeros kept). Built from the device Laplacian and
+// the device unknown/fixed maps of that solve.
+int export_system(pgcp_batch* b, int which, int32_t comp, int64_t* dims, int32_t* indptr, int32_t* indices,
+                  double* data, double* rhs, cudaStream_t s) {
+    if (which < 0 || which > 1) {
+        set_error("export_system: which must be 0 or 1");
+        return PGCP_E_INVALID;
+    }
+    SolveSystem* S = system_slot(b, which);
+    if (!S) {
+        set_error("export_system: no %s solve has run", which ? "harmonic" : "flatten");
+        return PGCP_E_INVALID;
+    }
+    int j = -1;
+    for (int q = 0; q < S->nslot; ++q)
+        if (S->comps[q] == comp) j = q;
+    if (j < 0) {
+        set_error("export_system: submesh %d was not part of the last solve", comp);
+        return PGCP_E_INVALID;
+    }
+    const int64_t v0 = b->h_vert_off[comp], nc = b->h_vert_off[comp + 1] - v0;
+    std::vector<int64_t> rp(nc + 1);
+    PGCP_TRY_CUDA(cudaMemcpyAsync(rp.data(), b->row_ptr.p + v0, (nc + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    PGCP_TRY_CUDA(cudaStreamSynchronize(s));
+    const int64_t e0 = rp[0], ne = rp[nc] - rp[0];
+    std::vector<int32_t> cl(ne), fr(nc), ur(nc), lp;
+    std::vector<double> vl(ne);
+    PGCP_TRY_CUDA(cudaMemcpyAsync(cl.data(), b->col.p + e0, ne * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    PGCP_TRY_CUDA(cudaMemcpyAsync(vl.data(), b->val.p + e0, ne * sizeof(double), cudaMemcpyDeviceToHost, s));
+    PGCP_TRY_CUDA(cudaMemcpyAsync(fr.data(), S->fixed_ref.p + S->h_sv_off[j], nc * sizeof(int32_t),
+                                  cudaMemcpyDeviceToHost, s));
+    PGCP_TRY_CUDA(cudaMemcpyAsync(ur.data(), S->urow.p + S->h_sv_off[j], nc * sizeof(int32_t),
+                                  cudaMemcpyDeviceToHost, s));
+    const int64_t lo = b->h_loop_off[comp], nb = b->h_loop_off[comp + 1] - lo;
+    lp.resize(nb);
+    PGCP_TRY_CUDA(cudaMemcpyAsync(lp.data(), b->loop.p + lo, nb * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    const int64_t nU = S->h_nu[j];
+    std::vector<double2> hb(nU > 0 ? nU : 1);
+    if (nU > 0)
+        PGCP_TRY_CUDA(cudaMemcpyAsync(hb.data(), S->b.p + 32 * S->h_sl_off[j], nU * sizeof(double2),
+                                      cudaMemcpyDeviceToHost, s));
+    PGCP_TRY_CUDA(cudaStreamSynchronize(s));
+    const int64_t rbase = 32 * S->h_sl_off[j];
+    std::vector<int64_t> pos(nc, -1);
+    for (int64_t v = 0; v < nc; ++v)
+        if (fr[v] < 0) pos[v] = ur[v] - rbase;
+    std::vector<int64_t> nxt(nc, -1), prv(nc, -1);
+    if (nb >= 3)
+        for (int64_t q = 0; q < nb; ++q) {
+            nxt[lp[q]] = lp[(q + 1) % nb];
+            prv[lp[q]] = lp[(q + nb - 1) % nb];
+        }
+    std::vector<int32_t> ip, ix;
+    std::vector<double> dv;
+    ip.push_back(0);
+    auto push_L = [&](int64_t u, int64_t shift, bool drop_zero) {
+        for (int64_t q = rp[u] - e0; q < rp[u + 1] - e0; ++q) {
+            int64_t c = cl[q];
+            if (pos[c] < 0) continue;
+            if (drop_zero && vl[q] == 0.0) continue;
+            ix.push_back((int32_t)(pos[c] + shift));
+            dv.push_back(vl[q]);
+        }
+    };
+    auto push_cpl = [&](int64_t u, int64_t shift, double sn) {
+        // (next: sn, prev: -sn), sorted by column
+        int64_t a = nxt[u] >= 0 ? pos[nxt[u]] : -1, c = prv[u] >= 0 ? pos[prv[u]] : -1;
+        std::pair<int64_t, double> e[2];
+        int k = 0;
+        if (a >= 0) e[k++] = {a + shift, sn};
+        if (c >= 0) e[k++] = {c + shift, -sn};
+        if (k == 2 && e[1].first < e[0].first) std::swap(e[0], e[1]);
+        for (int t = 0; t < k; ++t) {
+            ix.push_back((int32_t)e[t].first);
+            dv.push_back(e[t].second);
+        }
+    };
+    std::vector<double> hr;
+    std::vector<int64_t> U;
+    for (int64_t v = 0; v < nc; ++v)
+        if (pos[v] >= 0) U.push_back(v);
+    if (which == 0) {
+        for (int64_t r = 0; r < nU; ++r) {  // x rows: L | -2 M_xy
+            push_L(U[r], 0, true);
+            push_cpl(U[r], nU, -0.5);
+            ip.push_back((int32_t)ix.size());
+            hr.push_back(hb[r].x);
+        }
+        for (int64_t r = 0; r < nU; ++r) {  // y rows: 2 M_xy | L
+            push_cpl(U[r], 0, 0.5);
+            push_L(U[r], nU, true);
+            ip.push_back((int32_t)ix.size());
+            hr.push_back(hb[r].y);
+        }
+    } else {
+        for (int64_t r = 0; r < nU; ++r) {
+            push_L(U[r], 0, false);
+            ip.push_back((int32_t)ix.size());
+            hr.push_back(hb[r].x);
+            hr.push_back(hb[r].y);
+        }
+    }
+    dims[0] = (int64_t)ip.size() - 1;
+    dims[1] = (int64_t)ix.size();
+    if (indptr) std::copy(ip.begin(), ip.end(), indptr);
+    if (indices) std::copy(ix.begin(), ix.end(), indices);
+    if (data) std::copy(dv.begin(), dv.end(), data);
+    if (rhs) std::copy(hr.begin(), hr.end(), rhs);
+    return PGCP_OK;
+}
+
+}  // namespace pgcp

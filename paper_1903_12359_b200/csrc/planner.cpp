@@ -1,0 +1,337 @@
+// planner.cpp -- host-side weld-schedule planner (partition.py:149-324).
+//
+// Combinatorial, integer-exact: for every step the reference scans all
+// component pairs (O(K^3 L) overall, 82.6 s at K=256). Here the best run of
+// every *adjacent* pair (components sharing a boundary vertex) is cached and
+// only pairs involving the component that just grew are re-scanned, which
+// gives the identical choice (the key (-len, ca, cb, chain[0]) is a total
+// order over candidates) in O(K * deg * L).
+//
+// Output (two-call protocol): per step 8 int64 of meta
+//   comp_a, comp_b, k, closed, offset, len_a, len_b, len_merged
+// and the concatenated a_cycle | b_cycle | merged_cycle parent ids in idx.
+#include <algorithm>
+#include <cstdint>
+#include <map>
+#include <set>
+#include <string>
+#include <unordered_map>
+#include <unordered_set>
+#include <vector>
+
+#include "common.cuh"
+
+namespace {
+
+using Cycle = std::vector<int64_t>;
+using Runs = std::vector<Cycle>;
+
+// maximal runs of consecutive c1 vertices that are consecutive reversed in
+// c2 (partition.py:149-179); returns false in *full when not a full match
+bool cyclic_runs(const Cycle& c1, const Cycle& c2, Runs* runs, bool* full, std::string* err) {
+    runs->clear();
+    *full = false;
+    const size_t n1 = c1.size(), n2 = c2.size();
+    std::unordered_map<int64_t, int64_t> pos2;
+    pos2.reserve(n2 * 2);
+    for (size_t i = 0; i < n2; ++i) pos2[c2[i]] = (int64_t)i;
+    std::vector<char> ok(n1, 0);
+    bool all = n1 > 0, any = false;
+    for (size_t i = 0; i < n1; ++i) {
+        auto u = pos2.find(c1[i]);
+        auto v = pos2.find(c1[(i + 1) % n1]);
+        if (u != pos2.end() && v != pos2.end() && (v->second + 1) % (int64_t)n2 == u->second) ok[i] = 1;
+        all = all && ok[i];
+        any = any || ok[i];
+    }
+    if (all) {
+        if (n1 != n2) {
+            *err = "inconsistent full-cycle correspondence";
+            return false;
+        }
+        *full = true;
+        return true;
+    }
+    if (!any) return true;
+    size_t start = 0;
+    while (ok[start]) ++start;
+    size_t i = start;
+    for (size_t t = 0; t < n1; ++t) {
+        i = (i + 1) % n1;
+        size_t im1 = (i + n1 - 1) % n1;
+        if (ok[i] && !ok[im1]) {
+            size_t j = i;
+            Cycle chain{c1[j]};
+            while (ok[j % n1]) {
+                chain.push_back(c1[(j + 1) % n1]);
+                ++j;
+            }
+            runs->push_back(std::move(chain));
+        }
+    }
+    return true;
+}
+
+Cycle rotate_to(const Cycle& c, int64_t v) {
+    auto it = std::find(c.begin(), c.end(), v);
+    Cycle out(it, c.end());
+    out.insert(out.end(), c.begin(), it);
+    return out;
+}
+
+struct Step {
+    int64_t ca, cb, k, closed;
+    Cycle a, b, merged;
+};
+
+struct Key {
+    int64_t neglen, ca, cb, first;
+    bool operator<(const Key& o) const {
+        if (neglen != o.neglen) return neglen < o.neglen;
+        if (ca != o.ca) return ca < o.ca;
+        if (cb != o.cb) return cb < o.cb;
+        return first < o.first;
+    }
+};
+
+struct Planner {
+    std::map<int64_t, Cycle> cycles;
+    std::vector<Step> steps;
+    std::string err;
+
+    int glue(int64_t ca, int64_t cb, const Cycle& chain) {
+        std::unordered_set<int64_t> sa(cycles[ca].begin(), cycles[ca].end());
+        std::unordered_set<int64_t> sc(chain.begin(), chain.end());
+        for (int64_t v : cycles[cb])
+            if (sa.count(v) && !sc.count(v)) {
+                err = "components " + std::to_string(ca) + " and " + std::to_string(cb) +
+                      " share vertices beyond one contiguous arc; this cut layout needs multi-arc gluing, which "
+                      "is unsupported";
+                return PGCP_E_PARTITION;
+            }
+        Cycle a = rotate_to(cycles[ca], chain[0]);
+        Cycle rb(cycles[cb].rbegin(), cycles[cb].rend());
+        Cycle b = rotate_to(rb, chain[0]);
+        const int64_t k = (int64_t)chain.size() - 1;
+        if (!std::equal(chain.begin(), chain.end(), a.begin()) || !std::equal(chain.begin(), chain.end(), b.begin())) {
+            err = "arc is not a prefix of both component cycles";
+            return PGCP_E_PARTITION;
+        }
+        Cycle merged{chain.back()};
+        merged.insert(merged.end(), a.begin() + k + 1, a.end());
+        merged.push_back(chain.front());
+        merged.insert(merged.end(), b.rbegin(), b.rend() - (k + 1));
+        steps.push_back({ca, cb, k, 0, a, b, merged});
+        cycles.erase(cb);
+        cycles[ca] = merged;
+        return PGCP_OK;
+    }
+
+    int sphere_close() {
+        auto it = cycles.begin();
+        int64_t ca = it->first, cb = std::next(it)->first;
+        const Cycle& c1 = cycles[ca];
+        const Cycle& c2 = cycles[cb];
+        std::set<int64_t> s1(c1.begin(), c1.end()), s2(c2.begin(), c2.end());
+        if (s1 != s2 || c1.size() != c2.size()) {
+            err = "final two components do not share their full boundary";
+            return PGCP_E_PARTITION;
+        }
+        Runs runs;
+        bool full = false;
+        if (!cyclic_runs(c1, c2, &runs, &full, &err)) return PGCP_E_PARTITION;
+        if (!full) {
+            err = "final boundaries are not a reversed cyclic match";
+            return PGCP_E_PARTITION;
+        }
+        int64_t s = *std::min_element(c1.begin(), c1.end());
+        Cycle a = rotate_to(c1, s);
+        Cycle rb(c2.rbegin(), c2.rend());
+        Cycle b = rotate_to(rb, s);
+        steps.push_back({ca, cb, (int64_t)a.size() - 1, 1, a, b, {}});
+        return PGCP_OK;
+    }
+
+    int check_cover(const int64_t* cuts, int64_t ncuts) {
+        std::set<std::pair<int64_t, int64_t>> glued;
+        for (const Step& st : steps) {
+            std::vector<std::pair<int64_t, int64_t>> pairs;
+            for (int64_t i = 0; i < st.k; ++i) pairs.push_back({st.a[i], st.a[i + 1]});
+            if (st.closed) pairs.push_back({st.a[st.k], st.a[0]});
+            for (auto& e : pairs) {
+                auto key = std::make_pair(std::min(e.first, e.second), std::max(e.first, e.second));
+                if (!glued.insert(key).second) {
+                    err = "edge (" + std::to_string(key.first) + ", " + std::to_string(key.second) +
+                          ") glued twice in the schedule";
+                    return PGCP_E_PARTITION;
+                }
+            }
+        }
+        std::set<std::pair<int64_t, int64_t>> want;
+        for (int64_t i = 0; i < ncuts; ++i) want.insert({cuts[2 * i], cuts[2 * i + 1]});
+        if (glued != want) {
+            size_t missing = 0;
+            for (auto& e : want) missing += glued.count(e) ? 0 : 1;
+            err = "schedule does not cover all cut edges (" + std::to_string(missing) + " missing)";
+            return PGCP_E_PARTITION;
+        }
+        return PGCP_OK;
+    }
+
+    // best candidate of one pair (ca < cb); returns false if none
+    bool pair_best(int64_t ca, int64_t cb, Key* key, Cycle* chain, int* st) {
+        Runs runs;
+        bool full = false;
+        if (!cyclic_runs(cycles[ca], cycles[cb], &runs, &full, &err)) {
+            *st = PGCP_E_PARTITION;
+            return false;
+        }
+        if (full || runs.empty()) return false;
+        bool have = false;
+        for (auto& ch : runs) {
+            Key k{-(int64_t)ch.size(), ca, cb, ch[0]};
+            if (!have || k < *key) {
+                *key = k;
+                *chain = ch;
+                have = true;
+            }
+        }
+        return have;
+    }
+
+    int greedy(int target) {
+        // vertex -> components containing it
+        std::unordered_map<int64_t, std::set<int64_t>> owner;
+        for (auto& kv : cycles)
+            for (int64_t v : kv.second) owner[v].insert(kv.first);
+        std::map<std::pair<int64_t, int64_t>, std::pair<Key, Cycle>> cand;
+        auto rescan = [&](int64_t c) -> int {
+            std::set<int64_t> nb;
+            for (int64_t v : cycles[c])
+                for (int64_t o : owner[v])
+                    if (o != c) nb.insert(o);
+            for (int64_t o : nb) {
+                int64_t a = std::min(c, o), b = std::max(c, o);
+                Key k;
+                Cycle ch;
+                int st = PGCP_OK;
+                if (pair_best(a, b, &k, &ch, &st))
+                    cand[{a, b}] = {k, ch};
+                else
+                    cand.erase({a, b});
+                if (st != PGCP_OK) return st;
+            }
+            return PGCP_OK;
+        };
+        for (auto& kv : cycles) {
+            int st = rescan(kv.first);
+            if (st != PGCP_OK) return st;
+        }
+        while ((int)cycles.size() > target) {
+            if (cand.empty()) {
+                err = "no contiguous shared arc between any two components; multi-arc gluing in one step is "
+                      "unsupported";
+                return PGCP_E_PARTITION;
+            }
+            auto best = cand.begin();
+            for (auto it = cand.begin(); it != cand.end(); ++it)
+                if (it->second.first < best->second.first) best = it;
+            int64_t ca = best->first.first, cb = best->first.second;
+            Cycle chain = best->second.second;
+            // update ownership: cb's vertices now belong to ca
+            for (int64_t v : cycles[cb]) {
+                owner[v].erase(cb);
+                owner[v].insert(ca);
+            }
+            int st = glue(ca, cb, chain);
+            if (st != PGCP_OK) return st;
+            for (auto it = cand.begin(); it != cand.end();) {
+                if (it->first.first == cb || it->first.second == cb || it->first.first == ca ||
+                    it->first.second == ca)
+                    it = cand.erase(it);
+                else
+                    ++it;
+            }
+            std::unordered_set<int64_t> onca(cycles[ca].begin(), cycles[ca].end());
+            for (int64_t v : chain)
+                if (!onca.count(v)) owner[v].erase(ca);
+            st = rescan(ca);
+            if (st != PGCP_OK) return st;
+        }
+        return PGCP_OK;
+    }
+};
+
+}  // namespace
+
+extern "C" PGCP_API int pgcp_plan_weld_schedule(const int64_t* cyc, const int64_t* cyc_off, int32_t K,
+                                                const int64_t* cuts, int64_t ncuts, int mode_sphere,
+                                                const int32_t* pairs, int32_t npairs, int64_t* out_meta,
+                                                int64_t* out_idx, int64_t out_cap, int64_t* out_len) {
+    if (K < 0 || !cyc_off || !out_len) {
+        pgcp::set_error("plan_weld_schedule: invalid arguments");
+        return PGCP_E_INVALID;
+    }
+    Planner P;
+    for (int32_t i = 0; i < K; ++i) P.cycles[i] = Cycle(cyc + cyc_off[i], cyc + cyc_off[i + 1]);
+    int target = mode_sphere ? 2 : 1;
+    if (mode_sphere && K < 2) {
+        pgcp::set_error("sphere mode needs at least 2 submeshes");
+        return PGCP_E_PARTITION;
+    }
+    int st = PGCP_OK;
+    if (pairs && npairs > 0) {
+        for (int32_t q = 0; q < npairs && st == PGCP_OK; ++q) {
+            int64_t ca = std::min(pairs[2 * q], pairs[2 * q + 1]), cb = std::max(pairs[2 * q], pairs[2 * q + 1]);
+            if (!P.cycles.count(ca) || !P.cycles.count(cb)) {
+                P.err = "pair (" + std::to_string(ca) + ", " + std::to_string(cb) + ") is not two live components";
+                st = PGCP_E_PARTITION;
+                break;
+            }
+            Key k;
+            Cycle ch;
+            if (!P.pair_best(ca, cb, &k, &ch, &st)) {
+                if (st == PGCP_OK) {
+                    P.err = "components " + std::to_string(ca) + " and " + std::to_string(cb) + " share no open arc";
+                    st = PGCP_E_PARTITION;
+                }
+                break;
+            }
+            st = P.glue(ca, cb, ch);
+        }
+        if (st == PGCP_OK && (int)P.cycles.size() != target) {
+            P.err = "merge order leaves more than the target components";
+            st = PGCP_E_PARTITION;
+        }
+    } else {
+        st = P.greedy(target);
+    }
+    if (st == PGCP_OK && mode_sphere) st = P.sphere_close();
+    if (st == PGCP_OK) st = P.check_cover(cuts, ncuts);
+    if (st != PGCP_OK) {
+        pgcp::set_error("%s", P.err.c_str());
+        return st;
+    }
+    int64_t need = 0;
+    for (auto& s : P.steps) need += (int64_t)(s.a.size() + s.b.size() + s.merged.size());
+    out_len[0] = (int64_t)P.steps.size();
+    out_len[1] = need;
+    if (!out_meta || !out_idx || out_cap < need) return PGCP_OK;
+    int64_t off = 0;
+    for (size_t i = 0; i < P.steps.size(); ++i) {
+        const Step& s = P.steps[i];
+        int64_t* m = out_meta + 8 * i;
+        m[0] = s.ca;
+        m[1] = s.cb;
+        m[2] = s.k;
+        m[3] = s.closed;
+        m[4] = off;
+        m[5] = (int64_t)s.a.size();
+        m[6] = (int64_t)s.b.size();
+        m[7] = (int64_t)s.merged.size();
+        for (int64_t v : s.a) out_idx[off++] = v;
+        for (int64_t v : s.b) out_idx[off++] = v;
+        for (int64_t v : s.merged) out_idx[off++] = v;
+    }
+    return PGCP_OK;
+}

@@ -1,0 +1,607 @@
+// topology.cu -- device partition of a triangle mesh into disk-type submeshes.
+//
+// Replaces (reference, pure Python):
+//   mesh.py:91-111  TriMesh._validate (index range, repeated vertices,
+//                   repeated directed edge)
+//   mesh.py:146-203 boundary_directed_edges + boundary_loops
+//   mesh.py:206-223 validate_topology (chi, loop count)
+//   partition.py:48-59  validate_cuts
+//   partition.py:94-137 partition_mesh (face adjacency minus cut edges ->
+//                   connected components labelled in order of their minimum
+//                   face -> sorted vertex maps -> disk check -> boundary cycle)
+//
+// Everything is integer work over the face/half-edge arrays (HBM bound);
+// all outputs are deterministic (atomics only build sets whose order is fixed
+// afterwards by sorting or by the stable counting sort).
+#include <climits>
+
+#include "batch.cuh"
+
+namespace pgcp {
+namespace {
+
+enum : int {
+    ERR_FACE_RANGE = 1,
+    ERR_FACE_REPEAT = 2,
+    ERR_DIRECTED_DUP = 3,
+    ERR_VALENCE = 4,
+};
+
+__global__ void k_validate_faces(const int32_t* __restrict__ F, int64_t m, int64_t n, DevErr* err) {
+    GRID_STRIDE(f, m) {
+        int a = F[3 * f], b = F[3 * f + 1], c = F[3 * f + 2];
+        if (a < 0 || b < 0 || c < 0 || a >= n || b >= n || c >= n) {
+            dev_fail(err, ERR_FACE_RANGE, f);
+        } else if (a == b || b == c || c == a) {
+            dev_fail(err, ERR_FACE_REPEAT, f);
+        }
+    }
+}
+
+__global__ void k_count_inc(const int32_t* __restrict__ F, int64_t nc, int32_t* __restrict__ cnt) {
+    GRID_STRIDE(i, nc) { atomicAdd(&cnt[F[i]], 1); }
+}
+
+__global__ void k_fill_inc(const int32_t* __restrict__ F, int64_t m, const int64_t* __restrict__ off,
+                           int32_t* __restrict__ cursor, int32_t* __restrict__ inc) {
+    GRID_STRIDE(i, 3 * m) {
+        int v = F[i];
+        int pos = atomicAdd(&cursor[v], 1);
+        inc[off[v] + pos] = (int32_t)(i / 3);
+    }
+}
+
+// incident faces of every vertex in increasing face order (deterministic)
+__global__ void k_sort_inc(const int64_t* __restrict__ off, int32_t* __restrict__ inc, int64_t n) {
+    GRID_STRIDE(v, n) {
+        int64_t lo = off[v], hi = off[v + 1];
+        for (int64_t i = lo + 1; i < hi; ++i) {
+            int32_t x = inc[i];
+            int64_t j = i - 1;
+            while (j >= lo && inc[j] > x) {
+                inc[j + 1] = inc[j];
+                --j;
+            }
+            inc[j + 1] = x;
+        }
+    }
+}
+
+// half-edge h = 3f+c runs F[f][c] -> F[f][(c+1)%3]
+__device__ __forceinline__ int he_find(const int32_t* __restrict__ F, const int64_t* __restrict__ off,
+                                       const int32_t* __restrict__ inc, int around, int from, int to,
+                                       int skip_face) {
+    for (int64_t e = off[around]; e < off[around + 1]; ++e) {
+        int g = inc[e];
+        if (g == skip_face) continue;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            if (F[3 * g + c] == from && F[3 * g + (c + 1) % 3] == to) return 3 * g + c;
+        }
+    }
+    return -1;
+}
+
+__global__ void k_twin(const int32_t* __restrict__ F, int64_t m, const int64_t* __restrict__ off,
+                       const int32_t* __restrict__ inc, int32_t* __restrict__ twin, DevErr* err) {
+    GRID_STRIDE(h, 3 * m) {
+        int f = (int)(h / 3), c = (int)(h % 3);
+        int a = F[3 * f + c], b = F[3 * f + (c + 1) % 3];
+        // the same directed edge in another face: non-manifold / inconsistent
+        if (he_find(F, off, inc, a, a, b, f) >= 0) dev_fail(err, ERR_DIRECTED_DUP, f);
+        twin[h] = he_find(F, off, inc, b, b, a, f);
+    }
+}
+
+__global__ void k_mark_cuts(const int32_t* __restrict__ F, const int64_t* __restrict__ cuts, int64_t ncuts,
+                            int64_t n, const int64_t* __restrict__ off, const int32_t* __restrict__ inc,
+                            const int32_t* __restrict__ twin, int32_t* __restrict__ mark,
+                            uint8_t* __restrict__ he_cut, int* dup_flag, DevErr* nonedge) {
+    GRID_STRIDE(i, ncuts) {
+        int64_t u = cuts[2 * i], v = cuts[2 * i + 1];
+        if (u < 0 || v < 0 || u >= n || v >= n || u == v) {
+            dev_fail(nonedge, 1, i);
+            continue;
+        }
+        int h = he_find(F, off, inc, (int)u, (int)u, (int)v, -1);
+        if (h < 0) h = he_find(F, off, inc, (int)u, (int)v, (int)u, -1);
+        if (h < 0) {
+            dev_fail(nonedge, 1, i);
+            continue;
+        }
+        int t = twin[h];
+        int canon = (t >= 0 && t < h) ? t : h;
+        if (atomicAdd(&mark[canon], 1) > 0) atomicExch(dup_flag, 1);
+        he_cut[h] = 1;
+        if (t >= 0) he_cut[t] = 1;
+    }
+}
+
+// ----- union-find over faces (hook the larger root under the smaller: the
+// final root of every component is its minimum face index)
+__device__ __forceinline__ int uf_find(int* parent, int x) {
+    while (true) {
+        int p = __ldcg(&parent[x]);
+        if (p == x) return x;
+        int gp = __ldcg(&parent[p]);
+        if (gp != p) parent[x] = gp;  // path halving; only ever points up
+        x = p;
+    }
+}
+
+__global__ void k_uf_init(int* parent, int64_t m) {
+    GRID_STRIDE(f, m) parent[f] = (int)f;
+}
+
+__global__ void k_uf_union(const int32_t* __restrict__ twin, const uint8_t* __restrict__ he_cut,
+                           int64_t m, int* parent) {
+    GRID_STRIDE(h, 3 * m) {
+        int t = twin[h];
+        if (t < 0 || (he_cut && he_cut[h])) continue;
+        int f = (int)(h / 3), g = t / 3;
+        if (g <= f) continue;
+        int a = f, b = g;
+        while (true) {
+            a = uf_find(parent, a);
+            b = uf_find(parent, b);
+            if (a == b) break;
+            if (a < b) {
+                int tmp = a;
+                a = b;
+                b = tmp;
+            }
+            if (atomicCAS(&parent[a], a, b) == a) break;
+        }
+    }
+}
+
+__global__ void k_uf_roots(int* parent, int64_t m, int32_t* __restrict__ is_root) {
+    GRID_STRIDE(f, m) {
+        int r = uf_find(parent, (int)f);
+        is_root[f] = (r == (int)f) ? 1 : 0;
+    }
+}
+
+__global__ void k_face_comp(int* parent, int64_t m, const int64_t* __restrict__ rank,
+                            int32_t* __restrict__ face_comp) {
+    GRID_STRIDE(f, m) {
+        int r = uf_find(parent, (int)f);
+        face_comp[f] = (int32_t)rank[r];
+    }
+}
+
+// ----- local vertices: (parent vertex, submesh) pairs
+constexpr int MAX_VCOMP = 64;
+
+__device__ int distinct_comps(const int64_t* __restrict__ off, const int32_t* __restrict__ inc,
+                              const int32_t* __restrict__ face_comp, int64_t v, int* buf) {
+    int k = 0;
+    for (int64_t e = off[v]; e < off[v + 1]; ++e) {
+        int c = face_comp[inc[e]];
+        bool seen = false;
+        for (int j = 0; j < k; ++j) seen |= (buf[j] == c);
+        if (!seen) {
+            if (k == MAX_VCOMP) return -1;
+            // insertion into the sorted prefix
+            int j = k - 1;
+            while (j >= 0 && buf[j] > c) {
+                buf[j + 1] = buf[j];
+                --j;
+            }
+            buf[j + 1] = c;
+            ++k;
+        }
+    }
+    return k;
+}
+
+__global__ void k_lv_count(const int64_t* __restrict__ off, const int32_t* __restrict__ inc,
+                           const int32_t* __restrict__ face_comp, int64_t n, int32_t* __restrict__ cnt,
+                           DevErr* err) {
+    int buf[MAX_VCOMP];
+    GRID_STRIDE(v, n) {
+        int k = distinct_comps(off, inc, face_comp, v, buf);
+        if (k < 0) {
+            dev_fail(err, ERR_VALENCE, v);
+            k = 0;
+        }
+        cnt[v] = k;
+    }
+}
+
+__global__ void k_lv_fill(const int64_t* __restrict__ off, const int32_t* __restrict__ inc,
+                          const int32_t* __restrict__ face_comp, int64_t n, const int64_t* __restrict__ lv_off,
+                          int32_t* __restrict__ lv_comp, int32_t* __restrict__ lv_vert) {
+    int buf[MAX_VCOMP];
+    GRID_STRIDE(v, n) {
+        int k = distinct_comps(off, inc, face_comp, v, buf);
+        int64_t o = lv_off[v];
+        for (int j = 0; j < k; ++j) {
+            lv_comp[o + j] = buf[j];
+            lv_vert[o + j] = (int32_t)v;
+        }
+    }
+}
+
+__global__ void k_lv_gid(const int32_t* __restrict__ perm, int64_t ne, const int32_t* __restrict__ lv_vert,
+                         const int32_t* __restrict__ lv_comp, int32_t* __restrict__ lv_gid,
+                         int32_t* __restrict__ vmap, int32_t* __restrict__ comp_of_gid) {
+    GRID_STRIDE(p, ne) {
+        int e = perm[p];
+        lv_gid[e] = (int32_t)p;
+        vmap[p] = lv_vert[e];
+        comp_of_gid[p] = lv_comp[e];
+    }
+}
+
+__device__ __forceinline__ int lv_find(const int64_t* __restrict__ lv_off, const int32_t* __restrict__ lv_comp,
+                                       const int32_t* __restrict__ lv_gid, int v, int c) {
+    for (int64_t e = lv_off[v]; e < lv_off[v + 1]; ++e)
+        if (lv_comp[e] == c) return lv_gid[e];
+    return -1;
+}
+
+__global__ void k_face_count(const int32_t* __restrict__ face_comp, int64_t m, int32_t* __restrict__ fcnt) {
+    GRID_STRIDE(f, m) atomicAdd(&fcnt[face_comp[f]], 1);
+}
+
+// boundary half-edges of every submesh (twin absent or in another submesh)
+// and of the parent mesh (twin absent)
+__global__ void k_boundary(const int32_t* __restrict__ F, int64_t m, const int32_t* __restrict__ twin,
+                           const int32_t* __restrict__ face_comp, const int64_t* __restrict__ lv_off,
+                           const int32_t* __restrict__ lv_comp, const int32_t* __restrict__ lv_gid,
+                           int32_t* __restrict__ nxt, int32_t* __restrict__ bcnt, int32_t* __restrict__ start,
+                           int32_t* __restrict__ comp_bad, int32_t* __restrict__ pnxt, int32_t* pcount,
+                           int32_t* pstart, int32_t* pbad) {
+    GRID_STRIDE(h, 3 * m) {
+        int f = (int)(h / 3), c = (int)(h % 3);
+        int a = F[3 * f + c], b = F[3 * f + (c + 1) % 3];
+        int t = twin[h];
+        int cf = face_comp[f];
+        if (t < 0) {
+            atomicAdd(pcount, 1);
+            if (atomicCAS(&pnxt[a], -1, b) != -1) atomicExch(pbad, 1);
+            atomicMin(pstart, a);
+        }
+        if (t < 0 || face_comp[t / 3] != cf) {
+            int ga = lv_find(lv_off, lv_comp, lv_gid, a, cf);
+            int gb = lv_find(lv_off, lv_comp, lv_gid, b, cf);
+            atomicAdd(&bcnt[cf], 1);
+            if (atomicCAS(&nxt[ga], -1, gb) != -1) atomicExch(&comp_bad[cf], 1);
+            atomicMin(&start[cf], ga);
+        }
+    }
+}
+
+// one thread per submesh: chi, loop walk from the smallest boundary vertex
+__global__ void k_walk(int32_t K, const int64_t* __restrict__ vert_off, const int32_t* __restrict__ fcnt,
+                       const int32_t* __restrict__ bcnt, const int32_t* __restrict__ start,
+                       const int32_t* __restrict__ nxt, const int64_t* __restrict__ loop_off,
+                       int32_t* __restrict__ loop, int32_t* __restrict__ comp_bad, int32_t* __restrict__ chi_out,
+                       int32_t* __restrict__ loops_out) {
+    GRID_STRIDE(c, K) {
+        int64_t nc = vert_off[c + 1] - vert_off[c];
+        int64_t mc = fcnt[c], bc = bcnt[c];
+        int64_t twoE = 3 * mc + bc;
+        int64_t chi = nc - twoE / 2 + mc;
+        chi_out[c] = (int32_t)chi;
+        int loops = 0;
+        bool bad = comp_bad[c] != 0 || (twoE & 1);
+        if (!bad && bc > 0) {
+            int s = start[c];
+            int cur = s;
+            int64_t j = 0;
+            int64_t base = loop_off[c];
+            do {
+                if (j >= bc) {
+                    bad = true;
+                    break;
+                }
+                loop[base + j] = (int32_t)(cur - vert_off[c]);
+                ++j;
+                cur = nxt[cur];
+                if (cur < 0) {
+                    bad = true;
+                    break;
+                }
+            } while (cur != s);
+            loops = bad ? -1 : (j == bc ? 1 : -2);
+        } else if (bad) {
+            loops = -1;
+        }
+        loops_out[c] = loops;
+        if (bad || !(chi == 1 && loops == 1)) comp_bad[c] = 1;
+    }
+}
+
+__global__ void k_parent_walk(const int32_t* __restrict__ pnxt, const int32_t* pcount, const int32_t* pstart,
+                              const int32_t* pbad, int64_t* out_loops) {
+    if (blockIdx.x || threadIdx.x) return;
+    int pb = *pcount;
+    if (*pbad) {
+        *out_loops = -1;
+        return;
+    }
+    if (pb == 0) {
+        *out_loops = 0;
+        return;
+    }
+    int s = *pstart, cur = s;
+    int64_t j = 0;
+    do {
+        ++j;
+        cur = pnxt[cur];
+        if (cur < 0 || j > pb) {
+            *out_loops = -1;
+            return;
+        }
+    } while (cur != s);
+    *out_loops = (j == pb) ? 1 : -2;
+}
+
+__global__ void k_fill_i32(int32_t* p, int64_t n, int32_t v) {
+    GRID_STRIDE(i, n) p[i] = v;
+}
+
+__global__ void k_local_faces(const int32_t* __restrict__ F, const int32_t* __restrict__ perm, int64_t m,
+                              const int32_t* __restrict__ face_comp, const int64_t* __restrict__ lv_off,
+                              const int32_t* __restrict__ lv_comp, const int32_t* __restrict__ lv_gid,
+                              const int64_t* __restrict__ vert_off, int32_t* __restrict__ out) {
+    GRID_STRIDE(p, m) {
+        int f = perm[p];
+        int c = face_comp[f];
+        for (int j = 0; j < 3; ++j) {
+            int g = lv_find(lv_off, lv_comp, lv_gid, F[3 * f + j], c);
+            out[3 * p + j] = (int32_t)(g - vert_off[c]);
+        }
+    }
+}
+
+const char* face_err_text(int code) {
+    switch (code) {
+        case ERR_FACE_RANGE: return "face index out of range";
+        case ERR_FACE_REPEAT: return "has repeated vertices";
+        case ERR_DIRECTED_DUP: return "inconsistent orientation or non-manifold edge (directed edge repeated)";
+        default: return "invalid mesh";
+    }
+}
+
+int read_err(DevBuf<DevErr>& e, DevErr* h, cudaStream_t s) {
+    PGCP_TRY_CUDA(cudaMemcpyAsync(h, e.p, sizeof(DevErr), cudaMemcpyDeviceToHost, s));
+    PGCP_TRY_CUDA(cudaStreamSynchronize(s));
+    return PGCP_OK;
+}
+
+int reset_err(DevBuf<DevErr>& e, cudaStream_t s) {
+    DevErr h{0, 0, ~0ull, 0};
+    PGCP_TRY_CUDA(cudaMemcpyAsync(e.p, &h, sizeof(DevErr), cudaMemcpyHostToDevice, s));
+    PGCP_TRY_CUDA(cudaStreamSynchronize(s));  // h is a stack temporary
+    return PGCP_OK;
+}
+
+}  // namespace
+
+int build_partition(pgcp_batch* b, const int64_t* cuts, int64_t ncuts, bool no_cuts, cudaStream_t s) {
+    const int64_t n = b->n, m = b->m;
+    const int BT = 256;
+    DevBuf<DevErr> err;
+    PGCP_TRY(err.alloc(1, s));
+    PGCP_TRY(reset_err(err, s));
+    DevErr herr;
+
+    // --- parent validation (mesh.py:91-111)
+    k_validate_faces<<<grid_for(m, BT), BT, 0, s>>>(b->F.p, m, n, err.p);
+    PGCP_LAUNCH_CHECK();
+    PGCP_TRY(read_err(err, &herr, s));
+    if (herr.code) {
+        if (herr.code == ERR_FACE_RANGE)
+            set_error("face index out of range [0, %lld)", (long long)n);
+        else
+            set_error("face %llu has repeated vertices", herr.index);
+        return PGCP_E_MESH;
+    }
+
+    // --- vertex -> face incidence, sorted by face id
+    {
+        DevBuf<int32_t> cnt;
+        PGCP_TRY(cnt.alloc(n, s));
+        PGCP_TRY(cnt.zero(s));
+        k_count_inc<<<grid_for(3 * m, BT), BT, 0, s>>>(b->F.p, 3 * m, cnt.p);
+        PGCP_LAUNCH_CHECK();
+        PGCP_TRY(b->inc_off.alloc(n + 1, s));
+        PGCP_TRY(exclusive_scan_i32_to_i64(cnt.p, b->inc_off.p, n, s));
+        PGCP_TRY(cnt.zero(s));
+        PGCP_TRY(b->inc.alloc(3 * m, s));
+        k_fill_inc<<<grid_for(3 * m, BT), BT, 0, s>>>(b->F.p, m, b->inc_off.p, cnt.p, b->inc.p);
+        PGCP_LAUNCH_CHECK();
+        k_sort_inc<<<grid_for(n, BT), BT, 0, s>>>(b->inc_off.p, b->inc.p, n);
+        PGCP_LAUNCH_CHECK();
+    }
+
+    // --- half-edge twins + repeated directed edges
+    PGCP_TRY(b->twin.alloc(3 * m, s));
+    k_twin<<<grid_for(3 * m, BT), BT, 0, s>>>(b->F.p, m, b->inc_off.p, b->inc.p, b->twin.p, err.p);
+    PGCP_LAUNCH_CHECK();
+    PGCP_TRY(read_err(err, &herr, s));
+    if (herr.code) {
+        set_error("%s", face_err_text(herr.code));
+        return PGCP_E_MESH;
+    }
+
+    // --- cut edges (partition.py:48-59)
+    PGCP_TRY(b->he_cut.alloc(3 * m, s));
+    PGCP_TRY(b->he_cut.zero(s));
+    if (!no_cuts && ncuts > 0) {
+        DevBuf<int32_t> mark, dup;
+        PGCP_TRY(mark.alloc(3 * m, s));
+        PGCP_TRY(mark.zero(s));
+        PGCP_TRY(dup.alloc(1, s));
+        PGCP_TRY(dup.zero(s));
+        k_mark_cuts<<<grid_for(ncuts, BT), BT, 0, s>>>(b->F.p, cuts, ncuts, n, b->inc_off.p, b->inc.p,
+                                                      b->twin.p, mark.p, b->he_cut.p, dup.p, err.p);
+        PGCP_LAUNCH_CHECK();
+        int hdup = 0;
+        PGCP_TRY(fetch_scalar(dup.p, &hdup, s));
+        PGCP_TRY(read_err(err, &herr, s));
+        if (hdup) {
+            set_error("duplicate cut edges");
+            return PGCP_E_PARTITION;
+        }
+        if (herr.code) {
+            int64_t pair[2] = {-1, -1};
+            PGCP_TRY_CUDA(cudaMemcpyAsync(pair, cuts + 2 * herr.index, sizeof(pair), cudaMemcpyDeviceToHost, s));
+            PGCP_TRY_CUDA(cudaStreamSynchronize(s));
+            int64_t lo = pair[0] < pair[1] ? pair[0] : pair[1];
+            int64_t hi = pair[0] < pair[1] ? pair[1] : pair[0];
+            set_error("cut pair (%lld, %lld) is not a mesh edge", (long long)lo + 1, (long long)hi + 1);
+            return PGCP_E_PARTITION;
+        }
+    }
+
+    // --- connected components of the face graph minus cut edges
+    {
+        DevBuf<int> parent;
+        DevBuf<int32_t> is_root;
+        DevBuf<int64_t> rank;
+        PGCP_TRY(parent.alloc(m, s));
+        PGCP_TRY(is_root.alloc(m, s));
+        PGCP_TRY(rank.alloc(m + 1, s));
+        k_uf_init<<<grid_for(m, BT), BT, 0, s>>>(parent.p, m);
+        PGCP_LAUNCH_CHECK();
+        k_uf_union<<<grid_for(3 * m, BT), BT, 0, s>>>(b->twin.p, no_cuts ? nullptr : b->he_cut.p, m, parent.p);
+        PGCP_LAUNCH_CHECK();
+        k_uf_roots<<<grid_for(m, BT), BT, 0, s>>>(parent.p, m, is_root.p);
+        PGCP_LAUNCH_CHECK();
+        PGCP_TRY(exclusive_scan_i32_to_i64(is_root.p, rank.p, m, s));
+        PGCP_TRY(b->face_comp.alloc(m, s));
+        k_face_comp<<<grid_for(m, BT), BT, 0, s>>>(parent.p, m, rank.p, b->face_comp.p);
+        PGCP_LAUNCH_CHECK();
+        int64_t K = 0;
+        PGCP_TRY(fetch_scalar(rank.p + m, &K, s));
+        b->K = (int32_t)K;
+    }
+    const int32_t K = b->K;
+    if (K <= 0) {
+        set_error("mesh has no faces");
+        return PGCP_E_MESH;
+    }
+
+    // --- local vertices, grouped by submesh with sorted parent ids
+    DevBuf<int32_t> lv_vert, perm;
+    {
+        DevBuf<int32_t> cnt;
+        PGCP_TRY(cnt.alloc(n, s));
+        k_lv_count<<<grid_for(n, BT), BT, 0, s>>>(b->inc_off.p, b->inc.p, b->face_comp.p, n, cnt.p, err.p);
+        PGCP_LAUNCH_CHECK();
+        PGCP_TRY(b->lv_off.alloc(n + 1, s));
+        PGCP_TRY(exclusive_scan_i32_to_i64(cnt.p, b->lv_off.p, n, s));
+        PGCP_TRY(fetch_scalar(b->lv_off.p + n, &b->sum_n, s));
+        PGCP_TRY(read_err(err, &herr, s));
+        if (herr.code) {
+            set_error("vertex %llu touches more than %d submeshes", herr.index, MAX_VCOMP);
+            return PGCP_E_PARTITION;
+        }
+    }
+    const int64_t E = b->sum_n;
+    PGCP_TRY(b->lv_comp.alloc(E, s));
+    PGCP_TRY(lv_vert.alloc(E, s));
+    k_lv_fill<<<grid_for(n, BT), BT, 0, s>>>(b->inc_off.p, b->inc.p, b->face_comp.p, n, b->lv_off.p,
+                                           b->lv_comp.p, lv_vert.p);
+    PGCP_LAUNCH_CHECK();
+    PGCP_TRY(perm.alloc(E, s));
+    PGCP_TRY(b->vert_off.alloc(K + 1, s));
+    PGCP_TRY(stable_counting_sort(b->lv_comp.p, E, K, perm.p, b->vert_off.p, s));
+    PGCP_TRY(b->lv_gid.alloc(E, s));
+    PGCP_TRY(b->vmap.alloc(E, s));
+    PGCP_TRY(b->comp_of_gid.alloc(E, s));
+    k_lv_gid<<<grid_for(E, BT), BT, 0, s>>>(perm.p, E, lv_vert.p, b->lv_comp.p, b->lv_gid.p, b->vmap.p,
+                                          b->comp_of_gid.p);
+    PGCP_LAUNCH_CHECK();
+
+    // --- boundaries, topology, loops
+    DevBuf<int32_t> fcnt, bcnt, start, bad, chi, loops, pnxt, pscal;
+    PGCP_TRY(fcnt.alloc(K, s));
+    PGCP_TRY(fcnt.zero(s));
+    PGCP_TRY(bcnt.alloc(K, s));
+    PGCP_TRY(bcnt.zero(s));
+    PGCP_TRY(start.alloc(K, s));
+    PGCP_TRY(bad.alloc(K, s));
+    PGCP_TRY(bad.zero(s));
+    PGCP_TRY(chi.alloc(K, s));
+    PGCP_TRY(loops.alloc(K, s));
+    PGCP_TRY(pnxt.alloc(n, s));
+    PGCP_TRY(pscal.alloc(3, s));  // count, start, bad
+    PGCP_TRY(b->nxt.alloc(E, s));
+    k_fill_i32<<<grid_for(K, BT), BT, 0, s>>>(start.p, K, INT_MAX);
+    k_fill_i32<<<grid_for(E, BT), BT, 0, s>>>(b->nxt.p, E, -1);
+    k_fill_i32<<<grid_for(n, BT), BT, 0, s>>>(pnxt.p, n, -1);
+    {
+        int32_t init[3] = {0, INT_MAX, 0};
+        PGCP_TRY_CUDA(cudaMemcpyAsync(pscal.p, init, sizeof(init), cudaMemcpyHostToDevice, s));
+        PGCP_TRY_CUDA(cudaStreamSynchronize(s));
+    }
+    k_face_count<<<grid_for(m, BT), BT, 0, s>>>(b->face_comp.p, m, fcnt.p);
+    PGCP_LAUNCH_CHECK();
+    k_boundary<<<grid_for(3 * m, BT), BT, 0, s>>>(b->F.p, m, b->twin.p, b->face_comp.p, b->lv_off.p,
+                                                b->lv_comp.p, b->lv_gid.p, b->nxt.p, bcnt.p, start.p, bad.p,
+                                                pnxt.p, pscal.p, pscal.p + 1, pscal.p + 2);
+    PGCP_LAUNCH_CHECK();
+    PGCP_TRY(b->loop_off.alloc(K + 1, s));
+    PGCP_TRY(exclusive_scan_i32_to_i64(bcnt.p, b->loop_off.p, K, s));
+    PGCP_TRY(fetch_scalar(b->loop_off.p + K, &b->sum_nb, s));
+    PGCP_TRY(b->loop.alloc(b->sum_nb, s));
+    k_walk<<<grid_for(K, 64), 64, 0, s>>>(K, b->vert_off.p, fcnt.p, bcnt.p, start.p, b->nxt.p, b->loop_off.p,
+                                         b->loop.p, bad.p, chi.p, loops.p);
+    PGCP_LAUNCH_CHECK();
+    DevBuf<int64_t> ploops;
+    PGCP_TRY(ploops.alloc(1, s));
+    k_parent_walk<<<1, 32, 0, s>>>(pnxt.p, pscal.p, pscal.p + 1, pscal.p + 2, ploops.p);
+    PGCP_LAUNCH_CHECK();
+
+    // --- host copies of the small per-submesh tables
+    b->h_vert_off.resize(K + 1);
+    b->h_loop_off.resize(K + 1);
+    b->h_comp_chi.resize(K);
+    b->h_comp_loops.resize(K);
+    std::vector<int32_t> hbad(K), hp(3);
+    PGCP_TRY_CUDA(cudaMemcpyAsync(b->h_vert_off.data(), b->vert_off.p, (K + 1) * sizeof(int64_t),
+                                  cudaMemcpyDeviceToHost, s));
+    PGCP_TRY_CUDA(cudaMemcpyAsync(b->h_loop_off.data(), b->loop_off.p, (K + 1) * sizeof(int64_t),
+                                  cudaMemcpyDeviceToHost, s));
+    PGCP_TRY_CUDA(cudaMemcpyAsync(b->h_comp_chi.data(), chi.p, K * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    PGCP_TRY_CUDA(cudaMemcpyAsync(b->h_comp_loops.data(), loops.p, K * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    PGCP_TRY_CUDA(cudaMemcpyAsync(hbad.data(), bad.p, K * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    PGCP_TRY_CUDA(cudaMemcpyAsync(hp.data(), pscal.p, 3 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    int64_t hploops = 0;
+    PGCP_TRY_CUDA(cudaMemcpyAsync(&hploops, ploops.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    PGCP_TRY_CUDA(cudaStreamSynchronize(s));
+    // parent topology (mesh.py:206-223): chi = n - E + m with 2E = 3m + b
+    int64_t pb = hp[0];
+    b->parent_chi = n - (3 * m + pb) / 2 + m;
+    b->parent_loops = hploops;
+    b->bad_comp = -1;
+    for (int c = 0; c < K; ++c) {
+        if (hbad[c]) {
+            b->bad_comp = c;
+            break;
+        }
+    }
+    return PGCP_OK;
+}
+
+int local_faces(pgcp_batch* b, int64_t* face_off, int32_t* faces, cudaStream_t s) {
+    const int64_t m = b->m;
+    DevBuf<int32_t> perm;
+    DevBuf<int64_t> off;
+    PGCP_TRY(perm.alloc(m, s));
+    PGCP_TRY(off.alloc(b->K + 1, s));
+    PGCP_TRY(stable_counting_sort(b->face_comp.p, m, b->K, perm.p, off.p, s));
+    k_local_faces<<<grid_for(m, 256), 256, 0, s>>>(b->F.p, perm.p, m, b->face_comp.p, b->lv_off.p, b->lv_comp.p,
+                                                   b->lv_gid.p, b->vert_off.p, faces);
+    PGCP_LAUNCH_CHECK();
+    PGCP_TRY_CUDA(cudaMemcpyAsync(face_off, off.p, (b->K + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    PGCP_TRY_CUDA(cudaStreamSynchronize(s));
+    return PGCP_OK;
+}
+
+}  // namespace pgcp

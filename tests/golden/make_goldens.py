@@ -1,0 +1,322 @@
+"""Generate golden fixtures by running the REFERENCE implementation.
+
+Run in the build container (the reference is not on the GPU box):
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_goldens.py
+
+Every number stored here comes from the reference package `pgcp`
+(`/root/reference/pkg/src/pgcp`). Stage-wise intermediates are captured by
+wrapping the reference's own batch seam `pipeline._run_tasks`
+(`pipeline.py:105-109`) and its weld entry points as the pipeline calls them
+(`pipeline.py:184-204`), so nothing is re-derived outside the reference.
+Inputs are the repo's seeded generators (`paper_1903_12359_b200.generators`).
+"""
+
+import json
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.abspath(os.path.join(HERE, "..", "..")))
+
+import pgcp  # noqa: E402  (the reference)
+from pgcp import pipeline as ref_pipeline  # noqa: E402
+from pgcp import shapes as ref_shapes  # noqa: E402
+from scipy import sparse  # noqa: E402
+
+from paper_1903_12359_b200 import generators as gen  # noqa: E402
+
+
+def pack(out, name, arrays, dtype=None):
+    arrays = [np.asarray(a) if dtype is None else np.asarray(a, dtype=dtype) for a in arrays]
+    off = np.zeros(len(arrays) + 1, dtype=np.int64)
+    off[1:] = np.cumsum([len(a) for a in arrays])
+    out[name + "_off"] = off
+    out[name] = np.concatenate(arrays) if arrays else np.zeros(0)
+
+
+def pack_csr(out, name, mats, values=True):
+    pack(out, name + "_indptr", [m.indptr for m in mats], np.int32)
+    pack(out, name + "_indices", [m.indices for m in mats], np.int32)
+    if values:
+        pack(out, name + "_data", [m.data for m in mats], np.float64)
+
+
+def capture_run(V, F, cuts, mode, schedule_pairs=None):
+    """Run pgcp.parameterize and capture every stage's inputs/outputs."""
+    cap = {"tasks": [], "welds": [], "geo": None}
+    orig_run = ref_pipeline._run_tasks
+    orig_pw = ref_pipeline.partial_weld
+    orig_cw = ref_pipeline.closed_weld
+    orig_geo = ref_pipeline.geodesic_to_circle
+    orig_plan = ref_pipeline.plan_weld_schedule
+
+    def run_tasks(task, argslist, workers):
+        res = orig_run(task, argslist, workers)
+        cap["tasks"].append((task.__name__, argslist, res))
+        return res
+
+    def pw(a, b, k, hard_tol=1e-6):
+        r = orig_pw(a, b, k, hard_tol=hard_tol)
+        cap["welds"].append(("partial", np.array(a), np.array(b), k, r))
+        return r
+
+    def cw(a, b, hard_tol=1e-6):
+        r = orig_cw(a, b, hard_tol=hard_tol)
+        cap["welds"].append(("closed", np.array(a), np.array(b), len(a) - 1, r))
+        return r
+
+    def geo(points, interior=None):
+        r = orig_geo(points, interior)
+        cap["geo"] = (np.array(points), r[0])
+        return r
+
+    def plan(part, mode="free"):
+        if schedule_pairs is None:
+            steps = orig_plan(part, mode)
+        else:
+            steps = pairs_plan(part, schedule_pairs)
+        cap["steps"] = steps
+        return steps
+
+    ref_pipeline._run_tasks = run_tasks
+    ref_pipeline.partial_weld = pw
+    ref_pipeline.closed_weld = cw
+    ref_pipeline.geodesic_to_circle = geo
+    ref_pipeline.plan_weld_schedule = plan
+    try:
+        mesh = pgcp.TriMesh(V, F)
+        gp, rep = pgcp.parameterize(mesh, cuts, mode)
+    finally:
+        ref_pipeline._run_tasks = orig_run
+        ref_pipeline.partial_weld = orig_pw
+        ref_pipeline.closed_weld = orig_cw
+        ref_pipeline.geodesic_to_circle = orig_geo
+        ref_pipeline.plan_weld_schedule = orig_plan
+    return mesh, gp, rep, cap
+
+
+def pairs_plan(part, pairs):
+    """WeldSteps for an explicit merge order, built from the reference's own
+    planner primitives (`partition._cyclic_runs`, `_rotate_to`, `WeldStep`)."""
+    from pgcp import partition as P
+    cycles = {i: list(map(int, c)) for i, c in enumerate(part.boundary_cycles)}
+    steps = []
+    for ca, cb in pairs:
+        runs = P._cyclic_runs(cycles[ca], cycles[cb])
+        chain = min(runs, key=lambda ch: (-len(ch), ch[0]))
+        a_cycle = P._rotate_to(cycles[ca], chain[0])
+        b_cycle = P._rotate_to(list(reversed(cycles[cb])), chain[0])
+        k = len(chain) - 1
+        merged = [chain[-1]] + a_cycle[k + 1:] + [chain[0]] + list(reversed(b_cycle[k + 1:]))
+        steps.append(P.WeldStep(ca, cb, np.array(a_cycle), np.array(b_cycle), k, False,
+                                np.array(merged)))
+        del cycles[cb]
+        cycles[ca] = merged
+    return steps
+
+
+def stagewise_systems(sub_meshes, pins_list, g_list):
+    """Reference-built L, C_ff and L_II for each submesh, via the reference's
+    functions and the exact expressions of `flatten.py:157-166` /
+    `assemble.py:34-41`."""
+    Ls, Cffs, rhs_f, Liis, rhs_h = [], [], [], [], []
+    for sub, pins, g in zip(sub_meshes, pins_list, g_list):
+        n = sub.n_vertices
+        loops = pgcp.boundary_loops(sub)
+        L = pgcp.cotangent_laplacian(sub)
+        M = pgcp.area_matrix(sub, loops)
+        C = sparse.block_diag([L, L], format="csr") - 2.0 * M
+        p0, p1 = pins
+        fixed = np.array([p0, p1, p0 + n, p1 + n])
+        free = np.setdiff1d(np.arange(2 * n), fixed)
+        Cff = C[free][:, free]
+        rf = -C[free][:, fixed] @ np.array([0.0, 1.0, 0.0, 0.0])
+        loop = loops[0]
+        interior = np.setdiff1d(np.arange(n), loop)
+        Lii = L[interior][:, interior]
+        rh = -(L[interior][:, loop] @ g) if g is not None else np.zeros(len(interior), complex)
+        Ls.append(L)
+        Cffs.append(Cff.tocsr())
+        rhs_f.append(rf)
+        Liis.append(Lii.tocsr())
+        rhs_h.append(rh)
+    return Ls, Cffs, rhs_f, Liis, rhs_h
+
+
+def pipeline_case(name, V, F, cuts, mode, schedule_pairs=None, stagewise=True):
+    out = {"V": V, "F": np.asarray(F, dtype=np.int32),
+           "cuts": np.zeros((0, 2), np.int64) if cuts is None else np.asarray(cuts, np.int64),
+           "mode": np.array(mode)}
+    mesh, gp, rep, cap = capture_run(V, F, cuts, mode, schedule_pairs)
+    if cuts is None or len(cuts) == 0:
+        subs = [mesh]
+        vmaps = [np.arange(mesh.n_vertices)]
+        fa = np.zeros(mesh.n_faces, np.int64)
+        cycles = [pgcp.boundary_loops(mesh)[0]]
+    else:
+        part = pgcp.partition_mesh(mesh, cuts)
+        subs, vmaps, fa, cycles = part.submeshes, part.vertex_maps, part.face_assignment, part.boundary_cycles
+    out["face_assignment"] = fa
+    pack(out, "vertex_maps", vmaps, np.int64)
+    pack(out, "cycles", cycles, np.int64)
+    pack(out, "loops", [pgcp.boundary_loops(s)[0] for s in subs], np.int64)
+    steps = cap.get("steps", [])
+    out["step_meta"] = np.array([[s.comp_a, s.comp_b, s.k, int(s.closed)] for s in steps],
+                                dtype=np.int64).reshape(-1, 4)
+    pack(out, "step_a", [s.a_cycle for s in steps], np.int64)
+    pack(out, "step_b", [s.b_cycle for s in steps], np.int64)
+    pack(out, "step_merged", [s.merged_cycle for s in steps], np.int64)
+    tasks = {t[0]: t for t in cap["tasks"]}
+    flat = tasks["_dncp_task"][2]
+    pack(out, "flat", flat, np.complex128)
+    pins = [pgcp.flatten.default_pins(pgcp.boundary_loops(s)[0], s.vertices) for s in subs]
+    out["pins"] = np.array(pins, dtype=np.int64).reshape(-1, 2)
+    g_list = [None] * len(subs)
+    if "_harmonic_task" in tasks:
+        hargs = tasks["_harmonic_task"][1]
+        g_list = [a[3] for a in hargs]
+        pack(out, "harm_g", g_list, np.complex128)
+        pack(out, "harm", [r[0] for r in tasks["_harmonic_task"][2]], np.complex128)
+        out["flips_before"] = np.array([r[1]["flips_before"] for r in tasks["_harmonic_task"][2]])
+    # welds: inputs and outputs of every partial/closed weld as the pipeline called it
+    pack(out, "weld_in_a", [w[1] for w in cap["welds"]], np.complex128)
+    pack(out, "weld_in_b", [w[2] for w in cap["welds"]], np.complex128)
+    pack(out, "weld_out_a", [w[4].a for w in cap["welds"]], np.complex128)
+    pack(out, "weld_out_b", [w[4].b for w in cap["welds"]], np.complex128)
+    out["weld_k"] = np.array([w[3] for w in cap["welds"]], dtype=np.int64)
+    out["weld_closed"] = np.array([w[0] == "closed" for w in cap["welds"]])
+    out["weld_seam"] = np.array([w[4].seam_error for w in cap["welds"]])
+    if cap["geo"] is not None:
+        out["geo_in"], out["geo_out"] = cap["geo"]
+    if stagewise:
+        Ls, Cffs, rf, Liis, rh = stagewise_systems(subs, pins, g_list)
+        pack_csr(out, "L", Ls)
+        pack_csr(out, "Cff", Cffs, values=False)
+        pack(out, "rhs_f", rf, np.float64)
+        pack_csr(out, "Lii", Liis, values=False)
+        pack(out, "rhs_h", rh, np.complex128)
+    out["coords"] = np.asarray(gp.coords)
+    out["flips"] = np.array(rep.flips)
+    out["seam_residuals"] = np.array(rep.seam_residuals, dtype=np.float64)
+    out["distortion_json"] = np.array(json.dumps(rep.distortion))
+    out["ok"] = np.array(rep.ok)
+    path = os.path.join(HERE, f"{name}.npz")
+    np.savez_compressed(path, **out)
+    print(f"{name}: {os.path.getsize(path) / 1e3:.0f} KB  mode={mode} K={len(subs)} "
+          f"flips={rep.flips} mean|d|={rep.distortion['angular_abs']['mean']:.6f}")
+
+
+def known_answers():
+    """SPEC.md worked examples evaluated by the reference."""
+    out = {}
+    s3 = np.sqrt(3.0)
+    eq = pgcp.TriMesh(np.array([[0, 0, 0], [1, 0, 0], [0.5, s3 / 2, 0]], float),
+                      np.array([[0, 1, 2]]))
+    out["equilateral_L"] = pgcp.cotangent_laplacian(eq).toarray()
+    ri = pgcp.TriMesh(np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0]], float), np.array([[0, 1, 2]]))
+    Lri = pgcp.cotangent_laplacian(ri)
+    out["right_L_dense"] = Lri.toarray()
+    out["right_L_nnz"] = np.array(Lri.nnz)
+    sq = pgcp.TriMesh(np.array([[0, 0, 0], [1, 0, 0], [1, 1, 0], [0, 1, 0]], float),
+                      np.array([[0, 1, 2], [0, 2, 3]]))
+    M = pgcp.area_matrix(sq)
+    xy = np.concatenate([sq.vertices[:, 0], sq.vertices[:, 1]])
+    out["unit_square_area"] = np.array(xy @ (M @ xy))
+    out["mobius_to_unit_1pi"] = pgcp.mobius_apply(pgcp.mobius_to_unit(1 + 1j), 1 + 1j)
+    out["pair_align_identity"] = np.array(pgcp.mobius_pair_align(1j, -1j), dtype=complex)
+    out["opening_1"] = pgcp.opening_map(1.0)
+    out["opening_0"] = pgcp.opening_map(0.0)
+    out["closing_pm_i"] = pgcp.closing_map(np.array([1j, -1j]))
+    out["stereo_inv"] = pgcp.stereographic_inverse(np.array([0, pgcp.INF, 1.0]))
+    v = np.array([1.0, 2.0, 3.0, 4.0])
+    st = pgcp.summarize(v)
+    out["summ_1234"] = np.array([st["mean"], st["sd"], st["median"], st["iqr"]])
+    out["iqr_1to8"] = np.array(pgcp.summarize(np.arange(1.0, 9.0))["iqr"])
+    # stretch x2 of the unit right triangle: corner distortions
+    tri = pgcp.TriMesh(np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0]], float), np.array([[0, 1, 2]]))
+    d, valid = pgcp.angular_distortion(tri, np.array([0, 2, 1j]))
+    out["stretch_distortion"] = d
+    np.savez_compressed(os.path.join(HERE, "known_answers.npz"), **out)
+    print("known_answers written")
+
+
+def weld_corpus(seed=0, count=12):
+    """Random Jordan polygon pairs welded by the reference `partial_weld`
+    (SPEC acceptance criterion 1 shape): two star-shaped regions sharing an
+    arc of a common chord-split disk."""
+    rng = np.random.default_rng(seed)
+    out = {"a": [], "b": [], "k": [], "oa": [], "ob": [], "seam": []}
+    made = 0
+    while made < count:
+        m = int(rng.integers(20, 120))
+        k = int(rng.integers(2, m // 2))
+        # shared arc along the real axis from 1 to -1 (k+1 samples), region a
+        # above (boundary ccw: arc then upper curve back), region b below
+        # shared arc along the real axis from -1 to 1 (k+1 samples); region a
+        # above it (boundary ccw: arc, then the upper curve back to -1),
+        # region b below it (arc in the same order, region on the right)
+        x = np.sort(rng.uniform(-0.95, 0.95, k - 1))
+        arc = np.concatenate([[-1.0], x, [1.0]]) + 0j
+        tu = np.sort(rng.uniform(0.05, np.pi - 0.05, m - k))
+        upper = (1.0 + 0.3 * rng.uniform(-1, 1, len(tu))) * np.exp(1j * tu)
+        tl = np.sort(rng.uniform(np.pi + 0.05, 2 * np.pi - 0.05, m - k))[::-1]
+        lower = (1.0 + 0.3 * rng.uniform(-1, 1, len(tl))) * np.exp(1j * tl)
+        a = np.concatenate([arc, upper])
+        b = np.concatenate([arc, lower])
+        try:
+            r = pgcp.partial_weld(a, b, k)
+        except pgcp.WeldError:
+            continue
+        out["a"].append(a)
+        out["b"].append(b)
+        out["k"].append(k)
+        out["oa"].append(r.a)
+        out["ob"].append(r.b)
+        out["seam"].append(r.seam_error)
+        made += 1
+    res = {}
+    pack(res, "a", out["a"], np.complex128)
+    pack(res, "b", out["b"], np.complex128)
+    pack(res, "oa", out["oa"], np.complex128)
+    pack(res, "ob", out["ob"], np.complex128)
+    res["k"] = np.array(out["k"], dtype=np.int64)
+    res["seam"] = np.array(out["seam"])
+    np.savez_compressed(os.path.join(HERE, "weld_corpus.npz"), **res)
+    print(f"weld_corpus: {count} welds")
+
+
+def main():
+    known_answers()
+    weld_corpus()
+    V, F, cuts = gen.cfg1(seed=0)
+    pipeline_case("cfg1", V, F, cuts, "free")
+    V, F, cuts = gen.height_field_case(33, 4, layout="strips", seed=3)
+    pipeline_case("strips4", V, F, cuts, "free")
+    V, F, cuts = gen.height_field_case(31, 3, seed=5)
+    pipeline_case("blocks3x3", V, F, cuts, "free")
+    V, F, cuts = gen.height_field_case(30, 2, seed=7)
+    pipeline_case("disk2x2", V, F, cuts, "disk")
+    V, F = gen.height_field_grid(25, seed=11)
+    pipeline_case("k1free", V, F, None, "free")
+    pipeline_case("k1disk", V, F, None, "disk")
+    Vf, Ff = gen.flat_grid_arrays(20)
+    cf = gen.cuts_from_face_labels(Ff, gen.block_face_labels(21, 2))
+    pipeline_case("flat2x2", Vf, Ff, cf, "free")
+    sph = ref_shapes.icosphere(3)
+    lab = ref_shapes.hemisphere_labels(sph)
+    pipeline_case("sphere2", np.array(sph.vertices), np.array(sph.faces),
+                  ref_shapes.cuts_from_face_labels(sph, lab), "sphere")
+    lab = ref_shapes.azimuth_labels(sph, 4)
+    pipeline_case("sphere4", np.array(sph.vertices), np.array(sph.faces),
+                  ref_shapes.cuts_from_face_labels(sph, lab), "sphere")
+    # balanced rows->strips->tree schedule on 4x4 blocks (documented deviation)
+    V, F, cuts = gen.height_field_case(41, 4, seed=2)
+    pipeline_case("tree4x4", V, F, cuts, "free",
+                  schedule_pairs=gen.row_tree_schedule_order(4, 4))
+
+
+if __name__ == "__main__":
+    main()
