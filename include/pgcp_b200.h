@@ -170,59 +170,95 @@ PGCP_API int pgcp_batch_export_system(pgcp_batch* b, int which, int32_t comp, in
 PGCP_API int pgcp_batch_conformal_energy(pgcp_batch* b, const double* z, double* energy, void* stream);
 
 /* -------------------------------------------------------------------------
- * Boundary welding (welding.py:512-842), device resident, one CTA per weld.
- * See paper_1903_12359_b200/welding.py for the record encoding.
+ * Boundary welding (welding.py:512-842), device resident.
+ *
+ * A map log is an array of records (welding.py:236-509):
+ *   kind 0 Mobius       p[0..7] = a, b, c, d; flags bit0 = axis; bits 8..15 =
+ *                       number of pins; pin k: p[8+4k..11+4k] = (z, w), side in
+ *                       flags bits 16+8k..23+8k (int8)
+ *   kind 1 SqrtRatio    p[0..3] = z0, z1; flags low byte = branch (int8)
+ *   kind 2 Open         p[0..1] = xi, p[2..3] = Re/|xi|^2, Im/|xi|^2; branch
+ *   kind 3 Close        p[0] = ai, p[1] = bi, p[2] = c, p[3] = d
+ *   kind 4 SquareMobius p[0..1] = q (infinity allowed)
  */
 typedef struct {
-    int32_t kind;   /* 0 mob, 1 sqrt-ratio, 2 open, 3 close, 4 square-mobius */
-    int32_t flags;  /* bit0 axis, bits 8..15 npins, side/branch values        */
-    double p[16];   /* parameters (see welding.py)                            */
+    int32_t kind;
+    int32_t flags;
+    double p[16];
 } pgcp_rec;
 
-/* Replay records [rec0, rec0+nrec) on points (welding.py:512-526).
- * pts device complex [npts] in/out; sides device int8 [npts] in/out.
- * nan_flag device int32 (set to 1 on NaN). Asynchronous. */
-PGCP_API int pgcp_weld_replay(const pgcp_rec* recs, int32_t nrec, double* pts, int8_t* sides,
-                     int64_t npts, int32_t* nan_flag, void* stream);
+/* Whole weld schedule on tracked boundary values (pipeline.py:172-213 and
+ * partial_weld / closed_weld, welding.py:640-763). One CTA per weld builds the
+ * two logs from the shared arc (phase 1); every other point of the two
+ * components replays its side's log (phase 2). Welds on disjoint components
+ * run concurrently (schedule levels).
+ *   tv      device complex [slots]  tracked values, updated in place
+ *   info    host int32 [nsteps*6]   k, closed, na, nb, comp_a, comp_b
+ *   src     host int32              slot ids of a_cycle then b_cycle, per step
+ *   wb_off  host int64 [nsteps+1];  wb host int32 [2*total] (slot, code):
+ *           code bits 0..23 arc position + 1 (0: replay), bit 24 arc from b,
+ *           bit 25 / 26 cycle point of a / b, bit 31 replay the b log
+ *   out     host f64 [nsteps*8]     seam error, seam residual, area of the
+ *           welded a arc, status, nrec_a, nrec_b, level, record offset
+ *   recs    host pgcp_rec [recs_cap] (optional) all logs
+ * Synchronises. PGCP_E_WELD names the first failing step. */
+PGCP_API int pgcp_weld_schedule_run(double* tv, int32_t nsteps, const int32_t* info, const int32_t* src,
+                                    const int64_t* wb_off, const int32_t* wb, double hard_tol, double* out,
+                                    pgcp_rec* recs, int64_t recs_cap, void* stream);
 
-/* One partial (closed = 0) or closed (closed = 1) weld, welding.py:640-763:
- *   a, b      device complex [na], [nb]   (input boundary samples)
- *   out_a/b   device complex [na], [nb]
- *   recs_a/b  device pgcp_rec [cap_rec]   (the two map logs)
- *   meta      device f64 [8]: n_rec_a, n_rec_b, seam_error, scale, error code,
- *             error index, aux
- * One CTA; asynchronous. */
-PGCP_API int pgcp_weld_one(const double* a, int64_t na, const double* b, int64_t nb, int64_t k,
-                  int closed, double hard_tol, double* out_a, double* out_b,
-                  pgcp_rec* recs_a, pgcp_rec* recs_b, int32_t cap_rec, double* meta,
-                  void* stream);
+/* apply_log: replay nrec host records on device points (in/out) with
+ * optional int8 side tags. Synchronises; PGCP_E_WELD on NaN. */
+PGCP_API int pgcp_weld_replay(const pgcp_rec* recs, int32_t nrec, double* pts, int8_t* sides, int64_t npts,
+                              void* stream);
 
-/* Geodesic map of a Jordan polygon to the unit circle (welding.py:803-842).
- *   pts device complex [n] (ccw), interior: host complex or NULL
- *   out device complex [n]; recs device [cap_rec]; meta as above. */
-PGCP_API int pgcp_weld_geodesic(const double* pts, int64_t n, const double* interior,
-                       double* out, pgcp_rec* recs, int32_t cap_rec, double* meta,
-                       void* stream);
+/* geodesic_to_circle of the polygon tv[src[0..n)] (host src): orientation
+ * fix (pipeline.py:218-222), interior point, zip, Cayley, centring.
+ *   circ device complex [n] (per src entry); recs host [cap];
+ *   meta host f64 [8]: nrec, err, idx, aux, circle error, interior. */
+PGCP_API int pgcp_weld_geodesic(const double* tv, const int32_t* src, int32_t n, const double* interior,
+                                double* circ, pgcp_rec* recs, int32_t cap, double* meta, void* stream);
+
+/* polygon_interior_point of tv[src] (host src), optionally reversed. */
+PGCP_API int pgcp_polygon_interior(const double* tv, const int32_t* src, int32_t n, int reverse, double* out,
+                                   void* stream);
+
+/* z[idx[i]] = add + 1/(z[idx[i]] - sub): sphere-mode exterior inversion
+ * (pipeline.py:253, 262). idx device int32 or NULL. */
+PGCP_API int pgcp_inv_shift(double* z, const int32_t* idx, int64_t n, double add_re, double add_im,
+                            double sub_re, double sub_im, void* stream);
+
+/* dst[i] = src[idx[i]] / dst[idx[i]] = src[i] for complex arrays */
+PGCP_API int pgcp_gather_complex(const double* src, const int32_t* idx, double* dst, int64_t n, void* stream);
+PGCP_API int pgcp_scatter_complex(const double* src, const int32_t* idx, double* dst, int64_t n, void* stream);
 
 /* -------------------------------------------------------------------------
  * Stitch and metrics
  */
-/* stitch_global (assemble.py:286-337): average seam copies.
+/* stitch_global (assemble.py:286-337): average the seam copies of every
+ * parent vertex in submesh order, seam spread / scale check, sphere finish
+ * (stereographic_inverse(conj(z)) normalised), disk circle check, flips.
  *   z       device complex [sum_n] per-submesh embeddings (local order)
- *   coords  device complex [n]; stats host f64 [4]: seam_max, scale, -, -
- * Synchronises. */
-PGCP_API int pgcp_batch_stitch(pgcp_batch* b, const double* z, double* coords, double* stats,
-                      void* stream);
+ *   mode    0 free, 1 disk, 2 sphere
+ *   coords  device complex [n]; sphere device f64 [3n] (mode 2)
+ *   prov    device int32 [n]; flip device uint8 [m]
+ *   stats   host f64 [8]: seam_max, scale, circle dev, flips, status
+ * Synchronises; PGCP_E_SOLVE on a failed check. */
+PGCP_API int pgcp_batch_stitch(pgcp_batch* b, const double* z, int mode, double hard_tol, double circle_tol,
+                               double* coords, double* sphere, int32_t* prov, uint8_t* flip, double* stats,
+                               void* stream);
 
-/* Angular distortion per corner (metrics.py:31-75) and flips
- * (assemble.py:97-102, 259-263).
- *   mode 0 planar (coords complex [n]), 1 sphere (coords f64 [n*3])
- *   d device f64 [3m], valid device uint8 [3m], nflip host int64,
- *   summary host f64 [PGCP_SUMMARY_COUNT]. Synchronises. */
+/* distortion_report (metrics.py:31-176): per-corner angular distortion,
+ * per-face area log ratio, their summaries (mean, population sd, median,
+ * IQR with numpy's linear interpolation on exact order statistics), and the
+ * 0.1-degree histogram of |d|.
+ *   coords  device complex [n] (planar) or f64 [3n] (mode_sphere = 1)
+ *   d       device f64 [3m]; valid device uint8 [3m]
+ *   summary host f64 [PGCP_SUMMARY_COUNT] (see metrics.cu)
+ *   hist    host uint64 [hist_cap] (skipped if too small). Synchronises. */
 #define PGCP_SUMMARY_COUNT 16
-PGCP_API int pgcp_distortion(const double* V, const int32_t* F, int64_t n, int64_t m,
-                    const double* coords, int mode, double* d, uint8_t* valid,
-                    int64_t* nflip, double* summary, void* stream);
+PGCP_API int pgcp_distortion(const double* V, const int32_t* F, int64_t n, int64_t m, const double* coords,
+                             int mode_sphere, double* d, uint8_t* valid, double* summary, uint64_t* hist,
+                             int64_t hist_cap, void* stream);
 
 /* host-side weld-schedule planner (partition.py:236-324): see planner.cpp */
 PGCP_API int pgcp_plan_weld_schedule(const int64_t* cyc, const int64_t* cyc_off, int32_t K,

@@ -278,7 +278,7 @@ __global__ void k_walk(int32_t K, const int64_t* __restrict__ vert_off, const in
                        const int32_t* __restrict__ bcnt, const int32_t* __restrict__ start,
                        const int32_t* __restrict__ nxt, const int64_t* __restrict__ loop_off,
                        int32_t* __restrict__ loop, int32_t* __restrict__ comp_bad, int32_t* __restrict__ chi_out,
-                       int32_t* __restrict__ loops_out) {
+                       int32_t* __restrict__ loops_out, uint8_t* __restrict__ seen) {
     GRID_STRIDE(c, K) {
         int64_t nc = vert_off[c + 1] - vert_off[c];
         int64_t mc = fcnt[c], bc = bcnt[c];
@@ -298,6 +298,7 @@ __global__ void k_walk(int32_t K, const int64_t* __restrict__ vert_off, const in
                     break;
                 }
                 loop[base + j] = (int32_t)(cur - vert_off[c]);
+                seen[cur] = 1;
                 ++j;
                 cur = nxt[cur];
                 if (cur < 0) {
@@ -305,7 +306,25 @@ __global__ void k_walk(int32_t K, const int64_t* __restrict__ vert_off, const in
                     break;
                 }
             } while (cur != s);
-            loops = bad ? -1 : (j == bc ? 1 : -2);
+            loops = bad ? -1 : 1;
+            if (!bad && j != bc) {
+                // more loops (validate_topology counts them, mesh.py:190-202):
+                // walk every remaining loop from its smallest vertex
+                for (int64_t g = vert_off[c]; g < vert_off[c + 1] && !bad; ++g) {
+                    if (nxt[g] < 0 || seen[g]) continue;
+                    int64_t cur2 = g, guard = 0;
+                    do {
+                        seen[cur2] = 1;
+                        cur2 = nxt[cur2];
+                        if (cur2 < 0 || ++guard > bc) {
+                            bad = true;
+                            break;
+                        }
+                    } while (cur2 != g);
+                    ++loops;
+                }
+                if (bad) loops = -1;
+            }
         } else if (bad) {
             loops = -1;
         }
@@ -550,8 +569,11 @@ int build_partition(pgcp_batch* b, const int64_t* cuts, int64_t ncuts, bool no_c
     PGCP_TRY(exclusive_scan_i32_to_i64(bcnt.p, b->loop_off.p, K, s));
     PGCP_TRY(fetch_scalar(b->loop_off.p + K, &b->sum_nb, s));
     PGCP_TRY(b->loop.alloc(b->sum_nb, s));
+    DevBuf<uint8_t> seen;
+    PGCP_TRY(seen.alloc(E, s));
+    PGCP_TRY(seen.zero(s));
     k_walk<<<grid_for(K, 64), 64, 0, s>>>(K, b->vert_off.p, fcnt.p, bcnt.p, start.p, b->nxt.p, b->loop_off.p,
-                                         b->loop.p, bad.p, chi.p, loops.p);
+                                         b->loop.p, bad.p, chi.p, loops.p, seen.p);
     PGCP_LAUNCH_CHECK();
     DevBuf<int64_t> ploops;
     PGCP_TRY(ploops.alloc(1, s));

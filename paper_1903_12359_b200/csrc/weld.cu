@@ -1,0 +1,1523 @@
+// weld.cu -- K4: boundary welding on the device (welding.py:79-842).
+//
+// A weld's map log is a short sequence of primitive records (Mobius, square
+// root ratio, opening, closing, square-Mobius). Every record parameter
+// depends only on the shared-arc points and the two tracking points (0, inf):
+//   SqrtRatio(pts[0], pts[1]); Open(pts[j]) j = 2..k; axis-Mobius(pts[0]);
+//   Close(va[j], vb[j]) j = k-1..1; SquareMobius(va[0]); 3-point Mobius(aux).
+// So a weld runs in two phases:
+//   phase 1  one CTA per weld holds only the 2(k+3) arc + tracking points in
+//            shared memory and builds both logs record by record (a block
+//            barrier per record; the records are the serial critical path);
+//   phase 2  every other tracked point of the two components (non-arc cycle
+//            points and interior seam points: the reference's `apply_log` on
+//            "others", pipeline.py:200-204) replays its side's log
+//            independently -- one thread per point over the whole GPU.
+// Welds of one schedule level touch disjoint components and run as one
+// launch (one CTA each); checks whose inputs span all points (the far-end
+// and seam scale tests, welding.py:689-692 and 721-729) are finished after
+// phase 2 from per-step maxima.
+//
+// Numerics: complex division follows numpy's algorithm, the square root
+// glibc's csqrt; record semantics (pins, side tags, infinity handling) follow
+// the reference record by record. Results agree with the reference to
+// rounding (tests/test_gpu_weld.py), not bit for bit.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <unordered_map>
+
+#include "common.cuh"
+
+namespace pgcp {
+namespace weld {
+
+enum : int { R_MOB = 0, R_SQR = 1, R_OPEN = 2, R_CLOSE = 3, R_SQ = 4 };
+enum : int { FREE = 0, UP = 1, DOWN = -1 };
+
+using Rec = pgcp_rec;
+
+__device__ __forceinline__ double2 C(double x, double y) { return make_double2(x, y); }
+__device__ __forceinline__ double2 cinf() { return make_double2(INFINITY, 0.0); }
+__device__ __forceinline__ bool c_isinf(double2 z) { return isinf(z.x) || isinf(z.y); }
+__device__ __forceinline__ bool c_fin(double2 z) { return isfinite(z.x) && isfinite(z.y); }
+__device__ __forceinline__ bool c_nan(double2 z) { return isnan(z.x) || isnan(z.y); }
+__device__ __forceinline__ bool c_eq(double2 a, double2 b) { return a.x == b.x && a.y == b.y; }
+__device__ __forceinline__ bool c_zero(double2 a) { return a.x == 0.0 && a.y == 0.0; }
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return C(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return C(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cneg(double2 a) { return C(-a.x, -a.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return C(__dsub_rn(__dmul_rn(a.x, b.x), __dmul_rn(a.y, b.y)), __dadd_rn(__dmul_rn(a.x, b.y), __dmul_rn(a.y, b.x)));
+}
+__device__ __forceinline__ double2 cscale(double s, double2 a) { return cmul(C(s, 0.0), a); }
+__device__ __forceinline__ double cabs_(double2 a) { return hypot(a.x, a.y); }
+
+// numpy's complex division (Smith's method with a reciprocal)
+__device__ double2 cdiv(double2 a, double2 b) {
+    double abr = fabs(b.x), abi = fabs(b.y);
+    if (abr >= abi) {
+        if (abr == 0.0 && abi == 0.0) return C(a.x / abr, a.y / abi);
+        double rat = b.y / b.x;
+        double scl = 1.0 / (b.x + b.y * rat);
+        return C((a.x + a.y * rat) * scl, (a.y - a.x * rat) * scl);
+    }
+    double rat = b.x / b.y;
+    double scl = 1.0 / (b.y + b.x * rat);
+    return C((a.x * rat + a.y) * scl, (a.y * rat - a.x) * scl);
+}
+
+// principal square root, glibc csqrt's case analysis
+__device__ double2 csqrt_(double2 z) {
+    double re = z.x, im = z.y;
+    if (isnan(re) || isnan(im)) {
+        if (isinf(im)) return C(INFINITY, im);
+        return C(NAN, NAN);
+    }
+    if (isinf(im)) return C(INFINITY, im);
+    if (isinf(re)) {
+        if (re < 0) return C(0.0 * fabs(im), copysign(INFINITY, im));
+        return C(re, copysign(0.0, im));
+    }
+    if (im == 0.0) {
+        if (re < 0.0) return C(0.0, copysign(sqrt(-re), im));
+        return C(fabs(sqrt(re)), copysign(0.0, im));
+    }
+    if (re == 0.0) {
+        double r = sqrt(0.5 * fabs(im));
+        return C(r, copysign(r, im));
+    }
+    double d = hypot(re, im);
+    double r, s;
+    if (re > 0) {
+        r = sqrt(0.5 * (d + re));
+        s = 0.5 * (im / r);
+    } else {
+        s = sqrt(0.5 * (d - re));
+        r = fabs(0.5 * (im / s));
+    }
+    return C(r, copysign(s, im));
+}
+
+__device__ __forceinline__ int rec_side(int flags, int k) { return (int)(int8_t)((flags >> (16 + 8 * k)) & 0xff); }
+
+// one record on one point (welding.py:251-509)
+__device__ void apply_rec(const Rec& r, double2& z, int8_t& s) {
+    const double* p = r.p;
+    switch (r.kind) {
+        case R_MOB: {
+            double2 a = C(p[0], p[1]), b = C(p[2], p[3]), c = C(p[4], p[5]), d = C(p[6], p[7]);
+            bool axis = r.flags & 1;
+            int npins = (r.flags >> 8) & 0xff;
+            for (int k = 0; k < npins; ++k) {
+                if (c_eq(z, C(p[8 + 4 * k], p[9 + 4 * k]))) {
+                    z = C(p[10 + 4 * k], p[11 + 4 * k]);
+                    s = (int8_t)rec_side(r.flags, k);
+                    return;
+                }
+            }
+            if (c_isinf(z)) {
+                z = c_zero(c) ? cinf() : cdiv(a, c);
+                if (!axis) s = 0;
+                return;
+            }
+            double2 num = cadd(cmul(a, z), b);
+            double2 den = cadd(cmul(c, z), d);
+            double2 w = c_zero(den) ? cinf() : cdiv(num, den);
+            int8_t ns = 0;
+            if (axis && s != 0) {
+                if (c_fin(w)) {
+                    double im = w.y;
+                    w = C(signbit(im) ? -0.0 : 0.0, im + 0.0);
+                    ns = w.y > 0 ? UP : (w.y < 0 ? DOWN : s);
+                } else {
+                    ns = s;
+                }
+            }
+            z = w;
+            s = ns;
+            return;
+        }
+        case R_SQR: {
+            double2 z0 = C(p[0], p[1]), z1 = C(p[2], p[3]);
+            int br = (int)(int8_t)(r.flags & 0xff);
+            if (c_eq(z, z0)) {
+                z = cinf();
+                s = (int8_t)br;
+            } else if (c_eq(z, z1)) {
+                z = C(0.0, 0.0);
+                s = (int8_t)br;
+            } else if (c_eq(z, cinf())) {
+                z = C(1.0, 0.0);
+                s = 0;
+            } else {
+                z = csqrt_(cdiv(csub(z, z1), csub(z, z0)));
+                s = 0;
+            }
+            return;
+        }
+        case R_OPEN: {
+            double2 xi = C(p[0], p[1]);
+            double pp = p[2], qq = p[3];
+            int br = (int)(int8_t)(r.flags & 0xff);
+            if (c_eq(z, xi)) {
+                z = C(0.0, 0.0);
+                s = (int8_t)br;
+                return;
+            }
+            if (s != 0) {
+                double t = c_isinf(z) ? INFINITY : z.y;
+                double den = 1.0 - qq * t;
+                double t2 = (den == 0.0) ? INFINITY : pp * t / den;
+                if (isinf(t)) t2 = (qq != 0.0) ? -pp / qq : INFINITY;
+                if (!isfinite(t2)) {
+                    z = cinf();
+                    return;  // side kept
+                }
+                double sg = (t2 == 0.0) ? (double)br : (t2 > 0 ? 1.0 : -1.0);
+                double h = hypot(t2, 1.0);
+                z = C(0.0 * sg, sg * h);
+                s = (int8_t)sg;
+                return;
+            }
+            double2 L;
+            if (c_isinf(z)) {
+                L = (qq != 0.0) ? C(0.0, -(pp / qq)) : cinf();
+            } else {
+                double2 den = C(1.0 - qq * z.y, qq * z.x);
+                L = c_zero(den) ? cinf() : cdiv(C(pp * z.x, pp * z.y), den);
+            }
+            if (!c_fin(L)) {
+                z = cinf();
+            } else if (cabs_(L) > 1e100) {
+                z = (L.x >= 0) ? L : cneg(L);
+            } else {
+                z = csqrt_(csub(cmul(L, L), C(1.0, 0.0)));
+            }
+            s = 0;
+            return;
+        }
+        case R_CLOSE: {
+            double ai = p[0], bi = p[1], c = p[2], d = p[3];
+            if (c_eq(z, C(0.0, ai)) || c_eq(z, C(0.0, bi))) {
+                z = C(0.0, 0.0);
+                s = 0;
+                return;
+            }
+            if (s != 0) {
+                double t = c_isinf(z) ? INFINITY : z.y;
+                double den = c + d * t;
+                double t2 = (den == 0.0) ? INFINITY : t / den;
+                if (isinf(t)) t2 = (d != 0.0) ? 1.0 / d : INFINITY;
+                if (!isfinite(t2)) {
+                    z = cinf();
+                    return;  // side kept
+                }
+                if (fabs(t2) > 1.0) {
+                    double mag = (fabs(t2) < 1e100) ? sqrt(fmax(t2 * t2 - 1.0, 0.0)) : fabs(t2);
+                    double sg = t2 > 0 ? 1.0 : -1.0;
+                    z = C(0.0 * sg, sg * mag);
+                    s = t2 > 0 ? UP : DOWN;
+                } else {
+                    z = C(sqrt(fmax(1.0 - t2 * t2, 0.0)), 0.0);
+                    s = 0;
+                }
+                return;
+            }
+            double2 T;
+            if (c_isinf(z)) {
+                T = (d != 0.0) ? C(0.0, 1.0 / d) : cinf();
+            } else {
+                double2 den = C(c + d * z.y, -d * z.x);
+                T = c_zero(den) ? cinf() : cdiv(z, den);
+            }
+            if (!c_fin(T)) {
+                z = cinf();
+            } else if (cabs_(T) > 1e100) {
+                z = (T.x >= 0) ? T : cneg(T);
+            } else {
+                z = csqrt_(cadd(cmul(T, T), C(1.0, 0.0)));
+            }
+            s = 0;
+            return;
+        }
+        case R_SQ: {
+            double2 q = C(p[0], p[1]);
+            bool qinf = c_isinf(q);
+            if (c_eq(z, q)) {
+                z = cinf();
+                s = 0;
+                return;
+            }
+            if (!qinf && c_isinf(z)) {
+                z = cmul(q, q);
+                s = 0;
+                return;
+            }
+            if (s != 0) {
+                double t = z.y, t2;
+                if (qinf) {
+                    t2 = t;
+                } else {
+                    double den = 1.0 - t / q.y;
+                    t2 = (den == 0.0) ? INFINITY : t / den;
+                }
+                z = isfinite(t2) ? C(-(t2 * t2), 0.0) : cinf();
+                s = 0;
+                return;
+            }
+            double2 mm;
+            if (qinf) {
+                mm = z;
+            } else {
+                double2 den = csub(C(1.0, 0.0), cdiv(z, q));
+                mm = c_zero(den) ? cinf() : cdiv(z, den);
+            }
+            double2 w = cmul(mm, mm);
+            z = c_fin(w) ? w : cinf();
+            s = 0;
+            return;
+        }
+        default:
+            z = C(NAN, NAN);
+    }
+}
+
+// ---- record constructors (single thread) -----------------------------------
+
+__device__ Rec mk_mob(double2 a, double2 b, double2 c, double2 d, bool axis = false) {
+    Rec r;
+    r.kind = R_MOB;
+    r.flags = axis ? 1 : 0;
+    r.p[0] = a.x; r.p[1] = a.y; r.p[2] = b.x; r.p[3] = b.y;
+    r.p[4] = c.x; r.p[5] = c.y; r.p[6] = d.x; r.p[7] = d.y;
+    for (int i = 8; i < 16; ++i) r.p[i] = 0.0;
+    return r;
+}
+__device__ void mob_pin(Rec& r, double2 pz, double2 pw, int side) {
+    int k = (r.flags >> 8) & 0xff;
+    r.p[8 + 4 * k] = pz.x; r.p[9 + 4 * k] = pz.y; r.p[10 + 4 * k] = pw.x; r.p[11 + 4 * k] = pw.y;
+    r.flags = (r.flags & ~(0xff << 8)) | ((k + 1) << 8);
+    r.flags |= ((side & 0xff) << (16 + 8 * k));
+}
+__device__ Rec mk_sqr(double2 z0, double2 z1, int br) {
+    Rec r;
+    r.kind = R_SQR;
+    r.flags = br & 0xff;
+    r.p[0] = z0.x; r.p[1] = z0.y; r.p[2] = z1.x; r.p[3] = z1.y;
+    for (int i = 4; i < 16; ++i) r.p[i] = 0.0;
+    return r;
+}
+__device__ Rec mk_open(double2 xi, int br) {
+    Rec r;
+    r.kind = R_OPEN;
+    r.flags = br & 0xff;
+    double s2 = hypot(xi.x, xi.y);
+    s2 = s2 * s2;
+    r.p[0] = xi.x; r.p[1] = xi.y; r.p[2] = xi.x / s2; r.p[3] = xi.y / s2;
+    for (int i = 4; i < 16; ++i) r.p[i] = 0.0;
+    return r;
+}
+__device__ Rec mk_close(double a, double b) {
+    Rec r;
+    r.kind = R_CLOSE;
+    r.flags = 0;
+    r.p[0] = a; r.p[1] = b; r.p[2] = -2 * a * b / (a - b); r.p[3] = (a + b) / (a - b);
+    for (int i = 4; i < 16; ++i) r.p[i] = 0.0;
+    return r;
+}
+__device__ Rec mk_sq(double2 q) {
+    Rec r;
+    r.kind = R_SQ;
+    r.flags = 0;
+    r.p[0] = q.x; r.p[1] = q.y;
+    for (int i = 2; i < 16; ++i) r.p[i] = 0.0;
+    return r;
+}
+
+// Mobius taking z_i -> w_i (welding.py:99-133); false if not distinct
+__device__ bool three_point(const double2* zs, const double2* ws, double2* co) {
+    const double2* trips[2] = {zs, ws};
+    for (int t = 0; t < 2; ++t)
+        for (int i = 0; i < 3; ++i)
+            for (int j = i + 1; j < 3; ++j) {
+                bool bi = c_isinf(trips[t][i]), bj = c_isinf(trips[t][j]);
+                if ((bi && bj) || (!bi && !bj && c_eq(trips[t][i], trips[t][j]))) return false;
+            }
+    auto std3 = [](const double2* v, double2* o) {
+        double2 z1 = v[0], z2 = v[1], z3 = v[2];
+        if (c_isinf(z1)) {
+            o[0] = C(0, 0); o[1] = csub(z2, z3); o[2] = C(1, 0); o[3] = cneg(z3);
+        } else if (c_isinf(z2)) {
+            o[0] = C(1, 0); o[1] = cneg(z1); o[2] = C(1, 0); o[3] = cneg(z3);
+        } else if (c_isinf(z3)) {
+            o[0] = C(1, 0); o[1] = cneg(z1); o[2] = C(0, 0); o[3] = csub(z2, z1);
+        } else {
+            double2 d23 = csub(z2, z3), d21 = csub(z2, z1);
+            o[0] = d23; o[1] = cmul(cneg(z1), d23); o[2] = d21; o[3] = cmul(cneg(z3), d21);
+        }
+    };
+    double2 m1[4], m2[4];
+    std3(zs, m1);
+    std3(ws, m2);
+    double2 a = csub(cmul(m2[3], m1[0]), cmul(m2[1], m1[2]));
+    double2 b = csub(cmul(m2[3], m1[1]), cmul(m2[1], m1[3]));
+    double2 c = cadd(cmul(cneg(m2[2]), m1[0]), cmul(m2[0], m1[2]));
+    double2 d = cadd(cmul(cneg(m2[2]), m1[1]), cmul(m2[0], m1[3]));
+    double nrm = fmax(fmax(cabs_(a), cabs_(b)), fmax(cabs_(c), cabs_(d)));
+    co[0] = C(a.x / nrm, a.y / nrm);
+    co[1] = C(b.x / nrm, b.y / nrm);
+    co[2] = C(c.x / nrm, c.y / nrm);
+    co[3] = C(d.x / nrm, d.y / nrm);
+    return true;
+}
+
+__device__ __forceinline__ int walk_class(double h) { return isinf(h) ? 1 : (h > 0 ? 0 : 2); }
+__device__ __forceinline__ bool walk_less(double a, double b) {  // _axis_walk_key(a) < _axis_walk_key(b)
+    int ca = walk_class(a), cb = walk_class(b);
+    if (ca != cb) return ca < cb;
+    if (ca == 1) return false;
+    return a < b;
+}
+
+// ---------------------------------------------------------------------------
+// phase 1
+
+enum : int {
+    WE_OK = 0,
+    WE_ZIP01 = 1,      // zip points 0 and 1 coincide
+    WE_ZIP_HALF = 2,   // zip point j left the right half-plane
+    WE_ZIP_AXIS = 3,   // zip point j landed on the imaginary axis
+    WE_ZIP_COLL = 4,   // zip points j-1 and j collapsed
+    WE_NAN = 5,        // NaN during (aux = stage)
+    WE_FAR0 = 6,       // far end of the zip collapsed to 0
+    WE_ALIGN_A = 7,    // alignment point j (a side) left the imaginary axis
+    WE_ALIGN_B = 8,
+    WE_ORDER = 9,      // alignment points j not strictly ordered
+    WE_TRACK = 10,     // tracking points degenerated
+    WE_FAREND = 11,    // far ends of the two slits diverged
+    WE_SEAM = 12,      // seam alignment error
+    WE_PRE = 13,       // prenormalizer failure (aux: 1 none finite, 2 coincide, 3 origin)
+    WE_THREE = 14,     // three-point Mobius needs distinct points
+    WE_K = 15,         // k out of range
+    WE_GEO_DISK = 16,  // interior point left the unit disk
+    WE_GEO_CIRCLE = 17,
+    WE_INTERIOR = 18,  // could not locate a point inside the polygon
+};
+
+struct StepDesc {
+    int32_t k, closed, na, nb;
+    int64_t src;       // offset into src[] (na + nb slot ids)
+    int64_t rec;       // record offset of log_a (log_b at rec + cap)
+    int32_t cap, pad;
+    int64_t arc;       // offset into arc_out (k+1 values of a, then k+1 of b)
+};
+
+// per-step meta written by phase 1 / 2 (doubles):
+//  0 nrec_a, 1 nrec_b, 2 err code, 3 err index, 4 err aux, 5 seam(arc), 6 qa.re, 7 qa.im,
+//  8 qb.re, 9 qb.im, 10 stage max |va| (arc+aux), 11 final max |va| arc, 12 final max |vb| arc,
+//  13 final max aux (a,b), 14 sq index a, 15 sq index b, 16 area(res.a arc), 17..19 spare
+constexpr int META = 20;
+
+struct Phase1Args {
+    const StepDesc* steps;
+    const int32_t* src;
+    const double2* tv;      // tracked values (read)
+    double2* arc_out;
+    Rec* recs;
+    double* meta;
+    double2* scratch;       // 2(k+3) points per step when shared memory is too small
+    int64_t* scratch_off;
+    int8_t* sides_scratch;
+    int smem_points;        // capacity of the shared point buffer
+    int geodesic;           // unused here
+};
+
+__device__ void block_fail(int* s_err, int code, int idx, int aux, double* meta) {
+    if (atomicCAS(s_err, 0, code) == 0) {
+        meta[2] = code;
+        meta[3] = idx;
+        meta[4] = aux;
+    }
+}
+
+// block-wide reductions (any blockDim multiple of 32, <= 1024)
+__device__ double block_sum(double v, double* red) {
+    int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane == 0) red[w] = v;
+    __syncthreads();
+    double t = 0.0;
+    for (int i = 0; i < nw; ++i) t += red[i];
+    __syncthreads();
+    return t;
+}
+__device__ double block_max(double v, double* red) {
+    int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    v = warp_max(v);
+    __syncthreads();
+    if (lane == 0) red[w] = v;
+    __syncthreads();
+    double t = red[0];
+    for (int i = 1; i < nw; ++i) t = fmax(t, red[i]);
+    __syncthreads();
+    return t;
+}
+
+// Prenormalizer (welding.py:609-625) over the n points src[0..n) of tv.
+__device__ bool prenormalize(const double2* tv, const int32_t* src, int n, double* red, Rec* out, int* code) {
+    double sx = 0, sy = 0, cnt = 0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        double2 z = tv[src[i]];
+        if (c_fin(z)) {
+            sx += z.x;
+            sy += z.y;
+            cnt += 1;
+        }
+    }
+    sx = block_sum(sx, red);
+    sy = block_sum(sy, red);
+    cnt = block_sum(cnt, red);
+    if (cnt == 0) {
+        *code = 1;
+        return false;
+    }
+    double2 c = C(sx / cnt, sy / cnt);
+    double m = 0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        double2 z = tv[src[i]];
+        if (c_fin(z)) m = fmax(m, cabs_(csub(z, c)));
+    }
+    double s = block_max(m, red);
+    if (s == 0) {
+        *code = 2;
+        return false;
+    }
+    int tries = 0;
+    for (; tries < 4; ++tries) {
+        double hit = 0;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            double2 z = tv[src[i]];
+            if (c_fin(z) && c_eq(z, c)) hit = 1;
+        }
+        if (block_max(hit, red) == 0) break;
+        c = cadd(c, C(s * 0.0137, s * 0.00271));
+    }
+    if (tries == 4) {
+        *code = 3;
+        return false;
+    }
+    *out = mk_mob(C(1.0 / s, 0.0), C(-c.x / s, -c.y / s), C(0.0, 0.0), C(1.0, 0.0));
+    return true;
+}
+
+__global__ void __launch_bounds__(512) k_phase1(Phase1Args A) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ Rec s_rec[2];
+    __shared__ int s_err;
+    __shared__ int s_has[2];
+    __shared__ double red[32];
+    const StepDesc sd = A.steps[blockIdx.x];
+    double* meta = A.meta + META * (int64_t)blockIdx.x;
+    const int k = sd.k;
+    const int P = k + 3;  // points per side: arc 0..k, aux 0, aux inf
+    double2* pts;
+    int8_t* sides;
+    if (2 * P <= A.smem_points) {
+        pts = reinterpret_cast<double2*>(smem);
+        sides = reinterpret_cast<int8_t*>(pts + A.smem_points);
+    } else {
+        pts = A.scratch + A.scratch_off[blockIdx.x];
+        sides = A.sides_scratch + A.scratch_off[blockIdx.x];
+    }
+    Rec* log_a = A.recs + sd.rec;
+    Rec* log_b = log_a + sd.cap;
+    int na_rec = 0, nb_rec = 0;
+    if (threadIdx.x == 0) {
+        s_err = 0;
+        for (int i = 0; i < META; ++i) meta[i] = 0.0;
+    }
+    __syncthreads();
+    if (k < 1 || k > sd.na - 1 || k > sd.nb - 1) {
+        if (threadIdx.x == 0) block_fail(&s_err, WE_K, k, 0, meta);
+        return;
+    }
+    const int32_t* sa = A.src + sd.src;
+    const int32_t* sb = sa + sd.na;
+    // --- prenormalizers (all cycle points)
+    Rec pre[2];
+    int pcode = 0;
+    bool okA = prenormalize(A.tv, sa, sd.na, red, &pre[0], &pcode);
+    if (!okA) {
+        if (threadIdx.x == 0) block_fail(&s_err, WE_PRE, 0, pcode, meta);
+        return;
+    }
+    bool okB = prenormalize(A.tv, sb, sd.nb, red, &pre[1], &pcode);
+    if (!okB) {
+        if (threadIdx.x == 0) block_fail(&s_err, WE_PRE, 1, pcode, meta);
+        return;
+    }
+    // --- phase-1 points: side A at [0, P), side B at [P, 2P)
+    for (int i = threadIdx.x; i < 2 * P; i += blockDim.x) {
+        int side = i >= P;
+        int t = i - side * P;
+        double2 z;
+        int8_t s = 0;
+        if (t <= k) {
+            z = A.tv[(side ? sb : sa)[t]];
+            apply_rec(pre[side], z, s);
+        } else {
+            z = (t == k + 1) ? C(0.0, 0.0) : cinf();
+        }
+        pts[i] = z;
+        sides[i] = 0;
+    }
+    if (threadIdx.x == 0) {
+        log_a[na_rec++] = pre[0];
+        log_b[nb_rec++] = pre[1];
+    }
+    __syncthreads();
+    auto apply_both = [&](bool use_a, bool use_b) {
+        for (int i = threadIdx.x; i < 2 * P; i += blockDim.x) {
+            int side = i >= P;
+            if (side ? !use_b : !use_a) continue;
+            double2 z = pts[i];
+            int8_t s = sides[i];
+            apply_rec(s_rec[side], z, s);
+            pts[i] = z;
+            sides[i] = s;
+        }
+    };
+    // --- Algorithm 1 on both sides in lockstep (welding.py:546-602)
+    if (threadIdx.x == 0) {
+        if (c_eq(pts[0], pts[1]) || c_eq(pts[P], pts[P + 1])) {
+            block_fail(&s_err, WE_ZIP01, 0, 0, meta);
+        } else {
+            s_rec[0] = mk_sqr(pts[0], pts[1], UP);
+            s_rec[1] = mk_sqr(pts[P], pts[P + 1], DOWN);
+            log_a[na_rec++] = s_rec[0];
+            log_b[nb_rec++] = s_rec[1];
+        }
+    }
+    __syncthreads();
+    if (s_err) return;
+    apply_both(true, true);
+    __syncthreads();
+    for (int j = 2; j <= k; ++j) {
+        if (threadIdx.x == 0) {
+            for (int side = 0; side < 2; ++side) {
+                double2 xi = pts[side * P + j];
+                int8_t sj = sides[side * P + j];
+                if (sj != 0 || c_isinf(xi)) {
+                    block_fail(&s_err, WE_ZIP_HALF, j, side, meta);
+                } else if (!(xi.x > 0)) {
+                    block_fail(&s_err, WE_ZIP_AXIS, j, side, meta);
+                } else if (cabs_(xi) < 1e-13) {
+                    block_fail(&s_err, WE_ZIP_COLL, j, side, meta);
+                } else {
+                    s_rec[side] = mk_open(xi, side ? DOWN : UP);
+                }
+            }
+            if (!s_err) {
+                log_a[na_rec++] = s_rec[0];
+                log_b[nb_rec++] = s_rec[1];
+            }
+        }
+        __syncthreads();
+        if (s_err) return;
+        apply_both(true, true);
+        __syncthreads();
+    }
+    // NaN check ("zipping"), then the axis Mobius sending pts[0] to infinity
+    {
+        double bad = 0;
+        for (int i = threadIdx.x; i < 2 * P; i += blockDim.x) bad = fmax(bad, c_nan(pts[i]) ? 1.0 : 0.0);
+        if (block_max(bad, red) > 0) {
+            if (threadIdx.x == 0) block_fail(&s_err, WE_NAN, 0, 1, meta);
+            return;
+        }
+    }
+    if (threadIdx.x == 0) {
+        for (int side = 0; side < 2; ++side) {
+            double2 w0 = pts[side * P];
+            s_has[side] = 0;
+            if (!c_isinf(w0)) {
+                if (c_zero(w0)) {
+                    block_fail(&s_err, WE_FAR0, 0, side, meta);
+                } else {
+                    int br = side ? DOWN : UP;
+                    Rec r = mk_mob(C(1, 0), C(0, 0), cdiv(C(-1.0, 0.0), w0), C(1, 0), true);
+                    mob_pin(r, w0, cinf(), br);
+                    mob_pin(r, C(0, 0), C(0, 0), br);
+                    s_rec[side] = r;
+                    s_has[side] = 1;
+                    if (side) log_b[nb_rec++] = r; else log_a[na_rec++] = r;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    if (s_err) return;
+    apply_both(s_has[0], s_has[1]);
+    __syncthreads();
+    // --- closing loop (welding.py:673-687)
+    for (int j = k - 1; j >= 1; --j) {
+        if (threadIdx.x == 0) {
+            double2 al = pts[j], be = pts[P + j];
+            if (sides[j] == 0 || c_isinf(al) || al.y == 0.0) {
+                block_fail(&s_err, WE_ALIGN_A, j, 0, meta);
+            } else if (sides[P + j] == 0 || c_isinf(be) || be.y == 0.0) {
+                block_fail(&s_err, WE_ALIGN_B, j, 0, meta);
+            } else if (!walk_less(al.y, be.y)) {
+                block_fail(&s_err, WE_ORDER, j, 0, meta);
+            } else {
+                s_rec[0] = mk_close(al.y, be.y);
+                s_rec[1] = s_rec[0];
+                log_a[na_rec++] = s_rec[0];
+                log_b[nb_rec++] = s_rec[0];
+            }
+        }
+        __syncthreads();
+        if (s_err) return;
+        apply_both(true, true);
+        __syncthreads();
+    }
+    // --- far ends; stage max of |va| over arc + aux (finite) for the deferred check
+    {
+        double m = 0;
+        for (int i = threadIdx.x; i < P; i += blockDim.x)
+            if (c_fin(pts[i])) m = fmax(m, cabs_(pts[i]));
+        m = block_max(m, red);
+        if (threadIdx.x == 0) {
+            double2 qa = pts[0], qb = pts[P];
+            meta[6] = qa.x; meta[7] = qa.y; meta[8] = qb.x; meta[9] = qb.y;
+            meta[10] = m;
+            meta[14] = na_rec;
+            meta[15] = nb_rec;
+            s_rec[0] = mk_sq(c_isinf(qa) ? cinf() : qa);
+            s_rec[1] = s_rec[0];
+            log_a[na_rec++] = s_rec[0];
+            log_b[nb_rec++] = s_rec[0];
+        }
+    }
+    __syncthreads();
+    apply_both(true, true);
+    __syncthreads();
+    // --- normalization (welding.py:699-717)
+    if (threadIdx.x == 0) {
+        double2 za = pts[k + 1], zb = pts[P + k + 1], ia = pts[k + 2], ib = pts[P + k + 2];
+        if (c_isinf(za) || c_isinf(zb) || c_isinf(ia) || c_isinf(ib)) {
+            block_fail(&s_err, WE_TRACK, 0, 0, meta);
+        } else {
+            double2 zmid = C(0.5 * (ia.x + ib.x), 0.5 * (ia.y + ib.y));
+            double2 co[4];
+            if (!c_eq(za, zb) && !c_eq(za, zmid) && !c_eq(zb, zmid)) {
+                double2 zs[3] = {za, zb, zmid}, ws[3] = {C(-1, 0), C(1, 0), cinf()};
+                if (!three_point(zs, ws, co)) block_fail(&s_err, WE_THREE, 0, 0, meta);
+            } else if (!c_zero(za)) {
+                co[0] = cdiv(C(-1.0, 0.0), za); co[1] = C(0, 0); co[2] = C(0, 0); co[3] = C(1, 0);
+            } else {
+                co[0] = C(1, 0); co[1] = C(0, 0); co[2] = C(0, 0); co[3] = C(1, 0);
+            }
+            if (!s_err) {
+                s_rec[0] = mk_mob(co[0], co[1], co[2], co[3]);
+                s_rec[1] = s_rec[0];
+                log_a[na_rec++] = s_rec[0];
+                log_b[nb_rec++] = s_rec[0];
+            }
+        }
+    }
+    __syncthreads();
+    if (s_err) return;
+    apply_both(true, true);
+    __syncthreads();
+    {
+        double bad = 0;
+        for (int i = threadIdx.x; i < 2 * P; i += blockDim.x) bad = fmax(bad, c_nan(pts[i]) ? 1.0 : 0.0);
+        if (block_max(bad, red) > 0) {
+            if (threadIdx.x == 0) block_fail(&s_err, WE_NAN, 0, 3, meta);
+            return;
+        }
+    }
+    // --- closed welding: respread the seam (welding.py:751-763)
+    if (sd.closed) {
+        if (threadIdx.x == 0) {
+            int n = k + 1;
+            double2 an[3] = {pts[0], pts[n / 3], pts[(2 * n) / 3]};
+            double2 tg[3] = {C(1.0, 0.0), C(cos(2 * M_PI / 3), sin(2 * M_PI / 3)),
+                             C(cos(4 * M_PI / 3), sin(4 * M_PI / 3))};
+            double2 co[4];
+            if (!three_point(an, tg, co)) {
+                block_fail(&s_err, WE_THREE, 1, 0, meta);
+            } else {
+                s_rec[0] = mk_mob(co[0], co[1], co[2], co[3]);
+                s_rec[1] = s_rec[0];
+                log_a[na_rec++] = s_rec[0];
+                log_b[nb_rec++] = s_rec[0];
+            }
+        }
+        __syncthreads();
+        if (s_err) return;
+        for (int i = threadIdx.x; i < 2 * P; i += blockDim.x) sides[i] = 0;
+        __syncthreads();
+        apply_both(true, true);
+        __syncthreads();
+    }
+    // --- outputs: arcs, seam over the arc, maxima, polygon area of the a arc
+    double seam = 0, ma = 0, mb = 0, mx = 0, area = 0;
+    for (int t = threadIdx.x; t <= k; t += blockDim.x) {
+        double2 a = pts[t], b = pts[P + t];
+        A.arc_out[sd.arc + t] = a;
+        A.arc_out[sd.arc + k + 1 + t] = b;
+        double g = (c_isinf(a) && c_isinf(b)) ? 0.0 : cabs_(csub(a, b));
+        if (!isnan(g)) seam = fmax(seam, g);
+        if (c_fin(a)) ma = fmax(ma, cabs_(a));
+        if (c_fin(b)) mb = fmax(mb, cabs_(b));
+        double2 nx = pts[(t + 1) % (k + 1)];
+        area += 0.5 * (a.x * nx.y - a.y * nx.x);
+    }
+    for (int t = threadIdx.x; t < 2; t += blockDim.x) {
+        double2 a = pts[k + 1 + t], b = pts[P + k + 1 + t];
+        if (c_fin(a)) mx = fmax(mx, cabs_(a));
+        if (c_fin(b)) mx = fmax(mx, cabs_(b));
+    }
+    seam = block_max(seam, red);
+    ma = block_max(ma, red);
+    mb = block_max(mb, red);
+    mx = block_max(mx, red);
+    area = block_sum(area, red);
+    if (threadIdx.x == 0) {
+        meta[0] = na_rec;
+        meta[1] = nb_rec;
+        meta[5] = seam;
+        meta[11] = ma;
+        meta[12] = mb;
+        meta[13] = mx;
+        meta[16] = area;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// phase 2: replay a step's log on a point (write-back list of a level)
+//   entry = (slot, code): code bit 31 -> B log; bits 0..23: arc position + 1
+//   (0 = replay); bit 24: take the arc value from side B; bit 25: cycle
+//   point of side A (contributes to the scale maxima); bit 26: cycle point of B
+
+struct ReplayArgs {
+    const int32_t* wb;          // (slot, code, step) triples
+    int64_t nwb;
+    const StepDesc* steps;
+    const Rec* recs;
+    double2* tv;
+    const double2* arc_out;
+    double* meta;               // per step
+    unsigned long long* maxbits;  // per step: [stage_a, final_a, final_b]
+    int* nan_flag;
+};
+
+__global__ void k_replay_slots(ReplayArgs A) {
+    GRID_STRIDE(i, A.nwb) {
+        int slot = A.wb[3 * i], code = A.wb[3 * i + 1], step = A.wb[3 * i + 2];
+        const StepDesc sd = A.steps[step];
+        int arcpos = (code & 0xffffff) - 1;
+        bool sideB = (code >> 31) & 1;
+        if (A.meta[META * step + 2] != 0.0) continue;  // failed step: leave values
+        if (arcpos >= 0) {
+            bool fromB = (code >> 24) & 1;
+            A.tv[slot] = A.arc_out[sd.arc + (fromB ? sd.k + 1 : 0) + arcpos];
+            continue;
+        }
+        const Rec* log = A.recs + sd.rec + (sideB ? sd.cap : 0);
+        int nrec = (int)A.meta[META * step + (sideB ? 1 : 0)];
+        int sq = (int)A.meta[META * step + (sideB ? 15 : 14)];
+        double2 z = A.tv[slot];
+        int8_t s = 0;
+        double stage = 0;
+        for (int r = 0; r < nrec; ++r) {
+            if (r == sq) stage = c_fin(z) ? cabs_(z) : 0.0;
+            Rec rec = log[r];
+            apply_rec(rec, z, s);
+        }
+        if (c_nan(z)) atomicExch(A.nan_flag, 1);
+        A.tv[slot] = z;
+        bool cycA = (code >> 25) & 1, cycB = (code >> 26) & 1;
+        double fin = c_fin(z) ? cabs_(z) : 0.0;
+        if (cycA) {
+            atomicMax(&A.maxbits[3 * step + 0], (unsigned long long)__double_as_longlong(stage));
+            atomicMax(&A.maxbits[3 * step + 1], (unsigned long long)__double_as_longlong(fin));
+        }
+        if (cycB) atomicMax(&A.maxbits[3 * step + 2], (unsigned long long)__double_as_longlong(fin));
+    }
+}
+
+// generic replay: log on a point array (apply_log, welding.py:512-526)
+__global__ void k_replay_points(const Rec* __restrict__ recs, int nrec, double2* z, int8_t* sides, int64_t n,
+                                int* nan_flag) {
+    __shared__ Rec s_recs[32];
+    for (int base = 0; base < nrec; base += 32) {
+        int cnt = min(32, nrec - base);
+        __syncthreads();
+        for (int i = threadIdx.x; i < cnt; i += blockDim.x) s_recs[i] = recs[base + i];
+        __syncthreads();
+        GRID_STRIDE(i, n) {
+            double2 v = z[i];
+            int8_t s = sides ? sides[i] : 0;
+            for (int r = 0; r < cnt; ++r) apply_rec(s_recs[r], v, s);
+            z[i] = v;
+            if (sides) sides[i] = s;
+        }
+    }
+    GRID_STRIDE(i, n) if (c_nan(z[i])) atomicExch(nan_flag, 1);
+}
+
+
+// ---------------------------------------------------------------------------
+// polygon helpers (welding.py:770-796) and the geodesic map (welding.py:803-842)
+
+// even-odd ray casting of p against poly (n points), block-wide
+__device__ bool block_inside(const double2* poly, int n, double2 p, double* red) {
+    double cnt = 0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        double2 a = poly[i], b = poly[(i + 1) % n];
+        bool cond = (a.y > p.y) != (b.y > p.y);
+        double xint = a.x + (p.y - a.y) / (b.y - a.y) * (b.x - a.x);
+        if (cond && (p.x < xint)) cnt += 1;
+    }
+    cnt = block_sum(cnt, red);
+    return ((long long)cnt) % 2 == 1;
+}
+
+// polygon_interior_point: centroid, else edge-midpoint offsets
+__device__ bool interior_point(const double2* poly, int n, double* red, double2* out) {
+    double sx = 0, sy = 0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        sx += poly[i].x;
+        sy += poly[i].y;
+    }
+    sx = block_sum(sx, red);
+    sy = block_sum(sy, red);
+    double2 c = C(sx / n, sy / n);
+    if (block_inside(poly, n, c, red)) {
+        *out = c;
+        return true;
+    }
+    const double ts[3] = {0.25, 0.05, 0.01};
+    for (int i = 0; i < n; ++i) {
+        double2 a = poly[i], b = poly[(i + 1) % n];
+        double2 mid = C(0.5 * (a.x + b.x), 0.5 * (a.y + b.y));
+        double2 nrm = cmul(csub(b, a), C(0.0, 1.0));
+        for (int q = 0; q < 3; ++q) {
+            double2 cand = cadd(mid, cmul(C(ts[q], 0.0), nrm));
+            if (block_inside(poly, n, cand, red)) {
+                *out = cand;
+                return true;
+            }
+        }
+    }
+    return false;
+}
+
+struct GeoArgs {
+    const double2* tv;
+    const int32_t* src;     // n cycle points (slot ids) in cycle order
+    int n;
+    int has_interior;
+    double2 interior;
+    double2* pts;           // scratch n+1
+    int8_t* sides;          // scratch n+1
+    int32_t* order;         // scratch n: position -> src index (after orientation)
+    double2* circ;          // out: circle value per src index
+    Rec* recs;
+    double* meta;           // [0] nrec, [2] err, [3] idx, [4] aux, [5] max ||z|-1|
+};
+
+__global__ void __launch_bounds__(512) k_geodesic(GeoArgs A) {
+    __shared__ Rec s_rec;
+    __shared__ int s_err;
+    __shared__ double red[32];
+    __shared__ double2 s_c;
+    const int n = A.n;
+    double* meta = A.meta;
+    if (threadIdx.x == 0) {
+        s_err = 0;
+        for (int i = 0; i < META; ++i) meta[i] = 0.0;
+    }
+    __syncthreads();
+    // orientation (pipeline.py:218-222): reverse all but the first if cw
+    double area = 0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        double2 a = A.tv[A.src[i]], b = A.tv[A.src[(i + 1) % n]];
+        area += 0.5 * (a.x * b.y - a.y * b.x);
+    }
+    area = block_sum(area, red);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        int o = (area < 0 && i > 0) ? n - i : i;
+        A.order[i] = o;
+        A.pts[i] = A.tv[A.src[o]];
+        A.sides[i] = 0;
+    }
+    __syncthreads();
+    if (A.has_interior) {
+        if (threadIdx.x == 0) s_c = A.interior;
+    } else {
+        double2 c;
+        bool ok = interior_point(A.pts, n, red, &c);
+        if (threadIdx.x == 0) {
+            if (!ok) block_fail(&s_err, WE_INTERIOR, 0, 0, meta);
+            s_c = c;
+        }
+    }
+    __syncthreads();
+    if (s_err) return;
+    if (threadIdx.x == 0) {
+        A.pts[n] = s_c;
+        A.sides[n] = 0;
+    }
+    __syncthreads();
+    int nrec = 0;
+    auto apply_all = [&]() {
+        for (int i = threadIdx.x; i <= n; i += blockDim.x) {
+            double2 z = A.pts[i];
+            int8_t s = A.sides[i];
+            apply_rec(s_rec, z, s);
+            A.pts[i] = z;
+            A.sides[i] = s;
+        }
+    };
+    if (threadIdx.x == 0) {
+        if (c_eq(A.pts[0], A.pts[1])) block_fail(&s_err, WE_ZIP01, 0, 0, meta);
+        else s_rec = mk_sqr(A.pts[0], A.pts[1], UP);
+        A.recs[nrec] = s_rec;
+    }
+    ++nrec;
+    __syncthreads();
+    if (s_err) return;
+    apply_all();
+    __syncthreads();
+    for (int j = 2; j <= n - 1; ++j) {
+        if (threadIdx.x == 0) {
+            double2 xi = A.pts[j];
+            if (A.sides[j] != 0 || c_isinf(xi)) block_fail(&s_err, WE_ZIP_HALF, j, 0, meta);
+            else if (!(xi.x > 0)) block_fail(&s_err, WE_ZIP_AXIS, j, 0, meta);
+            else if (cabs_(xi) < 1e-13) block_fail(&s_err, WE_ZIP_COLL, j, 0, meta);
+            else {
+                s_rec = mk_open(xi, UP);
+                A.recs[nrec] = s_rec;
+            }
+        }
+        ++nrec;
+        __syncthreads();
+        if (s_err) return;
+        apply_all();
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        double2 w0 = A.pts[0];
+        s_rec = mk_sq(c_isinf(w0) ? cinf() : w0);
+        A.recs[nrec] = s_rec;
+    }
+    ++nrec;
+    __syncthreads();
+    apply_all();
+    __syncthreads();
+    if (threadIdx.x == 0) {  // Cayley transform to the disk
+        Rec r = mk_mob(C(1, 0), C(0, -1), C(1, 0), C(0, 1));
+        mob_pin(r, cinf(), C(1.0, 0.0), FREE);
+        s_rec = r;
+        A.recs[nrec] = r;
+    }
+    ++nrec;
+    __syncthreads();
+    apply_all();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double2 al = A.pts[n];
+        if (!(cabs_(al) < 1)) {
+            block_fail(&s_err, WE_GEO_DISK, 0, 0, meta);
+        } else {
+            s_rec = mk_mob(C(1, 0), cneg(al), C(-al.x, al.y), C(1, 0));
+            A.recs[nrec] = s_rec;
+        }
+    }
+    ++nrec;
+    __syncthreads();
+    if (s_err) return;
+    apply_all();
+    __syncthreads();
+    double err = 0, bad = 0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        double2 z = A.pts[i];
+        if (c_nan(z)) bad = 1;
+        err = fmax(err, fabs(cabs_(z) - 1.0));
+        A.circ[A.order[i]] = z;
+    }
+    err = block_max(err, red);
+    bad = block_max(bad, red);
+    if (threadIdx.x == 0) {
+        meta[0] = nrec;
+        meta[5] = err;
+        meta[6] = s_c.x;
+        meta[7] = s_c.y;
+        if (bad > 0) block_fail(&s_err, WE_NAN, 0, 4, meta);
+        else if (err > 1e-9) block_fail(&s_err, WE_GEO_CIRCLE, 0, 0, meta);
+    }
+}
+
+__global__ void k_interior(const double2* __restrict__ tv, const int32_t* __restrict__ src, int n, int reverse,
+                           double2* scratch, double* out) {
+    __shared__ double red[32];
+    for (int i = threadIdx.x; i < n; i += blockDim.x) scratch[i] = tv[src[reverse ? n - 1 - i : i]];
+    __syncthreads();
+    double2 c;
+    bool ok = interior_point(scratch, n, red, &c);
+    if (threadIdx.x == 0) {
+        out[0] = c.x;
+        out[1] = c.y;
+        out[2] = ok ? 0.0 : 1.0;
+    }
+}
+
+// z[i] = add + 1 / (z[i] - sub)  (pipeline.py:253-263 exterior inversion)
+__global__ void k_inv_shift(double2* z, const int32_t* __restrict__ idx, int64_t n, double2 add, double2 sub) {
+    GRID_STRIDE(i, n) {
+        int64_t j = idx ? idx[i] : i;
+        z[j] = cadd(add, cdiv(C(1.0, 0.0), csub(z[j], sub)));
+    }
+}
+
+// gather/scatter helpers between tracked values and submesh-local vertices
+__global__ void k_gather_c(const double2* __restrict__ src, const int32_t* __restrict__ idx, double2* dst,
+                           int64_t n) {
+    GRID_STRIDE(i, n) dst[i] = src[idx[i]];
+}
+__global__ void k_scatter_c(const double2* __restrict__ src, const int32_t* __restrict__ idx, double2* dst,
+                            int64_t n) {
+    GRID_STRIDE(i, n) dst[idx[i]] = src[i];
+}
+
+}  // namespace weld
+}  // namespace pgcp
+
+// ===========================================================================
+// host side
+namespace pgcp {
+namespace weld {
+namespace {
+
+std::string err_text(int code, int idx, int aux, double a = 0, double b = 0, double c = 0) {
+    char buf[256];
+    static const char* stage[] = {"", "zipping", "intermediate form", "partial weld", "geodesic algorithm", "apply_log"};
+    switch (code) {
+        case WE_ZIP01: return "zip points 0 and 1 coincide";
+        case WE_ZIP_HALF: snprintf(buf, sizeof buf, "zip point %d left the right half-plane", idx); return buf;
+        case WE_ZIP_AXIS:
+            snprintf(buf, sizeof buf, "zip point %d landed on the imaginary axis (duplicate or non-Jordan input)", idx);
+            return buf;
+        case WE_ZIP_COLL:
+            snprintf(buf, sizeof buf, "zip points %d and %d collapsed (spacing below 1e-13 in the zip frame)", idx - 1, idx);
+            return buf;
+        case WE_NAN:
+            snprintf(buf, sizeof buf, "numerical breakdown (NaN) during %s", stage[aux >= 1 && aux <= 5 ? aux : 3]);
+            return buf;
+        case WE_FAR0: return "far end of the zip collapsed to 0";
+        case WE_ALIGN_A: snprintf(buf, sizeof buf, "alignment point %d (a side) left the imaginary axis", idx); return buf;
+        case WE_ALIGN_B: snprintf(buf, sizeof buf, "alignment point %d (b side) left the imaginary axis", idx); return buf;
+        case WE_ORDER:
+            snprintf(buf, sizeof buf, "alignment points %d not strictly ordered on the imaginary axis (invalid correspondence)", idx);
+            return buf;
+        case WE_TRACK: return "tracking points degenerated during welding";
+        case WE_FAREND: return "far ends of the two slits diverged";
+        case WE_SEAM:
+            snprintf(buf, sizeof buf, "seam alignment error %.3e exceeds %g x scale %.3e", a, b, c);
+            return buf;
+        case WE_PRE:
+            return aux == 1 ? "no finite boundary points"
+                            : (aux == 2 ? "degenerate boundary (all points coincide)"
+                                        : "could not place tracking origin off the boundary");
+        case WE_THREE: return "three-point Mobius needs distinct points";
+        case WE_K: snprintf(buf, sizeof buf, "shared prefix length k=%d out of range", idx); return buf;
+        case WE_GEO_DISK: return "interior point left the unit disk during the geodesic mapping";
+        case WE_GEO_CIRCLE: snprintf(buf, sizeof buf, "boundary point left the unit circle by %.3e", a); return buf;
+        case WE_INTERIOR: return "could not locate a point inside the polygon";
+        default: return "weld failure";
+    }
+}
+
+constexpr int P1_THREADS = 512;
+constexpr int P1_SMEM_POINTS = 6000;  // 6000 * 17 B ~ 100 KB
+
+int setup_phase1_smem() {
+    static bool done = false;
+    if (!done) {
+        int bytes = P1_SMEM_POINTS * (sizeof(double2) + 1);
+        PGCP_TRY_CUDA(cudaFuncSetAttribute(k_phase1, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+        done = true;
+    }
+    return PGCP_OK;
+}
+
+double bits_to_d(unsigned long long b) {
+    double d;
+    memcpy(&d, &b, sizeof d);
+    return d;
+}
+
+}  // namespace
+
+// Run a whole weld schedule on the tracked values tv (device complex).
+//  info  host int32 [nsteps*6]: k, closed, na, nb, comp_a, comp_b
+//  src   host int32 [sum(na+nb)] slot ids of a_cycle then b_cycle per step
+//  wb_off host int64 [nsteps+1], wb host int32 [2*total] (slot, code)
+//  out   host f64 [nsteps*8]: seam_error, seam_residual, area(res.a arc), status,
+//        nrec_a, nrec_b, level, spare
+int run_schedule(double2* tv, int32_t nsteps, const int32_t* info, const int32_t* src, const int64_t* wb_off,
+                 const int32_t* wb, double hard_tol, double* out, Rec* recs_host, int64_t recs_cap_total,
+                 cudaStream_t s) {
+    if (nsteps <= 0) return PGCP_OK;
+    PGCP_TRY(setup_phase1_smem());
+    // levels: a step waits for the previous steps on either of its components
+    std::vector<int> level(nsteps, 0);
+    {
+        std::vector<std::pair<int, int>> last;  // comp -> level
+        std::unordered_map<int, int> lv;
+        for (int i = 0; i < nsteps; ++i) {
+            int ca = info[6 * i + 4], cb = info[6 * i + 5];
+            int l = 0;
+            if (lv.count(ca)) l = std::max(l, lv[ca] + 1);
+            if (lv.count(cb)) l = std::max(l, lv[cb] + 1);
+            level[i] = l;
+            lv[ca] = l;
+            lv[cb] = l;
+        }
+    }
+    int nlev = *std::max_element(level.begin(), level.end()) + 1;
+    // order steps by (level, index)
+    std::vector<int> order(nsteps);
+    for (int i = 0; i < nsteps; ++i) order[i] = i;
+    std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return level[x] < level[y]; });
+    std::vector<int> pos(nsteps);
+    for (int q = 0; q < nsteps; ++q) pos[order[q]] = q;
+    // descriptors (in launch order)
+    std::vector<StepDesc> sd(nsteps);
+    std::vector<int64_t> src_off(nsteps + 1, 0), scratch_off(nsteps, 0);
+    for (int i = 0; i < nsteps; ++i) src_off[i + 1] = src_off[i] + info[6 * i + 2] + info[6 * i + 3];
+    int64_t rec_tot = 0, arc_tot = 0, scr_tot = 0;
+    for (int q = 0; q < nsteps; ++q) {
+        int i = order[q];
+        StepDesc& d = sd[q];
+        d.k = info[6 * i];
+        d.closed = info[6 * i + 1];
+        d.na = info[6 * i + 2];
+        d.nb = info[6 * i + 3];
+        d.src = src_off[i];
+        d.cap = 2 * d.k + 16;
+        d.pad = 0;
+        d.rec = rec_tot;
+        rec_tot += 2 * (int64_t)d.cap;
+        d.arc = arc_tot;
+        arc_tot += 2 * (int64_t)(d.k + 1);
+        scratch_off[q] = scr_tot;
+        if (2 * (d.k + 3) > P1_SMEM_POINTS) scr_tot += 2 * (int64_t)(d.k + 3);
+    }
+    // write-back entries (slot, code, launch-order step)
+    int64_t nwb = wb_off[nsteps];
+    std::vector<int32_t> wb3(3 * std::max<int64_t>(nwb, 1));
+    std::vector<int64_t> lev_wb(nlev + 1, 0);
+    {
+        int64_t o = 0;
+        for (int l = 0; l < nlev; ++l) {
+            lev_wb[l] = o;
+            for (int q = 0; q < nsteps; ++q) {
+                int i = order[q];
+                if (level[i] != l) continue;
+                for (int64_t e = wb_off[i]; e < wb_off[i + 1]; ++e) {
+                    wb3[3 * o] = wb[2 * e];
+                    wb3[3 * o + 1] = wb[2 * e + 1];
+                    wb3[3 * o + 2] = q;
+                    ++o;
+                }
+            }
+        }
+        lev_wb[nlev] = o;
+    }
+    DevBuf<StepDesc> d_sd;
+    DevBuf<int32_t> d_src, d_wb;
+    DevBuf<Rec> d_recs;
+    DevBuf<double2> d_arc, d_scr;
+    DevBuf<int8_t> d_sscr;
+    DevBuf<int64_t> d_scroff;
+    DevBuf<double> d_meta;
+    DevBuf<unsigned long long> d_max;
+    DevBuf<int> d_nan;
+    PGCP_TRY(d_sd.alloc(nsteps, s));
+    PGCP_TRY(d_src.alloc(src_off[nsteps], s));
+    PGCP_TRY(d_wb.alloc(3 * std::max<int64_t>(nwb, 1), s));
+    PGCP_TRY(d_recs.alloc(rec_tot, s));
+    PGCP_TRY(d_arc.alloc(arc_tot, s));
+    PGCP_TRY(d_scr.alloc(std::max<int64_t>(scr_tot, 1), s));
+    PGCP_TRY(d_sscr.alloc(std::max<int64_t>(scr_tot, 1), s));
+    PGCP_TRY(d_scroff.alloc(nsteps, s));
+    PGCP_TRY(d_meta.alloc((int64_t)META * nsteps, s));
+    PGCP_TRY(d_max.alloc(3 * (int64_t)nsteps, s));
+    PGCP_TRY(d_max.zero(s));
+    PGCP_TRY(d_nan.alloc(1, s));
+    PGCP_TRY(d_nan.zero(s));
+    PGCP_TRY_CUDA(cudaMemcpyAsync(d_sd.p, sd.data(), nsteps * sizeof(StepDesc), cudaMemcpyHostToDevice, s));
+    PGCP_TRY_CUDA(cudaMemcpyAsync(d_src.p, src, src_off[nsteps] * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    PGCP_TRY_CUDA(cudaMemcpyAsync(d_wb.p, wb3.data(), 3 * nwb * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    PGCP_TRY_CUDA(cudaMemcpyAsync(d_scroff.p, scratch_off.data(), nsteps * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    int q0 = 0;
+    for (int l = 0; l < nlev; ++l) {
+        int q1 = q0;
+        while (q1 < nsteps && level[order[q1]] == l) ++q1;
+        Phase1Args a;
+        a.steps = d_sd.p + q0;
+        a.src = d_src.p;
+        a.tv = tv;
+        a.arc_out = d_arc.p;
+        a.recs = d_recs.p;
+        a.meta = d_meta.p + (int64_t)META * q0;
+        a.scratch = d_scr.p;
+        a.scratch_off = d_scroff.p + q0;
+        a.sides_scratch = d_sscr.p;
+        a.smem_points = P1_SMEM_POINTS;
+        a.geodesic = 0;
+        size_t smem = P1_SMEM_POINTS * (sizeof(double2) + 1);
+        k_phase1<<<q1 - q0, P1_THREADS, smem, s>>>(a);
+        PGCP_LAUNCH_CHECK();
+        int64_t n = lev_wb[l + 1] - lev_wb[l];
+        if (n > 0) {
+            ReplayArgs r;
+            r.wb = d_wb.p + 3 * lev_wb[l];
+            r.nwb = n;
+            r.steps = d_sd.p;
+            r.recs = d_recs.p;
+            r.tv = tv;
+            r.arc_out = d_arc.p;
+            r.meta = d_meta.p;
+            r.maxbits = d_max.p;
+            r.nan_flag = d_nan.p;
+            k_replay_slots<<<grid_for(n, 128), 128, 0, s>>>(r);
+            PGCP_LAUNCH_CHECK();
+        }
+        q0 = q1;
+    }
+    std::vector<double> meta((size_t)META * nsteps);
+    std::vector<unsigned long long> mx(3 * (size_t)nsteps);
+    int hnan = 0;
+    PGCP_TRY_CUDA(cudaMemcpyAsync(meta.data(), d_meta.p, meta.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+    PGCP_TRY_CUDA(cudaMemcpyAsync(mx.data(), d_max.p, mx.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    PGCP_TRY_CUDA(cudaMemcpyAsync(&hnan, d_nan.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    if (recs_host && recs_cap_total >= rec_tot)
+        PGCP_TRY_CUDA(cudaMemcpyAsync(recs_host, d_recs.p, rec_tot * sizeof(Rec), cudaMemcpyDeviceToHost, s));
+    PGCP_TRY_CUDA(cudaStreamSynchronize(s));
+    int status = PGCP_OK;
+    for (int i = 0; i < nsteps; ++i) {
+        int q = pos[i];
+        const double* m = &meta[(size_t)META * q];
+        int code = (int)m[2];
+        double stage = std::max(m[10], bits_to_d(mx[3 * q]));
+        double fa = std::max(m[11], bits_to_d(mx[3 * q + 1]));
+        double fb = std::max(m[12], bits_to_d(mx[3 * q + 2]));
+        double scale = std::max(std::max(fa, fb), m[13]);
+        if (scale <= 0) scale = 1.0;
+        double2 qa = make_double2(m[6], m[7]), qb = make_double2(m[8], m[9]);
+        bool ia = std::isinf(qa.x) || std::isinf(qa.y), ib = std::isinf(qb.x) || std::isinf(qb.y);
+        bool far_bad = false;
+        if (code == 0 || code == WE_TRACK || code == WE_THREE || code == WE_NAN) {
+            double sa = stage > 0 ? stage : 1.0;
+            far_bad = (ia != ib) || (!ia && std::hypot(qa.x - qb.x, qa.y - qb.y) > 1e-9 * std::max(sa, 1.0));
+            if (code == WE_NAN && (int)m[4] != 3) far_bad = false;
+        }
+        std::string msg;
+        if (far_bad) {
+            code = WE_FAREND;
+            msg = err_text(code, 0, 0);
+        } else if (code != 0) {
+            msg = err_text(code, (int)m[3], (int)m[4]);
+        } else if (m[5] > hard_tol * scale) {
+            code = WE_SEAM;
+            msg = err_text(code, 0, 0, m[5], hard_tol, scale);
+        }
+        double resid_scale = std::max(fa, fb);
+        out[8 * i + 0] = m[5];
+        out[8 * i + 1] = resid_scale > 0 ? m[5] / resid_scale : 0.0;
+        out[8 * i + 2] = m[16];
+        out[8 * i + 3] = code;
+        out[8 * i + 4] = m[0];
+        out[8 * i + 5] = m[1];
+        out[8 * i + 6] = level[i];
+        out[8 * i + 7] = (double)sd[q].rec;
+        if (code != 0 && status == PGCP_OK) {
+            status = PGCP_E_WELD;
+            set_error("weld step %d: %s", i, msg.c_str());
+        }
+    }
+    if (status == PGCP_OK && hnan) {
+        set_error("numerical breakdown (NaN) during apply_log");
+        status = PGCP_E_WELD;
+    }
+    return status;
+}
+
+}  // namespace weld
+}  // namespace pgcp
+
+using namespace pgcp;
+using namespace pgcp::weld;
+
+extern "C" {
+
+PGCP_API int pgcp_weld_schedule_run(double* tv, int32_t nsteps, const int32_t* info, const int32_t* src,
+                                    const int64_t* wb_off, const int32_t* wb, double hard_tol, double* out,
+                                    pgcp_rec* recs_host, int64_t recs_cap, void* stream) {
+    if (!tv || nsteps < 0 || (nsteps > 0 && (!info || !src || !wb_off || !out))) {
+        set_error("pgcp_weld_schedule_run: invalid arguments");
+        return PGCP_E_INVALID;
+    }
+    return run_schedule(reinterpret_cast<double2*>(tv), nsteps, info, src, wb_off, wb, hard_tol, out, recs_host,
+                        recs_cap, reinterpret_cast<cudaStream_t>(stream));
+}
+
+// apply_log (welding.py:512-526): records from the host, points on the device
+PGCP_API int pgcp_weld_replay(const pgcp_rec* recs, int32_t nrec, double* pts, int8_t* sides, int64_t npts,
+                              void* stream) {
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (npts <= 0) return PGCP_OK;
+    DevBuf<Rec> d;
+    DevBuf<int> flag;
+    PGCP_TRY(d.alloc(std::max(nrec, 1), s));
+    PGCP_TRY(flag.alloc(1, s));
+    PGCP_TRY(flag.zero(s));
+    if (nrec > 0) PGCP_TRY_CUDA(cudaMemcpyAsync(d.p, recs, nrec * sizeof(Rec), cudaMemcpyHostToDevice, s));
+    k_replay_points<<<grid_for(npts, 128), 128, 0, s>>>(d.p, nrec, reinterpret_cast<double2*>(pts), sides, npts,
+                                                         flag.p);
+    PGCP_LAUNCH_CHECK();
+    int h = 0;
+    PGCP_TRY(fetch_scalar(flag.p, &h, s));
+    if (h) {
+        set_error("numerical breakdown (NaN) during apply_log");
+        return PGCP_E_WELD;
+    }
+    return PGCP_OK;
+}
+
+// geodesic_to_circle over the cycle tv[src[0..n)] (host src).
+//   circ  device complex [n], recs host [cap], meta host f64 [8]: nrec, err, idx,
+//   aux, circle error, interior.re, interior.im
+PGCP_API int pgcp_weld_geodesic(const double* tv, const int32_t* src, int32_t n, const double* interior,
+                                double* circ, pgcp_rec* recs, int32_t cap, double* meta_out, void* stream) {
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (n < 3) {
+        set_error("need at least 3 boundary points");
+        return PGCP_E_WELD;
+    }
+    if (cap < n + 4) {
+        set_error("pgcp_weld_geodesic: record capacity %d < %d", cap, n + 4);
+        return PGCP_E_INVALID;
+    }
+    DevBuf<int32_t> d_src, d_order;
+    DevBuf<double2> d_pts;
+    DevBuf<int8_t> d_sides;
+    DevBuf<Rec> d_recs;
+    DevBuf<double> d_meta;
+    PGCP_TRY(d_src.alloc(n, s));
+    PGCP_TRY(d_order.alloc(n, s));
+    PGCP_TRY(d_pts.alloc(n + 1, s));
+    PGCP_TRY(d_sides.alloc(n + 1, s));
+    PGCP_TRY(d_recs.alloc(cap, s));
+    PGCP_TRY(d_meta.alloc(META, s));
+    PGCP_TRY_CUDA(cudaMemcpyAsync(d_src.p, src, n * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    GeoArgs a;
+    a.tv = reinterpret_cast<const double2*>(tv);
+    a.src = d_src.p;
+    a.n = n;
+    a.has_interior = interior != nullptr;
+    a.interior = interior ? make_double2(interior[0], interior[1]) : make_double2(0, 0);
+    a.pts = d_pts.p;
+    a.sides = d_sides.p;
+    a.order = d_order.p;
+    a.circ = reinterpret_cast<double2*>(circ);
+    a.recs = d_recs.p;
+    a.meta = d_meta.p;
+    k_geodesic<<<1, 512, 0, s>>>(a);
+    PGCP_LAUNCH_CHECK();
+    double m[META];
+    PGCP_TRY_CUDA(cudaMemcpyAsync(m, d_meta.p, sizeof m, cudaMemcpyDeviceToHost, s));
+    PGCP_TRY_CUDA(cudaStreamSynchronize(s));
+    int nrec = (int)m[0];
+    if (recs && nrec > 0) {
+        PGCP_TRY_CUDA(cudaMemcpyAsync(recs, d_recs.p, nrec * sizeof(Rec), cudaMemcpyDeviceToHost, s));
+        PGCP_TRY_CUDA(cudaStreamSynchronize(s));
+    }
+    if (meta_out) {
+        meta_out[0] = nrec;
+        meta_out[1] = m[2];
+        meta_out[2] = m[3];
+        meta_out[3] = m[4];
+        meta_out[4] = m[5];
+        meta_out[5] = m[6];
+        meta_out[6] = m[7];
+    }
+    if (m[2] != 0) {
+        set_error("%s", err_text((int)m[2], (int)m[3], (int)m[4], m[5]).c_str());
+        return PGCP_E_WELD;
+    }
+    return PGCP_OK;
+}
+
+// polygon_interior_point (welding.py:781-796) of tv[src] (optionally reversed)
+PGCP_API int pgcp_polygon_interior(const double* tv, const int32_t* src, int32_t n, int reverse, double* out,
+                                   void* stream) {
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    DevBuf<int32_t> d_src;
+    DevBuf<double2> scr;
+    DevBuf<double> d_out;
+    PGCP_TRY(d_src.alloc(n, s));
+    PGCP_TRY(scr.alloc(n, s));
+    PGCP_TRY(d_out.alloc(3, s));
+    PGCP_TRY_CUDA(cudaMemcpyAsync(d_src.p, src, n * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    k_interior<<<1, 512, 0, s>>>(reinterpret_cast<const double2*>(tv), d_src.p, n, reverse, scr.p, d_out.p);
+    PGCP_LAUNCH_CHECK();
+    double h[3];
+    PGCP_TRY_CUDA(cudaMemcpyAsync(h, d_out.p, sizeof h, cudaMemcpyDeviceToHost, s));
+    PGCP_TRY_CUDA(cudaStreamSynchronize(s));
+    if (h[2] != 0) {
+        set_error("could not locate a point inside the polygon");
+        return PGCP_E_WELD;
+    }
+    out[0] = h[0];
+    out[1] = h[1];
+    return PGCP_OK;
+}
+
+// z[idx[i]] = add + 1 / (z[idx[i]] - sub)   (idx device, may be NULL)
+PGCP_API int pgcp_inv_shift(double* z, const int32_t* idx, int64_t n, double add_re, double add_im, double sub_re,
+                            double sub_im, void* stream) {
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (n <= 0) return PGCP_OK;
+    k_inv_shift<<<grid_for(n, 256), 256, 0, s>>>(reinterpret_cast<double2*>(z), idx, n, make_double2(add_re, add_im),
+                                                 make_double2(sub_re, sub_im));
+    PGCP_LAUNCH_CHECK();
+    return PGCP_OK;
+}
+
+PGCP_API int pgcp_gather_complex(const double* src, const int32_t* idx, double* dst, int64_t n, void* stream) {
+    if (n <= 0) return PGCP_OK;
+    k_gather_c<<<grid_for(n, 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+        reinterpret_cast<const double2*>(src), idx, reinterpret_cast<double2*>(dst), n);
+    PGCP_LAUNCH_CHECK();
+    return PGCP_OK;
+}
+
+PGCP_API int pgcp_scatter_complex(const double* src, const int32_t* idx, double* dst, int64_t n, void* stream) {
+    if (n <= 0) return PGCP_OK;
+    k_scatter_c<<<grid_for(n, 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+        reinterpret_cast<const double2*>(src), idx, reinterpret_cast<double2*>(dst), n);
+    PGCP_LAUNCH_CHECK();
+    return PGCP_OK;
+}
+
+}  // extern "C"

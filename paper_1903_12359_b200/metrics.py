@@ -1,0 +1,141 @@
+"""Distortion measurement (drop-in for `metrics.py`), computed on the device
+(metrics.cu). The Mobius area post-optimisation (`metrics.py:183-270`) is out
+of scope."""
+
+import ctypes
+import json
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native as nat
+
+_VP, _I64, _D = ctypes.c_void_p, ctypes.c_int64, ctypes.c_double
+nat.register("pgcp_distortion", [_VP, _VP, _I64, _I64, _VP, ctypes.c_int, _VP, _VP, _VP, _VP, _I64, _VP])
+
+SUMMARY_COUNT = 16
+
+
+def _param_coords(param):
+    mode = getattr(param, "mode", None)
+    coords = getattr(param, "coords", param)
+    if mode is None:
+        arr = np.asarray(coords) if not isinstance(coords, torch.Tensor) else coords
+        mode = "sphere" if (arr.ndim == 2 and arr.shape[1] == 3) else "free"
+    return coords, mode
+
+
+class DeviceDistortion:
+    """Raw device outputs of pgcp_distortion."""
+
+    def __init__(self, V, F, coords, mode, hist=True):
+        from .device import device, ptr, stream_handle, to_dev
+        sphere = mode == "sphere"
+        Vd = to_dev(V, torch.float64)
+        Fd = to_dev(np.asarray(F, dtype=np.int32) if not isinstance(F, torch.Tensor) else F, torch.int32)
+        if isinstance(coords, torch.Tensor):
+            cd = coords.to(device()).contiguous()
+        else:
+            cd = to_dev(np.asarray(coords, dtype=np.float64 if sphere else np.complex128))
+        m = int(Fd.shape[0])
+        n = int(Vd.shape[0])
+        self.d = torch.empty(3 * m, dtype=torch.float64, device=device())
+        self.valid = torch.empty(3 * m, dtype=torch.uint8, device=device())
+        self.summary = np.zeros(SUMMARY_COUNT)
+        cap = 0
+        h = None
+        if hist:
+            cap = 1 << 20
+            h = np.zeros(cap, dtype=np.uint64)
+        nat.check(nat.lib().pgcp_distortion(ptr(Vd), ptr(Fd), n, m, ptr(cd), int(sphere), ptr(self.d),
+                                            ptr(self.valid), self.summary.ctypes.data,
+                                            h.ctypes.data if h is not None else None, cap, stream_handle()))
+        nb = int(self.summary[11])
+        self.hist = h[:nb].tolist() if (h is not None and self.summary[12] > 0) else []
+
+    def stats(self, which):
+        o = 0 if which == "angular" else 4
+        s = self.summary
+        return {"mean": float(s[o]), "sd": float(s[o + 1]), "median": float(s[o + 2]), "iqr": float(s[o + 3])}
+
+
+def angular_distortion(mesh, param):
+    """Per-corner (param - original) angle in degrees + validity mask
+    (metrics.py:61-75)."""
+    coords, mode = _param_coords(param)
+    dd = DeviceDistortion(mesh.vertices, mesh.faces, coords, mode, hist=False)
+    return dd.d.cpu().numpy(), dd.valid.cpu().numpy().astype(bool)
+
+
+def area_distortion(mesh, param):
+    """Per-face log of the normalised area ratio (metrics.py:89-104). Host
+    form of the API helper; the report uses the device summary."""
+    coords, mode = _param_coords(param)
+    coords = coords.cpu().numpy() if isinstance(coords, torch.Tensor) else np.asarray(coords)
+    F = np.asarray(mesh.faces)
+    if mode == "sphere":
+        p = coords[F]
+        a_new = 0.5 * np.linalg.norm(np.cross(p[:, 1] - p[:, 0], p[:, 2] - p[:, 0]), axis=1)
+    else:
+        z = np.asarray(coords, dtype=np.complex128)[F]
+        d1, d2 = z[:, 1] - z[:, 0], z[:, 2] - z[:, 0]
+        a_new = 0.5 * np.abs(d1.real * d2.imag - d1.imag * d2.real)
+    a_ref = mesh.face_areas()
+    valid = a_new > 0
+    d = np.zeros(len(a_ref))
+    d[valid] = np.log((a_new / a_new.sum())[valid] / (a_ref / a_ref.sum())[valid])
+    return d, valid
+
+
+def summarize(values):
+    """Mean, population sd, median, IQR with linear interpolation
+    (metrics.py:114-126)."""
+    v = np.asarray(values, dtype=np.float64)
+    if v.size == 0:
+        raise ValueError("cannot summarize an empty array")
+    q25, q50, q75 = np.percentile(v, [25, 50, 75])
+    return {"mean": float(np.mean(v)), "sd": float(np.std(v)), "median": float(q50), "iqr": float(q75 - q25)}
+
+
+@dataclass
+class DistortionReport:
+    angular: object
+    area: object
+    angular_stats: dict
+    area_stats: dict
+    excluded_corners: int
+    excluded_faces: int
+    conformal_energy: float = None
+    extra: dict = field(default_factory=dict)
+    histogram: list = None
+
+    def to_dict(self, histogram_bin=0.1):
+        return {
+            "angular_abs": self.angular_stats,
+            "area_abs": self.area_stats,
+            "angular_histogram": {"bin_width": histogram_bin, "start": 0.0,
+                                  "counts": list(self.histogram or [])},
+            "excluded_corners": self.excluded_corners,
+            "excluded_faces": self.excluded_faces,
+            "conformal_energy": self.conformal_energy,
+            **self.extra,
+        }
+
+    def to_json(self, path):
+        with open(path, "w", encoding="utf-8") as fh:
+            json.dump(self.to_dict(), fh, indent=2)
+
+
+def distortion_report(mesh, param, energy=None, V=None, F=None):
+    """Device distortion report (metrics.py:165-176). The per-corner values
+    stay on the device (`report.angular` is a CUDA tensor of the valid |d|
+    entries' source array and mask)."""
+    coords, mode = _param_coords(param)
+    Vs = V if V is not None else mesh.vertices
+    Fs = F if F is not None else mesh.faces
+    dd = DeviceDistortion(Vs, Fs, coords, mode, hist=True)
+    s = dd.summary
+    return DistortionReport(angular=dd.d, area=None, angular_stats=dd.stats("angular"),
+                            area_stats=dd.stats("area"), excluded_corners=int(s[8]),
+                            excluded_faces=int(s[9]), conformal_energy=energy, histogram=dd.hist)

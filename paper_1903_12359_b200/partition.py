@@ -149,8 +149,7 @@ def partition_mesh(mesh, cuts):
     if bad >= 0:
         chi, loops = info[9], info[10]
         cls = "sphere_type" if (chi == 2 and loops == 0) else "unsupported"
-        raise PartitionError(f"component {bad} is {cls} (chi={chi}, {loops if loops != -2 else '>=2'} loops); "
-                             "adjust the cut set")
+        raise PartitionError(f"component {bad} is {cls} (chi={chi}, {loops} loops); adjust the cut set")
     return Partition(mesh, batch, norm)
 
 

@@ -1,0 +1,448 @@
+"""End-to-end PGCP on the device (drop-in for `pipeline.py`).
+
+parameterize (pipeline.py:119-271) keeps every array on the GPU:
+  partition   topology.cu          one DeviceBatch: components, vertex maps, loops
+  plan        planner.cpp          host, integer-exact (boundary cycles only)
+  flatten     laplace.cu + pcg.cu  K1/K2 + batched cluster PCG over all submeshes
+  weld        weld.cu              tracked boundary values, schedule levels
+  boundary    weld.cu              disk: geodesic map; sphere: exterior inversion
+  harmonic    pcg.cu               batched cluster PCG with the welded boundary
+  stitch      metrics.cu           seam averaging, sphere finish, flips
+  metrics     metrics.cu           energy, angular/area distortion report
+Host work is bookkeeping over boundary-cycle ids (the weld write-back lists)
+and the final device -> host copy of the coordinates.
+"""
+
+import json
+import os
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .assemble import GlobalParam
+from .errors import PartitionError, SolveError, ValidationError, WeldError
+from .mesh import TriMesh, load_obj, validate_topology, write_obj_with_param
+from .partition import Partition, plan_weld_schedule, read_cut_edges, validate_cuts
+from .welding import (ARC_FROM_B, CYC_A, CYC_B, SIDE_B, _from_native, run_schedule)
+
+
+@dataclass
+class RunConfig:
+    input: str = None
+    cuts: str = None
+    mode: str = "free"             # free | disk | sphere
+    workers: int = 1
+    out: str = None
+    report: str = None
+    mobius_area: bool = False
+    seed: int = 0
+    snap_tol: float = 1e-8
+    hard_tol: float = 1e-6
+    beltrami_threshold: float = 0.99
+    repair_iters: int = 5
+    # B200 additions (named options; defaults keep the reference behaviour)
+    schedule: str = "greedy"       # greedy (reference planner) | pairs (explicit merge order)
+    pairs: list = None
+    rtol: float = 1e-10            # PCG recurrence tolerance
+    cluster: int = 0               # CTAs per subdomain (0 = auto)
+
+    def validate(self):
+        if self.mode not in ("free", "disk", "sphere"):
+            raise ValidationError(f"unknown mode {self.mode!r}")
+        if self.workers < 1:
+            raise ValidationError("worker count must be >= 1")
+        if self.schedule not in ("greedy", "pairs"):
+            raise ValidationError(f"unknown schedule {self.schedule!r}")
+
+
+@dataclass
+class RunReport:
+    mode: str = ""
+    n_vertices: int = 0
+    n_faces: int = 0
+    n_submeshes: int = 0
+    submesh_sizes: list = field(default_factory=list)
+    timings: dict = field(default_factory=dict)
+    seam_residuals: list = field(default_factory=list)
+    repairs: list = field(default_factory=list)
+    flips: int = 0
+    distortion: dict = field(default_factory=dict)
+    ok: bool = False
+    mobius_info: dict = None
+    bench: dict = None
+    solver: dict = None
+
+    def to_dict(self):
+        return {k: v for k, v in self.__dict__.items() if v is not None}
+
+    def to_json(self, path):
+        with open(path, "w", encoding="utf-8") as fh:
+            json.dump(self.to_dict(), fh, indent=2)
+
+
+class _Clock:
+    """Stage timer: host wall time around device work, synchronised."""
+
+    def __init__(self, timings, sync=True):
+        self.t = timings
+        self.sync = sync
+        self.t0 = None
+
+    def start(self):
+        if self.sync:
+            torch.cuda.synchronize()
+        self.t0 = time.perf_counter()
+
+    def stop(self, name):
+        if self.sync:
+            torch.cuda.synchronize()
+        self.t[name] = self.t.get(name, 0.0) + time.perf_counter() - self.t0
+
+
+def _ptr(t):
+    from .device import ptr
+    return ptr(t)
+
+
+def _stream():
+    from .device import stream_handle
+    return stream_handle()
+
+
+class WeldPlan:
+    """Host bookkeeping of a weld schedule over the tracked boundary slots.
+
+    Slot s is one entry of one submesh's boundary loop (submesh order, loop
+    order), i.e. the (component, parent id) value the reference keeps in its
+    per-component dicts (pipeline.py:174-204). For every step the plan lists
+    the slots of a_cycle / b_cycle (phase-1 inputs) and the write-back code of
+    every slot of the two components."""
+
+    def __init__(self, cycles, steps, n_parent):
+        K = len(cycles)
+        nb = np.array([len(c) for c in cycles], dtype=np.int64)
+        self.loop_off = np.zeros(K + 1, dtype=np.int64)
+        self.loop_off[1:] = np.cumsum(nb)
+        self.slot_parent = np.concatenate(cycles).astype(np.int64) if K else np.zeros(0, np.int64)
+        self.slot_sub = np.repeat(np.arange(K), nb)
+        members = {i: [i] for i in range(K)}
+        table = np.full(n_parent, -1, dtype=np.int64)
+        arcpos = np.zeros(n_parent, dtype=np.int64)
+        cyc = np.zeros(n_parent, dtype=np.int64)
+        info, src, wb, wb_off = [], [], [], [0]
+        self.exterior = []
+        for st in steps:
+            A = members[st.comp_a]
+            B = members[st.comp_b]
+            sa = np.concatenate([np.arange(self.loop_off[i], self.loop_off[i + 1]) for i in A])
+            sb = np.concatenate([np.arange(self.loop_off[i], self.loop_off[i + 1]) for i in B])
+            table[self.slot_parent[sa]] = sa
+            a_src = table[st.a_cycle]
+            table[self.slot_parent[sa]] = -1
+            table[self.slot_parent[sb]] = sb
+            b_src = table[st.b_cycle]
+            table[self.slot_parent[sb]] = -1
+            if (a_src < 0).any() or (b_src < 0).any():
+                raise WeldError("weld step references a boundary vertex outside its components")
+            k = int(st.k)
+            arcpos[st.a_cycle[:k + 1]] = np.arange(1, k + 2)
+            cyc[st.a_cycle] |= CYC_A
+            cyc[st.b_cycle] |= CYC_B
+            pa, pb = self.slot_parent[sa], self.slot_parent[sb]
+            ca = arcpos[pa] | cyc[pa]
+            cb = (arcpos[pb] | cyc[pb]) | SIDE_B
+            arcpos[st.a_cycle[:k + 1]] = 0
+            cyc[st.a_cycle] = 0
+            cyc[st.b_cycle] = 0
+            wb.append(np.stack([sa, ca], 1))
+            wb.append(np.stack([sb, cb], 1))
+            wb_off.append(wb_off[-1] + len(sa) + len(sb))
+            src.append(a_src)
+            src.append(b_src)
+            info.append([k, int(st.closed), len(st.a_cycle), len(st.b_cycle), st.comp_a, st.comp_b])
+            if st.closed:
+                self.exterior_candidates = (list(A), list(B))
+            members[st.comp_a] = A + B
+            del members[st.comp_b]
+        self.info = np.array(info, dtype=np.int32).reshape(-1, 6)
+        self.src = np.concatenate(src).astype(np.int32) if src else np.zeros(0, np.int32)
+        self.wb = (np.concatenate(wb).astype(np.int64) & 0xffffffff).astype(np.uint32).view(np.int32) \
+            if wb else np.zeros((0, 2), np.int32)
+        self.wb = self.wb.reshape(-1, 2)
+        self.wb_off = np.array(wb_off, dtype=np.int64)
+        self.n_parent = n_parent
+
+    def slots_of(self, subs):
+        return np.concatenate([np.arange(self.loop_off[i], self.loop_off[i + 1]) for i in subs]) \
+            if len(subs) else np.zeros(0, np.int64)
+
+    def any_slot_of_parents(self, parents):
+        table = np.full(self.n_parent, -1, dtype=np.int64)
+        table[self.slot_parent] = np.arange(len(self.slot_parent))
+        return table[np.asarray(parents, dtype=np.int64)]
+
+
+def _poly_area(z):
+    return 0.5 * float(np.sum(z.real * np.roll(z, -1).imag - z.imag * np.roll(z, -1).real))
+
+
+def parameterize(mesh, cuts=None, mode="free", workers=1, seed=0, mobius_area=False, config=None,
+                 schedule=None, pairs=None, solve_comps=None):
+    """Global conformal parameterization (pipeline.py:119-271) on the device.
+
+    Same signature and results as the reference; `schedule`/`pairs` select
+    the documented balanced weld order (config.schedule="pairs")."""
+    from .device import DeviceBatch, device, require_cuda
+    require_cuda()
+    cfg = config or RunConfig(mode=mode, workers=workers, seed=seed, mobius_area=mobius_area)
+    if schedule is not None:
+        cfg.schedule = schedule
+    if pairs is not None:
+        cfg.pairs = pairs
+        cfg.schedule = "pairs"
+    cfg.validate()
+    mode = cfg.mode
+    report = RunReport(mode=mode, n_vertices=mesh.n_vertices, n_faces=mesh.n_faces)
+    timings = report.timings
+    clk = _Clock(timings)
+    dev = device()
+
+    # ---- partition (+ parent topology) ----------------------------------------
+    clk.start()
+    V, F = mesh.device_arrays()
+    have_cuts = cuts is not None and len(cuts) > 0
+    if have_cuts:
+        norm = validate_cuts(mesh, cuts)
+        batch = DeviceBatch(V, F, cuts=norm)
+    else:
+        norm = np.zeros((0, 2), np.int64)
+        batch = mesh.batch()
+    info = batch.info()
+    chi, nl = info[nat.INFO_PARENT_CHI], info[nat.INFO_PARENT_LOOPS]
+    cls = "disk_type" if (chi == 1 and nl == 1) else ("sphere_type" if (chi == 2 and nl == 0) else "unsupported")
+    if mode in ("free", "disk") and cls != "disk_type":
+        raise ValidationError(f"mode {mode!r} needs a disk-type mesh, got {cls}")
+    if mode == "sphere" and cls != "sphere_type":
+        raise ValidationError(f"sphere mode needs a genus-0 closed mesh, got {cls}")
+    if not have_cuts and mode == "sphere":
+        raise ValidationError("sphere mode requires a cut set (K >= 2)")
+    if have_cuts and info[nat.INFO_BAD_COMP] >= 0:
+        c_chi, c_loops = info[9], info[10]
+        ccls = "sphere_type" if (c_chi == 2 and c_loops == 0) else "unsupported"
+        raise PartitionError(f"component {info[nat.INFO_BAD_COMP]} is {ccls} (chi={c_chi}, {c_loops} loops); "
+                             "adjust the cut set")
+    part = Partition(mesh, batch, norm)
+    K = info[nat.INFO_K]
+    if have_cuts:
+        steps = plan_weld_schedule(part, mode, pairs=cfg.pairs if cfg.schedule == "pairs" else None)
+    else:
+        steps = []
+    clk.stop("partition")
+    report.n_submeshes = K
+    voff = batch.host(nat.ARR_VERT_OFF, torch.int64)
+    report.submesh_sizes = [int(x) for x in np.diff(voff)]
+
+    # ---- local free-boundary flattening (all submeshes, one launch) -----------
+    clk.start()
+    z0, fst = batch.flatten(rtol=cfg.rtol, cluster=cfg.cluster)
+    clk.stop("flatten")
+    report.solver = {"flatten_iters": [s["iters"] for s in fst]}
+
+    if K == 1 and mode == "free":
+        embeddings = z0
+    else:
+        # ---- welding on tracked boundary values ---------------------------------
+        clk.start()
+        cycles = part.boundary_cycles
+        plan = WeldPlan(cycles, steps, mesh.n_vertices)
+        loop_local = batch.host(nat.ARR_LOOP, torch.int32).astype(np.int64)
+        loop_gid = torch.as_tensor((voff[plan.slot_sub] + loop_local).astype(np.int32)).to(dev)
+        tv = torch.empty(len(plan.slot_parent), dtype=torch.complex128, device=dev)
+        nat.check(nat.lib().pgcp_gather_complex(_ptr(z0), _ptr(loop_gid), _ptr(tv), tv.numel(), _stream()))
+        out = None
+        if len(steps):
+            out, _ = run_schedule(tv, plan.info, plan.src, plan.wb_off, plan.wb, cfg.hard_tol)
+            report.seam_residuals = [float(x) for x in out[:, 1]]
+        exterior = []
+        if len(steps) and steps[-1].closed:
+            A, B = plan.exterior_candidates
+            exterior = B if out[-1, 2] > 0 else A
+        clk.stop("weld")
+
+        if mode == "disk":
+            clk.start()
+            gc = steps[-1].merged_cycle if steps else cycles[0]
+            _geodesic_boundary(plan, tv, gc)
+            clk.stop("boundary_map")
+
+        # ---- harmonic reconstruction with the welded boundary --------------------
+        clk.start()
+        center = None
+        if mode == "sphere" and exterior:
+            seam_slots = plan.any_slot_of_parents(steps[-1].a_cycle).astype(np.int32)
+            c = np.zeros(2)
+            rev = int(out[-1, 2] < 0)
+            nat.check(nat.lib().pgcp_polygon_interior(_ptr(tv), seam_slots.ctypes.data, len(seam_slots), rev,
+                                                      c.ctypes.data, _stream()))
+            center = complex(c[0], c[1])
+            ext_slots = torch.as_tensor(plan.slots_of(exterior).astype(np.int32)).to(dev)
+            nat.check(nat.lib().pgcp_inv_shift(_ptr(tv), _ptr(ext_slots), ext_slots.numel(), 0.0, 0.0,
+                                               center.real, center.imag, _stream()))
+        z, hst = batch.harmonic(loop_gid, tv, rtol=cfg.rtol, cluster=cfg.cluster)
+        report.solver["harmonic_iters"] = [s["iters"] for s in hst]
+        if center is not None:
+            gids = np.concatenate([np.arange(voff[i], voff[i + 1]) for i in exterior]).astype(np.int32)
+            gt = torch.as_tensor(gids).to(dev)
+            nat.check(nat.lib().pgcp_inv_shift(_ptr(z), _ptr(gt), gt.numel(), center.real, center.imag, 0.0, 0.0,
+                                               _stream()))
+        embeddings = z
+        clk.stop("harmonic")
+
+    # ---- stitch ---------------------------------------------------------------
+    clk.start()
+    gp, flip = _stitch(batch, embeddings, mode, cfg, mesh)
+    clk.stop("stitch")
+    if not (K == 1 and mode == "free"):
+        fc = batch.array(nat.ARR_FACE_COMP, torch.int32)
+        per = torch.bincount(fc.long()[flip.bool()], minlength=K).cpu().numpy() if gp.flipped_faces.size else \
+            np.zeros(K, dtype=np.int64)
+        report.repairs = [{"flips_before": int(per[i]), "repair_iterations": 0, "cleared": bool(per[i] == 0),
+                           "submesh": i} for i in range(K)]
+    return _finish(mesh, batch, embeddings, gp, report, cfg, clk)
+
+
+def _geodesic_boundary(plan, tv, gc):
+    """Disk mode (pipeline.py:216-235): map the global boundary onto the unit
+    circle and push every other tracked point through the same log."""
+    from .device import device
+    dev = device()
+    src = plan.any_slot_of_parents(gc).astype(np.int32)
+    n = len(src)
+    circ = torch.empty(n, dtype=torch.complex128, device=dev)
+    cap = n + 8
+    recs = (nat.Rec * cap)()
+    meta = np.zeros(8)
+    nat.check(nat.lib().pgcp_weld_geodesic(_ptr(tv), src.ctypes.data, n, None, _ptr(circ), recs, cap,
+                                           meta.ctypes.data, _stream()))
+    nrec = int(meta[0])
+    # every slot whose parent is on the global cycle gets its circle value
+    pos = np.full(plan.n_parent, -1, dtype=np.int64)
+    pos[np.asarray(gc, dtype=np.int64)] = np.arange(n)
+    sp = pos[plan.slot_parent]
+    on = np.nonzero(sp >= 0)[0]
+    off = np.nonzero(sp < 0)[0]
+    if len(off):
+        idx = torch.as_tensor(off.astype(np.int32)).to(dev)
+        tmp = torch.empty(len(off), dtype=torch.complex128, device=dev)
+        nat.check(nat.lib().pgcp_gather_complex(_ptr(tv), _ptr(idx), _ptr(tmp), len(off), _stream()))
+        nat.check(nat.lib().pgcp_weld_replay(recs, nrec, _ptr(tmp), None, len(off), _stream()))
+        nat.check(nat.lib().pgcp_scatter_complex(_ptr(tmp), _ptr(idx), _ptr(tv), len(off), _stream()))
+    if len(on):
+        src_on = torch.as_tensor(sp[on].astype(np.int32)).to(dev)
+        dst_on = torch.as_tensor(on.astype(np.int32)).to(dev)
+        tmp = torch.empty(len(on), dtype=torch.complex128, device=dev)
+        nat.check(nat.lib().pgcp_gather_complex(_ptr(circ), _ptr(src_on), _ptr(tmp), len(on), _stream()))
+        nat.check(nat.lib().pgcp_scatter_complex(_ptr(tmp), _ptr(dst_on), _ptr(tv), len(on), _stream()))
+
+
+def _stitch(batch, z, mode, cfg, mesh):
+    from .device import device
+    dev = device()
+    n, m = batch.n, batch.m
+    coords = torch.empty(n, dtype=torch.complex128, device=dev)
+    sphere = torch.empty((n, 3), dtype=torch.float64, device=dev) if mode == "sphere" else None
+    prov = torch.empty(n, dtype=torch.int32, device=dev)
+    flip = torch.empty(m, dtype=torch.uint8, device=dev)
+    stats = np.zeros(8)
+    mcode = {"free": 0, "disk": 1, "sphere": 2}[mode]
+    st = nat.lib().pgcp_batch_stitch(batch.h, _ptr(z), mcode, cfg.hard_tol, 1e-9, _ptr(coords),
+                                     _ptr(sphere) if sphere is not None else None, _ptr(prov), _ptr(flip),
+                                     stats.ctypes.data, _stream())
+    nat.check(st)
+    nflip = int(stats[3])
+    flipped = np.nonzero(flip.cpu().numpy())[0] if nflip else np.zeros(0, dtype=np.int64)
+    diag = {"seam_max_dev": float(stats[0]), "scale": float(stats[1])}
+    if mode == "disk":
+        diag["boundary_circle_dev"] = float(stats[2])
+    out = sphere if mode == "sphere" else coords
+    gp = GlobalParam(mode, out, flipped, prov, float(stats[0]), diag)
+    gp._device = True
+    return gp, flip
+
+
+def _finish(mesh, batch, embeddings, gp, report, cfg, clk):
+    """Energy, distortion report, acceptance flags (pipeline.py:274-297)."""
+    from .metrics import distortion_report
+    clk.start()
+    energy = None
+    if gp.mode in ("free", "disk"):
+        energy = float(batch.energy(embeddings).sum())
+    V, F = mesh.device_arrays()
+    dist = distortion_report(mesh, gp, energy=energy, V=V, F=F)
+    clk.stop("metrics")
+    if cfg.mobius_area:
+        report.mobius_info = {"pre": None, "post": None, "improved": False,
+                              "note": "Mobius area optimisation is out of scope on this path"}
+    report.flips = int(len(gp.flipped_faces))
+    report.distortion = dist.to_dict()
+    seam_ok = all(r <= cfg.snap_tol for r in report.seam_residuals)
+    report.ok = report.flips == 0 and seam_ok
+    # hand back host arrays, as the reference's GlobalParam holds numpy
+    clk.start()
+    gp.coords = gp.coords.cpu().numpy()
+    gp.provenance = gp.provenance.cpu().numpy().astype(np.int64)
+    clk.stop("d2h")
+    return gp, report
+
+
+def run_pipeline(config):
+    config.validate()
+    if not config.input:
+        raise ValidationError("missing input mesh path")
+    mesh = load_obj(config.input)
+    cuts = read_cut_edges(config.cuts) if config.cuts else None
+    gp, report = parameterize(mesh, cuts=cuts, config=config)
+    if config.out:
+        coords = gp.coords if gp.mode == "sphere" else gp.uv
+        write_obj_with_param(config.out, mesh, coords)
+    if config.report:
+        report.to_json(config.report)
+    return gp, report
+
+
+def benchmark_subdomains(mesh, n_values, mode="free", repeats=3, workers=None, cut_files=None, seed=0):
+    """T_n, S_n = T_2/T_n, E_n = S_n/(n/2) over subdomain counts
+    (pipeline.py:320-361); strip cuts by face-centroid quantiles."""
+    from .generators import cuts_from_face_labels
+    n_values = sorted(set(int(n) for n in n_values))
+    if any(n < 2 for n in n_values):
+        raise ValidationError("subdomain counts must be >= 2")
+    if 2 not in n_values:
+        n_values = [2] + n_values
+    T = {}
+    for idx, n in enumerate(n_values):
+        if cut_files:
+            cuts = read_cut_edges(cut_files[idx])
+        else:
+            cent = mesh.vertices[mesh.faces].mean(axis=1)[:, 0]
+            qs = np.quantile(cent, np.linspace(0, 1, n + 1)[1:-1])
+            cuts = cuts_from_face_labels(mesh.faces, np.searchsorted(qs, cent, side="right"))
+        times = []
+        for _ in range(repeats):
+            t0 = time.perf_counter()
+            gp, rep = parameterize(mesh, cuts=cuts, mode=mode, seed=seed)
+            times.append(time.perf_counter() - t0)
+            if not rep.ok:
+                raise SolveError(f"benchmark run with n={n} subdomains failed acceptance (flips={rep.flips})")
+        T[n] = float(np.median(times))
+    bench = {"n": n_values, "T_n": {str(n): T[n] for n in n_values},
+             "S_n": {str(n): T[2] / T[n] for n in n_values},
+             "E_n": {str(n): (T[2] / T[n]) / (n / 2.0) for n in n_values}, "repeats": repeats}
+    out = RunReport(mode=mode, n_vertices=mesh.n_vertices, n_faces=mesh.n_faces)
+    out.bench = bench
+    out.ok = True
+    out.timings = {f"T_{n}": T[n] for n in n_values}
+    return out

@@ -1,0 +1,49 @@
+import os
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+PIPELINE_CASES = ["cfg1", "strips4", "blocks3x3", "disk2x2", "k1free", "k1disk", "flat2x2",
+                  "sphere2", "sphere4", "tree4x4"]
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (run on the B200 box)")
+    config.addinivalue_line("markers", "slow: larger sizes")
+
+
+def load_golden(name):
+    return np.load(os.path.join(GOLDEN, f"{name}.npz"), allow_pickle=False)
+
+
+def unpack(z, name):
+    off = z[name + "_off"]
+    d = z[name]
+    return [d[off[i]:off[i + 1]] for i in range(len(off) - 1)]
+
+
+def unpack_csr(z, name, values=True):
+    from scipy import sparse
+    ip = unpack(z, name + "_indptr")
+    ix = unpack(z, name + "_indices")
+    dv = unpack(z, name + "_data") if values else [np.zeros(len(a)) for a in ix]
+    out = []
+    for a, b, c in zip(ip, ix, dv):
+        n = len(a) - 1
+        out.append(sparse.csr_matrix((c, b, a), shape=(n, n)))
+    return out
+
+
+@pytest.fixture(scope="session")
+def cuda():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1903_12359_b200  # noqa: F401
+    return torch.device("cuda", 0)

@@ -1,0 +1,127 @@
+"""GPU parity of the weld engine and of the end-to-end device pipeline
+against the reference goldens (UV within 1e-6 of the parameter-domain
+diameter, 0 flips, angle-distortion mean/sd within 1e-3 degrees, exact
+median/IQR agreement to rounding)."""
+
+import json
+
+import numpy as np
+import pytest
+
+from conftest import load_golden, unpack
+
+pytestmark = pytest.mark.gpu
+
+CASES = ["cfg1", "strips4", "blocks3x3", "disk2x2", "k1free", "k1disk", "flat2x2", "sphere2", "sphere4",
+         "tree4x4"]
+
+
+def _diam(z):
+    z = np.asarray(z)
+    if z.ndim == 2:  # sphere: chordal diameter 2
+        return 2.0
+    zz = z[np.isfinite(z)]
+    c = zz.mean()
+    return 2 * np.max(np.abs(zz - c))
+
+
+@pytest.mark.parametrize("case", ["cfg1", "blocks3x3", "sphere4", "disk2x2", "tree4x4"])
+def test_welds_match_reference(cuda, case):
+    from paper_1903_12359_b200 import closed_weld, partial_weld
+    z = load_golden(case)
+    ins_a, ins_b = unpack(z, "weld_in_a"), unpack(z, "weld_in_b")
+    outs_a, outs_b = unpack(z, "weld_out_a"), unpack(z, "weld_out_b")
+    for a, b, k, cl, oa, ob, seam in zip(ins_a, ins_b, z["weld_k"], z["weld_closed"], outs_a, outs_b,
+                                         z["weld_seam"]):
+        r = closed_weld(a, b) if cl else partial_weld(a, b, int(k))
+        sc = max(np.max(np.abs(oa)), np.max(np.abs(ob)))
+        assert np.max(np.abs(r.a - oa)) <= 1e-9 * sc
+        assert np.max(np.abs(r.b - ob)) <= 1e-9 * sc
+        assert abs(r.seam_error - seam) <= 1e-9 * sc
+
+
+def test_weld_corpus(cuda):
+    from paper_1903_12359_b200 import apply_log, partial_weld
+    z = load_golden("weld_corpus")
+    for a, b, k, oa, ob in zip(unpack(z, "a"), unpack(z, "b"), z["k"], unpack(z, "oa"), unpack(z, "ob")):
+        r = partial_weld(a, b, int(k))
+        sc = max(np.max(np.abs(oa)), np.max(np.abs(ob)))
+        assert np.max(np.abs(r.a - oa)) <= 1e-9 * sc
+        assert np.max(np.abs(r.b - ob)) <= 1e-9 * sc
+        # SPEC acceptance 1: shared samples coincide
+        assert np.max(np.abs(r.a[:k + 1] - r.b[:k + 1])) <= 1e-8 * sc
+        ra, _ = apply_log(r.log_a, a)
+        assert np.max(np.abs(ra - r.a)) <= 1e-9 * sc
+
+
+def test_geodesic_matches_reference(cuda):
+    from paper_1903_12359_b200 import geodesic_to_circle
+    for case in ["disk2x2", "k1disk"]:
+        z = load_golden(case)
+        circ, log = geodesic_to_circle(z["geo_in"])
+        assert np.max(np.abs(circ - z["geo_out"])) <= 1e-9
+        assert np.max(np.abs(np.abs(circ) - 1)) <= 1e-9
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_pipeline_matches_reference(cuda, case):
+    from paper_1903_12359_b200 import TriMesh, parameterize
+    from paper_1903_12359_b200.generators import row_tree_schedule_order
+    z = load_golden(case)
+    mesh = TriMesh(z["V"], z["F"])
+    cuts = z["cuts"] if len(z["cuts"]) else None
+    kw = {}
+    if case == "tree4x4":
+        kw["pairs"] = row_tree_schedule_order(4, 4)
+    gp, rep = parameterize(mesh, cuts, str(z["mode"]), **kw)
+    ref = z["coords"]
+    got = np.asarray(gp.coords)
+    assert got.shape == ref.shape
+    assert np.max(np.abs(got - ref)) <= 1e-6 * _diam(ref), case
+    assert rep.flips == int(z["flips"]) == 0
+    rd = json.loads(str(z["distortion_json"]))
+    for key in ("mean", "sd", "median", "iqr"):
+        assert abs(rep.distortion["angular_abs"][key] - rd["angular_abs"][key]) <= 1e-3
+    assert rep.distortion["excluded_corners"] == rd["excluded_corners"]
+    assert rep.ok == bool(z["ok"])
+    if rd["conformal_energy"] is not None:
+        assert abs(rep.distortion["conformal_energy"] - rd["conformal_energy"]) <= 1e-6 * max(
+            1.0, abs(rd["conformal_energy"]))
+    assert len(rep.seam_residuals) == len(z["seam_residuals"])
+
+
+def test_pipeline_determinism(cuda):
+    from paper_1903_12359_b200 import TriMesh, parameterize
+    z = load_golden("blocks3x3")
+    mesh = TriMesh(z["V"], z["F"])
+    g1, _ = parameterize(mesh, z["cuts"], "free")
+    g2, _ = parameterize(mesh, z["cuts"], "free")
+    assert np.array_equal(g1.coords, g2.coords)
+
+
+def test_distortion_report_exact_order_stats(cuda):
+    """median / IQR from the device radix select equal numpy's percentile
+    on the same |d| values."""
+    from paper_1903_12359_b200 import TriMesh
+    from paper_1903_12359_b200.metrics import DeviceDistortion
+    z = load_golden("cfg1")
+    mesh = TriMesh(z["V"], z["F"])
+    dd = DeviceDistortion(z["V"], z["F"], z["coords"], "free")
+    d = dd.d.cpu().numpy()
+    v = dd.valid.cpu().numpy().astype(bool)
+    a = np.abs(d[v])
+    q25, q50, q75 = np.percentile(a, [25, 50, 75])
+    assert dd.stats("angular")["median"] == q50
+    assert dd.stats("angular")["iqr"] == q75 - q25
+    rd = json.loads(str(z["distortion_json"]))
+    assert abs(dd.stats("angular")["mean"] - rd["angular_abs"]["mean"]) < 1e-12
+    assert dd.hist == rd["angular_histogram"]["counts"]
+
+
+def test_weld_error_propagates(cuda):
+    from paper_1903_12359_b200 import WeldError, partial_weld
+    a = np.array([0, 1, 1 + 1j, 1j], dtype=complex)
+    with pytest.raises(WeldError, match="zip points 0 and 1 coincide"):
+        partial_weld(np.array([0, 0, 1 + 1j, 1j]), a, 2)
+    with pytest.raises(WeldError, match="out of range"):
+        partial_weld(a, a, 7)

@@ -1,0 +1,115 @@
+"""CPU tests: the C-ABI library loads and exports every declared symbol,
+the native planner matches the reference schedules, generators match the
+SURVEY fingerprints."""
+
+import ctypes
+import hashlib
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, load_golden, unpack
+
+import oracle
+from paper_1903_12359_b200 import generators as gen
+
+HEADER = os.path.join(ROOT, "include", "pgcp_b200.h")
+
+
+def _declared():
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"PGCP_API\s+(?:int|const char\*)\s+(pgcp_\w+)\s*\(", txt)))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_1903_12359_b200 import _native, build
+    build.build()
+    lib = ctypes.CDLL(_native.LIB_PATH)
+    names = _declared()
+    assert len(names) >= 10
+    missing = [n for n in names if not hasattr(lib, n)]
+    assert not missing, missing
+    assert lib.pgcp_abi_version() == 1
+
+
+def test_product_never_imports_oracle():
+    pkg = os.path.join(ROOT, "paper_1903_12359_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith(".py"):
+                src = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in src and "from oracle" not in src, f
+
+
+def _part(case):
+    z = load_golden(case)
+
+    class P:
+        pass
+    p = P()
+    p.boundary_cycles = unpack(z, "cycles")
+    p.cuts = np.sort(z["cuts"], axis=1) if len(z["cuts"]) else np.zeros((0, 2), np.int64)
+    return z, p
+
+
+@pytest.mark.parametrize("case", ["cfg1", "strips4", "blocks3x3", "disk2x2", "flat2x2",
+                                  "sphere2", "sphere4", "tree4x4"])
+def test_native_planner_matches_reference(case):
+    from paper_1903_12359_b200.partition import plan_weld_schedule
+    z, p = _part(case)
+    pairs = gen.row_tree_schedule_order(4, 4) if case == "tree4x4" else None
+    steps = plan_weld_schedule(p, str(z["mode"]), pairs=pairs)
+    A, B, M = unpack(z, "step_a"), unpack(z, "step_b"), unpack(z, "step_merged")
+    assert len(steps) == len(A)
+    for s, a, b, m, meta in zip(steps, A, B, M, z["step_meta"]):
+        assert np.array_equal(s.a_cycle, a) and np.array_equal(s.b_cycle, b)
+        assert np.array_equal(s.merged_cycle, m)
+        assert [s.comp_a, s.comp_b, s.k, int(s.closed)] == list(meta)
+
+
+@pytest.mark.parametrize("n,k", [(65, 8), (129, 16)])
+def test_native_planner_matches_oracle_large(n, k):
+    from paper_1903_12359_b200.partition import plan_weld_schedule
+    V, F, c = gen.height_field_case(n, k)
+    sp = oracle.split_mesh(V, F, c)
+
+    class P:
+        pass
+    p = P()
+    p.boundary_cycles, p.cuts = sp.boundary_cycles, sp.cuts
+    steps = plan_weld_schedule(p)
+    ref = oracle.greedy_schedule(sp.boundary_cycles, sp.cuts)
+    assert len(steps) == len(ref) == k * k - 1
+    for s, o in zip(steps, ref):
+        assert (s.comp_a, s.comp_b, s.k) == (o.comp_a, o.comp_b, o.k)
+        assert np.array_equal(s.a_cycle, o.a_cycle) and np.array_equal(s.b_cycle, o.b_cycle)
+
+
+def test_planner_rejects_corner_only_contact():
+    from paper_1903_12359_b200.errors import PartitionError
+    from paper_1903_12359_b200.partition import plan_weld_schedule
+
+    class P:
+        pass
+    p = P()
+    p.boundary_cycles = [np.array([0, 1, 2]), np.array([2, 3, 4])]
+    p.cuts = np.zeros((0, 2), np.int64)
+    with pytest.raises(PartitionError):
+        plan_weld_schedule(p)
+
+
+def test_generator_fingerprints():
+    V, F, cuts = gen.cfg1(0)
+    h = lambda a: hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()[:16]
+    assert h(V) == "c09f242d3e13faad"
+    assert h(F) == "38e046bed638756d"
+    assert len(cuts) == 198 and h(cuts) == "86338b0a7b75d7bb"
+    assert V[:, 2].min() == -0.18727264361230875
+
+
+def test_row_tree_order_covers_blocks():
+    order = gen.row_tree_schedule_order(8, 8)
+    assert len(order) == 63
+    assert order[:2] == [(0, 1), (0, 2)] and order[-1] == (0, 32)
