@@ -51,6 +51,8 @@ typedef struct pgcp_batch pgcp_batch;
 
 PGCP_API int pgcp_abi_version(void);
 PGCP_API const char* pgcp_last_error(void);
+/* number of kernels this library has launched in the process */
+PGCP_API unsigned long long pgcp_launch_count(void);
 
 /* -------------------------------------------------------------------------
  * Batch of disk-type submeshes of one parent mesh, device resident.
@@ -155,6 +157,13 @@ PGCP_API int pgcp_batch_harmonic(pgcp_batch* b, const int32_t* comps, int32_t nc
                         const int32_t* fixed_gid, const double* fixed_val, int64_t nfixed,
                         const pgcp_solve_opts* opts, double* z,
                         pgcp_solve_stat* stats, void* stream);
+
+/* Summary of the last flatten (0) / harmonic (1) solve: out[0] PCG kernel
+ * time in ms (CUDA events on the launch stream), [1] total iterations,
+ * [2] max iterations, [3] sum over submeshes of iterations x compulsory bytes
+ * per iteration (12 B per stored off-diagonal entry + 48 B per row), [4]
+ * stored entries, [5] unknown rows, [6] CTAs per cluster, [7] submeshes. */
+PGCP_API int pgcp_batch_last_solve(const pgcp_batch* b, int which, double* out, int nout);
 
 /* Exported solver systems for pattern parity (flatten.py:160-166 C_ff and
  * assemble.py:40 L_II), one submesh, CSR with int32 indptr/indices as scipy

@@ -66,6 +66,9 @@ _SIGS = {
                              ctypes.POINTER(SolveStat), _VP], ctypes.c_int),
     "pgcp_batch_export_system": ([_VP, ctypes.c_int, _I32, _PI64, _VP, _VP, _VP, _VP, _VP], ctypes.c_int),
     "pgcp_batch_conformal_energy": ([_VP, _VP, _PD, _VP], ctypes.c_int),
+    "pgcp_batch_stitch": ([_VP, _VP, ctypes.c_int, _D, _D, _VP, _VP, _VP, _VP, _VP, _VP], ctypes.c_int),
+    "pgcp_batch_last_solve": ([_VP, ctypes.c_int, _PD, ctypes.c_int], ctypes.c_int),
+    "pgcp_launch_count": ([], ctypes.c_ulonglong),
 }
 
 _OPTIONAL = {}

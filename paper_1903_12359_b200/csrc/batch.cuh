@@ -61,6 +61,8 @@ int solve_harmonic(pgcp_batch* b, const int32_t* comps, int32_t ncomp, const int
                    const double* fixed_val, int64_t nfixed, const pgcp_solve_opts* o, double* z,
                    pgcp_solve_stat* st, cudaStream_t s);
 void free_system(void* p);
+void solve_summary(const pgcp_batch* b, int which, double* out8);
+unsigned long long launch_count();
 int export_system(pgcp_batch* b, int which, int32_t comp, int64_t* dims, int32_t* indptr,
                   int32_t* indices, double* data, double* rhs, cudaStream_t s);
 // metrics.cu

@@ -28,6 +28,19 @@ int pgcp_abi_version(void) { return PGCP_ABI_VERSION; }
 
 const char* pgcp_last_error(void) { return get_error(); }
 
+unsigned long long pgcp_launch_count(void) { return pgcp::launch_count(); }
+
+int pgcp_batch_last_solve(const pgcp_batch* b, int which, double* out, int nout) {
+    if (!b || !out || which < 0 || which > 1) {
+        set_error("pgcp_batch_last_solve: invalid arguments");
+        return PGCP_E_INVALID;
+    }
+    double v[8];
+    pgcp::solve_summary(b, which, v);
+    for (int i = 0; i < nout && i < 8; ++i) out[i] = v[i];
+    return PGCP_OK;
+}
+
 int pgcp_batch_create(const double* V, const int32_t* F, int64_t n, int64_t m, const int64_t* cuts, int64_t ncuts,
                       uint32_t flags, void* stream, pgcp_batch** out) {
     if (!out || !V || !F || n <= 0 || m <= 0 || ncuts < 0 || (ncuts > 0 && !cuts)) {

@@ -1,4 +1,6 @@
 // common.cu -- errors, device-wide scans, stable counting sort.
+#include <atomic>
+
 #include "common.cuh"
 
 namespace pgcp {
@@ -15,6 +17,10 @@ void set_error(const char* fmt, ...) {
 }
 
 const char* get_error() { return g_err.c_str(); }
+
+static std::atomic<unsigned long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+unsigned long long launch_count() { return g_launches.load(); }
 
 // ---------------------------------------------------------------------------
 // scans

@@ -43,7 +43,14 @@ struct Status {
         if (_s != PGCP_OK) return _s; \
     } while (0)
 
-#define PGCP_LAUNCH_CHECK() PGCP_TRY_CUDA(cudaGetLastError())
+// every kernel launch site is followed by PGCP_LAUNCH_CHECK(), which also
+// counts the launch (pgcp_launch_count, bench.py's gpu_launches)
+void count_launch();
+#define PGCP_LAUNCH_CHECK()          \
+    do {                             \
+        ::pgcp::count_launch();      \
+        PGCP_TRY_CUDA(cudaGetLastError()); \
+    } while (0)
 
 // Device-side error record: the first (lowest index) failure wins so that the
 // reported item is deterministic.

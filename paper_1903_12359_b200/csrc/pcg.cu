@@ -48,6 +48,9 @@ struct SolveSystem {
     std::vector<int64_t> h_sv_off;   // slot -> compact vertex offset (nslot+1)
     int64_t nslices = 0, rows = 0, nnz = 0, ne = 0;
     int csize = 1;
+    // last run: PCG kernel time (CUDA events on the launch stream), iteration
+    // totals and the compulsory bytes of one iteration
+    double kernel_ms = 0, iters_sum = 0, iters_max = 0, bytes_iter_weighted = 0, nnz_off = 0, nrows_u = 0;
     DevBuf<int32_t> d_comps, slot_of_comp;
     DevBuf<int64_t> sl_off, sv_off, sl_ptr;
     DevBuf<uint32_t> sl_mask;
@@ -788,7 +791,13 @@ int run_solve(pgcp_batch* b, SolveSystem* S, const pgcp_solve_opts* o, double* z
     A.tol2 = rtol * rtol;
     A.maxit = (o && o->maxit > 0) ? o->maxit : 200000;
     A.chunk_cap = chunk;
+    cudaEvent_t e0, e1;
+    PGCP_TRY_CUDA(cudaEventCreate(&e0));
+    PGCP_TRY_CUDA(cudaEventCreate(&e1));
+    PGCP_TRY_CUDA(cudaEventRecord(e0, s));
     PGCP_TRY(launch_pcg(S, A, csize, s));
+    count_launch();
+    PGCP_TRY_CUDA(cudaEventRecord(e1, s));
     k_true_residual<<<nslot, 512, 0, s>>>(A);
     PGCP_LAUNCH_CHECK();
     k_scatter<<<grid_for(S->ne, 256), 256, 0, s>>>(S->ne, nslot, S->d_comps.p, S->sv_off.p, b->vert_off.p, S->urow.p,
@@ -801,9 +810,32 @@ int run_solve(pgcp_batch* b, SolveSystem* S, const pgcp_solve_opts* o, double* z
     }
     std::vector<int32_t> hit(nslot);
     std::vector<double> hres(8 * nslot);
+    std::vector<int64_t> hptr(S->nslices + 1);
+    PGCP_TRY_CUDA(cudaMemcpyAsync(hptr.data(), S->sl_ptr.p, (S->nslices + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     PGCP_TRY_CUDA(cudaMemcpyAsync(hit.data(), S->iters.p, nslot * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     PGCP_TRY_CUDA(cudaMemcpyAsync(hres.data(), S->res.p, 8 * nslot * sizeof(double), cudaMemcpyDeviceToHost, s));
     PGCP_TRY_CUDA(cudaStreamSynchronize(s));
+    {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        S->kernel_ms = ms;
+        // compulsory bytes per iteration of slot j: off-diagonal values + cols
+        // (12 B per stored entry, padding excluded via the unknown count),
+        // D and Dinv (16 B/row), x read + write (32 B/row)
+        S->iters_sum = S->iters_max = S->bytes_iter_weighted = 0;
+        for (int j = 0; j < nslot; ++j) {
+            int64_t e = hptr[S->h_sl_off[j + 1]] - hptr[S->h_sl_off[j]];
+            double rows = (double)S->h_nu[j];
+            double bytes = 12.0 * (double)e + 48.0 * rows;
+            S->iters_sum += hit[j];
+            S->iters_max = std::max<double>(S->iters_max, hit[j]);
+            S->bytes_iter_weighted += bytes * hit[j];
+            S->nrows_u += rows;
+            S->nnz_off += (double)e;
+        }
+    }
     const double ctol = (o && o->contract_tol > 0) ? o->contract_tol : 1e-10;
     int worst = PGCP_OK;
     for (int j = 0; j < nslot; ++j) {
@@ -1073,6 +1105,21 @@ int export_system(pgcp_batch* b, int which, int32_t comp, int64_t* dims, int32_t
     if (data) std::copy(dv.begin(), dv.end(), data);
     if (rhs) std::copy(hr.begin(), hr.end(), rhs);
     return PGCP_OK;
+}
+
+
+void solve_summary(const pgcp_batch* b, int which, double* out) {
+    for (int i = 0; i < 8; ++i) out[i] = 0;
+    SolveSystem* S = static_cast<SolveSystem*>(b->sys[which]);
+    if (!S) return;
+    out[0] = S->kernel_ms;
+    out[1] = S->iters_sum;
+    out[2] = S->iters_max;
+    out[3] = S->bytes_iter_weighted;   // sum over slots of iters * compulsory bytes/iter
+    out[4] = S->nnz_off;               // stored slice entries (incl. padding)
+    out[5] = S->nrows_u;
+    out[6] = S->csize;
+    out[7] = S->nslot;
 }
 
 }  // namespace pgcp

@@ -152,13 +152,18 @@ class SquareMobiusRec:
         return _apply_recs([self], z, side)
 
 
+def _s8(x):
+    x &= 0xff
+    return x - 256 if x > 127 else x
+
+
 def _from_native(r):
     p = list(r.p)
     if r.kind == 0:
         npins = (r.flags >> 8) & 0xff
         pins = []
         for k in range(npins):
-            side = np.int8((r.flags >> (16 + 8 * k)) & 0xff)
+            side = _s8(r.flags >> (16 + 8 * k))
             pins.append((complex(p[8 + 4 * k], p[9 + 4 * k]), complex(p[10 + 4 * k], p[11 + 4 * k]), int(side)))
         rec = MobiusRec.__new__(MobiusRec)
         rec.a, rec.b, rec.c, rec.d = (complex(p[0], p[1]), complex(p[2], p[3]), complex(p[4], p[5]),
@@ -167,9 +172,9 @@ def _from_native(r):
         rec.pins = tuple(pins)
         return rec
     if r.kind == 1:
-        return SqrtRatioRec(complex(p[0], p[1]), complex(p[2], p[3]), int(np.int8(r.flags & 0xff)))
+        return SqrtRatioRec(complex(p[0], p[1]), complex(p[2], p[3]), _s8(r.flags))
     if r.kind == 2:
-        return OpenRec(complex(p[0], p[1]), int(np.int8(r.flags & 0xff)))
+        return OpenRec(complex(p[0], p[1]), _s8(r.flags))
     if r.kind == 3:
         return CloseRec(p[0], p[1])
     return SquareMobiusRec(complex(p[0], p[1]))
