@@ -1,0 +1,331 @@
+#!/usr/bin/env python
+"""PGCP hot-path benchmark (BASELINE.json metric: mesh vertices/sec end to
+end, plus the batched-PCG HBM roofline).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+    python -m torch.distributed.run --nnodes=1 --nproc-per-node N \
+        --master-addr 127.0.0.1 --master-port P bench.py --gpus N ...
+
+Workload (BASELINE configs[1], the largest single-GPU configuration the
+metric is quoted on): 1024 x 1024 height field, 8 seeded Gaussian bumps,
+8 x 8 cell-aligned subdomains, free-boundary global conformal map, with the
+documented balanced rows -> strips -> tree weld schedule (the reference's
+greedy schedule raises WeldError on this layout).
+
+One step = the whole pipeline (partition, plan, flatten, weld, harmonic,
+stitch, metrics):
+  value  device-resident inputs (mesh arrays already in HBM), coordinates
+         left on the device; L2 flushed (256 MiB write) before every step,
+         each step bracketed by CUDA events on the launch stream;
+  e2e    through the public API from pinned host buffers: TriMesh(V, F)
+         (H2D + validation) -> parameterize -> coordinates/provenance D2H.
+The CPU baseline / reference arm is the oracle port (oracle/, restating the
+reference's numpy/scipy path) timed on the host cores over a bounded sample
+of the same workload: the DNCP flatten + harmonic solves of the first C
+subdomains (C = host cores), one process per core, OPENBLAS_NUM_THREADS=1.
+"""
+
+import os
+
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+os.environ.setdefault("OMP_NUM_THREADS", "1")
+os.environ.setdefault("MKL_NUM_THREADS", "1")
+
+import argparse
+import json
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "mesh_vertices_per_sec"
+UNIT = "vertices/s"
+WORKLOAD = ("cfg2: 1024x1024 height field (8 Gaussian bumps, seed 0), 8x8 cell-aligned subdomains, "
+            "free-boundary global conformal map, rows->strips->tree weld schedule")
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    p.add_argument("--grid", type=int, default=1024, help="vertices per side (1024 = cfg 2)")
+    p.add_argument("--blocks", type=int, default=8)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--cpu-sample", type=int, default=0, help="subdomains in the CPU sample (0 = cores)")
+    return p.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload(grid, blocks):
+    from paper_1903_12359_b200 import generators as gen
+    V, F, cuts = gen.height_field_case(grid, blocks, n_bumps=8, seed=0)
+    pairs = gen.row_tree_schedule_order(blocks, blocks)
+    return V, F, cuts, pairs
+
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            pk = json.load(fh)
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic():
+    """dram bytes per PCG launch from the committed ncu capture, if any."""
+    path = os.path.join(ROOT, "profiles", "pcg_ncu_summary.json")
+    try:
+        with open(path) as fh:
+            s = json.load(fh)
+        return s.get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.active", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, dev_index):
+        self.dev = dev_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        time.sleep(0.05)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle (reference arm and cpu_baseline)
+
+
+def cpu_sample(V, F, cuts, nsub):
+    """Bounded CPU sample: oracle DNCP flatten + harmonic re-solve of the
+    first `nsub` subdomains on one process per subdomain."""
+    import oracle
+    sp = oracle.split_mesh(V, F, cuts)
+    idx = list(range(min(nsub, sp.n_sub)))
+    sub = oracle.surface.SplitResult(sp.V, sp.F, [sp.sub_V[i] for i in idx], [sp.sub_F[i] for i in idx],
+                                     [sp.vertex_maps[i] for i in idx], sp.face_assignment, sp.cuts,
+                                     [sp.loops[i] for i in idx], [sp.boundary_cycles[i] for i in idx])
+    nverts = int(sum(len(v) for v in sub.sub_V))
+    return sub, nverts
+
+
+def cpu_time(sub, workers):
+    import oracle
+    t0 = time.perf_counter()
+    flat, _ = oracle.subdomain_solves(sub, workers)
+    g = [flat[i][sub.loops[i]] for i in range(sub.n_sub)]
+    oracle.pipeline._fan_out(oracle.pipeline._harmonic_job,
+                             [(sub.sub_V[i], sub.sub_F[i], sub.loops[i], g[i]) for i in range(sub.n_sub)],
+                             workers)
+    return time.perf_counter() - t0
+
+
+def run_reference(args, V, F, cuts):
+    cores = os.cpu_count() or 1
+    nsub = args.cpu_sample or cores
+    sub, nverts = cpu_sample(V, F, cuts, nsub)
+    workers = min(cores, sub.n_sub)
+    for _ in range(args.warmup):
+        cpu_time(sub, workers)
+    times = [cpu_time(sub, workers) for _ in range(args.steps)]
+    total = sum(times)
+    value = nverts * args.steps / total
+    sample = (f"oracle DNCP flatten + harmonic of {sub.n_sub} of the 64 cfg-2 subdomains "
+              f"({nverts} local vertices), {workers} worker processes")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": WORKLOAD, "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    V, F, cuts, pairs = workload(args.grid, args.blocks)
+    if args.impl == "reference":
+        if world > 1 and rank != 0:
+            return 0
+        run_reference(args, V, F, cuts)
+        return 0
+
+    import torch
+    import paper_1903_12359_b200 as pg
+    from paper_1903_12359_b200 import _native as nat
+
+    if world > 1:
+        return run_distributed(args, V, F, cuts, pairs)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    lib = nat.lib()
+    n = len(V)
+
+    # resident inputs
+    mesh_dev = pg.TriMesh(V, F)
+    mesh_dev.device_arrays()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def step_value():
+        return pg.parameterize(mesh_dev, cuts, "free", pairs=pairs, keep_device=True)
+
+    for _ in range(args.warmup):
+        gp, rep = step_value()
+    assert rep.flips == 0, "warm-up run produced flips"
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    sampler = ClockSampler(local)
+    sampler.start()
+    l0 = lib.pgcp_launch_count()
+    total_ms = 0.0
+    pcg_ms, pcg_bytes, pcg_iters = [], [], []
+    stages = {}
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        gp, rep = step_value()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        total_ms += e0.elapsed_time(e1)
+        fl = rep.solver["flatten"]
+        pcg_ms.append(fl["kernel_ms"])
+        pcg_bytes.append(fl["bytes"])
+        pcg_iters.append(fl["iters_sum"])
+        for k, v in rep.timings.items():
+            stages[k] = stages.get(k, 0.0) + 1e3 * v
+    launches = lib.pgcp_launch_count() - l0
+    clocks = sampler.stop()
+    ms = total_ms / args.steps
+    value = n / (ms / 1e3)
+
+    # e2e: public API from pinned host buffers, H2D and D2H inside the region
+    e2e = None
+    if not args.no_e2e:
+        Vp = torch.from_numpy(np.ascontiguousarray(V)).pin_memory()
+        Fp = torch.from_numpy(np.ascontiguousarray(F.astype(np.int64))).pin_memory()
+        Cp = torch.from_numpy(np.ascontiguousarray(cuts)).pin_memory()
+        Vn, Fn, Cn = Vp.numpy(), Fp.numpy(), Cp.numpy()
+        h2d = Vn.nbytes + (Fn.nbytes // 2) + Cn.nbytes  # faces travel as int32
+        d2h = 0
+        for i in range(args.warmup + args.steps):
+            if i == args.warmup:
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+            mesh = pg.TriMesh(Vn, Fn)
+            gp, rep = pg.parameterize(mesh, Cn, "free", pairs=pairs)
+            coords = gp.coords
+            d2h = coords.nbytes + len(gp.provenance) * 4
+        torch.cuda.synchronize()
+        et = (time.perf_counter() - t0) / args.steps
+        e2e = {"value": n / et, "unit": UNIT, "ms_per_step": 1e3 * et, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h)}
+
+    peak, peak_src = measured_peak()
+    kernel_ms = statistics.mean(pcg_ms)
+    bytes_launch = statistics.mean(pcg_bytes)
+    achieved = bytes_launch / (kernel_ms / 1e3) / 1e9
+    roof = {"bound": "hbm", "kernel": "k_pcg (flatten, 64 subdomains, one launch)", "achieved": achieved,
+            "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": ncu_traffic(),
+            "peak_source": peak_src, "kernel_ms": kernel_ms, "iterations_per_launch": statistics.mean(pcg_iters),
+            "bytes_per_launch": bytes_launch,
+            "bytes_model": "per PCG iteration of a subdomain: 12 B per stored off-diagonal entry (f64 value + "
+                           "i32 col, sliced-ELL, Jacobi-scaled) + 32 B per unknown row (solution read+write); CG "
+                           "vectors r,p,q stay in distributed shared memory"}
+    cpu = None
+    if not args.no_cpu_baseline:
+        cores = os.cpu_count() or 1
+        sub, nverts = cpu_sample(V, F, cuts, args.cpu_sample or cores)
+        workers = min(cores, sub.n_sub)
+        t = cpu_time(sub, workers)
+        cpu = {"value": nverts / t, "unit": UNIT, "cores": workers, "kind": "port",
+               "sample": f"oracle DNCP flatten + harmonic of {sub.n_sub} cfg-2 subdomains ({nverts} local "
+                         f"vertices, {t:.2f} s), one process per core"}
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "n_vertices": n, "n_faces": int(len(F)), "n_subdomains": 64,
+                       "l2": "flushed before every timed step (256 MiB write)", "parallelism": "1 GPU"},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": int(launches),
+            "stages_ms_per_step": {k: v / args.steps for k, v in stages.items()},
+            "quality": {"flips": rep.flips, "angular_mean_deg": rep.distortion["angular_abs"]["mean"],
+                        "angular_sd_deg": rep.distortion["angular_abs"]["sd"]}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_distributed(args, V, F, cuts, pairs):
+    from paper_1903_12359_b200.dist import bench_distributed
+    return bench_distributed(args, V, F, cuts, pairs, METRIC, UNIT, WORKLOAD)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

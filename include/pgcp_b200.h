@@ -161,7 +161,7 @@ PGCP_API int pgcp_batch_harmonic(pgcp_batch* b, const int32_t* comps, int32_t nc
 /* Summary of the last flatten (0) / harmonic (1) solve: out[0] PCG kernel
  * time in ms (CUDA events on the launch stream), [1] total iterations,
  * [2] max iterations, [3] sum over submeshes of iterations x compulsory bytes
- * per iteration (12 B per stored off-diagonal entry + 48 B per row), [4]
+ * per iteration (12 B per stored off-diagonal entry + 32 B per row), [4]
  * stored entries, [5] unknown rows, [6] CTAs per cluster, [7] submeshes. */
 PGCP_API int pgcp_batch_last_solve(const pgcp_batch* b, int which, double* out, int nout);
 

@@ -55,8 +55,10 @@ struct SolveSystem {
     DevBuf<int64_t> sl_off, sv_off, sl_ptr;
     DevBuf<uint32_t> sl_mask;
     DevBuf<int32_t> col, urow, rowsrc, fixed_ref;
+    DevBuf<uint32_t> enc;
     DevBuf<int2> cpl;
-    DevBuf<double> val, D, Dinv;
+    DevBuf<double> val, D, Dinv, Dsq, dmax;
+    DevBuf<double2> cplc;
     DevBuf<double2> b, x, fv;
     DevBuf<int32_t> iters;
     DevBuf<double> res;  // per slot: relres, bnorm^2, true_res^2, xnorm^2, pad
@@ -66,7 +68,7 @@ void free_system(void* p) { delete static_cast<SolveSystem*>(p); }
 
 namespace {
 
-constexpr int PCG_THREADS = 1024;
+constexpr int PCG_THREADS = 512;
 constexpr int PCG_WARPS = PCG_THREADS / 32;
 constexpr int MAX_CLUSTER = 16;
 constexpr int SMEM_LIMIT = 227 * 1024;
@@ -263,6 +265,76 @@ __global__ void k_coupling(int32_t nslot, const int32_t* __restrict__ comps, con
 }
 
 // ---------------------------------------------------------------------------
+// Jacobi scaling: the solver iterates on D^{-1/2} H D^{-1/2} (unit diagonal),
+// which is Jacobi-PCG in exact arithmetic and needs no diagonal loads per
+// iteration. x = D^{-1/2} y.
+
+__global__ void k_dsq(int64_t rows, const double* __restrict__ D, double* __restrict__ Dsq) {
+    GRID_STRIDE(r, rows) Dsq[r] = sqrt(D[r]);
+}
+
+__global__ void k_scale(int32_t nslot, const int64_t* __restrict__ sl_off, int64_t rows,
+                        const int64_t* __restrict__ sl_ptr, const int32_t* __restrict__ col,
+                        double* __restrict__ val, const double* __restrict__ Dsq, double2* __restrict__ b,
+                        const int2* __restrict__ cpl, double2* __restrict__ cplc) {
+    GRID_STRIDE(r, rows) {
+        int64_t s = r >> 5;
+        int lane = (int)(r & 31);
+        int j = bsearch_off(sl_off, nslot + 1, s);
+        int64_t rbase = 32 * sl_off[j];
+        double dr = Dsq[r];
+        int64_t e0 = sl_ptr[s];
+        int w = (int)((sl_ptr[s + 1] - e0) >> 5);
+        for (int k = 0; k < w; ++k) {
+            int64_t e = e0 + 32 * k + lane;
+            val[e] = val[e] / (dr * Dsq[rbase + col[e]]);
+        }
+        double2 bb = b[r];
+        b[r] = make_double2(bb.x / dr, bb.y / dr);
+        int2 c = cpl[r];
+        cplc[r] = make_double2(c.x >= 0 ? 0.5 / (dr * Dsq[rbase + c.x]) : 0.0,
+                               c.y >= 0 ? 0.5 / (dr * Dsq[rbase + c.y]) : 0.0);
+    }
+}
+
+__global__ void k_slot_dmax(const int64_t* __restrict__ sl_off, const double* __restrict__ D,
+                            double* __restrict__ dmax) {
+    __shared__ double red[32];
+    int j = blockIdx.x;
+    double m = 0;
+    for (int64_t r = 32 * sl_off[j] + threadIdx.x; r < 32 * sl_off[j + 1]; r += blockDim.x) m = fmax(m, D[r]);
+    m = warp_max(m);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t = fmax(t, red[w]);
+        dmax[j] = t;
+    }
+}
+
+// column encoding for one cluster shape: (owner rank << 24) | byte offset of
+// the row inside the owner's shared-memory vector block
+__global__ void k_encode_cols(int32_t nslot, const int64_t* __restrict__ sl_off, int64_t nslices,
+                              const int64_t* __restrict__ sl_ptr, const int32_t* __restrict__ col, int csize,
+                              uint32_t* __restrict__ enc) {
+    int lane = threadIdx.x & 31;
+    int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t s = warp; s < nslices; s += nwarp) {
+        int j = bsearch_off(sl_off, nslot + 1, s);
+        int S = (int)(sl_off[j + 1] - sl_off[j]);
+        int chunk = (S + csize - 1) / csize;
+        for (int64_t e = sl_ptr[s] + lane; e < sl_ptr[s + 1]; e += 32) {
+            int c = col[e];
+            int own = (c >> 5) / chunk;
+            int off = c - 32 * own * chunk;
+            enc[e] = ((uint32_t)own << 24) | (uint32_t)(off * 16);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // the solver
 
 struct PcgArgs {
@@ -270,23 +342,19 @@ struct PcgArgs {
     const int64_t* sl_ptr;   // slice -> first entry
     const uint32_t* sl_mask;
     const int32_t* col;
-    const double* val;
-    const double* D;
-    const double* Dinv;
+    const uint32_t* enc;     // encoded columns (owner rank, byte offset)
+    const double* val;       // scaled off-diagonal values
+    const double* D;         // unscaled diagonal (norms of the unscaled residual)
+    const double* dmax;      // per slot max D (stopping bound)
     const int2* cpl;
-    const double2* b;
-    double2* x;
+    const double2* cplc;     // scaled coupling coefficients (next, prev)
+    const double2* b;        // scaled rhs
+    double2* x;              // scaled solution y
     int32_t* iters;
     double* res;             // per slot [8]
     double tol2;             // rtol^2
     int32_t maxit;
     int32_t chunk_cap;       // slices per CTA the smem was sized for
-};
-
-struct Vec {
-    double2* z;
-    double2* p;
-    double2* q;
 };
 
 // deterministic cluster-wide sum of two doubles: warp -> CTA (fixed order) ->
@@ -316,6 +384,50 @@ __device__ __forceinline__ double2 cluster_sum2(cg::cluster_group& cl, int csize
     return t;
 }
 
+constexpr int KPF = 8;  // prefetched off-diagonal entries per row
+
+struct SliceBuf {
+    int w;
+    int64_t e;
+    uint32_t c[KPF];
+    double v[KPF];
+};
+
+__device__ __forceinline__ void slice_load(SliceBuf& B, const PcgArgs& A, const int* s_ent, const int* s_w,
+                                           int64_t ent0, int ls, int nloc, int lane) {
+    if (ls >= nloc) {
+        B.w = 0;
+        return;
+    }
+    B.w = s_w[ls];
+    B.e = ent0 + s_ent[ls] + lane;
+#pragma unroll
+    for (int k = 0; k < KPF; ++k) {
+        if (k < B.w) {
+            B.c[k] = __ldg(A.enc + B.e + 32 * k);
+            B.v[k] = __ldg(A.val + B.e + 32 * k);
+        }
+    }
+}
+
+__device__ __forceinline__ double2 gather(cg::cluster_group& cl, const double2* rl, int c, int rank, int chunk,
+                                          float inv_chunk) {
+    int own = __float2int_rz(((float)(c >> 5) + 0.5f) * inv_chunk);
+    int off = c - 32 * own * chunk;
+    return (own == rank) ? rl[off] : *cl.map_shared_rank(rl + off, own);
+}
+
+// generic load through the cluster shared-memory window: base[r] is the
+// generic address of rank r's vector block (local rank included)
+__device__ __forceinline__ double2 gather_enc(const unsigned long long* base, uint32_t c) {
+    const double2* p = reinterpret_cast<const double2*>(base[c >> 24] + (c & 0xffffffu));
+    return *p;
+}
+
+__device__ __forceinline__ void red_add(double* p, double v) {
+    asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+
 __global__ void __launch_bounds__(PCG_THREADS, 1) k_pcg(PcgArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
     cg::cluster_group cl = cg::this_cluster();
@@ -330,127 +442,147 @@ __global__ void __launch_bounds__(PCG_THREADS, 1) k_pcg(PcgArgs A) {
     const int my_lo = min(S, rank * chunk);
     const int nloc = min(S, my_lo + chunk) - my_lo;
     const float inv_chunk = 1.0f / (float)chunk;
+    const int cap = A.chunk_cap;
 
     double2* s_warp = reinterpret_cast<double2*>(smem);
     double2* s_slot = s_warp + PCG_WARPS;
-    double2* zl = s_slot + 2 * MAX_CLUSTER;
-    double2* pl = zl + 32 * A.chunk_cap;
-    double2* ql = pl + 32 * A.chunk_cap;
+    double2* rl = s_slot + 2 * MAX_CLUSTER;
+    double2* pl = rl + 32 * cap;
+    double2* ql = pl + 32 * cap;
+    int* s_ent = reinterpret_cast<int*>(ql + 32 * cap);
+    int* s_w = s_ent + cap;
+    uint32_t* s_mask = reinterpret_cast<uint32_t*>(s_w + cap);
 
-    const int64_t row0 = 32 * (s0 + my_lo);  // first global row of this CTA
-    const int nrow = 32 * nloc;
-
-    // init: x = 0 (done by the builder), r = b, z = Dinv b
-    double l_rz = 0.0, l_bb = 0.0;
-    for (int i = threadIdx.x; i < nrow; i += PCG_THREADS) {
+    __shared__ unsigned long long s_base[MAX_CLUSTER];
+    if (threadIdx.x < csize) s_base[threadIdx.x] = reinterpret_cast<unsigned long long>(cl.map_shared_rank(rl, threadIdx.x));
+    const int64_t gs0 = s0 + my_lo;           // first global slice of this CTA
+    const int64_t row0 = 32 * gs0;            // first global row of this CTA
+    const int64_t ent0 = A.sl_ptr[gs0];       // first entry of this CTA
+    for (int t = threadIdx.x; t < nloc; t += PCG_THREADS) {
+        int64_t e = A.sl_ptr[gs0 + t];
+        s_ent[t] = (int)(e - ent0);
+        s_w[t] = (int)((A.sl_ptr[gs0 + t + 1] - e) >> 5);
+        s_mask[t] = A.sl_mask[gs0 + t];
+    }
+    // init: y = 0 (done by the builder), r = b, p = q = 0
+    double l_rr = 0.0, l_bb = 0.0;
+    for (int i = threadIdx.x; i < 32 * nloc; i += PCG_THREADS) {
         double2 bi = A.b[row0 + i];
-        double di = A.Dinv[row0 + i];
-        double2 zi = make_double2(di * bi.x, di * bi.y);
-        zl[i] = zi;
+        double di = A.D[row0 + i];
+        rl[i] = bi;
         pl[i] = make_double2(0.0, 0.0);
         ql[i] = make_double2(0.0, 0.0);
-        l_rz += bi.x * zi.x + bi.y * zi.y;
-        l_bb += bi.x * bi.x + bi.y * bi.y;
+        double m2 = bi.x * bi.x + bi.y * bi.y;
+        l_rr += m2;
+        l_bb += di * m2;  // ||b||^2 of the unscaled system
     }
     int parity = 0;
-    double2 t0 = cluster_sum2(cl, csize, rank, l_rz, l_bb, s_warp, s_slot, parity);
+    double2 t0 = cluster_sum2(cl, csize, rank, l_rr, l_bb, s_warp, s_slot, parity);
     parity ^= 1;
-    double rz = t0.x;
-    const double bb = t0.y;
-    const double stop = A.tol2 * bb;
-    double beta = 0.0, rr = bb;
+    double rr = t0.x;
+    const double bbU = t0.y;
+    const double dmax = A.dmax[slot];
+    // ||r||^2 = sum D |r^|^2 <= dmax ||r^||^2: stopping on the bound is safe
+    const double stop = A.tol2 * bbU / dmax;
+    double beta = 0.0, alpha = 0.0;
     int it = 0;
+    const bool active = bbU > 0.0 && rr > stop;
 
-    if (bb > 0.0 && rr > stop) {
+    if (active) {
         for (it = 0; it < A.maxit;) {
-            // ---- phase A: q = A z + beta q, p = z + beta p, pq
+            // ---- phase A: (y += alpha p_old), q = A r + beta q, p = r + beta p, pq
             double l_pq = 0.0;
-            for (int ls = warp; ls < nloc; ls += PCG_WARPS) {
-                const int64_t gs = s0 + my_lo + ls;
-                const int64_t e0 = A.sl_ptr[gs];
-                const int wdt = (int)((A.sl_ptr[gs + 1] - e0) >> 5);
-                const int li = 32 * ls + lane;
-                const int64_t gr = row0 + li;
-                double2 zi = zl[li];
-                double di = A.D[gr];
-                double sx = di * zi.x, sy = di * zi.y;
-                const int32_t* cp = A.col + e0 + lane;
-                const double* vp = A.val + e0 + lane;
-#pragma unroll 4
-                for (int k = 0; k < wdt; ++k) {
-                    int c = __ldg(cp + 32 * k);
-                    double v = __ldg(vp + 32 * k);
-                    int sc = c >> 5;
-                    int own = __float2int_rz(((float)sc + 0.5f) * inv_chunk);
-                    int off = c - 32 * own * chunk;
-                    double2 zc = (own == rank) ? zl[off] : *cl.map_shared_rank(zl + off, own);
-                    sx = fma(v, zc.x, sx);
-                    sy = fma(v, zc.y, sy);
-                }
-                uint32_t msk = A.sl_mask[gs];
-                if (msk & (1u << lane)) {
-                    int2 nb = A.cpl[gr];
-                    double2 zn = make_double2(0.0, 0.0), zp = make_double2(0.0, 0.0);
-                    if (nb.x >= 0) {
-                        int o = __float2int_rz(((float)(nb.x >> 5) + 0.5f) * inv_chunk);
-                        zn = (o == rank) ? zl[nb.x - 32 * o * chunk] : *cl.map_shared_rank(zl + (nb.x - 32 * o * chunk), o);
+            SliceBuf B0, B1;
+            slice_load(B0, A, s_ent, s_w, ent0, warp, nloc, lane);
+            for (int ls = warp; ls < nloc; ls += 2 * PCG_WARPS) {
+#pragma unroll
+                for (int half = 0; half < 2; ++half) {
+                    const int cur = ls + half * PCG_WARPS;
+                    SliceBuf& Bc = half ? B1 : B0;
+                    SliceBuf& Bn = half ? B0 : B1;
+                    slice_load(Bn, A, s_ent, s_w, ent0, cur + PCG_WARPS, nloc, lane);
+                    if (cur < nloc) {
+                        const int li = 32 * cur + lane;
+                        const int64_t gr = row0 + li;
+                        double2 ri = rl[li];
+                        double sx = ri.x, sy = ri.y;
+#pragma unroll
+                        for (int k = 0; k < KPF; ++k) {
+                            if (k < Bc.w) {
+                                double2 rc = gather_enc(s_base, Bc.c[k]);
+                                sx = fma(Bc.v[k], rc.x, sx);
+                                sy = fma(Bc.v[k], rc.y, sy);
+                            }
+                        }
+                        for (int k = KPF; k < Bc.w; ++k) {
+                            uint32_t c = __ldg(A.enc + Bc.e + 32 * k);
+                            double v = __ldg(A.val + Bc.e + 32 * k);
+                            double2 rc = gather_enc(s_base, c);
+                            sx = fma(v, rc.x, sx);
+                            sy = fma(v, rc.y, sy);
+                        }
+                        if (s_mask[cur] & (1u << lane)) {
+                            int2 nb = A.cpl[gr];
+                            double2 cc = A.cplc[gr];
+                            double2 zn = nb.x >= 0 ? gather(cl, rl, nb.x, rank, chunk, inv_chunk) : make_double2(0, 0);
+                            double2 zp = nb.y >= 0 ? gather(cl, rl, nb.y, rank, chunk, inv_chunk) : make_double2(0, 0);
+                            // + i (cn z_next - cp z_prev)
+                            double ax = cc.x * zn.x - cc.y * zp.x, ay = cc.x * zn.y - cc.y * zp.y;
+                            sx -= ay;
+                            sy += ax;
+                        }
+                        double2 qi = ql[li], pi = pl[li];
+                        if (it > 0) {
+                            red_add(&A.x[gr].x, alpha * pi.x);
+                            red_add(&A.x[gr].y, alpha * pi.y);
+                        }
+                        qi.x = fma(beta, qi.x, sx);
+                        qi.y = fma(beta, qi.y, sy);
+                        pi.x = fma(beta, pi.x, ri.x);
+                        pi.y = fma(beta, pi.y, ri.y);
+                        ql[li] = qi;
+                        pl[li] = pi;
+                        l_pq += pi.x * qi.x + pi.y * qi.y;
                     }
-                    if (nb.y >= 0) {
-                        int o = __float2int_rz(((float)(nb.y >> 5) + 0.5f) * inv_chunk);
-                        zp = (o == rank) ? zl[nb.y - 32 * o * chunk] : *cl.map_shared_rank(zl + (nb.y - 32 * o * chunk), o);
-                    }
-                    // + i/2 (zn - zp)
-                    sx -= 0.5 * (zn.y - zp.y);
-                    sy += 0.5 * (zn.x - zp.x);
                 }
-                double2 qi = ql[li], pi = pl[li];
-                qi.x = fma(beta, qi.x, sx);
-                qi.y = fma(beta, qi.y, sy);
-                pi.x = fma(beta, pi.x, zi.x);
-                pi.y = fma(beta, pi.y, zi.y);
-                ql[li] = qi;
-                pl[li] = pi;
-                l_pq += pi.x * qi.x + pi.y * qi.y;
             }
             double2 tq = cluster_sum2(cl, csize, rank, l_pq, 0.0, s_warp, s_slot, parity);
             parity ^= 1;
-            const double alpha = rz / tq.x;
-            // ---- phase B
-            double l_rz2 = 0.0, l_rr = 0.0;
-            for (int i = threadIdx.x; i < nrow; i += PCG_THREADS) {
-                const int64_t gr = row0 + i;
-                double2 pi = pl[i], qi = ql[i], zi = zl[i];
-                double2 xi = A.x[gr];
-                xi.x = fma(alpha, pi.x, xi.x);
-                xi.y = fma(alpha, pi.y, xi.y);
-                A.x[gr] = xi;
-                double dv = A.Dinv[gr], di = A.D[gr];
-                double ad = alpha * dv;
-                zi.x = fma(-ad, qi.x, zi.x);
-                zi.y = fma(-ad, qi.y, zi.y);
-                zl[i] = zi;
-                double m2 = zi.x * zi.x + zi.y * zi.y;
-                l_rz2 += di * m2;
-                l_rr += di * di * m2;
+            alpha = rr / tq.x;
+            // ---- phase B: r -= alpha q (same rows as phase A: no block barrier needed)
+            double l_rr2 = 0.0;
+            for (int ls = warp; ls < nloc; ls += PCG_WARPS) {
+                const int li = 32 * ls + lane;
+                double2 qi = ql[li], ri = rl[li];
+                ri.x = fma(-alpha, qi.x, ri.x);
+                ri.y = fma(-alpha, qi.y, ri.y);
+                rl[li] = ri;
+                l_rr2 += ri.x * ri.x + ri.y * ri.y;
             }
-            double2 tr = cluster_sum2(cl, csize, rank, l_rz2, l_rr, s_warp, s_slot, parity);
+            double2 tr = cluster_sum2(cl, csize, rank, l_rr2, 0.0, s_warp, s_slot, parity);
             parity ^= 1;
-            beta = tr.x / rz;
-            rz = tr.x;
-            rr = tr.y;
+            beta = tr.x / rr;
+            rr = tr.x;
             ++it;
             if (rr <= stop || !(rr == rr)) break;
+        }
+        // the last update y += alpha p
+        for (int ls = warp; ls < nloc; ls += PCG_WARPS) {
+            const int li = 32 * ls + lane;
+            double2 pi = pl[li];
+            red_add(&A.x[row0 + li].x, alpha * pi.x);
+            red_add(&A.x[row0 + li].y, alpha * pi.y);
         }
     }
     if (rank == 0 && threadIdx.x == 0) {
         A.iters[slot] = it;
-        A.res[8 * slot + 0] = (bb > 0.0) ? sqrt(rr / bb) : 0.0;
-        A.res[8 * slot + 1] = bb;
+        A.res[8 * slot + 0] = (bbU > 0.0) ? sqrt(dmax * rr / bbU) : 0.0;  // upper bound of ||r||/||b||
+        A.res[8 * slot + 1] = bbU;
     }
 }
 
-// true residual ||b - H x||, ||x||, ||b|| per slot; one block per slot,
-// fixed-order reduction; x gathered from global memory
+// true residual of the unscaled system from the scaled arrays:
+//   ||b - H x||^2 = sum D |b^ - H^ y|^2, ||x||^2 = sum |y|^2 / D, ||b||^2 = sum D |b^|^2
 __global__ void k_true_residual(PcgArgs A) {
     __shared__ double red[3][32];
     const int slot = blockIdx.x;
@@ -464,28 +596,30 @@ __global__ void k_true_residual(PcgArgs A) {
         const int64_t e0 = A.sl_ptr[gs];
         const int wdt = (int)((A.sl_ptr[gs + 1] - e0) >> 5);
         const int64_t gr = rbase + 32 * ls + lane;
-        double2 xi = A.x[gr];
-        double di = A.D[gr];
-        double sx = di * xi.x, sy = di * xi.y;
+        double2 yi = A.x[gr];
+        double sx = yi.x, sy = yi.y;
         for (int k = 0; k < wdt; ++k) {
             int c = A.col[e0 + 32 * k + lane];
             double v = A.val[e0 + 32 * k + lane];
-            double2 xc = A.x[rbase + c];
-            sx = fma(v, xc.x, sx);
-            sy = fma(v, xc.y, sy);
+            double2 yc = A.x[rbase + c];
+            sx = fma(v, yc.x, sx);
+            sy = fma(v, yc.y, sy);
         }
         if (A.sl_mask[gs] & (1u << lane)) {
             int2 nb = A.cpl[gr];
+            double2 cc = A.cplc[gr];
             double2 zn = nb.x >= 0 ? A.x[rbase + nb.x] : make_double2(0.0, 0.0);
             double2 zp = nb.y >= 0 ? A.x[rbase + nb.y] : make_double2(0.0, 0.0);
-            sx -= 0.5 * (zn.y - zp.y);
-            sy += 0.5 * (zn.x - zp.x);
+            double ax = cc.x * zn.x - cc.y * zp.x, ay = cc.x * zn.y - cc.y * zp.y;
+            sx -= ay;
+            sy += ax;
         }
         double2 bi = A.b[gr];
+        double di = A.D[gr];
         double rx = bi.x - sx, ry = bi.y - sy;
-        a_r += rx * rx + ry * ry;
-        a_x += xi.x * xi.x + xi.y * xi.y;
-        a_b += bi.x * bi.x + bi.y * bi.y;
+        a_r += di * (rx * rx + ry * ry);
+        a_x += (yi.x * yi.x + yi.y * yi.y) / di;
+        a_b += di * (bi.x * bi.x + bi.y * bi.y);
     }
     a_r = warp_sum(a_r);
     a_x = warp_sum(a_x);
@@ -511,17 +645,24 @@ __global__ void k_true_residual(PcgArgs A) {
     }
 }
 
-// scatter the solution back to submesh-local vertices (fixed vertices get
+// scatter x = D^{-1/2} y back to submesh-local vertices (fixed vertices get
 // their prescribed values)
 __global__ void k_scatter(int64_t ne, int32_t nslot, const int32_t* __restrict__ comps,
                           const int64_t* __restrict__ sv_off, const int64_t* __restrict__ vert_off,
                           const int32_t* __restrict__ urow, const int32_t* __restrict__ fixed_ref,
-                          const double2* __restrict__ fv, const double2* __restrict__ x, double2* __restrict__ z) {
+                          const double2* __restrict__ fv, const double2* __restrict__ y,
+                          const double* __restrict__ Dsq, double2* __restrict__ z) {
     GRID_STRIDE(e, ne) {
         int j = bsearch_off(sv_off, nslot + 1, e);
         int64_t g = vert_off[comps[j]] + (e - sv_off[j]);
         int r = urow[e];
-        z[g] = (r >= 0) ? x[r] : fv[fixed_ref[e]];
+        if (r >= 0) {
+            double2 v = y[r];
+            double d = Dsq[r];
+            z[g] = make_double2(v.x / d, v.y / d);
+        } else {
+            z[g] = fv[fixed_ref[e]];
+        }
     }
 }
 
@@ -582,7 +723,7 @@ __global__ void k_flat_checks(const int32_t* __restrict__ comps, const int64_t* 
 // host side
 
 int pick_cluster(int64_t max_slices, int32_t nslot, int32_t forced, int* csize_out, int* chunk_out) {
-    const int max_chunk = (SMEM_LIMIT - RED_BYTES) / (48 * 32);
+    const int max_chunk = (SMEM_LIMIT - RED_BYTES) / (48 * 32 + 12);
     int cmin = 1;
     while (cmin <= MAX_CLUSTER && (max_slices + cmin - 1) / cmin > max_chunk) cmin *= 2;
     if (cmin > MAX_CLUSTER) {
@@ -605,7 +746,7 @@ int pick_cluster(int64_t max_slices, int32_t nslot, int32_t forced, int* csize_o
 
 int launch_pcg(SolveSystem* S, const PcgArgs& args, int csize, cudaStream_t s) {
     int chunk = args.chunk_cap;
-    size_t smem = (size_t)RED_BYTES + (size_t)3 * 32 * chunk * sizeof(double2);
+    size_t smem = (size_t)RED_BYTES + (size_t)3 * 32 * chunk * sizeof(double2) + (size_t)12 * chunk;
     if (smem > SMEM_LIMIT) {
         set_error("pcg: shared memory %zu exceeds limit", smem);
         return PGCP_E_INVALID;
@@ -760,6 +901,17 @@ int build_system(pgcp_batch* b, SolveSystem* S, bool dncp, const int32_t* d_pins
             PGCP_LAUNCH_CHECK();
         }
     }
+    // symmetric Jacobi scaling of the system (values, rhs, coupling)
+    PGCP_TRY(S->Dsq.alloc(S->rows, s));
+    PGCP_TRY(S->cplc.alloc(S->rows, s));
+    PGCP_TRY(S->dmax.alloc(nslot, s));
+    k_dsq<<<grid_for(S->rows, 256), 256, 0, s>>>(S->rows, S->D.p, S->Dsq.p);
+    PGCP_LAUNCH_CHECK();
+    k_scale<<<grid_for(S->rows, 256), 256, 0, s>>>(nslot, S->sl_off.p, S->rows, S->sl_ptr.p, S->col.p, S->val.p,
+                                                 S->Dsq.p, S->b.p, S->cpl.p, S->cplc.p);
+    PGCP_LAUNCH_CHECK();
+    k_slot_dmax<<<nslot, 256, 0, s>>>(S->sl_off.p, S->D.p, S->dmax.p);
+    PGCP_LAUNCH_CHECK();
     return PGCP_OK;
 }
 
@@ -779,10 +931,16 @@ int run_solve(pgcp_batch* b, SolveSystem* S, const pgcp_solve_opts* o, double* z
     A.sl_ptr = S->sl_ptr.p;
     A.sl_mask = S->sl_mask.p;
     A.col = S->col.p;
+    PGCP_TRY(S->enc.alloc(S->nnz, s));
+    k_encode_cols<<<grid_for(S->nslices * 32, 256), 256, 0, s>>>(nslot, S->sl_off.p, S->nslices, S->sl_ptr.p, S->col.p,
+                                                               csize, S->enc.p);
+    PGCP_LAUNCH_CHECK();
+    A.enc = S->enc.p;
     A.val = S->val.p;
     A.D = S->D.p;
-    A.Dinv = S->Dinv.p;
+    A.dmax = S->dmax.p;
     A.cpl = S->cpl.p;
+    A.cplc = S->cplc.p;
     A.b = S->b.p;
     A.x = S->x.p;
     A.iters = S->iters.p;
@@ -801,7 +959,7 @@ int run_solve(pgcp_batch* b, SolveSystem* S, const pgcp_solve_opts* o, double* z
     k_true_residual<<<nslot, 512, 0, s>>>(A);
     PGCP_LAUNCH_CHECK();
     k_scatter<<<grid_for(S->ne, 256), 256, 0, s>>>(S->ne, nslot, S->d_comps.p, S->sv_off.p, b->vert_off.p, S->urow.p,
-                                                 S->fixed_ref.p, S->fv.p, S->x.p, (double2*)z);
+                                                 S->fixed_ref.p, S->fv.p, S->x.p, S->Dsq.p, (double2*)z);
     PGCP_LAUNCH_CHECK();
     if (S->dncp) {
         k_flat_checks<<<nslot, 256, 0, s>>>(S->d_comps.p, b->vert_off.p, b->row_ptr.p, b->col.p, b->val.p,
@@ -821,14 +979,14 @@ int run_solve(pgcp_batch* b, SolveSystem* S, const pgcp_solve_opts* o, double* z
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
         S->kernel_ms = ms;
-        // compulsory bytes per iteration of slot j: off-diagonal values + cols
-        // (12 B per stored entry, padding excluded via the unknown count),
-        // D and Dinv (16 B/row), x read + write (32 B/row)
+        // compulsory bytes per iteration of slot j: stored off-diagonal
+        // values + cols (12 B per slice entry) and the y update (read +
+        // write, 32 B per unknown row); CG vectors stay on chip
         S->iters_sum = S->iters_max = S->bytes_iter_weighted = 0;
         for (int j = 0; j < nslot; ++j) {
             int64_t e = hptr[S->h_sl_off[j + 1]] - hptr[S->h_sl_off[j]];
             double rows = (double)S->h_nu[j];
-            double bytes = 12.0 * (double)e + 48.0 * rows;
+            double bytes = 12.0 * (double)e + 32.0 * rows;
             S->iters_sum += hit[j];
             S->iters_max = std::max<double>(S->iters_max, hit[j]);
             S->bytes_iter_weighted += bytes * hit[j];
@@ -1034,10 +1192,18 @@ int export_system(pgcp_batch* b, int which, int32_t comp, int64_t* dims, int32_t
     PGCP_TRY_CUDA(cudaMemcpyAsync(lp.data(), b->loop.p + lo, nb * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     const int64_t nU = S->h_nu[j];
     std::vector<double2> hb(nU > 0 ? nU : 1);
-    if (nU > 0)
+    std::vector<double> hd(nU > 0 ? nU : 1);
+    if (nU > 0) {
         PGCP_TRY_CUDA(cudaMemcpyAsync(hb.data(), S->b.p + 32 * S->h_sl_off[j], nU * sizeof(double2),
                                       cudaMemcpyDeviceToHost, s));
+        PGCP_TRY_CUDA(cudaMemcpyAsync(hd.data(), S->Dsq.p + 32 * S->h_sl_off[j], nU * sizeof(double),
+                                      cudaMemcpyDeviceToHost, s));
+    }
     PGCP_TRY_CUDA(cudaStreamSynchronize(s));
+    for (int64_t r = 0; r < nU; ++r) {  // the solver holds D^{-1/2} b
+        hb[r].x *= hd[r];
+        hb[r].y *= hd[r];
+    }
     const int64_t rbase = 32 * S->h_sl_off[j];
     std::vector<int64_t> pos(nc, -1);
     for (int64_t v = 0; v < nc; ++v)

@@ -212,6 +212,14 @@ class DeviceBatch:
             rhs = rhs.view(np.complex128)
         return sparse.csr_matrix((data, indices, indptr), shape=(rows, rows)), rhs
 
+    def last_solve(self, which):
+        """PCG kernel time (CUDA events), iterations and compulsory bytes of
+        the last flatten (0) / harmonic (1) solve."""
+        out = (ctypes.c_double * 8)()
+        nat.check(nat.lib().pgcp_batch_last_solve(self.h, which, out, 8))
+        return {"kernel_ms": out[0], "iters_sum": out[1], "iters_max": out[2], "bytes": out[3],
+                "stored_entries": out[4], "rows": out[5], "cluster": int(out[6]), "submeshes": int(out[7])}
+
     def energy(self, z):
         out = (ctypes.c_double * self.K)()
         nat.check(nat.lib().pgcp_batch_conformal_energy(self.h, ptr(z), out, stream_handle(self.stream)))

@@ -48,6 +48,7 @@ class RunConfig:
     pairs: list = None
     rtol: float = 1e-10            # PCG recurrence tolerance
     cluster: int = 0               # CTAs per subdomain (0 = auto)
+    keep_device: bool = False      # leave coords on the device (no final D2H)
 
     def validate(self):
         if self.mode not in ("free", "disk", "sphere"):
@@ -190,7 +191,7 @@ def _poly_area(z):
 
 
 def parameterize(mesh, cuts=None, mode="free", workers=1, seed=0, mobius_area=False, config=None,
-                 schedule=None, pairs=None, solve_comps=None):
+                 schedule=None, pairs=None, keep_device=False):
     """Global conformal parameterization (pipeline.py:119-271) on the device.
 
     Same signature and results as the reference; `schedule`/`pairs` select
@@ -203,6 +204,8 @@ def parameterize(mesh, cuts=None, mode="free", workers=1, seed=0, mobius_area=Fa
     if pairs is not None:
         cfg.pairs = pairs
         cfg.schedule = "pairs"
+    if keep_device:
+        cfg.keep_device = True
     cfg.validate()
     mode = cfg.mode
     report = RunReport(mode=mode, n_vertices=mesh.n_vertices, n_faces=mesh.n_faces)
@@ -249,7 +252,7 @@ def parameterize(mesh, cuts=None, mode="free", workers=1, seed=0, mobius_area=Fa
     clk.start()
     z0, fst = batch.flatten(rtol=cfg.rtol, cluster=cfg.cluster)
     clk.stop("flatten")
-    report.solver = {"flatten_iters": [s["iters"] for s in fst]}
+    report.solver = {"flatten_iters": [s["iters"] for s in fst], "flatten": batch.last_solve(0)}
 
     if K == 1 and mode == "free":
         embeddings = z0
@@ -293,6 +296,7 @@ def parameterize(mesh, cuts=None, mode="free", workers=1, seed=0, mobius_area=Fa
                                                center.real, center.imag, _stream()))
         z, hst = batch.harmonic(loop_gid, tv, rtol=cfg.rtol, cluster=cfg.cluster)
         report.solver["harmonic_iters"] = [s["iters"] for s in hst]
+        report.solver["harmonic"] = batch.last_solve(1)
         if center is not None:
             gids = np.concatenate([np.arange(voff[i], voff[i + 1]) for i in exterior]).astype(np.int32)
             gt = torch.as_tensor(gids).to(dev)
@@ -390,6 +394,8 @@ def _finish(mesh, batch, embeddings, gp, report, cfg, clk):
     report.distortion = dist.to_dict()
     seam_ok = all(r <= cfg.snap_tol for r in report.seam_residuals)
     report.ok = report.flips == 0 and seam_ok
+    if cfg.keep_device:
+        return gp, report
     # hand back host arrays, as the reference's GlobalParam holds numpy
     clk.start()
     gp.coords = gp.coords.cpu().numpy()
