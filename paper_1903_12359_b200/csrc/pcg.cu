@@ -32,6 +32,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 #include "batch.cuh"
 
@@ -56,6 +58,7 @@ struct SolveSystem {
     DevBuf<uint32_t> sl_mask;
     DevBuf<int32_t> col, urow, rowsrc, fixed_ref;
     DevBuf<uint32_t> enc;
+    DevBuf<uint8_t> remote;
     DevBuf<int2> cpl;
     DevBuf<double> val, D, Dinv, Dsq, dmax;
     DevBuf<double2> cplc;
@@ -72,7 +75,7 @@ constexpr int PCG_THREADS = 512;
 constexpr int PCG_WARPS = PCG_THREADS / 32;
 constexpr int MAX_CLUSTER = 16;
 constexpr int SMEM_LIMIT = 227 * 1024;
-constexpr int RED_BYTES = 2 * MAX_CLUSTER * 2 * 8 + PCG_WARPS * 2 * 8 + 64;
+constexpr int RED_BYTES = 2 * MAX_CLUSTER * 2 * 8 + 32 * 2 * 8 + 64;
 
 __device__ __forceinline__ int bsearch_off(const int64_t* __restrict__ off, int n, int64_t e) {
     int lo = 0, hi = n - 1;  // largest j with off[j] <= e
@@ -81,6 +84,14 @@ __device__ __forceinline__ int bsearch_off(const int64_t* __restrict__ off, int 
         if (off[mid] <= e) lo = mid; else hi = mid - 1;
     }
     return lo;
+}
+
+// Paired sliced-ELL: slice s (32 rows) stores entry k of row `lane` at
+// sl_ptr[s] + 64 (k / 2) + 2 lane + (k % 2); widths are even, so one 16-byte
+// load per lane fetches two values (and one 8-byte load two columns) and a
+// warp's load is a single contiguous 512 B (256 B) transaction.
+__host__ __device__ __forceinline__ int64_t sell_pos(int64_t e0, int k, int lane) {
+    return e0 + ((int64_t)(k >> 1) << 6) + (lane << 1) + (k & 1);
 }
 
 // ---------------------------------------------------------------------------
@@ -161,6 +172,7 @@ __global__ void k_slice_len(BuildArgs a, int64_t nslices, int64_t* __restrict__ 
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) cnt = max(cnt, __shfl_xor_sync(0xffffffffu, cnt, o));
+        cnt = (cnt + 1) & ~1;  // even widths (paired layout)
         if (lane == 0) len[s] = 32 * (int64_t)cnt;
     }
 }
@@ -195,8 +207,8 @@ __global__ void k_fill_rows(BuildArgs a, int64_t rows, const int64_t* __restrict
                 int64_t ee = a.sv_off[j] + lc;
                 int ur = a.urow[ee];
                 if (ur >= 0) {
-                    ocol[p0 + 32 * k + lane] = (int32_t)(ur - rbase);
-                    oval[p0 + 32 * k + lane] = v;
+                    ocol[sell_pos(p0, k, lane)] = (int32_t)(ur - rbase);
+                    oval[sell_pos(p0, k, lane)] = v;
                     ++k;
                 } else {
                     double2 f = a.fv[a.fixed_ref[ee]];
@@ -206,8 +218,8 @@ __global__ void k_fill_rows(BuildArgs a, int64_t rows, const int64_t* __restrict
             }
         }
         for (; k < w; ++k) {
-            ocol[p0 + 32 * k + lane] = selfrow;
-            oval[p0 + 32 * k + lane] = 0.0;
+            ocol[sell_pos(p0, k, lane)] = selfrow;
+            oval[sell_pos(p0, k, lane)] = 0.0;
         }
         D[r] = d;
         Dinv[r] = 1.0 / d;
@@ -286,7 +298,7 @@ __global__ void k_scale(int32_t nslot, const int64_t* __restrict__ sl_off, int64
         int64_t e0 = sl_ptr[s];
         int w = (int)((sl_ptr[s + 1] - e0) >> 5);
         for (int k = 0; k < w; ++k) {
-            int64_t e = e0 + 32 * k + lane;
+            int64_t e = sell_pos(e0, k, lane);
             val[e] = val[e] / (dr * Dsq[rbase + col[e]]);
         }
         double2 bb = b[r];
@@ -313,11 +325,13 @@ __global__ void k_slot_dmax(const int64_t* __restrict__ sl_off, const double* __
     }
 }
 
-// column encoding for one cluster shape: (owner rank << 24) | byte offset of
-// the row inside the owner's shared-memory vector block
+// column encoding for one cluster shape: a row owned by this CTA is the byte
+// offset of its vector entry in the CTA's shared block; a row owned by
+// another CTA of the cluster is (1 << 31) | (owner rank << 24) | byte offset.
+// remote[s] = 1 if slice s has any remote entry (the kernel's slow path).
 __global__ void k_encode_cols(int32_t nslot, const int64_t* __restrict__ sl_off, int64_t nslices,
                               const int64_t* __restrict__ sl_ptr, const int32_t* __restrict__ col, int csize,
-                              uint32_t* __restrict__ enc) {
+                              uint32_t* __restrict__ enc, uint8_t* __restrict__ remote) {
     int lane = threadIdx.x & 31;
     int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -325,12 +339,21 @@ __global__ void k_encode_cols(int32_t nslot, const int64_t* __restrict__ sl_off,
         int j = bsearch_off(sl_off, nslot + 1, s);
         int S = (int)(sl_off[j + 1] - sl_off[j]);
         int chunk = (S + csize - 1) / csize;
+        int me = (int)(s - sl_off[j]) / chunk;  // owner of this slice
+        bool rem = false;
         for (int64_t e = sl_ptr[s] + lane; e < sl_ptr[s + 1]; e += 32) {
             int c = col[e];
             int own = (c >> 5) / chunk;
             int off = c - 32 * own * chunk;
-            enc[e] = ((uint32_t)own << 24) | (uint32_t)(off * 16);
+            if (own == me) {
+                enc[e] = (uint32_t)(off * 16);
+            } else {
+                enc[e] = 0x80000000u | ((uint32_t)own << 24) | (uint32_t)(off * 16);
+                rem = true;
+            }
         }
+        rem = __any_sync(0xffffffffu, rem);
+        if (lane == 0) remote[s] = rem;
     }
 }
 
@@ -342,7 +365,8 @@ struct PcgArgs {
     const int64_t* sl_ptr;   // slice -> first entry
     const uint32_t* sl_mask;
     const int32_t* col;
-    const uint32_t* enc;     // encoded columns (owner rank, byte offset)
+    const uint32_t* enc;     // encoded columns (see k_encode_cols)
+    const uint8_t* remote;   // slice has entries owned by another CTA
     const double* val;       // scaled off-diagonal values
     const double* D;         // unscaled diagonal (norms of the unscaled residual)
     const double* dmax;      // per slot max D (stopping bound)
@@ -355,10 +379,12 @@ struct PcgArgs {
     double tol2;             // rtol^2
     int32_t maxit;
     int32_t chunk_cap;       // slices per CTA the smem was sized for
+    long long* timing;       // optional: per CTA [phaseA, red1, phaseB, red2] cycles (iterations 64..191)
 };
 
 // deterministic cluster-wide sum of two doubles: warp -> CTA (fixed order) ->
 // every CTA receives every CTA's partial through DSMEM -> fixed-order sum
+template <int NW>
 __device__ __forceinline__ double2 cluster_sum2(cg::cluster_group& cl, int csize, int rank, double a, double b,
                                                 double2* s_warp, double2* s_slot, int parity) {
     int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -367,7 +393,7 @@ __device__ __forceinline__ double2 cluster_sum2(cg::cluster_group& cl, int csize
     if (lane == 0) s_warp[w] = make_double2(a, b);
     __syncthreads();
     if (w == 0) {
-        double2 v = (lane < PCG_WARPS) ? s_warp[lane] : make_double2(0.0, 0.0);
+        double2 v = (lane < NW) ? s_warp[lane] : make_double2(0.0, 0.0);
         double ta = warp_sum(v.x), tb = warp_sum(v.y);
         if (lane < csize) {
             double2* dst = cl.map_shared_rank(s_slot + parity * MAX_CLUSTER, lane);
@@ -384,28 +410,45 @@ __device__ __forceinline__ double2 cluster_sum2(cg::cluster_group& cl, int csize
     return t;
 }
 
-constexpr int KPF = 8;  // prefetched off-diagonal entries per row
+constexpr int KPF = 8;  // prefetched off-diagonal entries per row (4 pairs)
 
 struct SliceBuf {
-    int w;
-    int64_t e;
+    double2 y;    // this lane's solution entry (updated in place, one owner thread)
+    int w;        // even width
+    int remote;   // any entry of the slice owned by another CTA
+    int off;      // entry offset of this lane's first pair, relative to the CTA's first entry
     uint32_t c[KPF];
     double v[KPF];
 };
 
-__device__ __forceinline__ void slice_load(SliceBuf& B, const PcgArgs& A, const int* s_ent, const int* s_w,
-                                           int64_t ent0, int ls, int nloc, int lane) {
-    if (ls >= nloc) {
-        B.w = 0;
-        return;
-    }
-    B.w = s_w[ls];
-    B.e = ent0 + s_ent[ls] + lane;
+__device__ __forceinline__ void slice_load(SliceBuf& B, const double* __restrict__ valc,
+                                           const uint32_t* __restrict__ encc, const int* s_ent, const int* s_w,
+                                           int ls, int nloc, int lane, const double2* yrow, bool need_y) {
+    // entries past the width become (own row, 0.0): the gathers below are
+    // straight-line and issue back to back
+    const uint32_t self = (uint32_t)((32 * ls + lane) * 16);
+    B.w = 0;
+    B.remote = 0;
+    B.off = 0;
 #pragma unroll
     for (int k = 0; k < KPF; ++k) {
-        if (k < B.w) {
-            B.c[k] = __ldg(A.enc + B.e + 32 * k);
-            B.v[k] = __ldg(A.val + B.e + 32 * k);
+        B.c[k] = self;
+        B.v[k] = 0.0;
+    }
+    if (ls >= nloc) return;
+    if (need_y) B.y = yrow[32 * ls + lane];
+    B.w = s_w[ls] & 0xffff;
+    B.remote = s_w[ls] >> 16;
+    B.off = s_ent[ls] + (lane << 1);
+#pragma unroll
+    for (int p = 0; p < KPF / 2; ++p) {
+        if (2 * p < B.w) {
+            double2 vv = __ldg(reinterpret_cast<const double2*>(valc + B.off + (p << 6)));
+            uint2 cc = __ldg(reinterpret_cast<const uint2*>(encc + B.off + (p << 6)));
+            B.v[2 * p] = vv.x;
+            B.v[2 * p + 1] = vv.y;
+            B.c[2 * p] = cc.x;
+            B.c[2 * p + 1] = cc.y;
         }
     }
 }
@@ -419,16 +462,26 @@ __device__ __forceinline__ double2 gather(cg::cluster_group& cl, const double2* 
 
 // generic load through the cluster shared-memory window: base[r] is the
 // generic address of rank r's vector block (local rank included)
-__device__ __forceinline__ double2 gather_enc(const unsigned long long* base, uint32_t c) {
-    const double2* p = reinterpret_cast<const double2*>(base[c >> 24] + (c & 0xffffffu));
+__device__ __forceinline__ double2 gather_enc(const unsigned long long* base, const double2* rl, uint32_t c) {
+    if (!(c >> 31)) return *reinterpret_cast<const double2*>(reinterpret_cast<const char*>(rl) + c);
+    const double2* p = reinterpret_cast<const double2*>(base[(c >> 24) & 0x7f] + (c & 0xffffffu));
     return *p;
+}
+
+// branch-free generic gather for slices with remote entries: local entries go
+// through the generic address of this CTA's own block (base[rank])
+__device__ __forceinline__ double2 gather_gen(const unsigned long long* base, int rank, uint32_t c) {
+    const int own = (c >> 31) ? (int)((c >> 24) & 0x7f) : rank;
+    return *reinterpret_cast<const double2*>(base[own] + (c & 0xffffffu));
 }
 
 __device__ __forceinline__ void red_add(double* p, double v) {
     asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
 
-__global__ void __launch_bounds__(PCG_THREADS, 1) k_pcg(PcgArgs A) {
+template <int NT, bool PF>
+__global__ void __launch_bounds__(NT, 1) k_pcg(PcgArgs A) {
+    constexpr int PCG_WARPS = NT / 32;
     extern __shared__ __align__(16) unsigned char smem[];
     cg::cluster_group cl = cg::this_cluster();
     const int csize = (int)cl.num_blocks();
@@ -458,15 +511,15 @@ __global__ void __launch_bounds__(PCG_THREADS, 1) k_pcg(PcgArgs A) {
     const int64_t gs0 = s0 + my_lo;           // first global slice of this CTA
     const int64_t row0 = 32 * gs0;            // first global row of this CTA
     const int64_t ent0 = A.sl_ptr[gs0];       // first entry of this CTA
-    for (int t = threadIdx.x; t < nloc; t += PCG_THREADS) {
+    for (int t = threadIdx.x; t < nloc; t += NT) {
         int64_t e = A.sl_ptr[gs0 + t];
         s_ent[t] = (int)(e - ent0);
-        s_w[t] = (int)((A.sl_ptr[gs0 + t + 1] - e) >> 5);
+        s_w[t] = (int)((A.sl_ptr[gs0 + t + 1] - e) >> 5) | ((int)A.remote[gs0 + t] << 16);
         s_mask[t] = A.sl_mask[gs0 + t];
     }
     // init: y = 0 (done by the builder), r = b, p = q = 0
     double l_rr = 0.0, l_bb = 0.0;
-    for (int i = threadIdx.x; i < 32 * nloc; i += PCG_THREADS) {
+    for (int i = threadIdx.x; i < 32 * nloc; i += NT) {
         double2 bi = A.b[row0 + i];
         double di = A.D[row0 + i];
         rl[i] = bi;
@@ -477,7 +530,7 @@ __global__ void __launch_bounds__(PCG_THREADS, 1) k_pcg(PcgArgs A) {
         l_bb += di * m2;  // ||b||^2 of the unscaled system
     }
     int parity = 0;
-    double2 t0 = cluster_sum2(cl, csize, rank, l_rr, l_bb, s_warp, s_slot, parity);
+    double2 t0 = cluster_sum2<PCG_WARPS>(cl, csize, rank, l_rr, l_bb, s_warp, s_slot, parity);
     parity ^= 1;
     double rr = t0.x;
     const double bbU = t0.y;
@@ -489,35 +542,52 @@ __global__ void __launch_bounds__(PCG_THREADS, 1) k_pcg(PcgArgs A) {
     const bool active = bbU > 0.0 && rr > stop;
 
     if (active) {
+        long long tA = 0, tR1 = 0, tB = 0, tR2 = 0;
         for (it = 0; it < A.maxit;) {
+            const bool timed = A.timing && it >= 64 && it < 192;
+            long long c0 = timed ? clock64() : 0;
             // ---- phase A: (y += alpha p_old), q = A r + beta q, p = r + beta p, pq
             double l_pq = 0.0;
             SliceBuf B0, B1;
-            slice_load(B0, A, s_ent, s_w, ent0, warp, nloc, lane);
+            const double* valc = A.val + ent0;
+            const uint32_t* encc = A.enc + ent0;
+            double2* yrow = A.x + row0;
+            if (PF) slice_load(B0, valc, encc, s_ent, s_w, warp, nloc, lane, yrow, it > 0);
             for (int ls = warp; ls < nloc; ls += 2 * PCG_WARPS) {
 #pragma unroll
                 for (int half = 0; half < 2; ++half) {
                     const int cur = ls + half * PCG_WARPS;
                     SliceBuf& Bc = half ? B1 : B0;
                     SliceBuf& Bn = half ? B0 : B1;
-                    slice_load(Bn, A, s_ent, s_w, ent0, cur + PCG_WARPS, nloc, lane);
+                    if (PF) {
+                        slice_load(Bn, valc, encc, s_ent, s_w, cur + PCG_WARPS, nloc, lane, yrow, it > 0);
+                    } else {
+                        slice_load(Bc, valc, encc, s_ent, s_w, cur, nloc, lane, yrow, it > 0);
+                    }
                     if (cur < nloc) {
                         const int li = 32 * cur + lane;
                         const int64_t gr = row0 + li;
                         double2 ri = rl[li];
                         double sx = ri.x, sy = ri.y;
+                        double2 g[KPF];
+                        if (!Bc.remote) {
+#pragma unroll
+                            for (int k = 0; k < KPF; ++k)
+                                g[k] = *reinterpret_cast<const double2*>(reinterpret_cast<const char*>(rl) + Bc.c[k]);
+                        } else {
+#pragma unroll
+                            for (int k = 0; k < KPF; ++k) g[k] = gather_gen(s_base, rank, Bc.c[k]);
+                        }
 #pragma unroll
                         for (int k = 0; k < KPF; ++k) {
-                            if (k < Bc.w) {
-                                double2 rc = gather_enc(s_base, Bc.c[k]);
-                                sx = fma(Bc.v[k], rc.x, sx);
-                                sy = fma(Bc.v[k], rc.y, sy);
-                            }
+                            sx = fma(Bc.v[k], g[k].x, sx);
+                            sy = fma(Bc.v[k], g[k].y, sy);
                         }
                         for (int k = KPF; k < Bc.w; ++k) {
-                            uint32_t c = __ldg(A.enc + Bc.e + 32 * k);
-                            double v = __ldg(A.val + Bc.e + 32 * k);
-                            double2 rc = gather_enc(s_base, c);
+                            const int e = Bc.off + ((k >> 1) << 6) + (k & 1);
+                            uint32_t c = __ldg(encc + e);
+                            double v = __ldg(valc + e);
+                            double2 rc = gather_enc(s_base, rl, c);
                             sx = fma(v, rc.x, sx);
                             sy = fma(v, rc.y, sy);
                         }
@@ -532,9 +602,11 @@ __global__ void __launch_bounds__(PCG_THREADS, 1) k_pcg(PcgArgs A) {
                             sy += ax;
                         }
                         double2 qi = ql[li], pi = pl[li];
-                        if (it > 0) {
-                            red_add(&A.x[gr].x, alpha * pi.x);
-                            red_add(&A.x[gr].y, alpha * pi.y);
+                        if (it > 0) {  // y += alpha p (previous iteration), plain load/store
+                            double2 yv = Bc.y;
+                            yv.x = fma(alpha, pi.x, yv.x);
+                            yv.y = fma(alpha, pi.y, yv.y);
+                            yrow[li] = yv;
                         }
                         qi.x = fma(beta, qi.x, sx);
                         qi.y = fma(beta, qi.y, sy);
@@ -546,11 +618,14 @@ __global__ void __launch_bounds__(PCG_THREADS, 1) k_pcg(PcgArgs A) {
                     }
                 }
             }
-            double2 tq = cluster_sum2(cl, csize, rank, l_pq, 0.0, s_warp, s_slot, parity);
+            long long c1 = timed ? clock64() : 0;
+            double2 tq = cluster_sum2<PCG_WARPS>(cl, csize, rank, l_pq, 0.0, s_warp, s_slot, parity);
             parity ^= 1;
             alpha = rr / tq.x;
+            long long c2 = timed ? clock64() : 0;
             // ---- phase B: r -= alpha q (same rows as phase A: no block barrier needed)
             double l_rr2 = 0.0;
+#pragma unroll 4
             for (int ls = warp; ls < nloc; ls += PCG_WARPS) {
                 const int li = 32 * ls + lane;
                 double2 qi = ql[li], ri = rl[li];
@@ -559,19 +634,36 @@ __global__ void __launch_bounds__(PCG_THREADS, 1) k_pcg(PcgArgs A) {
                 rl[li] = ri;
                 l_rr2 += ri.x * ri.x + ri.y * ri.y;
             }
-            double2 tr = cluster_sum2(cl, csize, rank, l_rr2, 0.0, s_warp, s_slot, parity);
+            long long c3 = timed ? clock64() : 0;
+            double2 tr = cluster_sum2<PCG_WARPS>(cl, csize, rank, l_rr2, 0.0, s_warp, s_slot, parity);
             parity ^= 1;
+            if (timed) {
+                long long c4 = clock64();
+                tA += c1 - c0;
+                tR1 += c2 - c1;
+                tB += c3 - c2;
+                tR2 += c4 - c3;
+            }
             beta = tr.x / rr;
             rr = tr.x;
             ++it;
             if (rr <= stop || !(rr == rr)) break;
         }
+        if (A.timing && threadIdx.x == 0) {
+            long long* t = A.timing + 4 * blockIdx.x;
+            t[0] = tA;
+            t[1] = tR1;
+            t[2] = tB;
+            t[3] = tR2;
+        }
         // the last update y += alpha p
         for (int ls = warp; ls < nloc; ls += PCG_WARPS) {
             const int li = 32 * ls + lane;
             double2 pi = pl[li];
-            red_add(&A.x[row0 + li].x, alpha * pi.x);
-            red_add(&A.x[row0 + li].y, alpha * pi.y);
+            double2 yv = A.x[row0 + li];
+            yv.x = fma(alpha, pi.x, yv.x);
+            yv.y = fma(alpha, pi.y, yv.y);
+            A.x[row0 + li] = yv;
         }
     }
     if (rank == 0 && threadIdx.x == 0) {
@@ -599,8 +691,8 @@ __global__ void k_true_residual(PcgArgs A) {
         double2 yi = A.x[gr];
         double sx = yi.x, sy = yi.y;
         for (int k = 0; k < wdt; ++k) {
-            int c = A.col[e0 + 32 * k + lane];
-            double v = A.val[e0 + 32 * k + lane];
+            int c = A.col[sell_pos(e0, k, lane)];
+            double v = A.val[sell_pos(e0, k, lane)];
             double2 yc = A.x[rbase + c];
             sx = fma(v, yc.x, sx);
             sy = fma(v, yc.y, sy);
@@ -744,18 +836,14 @@ int pick_cluster(int64_t max_slices, int32_t nslot, int32_t forced, int* csize_o
     return PGCP_OK;
 }
 
-int launch_pcg(SolveSystem* S, const PcgArgs& args, int csize, cudaStream_t s) {
-    int chunk = args.chunk_cap;
-    size_t smem = (size_t)RED_BYTES + (size_t)3 * 32 * chunk * sizeof(double2) + (size_t)12 * chunk;
-    if (smem > SMEM_LIMIT) {
-        set_error("pcg: shared memory %zu exceeds limit", smem);
-        return PGCP_E_INVALID;
-    }
-    PGCP_TRY_CUDA(cudaFuncSetAttribute(k_pcg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    if (csize > 8) PGCP_TRY_CUDA(cudaFuncSetAttribute(k_pcg, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+template <int NT, bool PF>
+int launch_pcg_t(SolveSystem* S, const PcgArgs& args, int csize, size_t smem, cudaStream_t s) {
+    auto kern = k_pcg<NT, PF>;
+    PGCP_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (csize > 8) PGCP_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(S->nslot * csize), 1, 1);
-    cfg.blockDim = dim3(PCG_THREADS, 1, 1);
+    cfg.blockDim = dim3(NT, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
@@ -766,15 +854,33 @@ int launch_pcg(SolveSystem* S, const PcgArgs& args, int csize, cudaStream_t s) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     int nclusters = 0;
-    cudaError_t oe = cudaOccupancyMaxActiveClusters(&nclusters, k_pcg, &cfg);
+    cudaError_t oe = cudaOccupancyMaxActiveClusters(&nclusters, kern, &cfg);
     if (oe != cudaSuccess || nclusters < 1) {
         set_error("pcg: cluster of %d CTAs with %zu B shared memory cannot be scheduled (%s)", csize, smem,
                   cudaGetErrorString(oe));
         cudaGetLastError();
         return PGCP_E_CUDA;
     }
-    PGCP_TRY_CUDA(cudaLaunchKernelEx(&cfg, k_pcg, args));
+    PGCP_TRY_CUDA(cudaLaunchKernelEx(&cfg, kern, args));
     return PGCP_OK;
+}
+
+int launch_pcg(SolveSystem* S, const PcgArgs& args, int csize, cudaStream_t s) {
+    int chunk = args.chunk_cap;
+    size_t smem = (size_t)RED_BYTES + (size_t)3 * 32 * chunk * sizeof(double2) + (size_t)12 * chunk;
+    if (smem > SMEM_LIMIT) {
+        set_error("pcg: shared memory %zu exceeds limit", smem);
+        return PGCP_E_INVALID;
+    }
+    const char* v = getenv("PGCP_PCG_VARIANT");
+    int variant = v ? atoi(v) : 0;
+    switch (variant) {
+        case 1: return launch_pcg_t<1024, false>(S, args, csize, smem, s);
+        case 2: return launch_pcg_t<768, false>(S, args, csize, smem, s);
+        case 3: return launch_pcg_t<512, false>(S, args, csize, smem, s);
+        case 4: return launch_pcg_t<256, true>(S, args, csize, smem, s);
+        default: return launch_pcg_t<512, true>(S, args, csize, smem, s);
+    }
 }
 
 // Build the slot system. pins (device int32 [2*nslot]) for DNCP, or the fixed
@@ -932,10 +1038,12 @@ int run_solve(pgcp_batch* b, SolveSystem* S, const pgcp_solve_opts* o, double* z
     A.sl_mask = S->sl_mask.p;
     A.col = S->col.p;
     PGCP_TRY(S->enc.alloc(S->nnz, s));
+    PGCP_TRY(S->remote.alloc(S->nslices, s));
     k_encode_cols<<<grid_for(S->nslices * 32, 256), 256, 0, s>>>(nslot, S->sl_off.p, S->nslices, S->sl_ptr.p, S->col.p,
-                                                               csize, S->enc.p);
+                                                               csize, S->enc.p, S->remote.p);
     PGCP_LAUNCH_CHECK();
     A.enc = S->enc.p;
+    A.remote = S->remote.p;
     A.val = S->val.p;
     A.D = S->D.p;
     A.dmax = S->dmax.p;
@@ -949,6 +1057,14 @@ int run_solve(pgcp_batch* b, SolveSystem* S, const pgcp_solve_opts* o, double* z
     A.tol2 = rtol * rtol;
     A.maxit = (o && o->maxit > 0) ? o->maxit : 200000;
     A.chunk_cap = chunk;
+    DevBuf<long long> tbuf;
+    A.timing = nullptr;
+    const bool want_timing = getenv("PGCP_PCG_TIMING") != nullptr;
+    if (want_timing) {
+        PGCP_TRY(tbuf.alloc(4 * (int64_t)nslot * csize, s));
+        PGCP_TRY(tbuf.zero(s));
+        A.timing = tbuf.p;
+    }
     cudaEvent_t e0, e1;
     PGCP_TRY_CUDA(cudaEventCreate(&e0));
     PGCP_TRY_CUDA(cudaEventCreate(&e1));
@@ -973,6 +1089,15 @@ int run_solve(pgcp_batch* b, SolveSystem* S, const pgcp_solve_opts* o, double* z
     PGCP_TRY_CUDA(cudaMemcpyAsync(hit.data(), S->iters.p, nslot * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     PGCP_TRY_CUDA(cudaMemcpyAsync(hres.data(), S->res.p, 8 * nslot * sizeof(double), cudaMemcpyDeviceToHost, s));
     PGCP_TRY_CUDA(cudaStreamSynchronize(s));
+    if (want_timing) {
+        std::vector<long long> ht(4 * (size_t)nslot * csize);
+        PGCP_TRY_CUDA(cudaMemcpy(ht.data(), tbuf.p, ht.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+        double acc[4] = {0, 0, 0, 0};
+        for (size_t i = 0; i < ht.size(); ++i) acc[i % 4] += (double)ht[i];
+        double nct = (double)nslot * csize * 128.0;
+        fprintf(stderr, "[pcg timing] cycles/iter per CTA: phaseA %.0f red1 %.0f phaseB %.0f red2 %.0f (csize %d)\n",
+                acc[0] / nct, acc[1] / nct, acc[2] / nct, acc[3] / nct, csize);
+    }
     {
         float ms = 0;
         cudaEventElapsedTime(&ms, e0, e1);

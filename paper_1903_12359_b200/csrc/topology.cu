@@ -38,6 +38,79 @@ __global__ void k_validate_faces(const int32_t* __restrict__ F, int64_t m, int64
     }
 }
 
+// bounding box (mesh.py:134-138) and degenerate faces (mesh.py:99-104):
+// area < 1e-12 * diag^2
+__device__ __forceinline__ void atomic_min_d(double* p, double v) {
+    unsigned long long* a = reinterpret_cast<unsigned long long*>(p);
+    unsigned long long old = *a, assumed;
+    do {
+        assumed = old;
+        if (__longlong_as_double(assumed) <= v) return;
+        old = atomicCAS(a, assumed, __double_as_longlong(v));
+    } while (old != assumed);
+}
+__device__ __forceinline__ void atomic_max_d(double* p, double v) {
+    unsigned long long* a = reinterpret_cast<unsigned long long*>(p);
+    unsigned long long old = *a, assumed;
+    do {
+        assumed = old;
+        if (__longlong_as_double(assumed) >= v) return;
+        old = atomicCAS(a, assumed, __double_as_longlong(v));
+    } while (old != assumed);
+}
+
+__global__ void k_bbox(const double* __restrict__ V, int64_t n, double* bb) {
+    __shared__ double red[6][32];
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    GRID_STRIDE(v, n) {
+        for (int d = 0; d < 3; ++d) {
+            double x = V[3 * v + d];
+            lo[d] = fmin(lo[d], x);
+            hi[d] = fmax(hi[d], x);
+        }
+    }
+    int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int d = 0; d < 3; ++d) {
+        double a = lo[d], b = hi[d];
+        for (int o = 16; o > 0; o >>= 1) {
+            a = fmin(a, __shfl_xor_sync(0xffffffffu, a, o));
+            b = fmax(b, __shfl_xor_sync(0xffffffffu, b, o));
+        }
+        if (lane == 0) {
+            red[d][w] = a;
+            red[3 + d][w] = b;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+        int d = threadIdx.x;
+        double a = INFINITY, b = -INFINITY;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
+            a = fmin(a, red[d][i]);
+            b = fmax(b, red[3 + d][i]);
+        }
+        atomic_min_d(&bb[d], a);
+        atomic_max_d(&bb[3 + d], b);
+    }
+}
+
+__global__ void k_degenerate(const double* __restrict__ V, const int32_t* __restrict__ F, int64_t m,
+                             const double* __restrict__ bb, DevErr* err) {
+    const double dx = bb[3] - bb[0], dy = bb[4] - bb[1], dz = bb[5] - bb[2];
+    const double diag = sqrt((dx * dx + dy * dy) + dz * dz);
+    const double lim = 1e-12 * diag * diag;
+    GRID_STRIDE(f, m) {
+        const double* a = V + 3 * F[3 * f];
+        const double* b = V + 3 * F[3 * f + 1];
+        const double* c = V + 3 * F[3 * f + 2];
+        double ux = b[0] - a[0], uy = b[1] - a[1], uz = b[2] - a[2];
+        double vx = c[0] - a[0], vy = c[1] - a[1], vz = c[2] - a[2];
+        double cx = uy * vz - uz * vy, cy = uz * vx - ux * vz, cz = ux * vy - uy * vx;
+        double area = 0.5 * sqrt((cx * cx + cy * cy) + cz * cz);
+        if (area < lim) dev_fail(err, 5, f);
+    }
+}
+
 __global__ void k_count_inc(const int32_t* __restrict__ F, int64_t nc, int32_t* __restrict__ cnt) {
     GRID_STRIDE(i, nc) { atomicAdd(&cnt[F[i]], 1); }
 }
@@ -418,6 +491,23 @@ int build_partition(pgcp_batch* b, const int64_t* cuts, int64_t ncuts, bool no_c
         else
             set_error("face %llu has repeated vertices", herr.index);
         return PGCP_E_MESH;
+    }
+
+    // --- degenerate faces against the bounding-box diagonal
+    {
+        DevBuf<double> bb;
+        PGCP_TRY(bb.alloc(6, s));
+        double init[6] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        PGCP_TRY_CUDA(cudaMemcpyAsync(bb.p, init, sizeof(init), cudaMemcpyHostToDevice, s));
+        k_bbox<<<grid_for(n, 256, 296), 256, 0, s>>>(b->V.p, n, bb.p);
+        PGCP_LAUNCH_CHECK();
+        k_degenerate<<<grid_for(m, 256), 256, 0, s>>>(b->V.p, b->F.p, m, bb.p, err.p);
+        PGCP_LAUNCH_CHECK();
+        PGCP_TRY(read_err(err, &herr, s));
+        if (herr.code) {
+            set_error("degenerate face %llu (area below epsilon)", herr.index);
+            return PGCP_E_MESH;
+        }
     }
 
     // --- vertex -> face incidence, sorted by face id
