@@ -99,6 +99,7 @@ PGCP_API int pgcp_batch_info(const pgcp_batch* b, int64_t* info, int ninfo);
 #define PGCP_ARR_L_VAL 7       /* f64   [nnz]                                      */
 #define PGCP_ARR_W3 8          /* f64   [3m]      half-cotangent per face corner    */
 #define PGCP_ARR_PINS 9        /* int32 [2K]      default pins (local)              */
+#define PGCP_ARR_CYCLES 10     /* int32 [sum_nb]  boundary cycles, parent ids       */
 PGCP_API int pgcp_batch_array(const pgcp_batch* b, int which, void** ptr, int64_t* count);
 
 /* Local faces of every submesh, faces in increasing parent-face order

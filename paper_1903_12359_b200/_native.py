@@ -17,7 +17,7 @@ OK = 0
 E_INVALID, E_MESH, E_PARTITION, E_SOLVE, E_NOCONV, E_WELD, E_CUDA, E_VALIDATION = range(1, 9)
 
 ARR_FACE_COMP, ARR_VERT_OFF, ARR_VMAP, ARR_LOOP_OFF, ARR_LOOP, ARR_L_ROWPTR, ARR_L_COL, \
-    ARR_L_VAL, ARR_W3, ARR_PINS = range(10)
+    ARR_L_VAL, ARR_W3, ARR_PINS, ARR_CYCLES = range(11)
 
 INFO_K, INFO_SUM_N, INFO_SUM_NB, INFO_NNZ_L, INFO_PARENT_CHI, INFO_PARENT_LOOPS, INFO_N, \
     INFO_M, INFO_BAD_COMP = range(9)

@@ -33,6 +33,7 @@ struct pgcp_batch {
     pgcp::DevBuf<int32_t> vmap, lv_comp, lv_gid, loop, nxt, comp_of_gid;
     std::vector<int32_t> h_comp_chi, h_comp_loops;
     pgcp::DevBuf<int32_t> pins;
+    pgcp::DevBuf<int32_t> cyc;  // boundary cycles in parent ids (loop order)
     pgcp::DevBuf<double> w3;
     pgcp::DevBuf<int64_t> row_ptr;
     pgcp::DevBuf<int32_t> col;

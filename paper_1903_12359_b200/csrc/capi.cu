@@ -123,6 +123,7 @@ int pgcp_batch_array(const pgcp_batch* b, int which, void** ptr, int64_t* count)
         case PGCP_ARR_L_VAL: *ptr = b->val.p; *count = b->has_laplacian ? b->nnz : 0; break;
         case PGCP_ARR_W3: *ptr = b->w3.p; *count = b->w3.p ? 3 * b->m : 0; break;
         case PGCP_ARR_PINS: *ptr = b->pins.p; *count = b->pins.p ? 2 * (int64_t)b->K : 0; break;
+        case PGCP_ARR_CYCLES: *ptr = b->cyc.p; *count = b->sum_nb; break;
         default:
             set_error("pgcp_batch_array: unknown array id %d", which);
             return PGCP_E_INVALID;

@@ -26,21 +26,39 @@ namespace {
 using Cycle = std::vector<int64_t>;
 using Runs = std::vector<Cycle>;
 
+// flat scratch indexed by parent vertex id (generation-stamped, no resets)
+struct Scratch {
+    std::vector<int64_t> pos;     // position in the current c2
+    std::vector<uint32_t> gen;    // generation of pos[]
+    std::vector<uint32_t> mark;   // generation marks for set tests
+    uint32_t g = 0, gm = 0;
+    void ensure(int64_t n) {
+        if ((int64_t)pos.size() < n) {
+            pos.assign(n, 0);
+            gen.assign(n, 0);
+            mark.assign(n, 0);
+        }
+    }
+};
+thread_local Scratch g_scr;
+
 // maximal runs of consecutive c1 vertices that are consecutive reversed in
-// c2 (partition.py:149-179); returns false in *full when not a full match
+// c2 (partition.py:149-179); *full when the whole cycle matches
 bool cyclic_runs(const Cycle& c1, const Cycle& c2, Runs* runs, bool* full, std::string* err) {
     runs->clear();
     *full = false;
     const size_t n1 = c1.size(), n2 = c2.size();
-    std::unordered_map<int64_t, int64_t> pos2;
-    pos2.reserve(n2 * 2);
-    for (size_t i = 0; i < n2; ++i) pos2[c2[i]] = (int64_t)i;
+    Scratch& S = g_scr;
+    const uint32_t g = ++S.g;
+    for (size_t i = 0; i < n2; ++i) {
+        S.pos[c2[i]] = (int64_t)i;
+        S.gen[c2[i]] = g;
+    }
     std::vector<char> ok(n1, 0);
     bool all = n1 > 0, any = false;
     for (size_t i = 0; i < n1; ++i) {
-        auto u = pos2.find(c1[i]);
-        auto v = pos2.find(c1[(i + 1) % n1]);
-        if (u != pos2.end() && v != pos2.end() && (v->second + 1) % (int64_t)n2 == u->second) ok[i] = 1;
+        int64_t u = c1[i], v = c1[(i + 1) % n1];
+        if (S.gen[u] == g && S.gen[v] == g && (S.pos[v] + 1) % (int64_t)n2 == S.pos[u]) ok[i] = 1;
         all = all && ok[i];
         any = any || ok[i];
     }
@@ -100,10 +118,13 @@ struct Planner {
     std::string err;
 
     int glue(int64_t ca, int64_t cb, const Cycle& chain) {
-        std::unordered_set<int64_t> sa(cycles[ca].begin(), cycles[ca].end());
-        std::unordered_set<int64_t> sc(chain.begin(), chain.end());
+        Scratch& S = g_scr;
+        const uint32_t ga = ++S.gm;   // on a's cycle
+        for (int64_t v : cycles[ca]) S.mark[v] = ga;
+        const uint32_t gc = ++S.gm;   // on the chain (overrides)
+        for (int64_t v : chain) S.mark[v] = gc;
         for (int64_t v : cycles[cb])
-            if (sa.count(v) && !sc.count(v)) {
+            if (S.mark[v] == ga) {
                 err = "components " + std::to_string(ca) + " and " + std::to_string(cb) +
                       " share vertices beyond one contiguous arc; this cut layout needs multi-arc gluing, which "
                       "is unsupported";
@@ -264,6 +285,22 @@ struct Planner {
 
 }  // namespace
 
+namespace {
+// the two-call protocol (sizes, then copy-out) must not plan twice: keep the
+// last plan of this thread keyed by a checksum of its inputs
+struct PlanCache {
+    uint64_t key = 0;
+    bool valid = false;
+    std::vector<Step> steps;
+};
+thread_local PlanCache g_cache;
+
+uint64_t mix(uint64_t h, uint64_t v) {
+    h ^= v + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+    return h;
+}
+}  // namespace
+
 extern "C" PGCP_API int pgcp_plan_weld_schedule(const int64_t* cyc, const int64_t* cyc_off, int32_t K,
                                                 const int64_t* cuts, int64_t ncuts, int mode_sphere,
                                                 const int32_t* pairs, int32_t npairs, int64_t* out_meta,
@@ -272,54 +309,74 @@ extern "C" PGCP_API int pgcp_plan_weld_schedule(const int64_t* cyc, const int64_
         pgcp::set_error("plan_weld_schedule: invalid arguments");
         return PGCP_E_INVALID;
     }
-    Planner P;
-    for (int32_t i = 0; i < K; ++i) P.cycles[i] = Cycle(cyc + cyc_off[i], cyc + cyc_off[i + 1]);
-    int target = mode_sphere ? 2 : 1;
-    if (mode_sphere && K < 2) {
-        pgcp::set_error("sphere mode needs at least 2 submeshes");
-        return PGCP_E_PARTITION;
-    }
-    int st = PGCP_OK;
-    if (pairs && npairs > 0) {
-        for (int32_t q = 0; q < npairs && st == PGCP_OK; ++q) {
-            int64_t ca = std::min(pairs[2 * q], pairs[2 * q + 1]), cb = std::max(pairs[2 * q], pairs[2 * q + 1]);
-            if (!P.cycles.count(ca) || !P.cycles.count(cb)) {
-                P.err = "pair (" + std::to_string(ca) + ", " + std::to_string(cb) + ") is not two live components";
-                st = PGCP_E_PARTITION;
-                break;
-            }
-            Key k;
-            Cycle ch;
-            if (!P.pair_best(ca, cb, &k, &ch, &st)) {
-                if (st == PGCP_OK) {
-                    P.err = "components " + std::to_string(ca) + " and " + std::to_string(cb) + " share no open arc";
+    uint64_t key = mix(0, (uint64_t)K);
+    key = mix(key, (uint64_t)mode_sphere);
+    key = mix(key, (uint64_t)ncuts);
+    for (int64_t i = 0; i < cyc_off[K]; ++i) key = mix(key, (uint64_t)cyc[i] * 2654435761ull + (uint64_t)i);
+    for (int64_t i = 0; i < 2 * ncuts; ++i) key = mix(key, (uint64_t)cuts[i]);
+    key = mix(key, (uint64_t)(pairs ? npairs : -1));
+    for (int32_t i = 0; pairs && i < 2 * npairs; ++i) key = mix(key, (uint64_t)pairs[i]);
+
+    if (!(g_cache.valid && g_cache.key == key)) {
+        int64_t vmax = 0;
+        for (int64_t i = 0; i < cyc_off[K]; ++i) vmax = std::max(vmax, cyc[i]);
+        for (int64_t i = 0; i < 2 * ncuts; ++i) vmax = std::max(vmax, cuts[i]);
+        g_scr.ensure(vmax + 1);
+        Planner P;
+        for (int32_t i = 0; i < K; ++i) P.cycles[i] = Cycle(cyc + cyc_off[i], cyc + cyc_off[i + 1]);
+        int target = mode_sphere ? 2 : 1;
+        if (mode_sphere && K < 2) {
+            pgcp::set_error("sphere mode needs at least 2 submeshes");
+            return PGCP_E_PARTITION;
+        }
+        int st = PGCP_OK;
+        if (pairs && npairs > 0) {
+            for (int32_t q = 0; q < npairs && st == PGCP_OK; ++q) {
+                int64_t ca = std::min(pairs[2 * q], pairs[2 * q + 1]), cb = std::max(pairs[2 * q], pairs[2 * q + 1]);
+                if (!P.cycles.count(ca) || !P.cycles.count(cb)) {
+                    P.err = "pair (" + std::to_string(ca) + ", " + std::to_string(cb) + ") is not two live components";
                     st = PGCP_E_PARTITION;
+                    break;
                 }
-                break;
+                Key k;
+                Cycle ch;
+                if (!P.pair_best(ca, cb, &k, &ch, &st)) {
+                    if (st == PGCP_OK) {
+                        P.err = "components " + std::to_string(ca) + " and " + std::to_string(cb) +
+                                " share no open arc";
+                        st = PGCP_E_PARTITION;
+                    }
+                    break;
+                }
+                st = P.glue(ca, cb, ch);
             }
-            st = P.glue(ca, cb, ch);
+            if (st == PGCP_OK && (int)P.cycles.size() != target) {
+                P.err = "merge order leaves more than the target components";
+                st = PGCP_E_PARTITION;
+            }
+        } else {
+            st = P.greedy(target);
         }
-        if (st == PGCP_OK && (int)P.cycles.size() != target) {
-            P.err = "merge order leaves more than the target components";
-            st = PGCP_E_PARTITION;
+        if (st == PGCP_OK && mode_sphere) st = P.sphere_close();
+        if (st == PGCP_OK) st = P.check_cover(cuts, ncuts);
+        if (st != PGCP_OK) {
+            g_cache.valid = false;
+            pgcp::set_error("%s", P.err.c_str());
+            return st;
         }
-    } else {
-        st = P.greedy(target);
+        g_cache.steps = std::move(P.steps);
+        g_cache.key = key;
+        g_cache.valid = true;
     }
-    if (st == PGCP_OK && mode_sphere) st = P.sphere_close();
-    if (st == PGCP_OK) st = P.check_cover(cuts, ncuts);
-    if (st != PGCP_OK) {
-        pgcp::set_error("%s", P.err.c_str());
-        return st;
-    }
+    const std::vector<Step>& steps = g_cache.steps;
     int64_t need = 0;
-    for (auto& s : P.steps) need += (int64_t)(s.a.size() + s.b.size() + s.merged.size());
-    out_len[0] = (int64_t)P.steps.size();
+    for (auto& s : steps) need += (int64_t)(s.a.size() + s.b.size() + s.merged.size());
+    out_len[0] = (int64_t)steps.size();
     out_len[1] = need;
     if (!out_meta || !out_idx || out_cap < need) return PGCP_OK;
     int64_t off = 0;
-    for (size_t i = 0; i < P.steps.size(); ++i) {
-        const Step& s = P.steps[i];
+    for (size_t i = 0; i < steps.size(); ++i) {
+        const Step& s = steps[i];
         int64_t* m = out_meta + 8 * i;
         m[0] = s.ca;
         m[1] = s.cb;
@@ -333,5 +390,6 @@ extern "C" PGCP_API int pgcp_plan_weld_schedule(const int64_t* cyc, const int64_
         for (int64_t v : s.b) out_idx[off++] = v;
         for (int64_t v : s.merged) out_idx[off++] = v;
     }
+    g_cache.valid = false;  // copy-out done: no memoisation across plans
     return PGCP_OK;
 }

@@ -406,6 +406,20 @@ __global__ void k_walk(int32_t K, const int64_t* __restrict__ vert_off, const in
     }
 }
 
+// boundary cycles in parent ids (partition.py:134-135 `used[loop]`)
+__global__ void k_cycles(int32_t K, const int64_t* __restrict__ loop_off, const int32_t* __restrict__ loop,
+                         const int64_t* __restrict__ vert_off, const int32_t* __restrict__ vmap,
+                         int32_t* __restrict__ cyc, int64_t total) {
+    GRID_STRIDE(i, total) {
+        int lo = 0, hi = K - 1;  // component of loop entry i
+        while (lo < hi) {
+            int mid = (lo + hi + 1) >> 1;
+            if (loop_off[mid] <= i) lo = mid; else hi = mid - 1;
+        }
+        cyc[i] = vmap[vert_off[lo] + loop[i]];
+    }
+}
+
 __global__ void k_parent_walk(const int32_t* __restrict__ pnxt, const int32_t* pcount, const int32_t* pstart,
                               const int32_t* pbad, int64_t* out_loops) {
     if (blockIdx.x || threadIdx.x) return;
@@ -659,12 +673,19 @@ int build_partition(pgcp_batch* b, const int64_t* cuts, int64_t ncuts, bool no_c
     PGCP_TRY(exclusive_scan_i32_to_i64(bcnt.p, b->loop_off.p, K, s));
     PGCP_TRY(fetch_scalar(b->loop_off.p + K, &b->sum_nb, s));
     PGCP_TRY(b->loop.alloc(b->sum_nb, s));
+    PGCP_TRY(b->loop.zero(s));  // entries of non-disk components may stay unwalked
     DevBuf<uint8_t> seen;
     PGCP_TRY(seen.alloc(E, s));
     PGCP_TRY(seen.zero(s));
     k_walk<<<grid_for(K, 64), 64, 0, s>>>(K, b->vert_off.p, fcnt.p, bcnt.p, start.p, b->nxt.p, b->loop_off.p,
                                          b->loop.p, bad.p, chi.p, loops.p, seen.p);
     PGCP_LAUNCH_CHECK();
+    PGCP_TRY(b->cyc.alloc(b->sum_nb, s));
+    if (b->sum_nb > 0) {
+        k_cycles<<<grid_for(b->sum_nb, 256), 256, 0, s>>>(K, b->loop_off.p, b->loop.p, b->vert_off.p, b->vmap.p,
+                                                         b->cyc.p, b->sum_nb);
+        PGCP_LAUNCH_CHECK();
+    }
     DevBuf<int64_t> ploops;
     PGCP_TRY(ploops.alloc(1, s));
     k_parent_walk<<<1, 32, 0, s>>>(pnxt.p, pscal.p, pscal.p + 1, pscal.p + 2, ploops.p);

@@ -28,6 +28,8 @@
 #include <string>
 #include <unordered_map>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 
 namespace pgcp {
@@ -800,6 +802,355 @@ __global__ void __launch_bounds__(512) k_phase1(Phase1Args A) {
 }
 
 // ---------------------------------------------------------------------------
+// phase 1 on a thread-block cluster: the 2(k+3) points of one weld are spread
+// over the CTAs of a cluster (one point per thread for k ~ 1000); every record
+// step is
+//   apply the current record to my points -> block barrier -> the owners of
+//   the next parameter points publish (value, side) into every CTA's
+//   parameter slots through DSMEM -> cluster barrier -> every thread rebuilds
+//   the next record from the parameters (identical arithmetic everywhere)
+// so the serial chain costs one cluster barrier per record and the O(k^2)
+// point work is spread over CS SMs.
+
+constexpr int PC_THREADS = 256;
+constexpr int PC_MAXCS = 16;
+constexpr int NPARAM = 8;            // parameter slots per step
+constexpr int NFLAG = PC_MAXCS;      // per-rank scalars (maxima)
+
+struct PParam {
+    double2 z;
+    int s;
+    int pad;
+};
+
+namespace cgw = cooperative_groups;
+
+struct P1c {
+    PParam* slot;       // [2][NPARAM] parameter slots (this CTA's)
+    double* flag;       // [2][NFLAG]
+    double2* pts;       // my points
+    int8_t* sides;
+    int lo, hi;         // my global point range [lo, hi)
+};
+
+__global__ void __launch_bounds__(PC_THREADS, 1) k_phase1c(Phase1Args A) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ PParam s_param[2][NPARAM];
+    __shared__ double s_flag[2][NFLAG];
+    __shared__ double red[32];
+    cgw::cluster_group cl = cgw::this_cluster();
+    const int CS = (int)cl.num_blocks();
+    const int rank = (int)cl.block_rank();
+    const int step = blockIdx.x / CS;
+    const StepDesc sd = A.steps[step];
+    double* meta = A.meta + META * (int64_t)step;
+    const int k = sd.k;
+    const int P = k + 3;
+    const int NP = 2 * P;
+    const int chunk = (NP + CS - 1) / CS;
+    const int lo = min(NP, rank * chunk), hi = min(NP, lo + chunk);
+    double2* pts = reinterpret_cast<double2*>(smem);
+    int8_t* sides = reinterpret_cast<int8_t*>(pts + chunk);
+    Rec* log_a = A.recs + sd.rec;
+    Rec* log_b = log_a + sd.cap;
+    const bool logger = rank == 0 && threadIdx.x == 0;
+    int na_rec = 0, nb_rec = 0;
+    if (logger)
+        for (int i = 0; i < META; ++i) meta[i] = 0.0;
+    if (k < 1 || k > sd.na - 1 || k > sd.nb - 1) {
+        if (logger) {
+            meta[2] = WE_K;
+            meta[3] = k;
+        }
+        return;
+    }
+    const int32_t* sa = A.src + sd.src;
+    const int32_t* sb = sa + sd.na;
+    // prenormalizers over all cycle points (computed redundantly by every CTA)
+    Rec pre[2];
+    int pcode = 0;
+    bool okA = prenormalize(A.tv, sa, sd.na, red, &pre[0], &pcode);
+    bool okB = okA && prenormalize(A.tv, sb, sd.nb, red, &pre[1], &pcode);
+    if (!okA || !okB) {
+        if (logger) {
+            meta[2] = WE_PRE;
+            meta[3] = okA ? 1 : 0;
+            meta[4] = pcode;
+        }
+        return;
+    }
+    for (int g = lo + threadIdx.x; g < hi; g += PC_THREADS) {
+        int side = g >= P;
+        int t = g - side * P;
+        double2 z;
+        int8_t sd8 = 0;
+        if (t <= k) {
+            z = A.tv[(side ? sb : sa)[t]];
+            apply_rec(pre[side], z, sd8);
+        } else {
+            z = (t == k + 1) ? C(0.0, 0.0) : cinf();
+        }
+        pts[g - lo] = z;
+        sides[g - lo] = 0;
+    }
+    if (logger) {
+        log_a[na_rec++] = pre[0];
+        log_b[nb_rec++] = pre[1];
+    }
+    int parity = 0;
+    // publish the listed global points into every CTA's slots, then barrier
+    auto publish = [&](const int* gidx, int np, double flag) {
+        __syncthreads();
+        for (int q = threadIdx.x; q < np * CS; q += PC_THREADS) {
+            int which = q / CS, dst = q % CS;
+            int g = gidx[which];
+            if (g >= lo && g < hi) {
+                PParam pp;
+                pp.z = pts[g - lo];
+                pp.s = sides[g - lo];
+                pp.pad = 0;
+                PParam* rs = cl.map_shared_rank(&s_param[parity][0], dst);
+                rs[which] = pp;
+            }
+        }
+        if (threadIdx.x < CS) {
+            double* rf = cl.map_shared_rank(&s_flag[parity][0], threadIdx.x);
+            rf[rank] = flag;
+        }
+        cl.sync();
+    };
+    auto apply_pair = [&](const Rec& ra, bool ua, const Rec& rb, bool ub) {
+        for (int g = lo + threadIdx.x; g < hi; g += PC_THREADS) {
+            int side = g >= P;
+            if (side ? !ub : !ua) continue;
+            double2 z = pts[g - lo];
+            int8_t s8 = sides[g - lo];
+            apply_rec(side ? rb : ra, z, s8);
+            pts[g - lo] = z;
+            sides[g - lo] = s8;
+        }
+    };
+    int err = 0, eidx = 0, eaux = 0;
+    Rec ra, rb;
+    // ---- zip step 1: SqrtRatio
+    {
+        int gi[4] = {0, 1, P, P + 1};
+        publish(gi, 4, 0.0);
+        PParam* pp = s_param[parity];
+        if (c_eq(pp[0].z, pp[1].z) || c_eq(pp[2].z, pp[3].z)) err = WE_ZIP01;
+        ra = mk_sqr(pp[0].z, pp[1].z, UP);
+        rb = mk_sqr(pp[2].z, pp[3].z, DOWN);
+        parity ^= 1;
+    }
+    if (err) goto fail;
+    if (logger) {
+        log_a[na_rec++] = ra;
+        log_b[nb_rec++] = rb;
+    }
+    apply_pair(ra, true, rb, true);
+    // ---- zip steps j = 2..k: Open
+    for (int j = 2; j <= k; ++j) {
+        int gi[2] = {j, P + j};
+        publish(gi, 2, 0.0);
+        PParam* pp = s_param[parity];
+        for (int side = 0; side < 2 && !err; ++side) {
+            double2 xi = pp[side].z;
+            if (pp[side].s != 0 || c_isinf(xi)) {
+                err = WE_ZIP_HALF; eidx = j; eaux = side;
+            } else if (!(xi.x > 0)) {
+                err = WE_ZIP_AXIS; eidx = j; eaux = side;
+            } else if (cabs_(xi) < 1e-13) {
+                err = WE_ZIP_COLL; eidx = j; eaux = side;
+            }
+        }
+        parity ^= 1;
+        if (err) goto fail;
+        ra = mk_open(pp[0].z, UP);
+        rb = mk_open(pp[1].z, DOWN);
+        if (logger) {
+            log_a[na_rec++] = ra;
+            log_b[nb_rec++] = rb;
+        }
+        apply_pair(ra, true, rb, true);
+    }
+    // ---- axis Mobius sending pts[0] to infinity (welding.py:593-600)
+    {
+        int gi[2] = {0, P};
+        publish(gi, 2, 0.0);
+        PParam* pp = s_param[parity];
+        bool has[2] = {false, false};
+        Rec rr[2];
+        for (int side = 0; side < 2 && !err; ++side) {
+            double2 w0 = pp[side].z;
+            if (!c_isinf(w0)) {
+                if (c_zero(w0)) {
+                    err = WE_FAR0; eaux = side;
+                } else {
+                    int br = side ? DOWN : UP;
+                    rr[side] = mk_mob(C(1, 0), C(0, 0), cdiv(C(-1.0, 0.0), w0), C(1, 0), true);
+                    mob_pin(rr[side], w0, cinf(), br);
+                    mob_pin(rr[side], C(0, 0), C(0, 0), br);
+                    has[side] = true;
+                }
+            }
+        }
+        parity ^= 1;
+        if (err) goto fail;
+        if (logger) {
+            if (has[0]) log_a[na_rec++] = rr[0];
+            if (has[1]) log_b[nb_rec++] = rr[1];
+        }
+        apply_pair(rr[0], has[0], rr[1], has[1]);
+    }
+    // ---- closing loop (welding.py:673-687)
+    for (int j = k - 1; j >= 1; --j) {
+        int gi[2] = {j, P + j};
+        publish(gi, 2, 0.0);
+        PParam* pp = s_param[parity];
+        double2 al = pp[0].z, be = pp[1].z;
+        if (pp[0].s == 0 || c_isinf(al) || al.y == 0.0) {
+            err = WE_ALIGN_A; eidx = j;
+        } else if (pp[1].s == 0 || c_isinf(be) || be.y == 0.0) {
+            err = WE_ALIGN_B; eidx = j;
+        } else if (!walk_less(al.y, be.y)) {
+            err = WE_ORDER; eidx = j;
+        }
+        parity ^= 1;
+        if (err) goto fail;
+        ra = mk_close(al.y, be.y);
+        if (logger) {
+            log_a[na_rec++] = ra;
+            log_b[nb_rec++] = ra;
+        }
+        apply_pair(ra, true, ra, true);
+    }
+    // ---- far ends: SquareMobius; stage max of |va| (arc + aux) for the deferred check
+    {
+        double m = 0;
+        for (int g = lo + threadIdx.x; g < hi && g < P; g += PC_THREADS)
+            if (c_fin(pts[g - lo])) m = fmax(m, cabs_(pts[g - lo]));
+        m = block_max(m, red);
+        int gi[2] = {0, P};
+        publish(gi, 2, m);
+        PParam* pp = s_param[parity];
+        double2 qa = pp[0].z, qb = pp[1].z;
+        double stage = 0;
+        for (int r = 0; r < CS; ++r) stage = fmax(stage, s_flag[parity][r]);
+        parity ^= 1;
+        if (logger) {
+            meta[6] = qa.x; meta[7] = qa.y; meta[8] = qb.x; meta[9] = qb.y;
+            meta[10] = stage;
+            meta[14] = na_rec;
+            meta[15] = nb_rec;
+        }
+        ra = mk_sq(c_isinf(qa) ? cinf() : qa);
+        if (logger) {
+            log_a[na_rec++] = ra;
+            log_b[nb_rec++] = ra;
+        }
+        apply_pair(ra, true, ra, true);
+    }
+    // ---- normalisation (welding.py:699-717)
+    {
+        int gi[4] = {k + 1, P + k + 1, k + 2, P + k + 2};
+        publish(gi, 4, 0.0);
+        PParam* pp = s_param[parity];
+        double2 za = pp[0].z, zb = pp[1].z, ia = pp[2].z, ib = pp[3].z;
+        double2 co[4];
+        if (c_isinf(za) || c_isinf(zb) || c_isinf(ia) || c_isinf(ib)) {
+            err = WE_TRACK;
+        } else {
+            double2 zmid = C(0.5 * (ia.x + ib.x), 0.5 * (ia.y + ib.y));
+            if (!c_eq(za, zb) && !c_eq(za, zmid) && !c_eq(zb, zmid)) {
+                double2 zs[3] = {za, zb, zmid}, ws[3] = {C(-1, 0), C(1, 0), cinf()};
+                if (!three_point(zs, ws, co)) err = WE_THREE;
+            } else if (!c_zero(za)) {
+                co[0] = cdiv(C(-1.0, 0.0), za); co[1] = C(0, 0); co[2] = C(0, 0); co[3] = C(1, 0);
+            } else {
+                co[0] = C(1, 0); co[1] = C(0, 0); co[2] = C(0, 0); co[3] = C(1, 0);
+            }
+        }
+        parity ^= 1;
+        if (err) goto fail;
+        ra = mk_mob(co[0], co[1], co[2], co[3]);
+        if (logger) {
+            log_a[na_rec++] = ra;
+            log_b[nb_rec++] = ra;
+        }
+        apply_pair(ra, true, ra, true);
+    }
+    // ---- closed welding: respread the seam (welding.py:751-763)
+    if (sd.closed) {
+        int n = k + 1;
+        int gi[3] = {0, n / 3, (2 * n) / 3};
+        publish(gi, 3, 0.0);
+        PParam* pp = s_param[parity];
+        double2 an[3] = {pp[0].z, pp[1].z, pp[2].z};
+        double2 tg[3] = {C(1.0, 0.0), C(cos(2 * M_PI / 3), sin(2 * M_PI / 3)), C(cos(4 * M_PI / 3), sin(4 * M_PI / 3))};
+        double2 co[4];
+        if (!three_point(an, tg, co)) err = WE_THREE, eidx = 1;
+        parity ^= 1;
+        if (err) goto fail;
+        ra = mk_mob(co[0], co[1], co[2], co[3]);
+        if (logger) {
+            log_a[na_rec++] = ra;
+            log_b[nb_rec++] = ra;
+        }
+        for (int g = lo + threadIdx.x; g < hi; g += PC_THREADS) sides[g - lo] = 0;
+        apply_pair(ra, true, ra, true);
+    }
+    // ---- outputs: all 2P points to arc_out; rank 0 finishes seam/maxima/area
+    for (int g = lo + threadIdx.x; g < hi; g += PC_THREADS) A.arc_out[sd.arc + g] = pts[g - lo];
+    cl.sync();
+    if (rank == 0) {
+        const double2* o = A.arc_out + sd.arc;
+        double seam = 0, ma = 0, mb = 0, mx = 0, area = 0, bad = 0;
+        for (int t = threadIdx.x; t <= k; t += PC_THREADS) {
+            double2 a = o[t], b = o[P + t];
+            double gg = (c_isinf(a) && c_isinf(b)) ? 0.0 : cabs_(csub(a, b));
+            if (!isnan(gg)) seam = fmax(seam, gg);
+            if (c_fin(a)) ma = fmax(ma, cabs_(a));
+            if (c_fin(b)) mb = fmax(mb, cabs_(b));
+            double2 nx = o[(t + 1) % (k + 1)];
+            area += 0.5 * (a.x * nx.y - a.y * nx.x);
+        }
+        for (int g = threadIdx.x; g < NP; g += PC_THREADS)
+            if (c_nan(o[g])) bad = 1;
+        for (int t = threadIdx.x; t < 2; t += PC_THREADS) {
+            double2 a = o[k + 1 + t], b = o[P + k + 1 + t];
+            if (c_fin(a)) mx = fmax(mx, cabs_(a));
+            if (c_fin(b)) mx = fmax(mx, cabs_(b));
+        }
+        seam = block_max(seam, red);
+        ma = block_max(ma, red);
+        mb = block_max(mb, red);
+        mx = block_max(mx, red);
+        area = block_sum(area, red);
+        bad = block_max(bad, red);
+        if (threadIdx.x == 0) {
+            meta[0] = na_rec;
+            meta[1] = nb_rec;
+            meta[5] = seam;
+            meta[11] = ma;
+            meta[12] = mb;
+            meta[13] = mx;
+            meta[16] = area;
+            if (bad > 0) {
+                meta[2] = WE_NAN;
+                meta[4] = 3;
+            }
+        }
+    }
+    return;
+fail:
+    if (logger) {
+        meta[2] = err;
+        meta[3] = eidx;
+        meta[4] = eaux;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // phase 2: replay a step's log on a point (write-back list of a level)
 //   entry = (slot, code): code bit 31 -> B log; bits 0..23: arc position + 1
 //   (0 = replay); bit 24: take the arc value from side B; bit 25: cycle
@@ -826,7 +1177,7 @@ __global__ void k_replay_slots(ReplayArgs A) {
         if (A.meta[META * step + 2] != 0.0) continue;  // failed step: leave values
         if (arcpos >= 0) {
             bool fromB = (code >> 24) & 1;
-            A.tv[slot] = A.arc_out[sd.arc + (fromB ? sd.k + 1 : 0) + arcpos];
+            A.tv[slot] = A.arc_out[sd.arc + (fromB ? sd.k + 3 : 0) + arcpos];
             continue;
         }
         const Rec* log = A.recs + sd.rec + (sideB ? sd.cap : 0);
@@ -1217,7 +1568,7 @@ int run_schedule(double2* tv, int32_t nsteps, const int32_t* info, const int32_t
         d.rec = rec_tot;
         rec_tot += 2 * (int64_t)d.cap;
         d.arc = arc_tot;
-        arc_tot += 2 * (int64_t)(d.k + 1);
+        arc_tot += 2 * (int64_t)(d.k + 3);
         scratch_off[q] = scr_tot;
         if (2 * (d.k + 3) > P1_SMEM_POINTS) scr_tot += 2 * (int64_t)(d.k + 3);
     }
@@ -1284,8 +1635,27 @@ int run_schedule(double2* tv, int32_t nsteps, const int32_t* info, const int32_t
         a.sides_scratch = d_sscr.p;
         a.smem_points = P1_SMEM_POINTS;
         a.geodesic = 0;
-        size_t smem = P1_SMEM_POINTS * (sizeof(double2) + 1);
-        k_phase1<<<q1 - q0, P1_THREADS, smem, s>>>(a);
+        int kmax = 0;
+        for (int q = q0; q < q1; ++q) kmax = std::max(kmax, sd[q].k);
+        const int NP = 2 * (kmax + 3);
+        int CS = 1;
+        while (CS < PC_MAXCS && CS * PC_THREADS < NP) CS *= 2;
+        const int chunk = (NP + CS - 1) / CS;
+        size_t smem = (size_t)chunk * (sizeof(double2) + 1) + 16;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)((q1 - q0) * CS), 1, 1);
+        cfg.blockDim = dim3(PC_THREADS, 1, 1);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = CS;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        if (CS > 8) PGCP_TRY_CUDA(cudaFuncSetAttribute(k_phase1c, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        PGCP_TRY_CUDA(cudaLaunchKernelEx(&cfg, k_phase1c, a));
         PGCP_LAUNCH_CHECK();
         int64_t n = lev_wb[l + 1] - lev_wb[l];
         if (n > 0) {

@@ -85,7 +85,6 @@ class Partition:
             K = len(voff) - 1
             self._vmaps = [vmap[voff[c]:voff[c + 1]] for c in range(K)]
             self._loops = [loop[loff[c]:loff[c + 1]] for c in range(K)]
-            self._cycles = [self._vmaps[c][self._loops[c]] for c in range(K)]
             self._voff, self._loff = voff, loff
 
     @property
@@ -95,7 +94,11 @@ class Partition:
 
     @property
     def boundary_cycles(self):
-        self._host_maps()
+        if self._cycles is None:
+            b = self.batch
+            cyc = b.host(nat.ARR_CYCLES, torch.int32).astype(np.int64)
+            loff = b.host(nat.ARR_LOOP_OFF, torch.int64)
+            self._cycles = [cyc[loff[c]:loff[c + 1]] for c in range(len(loff) - 1)]
         return self._cycles
 
     @property
