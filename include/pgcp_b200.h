@@ -233,7 +233,7 @@ PGCP_API int pgcp_polygon_interior(const double* tv, const int32_t* src, int32_t
                                    void* stream);
 
 /* z[idx[i]] = add + 1/(z[idx[i]] - sub): sphere-mode exterior inversion
- * (pipeline.py:253, 262). idx device int32 or NULL. */
+ * (pipeline.py:254, 263). idx device int32 or NULL. */
 PGCP_API int pgcp_inv_shift(double* z, const int32_t* idx, int64_t n, double add_re, double add_im,
                             double sub_re, double sub_im, void* stream);
 

@@ -165,6 +165,9 @@ class DeviceBatch:
         carr, nc, nslot = self._comps(comps)
         z = out if out is not None else torch.zeros(self.info()[nat.INFO_SUM_N], dtype=torch.complex128,
                                                     device=device())
+        if comps is not None and nc == 0:  # an empty shard (more ranks than submeshes)
+            self.last_stats = []
+            return z, []
         parr = None
         if pins is not None:
             flat = np.asarray(pins, dtype=np.int32).ravel()
@@ -186,6 +189,9 @@ class DeviceBatch:
         fv = to_dev(fixed_val, torch.complex128)
         z = out if out is not None else torch.zeros(self.info()[nat.INFO_SUM_N], dtype=torch.complex128,
                                                     device=device())
+        if comps is not None and nc == 0:
+            self.last_stats = []
+            return z, []
         stats = (nat.SolveStat * max(nslot, 1))()
         st = nat.lib().pgcp_batch_harmonic(self.h, carr, nc, ptr(fg), ptr(fv), int(fg.numel()),
                                            ctypes.byref(self._opts(rtol, contract_tol, maxit, cluster)), ptr(z),

@@ -191,11 +191,14 @@ def _poly_area(z):
 
 
 def parameterize(mesh, cuts=None, mode="free", workers=1, seed=0, mobius_area=False, config=None,
-                 schedule=None, pairs=None, keep_device=False):
+                 schedule=None, pairs=None, keep_device=False, shard=None):
     """Global conformal parameterization (pipeline.py:119-271) on the device.
 
     Same signature and results as the reference; `schedule`/`pairs` select
-    the documented balanced weld order (config.schedule="pairs")."""
+    the documented balanced weld order (config.schedule="pairs"). `shard`
+    (dist.Shard) splits the flatten/harmonic solves across ranks: each rank
+    solves its own subdomains and one sum-all-reduce per stage assembles the
+    boundary values / embeddings (dist.py)."""
     from .device import DeviceBatch, device, require_cuda
     require_cuda()
     cfg = config or RunConfig(mode=mode, workers=workers, seed=seed, mobius_area=mobius_area)
@@ -248,11 +251,15 @@ def parameterize(mesh, cuts=None, mode="free", workers=1, seed=0, mobius_area=Fa
     voff = batch.host(nat.ARR_VERT_OFF, torch.int64)
     report.submesh_sizes = [int(x) for x in np.diff(voff)]
 
+    own = shard.comps(report.submesh_sizes) if (shard is not None and K > 1) else None
+
     # ---- local free-boundary flattening (all submeshes, one launch) -----------
     clk.start()
-    z0, fst = batch.flatten(rtol=cfg.rtol, cluster=cfg.cluster)
+    z0, fst = batch.flatten(comps=own, rtol=cfg.rtol, cluster=cfg.cluster)
     clk.stop("flatten")
     report.solver = {"flatten_iters": [s["iters"] for s in fst], "flatten": batch.last_solve(0)}
+    if own is not None:
+        report.solver["shard"] = own
 
     if K == 1 and mode == "free":
         embeddings = z0
@@ -265,6 +272,8 @@ def parameterize(mesh, cuts=None, mode="free", workers=1, seed=0, mobius_area=Fa
         loop_gid = torch.as_tensor((voff[plan.slot_sub] + loop_local).astype(np.int32)).to(dev)
         tv = torch.empty(len(plan.slot_parent), dtype=torch.complex128, device=dev)
         nat.check(nat.lib().pgcp_gather_complex(_ptr(z0), _ptr(loop_gid), _ptr(tv), tv.numel(), _stream()))
+        if own is not None:
+            shard.sum_(tv)  # boundary values of the other ranks' subdomains (zeros here)
         out = None
         if len(steps):
             out, _ = run_schedule(tv, plan.info, plan.src, plan.wb_off, plan.wb, cfg.hard_tol)
@@ -294,9 +303,11 @@ def parameterize(mesh, cuts=None, mode="free", workers=1, seed=0, mobius_area=Fa
             ext_slots = torch.as_tensor(plan.slots_of(exterior).astype(np.int32)).to(dev)
             nat.check(nat.lib().pgcp_inv_shift(_ptr(tv), _ptr(ext_slots), ext_slots.numel(), 0.0, 0.0,
                                                center.real, center.imag, _stream()))
-        z, hst = batch.harmonic(loop_gid, tv, rtol=cfg.rtol, cluster=cfg.cluster)
+        z, hst = batch.harmonic(loop_gid, tv, comps=own, rtol=cfg.rtol, cluster=cfg.cluster)
         report.solver["harmonic_iters"] = [s["iters"] for s in hst]
         report.solver["harmonic"] = batch.last_solve(1)
+        if own is not None:
+            shard.sum_(z)
         if center is not None:
             gids = np.concatenate([np.arange(voff[i], voff[i + 1]) for i in exterior]).astype(np.int32)
             gt = torch.as_tensor(gids).to(dev)
