@@ -248,10 +248,6 @@ struct Plain {
     const double* x;
     __device__ double operator()(int64_t i) const { return x[i]; }
 };
-struct PosArea {
-    const double* x;
-    __device__ double operator()(int64_t i) const { return x[i] > 0 ? 1.0 : 0.0; }
-};
 
 __global__ void k_area_logratio(int64_t m, const double* __restrict__ a_new, const double* __restrict__ a_ref,
                                 double sum_new, double sum_ref, double* __restrict__ absd) {
@@ -262,36 +258,90 @@ __global__ void k_area_logratio(int64_t m, const double* __restrict__ a_new, con
 }
 
 // ---- radix select on non-negative doubles (bits are order-preserving)
-constexpr int RBITS = 16;
+// 12-bit digits (6 passes: shifts 52, 40, 28, 16, 4, then the last 4 bits),
+// block-private shared-memory histograms with warp-aggregated increments;
+// selections that share their prefix share one histogram.
+constexpr int RBITS = 12;
 constexpr int RBINS = 1 << RBITS;
+constexpr int NSEL = 7;
+constexpr int SEL_PASSES = 6;
+constexpr int SEL_BLOCKS = 296;
 
 struct SelState {
     unsigned long long prefix;  // selected high bits so far
     long long rank;             // remaining rank within the prefix
 };
 
-__global__ void k_sel_hist(const double* __restrict__ x, int64_t n, int pass, const SelState* __restrict__ st,
-                           int nsel, unsigned int* __restrict__ hist) {
-    const int shift = 64 - RBITS * (pass + 1);
-    GRID_STRIDE(i, n) {
-        double v = x[i];
-        if (v < 0) continue;
-        unsigned long long b = (unsigned long long)__double_as_longlong(v);
-        for (int s = 0; s < nsel; ++s) {
-            bool match = pass == 0 || ((b >> (shift + RBITS)) == (st[s].prefix >> (shift + RBITS)));
-            if (match) atomicAdd(&hist[(int64_t)s * RBINS + ((b >> shift) & (RBINS - 1))], 1u);
+__host__ __device__ inline int sel_shift(int pass) { return pass < 5 ? 64 - RBITS * (pass + 1) : 0; }
+__host__ __device__ inline int sel_width(int pass) { return pass < 5 ? RBITS : 4; }
+
+// representative (first selection with the same prefix) of selection s
+__device__ inline int sel_rep(const SelState* st, int s) {
+    for (int t = 0; t < s; ++t)
+        if (st[t].prefix == st[s].prefix) return t;
+    return s;
+}
+
+__global__ void __launch_bounds__(512) k_sel_hist(const double* __restrict__ x, int64_t n, int pass,
+                                                  const SelState* __restrict__ st, unsigned int* __restrict__ hist,
+                                                  int* __restrict__ rep_out) {
+    extern __shared__ unsigned int sh[];  // [NSEL][RBINS]
+    __shared__ unsigned long long pre[NSEL];
+    __shared__ int rep[NSEL];
+    const int shift = sel_shift(pass);
+    const int width = sel_width(pass);
+    const int nb = 1 << width;
+    if (threadIdx.x < NSEL) {
+        pre[threadIdx.x] = st[threadIdx.x].prefix;
+        rep[threadIdx.x] = sel_rep(st, threadIdx.x);
+        if (blockIdx.x == 0) rep_out[threadIdx.x] = rep[threadIdx.x];
+    }
+    for (int i = threadIdx.x; i < NSEL * RBINS; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+    const int hs = shift + width;  // bits above the current digit
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t n_round = (n + 31) & ~(int64_t)31;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_round; i += stride) {
+        double v = i < n ? x[i] : -1.0;
+        bool ok = v >= 0;
+        unsigned long long b = ok ? (unsigned long long)__double_as_longlong(v) : 0ull;
+        int digit = (int)((b >> shift) & (unsigned long long)(nb - 1));
+        for (int s = 0; s < NSEL; ++s) {
+            if (rep[s] != s) continue;
+            bool m = ok && (hs >= 64 || (b >> hs) == (pre[s] >> hs));
+            unsigned int act = __ballot_sync(0xffffffffu, m);
+            if (!act) continue;
+            if (m) {
+                unsigned int peers = __match_any_sync(act, digit);
+                if (lane == __ffs(peers) - 1) atomicAdd(&sh[s * RBINS + digit], (unsigned int)__popc(peers));
+            }
+        }
+    }
+    __syncthreads();
+    for (int s = 0; s < NSEL; ++s) {
+        if (rep[s] != s) continue;
+        for (int i = threadIdx.x; i < nb; i += blockDim.x) {
+            unsigned int c = sh[s * RBINS + i];
+            if (c) atomicAdd(&hist[s * RBINS + i], c);
         }
     }
 }
 
-__global__ void k_sel_pick(int pass, SelState* st, const unsigned int* __restrict__ hist) {
-    // one block per selection; serial scan by thread 0 over chunk sums
+__global__ void k_sel_pick(int pass, SelState* st, const unsigned int* __restrict__ hist,
+                           const int* __restrict__ rep) {
+    // one block per selection; chunk sums, then a serial scan by thread 0
     __shared__ unsigned long long chunk[256];
     const int s = blockIdx.x;
-    const unsigned int* h = hist + (int64_t)s * RBINS;
-    const int per = RBINS / 256;
+    const int width = sel_width(pass);
+    const int nb = 1 << width;
+    const unsigned int* h = hist + (int64_t)rep[s] * RBINS;
+    const int per = (nb + 255) / 256;
     unsigned long long t = 0;
-    for (int i = 0; i < per; ++i) t += h[threadIdx.x * per + i];
+    for (int i = 0; i < per; ++i) {
+        int j = threadIdx.x * per + i;
+        if (j < nb) t += h[j];
+    }
     chunk[threadIdx.x] = t;
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -302,14 +352,54 @@ __global__ void k_sel_pick(int pass, SelState* st, const unsigned int* __restric
             ++c;
         }
         int d = c * per;
-        while (d < RBINS - 1 && r >= (long long)h[d]) {
+        while (d < nb - 1 && r >= (long long)h[d]) {
             r -= h[d];
             ++d;
         }
-        const int shift = 64 - RBITS * (pass + 1);
-        st[s].prefix |= ((unsigned long long)d) << shift;
+        st[s].prefix |= ((unsigned long long)d) << sel_shift(pass);
         st[s].rank = r;
     }
+}
+
+// np.histogram with explicit edges: bin j holds edges[j] <= v < edges[j+1],
+// the last bin also v == edges[nb]. Edges and counts in shared memory
+// (nb <= HIST_SMEM_BINS), warp-aggregated increments, one global add per
+// non-empty bin per block.
+constexpr int HIST_SMEM_BINS = 3072;
+
+__device__ inline int hist_bin(const double* e, int nb, double v) {
+    if (!(v >= e[0]) || v > e[nb]) return -1;
+    int lo = 0, hi = nb;  // largest j with e[j] <= v
+    while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if (e[mid] <= v) lo = mid; else hi = mid - 1;
+    }
+    return lo >= nb ? nb - 1 : lo;
+}
+
+__global__ void __launch_bounds__(512) k_hist_bins_smem(const double* __restrict__ x, int64_t n,
+                                                        const double* __restrict__ edges, int nb,
+                                                        unsigned long long* __restrict__ counts) {
+    __shared__ double se[HIST_SMEM_BINS + 1];
+    __shared__ unsigned int sc[HIST_SMEM_BINS];
+    for (int i = threadIdx.x; i <= nb; i += blockDim.x) se[i] = edges[i];
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) sc[i] = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t n_round = (n + 31) & ~(int64_t)31;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_round; i += stride) {
+        double v = i < n ? x[i] : -1.0;
+        int bin = v >= 0 ? hist_bin(se, nb, v) : -1;
+        unsigned int act = __ballot_sync(0xffffffffu, bin >= 0);
+        if (bin >= 0) {
+            unsigned int peers = __match_any_sync(act, bin);
+            if (lane == __ffs(peers) - 1) atomicAdd(&sc[bin], (unsigned int)__popc(peers));
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < nb; i += blockDim.x)
+        if (sc[i]) atomicAdd(&counts[i], (unsigned long long)sc[i]);
 }
 
 __global__ void k_hist_bins(const double* __restrict__ x, int64_t n, const double* __restrict__ edges, int nb,
@@ -317,15 +407,8 @@ __global__ void k_hist_bins(const double* __restrict__ x, int64_t n, const doubl
     GRID_STRIDE(i, n) {
         double v = x[i];
         if (v < 0) continue;
-        // searchsorted semantics of np.histogram with explicit edges
-        if (v < edges[0] || v > edges[nb]) continue;
-        int lo = 0, hi = nb;  // largest j with edges[j] <= v
-        while (lo < hi) {
-            int mid = (lo + hi + 1) >> 1;
-            if (edges[mid] <= v) lo = mid; else hi = mid - 1;
-        }
-        if (lo >= nb) lo = nb - 1;
-        atomicAdd(&counts[lo], 1ull);
+        int bin = hist_bin(edges, nb, v);
+        if (bin >= 0) atomicAdd(&counts[bin], 1ull);
     }
 }
 
@@ -386,14 +469,23 @@ int summarize_dev(const double* x, int64_t n, double* out4, int64_t* count, DevB
     for (int q = 0; q < 7; ++q) hs[q] = {0ull, (long long)ranks[q]};
     DevBuf<SelState> st;
     DevBuf<unsigned int> hist;
+    DevBuf<int> rep;
+    PGCP_TRY(rep.alloc(NSEL, s));
     PGCP_TRY(st.alloc(7, s));
-    PGCP_TRY(hist.alloc(7 * (int64_t)RBINS, s));
+    PGCP_TRY(hist.alloc(NSEL * (int64_t)RBINS, s));
     PGCP_TRY_CUDA(cudaMemcpyAsync(st.p, hs, sizeof hs, cudaMemcpyHostToDevice, s));
-    for (int pass = 0; pass < 64 / RBITS; ++pass) {
+    const size_t smem = NSEL * RBINS * sizeof(unsigned int);
+    static bool attr = false;
+    if (!attr) {
+        PGCP_TRY_CUDA(cudaFuncSetAttribute(k_sel_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    const int blocks = (int)std::min<int64_t>(SEL_BLOCKS, (n + 511) / 512);
+    for (int pass = 0; pass < SEL_PASSES; ++pass) {
         PGCP_TRY(hist.zero(s));
-        k_sel_hist<<<grid_for(n, 256), 256, 0, s>>>(x, n, pass, st.p, 7, hist.p);
+        k_sel_hist<<<blocks, 512, smem, s>>>(x, n, pass, st.p, hist.p, rep.p);
         PGCP_LAUNCH_CHECK();
-        k_sel_pick<<<7, 256, 0, s>>>(pass, st.p, hist.p);
+        k_sel_pick<<<NSEL, 256, 0, s>>>(pass, st.p, hist.p, rep.p);
         PGCP_LAUNCH_CHECK();
     }
     PGCP_TRY_CUDA(cudaMemcpyAsync(hs, st.p, sizeof hs, cudaMemcpyDeviceToHost, s));
@@ -547,7 +639,11 @@ PGCP_API int pgcp_distortion(const double* V, const int32_t* F, int64_t n, int64
         PGCP_TRY(cnt.alloc(nb, s));
         PGCP_TRY(cnt.zero(s));
         PGCP_TRY_CUDA(cudaMemcpyAsync(de.p, edges.data(), len * sizeof(double), cudaMemcpyHostToDevice, s));
-        k_hist_bins<<<grid_for(3 * m, 256), 256, 0, s>>>(absd.p, 3 * m, de.p, (int)nb, cnt.p);
+        if (nb <= HIST_SMEM_BINS)
+            k_hist_bins_smem<<<(int)std::min<int64_t>(SEL_BLOCKS, (3 * m + 511) / 512), 512, 0, s>>>(
+                absd.p, 3 * m, de.p, (int)nb, cnt.p);
+        else
+            k_hist_bins<<<grid_for(3 * m, 256), 256, 0, s>>>(absd.p, 3 * m, de.p, (int)nb, cnt.p);
         PGCP_LAUNCH_CHECK();
         PGCP_TRY_CUDA(cudaMemcpyAsync(hist, cnt.p, nb * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
         PGCP_TRY_CUDA(cudaStreamSynchronize(s));

@@ -71,8 +71,6 @@ void free_system(void* p) { delete static_cast<SolveSystem*>(p); }
 
 namespace {
 
-constexpr int PCG_THREADS = 512;
-constexpr int PCG_WARPS = PCG_THREADS / 32;
 constexpr int MAX_CLUSTER = 16;
 constexpr int SMEM_LIMIT = 227 * 1024;
 constexpr int RED_BYTES = 2 * MAX_CLUSTER * 2 * 8 + 32 * 2 * 8 + 64;
@@ -475,9 +473,6 @@ __device__ __forceinline__ double2 gather_gen(const unsigned long long* base, in
     return *reinterpret_cast<const double2*>(base[own] + (c & 0xffffffu));
 }
 
-__device__ __forceinline__ void red_add(double* p, double v) {
-    asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
-}
 
 template <int NT, bool PF>
 __global__ void __launch_bounds__(NT, 1) k_pcg(PcgArgs A) {

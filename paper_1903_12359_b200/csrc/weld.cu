@@ -429,10 +429,6 @@ struct Phase1Args {
     double2* arc_out;
     Rec* recs;
     double* meta;
-    double2* scratch;       // 2(k+3) points per step when shared memory is too small
-    int64_t* scratch_off;
-    int8_t* sides_scratch;
-    int smem_points;        // capacity of the shared point buffer
     int geodesic;           // unused here
 };
 
@@ -513,292 +509,6 @@ __device__ bool prenormalize(const double2* tv, const int32_t* src, int n, doubl
     }
     *out = mk_mob(C(1.0 / s, 0.0), C(-c.x / s, -c.y / s), C(0.0, 0.0), C(1.0, 0.0));
     return true;
-}
-
-__global__ void __launch_bounds__(512) k_phase1(Phase1Args A) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ Rec s_rec[2];
-    __shared__ int s_err;
-    __shared__ int s_has[2];
-    __shared__ double red[32];
-    const StepDesc sd = A.steps[blockIdx.x];
-    double* meta = A.meta + META * (int64_t)blockIdx.x;
-    const int k = sd.k;
-    const int P = k + 3;  // points per side: arc 0..k, aux 0, aux inf
-    double2* pts;
-    int8_t* sides;
-    if (2 * P <= A.smem_points) {
-        pts = reinterpret_cast<double2*>(smem);
-        sides = reinterpret_cast<int8_t*>(pts + A.smem_points);
-    } else {
-        pts = A.scratch + A.scratch_off[blockIdx.x];
-        sides = A.sides_scratch + A.scratch_off[blockIdx.x];
-    }
-    Rec* log_a = A.recs + sd.rec;
-    Rec* log_b = log_a + sd.cap;
-    int na_rec = 0, nb_rec = 0;
-    if (threadIdx.x == 0) {
-        s_err = 0;
-        for (int i = 0; i < META; ++i) meta[i] = 0.0;
-    }
-    __syncthreads();
-    if (k < 1 || k > sd.na - 1 || k > sd.nb - 1) {
-        if (threadIdx.x == 0) block_fail(&s_err, WE_K, k, 0, meta);
-        return;
-    }
-    const int32_t* sa = A.src + sd.src;
-    const int32_t* sb = sa + sd.na;
-    // --- prenormalizers (all cycle points)
-    Rec pre[2];
-    int pcode = 0;
-    bool okA = prenormalize(A.tv, sa, sd.na, red, &pre[0], &pcode);
-    if (!okA) {
-        if (threadIdx.x == 0) block_fail(&s_err, WE_PRE, 0, pcode, meta);
-        return;
-    }
-    bool okB = prenormalize(A.tv, sb, sd.nb, red, &pre[1], &pcode);
-    if (!okB) {
-        if (threadIdx.x == 0) block_fail(&s_err, WE_PRE, 1, pcode, meta);
-        return;
-    }
-    // --- phase-1 points: side A at [0, P), side B at [P, 2P)
-    for (int i = threadIdx.x; i < 2 * P; i += blockDim.x) {
-        int side = i >= P;
-        int t = i - side * P;
-        double2 z;
-        int8_t s = 0;
-        if (t <= k) {
-            z = A.tv[(side ? sb : sa)[t]];
-            apply_rec(pre[side], z, s);
-        } else {
-            z = (t == k + 1) ? C(0.0, 0.0) : cinf();
-        }
-        pts[i] = z;
-        sides[i] = 0;
-    }
-    if (threadIdx.x == 0) {
-        log_a[na_rec++] = pre[0];
-        log_b[nb_rec++] = pre[1];
-    }
-    __syncthreads();
-    auto apply_both = [&](bool use_a, bool use_b) {
-        for (int i = threadIdx.x; i < 2 * P; i += blockDim.x) {
-            int side = i >= P;
-            if (side ? !use_b : !use_a) continue;
-            double2 z = pts[i];
-            int8_t s = sides[i];
-            apply_rec(s_rec[side], z, s);
-            pts[i] = z;
-            sides[i] = s;
-        }
-    };
-    // --- Algorithm 1 on both sides in lockstep (welding.py:546-602)
-    if (threadIdx.x == 0) {
-        if (c_eq(pts[0], pts[1]) || c_eq(pts[P], pts[P + 1])) {
-            block_fail(&s_err, WE_ZIP01, 0, 0, meta);
-        } else {
-            s_rec[0] = mk_sqr(pts[0], pts[1], UP);
-            s_rec[1] = mk_sqr(pts[P], pts[P + 1], DOWN);
-            log_a[na_rec++] = s_rec[0];
-            log_b[nb_rec++] = s_rec[1];
-        }
-    }
-    __syncthreads();
-    if (s_err) return;
-    apply_both(true, true);
-    __syncthreads();
-    for (int j = 2; j <= k; ++j) {
-        if (threadIdx.x == 0) {
-            for (int side = 0; side < 2; ++side) {
-                double2 xi = pts[side * P + j];
-                int8_t sj = sides[side * P + j];
-                if (sj != 0 || c_isinf(xi)) {
-                    block_fail(&s_err, WE_ZIP_HALF, j, side, meta);
-                } else if (!(xi.x > 0)) {
-                    block_fail(&s_err, WE_ZIP_AXIS, j, side, meta);
-                } else if (cabs_(xi) < 1e-13) {
-                    block_fail(&s_err, WE_ZIP_COLL, j, side, meta);
-                } else {
-                    s_rec[side] = mk_open(xi, side ? DOWN : UP);
-                }
-            }
-            if (!s_err) {
-                log_a[na_rec++] = s_rec[0];
-                log_b[nb_rec++] = s_rec[1];
-            }
-        }
-        __syncthreads();
-        if (s_err) return;
-        apply_both(true, true);
-        __syncthreads();
-    }
-    // NaN check ("zipping"), then the axis Mobius sending pts[0] to infinity
-    {
-        double bad = 0;
-        for (int i = threadIdx.x; i < 2 * P; i += blockDim.x) bad = fmax(bad, c_nan(pts[i]) ? 1.0 : 0.0);
-        if (block_max(bad, red) > 0) {
-            if (threadIdx.x == 0) block_fail(&s_err, WE_NAN, 0, 1, meta);
-            return;
-        }
-    }
-    if (threadIdx.x == 0) {
-        for (int side = 0; side < 2; ++side) {
-            double2 w0 = pts[side * P];
-            s_has[side] = 0;
-            if (!c_isinf(w0)) {
-                if (c_zero(w0)) {
-                    block_fail(&s_err, WE_FAR0, 0, side, meta);
-                } else {
-                    int br = side ? DOWN : UP;
-                    Rec r = mk_mob(C(1, 0), C(0, 0), cdiv(C(-1.0, 0.0), w0), C(1, 0), true);
-                    mob_pin(r, w0, cinf(), br);
-                    mob_pin(r, C(0, 0), C(0, 0), br);
-                    s_rec[side] = r;
-                    s_has[side] = 1;
-                    if (side) log_b[nb_rec++] = r; else log_a[na_rec++] = r;
-                }
-            }
-        }
-    }
-    __syncthreads();
-    if (s_err) return;
-    apply_both(s_has[0], s_has[1]);
-    __syncthreads();
-    // --- closing loop (welding.py:673-687)
-    for (int j = k - 1; j >= 1; --j) {
-        if (threadIdx.x == 0) {
-            double2 al = pts[j], be = pts[P + j];
-            if (sides[j] == 0 || c_isinf(al) || al.y == 0.0) {
-                block_fail(&s_err, WE_ALIGN_A, j, 0, meta);
-            } else if (sides[P + j] == 0 || c_isinf(be) || be.y == 0.0) {
-                block_fail(&s_err, WE_ALIGN_B, j, 0, meta);
-            } else if (!walk_less(al.y, be.y)) {
-                block_fail(&s_err, WE_ORDER, j, 0, meta);
-            } else {
-                s_rec[0] = mk_close(al.y, be.y);
-                s_rec[1] = s_rec[0];
-                log_a[na_rec++] = s_rec[0];
-                log_b[nb_rec++] = s_rec[0];
-            }
-        }
-        __syncthreads();
-        if (s_err) return;
-        apply_both(true, true);
-        __syncthreads();
-    }
-    // --- far ends; stage max of |va| over arc + aux (finite) for the deferred check
-    {
-        double m = 0;
-        for (int i = threadIdx.x; i < P; i += blockDim.x)
-            if (c_fin(pts[i])) m = fmax(m, cabs_(pts[i]));
-        m = block_max(m, red);
-        if (threadIdx.x == 0) {
-            double2 qa = pts[0], qb = pts[P];
-            meta[6] = qa.x; meta[7] = qa.y; meta[8] = qb.x; meta[9] = qb.y;
-            meta[10] = m;
-            meta[14] = na_rec;
-            meta[15] = nb_rec;
-            s_rec[0] = mk_sq(c_isinf(qa) ? cinf() : qa);
-            s_rec[1] = s_rec[0];
-            log_a[na_rec++] = s_rec[0];
-            log_b[nb_rec++] = s_rec[0];
-        }
-    }
-    __syncthreads();
-    apply_both(true, true);
-    __syncthreads();
-    // --- normalization (welding.py:699-717)
-    if (threadIdx.x == 0) {
-        double2 za = pts[k + 1], zb = pts[P + k + 1], ia = pts[k + 2], ib = pts[P + k + 2];
-        if (c_isinf(za) || c_isinf(zb) || c_isinf(ia) || c_isinf(ib)) {
-            block_fail(&s_err, WE_TRACK, 0, 0, meta);
-        } else {
-            double2 zmid = C(0.5 * (ia.x + ib.x), 0.5 * (ia.y + ib.y));
-            double2 co[4];
-            if (!c_eq(za, zb) && !c_eq(za, zmid) && !c_eq(zb, zmid)) {
-                double2 zs[3] = {za, zb, zmid}, ws[3] = {C(-1, 0), C(1, 0), cinf()};
-                if (!three_point(zs, ws, co)) block_fail(&s_err, WE_THREE, 0, 0, meta);
-            } else if (!c_zero(za)) {
-                co[0] = cdiv(C(-1.0, 0.0), za); co[1] = C(0, 0); co[2] = C(0, 0); co[3] = C(1, 0);
-            } else {
-                co[0] = C(1, 0); co[1] = C(0, 0); co[2] = C(0, 0); co[3] = C(1, 0);
-            }
-            if (!s_err) {
-                s_rec[0] = mk_mob(co[0], co[1], co[2], co[3]);
-                s_rec[1] = s_rec[0];
-                log_a[na_rec++] = s_rec[0];
-                log_b[nb_rec++] = s_rec[0];
-            }
-        }
-    }
-    __syncthreads();
-    if (s_err) return;
-    apply_both(true, true);
-    __syncthreads();
-    {
-        double bad = 0;
-        for (int i = threadIdx.x; i < 2 * P; i += blockDim.x) bad = fmax(bad, c_nan(pts[i]) ? 1.0 : 0.0);
-        if (block_max(bad, red) > 0) {
-            if (threadIdx.x == 0) block_fail(&s_err, WE_NAN, 0, 3, meta);
-            return;
-        }
-    }
-    // --- closed welding: respread the seam (welding.py:751-763)
-    if (sd.closed) {
-        if (threadIdx.x == 0) {
-            int n = k + 1;
-            double2 an[3] = {pts[0], pts[n / 3], pts[(2 * n) / 3]};
-            double2 tg[3] = {C(1.0, 0.0), C(cos(2 * M_PI / 3), sin(2 * M_PI / 3)),
-                             C(cos(4 * M_PI / 3), sin(4 * M_PI / 3))};
-            double2 co[4];
-            if (!three_point(an, tg, co)) {
-                block_fail(&s_err, WE_THREE, 1, 0, meta);
-            } else {
-                s_rec[0] = mk_mob(co[0], co[1], co[2], co[3]);
-                s_rec[1] = s_rec[0];
-                log_a[na_rec++] = s_rec[0];
-                log_b[nb_rec++] = s_rec[0];
-            }
-        }
-        __syncthreads();
-        if (s_err) return;
-        for (int i = threadIdx.x; i < 2 * P; i += blockDim.x) sides[i] = 0;
-        __syncthreads();
-        apply_both(true, true);
-        __syncthreads();
-    }
-    // --- outputs: arcs, seam over the arc, maxima, polygon area of the a arc
-    double seam = 0, ma = 0, mb = 0, mx = 0, area = 0;
-    for (int t = threadIdx.x; t <= k; t += blockDim.x) {
-        double2 a = pts[t], b = pts[P + t];
-        A.arc_out[sd.arc + t] = a;
-        A.arc_out[sd.arc + k + 1 + t] = b;
-        double g = (c_isinf(a) && c_isinf(b)) ? 0.0 : cabs_(csub(a, b));
-        if (!isnan(g)) seam = fmax(seam, g);
-        if (c_fin(a)) ma = fmax(ma, cabs_(a));
-        if (c_fin(b)) mb = fmax(mb, cabs_(b));
-        double2 nx = pts[(t + 1) % (k + 1)];
-        area += 0.5 * (a.x * nx.y - a.y * nx.x);
-    }
-    for (int t = threadIdx.x; t < 2; t += blockDim.x) {
-        double2 a = pts[k + 1 + t], b = pts[P + k + 1 + t];
-        if (c_fin(a)) mx = fmax(mx, cabs_(a));
-        if (c_fin(b)) mx = fmax(mx, cabs_(b));
-    }
-    seam = block_max(seam, red);
-    ma = block_max(ma, red);
-    mb = block_max(mb, red);
-    mx = block_max(mx, red);
-    area = block_sum(area, red);
-    if (threadIdx.x == 0) {
-        meta[0] = na_rec;
-        meta[1] = nb_rec;
-        meta[5] = seam;
-        meta[11] = ma;
-        meta[12] = mb;
-        meta[13] = mx;
-        meta[16] = area;
-    }
 }
 
 // ---------------------------------------------------------------------------
@@ -1496,18 +1206,6 @@ std::string err_text(int code, int idx, int aux, double a = 0, double b = 0, dou
     }
 }
 
-constexpr int P1_THREADS = 512;
-constexpr int P1_SMEM_POINTS = 6000;  // 6000 * 17 B ~ 100 KB
-
-int setup_phase1_smem() {
-    static bool done = false;
-    if (!done) {
-        int bytes = P1_SMEM_POINTS * (sizeof(double2) + 1);
-        PGCP_TRY_CUDA(cudaFuncSetAttribute(k_phase1, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-        done = true;
-    }
-    return PGCP_OK;
-}
 
 double bits_to_d(unsigned long long b) {
     double d;
@@ -1527,7 +1225,6 @@ int run_schedule(double2* tv, int32_t nsteps, const int32_t* info, const int32_t
                  const int32_t* wb, double hard_tol, double* out, Rec* recs_host, int64_t recs_cap_total,
                  cudaStream_t s) {
     if (nsteps <= 0) return PGCP_OK;
-    PGCP_TRY(setup_phase1_smem());
     // levels: a step waits for the previous steps on either of its components
     std::vector<int> level(nsteps, 0);
     {
@@ -1552,9 +1249,9 @@ int run_schedule(double2* tv, int32_t nsteps, const int32_t* info, const int32_t
     for (int q = 0; q < nsteps; ++q) pos[order[q]] = q;
     // descriptors (in launch order)
     std::vector<StepDesc> sd(nsteps);
-    std::vector<int64_t> src_off(nsteps + 1, 0), scratch_off(nsteps, 0);
+    std::vector<int64_t> src_off(nsteps + 1, 0);
     for (int i = 0; i < nsteps; ++i) src_off[i + 1] = src_off[i] + info[6 * i + 2] + info[6 * i + 3];
-    int64_t rec_tot = 0, arc_tot = 0, scr_tot = 0;
+    int64_t rec_tot = 0, arc_tot = 0;
     for (int q = 0; q < nsteps; ++q) {
         int i = order[q];
         StepDesc& d = sd[q];
@@ -1569,8 +1266,6 @@ int run_schedule(double2* tv, int32_t nsteps, const int32_t* info, const int32_t
         rec_tot += 2 * (int64_t)d.cap;
         d.arc = arc_tot;
         arc_tot += 2 * (int64_t)(d.k + 3);
-        scratch_off[q] = scr_tot;
-        if (2 * (d.k + 3) > P1_SMEM_POINTS) scr_tot += 2 * (int64_t)(d.k + 3);
     }
     // write-back entries (slot, code, launch-order step)
     int64_t nwb = wb_off[nsteps];
@@ -1596,9 +1291,7 @@ int run_schedule(double2* tv, int32_t nsteps, const int32_t* info, const int32_t
     DevBuf<StepDesc> d_sd;
     DevBuf<int32_t> d_src, d_wb;
     DevBuf<Rec> d_recs;
-    DevBuf<double2> d_arc, d_scr;
-    DevBuf<int8_t> d_sscr;
-    DevBuf<int64_t> d_scroff;
+    DevBuf<double2> d_arc;
     DevBuf<double> d_meta;
     DevBuf<unsigned long long> d_max;
     DevBuf<int> d_nan;
@@ -1607,9 +1300,6 @@ int run_schedule(double2* tv, int32_t nsteps, const int32_t* info, const int32_t
     PGCP_TRY(d_wb.alloc(3 * std::max<int64_t>(nwb, 1), s));
     PGCP_TRY(d_recs.alloc(rec_tot, s));
     PGCP_TRY(d_arc.alloc(arc_tot, s));
-    PGCP_TRY(d_scr.alloc(std::max<int64_t>(scr_tot, 1), s));
-    PGCP_TRY(d_sscr.alloc(std::max<int64_t>(scr_tot, 1), s));
-    PGCP_TRY(d_scroff.alloc(nsteps, s));
     PGCP_TRY(d_meta.alloc((int64_t)META * nsteps, s));
     PGCP_TRY(d_max.alloc(3 * (int64_t)nsteps, s));
     PGCP_TRY(d_max.zero(s));
@@ -1618,7 +1308,6 @@ int run_schedule(double2* tv, int32_t nsteps, const int32_t* info, const int32_t
     PGCP_TRY_CUDA(cudaMemcpyAsync(d_sd.p, sd.data(), nsteps * sizeof(StepDesc), cudaMemcpyHostToDevice, s));
     PGCP_TRY_CUDA(cudaMemcpyAsync(d_src.p, src, src_off[nsteps] * sizeof(int32_t), cudaMemcpyHostToDevice, s));
     PGCP_TRY_CUDA(cudaMemcpyAsync(d_wb.p, wb3.data(), 3 * nwb * sizeof(int32_t), cudaMemcpyHostToDevice, s));
-    PGCP_TRY_CUDA(cudaMemcpyAsync(d_scroff.p, scratch_off.data(), nsteps * sizeof(int64_t), cudaMemcpyHostToDevice, s));
     int q0 = 0;
     for (int l = 0; l < nlev; ++l) {
         int q1 = q0;
@@ -1630,10 +1319,6 @@ int run_schedule(double2* tv, int32_t nsteps, const int32_t* info, const int32_t
         a.arc_out = d_arc.p;
         a.recs = d_recs.p;
         a.meta = d_meta.p + (int64_t)META * q0;
-        a.scratch = d_scr.p;
-        a.scratch_off = d_scroff.p + q0;
-        a.sides_scratch = d_sscr.p;
-        a.smem_points = P1_SMEM_POINTS;
         a.geodesic = 0;
         int kmax = 0;
         for (int q = q0; q < q1; ++q) kmax = std::max(kmax, sd[q].k);

@@ -5,6 +5,7 @@ torch.distributed; every computation is a libpgcp_b200 kernel.
 """
 
 import ctypes
+import warnings
 
 import numpy as np
 import torch
@@ -44,7 +45,11 @@ def to_dev(a, dtype=None):
     arr = np.ascontiguousarray(a)
     if dtype is None:
         dtype = _DT[arr.dtype]
-    return torch.from_numpy(arr).to(device=device(), dtype=dtype)
+    with warnings.catch_warnings():
+        # frozen (read-only) mesh arrays: the tensor is only a copy source
+        warnings.simplefilter("ignore", UserWarning)
+        host = torch.from_numpy(arr)
+    return host.to(device=device(), dtype=dtype)
 
 
 def ptr(t):
