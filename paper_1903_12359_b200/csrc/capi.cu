@@ -7,6 +7,22 @@ namespace {
 
 cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Scratch buffers are stream-ordered allocations from the device's default
+// pool. Keep freed blocks cached in the pool (release threshold = max): with
+// the default threshold of 0 every stream synchronisation hands the memory
+// back to the driver and the next call maps it again.
+void keep_pool(int dev) {
+    static bool done[64] = {false};
+    if (dev < 0 || dev >= 64 || done[dev]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+    done[dev] = true;
+}
+
 int set_device_of(const void* ptr) {
     if (!ptr) return PGCP_OK;
     cudaPointerAttributes at;
@@ -17,6 +33,7 @@ int set_device_of(const void* ptr) {
         return PGCP_E_INVALID;
     }
     PGCP_TRY_CUDA(cudaSetDevice(at.device));
+    keep_pool(at.device);
     return PGCP_OK;
 }
 

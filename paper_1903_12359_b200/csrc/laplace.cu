@@ -191,38 +191,56 @@ __global__ void k_row_fill(int64_t sum_n, const int32_t* __restrict__ vmap, cons
     }
 }
 
-// default pins: sequential arclength per loop (flatten.py:113-122)
+// default pins (flatten.py:113-122): one warp per loop. The lanes compute 32
+// segment lengths at a time; lane 0 adds them in loop order, so the running
+// sums (cumsum) and the argmin (first minimum) are the reference's exactly.
 __global__ void k_default_pins(int32_t K, const int64_t* __restrict__ loop_off, const int32_t* __restrict__ loop,
                                const int64_t* __restrict__ vert_off, const int32_t* __restrict__ vmap,
                                const double* __restrict__ V, int32_t* __restrict__ pins) {
-    GRID_STRIDE(c, K) {
-        int64_t lo = loop_off[c], nb = loop_off[c + 1] - lo;
-        int64_t vb = vert_off[c];
-        if (nb <= 0) {
-            pins[2 * c] = pins[2 * c + 1] = -1;
-            continue;
+    const int lane = threadIdx.x & 31;
+    const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (c >= K) return;
+    const int64_t lo = loop_off[c], nb = loop_off[c + 1] - lo;
+    const int64_t vb = vert_off[c];
+    if (nb <= 0) {
+        if (lane == 0) pins[2 * c] = pins[2 * c + 1] = -1;
+        return;
+    }
+    auto seg = [&](int64_t j) {
+        int a = vmap[vb + loop[lo + j]];
+        int b = vmap[vb + loop[lo + (j + 1) % nb]];
+        double dx = __dsub_rn(V[3 * b], V[3 * a]);
+        double dy = __dsub_rn(V[3 * b + 1], V[3 * a + 1]);
+        double dz = __dsub_rn(V[3 * b + 2], V[3 * a + 2]);
+        return __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
+    };
+    double total = 0.0;
+    for (int64_t j0 = 0; j0 < nb; j0 += 32) {
+        double sl = j0 + lane < nb ? seg(j0 + lane) : 0.0;
+        const int cnt = (int)min((int64_t)32, nb - j0);
+        for (int t = 0; t < cnt; ++t) {
+            double v = __shfl_sync(0xffffffffu, sl, t);
+            total = __dadd_rn(total, v);
         }
-        auto seg = [&](int64_t j) {
-            int a = vmap[vb + loop[lo + j]];
-            int b = vmap[vb + loop[lo + (j + 1) % nb]];
-            double dx = __dsub_rn(V[3 * b], V[3 * a]);
-            double dy = __dsub_rn(V[3 * b + 1], V[3 * a + 1]);
-            double dz = __dsub_rn(V[3 * b + 2], V[3 * a + 2]);
-            return __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
-        };
-        double total = 0.0;
-        for (int64_t j = 0; j < nb; ++j) total = __dadd_rn(total, seg(j));
-        double half = total / 2.0;
-        double cum = 0.0, best = fabs(0.0 - half);
-        int64_t bj = 0;
-        for (int64_t j = 1; j < nb; ++j) {
-            cum = __dadd_rn(cum, seg(j - 1));
+    }
+    const double half = total / 2.0;
+    double cum = 0.0, best = fabs(0.0 - half);
+    int64_t bj = 0;
+    // cum after segment j-1 is compared at position j (j = 1..nb-1)
+    for (int64_t j0 = 0; j0 < nb - 1; j0 += 32) {
+        double sl = j0 + lane < nb - 1 ? seg(j0 + lane) : 0.0;
+        const int cnt = (int)min((int64_t)32, nb - 1 - j0);
+        for (int t = 0; t < cnt; ++t) {
+            double v = __shfl_sync(0xffffffffu, sl, t);
+            cum = __dadd_rn(cum, v);
             double d = fabs(__dsub_rn(cum, half));
             if (d < best) {
                 best = d;
-                bj = j;
+                bj = j0 + t + 1;
             }
         }
+    }
+    if (lane == 0) {
         if (bj == 0) bj = nb / 2;
         pins[2 * c] = loop[lo];
         pins[2 * c + 1] = loop[lo + bj];
@@ -317,7 +335,7 @@ int build_laplacian(pgcp_batch* b, int64_t* clamped, cudaStream_t s) {
 
 int default_pins(pgcp_batch* b, cudaStream_t s) {
     PGCP_TRY(b->pins.alloc(2 * (int64_t)b->K, s));
-    k_default_pins<<<grid_for(b->K, 64), 64, 0, s>>>(b->K, b->loop_off.p, b->loop.p, b->vert_off.p, b->vmap.p,
+    k_default_pins<<<(unsigned)((b->K + 3) / 4), 128, 0, s>>>(b->K, b->loop_off.p, b->loop.p, b->vert_off.p, b->vmap.p,
                                                     b->V.p, b->pins.p);
     PGCP_LAUNCH_CHECK();
     return PGCP_OK;

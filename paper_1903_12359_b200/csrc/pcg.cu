@@ -29,6 +29,7 @@
 //      rz = sum D|z|^2, rr = sum D^2|z|^2   (residual r = D z)
 // using A p_new = A z + beta A p_old, so only z is ever gathered.
 #include <cooperative_groups.h>
+#include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
 #include <cmath>
@@ -65,6 +66,18 @@ struct SolveSystem {
     DevBuf<double2> b, x, fv;
     DevBuf<int32_t> iters;
     DevBuf<double> res;  // per slot: relres, bnorm^2, true_res^2, xnorm^2, pad
+    // two-level preconditioner (see k_pcg2)
+    bool coarse = false;
+    int gmax = 8;
+    DevBuf<int32_t> cell, aggr, aoff;
+    DevBuf<float2> pxy_row;
+    DevBuf<float4> wr;
+    DevBuf<int64_t> nu_d, abase, eoff;
+    DevBuf<double2> einv, p;
+    DevBuf<float2> einv32;
+    DevBuf<int64_t> eoff32;
+    std::vector<int64_t> h_abase;
+    double coarse_ms = 0;
 };
 
 void free_system(void* p) { delete static_cast<SolveSystem*>(p); }
@@ -358,6 +371,619 @@ __global__ void k_encode_cols(int32_t nslot, const int64_t* __restrict__ sl_off,
 // ---------------------------------------------------------------------------
 // the solver
 
+// ---------------------------------------------------------------------------
+// Two-level preconditioner (additive coarse correction on top of Jacobi).
+//
+// Unknowns of every slot are reordered into geometric cells: principal frame
+// of the slot's vertices, G quantile strips along the first axis, G cells per
+// strip along the second (G = min(8, sqrt(nu / 128))). Cells cut by a CTA
+// boundary of the cluster split become two aggregates, so every aggregate is
+// a contiguous row range owned by one CTA. The coarse space holds the linear
+// functions (1, u, v) of each aggregate (u, v local cell coordinates); in the
+// Jacobi-scaled space W^ = D^{1/2} W and the preconditioner is
+//     M^-1 = I + W^ E^-1 W^T,   E = W^T A^ W^   (complex Hermitian, dense)
+// which is symmetric positive definite, so CG keeps its real alpha / beta.
+// E^-1 is formed once per solve (Gauss-Jordan per slot, dependent coarse
+// functions dropped).
+
+constexpr int COARSE_GMAX = 8;
+constexpr int AGG_MAX = 80;               // aggregates per slot: G^2 + CTA splits
+constexpr int NC_MAX = 3 * AGG_MAX;       // coarse dofs per slot
+constexpr int ITEMS_MAX = AGG_MAX;        // (aggregate, part) work items per CTA
+constexpr int COARSE_BYTES = 3 * NC_MAX * 16 + ITEMS_MAX * 6 * 8;
+
+__host__ __device__ inline int coarse_G(int64_t nu, int gmax) {
+    int g = (int)sqrt((double)nu / 128.0);
+    return g < 1 ? 1 : (g > gmax ? gmax : g);
+}
+
+__device__ __forceinline__ uint32_t f32_order(float f) {
+    uint32_t u = __float_as_uint(f);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+// symmetric 3x3 eigenvectors by cyclic Jacobi; columns of v sorted by
+// decreasing eigenvalue
+__device__ void eig3(double a[3][3], double v[3][3]) {
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) v[i][j] = (i == j) ? 1.0 : 0.0;
+    for (int sweep = 0; sweep < 16; ++sweep) {
+        double off = fabs(a[0][1]) + fabs(a[0][2]) + fabs(a[1][2]);
+        if (off == 0.0) break;
+        for (int p = 0; p < 2; ++p)
+            for (int q = p + 1; q < 3; ++q) {
+                if (a[p][q] == 0.0) continue;
+                double th = (a[q][q] - a[p][p]) / (2.0 * a[p][q]);
+                double t = (th >= 0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
+                double c = 1.0 / sqrt(t * t + 1.0), s = t * c;
+                for (int k = 0; k < 3; ++k) {  // a = J^T a J
+                    double akp = a[k][p], akq = a[k][q];
+                    a[k][p] = c * akp - s * akq;
+                    a[k][q] = s * akp + c * akq;
+                }
+                for (int k = 0; k < 3; ++k) {
+                    double apk = a[p][k], aqk = a[q][k];
+                    a[p][k] = c * apk - s * aqk;
+                    a[q][k] = s * apk + c * aqk;
+                }
+                for (int k = 0; k < 3; ++k) {
+                    double vkp = v[k][p], vkq = v[k][q];
+                    v[k][p] = c * vkp - s * vkq;
+                    v[k][q] = s * vkp + c * vkq;
+                }
+            }
+    }
+    int o[3] = {0, 1, 2};
+    for (int i = 0; i < 3; ++i)
+        for (int j = i + 1; j < 3; ++j)
+            if (a[o[j]][o[j]] > a[o[i]][o[i]]) {
+                int t = o[i];
+                o[i] = o[j];
+                o[j] = t;
+            }
+    double w[3][3];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) w[i][j] = v[i][o[j]];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) v[i][j] = w[i][j];
+}
+
+__device__ __forceinline__ const double* vtx_of(int64_t e, int j, const int32_t* comps, const int64_t* sv_off,
+                                                const int64_t* vert_off, const int32_t* vmap, const double* V) {
+    int c = comps[j];
+    int v = vmap[vert_off[c] + (e - sv_off[j])];
+    return V + 3 * (int64_t)v;
+}
+
+// per slot: mean and principal frame (e1, e2) of the unknown vertices
+__global__ void k_pca(int32_t nslot, const int32_t* __restrict__ comps, const int64_t* __restrict__ sv_off,
+                      const int64_t* __restrict__ vert_off, const int32_t* __restrict__ vmap,
+                      const double* __restrict__ V, const int32_t* __restrict__ fixed_ref,
+                      double* __restrict__ frame) {
+    __shared__ double red[10][32];
+    const int j = blockIdx.x;
+    double acc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    for (int64_t e = sv_off[j] + threadIdx.x; e < sv_off[j + 1]; e += blockDim.x) {
+        if (fixed_ref[e] >= 0) continue;
+        const double* p = vtx_of(e, j, comps, sv_off, vert_off, vmap, V);
+        double x = p[0], y = p[1], z = p[2];
+        acc[0] += 1.0;
+        acc[1] += x;
+        acc[2] += y;
+        acc[3] += z;
+        acc[4] += x * x;
+        acc[5] += x * y;
+        acc[6] += x * z;
+        acc[7] += y * y;
+        acc[8] += y * z;
+        acc[9] += z * z;
+    }
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int i = 0; i < 10; ++i) {
+        double t = warp_sum(acc[i]);
+        if (lane == 0) red[i][w] = t;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s[10];
+        for (int i = 0; i < 10; ++i) {
+            s[i] = 0.0;
+            for (int q = 0; q < nw; ++q) s[i] += red[i][q];
+        }
+        double n = s[0] > 0 ? s[0] : 1.0;
+        double m[3] = {s[1] / n, s[2] / n, s[3] / n};
+        double a[3][3];
+        a[0][0] = s[4] / n - m[0] * m[0];
+        a[0][1] = a[1][0] = s[5] / n - m[0] * m[1];
+        a[0][2] = a[2][0] = s[6] / n - m[0] * m[2];
+        a[1][1] = s[7] / n - m[1] * m[1];
+        a[1][2] = a[2][1] = s[8] / n - m[1] * m[2];
+        a[2][2] = s[9] / n - m[2] * m[2];
+        double v[3][3];
+        eig3(a, v);
+        double* f = frame + 9 * j;
+        for (int i = 0; i < 3; ++i) {
+            f[i] = m[i];
+            f[3 + i] = v[i][0];
+            f[6 + i] = v[i][1];
+        }
+    }
+}
+
+// projected coordinates of every unknown and the first sort key (slot, px)
+__global__ void k_proj(int64_t ne, int32_t nslot, const int32_t* __restrict__ comps,
+                       const int64_t* __restrict__ sv_off, const int64_t* __restrict__ vert_off,
+                       const int32_t* __restrict__ vmap, const double* __restrict__ V,
+                       const int32_t* __restrict__ fixed_ref, const int64_t* __restrict__ uscan,
+                       const double* __restrict__ frame, float2* __restrict__ pxy,
+                       unsigned long long* __restrict__ key, int32_t* __restrict__ val,
+                       uint32_t* __restrict__ bbox) {
+    GRID_STRIDE(e, ne) {
+        if (fixed_ref[e] >= 0) continue;
+        int j = bsearch_off(sv_off, nslot + 1, e);
+        const double* p = vtx_of(e, j, comps, sv_off, vert_off, vmap, V);
+        const double* f = frame + 9 * j;
+        double dx = p[0] - f[0], dy = p[1] - f[1], dz = p[2] - f[2];
+        float px = (float)(dx * f[3] + dy * f[4] + dz * f[5]);
+        float py = (float)(dx * f[6] + dy * f[7] + dz * f[8]);
+        int64_t u = uscan[e];
+        pxy[u] = make_float2(px, py);
+        key[u] = ((unsigned long long)j << 32) | f32_order(px);
+        val[u] = (int32_t)e;
+        atomicMin(&bbox[4 * j], f32_order(px));
+        atomicMax(&bbox[4 * j + 1], f32_order(px));
+        atomicMin(&bbox[4 * j + 2], f32_order(py));
+        atomicMax(&bbox[4 * j + 3], f32_order(py));
+    }
+}
+
+__device__ __forceinline__ float f32_unorder(uint32_t u) {
+    return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
+}
+
+__device__ __forceinline__ uint32_t spread16(uint32_t x) {
+    x &= 0xffffu;
+    x = (x | (x << 8)) & 0x00ff00ffu;
+    x = (x | (x << 4)) & 0x0f0f0f0fu;
+    x = (x | (x << 2)) & 0x33333333u;
+    x = (x | (x << 1)) & 0x55555555u;
+    return x;
+}
+
+// third key: (slot, cell, Morton code of the position in the slot's box), so
+// rows inside a cell follow a Z-curve (neighbours stay close in the row order)
+__global__ void k_cell_keys(int64_t nU, const unsigned long long* __restrict__ key_in,
+                            const int32_t* __restrict__ val_in, const int64_t* __restrict__ sv_off,
+                            const int64_t* __restrict__ uscan, const float2* __restrict__ pxy,
+                            const uint32_t* __restrict__ bbox, int gmax, unsigned long long* __restrict__ key,
+                            int32_t* __restrict__ val) {
+    GRID_STRIDE(k, nU) {
+        unsigned long long kk = key_in[k];
+        int j = (int)(kk >> 40);
+        int ax = (int)((kk >> 32) & 0xff);
+        int32_t e = val_in[k];
+        int64_t us = uscan[sv_off[j]], nu = uscan[sv_off[j + 1]] - us;
+        int G = coarse_G(nu, gmax);
+        int64_t rho = k - us;
+        int64_t s0 = (ax * nu + G - 1) / G, s1 = ((ax + 1) * nu + G - 1) / G;
+        int ay = s1 > s0 ? (int)((rho - s0) * G / (s1 - s0)) : 0;
+        float2 p = pxy[uscan[e]];
+        float x0 = f32_unorder(bbox[4 * j]), x1 = f32_unorder(bbox[4 * j + 1]);
+        float y0 = f32_unorder(bbox[4 * j + 2]), y1 = f32_unorder(bbox[4 * j + 3]);
+        float ex = x1 > x0 ? 65535.0f / (x1 - x0) : 0.0f, ey = y1 > y0 ? 65535.0f / (y1 - y0) : 0.0f;
+        uint32_t qx = (uint32_t)fminf(65535.0f, fmaxf(0.0f, (p.x - x0) * ex));
+        uint32_t qy = (uint32_t)fminf(65535.0f, fmaxf(0.0f, (p.y - y0) * ey));
+        uint32_t mort = spread16(qx) | (spread16(qy) << 1);
+        key[k] = ((unsigned long long)j << 40) | ((unsigned long long)(ax * G + ay) << 32) | mort;
+        val[k] = e;
+    }
+}
+
+// strip index along the first axis and the second sort key (slot, strip, py)
+__global__ void k_strip(int64_t nU, const unsigned long long* __restrict__ key_in, const int32_t* __restrict__ val_in,
+                        const int64_t* __restrict__ sv_off, const int64_t* __restrict__ uscan,
+                        const float2* __restrict__ pxy, int gmax, unsigned long long* __restrict__ key,
+                        int32_t* __restrict__ val) {
+    GRID_STRIDE(k, nU) {
+        int j = (int)(key_in[k] >> 32);
+        int32_t e = val_in[k];
+        int64_t us = uscan[sv_off[j]], nu = uscan[sv_off[j + 1]] - us;
+        int G = coarse_G(nu, gmax);
+        int64_t rho = k - us;
+        int ax = (int)(rho * G / nu);
+        float py = pxy[uscan[e]].y;
+        key[k] = ((unsigned long long)j << 40) | ((unsigned long long)ax << 32) | f32_order(py);
+        val[k] = e;
+    }
+}
+
+// final row numbering (slot-local row = rank in the (strip, py) order) and the
+// cell of every row
+__global__ void k_rows_by_cell(int64_t nU, const unsigned long long* __restrict__ key_in,
+                               const int32_t* __restrict__ val_in, const int64_t* __restrict__ sv_off,
+                               const int64_t* __restrict__ sl_off, const int64_t* __restrict__ uscan,
+                               const float2* __restrict__ pxy, int gmax, int32_t* __restrict__ urow,
+                               int32_t* __restrict__ rowsrc, int32_t* __restrict__ cell,
+                               float2* __restrict__ pxy_row) {
+    GRID_STRIDE(k, nU) {
+        unsigned long long kk = key_in[k];
+        int j = (int)(kk >> 40);
+        int32_t e = val_in[k];
+        int64_t us = uscan[sv_off[j]];
+        int64_t r = 32 * sl_off[j] + (k - us);
+        urow[e] = (int32_t)r;
+        rowsrc[r] = e;
+        cell[r] = (int)((kk >> 32) & 0xff);
+        pxy_row[r] = pxy[uscan[e]];
+    }
+}
+
+// aggregate starts: first row of a slot, a cell change, or a CTA boundary
+__global__ void k_agg_flag(int64_t rows, int32_t nslot, const int64_t* __restrict__ sl_off,
+                           const int64_t* __restrict__ nu_slot, const int32_t* __restrict__ cell, int csize,
+                           int32_t* __restrict__ flag) {
+    GRID_STRIDE(r, rows) {
+        int j = bsearch_off(sl_off, nslot + 1, r >> 5);
+        int64_t lr = r - 32 * sl_off[j];
+        int64_t S = sl_off[j + 1] - sl_off[j];
+        int64_t chunk = (S + csize - 1) / csize;
+        int f = 0;
+        if (lr == 0) {
+            f = 1;
+        } else if (lr < nu_slot[j]) {
+            int64_t cta = (lr >> 5) / chunk, ctap = ((lr - 1) >> 5) / chunk;
+            f = (cell[r] != cell[r - 1] || cta != ctap) ? 1 : 0;
+        }
+        flag[r] = f;
+    }
+}
+
+__global__ void k_agg_index(int64_t rows, const int32_t* __restrict__ flag, const int64_t* __restrict__ scan,
+                            int32_t* __restrict__ aggr, int32_t* __restrict__ aoff) {
+    GRID_STRIDE(r, rows) {
+        int32_t a = (int32_t)(scan[r] + flag[r] - 1);
+        aggr[r] = a;
+        if (flag[r]) aoff[a] = (int32_t)r;
+    }
+}
+
+__global__ void k_slot_abase(int32_t nslot, const int64_t* __restrict__ sl_off, const int64_t* __restrict__ scan,
+                             int64_t* __restrict__ abase) {
+    GRID_STRIDE(j, nslot + 1) abase[j] = scan[32 * sl_off[j]];
+}
+
+// per aggregate: centroid and extent of the cell coordinates -> coarse weights
+// w^ = sqrt(D) (1, u, v) per real row (padding rows: 0)
+__global__ void k_agg_weights(int32_t nagg_total, const int32_t* __restrict__ aoff, int32_t nslot,
+                              const int64_t* __restrict__ sl_off, const int64_t* __restrict__ nu_slot,
+                              const float2* __restrict__ pxy_row, const double* __restrict__ Dsq,
+                              float4* __restrict__ wr) {
+    __shared__ double red[3][32];
+    __shared__ double s_c[3];
+    const int A = blockIdx.x;
+    const int64_t r0 = aoff[A], r1 = aoff[A + 1];
+    const int j = bsearch_off(sl_off, nslot + 1, r0 >> 5);
+    const int64_t rend = min(r1, 32 * sl_off[j] + nu_slot[j]);  // real rows
+    double sx = 0, sy = 0, n = 0;
+    for (int64_t r = r0 + threadIdx.x; r < rend; r += blockDim.x) {
+        float2 p = pxy_row[r];
+        sx += p.x;
+        sy += p.y;
+        n += 1.0;
+    }
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    sx = warp_sum(sx);
+    sy = warp_sum(sy);
+    n = warp_sum(n);
+    if (lane == 0) {
+        red[0][w] = sx;
+        red[1][w] = sy;
+        red[2][w] = n;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0, b = 0, c = 0;
+        for (int q = 0; q < nw; ++q) {
+            a += red[0][q];
+            b += red[1][q];
+            c += red[2][q];
+        }
+        s_c[0] = c > 0 ? a / c : 0.0;
+        s_c[1] = c > 0 ? b / c : 0.0;
+    }
+    __syncthreads();
+    const double cx = s_c[0], cy = s_c[1];
+    double m = 0.0;
+    for (int64_t r = r0 + threadIdx.x; r < rend; r += blockDim.x) {
+        float2 p = pxy_row[r];
+        m = fmax(m, fmax(fabs(p.x - cx), fabs(p.y - cy)));
+    }
+    m = warp_max(m);
+    __syncthreads();
+    if (lane == 0) red[0][w] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0;
+        for (int q = 0; q < nw; ++q) t = fmax(t, red[0][q]);
+        s_c[2] = t;
+    }
+    __syncthreads();
+    const double sc = s_c[2] > 0 ? 1.0 / s_c[2] : 0.0;
+    for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+        if (r < rend) {
+            float2 p = pxy_row[r];
+            double d = Dsq[r];
+            wr[r] = make_float4((float)d, (float)(d * (p.x - cx) * sc), (float)(d * (p.y - cy) * sc), 0.0f);
+        } else {
+            wr[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    }
+}
+
+
+// E = W^T A^ W^ restricted to the rows of one aggregate (block per
+// aggregate). A^ = I + scaled off-diagonals + i (cn e_next - cp e_prev).
+// Every warp takes 32-row chunks; per neighbour aggregate b each lane forms
+// y_t = sum_j A^_ij w_j[t] over its row's entries in b, the 9 products
+// w_i[s] y_t are warp-summed into the warp's accumulator, and the warps'
+// accumulators are added in warp order (deterministic).
+constexpr int E_WARPS = 8;
+constexpr int E_NBMAX = 16;  // neighbour aggregates per aggregate
+
+__global__ void __launch_bounds__(32 * E_WARPS) k_coarse_E(
+        int32_t nslot, const int64_t* __restrict__ sl_off, const int64_t* __restrict__ sl_ptr,
+        const uint32_t* __restrict__ sl_mask, const int32_t* __restrict__ col, const double* __restrict__ val,
+        const int2* __restrict__ cpl, const double2* __restrict__ cplc, const int32_t* __restrict__ aoff,
+        const int32_t* __restrict__ aggr, const int64_t* __restrict__ abase, const float4* __restrict__ wr,
+        const int64_t* __restrict__ eoff, double2* __restrict__ E, int* __restrict__ overflow) {
+    __shared__ int s_flag[AGG_MAX];
+    __shared__ int s_nb[AGG_MAX];
+    __shared__ int s_cnt;
+    __shared__ double2 acc[E_WARPS][9 * E_NBMAX];
+    const int A = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t r0 = aoff[A], r1 = aoff[A + 1];
+    const int j = bsearch_off(sl_off, nslot + 1, r0 >> 5);
+    const int64_t rbase = 32 * sl_off[j];
+    const int a0 = (int)abase[j];
+    const int nag = (int)(abase[j + 1] - a0);
+    const int nc = 3 * nag;
+    for (int i = threadIdx.x; i < AGG_MAX; i += blockDim.x) s_flag[i] = 0;
+    for (int i = threadIdx.x; i < E_WARPS * 9 * E_NBMAX; i += blockDim.x)
+        acc[i / (9 * E_NBMAX)][i % (9 * E_NBMAX)] = make_double2(0.0, 0.0);
+    __syncthreads();
+    for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+        const int64_t s = r >> 5;
+        const int ln = (int)(r & 31);
+        const int64_t e0 = sl_ptr[s];
+        const int wdt = (int)((sl_ptr[s + 1] - e0) >> 5);
+        s_flag[aggr[r] - a0] = 1;
+        for (int k = 0; k < wdt; ++k) s_flag[aggr[rbase + col[sell_pos(e0, k, ln)]] - a0] = 1;
+        if (sl_mask[s] & (1u << ln)) {
+            int2 nb = cpl[r];
+            if (nb.x >= 0) s_flag[aggr[rbase + nb.x] - a0] = 1;
+            if (nb.y >= 0) s_flag[aggr[rbase + nb.y] - a0] = 1;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int c = 0;
+        for (int i = 0; i < nag && i < AGG_MAX; ++i)
+            if (s_flag[i]) {
+                if (c < E_NBMAX) s_nb[c] = i;
+                ++c;
+            }
+        if (c > E_NBMAX) {
+            atomicExch(overflow, 1);
+            c = E_NBMAX;
+        }
+        s_cnt = c;
+    }
+    __syncthreads();
+    const int NB = s_cnt;
+    for (int64_t cbase = r0 + 32 * warp; cbase < r1; cbase += 32 * E_WARPS) {
+        const int64_t r = cbase + lane;
+        const bool have = r < r1;
+        float4 wi = make_float4(0.f, 0.f, 0.f, 0.f);
+        int64_t e0 = 0;
+        int wdt = 0, ln = 0, ai = -1;
+        bool cp = false;
+        int2 nb = make_int2(-1, -1);
+        double2 cc = make_double2(0.0, 0.0);
+        if (have) {
+            wi = wr[r];
+            const int64_t s = r >> 5;
+            ln = (int)(r & 31);
+            e0 = sl_ptr[s];
+            wdt = (int)((sl_ptr[s + 1] - e0) >> 5);
+            ai = aggr[r];
+            cp = (sl_mask[s] >> ln) & 1u;
+            if (cp) {
+                nb = cpl[r];
+                cc = cplc[r];
+            }
+        }
+        for (int bi = 0; bi < NB; ++bi) {
+            const int b = s_nb[bi] + a0;
+            double yr[3] = {0.0, 0.0, 0.0}, yi[3] = {0.0, 0.0, 0.0};
+            if (have) {
+                if (ai == b) {
+                    yr[0] += wi.x;
+                    yr[1] += wi.y;
+                    yr[2] += wi.z;
+                }
+                for (int k = 0; k < wdt; ++k) {
+                    const int64_t q = sell_pos(e0, k, ln);
+                    const int64_t rc = rbase + col[q];
+                    if (aggr[rc] == b) {
+                        const float4 wc = wr[rc];
+                        const double v = val[q];
+                        yr[0] += v * wc.x;
+                        yr[1] += v * wc.y;
+                        yr[2] += v * wc.z;
+                    }
+                }
+                if (cp) {
+                    if (nb.x >= 0 && aggr[rbase + nb.x] == b) {
+                        const float4 wc = wr[rbase + nb.x];
+                        yi[0] += cc.x * wc.x;
+                        yi[1] += cc.x * wc.y;
+                        yi[2] += cc.x * wc.z;
+                    }
+                    if (nb.y >= 0 && aggr[rbase + nb.y] == b) {
+                        const float4 wc = wr[rbase + nb.y];
+                        yi[0] -= cc.y * wc.x;
+                        yi[1] -= cc.y * wc.y;
+                        yi[2] -= cc.y * wc.z;
+                    }
+                }
+            }
+            const double ws[3] = {(double)wi.x, (double)wi.y, (double)wi.z};
+#pragma unroll
+            for (int sx = 0; sx < 3; ++sx)
+#pragma unroll
+                for (int t = 0; t < 3; ++t) {
+                    double cr = warp_sum(ws[sx] * yr[t]);
+                    double ci = warp_sum(ws[sx] * yi[t]);
+                    if (lane == 0) {
+                        double2& a = acc[warp][(sx * E_NBMAX + bi) * 3 + t];
+                        a.x += cr;
+                        a.y += ci;
+                    }
+                }
+        }
+    }
+    __syncthreads();
+    double2* Eslot = E + eoff[j];
+    const int arow = A - a0;
+    for (int t = threadIdx.x; t < 9 * NB; t += blockDim.x) {
+        const int sx = t / (3 * NB), rem = t % (3 * NB), bi = rem / 3, tt = rem % 3;
+        double2 v = make_double2(0.0, 0.0);
+        for (int w = 0; w < E_WARPS; ++w) {
+            const double2 a = acc[w][(sx * E_NBMAX + bi) * 3 + tt];
+            v.x += a.x;
+            v.y += a.y;
+        }
+        Eslot[(int64_t)(3 * arow + sx) * nc + 3 * s_nb[bi] + tt] = v;
+    }
+}
+
+// In-place Gauss-Jordan inverse of every slot's Hermitian positive
+// semi-definite E on a thread-block cluster: the rows are spread over the
+// CTAs' shared memory, the pivot row is broadcast through DSMEM (double
+// buffered, one cluster barrier per pivot). Coarse functions whose pivot
+// falls below 1e-10 of the largest diagonal are dependent and dropped
+// (row/col zeroed). Output: E^-1, made exactly Hermitian.
+constexpr int INV_THREADS = 512;
+
+__global__ void __launch_bounds__(INV_THREADS, 1) k_coarse_inv(const int64_t* __restrict__ abase,
+                                                               const int64_t* __restrict__ eoff,
+                                                               double2* __restrict__ E) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    cg::cluster_group cl = cg::this_cluster();
+    const int CS = (int)cl.num_blocks();
+    const int rank = (int)cl.block_rank();
+    const int j = blockIdx.x / CS;
+    const int n = 3 * (int)(abase[j + 1] - abase[j]);
+    const int rpc = (n + CS - 1) / CS;                 // rows per CTA
+    const int i0 = min(n, rank * rpc), i1 = min(n, i0 + rpc);
+    const int nr = i1 - i0;
+    double2* Ml = reinterpret_cast<double2*>(smem);    // [rpc][n] my rows
+    double2* rowk = Ml + (size_t)rpc * n;              // [2][n] pivot row (broadcast)
+    double2* colk = rowk + 2 * n;                      // [rpc]  my entries of the pivot column
+    double* s_misc = reinterpret_cast<double*>(colk + rpc);  // [0] dref
+    double2* M = E + eoff[j];
+    for (int t = threadIdx.x; t < nr * n; t += INV_THREADS) Ml[t] = M[(int64_t)i0 * n + t];
+    if (threadIdx.x == 0) {
+        double d = 0.0;
+        for (int i = 0; i < n; ++i) d = fmax(d, M[(int64_t)i * n + i].x);
+        s_misc[0] = d;
+    }
+    __syncthreads();
+    const double tol = 1e-10 * s_misc[0];
+    // pivot row 0 -> everyone
+    int par = 0;
+    auto publish = [&](int k, int pr) {
+        if (k < n && k >= i0 && k < i1) {
+            for (int q = threadIdx.x; q < n * CS; q += INV_THREADS) {
+                const int c = q / CS, dst = q - c * CS;
+                double2* rk = cl.map_shared_rank(rowk + pr * n, dst);
+                rk[c] = Ml[(size_t)(k - i0) * n + c];
+            }
+        }
+    };
+    publish(0, par);
+    cl.sync();
+    for (int k = 0; k < n; ++k) {
+        const double2* rk = rowk + par * n;
+        const double p = rk[k].x;
+        const bool drop = !(p > tol);
+        for (int i = threadIdx.x; i < nr; i += INV_THREADS) colk[i] = Ml[(size_t)i * n + k];
+        __syncthreads();
+        if (drop) {
+            for (int t = threadIdx.x; t < nr * n; t += INV_THREADS) {
+                const int i = t / n, c = t - i * n;
+                if (i0 + i == k || c == k) Ml[t] = make_double2(0.0, 0.0);
+            }
+        } else {
+            const double ip = 1.0 / p;
+            for (int t = threadIdx.x; t < nr * n; t += INV_THREADS) {
+                const int i = t / n, c = t - i * n;
+                const int gi = i0 + i;
+                double2 v;
+                if (gi == k && c == k) {
+                    v = make_double2(ip, 0.0);
+                } else if (gi == k) {
+                    v = make_double2(rk[c].x * ip, rk[c].y * ip);
+                } else if (c == k) {
+                    v = make_double2(-colk[i].x * ip, -colk[i].y * ip);
+                } else {
+                    const double2 a = colk[i], b = rk[c];
+                    const double2 m = Ml[t];
+                    v = make_double2(m.x - (a.x * b.x - a.y * b.y) * ip, m.y - (a.x * b.y + a.y * b.x) * ip);
+                }
+                Ml[t] = v;
+            }
+        }
+        __syncthreads();
+        par ^= 1;
+        publish(k + 1, par);
+        cl.sync();
+    }
+    for (int t = threadIdx.x; t < nr * n; t += INV_THREADS) M[(int64_t)i0 * n + t] = Ml[t];
+}
+
+// float copy of (E^-1 + E^-H) / 2: exactly Hermitian after rounding (the
+// preconditioner stays symmetric), rows padded to a multiple of 8 columns
+__global__ void k_hermitize(const int64_t* __restrict__ abase, const int64_t* __restrict__ eoff,
+                            const double2* __restrict__ E, const int64_t* __restrict__ eoff32,
+                            float2* __restrict__ E32) {
+    const int j = blockIdx.x;
+    const int n = 3 * (int)(abase[j + 1] - abase[j]);
+    const int np = (n + 7) & ~7;
+    const double2* M = E + eoff[j];
+    float2* O = E32 + eoff32[j];
+    for (int64_t t = threadIdx.x; t < (int64_t)n * np; t += blockDim.x) {
+        const int i = (int)(t / np), c = (int)(t % np);
+        if (c >= n) {
+            O[t] = make_float2(0.f, 0.f);
+            continue;
+        }
+        const double2 a = M[(int64_t)i * n + c], b = M[(int64_t)c * n + i];
+        O[t] = (c < i) ? make_float2((float)(0.5 * (b.x + a.x)), -(float)(0.5 * (b.y - a.y)))
+                       : make_float2((float)(0.5 * (a.x + b.x)), (float)(0.5 * (a.y - b.y)));
+    }
+}
+
+struct CoarseArgs {
+    const int64_t* abase;    // slot -> first aggregate (global id), nslot + 1
+    const int32_t* aoff;     // aggregate -> first row (global padded row), NA + 1
+    const float4* wr;        // row -> scaled coarse weights (w0, w1, w2, 0)
+    const float2* einv32;    // per slot E^-1, row-major, rows padded to a multiple of 8 columns
+    const int64_t* eoff32;   // slot -> offset into einv32
+    double2* p;              // search direction (rows)
+};
+
 struct PcgArgs {
     const int64_t* sl_off;   // slot -> first slice
     const int64_t* sl_ptr;   // slice -> first entry
@@ -378,6 +1004,7 @@ struct PcgArgs {
     int32_t maxit;
     int32_t chunk_cap;       // slices per CTA the smem was sized for
     long long* timing;       // optional: per CTA [phaseA, red1, phaseB, red2] cycles (iterations 64..191)
+    CoarseArgs C;
 };
 
 // deterministic cluster-wide sum of two doubles: warp -> CTA (fixed order) ->
@@ -412,6 +1039,7 @@ constexpr int KPF = 8;  // prefetched off-diagonal entries per row (4 pairs)
 
 struct SliceBuf {
     double2 y;    // this lane's solution entry (updated in place, one owner thread)
+    double2 p;    // this lane's search direction (k_pcg2: p lives in global memory)
     int w;        // even width
     int remote;   // any entry of the slice owned by another CTA
     int off;      // entry offset of this lane's first pair, relative to the CTA's first entry
@@ -421,7 +1049,8 @@ struct SliceBuf {
 
 __device__ __forceinline__ void slice_load(SliceBuf& B, const double* __restrict__ valc,
                                            const uint32_t* __restrict__ encc, const int* s_ent, const int* s_w,
-                                           int ls, int nloc, int lane, const double2* yrow, bool need_y) {
+                                           int ls, int nloc, int lane, const double2* yrow, bool need_y,
+                                           const double2* prow = nullptr) {
     // entries past the width become (own row, 0.0): the gathers below are
     // straight-line and issue back to back
     const uint32_t self = (uint32_t)((32 * ls + lane) * 16);
@@ -435,6 +1064,7 @@ __device__ __forceinline__ void slice_load(SliceBuf& B, const double* __restrict
     }
     if (ls >= nloc) return;
     if (need_y) B.y = yrow[32 * ls + lane];
+    if (prow) B.p = prow[32 * ls + lane];
     B.w = s_w[ls] & 0xffff;
     B.remote = s_w[ls] >> 16;
     B.off = s_ent[ls] + (lane << 1);
@@ -645,7 +1275,7 @@ __global__ void __launch_bounds__(NT, 1) k_pcg(PcgArgs A) {
             if (rr <= stop || !(rr == rr)) break;
         }
         if (A.timing && threadIdx.x == 0) {
-            long long* t = A.timing + 4 * blockIdx.x;
+            long long* t = A.timing + 8 * blockIdx.x;
             t[0] = tA;
             t[1] = tR1;
             t[2] = tB;
@@ -664,6 +1294,380 @@ __global__ void __launch_bounds__(NT, 1) k_pcg(PcgArgs A) {
     if (rank == 0 && threadIdx.x == 0) {
         A.iters[slot] = it;
         A.res[8 * slot + 0] = (bbU > 0.0) ? sqrt(dmax * rr / bbU) : 0.0;  // upper bound of ||r||/||b||
+        A.res[8 * slot + 1] = bbU;
+    }
+}
+
+
+// ---------------------------------------------------------------------------
+// two-level PCG: one cluster per slot, z (the preconditioned residual, the
+// only gathered vector), q and r in distributed shared memory, p in global
+// memory (row-local). Three cluster reductions per iteration:
+//   A: q = A z + beta q; y += alpha p; p = z + beta p; <p,q>           [SYNC1]
+//   B: r -= alpha q; <r,r>; g = W^T r over my aggregates -> every CTA  [SYNC2]
+//   C: mu = E^-1 g on my aggregates; z = r + W^ mu; rho = <r,z>        [SYNC3]
+template <int NT>
+__global__ void __launch_bounds__(NT, 1) k_pcg2(PcgArgs A) {
+    constexpr int NW = NT / 32;
+    extern __shared__ __align__(16) unsigned char smem[];
+    cg::cluster_group cl = cg::this_cluster();
+    const int csize = (int)cl.num_blocks();
+    const int rank = (int)cl.block_rank();
+    const int slot = blockIdx.x / csize;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+
+    const int64_t s0 = A.sl_off[slot];
+    const int S = (int)(A.sl_off[slot + 1] - s0);
+    const int chunk = (S + csize - 1) / csize;
+    const int my_lo = min(S, rank * chunk);
+    const int nloc = min(S, my_lo + chunk) - my_lo;
+    const float inv_chunk = 1.0f / (float)chunk;
+    const int cap = A.chunk_cap;
+
+    double2* s_warp = reinterpret_cast<double2*>(smem);
+    double2* s_slot = s_warp + NW;
+    double2* zl = s_slot + 2 * MAX_CLUSTER;
+    double2* ql = zl + 32 * cap;
+    double2* rl = ql + 32 * cap;
+    double2* gbuf = rl + 32 * cap;          // [2][NC_MAX]
+    double2* mu = gbuf + 2 * NC_MAX;        // [NC_MAX] (my aggregates)
+    double* part = reinterpret_cast<double*>(mu + NC_MAX);  // [ITEMS_MAX][6]
+    int* s_ent = reinterpret_cast<int*>(part + 6 * ITEMS_MAX);
+    int* s_w = s_ent + cap;
+    uint32_t* s_mask = reinterpret_cast<uint32_t*>(s_w + cap);
+
+    __shared__ unsigned long long s_base[MAX_CLUSTER];
+    if (threadIdx.x < csize) s_base[threadIdx.x] = reinterpret_cast<unsigned long long>(cl.map_shared_rank(zl, threadIdx.x));
+    const int64_t gs0 = s0 + my_lo;
+    const int64_t row0 = 32 * gs0;
+    const int64_t rowN = row0 + 32 * (int64_t)nloc;
+    const int64_t ent0 = A.sl_ptr[gs0];
+    for (int t = threadIdx.x; t < nloc; t += NT) {
+        int64_t e = A.sl_ptr[gs0 + t];
+        s_ent[t] = (int)(e - ent0);
+        s_w[t] = (int)((A.sl_ptr[gs0 + t + 1] - e) >> 5) | ((int)A.remote[gs0 + t] << 16);
+        s_mask[t] = A.sl_mask[gs0 + t];
+    }
+    // my aggregates [a_lo, a_hi) (global ids; aggregates never straddle CTAs)
+    const int a0 = (int)A.C.abase[slot];
+    const int nag = (int)(A.C.abase[slot + 1] - a0);
+    const int nc = 3 * nag;
+    int a_lo = a0, a_hi = a0;
+    if (nloc > 0) {
+        int lo = a0, hi = a0 + nag;  // first aggregate starting at or after row0 / rowN
+        while (lo < hi) {
+            int mid = (lo + hi) >> 1;
+            if (A.C.aoff[mid] < row0) lo = mid + 1; else hi = mid;
+        }
+        a_lo = lo;
+        lo = a_lo;
+        hi = a0 + nag;
+        while (lo < hi) {
+            int mid = (lo + hi) >> 1;
+            if (A.C.aoff[mid] < rowN) lo = mid + 1; else hi = mid;
+        }
+        a_hi = lo;
+    }
+    const int naggs = a_hi - a_lo;
+    const int npart = max(1, NW / max(naggs, 1));
+    const int nitems = naggs * npart;
+    const int ncp = (nc + 7) & ~7;  // padded row stride of the float copy
+    const float2* Einv = A.C.einv32 + A.C.eoff32[slot];
+    const int crow0 = 3 * (a_lo - a0);  // my first coarse row
+    double2* pg = A.C.p;
+    const float4* wr = A.C.wr;
+
+    auto item_range = [&](int t, int& a_rel, int64_t& rb, int64_t& re) {
+        a_rel = t / npart;
+        const int pt = t - a_rel * npart;
+        const int64_t r0 = A.C.aoff[a_lo + a_rel], r1 = A.C.aoff[a_lo + a_rel + 1];
+        const int64_t per = (r1 - r0 + npart - 1) / npart;
+        rb = r0 + pt * per;
+        re = min(r1, rb + per);
+    };
+    // B: (optionally r -= alpha q), <r,r>, g = W^T r for my aggregates, sent
+    // to every CTA's gbuf[par]; returns this thread's <r,r> share
+    auto restrict_r = [&](bool upd, double alpha, int par) -> double {
+        double l_rr = 0.0;
+        for (int t = warp; t < nitems; t += NW) {
+            int a_rel;
+            int64_t rb, re;
+            item_range(t, a_rel, rb, re);
+            double g0x = 0, g0y = 0, g1x = 0, g1y = 0, g2x = 0, g2y = 0;
+            for (int64_t rq = rb + lane; rq < re; rq += 128) {
+                float4 w[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int64_t r = rq + 32 * u;
+                    w[u] = r < re ? wr[r] : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int64_t r = rq + 32 * u;
+                    if (r >= re) break;
+                    const int li = (int)(r - row0);
+                    double2 ri = rl[li];
+                    if (upd) {
+                        const double2 qi = ql[li];
+                        ri.x = fma(-alpha, qi.x, ri.x);
+                        ri.y = fma(-alpha, qi.y, ri.y);
+                        rl[li] = ri;
+                    }
+                    l_rr += ri.x * ri.x + ri.y * ri.y;
+                    g0x = fma((double)w[u].x, ri.x, g0x);
+                    g0y = fma((double)w[u].x, ri.y, g0y);
+                    g1x = fma((double)w[u].y, ri.x, g1x);
+                    g1y = fma((double)w[u].y, ri.y, g1y);
+                    g2x = fma((double)w[u].z, ri.x, g2x);
+                    g2y = fma((double)w[u].z, ri.y, g2y);
+                }
+            }
+            g0x = warp_sum(g0x);
+            g0y = warp_sum(g0y);
+            g1x = warp_sum(g1x);
+            g1y = warp_sum(g1y);
+            g2x = warp_sum(g2x);
+            g2y = warp_sum(g2y);
+            if (lane == 0) {
+                double* pp = part + 6 * t;
+                pp[0] = g0x;
+                pp[1] = g0y;
+                pp[2] = g1x;
+                pp[3] = g1y;
+                pp[4] = g2x;
+                pp[5] = g2y;
+            }
+        }
+        if (upd) {  // rows outside every aggregate do not exist; all rows are covered above
+        }
+        __syncthreads();
+        for (int q = threadIdx.x; q < 3 * naggs * csize; q += NT) {
+            const int cq = q / csize, dst = q - cq * csize;
+            const int a_rel = cq / 3, sidx = cq - 3 * a_rel;
+            double gx = 0.0, gy = 0.0;
+            for (int pt = 0; pt < npart; ++pt) {
+                const double* pp = part + 6 * (a_rel * npart + pt);
+                gx += pp[2 * sidx];
+                gy += pp[2 * sidx + 1];
+            }
+            double2* gb = cl.map_shared_rank(gbuf + par * NC_MAX, dst);
+            gb[crow0 + cq] = make_double2(gx, gy);
+        }
+        return l_rr;
+    };
+    // C: mu = E^-1 g (my coarse rows), z = r + W^ mu, returns <r,z> share
+    auto prolong_z = [&](int par) -> double {
+        const double2* g = gbuf + par * NC_MAX;
+        for (int q = warp; q < 3 * naggs; q += NW) {
+            const float2* er = Einv + (int64_t)(crow0 + q) * ncp;
+            double mx = 0.0, my = 0.0;
+            float2 e[NC_MAX / 32];
+#pragma unroll
+            for (int u = 0; u < NC_MAX / 32; ++u) {  // lane-strided columns: coalesced, conflict-free
+                const int c = lane + 32 * u;
+                e[u] = c < nc ? er[c] : make_float2(0.f, 0.f);
+            }
+#pragma unroll
+            for (int u = 0; u < NC_MAX / 32; ++u) {
+                const int c = lane + 32 * u;
+                if (c < nc) {
+                    const double2 gg = g[c];
+                    mx = fma((double)e[u].x, gg.x, mx);
+                    mx = fma(-(double)e[u].y, gg.y, mx);
+                    my = fma((double)e[u].x, gg.y, my);
+                    my = fma((double)e[u].y, gg.x, my);
+                }
+            }
+            mx = warp_sum(mx);
+            my = warp_sum(my);
+            if (lane == 0) mu[q] = make_double2(mx, my);
+        }
+        __syncthreads();
+        double l_rz = 0.0;
+        for (int t = warp; t < nitems; t += NW) {
+            int a_rel;
+            int64_t rb, re;
+            item_range(t, a_rel, rb, re);
+            const double2 m0 = mu[3 * a_rel], m1 = mu[3 * a_rel + 1], m2 = mu[3 * a_rel + 2];
+            for (int64_t rq = rb + lane; rq < re; rq += 128) {
+                float4 w[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int64_t r = rq + 32 * u;
+                    w[u] = r < re ? wr[r] : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int64_t r = rq + 32 * u;
+                    if (r >= re) break;
+                    const int li = (int)(r - row0);
+                    const double2 ri = rl[li];
+                    double2 zi;
+                    zi.x = ri.x + (double)w[u].x * m0.x + (double)w[u].y * m1.x + (double)w[u].z * m2.x;
+                    zi.y = ri.y + (double)w[u].x * m0.y + (double)w[u].y * m1.y + (double)w[u].z * m2.y;
+                    zl[li] = zi;
+                    l_rz += ri.x * zi.x + ri.y * zi.y;
+                }
+            }
+        }
+        return l_rz;
+    };
+
+    // init: y = 0 (builder), r = b, p = q = 0; coarse buffers zero (columns
+    // past nc meet zero padding of E^-1 and must not hold NaN garbage)
+    for (int i = threadIdx.x; i < 2 * NC_MAX; i += NT) gbuf[i] = make_double2(0.0, 0.0);
+    double l_rr = 0.0, l_bb = 0.0;
+    for (int i = threadIdx.x; i < 32 * nloc; i += NT) {
+        double2 bi = A.b[row0 + i];
+        double di = A.D[row0 + i];
+        rl[i] = bi;
+        zl[i] = bi;
+        ql[i] = make_double2(0.0, 0.0);
+        pg[row0 + i] = make_double2(0.0, 0.0);
+        double m2 = bi.x * bi.x + bi.y * bi.y;
+        l_rr += m2;
+        l_bb += di * m2;
+    }
+    int parity = 0, gpar = 0;
+    double2 t0 = cluster_sum2<NW>(cl, csize, rank, l_rr, l_bb, s_warp, s_slot, parity);
+    parity ^= 1;
+    double rr = t0.x;
+    const double bbU = t0.y;
+    const double dmax = A.dmax[slot];
+    const double stop = A.tol2 * bbU / dmax;
+    double beta = 0.0, alpha = 0.0, rho = 0.0;
+    int it = 0;
+    const bool active = bbU > 0.0 && rr > stop;
+
+    if (active) {
+        // z0 = M r0, rho0 = <r0, z0>
+        restrict_r(false, 0.0, gpar);
+        cluster_sum2<NW>(cl, csize, rank, 0.0, 0.0, s_warp, s_slot, parity);
+        parity ^= 1;
+        double l_rz = prolong_z(gpar);
+        gpar ^= 1;
+        double2 tz = cluster_sum2<NW>(cl, csize, rank, l_rz, 0.0, s_warp, s_slot, parity);
+        parity ^= 1;
+        rho = tz.x;
+        const double* valc = A.val + ent0;
+        const uint32_t* encc = A.enc + ent0;
+        double2* yrow = A.x + row0;
+        double2* prow = pg + row0;
+        long long tm[6] = {0, 0, 0, 0, 0, 0};
+        for (it = 0; it < A.maxit;) {
+            const bool timed = A.timing && it >= 64 && it < 192;
+            long long c0 = timed ? clock64() : 0;
+            // ---- A: q = A z + beta q, y += alpha p_old, p = z + beta p, <p,q>
+            double l_pq = 0.0;
+            SliceBuf B0, B1;
+            slice_load(B0, valc, encc, s_ent, s_w, warp, nloc, lane, yrow, it > 0, prow);
+            for (int ls = warp; ls < nloc; ls += 2 * NW) {
+#pragma unroll
+                for (int half = 0; half < 2; ++half) {
+                    const int cur = ls + half * NW;
+                    SliceBuf& Bc = half ? B1 : B0;
+                    SliceBuf& Bn = half ? B0 : B1;
+                    slice_load(Bn, valc, encc, s_ent, s_w, cur + NW, nloc, lane, yrow, it > 0, prow);
+                    if (cur < nloc) {
+                        const int li = 32 * cur + lane;
+                        const int64_t gr = row0 + li;
+                        double2 zi = zl[li];
+                        double sx = zi.x, sy = zi.y;
+                        double2 g[KPF];
+                        if (!Bc.remote) {
+#pragma unroll
+                            for (int k = 0; k < KPF; ++k)
+                                g[k] = *reinterpret_cast<const double2*>(reinterpret_cast<const char*>(zl) + Bc.c[k]);
+                        } else {
+#pragma unroll
+                            for (int k = 0; k < KPF; ++k) g[k] = gather_gen(s_base, rank, Bc.c[k]);
+                        }
+#pragma unroll
+                        for (int k = 0; k < KPF; ++k) {
+                            sx = fma(Bc.v[k], g[k].x, sx);
+                            sy = fma(Bc.v[k], g[k].y, sy);
+                        }
+                        for (int k = KPF; k < Bc.w; ++k) {
+                            const int e = Bc.off + ((k >> 1) << 6) + (k & 1);
+                            uint32_t c = __ldg(encc + e);
+                            double v = __ldg(valc + e);
+                            double2 rc = gather_enc(s_base, zl, c);
+                            sx = fma(v, rc.x, sx);
+                            sy = fma(v, rc.y, sy);
+                        }
+                        if (s_mask[cur] & (1u << lane)) {
+                            int2 nb = A.cpl[gr];
+                            double2 cc = A.cplc[gr];
+                            double2 zn = nb.x >= 0 ? gather(cl, zl, nb.x, rank, chunk, inv_chunk) : make_double2(0, 0);
+                            double2 zp = nb.y >= 0 ? gather(cl, zl, nb.y, rank, chunk, inv_chunk) : make_double2(0, 0);
+                            double ax = cc.x * zn.x - cc.y * zp.x, ay = cc.x * zn.y - cc.y * zp.y;
+                            sx -= ay;
+                            sy += ax;
+                        }
+                        double2 qi = ql[li];
+                        double2 pi = Bc.p;
+                        if (it > 0) {
+                            double2 yv = Bc.y;
+                            yv.x = fma(alpha, pi.x, yv.x);
+                            yv.y = fma(alpha, pi.y, yv.y);
+                            yrow[li] = yv;
+                        }
+                        qi.x = fma(beta, qi.x, sx);
+                        qi.y = fma(beta, qi.y, sy);
+                        pi.x = fma(beta, pi.x, zi.x);
+                        pi.y = fma(beta, pi.y, zi.y);
+                        ql[li] = qi;
+                        prow[li] = pi;
+                        l_pq += pi.x * qi.x + pi.y * qi.y;
+                    }
+                }
+            }
+            long long c1 = timed ? clock64() : 0;
+            double2 tq = cluster_sum2<NW>(cl, csize, rank, l_pq, 0.0, s_warp, s_slot, parity);
+            parity ^= 1;
+            alpha = rho / tq.x;
+            long long c2 = timed ? clock64() : 0;
+            // ---- B: r -= alpha q, <r,r>, g = W^T r
+            double l_rr2 = restrict_r(true, alpha, gpar);
+            long long c3 = timed ? clock64() : 0;
+            double2 tr = cluster_sum2<NW>(cl, csize, rank, l_rr2, 0.0, s_warp, s_slot, parity);
+            parity ^= 1;
+            rr = tr.x;
+            ++it;
+            if (rr <= stop || !(rr == rr)) break;
+            long long c4 = timed ? clock64() : 0;
+            // ---- C: z = M r, rho = <r,z>
+            double l_rz2 = prolong_z(gpar);
+            gpar ^= 1;
+            long long c5 = timed ? clock64() : 0;
+            double2 tz2 = cluster_sum2<NW>(cl, csize, rank, l_rz2, 0.0, s_warp, s_slot, parity);
+            parity ^= 1;
+            beta = tz2.x / rho;
+            rho = tz2.x;
+            if (timed) {
+                long long c6 = clock64();
+                tm[0] += c1 - c0;
+                tm[1] += c2 - c1;
+                tm[2] += c3 - c2;
+                tm[3] += c4 - c3;
+                tm[4] += c5 - c4;
+                tm[5] += c6 - c5;
+            }
+        }
+        if (A.timing && threadIdx.x == 0)
+            for (int q = 0; q < 6; ++q) A.timing[8 * blockIdx.x + q] = tm[q];
+        // the last update y += alpha p
+        for (int i = threadIdx.x; i < 32 * nloc; i += NT) {
+            double2 pi = prow[i];
+            double2 yv = yrow[i];
+            yv.x = fma(alpha, pi.x, yv.x);
+            yv.y = fma(alpha, pi.y, yv.y);
+            yrow[i] = yv;
+        }
+    }
+    if (rank == 0 && threadIdx.x == 0) {
+        A.iters[slot] = it;
+        A.res[8 * slot + 0] = (bbU > 0.0) ? sqrt(dmax * rr / bbU) : 0.0;
         A.res[8 * slot + 1] = bbU;
     }
 }
@@ -809,8 +1813,8 @@ __global__ void k_flat_checks(const int32_t* __restrict__ comps, const int64_t* 
 // ---------------------------------------------------------------------------
 // host side
 
-int pick_cluster(int64_t max_slices, int32_t nslot, int32_t forced, int* csize_out, int* chunk_out) {
-    const int max_chunk = (SMEM_LIMIT - RED_BYTES) / (48 * 32 + 12);
+int pick_cluster(int64_t max_slices, int32_t nslot, int32_t forced, bool coarse, int* csize_out, int* chunk_out) {
+    const int max_chunk = (SMEM_LIMIT - RED_BYTES - (coarse ? COARSE_BYTES : 0)) / (48 * 32 + 12);
     int cmin = 1;
     while (cmin <= MAX_CLUSTER && (max_slices + cmin - 1) / cmin > max_chunk) cmin *= 2;
     if (cmin > MAX_CLUSTER) {
@@ -860,13 +1864,44 @@ int launch_pcg_t(SolveSystem* S, const PcgArgs& args, int csize, size_t smem, cu
     return PGCP_OK;
 }
 
+template <int NT>
+int launch_pcg2_t(SolveSystem* S, const PcgArgs& args, int csize, size_t smem, cudaStream_t s) {
+    auto kern = k_pcg2<NT>;
+    PGCP_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (csize > 8) PGCP_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(S->nslot * csize), 1, 1);
+    cfg.blockDim = dim3(NT, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = csize;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int nclusters = 0;
+    cudaError_t oe = cudaOccupancyMaxActiveClusters(&nclusters, kern, &cfg);
+    if (oe != cudaSuccess || nclusters < 1) {
+        set_error("pcg: cluster of %d CTAs with %zu B shared memory cannot be scheduled (%s)", csize, smem,
+                  cudaGetErrorString(oe));
+        cudaGetLastError();
+        return PGCP_E_CUDA;
+    }
+    PGCP_TRY_CUDA(cudaLaunchKernelEx(&cfg, kern, args));
+    return PGCP_OK;
+}
+
 int launch_pcg(SolveSystem* S, const PcgArgs& args, int csize, cudaStream_t s) {
     int chunk = args.chunk_cap;
-    size_t smem = (size_t)RED_BYTES + (size_t)3 * 32 * chunk * sizeof(double2) + (size_t)12 * chunk;
+    size_t smem = (size_t)RED_BYTES + (size_t)3 * 32 * chunk * sizeof(double2) + (size_t)12 * chunk +
+                  (S->coarse ? (size_t)COARSE_BYTES : 0);
     if (smem > SMEM_LIMIT) {
         set_error("pcg: shared memory %zu exceeds limit", smem);
         return PGCP_E_INVALID;
     }
+    if (S->coarse) return launch_pcg2_t<512>(S, args, csize, smem, s);
     const char* v = getenv("PGCP_PCG_VARIANT");
     int variant = v ? atoi(v) : 0;
     switch (variant) {
@@ -876,6 +1911,176 @@ int launch_pcg(SolveSystem* S, const PcgArgs& args, int csize, cudaStream_t s) {
         case 4: return launch_pcg_t<256, true>(S, args, csize, smem, s);
         default: return launch_pcg_t<512, true>(S, args, csize, smem, s);
     }
+}
+
+// Coarse-space row order (see k_pcg2): unknowns sorted by (slot, strip of
+// the first principal axis, second principal coordinate). Sets urow/rowsrc,
+// the cell of every row and its cell coordinates.
+int order_rows_by_cell(pgcp_batch* b, SolveSystem* S, const int64_t* uscan, const std::vector<int64_t>& hus,
+                       cudaStream_t s) {
+    const int32_t nslot = S->nslot;
+    const int64_t nU = hus[nslot] - hus[0];
+    PGCP_TRY(S->urow.fill_bytes(0xff, s));
+    PGCP_TRY(S->cell.alloc(S->rows, s));
+    PGCP_TRY(S->cell.zero(s));
+    PGCP_TRY(S->pxy_row.alloc(S->rows, s));
+    PGCP_TRY(S->pxy_row.zero(s));
+    if (nU <= 0) return PGCP_OK;
+    DevBuf<double> frame;
+    DevBuf<float2> pxy;
+    DevBuf<unsigned long long> k1, k2;
+    DevBuf<int32_t> v1, v2;
+    PGCP_TRY(frame.alloc(9 * (int64_t)nslot, s));
+    PGCP_TRY(pxy.alloc(nU, s));
+    PGCP_TRY(k1.alloc(nU, s));
+    PGCP_TRY(k2.alloc(nU, s));
+    PGCP_TRY(v1.alloc(nU, s));
+    PGCP_TRY(v2.alloc(nU, s));
+    k_pca<<<nslot, 256, 0, s>>>(nslot, S->d_comps.p, S->sv_off.p, b->vert_off.p, b->vmap.p, b->V.p, S->fixed_ref.p,
+                                frame.p);
+    PGCP_LAUNCH_CHECK();
+    DevBuf<uint32_t> bbox;
+    PGCP_TRY(bbox.alloc(4 * (int64_t)nslot, s));
+    {
+        std::vector<uint32_t> hb(4 * (size_t)nslot);
+        for (int j = 0; j < nslot; ++j) {
+            hb[4 * j] = 0xffffffffu;
+            hb[4 * j + 1] = 0u;
+            hb[4 * j + 2] = 0xffffffffu;
+            hb[4 * j + 3] = 0u;
+        }
+        PGCP_TRY_CUDA(cudaMemcpyAsync(bbox.p, hb.data(), hb.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+        PGCP_TRY_CUDA(cudaStreamSynchronize(s));  // hb is a local
+    }
+    k_proj<<<grid_for(S->ne, 256), 256, 0, s>>>(S->ne, nslot, S->d_comps.p, S->sv_off.p, b->vert_off.p, b->vmap.p,
+                                              b->V.p, S->fixed_ref.p, uscan, frame.p, pxy.p, k1.p, v1.p, bbox.p);
+    PGCP_LAUNCH_CHECK();
+    int sbits = 1;
+    while ((1ll << sbits) <= nslot) ++sbits;
+    size_t tmp_bytes = 0, t2 = 0;
+    PGCP_TRY_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k1.p, k2.p, v1.p, v2.p, (int)nU, 0, 32 + sbits, s));
+    PGCP_TRY_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t2, k2.p, k1.p, v2.p, v1.p, (int)nU, 0, 40 + sbits, s));
+    DevBuf<unsigned char> tmp;
+    PGCP_TRY(tmp.alloc((int64_t)std::max(tmp_bytes, t2), s));
+    tmp_bytes = std::max(tmp_bytes, t2);
+    PGCP_TRY_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, k1.p, k2.p, v1.p, v2.p, (int)nU, 0, 32 + sbits, s));
+    count_launch();
+    // sorted (k2, v2) -> strip keys into (k1, v1)
+    k_strip<<<grid_for(nU, 256), 256, 0, s>>>(nU, k2.p, v2.p, S->sv_off.p, uscan, pxy.p, S->gmax, k1.p, v1.p);
+    PGCP_LAUNCH_CHECK();
+    PGCP_TRY_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, k1.p, k2.p, v1.p, v2.p, (int)nU, 0, 40 + sbits, s));
+    count_launch();
+    k_cell_keys<<<grid_for(nU, 256), 256, 0, s>>>(nU, k2.p, v2.p, S->sv_off.p, uscan, pxy.p, bbox.p, S->gmax, k1.p,
+                                                v1.p);
+    PGCP_LAUNCH_CHECK();
+    PGCP_TRY_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, k1.p, k2.p, v1.p, v2.p, (int)nU, 0, 40 + sbits, s));
+    count_launch();
+    k_rows_by_cell<<<grid_for(nU, 256), 256, 0, s>>>(nU, k2.p, v2.p, S->sv_off.p, S->sl_off.p, uscan, pxy.p, S->gmax,
+                                                   S->urow.p, S->rowsrc.p, S->cell.p, S->pxy_row.p);
+    PGCP_LAUNCH_CHECK();
+    return PGCP_OK;
+}
+
+// Aggregates for the cluster split `csize`, coarse weights, E and E^-1.
+int build_coarse(SolveSystem* S, int csize, cudaStream_t s) {
+    const int32_t nslot = S->nslot;
+    std::vector<int64_t> hnu(S->h_nu.begin(), S->h_nu.end());
+    PGCP_TRY(S->nu_d.alloc(nslot, s));
+    PGCP_TRY_CUDA(cudaMemcpyAsync(S->nu_d.p, hnu.data(), nslot * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    DevBuf<int32_t> flag;
+    DevBuf<int64_t> scan;
+    PGCP_TRY(flag.alloc(S->rows, s));
+    PGCP_TRY(scan.alloc(S->rows + 1, s));
+    k_agg_flag<<<grid_for(S->rows, 256), 256, 0, s>>>(S->rows, nslot, S->sl_off.p, S->nu_d.p, S->cell.p, csize,
+                                                    flag.p);
+    PGCP_LAUNCH_CHECK();
+    PGCP_TRY(exclusive_scan_i32_to_i64(flag.p, scan.p, S->rows, s));
+    S->h_abase.assign(nslot + 1, 0);
+    PGCP_TRY(S->abase.alloc(nslot + 1, s));
+    k_slot_abase<<<grid_for(nslot + 1, 128), 128, 0, s>>>(nslot, S->sl_off.p, scan.p, S->abase.p);
+    PGCP_LAUNCH_CHECK();
+    PGCP_TRY_CUDA(cudaMemcpyAsync(S->h_abase.data(), S->abase.p, (nslot + 1) * sizeof(int64_t),
+                                  cudaMemcpyDeviceToHost, s));
+    PGCP_TRY_CUDA(cudaStreamSynchronize(s));
+    const int64_t NA = S->h_abase[nslot];
+    std::vector<int64_t> heoff(nslot + 1, 0);
+    for (int j = 0; j < nslot; ++j) {
+        int64_t na = S->h_abase[j + 1] - S->h_abase[j];
+        if (na > AGG_MAX) {
+            set_error("coarse space: %lld aggregates in one subdomain (max %d)", (long long)na, AGG_MAX);
+            return PGCP_E_INVALID;
+        }
+        heoff[j + 1] = heoff[j] + 9 * na * na;
+    }
+    PGCP_TRY(S->aggr.alloc(S->rows, s));
+    PGCP_TRY(S->aoff.alloc(NA + 1, s));
+    k_agg_index<<<grid_for(S->rows, 256), 256, 0, s>>>(S->rows, flag.p, scan.p, S->aggr.p, S->aoff.p);
+    PGCP_LAUNCH_CHECK();
+    const int32_t rows32 = (int32_t)S->rows;
+    PGCP_TRY_CUDA(cudaMemcpyAsync(S->aoff.p + NA, &rows32, sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    PGCP_TRY(S->eoff.alloc(nslot + 1, s));
+    PGCP_TRY_CUDA(cudaMemcpyAsync(S->eoff.p, heoff.data(), (nslot + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    PGCP_TRY(S->wr.alloc(S->rows, s));
+    k_agg_weights<<<(unsigned)NA, 128, 0, s>>>((int32_t)NA, S->aoff.p, nslot, S->sl_off.p, S->nu_d.p, S->pxy_row.p,
+                                              S->Dsq.p, S->wr.p);
+    PGCP_LAUNCH_CHECK();
+    PGCP_TRY(S->einv.alloc(heoff[nslot], s));
+    PGCP_TRY(S->einv.zero(s));
+    DevBuf<int> ovf;
+    PGCP_TRY(ovf.alloc(1, s));
+    PGCP_TRY(ovf.zero(s));
+    k_coarse_E<<<(unsigned)NA, 32 * E_WARPS, 0, s>>>(nslot, S->sl_off.p, S->sl_ptr.p, S->sl_mask.p, S->col.p,
+                                                    S->val.p, S->cpl.p, S->cplc.p, S->aoff.p, S->aggr.p,
+                                                    S->abase.p, S->wr.p, S->eoff.p, S->einv.p, ovf.p);
+    PGCP_LAUNCH_CHECK();
+    {
+        int nmax = 0;
+        for (int j = 0; j < nslot; ++j) nmax = std::max<int>(nmax, 3 * (int)(S->h_abase[j + 1] - S->h_abase[j]));
+        int CS = 1;
+        auto inv_smem = [&](int cs) {
+            int rpc = (nmax + cs - 1) / cs;
+            return (size_t)rpc * nmax * 16 + (size_t)2 * nmax * 16 + (size_t)rpc * 16 + 64;
+        };
+        while (CS < 16 && inv_smem(CS) > 200 * 1024) CS *= 2;
+        const size_t smem = inv_smem(CS);
+        PGCP_TRY_CUDA(cudaFuncSetAttribute(k_coarse_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        if (CS > 8) PGCP_TRY_CUDA(cudaFuncSetAttribute(k_coarse_inv, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)(nslot * CS), 1, 1);
+        cfg.blockDim = dim3(INV_THREADS, 1, 1);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = CS;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        PGCP_TRY_CUDA(cudaLaunchKernelEx(&cfg, k_coarse_inv, S->abase.p, S->eoff.p, S->einv.p));
+        PGCP_LAUNCH_CHECK();
+        std::vector<int64_t> he32(nslot + 1, 0);
+        for (int j = 0; j < nslot; ++j) {
+            int64_t n = 3 * (S->h_abase[j + 1] - S->h_abase[j]);
+            he32[j + 1] = he32[j] + n * ((n + 7) & ~7ll);
+        }
+        PGCP_TRY(S->eoff32.alloc(nslot + 1, s));
+        PGCP_TRY_CUDA(cudaMemcpyAsync(S->eoff32.p, he32.data(), (nslot + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+        PGCP_TRY(S->einv32.alloc(std::max<int64_t>(he32[nslot], 1), s));
+        k_hermitize<<<nslot, 512, 0, s>>>(S->abase.p, S->eoff.p, S->einv.p, S->eoff32.p, S->einv32.p);
+        PGCP_LAUNCH_CHECK();
+        PGCP_TRY_CUDA(cudaStreamSynchronize(s));  // he32 is a local
+    }
+    PGCP_TRY(S->p.alloc(S->rows, s));
+    int hovf = 0;
+    PGCP_TRY_CUDA(cudaMemcpyAsync(&hovf, ovf.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    // unconditional: the host vectors above are locals of this frame
+    PGCP_TRY_CUDA(cudaStreamSynchronize(s));
+    if (hovf) {
+        set_error("coarse space: an aggregate touches more than %d neighbouring aggregates", E_NBMAX);
+        return PGCP_E_INVALID;
+    }
+    return PGCP_OK;
 }
 
 // Build the slot system. pins (device int32 [2*nslot]) for DNCP, or the fixed
@@ -953,9 +2158,19 @@ int build_system(pgcp_batch* b, SolveSystem* S, bool dncp, const int32_t* d_pins
     PGCP_TRY(S->urow.alloc(S->ne, s));
     PGCP_TRY(S->rowsrc.alloc(S->rows, s));
     PGCP_TRY(S->rowsrc.fill_bytes(0xff, s));
-    k_urow<<<grid_for(S->ne, 256), 256, 0, s>>>(S->ne, nslot, S->sv_off.p, S->sl_off.p, uscan.p, S->fixed_ref.p,
-                                              S->urow.p, S->rowsrc.p);
-    PGCP_LAUNCH_CHECK();
+    {
+        const char* ev = getenv("PGCP_PCG_COARSE");
+        S->coarse = !(ev && atoi(ev) == 0);
+        const char* eg = getenv("PGCP_PCG_GMAX");
+        S->gmax = eg ? std::max(1, std::min(COARSE_GMAX, atoi(eg))) : COARSE_GMAX;
+    }
+    if (S->coarse) {
+        PGCP_TRY(order_rows_by_cell(b, S, uscan.p, hus, s));
+    } else {
+        k_urow<<<grid_for(S->ne, 256), 256, 0, s>>>(S->ne, nslot, S->sv_off.p, S->sl_off.p, uscan.p, S->fixed_ref.p,
+                                                  S->urow.p, S->rowsrc.p);
+        PGCP_LAUNCH_CHECK();
+    }
 
     BuildArgs a;
     a.nslot = nslot;
@@ -1022,8 +2237,22 @@ int run_solve(pgcp_batch* b, SolveSystem* S, const pgcp_solve_opts* o, double* z
     int64_t max_sl = 0;
     for (int j = 0; j < nslot; ++j) max_sl = std::max(max_sl, S->h_sl_off[j + 1] - S->h_sl_off[j]);
     int csize = 1, chunk = 1;
-    PGCP_TRY(pick_cluster(max_sl, nslot, o ? o->cluster : 0, &csize, &chunk));
+    PGCP_TRY(pick_cluster(max_sl, nslot, o ? o->cluster : 0, S->coarse, &csize, &chunk));
     S->csize = csize;
+    if (S->coarse) {
+        cudaEvent_t c0, c1;
+        PGCP_TRY_CUDA(cudaEventCreate(&c0));
+        PGCP_TRY_CUDA(cudaEventCreate(&c1));
+        PGCP_TRY_CUDA(cudaEventRecord(c0, s));
+        PGCP_TRY(build_coarse(S, csize, s));
+        PGCP_TRY_CUDA(cudaEventRecord(c1, s));
+        PGCP_TRY_CUDA(cudaEventSynchronize(c1));
+        float cms = 0;
+        cudaEventElapsedTime(&cms, c0, c1);
+        cudaEventDestroy(c0);
+        cudaEventDestroy(c1);
+        S->coarse_ms = cms;
+    }
     PGCP_TRY(S->iters.alloc(nslot, s));
     PGCP_TRY(S->res.alloc(8 * (int64_t)nslot, s));
     PGCP_TRY(S->res.zero(s));
@@ -1052,11 +2281,17 @@ int run_solve(pgcp_batch* b, SolveSystem* S, const pgcp_solve_opts* o, double* z
     A.tol2 = rtol * rtol;
     A.maxit = (o && o->maxit > 0) ? o->maxit : 200000;
     A.chunk_cap = chunk;
+    A.C.abase = S->abase.p;
+    A.C.aoff = S->aoff.p;
+    A.C.wr = S->wr.p;
+    A.C.einv32 = S->einv32.p;
+    A.C.eoff32 = S->eoff32.p;
+    A.C.p = S->p.p;
     DevBuf<long long> tbuf;
     A.timing = nullptr;
     const bool want_timing = getenv("PGCP_PCG_TIMING") != nullptr;
     if (want_timing) {
-        PGCP_TRY(tbuf.alloc(4 * (int64_t)nslot * csize, s));
+        PGCP_TRY(tbuf.alloc(8 * (int64_t)nslot * csize, s));
         PGCP_TRY(tbuf.zero(s));
         A.timing = tbuf.p;
     }
@@ -1085,13 +2320,18 @@ int run_solve(pgcp_batch* b, SolveSystem* S, const pgcp_solve_opts* o, double* z
     PGCP_TRY_CUDA(cudaMemcpyAsync(hres.data(), S->res.p, 8 * nslot * sizeof(double), cudaMemcpyDeviceToHost, s));
     PGCP_TRY_CUDA(cudaStreamSynchronize(s));
     if (want_timing) {
-        std::vector<long long> ht(4 * (size_t)nslot * csize);
+        std::vector<long long> ht(8 * (size_t)nslot * csize);
         PGCP_TRY_CUDA(cudaMemcpy(ht.data(), tbuf.p, ht.size() * sizeof(long long), cudaMemcpyDeviceToHost));
-        double acc[4] = {0, 0, 0, 0};
-        for (size_t i = 0; i < ht.size(); ++i) acc[i % 4] += (double)ht[i];
+        double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (size_t i = 0; i < ht.size(); ++i) acc[i % 8] += (double)ht[i];
         double nct = (double)nslot * csize * 128.0;
-        fprintf(stderr, "[pcg timing] cycles/iter per CTA: phaseA %.0f red1 %.0f phaseB %.0f red2 %.0f (csize %d)\n",
-                acc[0] / nct, acc[1] / nct, acc[2] / nct, acc[3] / nct, csize);
+        if (S->coarse)
+            fprintf(stderr, "[pcg timing] cycles/iter per CTA: A %.0f sync1 %.0f B %.0f sync2 %.0f C %.0f sync3 %.0f "
+                    "(csize %d, coarse setup %.2f ms)\n", acc[0] / nct, acc[1] / nct, acc[2] / nct, acc[3] / nct,
+                    acc[4] / nct, acc[5] / nct, csize, S->coarse_ms);
+        else
+            fprintf(stderr, "[pcg timing] cycles/iter per CTA: phaseA %.0f red1 %.0f phaseB %.0f red2 %.0f (csize %d)\n",
+                    acc[0] / nct, acc[1] / nct, acc[2] / nct, acc[3] / nct, csize);
     }
     {
         float ms = 0;
@@ -1101,12 +2341,19 @@ int run_solve(pgcp_batch* b, SolveSystem* S, const pgcp_solve_opts* o, double* z
         S->kernel_ms = ms;
         // compulsory bytes per iteration of slot j: stored off-diagonal
         // values + cols (12 B per slice entry) and the y update (read +
-        // write, 32 B per unknown row); CG vectors stay on chip
+        // write, 32 B per unknown row); CG vectors stay on chip. Two-level
+        // (k_pcg2) adds p read + write (32 B/row), the coarse weights read
+        // twice (2 x 16 B/row) and the float E^-1 (8 nc ncp B per slot).
         S->iters_sum = S->iters_max = S->bytes_iter_weighted = 0;
         for (int j = 0; j < nslot; ++j) {
             int64_t e = hptr[S->h_sl_off[j + 1]] - hptr[S->h_sl_off[j]];
             double rows = (double)S->h_nu[j];
             double bytes = 12.0 * (double)e + 32.0 * rows;
+            if (S->coarse) {
+                double nc = 3.0 * (double)(S->h_abase[j + 1] - S->h_abase[j]);
+                double ncp = (double)(((int64_t)nc + 7) & ~7ll);
+                bytes += 64.0 * rows + 8.0 * nc * ncp;
+            }
             S->iters_sum += hit[j];
             S->iters_max = std::max<double>(S->iters_max, hit[j]);
             S->bytes_iter_weighted += bytes * hit[j];
@@ -1325,9 +2572,17 @@ int export_system(pgcp_batch* b, int which, int32_t comp, int64_t* dims, int32_t
         hb[r].y *= hd[r];
     }
     const int64_t rbase = 32 * S->h_sl_off[j];
-    std::vector<int64_t> pos(nc, -1);
-    for (int64_t v = 0; v < nc; ++v)
-        if (fr[v] < 0) pos[v] = ur[v] - rbase;
+    // columns in the reference's order (unknowns by vertex id); the solver's
+    // row of vertex v is ur[v] - rbase (cell order with the coarse space)
+    std::vector<int64_t> pos(nc, -1), srow(nc, -1);
+    {
+        int64_t k = 0;
+        for (int64_t v = 0; v < nc; ++v)
+            if (fr[v] < 0) {
+                pos[v] = k++;
+                srow[v] = ur[v] - rbase;
+            }
+    }
     std::vector<int64_t> nxt(nc, -1), prv(nc, -1);
     if (nb >= 3)
         for (int64_t q = 0; q < nb; ++q) {
@@ -1368,20 +2623,20 @@ int export_system(pgcp_batch* b, int which, int32_t comp, int64_t* dims, int32_t
             push_L(U[r], 0, true);
             push_cpl(U[r], nU, -0.5);
             ip.push_back((int32_t)ix.size());
-            hr.push_back(hb[r].x);
+            hr.push_back(hb[srow[U[r]]].x);
         }
         for (int64_t r = 0; r < nU; ++r) {  // y rows: 2 M_xy | L
             push_cpl(U[r], 0, 0.5);
             push_L(U[r], nU, true);
             ip.push_back((int32_t)ix.size());
-            hr.push_back(hb[r].y);
+            hr.push_back(hb[srow[U[r]]].y);
         }
     } else {
         for (int64_t r = 0; r < nU; ++r) {
             push_L(U[r], 0, false);
             ip.push_back((int32_t)ix.size());
-            hr.push_back(hb[r].x);
-            hr.push_back(hb[r].y);
+            hr.push_back(hb[srow[U[r]]].x);
+            hr.push_back(hb[srow[U[r]]].y);
         }
     }
     dims[0] = (int64_t)ip.size() - 1;

@@ -393,3 +393,112 @@ extern "C" PGCP_API int pgcp_plan_weld_schedule(const int64_t* cyc, const int64_
     g_cache.valid = false;  // copy-out done: no memoisation across plans
     return PGCP_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Weld plan over tracked boundary slots (the bookkeeping of pipeline.py:
+// 172-213 on per-component dicts, flattened): slot s = one entry of one
+// submesh's boundary loop (submesh order, loop order). For every step the
+// slots of a_cycle / b_cycle (phase-1 inputs; a parent vertex present in
+// several loops of a component resolves to its last slot) and the
+// write-back code of every slot of the two components:
+//   bits 0..23 arc position + 1 (0: replay), bit 25 / 26 on a_cycle / b_cycle,
+//   bit 31 slot of the b side.
+// Inputs: cycles (parent ids, cyc_off[K+1]) and the planner's flat output
+// (meta[8*nsteps], idx). Outputs (two-call protocol, lens[0] = total src
+// entries, lens[1] = total write-back entries):
+//   info[6*nsteps] (k, closed, na, nb, comp_a, comp_b), src, wb_off[nsteps+1],
+//   wb[2*total] (slot, code), ext[K] = 1 / 2 for the submeshes on the a / b
+//   side of the closing (sphere) step, else 0.
+extern "C" PGCP_API int pgcp_weld_plan(const int64_t* cyc, const int64_t* cyc_off, int32_t K, const int64_t* meta,
+                                       const int64_t* idx, int32_t nsteps, int64_t n_parent, int32_t* info,
+                                       int32_t* src, int64_t* wb_off, int32_t* wb, int32_t* ext, int64_t* lens) {
+    if (K < 0 || nsteps < 0 || !cyc_off || !lens || (nsteps > 0 && (!meta || !idx))) {
+        pgcp::set_error("weld_plan: invalid arguments");
+        return PGCP_E_INVALID;
+    }
+    // members of every live component (submesh lists, in merge order)
+    std::vector<std::vector<int32_t>> members(K);
+    for (int32_t i = 0; i < K; ++i) members[i] = {i};
+    int64_t nsrc = 0, nwb = 0;
+    for (int32_t q = 0; q < nsteps; ++q) {
+        const int64_t* m = meta + 8 * (int64_t)q;
+        nsrc += m[5] + m[6];
+        int64_t ca = m[0], cb = m[1];
+        if (ca < 0 || ca >= K || cb < 0 || cb >= K) {
+            pgcp::set_error("weld_plan: component id out of range");
+            return PGCP_E_INVALID;
+        }
+        for (int32_t sub : members[ca]) nwb += cyc_off[sub + 1] - cyc_off[sub];
+        for (int32_t sub : members[cb]) nwb += cyc_off[sub + 1] - cyc_off[sub];
+        members[ca].insert(members[ca].end(), members[cb].begin(), members[cb].end());
+        members[cb].clear();
+    }
+    lens[0] = nsrc;
+    lens[1] = nwb;
+    if (!info || !src || !wb_off || !wb) return PGCP_OK;
+    for (int32_t i = 0; i < K; ++i) members[i] = {i};
+    if (ext)
+        for (int32_t i = 0; i < K; ++i) ext[i] = 0;
+    std::vector<int32_t> table((size_t)std::max<int64_t>(n_parent, 1), -1);
+    std::vector<int32_t> code((size_t)std::max<int64_t>(n_parent, 1), 0);
+    const int32_t CYC_A = 1 << 25, CYC_B = 1 << 26;
+    const uint32_t SIDE_B = 1u << 31;
+    int64_t so = 0, wo = 0;
+    wb_off[0] = 0;
+    for (int32_t q = 0; q < nsteps; ++q) {
+        const int64_t* m = meta + 8 * (int64_t)q;
+        const int64_t ca = m[0], cb = m[1], k = m[2], closed = m[3], o = m[4], na = m[5], nb = m[6];
+        const int64_t* ac = idx + o;
+        const int64_t* bc = ac + na;
+        auto slots_src = [&](const std::vector<int32_t>& mem, const int64_t* cy, int64_t len) -> int {
+            for (int32_t sub : mem)
+                for (int64_t t = cyc_off[sub]; t < cyc_off[sub + 1]; ++t) table[cyc[t]] = (int32_t)t;
+            int bad = 0;
+            for (int64_t i = 0; i < len; ++i) {
+                int64_t v = cy[i];
+                int32_t sl = (v >= 0 && v < n_parent) ? table[v] : -1;
+                if (sl < 0) bad = 1;
+                src[so++] = sl;
+            }
+            for (int32_t sub : mem)
+                for (int64_t t = cyc_off[sub]; t < cyc_off[sub + 1]; ++t) table[cyc[t]] = -1;
+            return bad;
+        };
+        if (slots_src(members[ca], ac, na) | slots_src(members[cb], bc, nb)) {
+            pgcp::set_error("weld step references a boundary vertex outside its components");
+            return PGCP_E_WELD;
+        }
+        for (int64_t i = 0; i <= k && i < na; ++i) code[ac[i]] = (int32_t)(i + 1);
+        for (int64_t i = 0; i < na; ++i) code[ac[i]] |= CYC_A;
+        for (int64_t i = 0; i < nb; ++i) code[bc[i]] |= CYC_B;
+        for (int32_t sub : members[ca])
+            for (int64_t t = cyc_off[sub]; t < cyc_off[sub + 1]; ++t) {
+                wb[2 * wo] = (int32_t)t;
+                wb[2 * wo + 1] = code[cyc[t]];
+                ++wo;
+            }
+        for (int32_t sub : members[cb])
+            for (int64_t t = cyc_off[sub]; t < cyc_off[sub + 1]; ++t) {
+                wb[2 * wo] = (int32_t)t;
+                wb[2 * wo + 1] = (int32_t)((uint32_t)code[cyc[t]] | SIDE_B);
+                ++wo;
+            }
+        for (int64_t i = 0; i < na; ++i) code[ac[i]] = 0;
+        for (int64_t i = 0; i < nb; ++i) code[bc[i]] = 0;
+        wb_off[q + 1] = wo;
+        int32_t* in = info + 6 * (int64_t)q;
+        in[0] = (int32_t)k;
+        in[1] = (int32_t)closed;
+        in[2] = (int32_t)na;
+        in[3] = (int32_t)nb;
+        in[4] = (int32_t)ca;
+        in[5] = (int32_t)cb;
+        if (closed && ext) {
+            for (int32_t sub : members[ca]) ext[sub] = 1;
+            for (int32_t sub : members[cb]) ext[sub] = 2;
+        }
+        members[ca].insert(members[ca].end(), members[cb].begin(), members[cb].end());
+        members[cb].clear();
+    }
+    return PGCP_OK;
+}

@@ -314,8 +314,21 @@ __device__ __forceinline__ int lv_find(const int64_t* __restrict__ lv_off, const
     return -1;
 }
 
+// faces per component; consecutive faces mostly share a component, so the
+// increments are aggregated per warp (one atomic per distinct component)
 __global__ void k_face_count(const int32_t* __restrict__ face_comp, int64_t m, int32_t* __restrict__ fcnt) {
-    GRID_STRIDE(f, m) atomicAdd(&fcnt[face_comp[f]], 1);
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t m_round = (m + 31) & ~(int64_t)31;
+    for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < m_round; f += stride) {
+        const bool ok = f < m;
+        const int c = ok ? face_comp[f] : -1;
+        const unsigned act = __ballot_sync(0xffffffffu, ok);
+        if (ok) {
+            const unsigned peers = __match_any_sync(act, c);
+            if (lane == __ffs(peers) - 1) atomicAdd(&fcnt[c], __popc(peers));
+        }
+    }
 }
 
 // boundary half-edges of every submesh (twin absent or in another submesh)
@@ -325,16 +338,21 @@ __global__ void k_boundary(const int32_t* __restrict__ F, int64_t m, const int32
                            const int32_t* __restrict__ lv_comp, const int32_t* __restrict__ lv_gid,
                            int32_t* __restrict__ nxt, int32_t* __restrict__ bcnt, int32_t* __restrict__ start,
                            int32_t* __restrict__ comp_bad, int32_t* __restrict__ pnxt, int32_t* pcount,
-                           int32_t* pstart, int32_t* pbad) {
+                           int32_t* pstart, int32_t* pbad, int32_t* __restrict__ node, int32_t* __restrict__ idx,
+                           int32_t* nnode, int32_t* __restrict__ pnode, int32_t* __restrict__ pidx, int64_t n) {
     GRID_STRIDE(h, 3 * m) {
         int f = (int)(h / 3), c = (int)(h % 3);
         int a = F[3 * f + c], b = F[3 * f + (c + 1) % 3];
         int t = twin[h];
         int cf = face_comp[f];
         if (t < 0) {
-            atomicAdd(pcount, 1);
+            int k = atomicAdd(pcount, 1);
             if (atomicCAS(&pnxt[a], -1, b) != -1) atomicExch(pbad, 1);
             atomicMin(pstart, a);
+            if (k < n) {
+                pnode[k] = a;
+                pidx[a] = k;
+            }
         }
         if (t < 0 || face_comp[t / 3] != cf) {
             int ga = lv_find(lv_off, lv_comp, lv_gid, a, cf);
@@ -342,8 +360,119 @@ __global__ void k_boundary(const int32_t* __restrict__ F, int64_t m, const int32
             atomicAdd(&bcnt[cf], 1);
             if (atomicCAS(&nxt[ga], -1, gb) != -1) atomicExch(&comp_bad[cf], 1);
             atomicMin(&start[cf], ga);
+            int k = atomicAdd(nnode, 1);
+            node[k] = ga;
+            idx[ga] = k;
         }
     }
+}
+
+// ---- parallel boundary walks (pointer jumping instead of sequential walks)
+// Component loops: the cycle of every submesh is cut before its smallest
+// vertex `start`; list ranking gives every node its distance to the cut, so
+// its loop position is (L - 1) - dist. Nodes that never reach the cut lie on
+// another loop (the component is then re-walked sequentially by k_walk for
+// the reference's diagnostics).
+__global__ void k_lr_init(int64_t nn, const int32_t* __restrict__ node, const int32_t* __restrict__ idx,
+                          const int32_t* __restrict__ nxt, const int32_t* __restrict__ comp_of_gid,
+                          const int32_t* __restrict__ start, int32_t* __restrict__ succ, int32_t* __restrict__ dist,
+                          int32_t* __restrict__ comp_flag) {
+    GRID_STRIDE(k, nn) {
+        int g = node[k];
+        int c = comp_of_gid[g];
+        int nx = nxt[g];
+        int sc = -1;
+        if (nx < 0) {
+            comp_flag[c] = 1;
+        } else if (nx != start[c]) {
+            sc = idx[nx];
+            if (sc < 0) comp_flag[c] = 1;  // nx has no outgoing boundary edge
+        }
+        succ[k] = sc;
+        dist[k] = sc < 0 ? 0 : 1;
+    }
+}
+
+__global__ void k_lr_step(int64_t nn, const int32_t* __restrict__ succ_in, const int32_t* __restrict__ dist_in,
+                          int32_t* __restrict__ succ_out, int32_t* __restrict__ dist_out) {
+    GRID_STRIDE(k, nn) {
+        int sc = succ_in[k];
+        if (sc >= 0) {
+            dist_out[k] = dist_in[k] + dist_in[sc];
+            succ_out[k] = succ_in[sc];
+        } else {
+            dist_out[k] = dist_in[k];
+            succ_out[k] = -1;
+        }
+    }
+}
+
+__global__ void k_lr_finish(int64_t nn, const int32_t* __restrict__ node, const int32_t* __restrict__ idx,
+                            const int32_t* __restrict__ comp_of_gid, const int32_t* __restrict__ start,
+                            const int32_t* __restrict__ succ, const int32_t* __restrict__ dist,
+                            const int32_t* __restrict__ bcnt, const int64_t* __restrict__ vert_off,
+                            const int64_t* __restrict__ loop_off, const int32_t* __restrict__ comp_bad,
+                            int32_t* __restrict__ comp_flag, int32_t* __restrict__ loop) {
+    GRID_STRIDE(k, nn) {
+        int g = node[k];
+        int c = comp_of_gid[g];
+        if (comp_bad[c] || comp_flag[c]) continue;
+        if (succ[k] >= 0) {  // not on the start's loop
+            comp_flag[c] = 1;
+            continue;
+        }
+        int L = dist[idx[start[c]]] + 1;
+        if (L != bcnt[c]) {
+            comp_flag[c] = 1;
+            continue;
+        }
+        int pos = L - 1 - dist[k];
+        loop[loop_off[c] + pos] = (int32_t)(g - vert_off[c]);
+    }
+}
+
+// parent boundary: every node learns the minimum vertex of its cycle (min
+// label pointer jumping on the closed cycles); one loop iff the cycle of the
+// smallest boundary vertex holds every boundary edge
+__global__ void k_plab_init(int64_t nn, const int32_t* __restrict__ pnode, const int32_t* __restrict__ pidx,
+                            const int32_t* __restrict__ pnxt, int32_t* __restrict__ jump, int32_t* __restrict__ lab,
+                            int32_t* pbad) {
+    GRID_STRIDE(k, nn) {
+        int v = pnode[k];
+        int nx = pnxt[v];
+        int jn = nx < 0 ? -1 : pidx[nx];
+        if (jn < 0) {
+            atomicExch(pbad, 1);
+            jump[k] = (int32_t)k;
+        } else {
+            jump[k] = jn;
+        }
+        lab[k] = v;
+    }
+}
+
+__global__ void k_plab_step(int64_t nn, const int32_t* __restrict__ jump_in, const int32_t* __restrict__ lab_in,
+                            int32_t* __restrict__ jump_out, int32_t* __restrict__ lab_out) {
+    GRID_STRIDE(k, nn) {
+        int jn = jump_in[k];
+        lab_out[k] = min(lab_in[k], lab_in[jn]);
+        jump_out[k] = jump_in[jn];
+    }
+}
+
+__global__ void k_plab_finish(int64_t nn, const int32_t* __restrict__ lab, const int32_t* pstart,
+                              const int32_t* pcount, const int32_t* pbad, int32_t* on_start,
+                              int64_t* __restrict__ out_loops) {
+    GRID_STRIDE(k, nn) if (lab[k] == *pstart) atomicAdd(on_start, 1);
+}
+
+__global__ void k_plab_result(const int32_t* pcount, const int32_t* pbad, const int32_t* on_start, int64_t n,
+                              int64_t* out_loops) {
+    if (blockIdx.x || threadIdx.x) return;
+    int pb = *pcount;
+    if (*pbad || pb > n) *out_loops = -1;
+    else if (pb == 0) *out_loops = 0;
+    else *out_loops = (*on_start == pb) ? 1 : -2;
 }
 
 // one thread per submesh: chi, loop walk from the smallest boundary vertex
@@ -351,7 +480,8 @@ __global__ void k_walk(int32_t K, const int64_t* __restrict__ vert_off, const in
                        const int32_t* __restrict__ bcnt, const int32_t* __restrict__ start,
                        const int32_t* __restrict__ nxt, const int64_t* __restrict__ loop_off,
                        int32_t* __restrict__ loop, int32_t* __restrict__ comp_bad, int32_t* __restrict__ chi_out,
-                       int32_t* __restrict__ loops_out, uint8_t* __restrict__ seen) {
+                       int32_t* __restrict__ loops_out, uint8_t* __restrict__ seen,
+                       const int32_t* __restrict__ comp_flag) {
     GRID_STRIDE(c, K) {
         int64_t nc = vert_off[c + 1] - vert_off[c];
         int64_t mc = fcnt[c], bc = bcnt[c];
@@ -360,6 +490,14 @@ __global__ void k_walk(int32_t K, const int64_t* __restrict__ vert_off, const in
         chi_out[c] = (int32_t)chi;
         int loops = 0;
         bool bad = comp_bad[c] != 0 || (twoE & 1);
+        if (!bad && !comp_flag[c]) {
+            // single loop already placed by the list ranking (k_lr_finish)
+            loops = bc > 0 ? 1 : 0;
+            loops_out[c] = loops;
+            if (!(chi == 1 && loops == 1)) comp_bad[c] = 1;
+            continue;
+        }
+        for (int64_t q = loop_off[c]; q < loop_off[c] + bc && q < loop_off[c + 1]; ++q) loop[q] = 0;
         if (!bad && bc > 0) {
             int s = start[c];
             int cur = s;
@@ -420,30 +558,6 @@ __global__ void k_cycles(int32_t K, const int64_t* __restrict__ loop_off, const 
     }
 }
 
-__global__ void k_parent_walk(const int32_t* __restrict__ pnxt, const int32_t* pcount, const int32_t* pstart,
-                              const int32_t* pbad, int64_t* out_loops) {
-    if (blockIdx.x || threadIdx.x) return;
-    int pb = *pcount;
-    if (*pbad) {
-        *out_loops = -1;
-        return;
-    }
-    if (pb == 0) {
-        *out_loops = 0;
-        return;
-    }
-    int s = *pstart, cur = s;
-    int64_t j = 0;
-    do {
-        ++j;
-        cur = pnxt[cur];
-        if (cur < 0 || j > pb) {
-            *out_loops = -1;
-            return;
-        }
-    } while (cur != s);
-    *out_loops = (j == pb) ? 1 : -2;
-}
 
 __global__ void k_fill_i32(int32_t* p, int64_t n, int32_t v) {
     GRID_STRIDE(i, n) p[i] = v;
@@ -653,13 +767,20 @@ int build_partition(pgcp_batch* b, const int64_t* cuts, int64_t ncuts, bool no_c
     PGCP_TRY(chi.alloc(K, s));
     PGCP_TRY(loops.alloc(K, s));
     PGCP_TRY(pnxt.alloc(n, s));
-    PGCP_TRY(pscal.alloc(3, s));  // count, start, bad
+    PGCP_TRY(pscal.alloc(5, s));  // count, start, bad, nodes, on_start
     PGCP_TRY(b->nxt.alloc(E, s));
+    DevBuf<int32_t> node, idx, pnode, pidx;
+    PGCP_TRY(node.alloc(3 * m, s));
+    PGCP_TRY(idx.alloc(E, s));
+    PGCP_TRY(pnode.alloc(n, s));
+    PGCP_TRY(pidx.alloc(n, s));
+    PGCP_TRY(idx.fill_bytes(0xff, s));
+    PGCP_TRY(pidx.fill_bytes(0xff, s));
     k_fill_i32<<<grid_for(K, BT), BT, 0, s>>>(start.p, K, INT_MAX);
     k_fill_i32<<<grid_for(E, BT), BT, 0, s>>>(b->nxt.p, E, -1);
     k_fill_i32<<<grid_for(n, BT), BT, 0, s>>>(pnxt.p, n, -1);
     {
-        int32_t init[3] = {0, INT_MAX, 0};
+        int32_t init[5] = {0, INT_MAX, 0, 0, 0};
         PGCP_TRY_CUDA(cudaMemcpyAsync(pscal.p, init, sizeof(init), cudaMemcpyHostToDevice, s));
         PGCP_TRY_CUDA(cudaStreamSynchronize(s));
     }
@@ -667,7 +788,8 @@ int build_partition(pgcp_batch* b, const int64_t* cuts, int64_t ncuts, bool no_c
     PGCP_LAUNCH_CHECK();
     k_boundary<<<grid_for(3 * m, BT), BT, 0, s>>>(b->F.p, m, b->twin.p, b->face_comp.p, b->lv_off.p,
                                                 b->lv_comp.p, b->lv_gid.p, b->nxt.p, bcnt.p, start.p, bad.p,
-                                                pnxt.p, pscal.p, pscal.p + 1, pscal.p + 2);
+                                                pnxt.p, pscal.p, pscal.p + 1, pscal.p + 2, node.p, idx.p,
+                                                pscal.p + 3, pnode.p, pidx.p, n);
     PGCP_LAUNCH_CHECK();
     PGCP_TRY(b->loop_off.alloc(K + 1, s));
     PGCP_TRY(exclusive_scan_i32_to_i64(bcnt.p, b->loop_off.p, K, s));
@@ -677,8 +799,33 @@ int build_partition(pgcp_batch* b, const int64_t* cuts, int64_t ncuts, bool no_c
     DevBuf<uint8_t> seen;
     PGCP_TRY(seen.alloc(E, s));
     PGCP_TRY(seen.zero(s));
+    DevBuf<int32_t> cflag;
+    PGCP_TRY(cflag.alloc(K, s));
+    PGCP_TRY(cflag.zero(s));
+    int rounds = 1;
+    while ((1ll << rounds) < b->sum_nb + 2) ++rounds;
+    if (b->sum_nb > 0) {
+        DevBuf<int32_t> sa, da, sb, db;
+        PGCP_TRY(sa.alloc(b->sum_nb, s));
+        PGCP_TRY(da.alloc(b->sum_nb, s));
+        PGCP_TRY(sb.alloc(b->sum_nb, s));
+        PGCP_TRY(db.alloc(b->sum_nb, s));
+        k_lr_init<<<grid_for(b->sum_nb, BT), BT, 0, s>>>(b->sum_nb, node.p, idx.p, b->nxt.p, b->comp_of_gid.p,
+                                                        start.p, sa.p, da.p, cflag.p);
+        PGCP_LAUNCH_CHECK();
+        for (int r = 0; r < rounds; ++r) {
+            k_lr_step<<<grid_for(b->sum_nb, BT), BT, 0, s>>>(b->sum_nb, sa.p, da.p, sb.p, db.p);
+            PGCP_LAUNCH_CHECK();
+            std::swap(sa.p, sb.p);
+            std::swap(da.p, db.p);
+        }
+        k_lr_finish<<<grid_for(b->sum_nb, BT), BT, 0, s>>>(b->sum_nb, node.p, idx.p, b->comp_of_gid.p, start.p,
+                                                          sa.p, da.p, bcnt.p, b->vert_off.p, b->loop_off.p, bad.p,
+                                                          cflag.p, b->loop.p);
+        PGCP_LAUNCH_CHECK();
+    }
     k_walk<<<grid_for(K, 64), 64, 0, s>>>(K, b->vert_off.p, fcnt.p, bcnt.p, start.p, b->nxt.p, b->loop_off.p,
-                                         b->loop.p, bad.p, chi.p, loops.p, seen.p);
+                                         b->loop.p, bad.p, chi.p, loops.p, seen.p, cflag.p);
     PGCP_LAUNCH_CHECK();
     PGCP_TRY(b->cyc.alloc(b->sum_nb, s));
     if (b->sum_nb > 0) {
@@ -688,8 +835,34 @@ int build_partition(pgcp_batch* b, const int64_t* cuts, int64_t ncuts, bool no_c
     }
     DevBuf<int64_t> ploops;
     PGCP_TRY(ploops.alloc(1, s));
-    k_parent_walk<<<1, 32, 0, s>>>(pnxt.p, pscal.p, pscal.p + 1, pscal.p + 2, ploops.p);
-    PGCP_LAUNCH_CHECK();
+    {
+        // parent boundary cycles: at most n nodes (more means a broken boundary)
+        int32_t hpc = 0;
+        PGCP_TRY(fetch_scalar(pscal.p, &hpc, s));
+        const int64_t pn = std::min<int64_t>(hpc, n);
+        if (pn > 0) {
+            DevBuf<int32_t> ja, la, jb, lb;
+            PGCP_TRY(ja.alloc(pn, s));
+            PGCP_TRY(la.alloc(pn, s));
+            PGCP_TRY(jb.alloc(pn, s));
+            PGCP_TRY(lb.alloc(pn, s));
+            k_plab_init<<<grid_for(pn, BT), BT, 0, s>>>(pn, pnode.p, pidx.p, pnxt.p, ja.p, la.p, pscal.p + 2);
+            PGCP_LAUNCH_CHECK();
+            int pr = 1;
+            while ((1ll << pr) < pn + 2) ++pr;
+            for (int r = 0; r < pr; ++r) {
+                k_plab_step<<<grid_for(pn, BT), BT, 0, s>>>(pn, ja.p, la.p, jb.p, lb.p);
+                PGCP_LAUNCH_CHECK();
+                std::swap(ja.p, jb.p);
+                std::swap(la.p, lb.p);
+            }
+            k_plab_finish<<<grid_for(pn, BT), BT, 0, s>>>(pn, la.p, pscal.p + 1, pscal.p, pscal.p + 2, pscal.p + 4,
+                                                         ploops.p);
+            PGCP_LAUNCH_CHECK();
+        }
+        k_plab_result<<<1, 32, 0, s>>>(pscal.p, pscal.p + 2, pscal.p + 4, n, ploops.p);
+        PGCP_LAUNCH_CHECK();
+    }
 
     // --- host copies of the small per-submesh tables
     b->h_vert_off.resize(K + 1);

@@ -522,7 +522,6 @@ __device__ bool prenormalize(const double2* tv, const int32_t* src, int n, doubl
 // so the serial chain costs one cluster barrier per record and the O(k^2)
 // point work is spread over CS SMs.
 
-constexpr int PC_THREADS = 256;
 constexpr int PC_MAXCS = 16;
 constexpr int NPARAM = 8;            // parameter slots per step
 constexpr int NFLAG = PC_MAXCS;      // per-rank scalars (maxima)
@@ -543,7 +542,8 @@ struct P1c {
     int lo, hi;         // my global point range [lo, hi)
 };
 
-__global__ void __launch_bounds__(PC_THREADS, 1) k_phase1c(Phase1Args A) {
+template <int NT>
+__global__ void __launch_bounds__(NT, 1) k_phase1c(Phase1Args A) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ PParam s_param[2][NPARAM];
     __shared__ double s_flag[2][NFLAG];
@@ -589,7 +589,7 @@ __global__ void __launch_bounds__(PC_THREADS, 1) k_phase1c(Phase1Args A) {
         }
         return;
     }
-    for (int g = lo + threadIdx.x; g < hi; g += PC_THREADS) {
+    for (int g = lo + threadIdx.x; g < hi; g += NT) {
         int side = g >= P;
         int t = g - side * P;
         double2 z;
@@ -611,7 +611,7 @@ __global__ void __launch_bounds__(PC_THREADS, 1) k_phase1c(Phase1Args A) {
     // publish the listed global points into every CTA's slots, then barrier
     auto publish = [&](const int* gidx, int np, double flag) {
         __syncthreads();
-        for (int q = threadIdx.x; q < np * CS; q += PC_THREADS) {
+        for (int q = threadIdx.x; q < np * CS; q += NT) {
             int which = q / CS, dst = q % CS;
             int g = gidx[which];
             if (g >= lo && g < hi) {
@@ -630,7 +630,7 @@ __global__ void __launch_bounds__(PC_THREADS, 1) k_phase1c(Phase1Args A) {
         cl.sync();
     };
     auto apply_pair = [&](const Rec& ra, bool ua, const Rec& rb, bool ub) {
-        for (int g = lo + threadIdx.x; g < hi; g += PC_THREADS) {
+        for (int g = lo + threadIdx.x; g < hi; g += NT) {
             int side = g >= P;
             if (side ? !ub : !ua) continue;
             double2 z = pts[g - lo];
@@ -737,7 +737,7 @@ __global__ void __launch_bounds__(PC_THREADS, 1) k_phase1c(Phase1Args A) {
     // ---- far ends: SquareMobius; stage max of |va| (arc + aux) for the deferred check
     {
         double m = 0;
-        for (int g = lo + threadIdx.x; g < hi && g < P; g += PC_THREADS)
+        for (int g = lo + threadIdx.x; g < hi && g < P; g += NT)
             if (c_fin(pts[g - lo])) m = fmax(m, cabs_(pts[g - lo]));
         m = block_max(m, red);
         int gi[2] = {0, P};
@@ -806,16 +806,16 @@ __global__ void __launch_bounds__(PC_THREADS, 1) k_phase1c(Phase1Args A) {
             log_a[na_rec++] = ra;
             log_b[nb_rec++] = ra;
         }
-        for (int g = lo + threadIdx.x; g < hi; g += PC_THREADS) sides[g - lo] = 0;
+        for (int g = lo + threadIdx.x; g < hi; g += NT) sides[g - lo] = 0;
         apply_pair(ra, true, ra, true);
     }
     // ---- outputs: all 2P points to arc_out; rank 0 finishes seam/maxima/area
-    for (int g = lo + threadIdx.x; g < hi; g += PC_THREADS) A.arc_out[sd.arc + g] = pts[g - lo];
+    for (int g = lo + threadIdx.x; g < hi; g += NT) A.arc_out[sd.arc + g] = pts[g - lo];
     cl.sync();
     if (rank == 0) {
         const double2* o = A.arc_out + sd.arc;
         double seam = 0, ma = 0, mb = 0, mx = 0, area = 0, bad = 0;
-        for (int t = threadIdx.x; t <= k; t += PC_THREADS) {
+        for (int t = threadIdx.x; t <= k; t += NT) {
             double2 a = o[t], b = o[P + t];
             double gg = (c_isinf(a) && c_isinf(b)) ? 0.0 : cabs_(csub(a, b));
             if (!isnan(gg)) seam = fmax(seam, gg);
@@ -824,9 +824,9 @@ __global__ void __launch_bounds__(PC_THREADS, 1) k_phase1c(Phase1Args A) {
             double2 nx = o[(t + 1) % (k + 1)];
             area += 0.5 * (a.x * nx.y - a.y * nx.x);
         }
-        for (int g = threadIdx.x; g < NP; g += PC_THREADS)
+        for (int g = threadIdx.x; g < NP; g += NT)
             if (c_nan(o[g])) bad = 1;
-        for (int t = threadIdx.x; t < 2; t += PC_THREADS) {
+        for (int t = threadIdx.x; t < 2; t += NT) {
             double2 a = o[k + 1 + t], b = o[P + k + 1 + t];
             if (c_fin(a)) mx = fmax(mx, cabs_(a));
             if (c_fin(b)) mx = fmax(mx, cabs_(b));
@@ -1207,6 +1207,19 @@ std::string err_text(int code, int idx, int aux, double a = 0, double b = 0, dou
 }
 
 
+int env_int(const char* name, int dflt) {
+    const char* v = getenv(name);
+    return v && *v ? atoi(v) : dflt;
+}
+
+template <int NT>
+int prep_phase1(int CS, size_t smem) {
+    if (CS > 8) PGCP_TRY_CUDA(cudaFuncSetAttribute(k_phase1c<NT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    if (smem > 48 * 1024)
+        PGCP_TRY_CUDA(cudaFuncSetAttribute(k_phase1c<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    return PGCP_OK;
+}
+
 double bits_to_d(unsigned long long b) {
     double d;
     memcpy(&d, &b, sizeof d);
@@ -1323,13 +1336,14 @@ int run_schedule(double2* tv, int32_t nsteps, const int32_t* info, const int32_t
         int kmax = 0;
         for (int q = q0; q < q1; ++q) kmax = std::max(kmax, sd[q].k);
         const int NP = 2 * (kmax + 3);
-        int CS = 1;
-        while (CS < PC_MAXCS && CS * PC_THREADS < NP) CS *= 2;
+        const int ppt = std::max(1, env_int("PGCP_WELD_PPT", 1));
+        const int NT = env_int("PGCP_WELD_NT", 256) >= 512 ? 512 : 256;
+        int CS = std::min(PC_MAXCS, (NP + NT * ppt - 1) / (NT * ppt));
         const int chunk = (NP + CS - 1) / CS;
         size_t smem = (size_t)chunk * (sizeof(double2) + 1) + 16;
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)((q1 - q0) * CS), 1, 1);
-        cfg.blockDim = dim3(PC_THREADS, 1, 1);
+        cfg.blockDim = dim3(NT, 1, 1);
         cfg.dynamicSmemBytes = smem;
         cfg.stream = s;
         cudaLaunchAttribute attr[1];
@@ -1339,8 +1353,13 @@ int run_schedule(double2* tv, int32_t nsteps, const int32_t* info, const int32_t
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        if (CS > 8) PGCP_TRY_CUDA(cudaFuncSetAttribute(k_phase1c, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        PGCP_TRY_CUDA(cudaLaunchKernelEx(&cfg, k_phase1c, a));
+        if (NT == 512) {
+            PGCP_TRY(prep_phase1<512>(CS, smem));
+            PGCP_TRY_CUDA(cudaLaunchKernelEx(&cfg, k_phase1c<512>, a));
+        } else {
+            PGCP_TRY(prep_phase1<256>(CS, smem));
+            PGCP_TRY_CUDA(cudaLaunchKernelEx(&cfg, k_phase1c<256>, a));
+        }
         PGCP_LAUNCH_CHECK();
         int64_t n = lev_wb[l + 1] - lev_wb[l];
         if (n > 0) {

@@ -48,12 +48,14 @@ def write_cut_edges(path, cuts):
 
 
 def validate_cuts(mesh, cuts):
-    """Sorted pairs; duplicates rejected here, non-edges by the device
-    partition (partition.py:48-59)."""
+    """Sorted pairs (partition.py:48-59); duplicates rejected here, non-edges
+    by the device partition (k_mark_cuts), with the reference's messages."""
     cuts = np.asarray(cuts, dtype=np.int64).reshape(-1, 2)
     norm = np.sort(cuts, axis=1)
-    if len(norm) and len(np.unique(norm, axis=0)) != len(norm):
-        raise PartitionError("duplicate cut edges")
+    if len(norm) > 1:  # duplicates first, as the reference (also duplicate non-edges)
+        key = np.sort(norm[:, 0] * (int(norm.max()) + 1) + norm[:, 1])
+        if np.any(key[1:] == key[:-1]):
+            raise PartitionError("duplicate cut edges")
     return norm
 
 
@@ -200,14 +202,21 @@ def plan_weld_schedule(partition, mode="free", pairs=None):
     meta = np.empty((max(nsteps, 1), 8), dtype=np.int64)
     idx = np.empty(max(nidx, 1), dtype=np.int64)
     nat.check(L.pgcp_plan_weld_schedule(*args, meta.ctypes.data, idx.ctypes.data, nidx, ln))
-    steps = []
+    steps = StepList()
     for s in range(nsteps):
         ca, cb, k, closed, o, la, lb, lm = meta[s]
         a = idx[o:o + la].copy()
         b = idx[o + la:o + la + lb].copy()
         mg = idx[o + la + lb:o + la + lb + lm].copy()
         steps.append(WeldStep(int(ca), int(cb), a, b, int(k), bool(closed), mg))
+    steps.meta, steps.idx = meta, idx  # flat planner output (WeldPlan's native input)
     return steps
+
+
+class StepList(list):
+    """List of WeldStep that also carries the planner's flat arrays."""
+    meta = None
+    idx = None
 
 
 def _cyclic_runs(c1, c2):

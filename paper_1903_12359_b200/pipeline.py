@@ -13,6 +13,7 @@ Host work is bookkeeping over boundary-cycle ids (the weld write-back lists)
 and the final device -> host copy of the coordinates.
 """
 
+import ctypes
 import json
 import os
 import time
@@ -113,77 +114,70 @@ def _stream():
     return stream_handle()
 
 
+nat.register("pgcp_weld_plan",
+             [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32,
+              ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+              ctypes.POINTER(ctypes.c_int64)])
+
+
 class WeldPlan:
-    """Host bookkeeping of a weld schedule over the tracked boundary slots.
+    """Bookkeeping of a weld schedule over the tracked boundary slots.
 
     Slot s is one entry of one submesh's boundary loop (submesh order, loop
     order), i.e. the (component, parent id) value the reference keeps in its
     per-component dicts (pipeline.py:174-204). For every step the plan lists
     the slots of a_cycle / b_cycle (phase-1 inputs) and the write-back code of
-    every slot of the two components."""
+    every slot of the two components (native: planner.cpp pgcp_weld_plan)."""
 
     def __init__(self, cycles, steps, n_parent):
         K = len(cycles)
         nb = np.array([len(c) for c in cycles], dtype=np.int64)
         self.loop_off = np.zeros(K + 1, dtype=np.int64)
         self.loop_off[1:] = np.cumsum(nb)
-        self.slot_parent = np.concatenate(cycles).astype(np.int64) if K else np.zeros(0, np.int64)
+        self.slot_parent = np.ascontiguousarray(np.concatenate(cycles).astype(np.int64)) if K else \
+            np.zeros(0, np.int64)
         self.slot_sub = np.repeat(np.arange(K), nb)
-        members = {i: [i] for i in range(K)}
-        table = np.full(n_parent, -1, dtype=np.int64)
-        arcpos = np.zeros(n_parent, dtype=np.int64)
-        cyc = np.zeros(n_parent, dtype=np.int64)
-        info, src, wb, wb_off = [], [], [], [0]
-        self.exterior = []
-        for st in steps:
-            A = members[st.comp_a]
-            B = members[st.comp_b]
-            sa = np.concatenate([np.arange(self.loop_off[i], self.loop_off[i + 1]) for i in A])
-            sb = np.concatenate([np.arange(self.loop_off[i], self.loop_off[i + 1]) for i in B])
-            table[self.slot_parent[sa]] = sa
-            a_src = table[st.a_cycle]
-            table[self.slot_parent[sa]] = -1
-            table[self.slot_parent[sb]] = sb
-            b_src = table[st.b_cycle]
-            table[self.slot_parent[sb]] = -1
-            if (a_src < 0).any() or (b_src < 0).any():
-                raise WeldError("weld step references a boundary vertex outside its components")
-            k = int(st.k)
-            arcpos[st.a_cycle[:k + 1]] = np.arange(1, k + 2)
-            cyc[st.a_cycle] |= CYC_A
-            cyc[st.b_cycle] |= CYC_B
-            pa, pb = self.slot_parent[sa], self.slot_parent[sb]
-            ca = arcpos[pa] | cyc[pa]
-            cb = (arcpos[pb] | cyc[pb]) | SIDE_B
-            arcpos[st.a_cycle[:k + 1]] = 0
-            cyc[st.a_cycle] = 0
-            cyc[st.b_cycle] = 0
-            wb.append(np.stack([sa, ca], 1))
-            wb.append(np.stack([sb, cb], 1))
-            wb_off.append(wb_off[-1] + len(sa) + len(sb))
-            src.append(a_src)
-            src.append(b_src)
-            info.append([k, int(st.closed), len(st.a_cycle), len(st.b_cycle), st.comp_a, st.comp_b])
-            if st.closed:
-                self.exterior_candidates = (list(A), list(B))
-            members[st.comp_a] = A + B
-            del members[st.comp_b]
-        self.info = np.array(info, dtype=np.int32).reshape(-1, 6)
-        self.src = np.concatenate(src).astype(np.int32) if src else np.zeros(0, np.int32)
-        self.wb = (np.concatenate(wb).astype(np.int64) & 0xffffffff).astype(np.uint32).view(np.int32) \
-            if wb else np.zeros((0, 2), np.int32)
-        self.wb = self.wb.reshape(-1, 2)
-        self.wb_off = np.array(wb_off, dtype=np.int64)
         self.n_parent = n_parent
+        self._table = None
+        meta, idx = getattr(steps, "meta", None), getattr(steps, "idx", None)
+        ns = len(steps)
+        if meta is None:
+            meta = np.zeros((max(ns, 1), 8), dtype=np.int64)
+            parts, o = [], 0
+            for q, st in enumerate(steps):
+                la, lb, lm = len(st.a_cycle), len(st.b_cycle), len(st.merged_cycle)
+                meta[q] = (st.comp_a, st.comp_b, st.k, int(st.closed), o, la, lb, lm)
+                parts += [st.a_cycle, st.b_cycle, st.merged_cycle]
+                o += la + lb + lm
+            idx = np.ascontiguousarray(np.concatenate(parts).astype(np.int64)) if parts else np.zeros(1, np.int64)
+        L = nat.lib()
+        lens = (ctypes.c_int64 * 2)()
+        args = [self.slot_parent.ctypes.data, self.loop_off.ctypes.data, K, meta.ctypes.data, idx.ctypes.data, ns,
+                int(n_parent)]
+        nat.check(L.pgcp_weld_plan(*args, None, None, None, None, None, lens))
+        self.info = np.zeros((max(ns, 1), 6), dtype=np.int32)
+        self.src = np.zeros(max(lens[0], 1), dtype=np.int32)
+        self.wb_off = np.zeros(ns + 1, dtype=np.int64)
+        self.wb = np.zeros((max(lens[1], 1), 2), dtype=np.int32)
+        ext = np.zeros(max(K, 1), dtype=np.int32)
+        nat.check(L.pgcp_weld_plan(*args, self.info.ctypes.data, self.src.ctypes.data, self.wb_off.ctypes.data,
+                                   self.wb.ctypes.data, ext.ctypes.data, lens))
+        self.info = self.info[:ns]
+        self.src = self.src[:lens[0]]
+        self.wb = self.wb[:lens[1]]
+        if ns and steps[-1].closed:
+            self.exterior_candidates = ([int(i) for i in np.nonzero(ext[:K] == 1)[0]],
+                                        [int(i) for i in np.nonzero(ext[:K] == 2)[0]])
 
     def slots_of(self, subs):
         return np.concatenate([np.arange(self.loop_off[i], self.loop_off[i + 1]) for i in subs]) \
             if len(subs) else np.zeros(0, np.int64)
 
     def any_slot_of_parents(self, parents):
-        table = np.full(self.n_parent, -1, dtype=np.int64)
-        table[self.slot_parent] = np.arange(len(self.slot_parent))
-        return table[np.asarray(parents, dtype=np.int64)]
+        if self._table is None:
+            self._table = np.full(self.n_parent, -1, dtype=np.int64)
+            self._table[self.slot_parent] = np.arange(len(self.slot_parent))
+        return self._table[np.asarray(parents, dtype=np.int64)]
 
 
 def _poly_area(z):
