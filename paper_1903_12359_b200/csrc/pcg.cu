@@ -1036,18 +1036,22 @@ __device__ __forceinline__ double2 cluster_sum2(cg::cluster_group& cl, int csize
 }
 
 constexpr int KPF = 8;  // prefetched off-diagonal entries per row (4 pairs)
+constexpr int KPF2 = 6;  // k_pcg2 (register budget: p is prefetched as well)
 
-struct SliceBuf {
+template <int KP>
+struct SliceBufT {
     double2 y;    // this lane's solution entry (updated in place, one owner thread)
     double2 p;    // this lane's search direction (k_pcg2: p lives in global memory)
     int w;        // even width
     int remote;   // any entry of the slice owned by another CTA
     int off;      // entry offset of this lane's first pair, relative to the CTA's first entry
-    uint32_t c[KPF];
-    double v[KPF];
+    uint32_t c[KP];
+    double v[KP];
 };
+using SliceBuf = SliceBufT<KPF>;
 
-__device__ __forceinline__ void slice_load(SliceBuf& B, const double* __restrict__ valc,
+template <int KP>
+__device__ __forceinline__ void slice_load(SliceBufT<KP>& B, const double* __restrict__ valc,
                                            const uint32_t* __restrict__ encc, const int* s_ent, const int* s_w,
                                            int ls, int nloc, int lane, const double2* yrow, bool need_y,
                                            const double2* prow = nullptr) {
@@ -1058,7 +1062,7 @@ __device__ __forceinline__ void slice_load(SliceBuf& B, const double* __restrict
     B.remote = 0;
     B.off = 0;
 #pragma unroll
-    for (int k = 0; k < KPF; ++k) {
+    for (int k = 0; k < KP; ++k) {
         B.c[k] = self;
         B.v[k] = 0.0;
     }
@@ -1069,7 +1073,7 @@ __device__ __forceinline__ void slice_load(SliceBuf& B, const double* __restrict
     B.remote = s_w[ls] >> 16;
     B.off = s_ent[ls] + (lane << 1);
 #pragma unroll
-    for (int p = 0; p < KPF / 2; ++p) {
+    for (int p = 0; p < KP / 2; ++p) {
         if (2 * p < B.w) {
             double2 vv = __ldg(reinterpret_cast<const double2*>(valc + B.off + (p << 6)));
             uint2 cc = __ldg(reinterpret_cast<const uint2*>(encc + B.off + (p << 6)));
@@ -1559,35 +1563,35 @@ __global__ void __launch_bounds__(NT, 1) k_pcg2(PcgArgs A) {
             long long c0 = timed ? clock64() : 0;
             // ---- A: q = A z + beta q, y += alpha p_old, p = z + beta p, <p,q>
             double l_pq = 0.0;
-            SliceBuf B0, B1;
+            SliceBufT<KPF2> B0, B1;
             slice_load(B0, valc, encc, s_ent, s_w, warp, nloc, lane, yrow, it > 0, prow);
             for (int ls = warp; ls < nloc; ls += 2 * NW) {
 #pragma unroll
                 for (int half = 0; half < 2; ++half) {
                     const int cur = ls + half * NW;
-                    SliceBuf& Bc = half ? B1 : B0;
-                    SliceBuf& Bn = half ? B0 : B1;
+                    SliceBufT<KPF2>& Bc = half ? B1 : B0;
+                    SliceBufT<KPF2>& Bn = half ? B0 : B1;
                     slice_load(Bn, valc, encc, s_ent, s_w, cur + NW, nloc, lane, yrow, it > 0, prow);
                     if (cur < nloc) {
                         const int li = 32 * cur + lane;
                         const int64_t gr = row0 + li;
                         double2 zi = zl[li];
                         double sx = zi.x, sy = zi.y;
-                        double2 g[KPF];
+                        double2 g[KPF2];
                         if (!Bc.remote) {
 #pragma unroll
-                            for (int k = 0; k < KPF; ++k)
+                            for (int k = 0; k < KPF2; ++k)
                                 g[k] = *reinterpret_cast<const double2*>(reinterpret_cast<const char*>(zl) + Bc.c[k]);
                         } else {
 #pragma unroll
-                            for (int k = 0; k < KPF; ++k) g[k] = gather_gen(s_base, rank, Bc.c[k]);
+                            for (int k = 0; k < KPF2; ++k) g[k] = gather_gen(s_base, rank, Bc.c[k]);
                         }
 #pragma unroll
-                        for (int k = 0; k < KPF; ++k) {
+                        for (int k = 0; k < KPF2; ++k) {
                             sx = fma(Bc.v[k], g[k].x, sx);
                             sy = fma(Bc.v[k], g[k].y, sy);
                         }
-                        for (int k = KPF; k < Bc.w; ++k) {
+                        for (int k = KPF2; k < Bc.w; ++k) {
                             const int e = Bc.off + ((k >> 1) << 6) + (k & 1);
                             uint32_t c = __ldg(encc + e);
                             double v = __ldg(valc + e);

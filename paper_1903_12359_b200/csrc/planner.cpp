@@ -174,25 +174,34 @@ struct Planner {
     }
 
     int check_cover(const int64_t* cuts, int64_t ncuts) {
-        std::set<std::pair<int64_t, int64_t>> glued;
+        // sorted edge lists instead of ordered sets: the glued edges must be
+        // distinct and equal to the cut set
+        std::vector<std::pair<int64_t, int64_t>> glued;
         for (const Step& st : steps) {
-            std::vector<std::pair<int64_t, int64_t>> pairs;
-            for (int64_t i = 0; i < st.k; ++i) pairs.push_back({st.a[i], st.a[i + 1]});
-            if (st.closed) pairs.push_back({st.a[st.k], st.a[0]});
-            for (auto& e : pairs) {
-                auto key = std::make_pair(std::min(e.first, e.second), std::max(e.first, e.second));
-                if (!glued.insert(key).second) {
-                    err = "edge (" + std::to_string(key.first) + ", " + std::to_string(key.second) +
-                          ") glued twice in the schedule";
-                    return PGCP_E_PARTITION;
-                }
-            }
+            for (int64_t i = 0; i < st.k; ++i)
+                glued.push_back({std::min(st.a[i], st.a[i + 1]), std::max(st.a[i], st.a[i + 1])});
+            if (st.closed) glued.push_back({std::min(st.a[st.k], st.a[0]), std::max(st.a[st.k], st.a[0])});
         }
-        std::set<std::pair<int64_t, int64_t>> want;
-        for (int64_t i = 0; i < ncuts; ++i) want.insert({cuts[2 * i], cuts[2 * i + 1]});
-        if (glued != want) {
+        std::vector<std::pair<int64_t, int64_t>> order = glued;
+        std::sort(order.begin(), order.end());
+        for (size_t i = 1; i < order.size(); ++i)
+            if (order[i] == order[i - 1]) {
+                // report the first duplicate in schedule order, as the set-based check would
+                std::set<std::pair<int64_t, int64_t>> seen;
+                for (auto& e : glued)
+                    if (!seen.insert(e).second) {
+                        err = "edge (" + std::to_string(e.first) + ", " + std::to_string(e.second) +
+                              ") glued twice in the schedule";
+                        return PGCP_E_PARTITION;
+                    }
+            }
+        std::vector<std::pair<int64_t, int64_t>> want((size_t)ncuts);
+        for (int64_t i = 0; i < ncuts; ++i) want[i] = {cuts[2 * i], cuts[2 * i + 1]};
+        std::sort(want.begin(), want.end());
+        want.erase(std::unique(want.begin(), want.end()), want.end());
+        if (order != want) {
             size_t missing = 0;
-            for (auto& e : want) missing += glued.count(e) ? 0 : 1;
+            for (auto& e : want) missing += std::binary_search(order.begin(), order.end(), e) ? 0 : 1;
             err = "schedule does not cover all cut edges (" + std::to_string(missing) + " missing)";
             return PGCP_E_PARTITION;
         }
@@ -439,8 +448,12 @@ extern "C" PGCP_API int pgcp_weld_plan(const int64_t* cyc, const int64_t* cyc_of
     for (int32_t i = 0; i < K; ++i) members[i] = {i};
     if (ext)
         for (int32_t i = 0; i < K; ++i) ext[i] = 0;
-    std::vector<int32_t> table((size_t)std::max<int64_t>(n_parent, 1), -1);
-    std::vector<int32_t> code((size_t)std::max<int64_t>(n_parent, 1), 0);
+    // persistent per-thread scratch over parent ids (restored after every use)
+    thread_local std::vector<int32_t> table, code;
+    if ((int64_t)table.size() < std::max<int64_t>(n_parent, 1)) {
+        table.assign((size_t)std::max<int64_t>(n_parent, 1), -1);
+        code.assign((size_t)std::max<int64_t>(n_parent, 1), 0);
+    }
     const int32_t CYC_A = 1 << 25, CYC_B = 1 << 26;
     const uint32_t SIDE_B = 1u << 31;
     int64_t so = 0, wo = 0;
