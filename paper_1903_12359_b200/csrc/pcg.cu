@@ -128,6 +128,11 @@ __global__ void k_fixed_list(int64_t nfixed, const int32_t* __restrict__ gid, co
     }
 }
 
+__global__ void k_gather_i64(const int64_t* __restrict__ src, const int64_t* __restrict__ idx, int64_t n,
+                             int64_t* __restrict__ dst) {
+    GRID_STRIDE(i, n) dst[i] = src[idx[i]];
+}
+
 __global__ void k_unknown_flag(int64_t ne, const int32_t* __restrict__ fixed_ref, int32_t* __restrict__ flag) {
     GRID_STRIDE(e, ne) flag[e] = fixed_ref[e] < 0 ? 1 : 0;
 }
@@ -1564,65 +1569,71 @@ __global__ void __launch_bounds__(NT, 1) k_pcg2(PcgArgs A) {
             // ---- A: q = A z + beta q, y += alpha p_old, p = z + beta p, <p,q>
             double l_pq = 0.0;
             SliceBufT<KPF2> B0, B1;
-            slice_load(B0, valc, encc, s_ent, s_w, warp, nloc, lane, yrow, it > 0, prow);
-            for (int ls = warp; ls < nloc; ls += 2 * NW) {
+            auto row_body = [&](SliceBufT<KPF2>& Bc, int cur, double2& pref, double2& yref) {
+                const int li = 32 * cur + lane;
+                const int64_t gr = row0 + li;
+                double2 zi = zl[li];
+                double sx = zi.x, sy = zi.y;
+                double2 g[KPF2];
+                if (!Bc.remote) {
 #pragma unroll
-                for (int half = 0; half < 2; ++half) {
-                    const int cur = ls + half * NW;
-                    SliceBufT<KPF2>& Bc = half ? B1 : B0;
-                    SliceBufT<KPF2>& Bn = half ? B0 : B1;
-                    slice_load(Bn, valc, encc, s_ent, s_w, cur + NW, nloc, lane, yrow, it > 0, prow);
-                    if (cur < nloc) {
-                        const int li = 32 * cur + lane;
-                        const int64_t gr = row0 + li;
-                        double2 zi = zl[li];
-                        double sx = zi.x, sy = zi.y;
-                        double2 g[KPF2];
-                        if (!Bc.remote) {
+                    for (int k = 0; k < KPF2; ++k)
+                        g[k] = *reinterpret_cast<const double2*>(reinterpret_cast<const char*>(zl) + Bc.c[k]);
+                } else {
 #pragma unroll
-                            for (int k = 0; k < KPF2; ++k)
-                                g[k] = *reinterpret_cast<const double2*>(reinterpret_cast<const char*>(zl) + Bc.c[k]);
-                        } else {
+                    for (int k = 0; k < KPF2; ++k) g[k] = gather_gen(s_base, rank, Bc.c[k]);
+                }
 #pragma unroll
-                            for (int k = 0; k < KPF2; ++k) g[k] = gather_gen(s_base, rank, Bc.c[k]);
-                        }
+                for (int k = 0; k < KPF2; ++k) {
+                    sx = fma(Bc.v[k], g[k].x, sx);
+                    sy = fma(Bc.v[k], g[k].y, sy);
+                }
+                for (int k = KPF2; k < Bc.w; ++k) {
+                    const int e = Bc.off + ((k >> 1) << 6) + (k & 1);
+                    uint32_t c = __ldg(encc + e);
+                    double v = __ldg(valc + e);
+                    double2 rc = gather_enc(s_base, zl, c);
+                    sx = fma(v, rc.x, sx);
+                    sy = fma(v, rc.y, sy);
+                }
+                if (s_mask[cur] & (1u << lane)) {
+                    int2 nb = A.cpl[gr];
+                    double2 cc = A.cplc[gr];
+                    double2 zn = nb.x >= 0 ? gather(cl, zl, nb.x, rank, chunk, inv_chunk) : make_double2(0, 0);
+                    double2 zp = nb.y >= 0 ? gather(cl, zl, nb.y, rank, chunk, inv_chunk) : make_double2(0, 0);
+                    double ax = cc.x * zn.x - cc.y * zp.x, ay = cc.x * zn.y - cc.y * zp.y;
+                    sx -= ay;
+                    sy += ax;
+                }
+                double2 qi = ql[li];
+                double2 pi = pref;
+                yref.x = fma(alpha, pi.x, yref.x);  // alpha = 0 in the first iteration
+                yref.y = fma(alpha, pi.y, yref.y);
+                qi.x = fma(beta, qi.x, sx);
+                qi.y = fma(beta, qi.y, sy);
+                pi.x = fma(beta, pi.x, zi.x);
+                pi.y = fma(beta, pi.y, zi.y);
+                ql[li] = qi;
+                pref = pi;
+                l_pq += pi.x * qi.x + pi.y * qi.y;
+            };
+            {
+                slice_load(B0, valc, encc, s_ent, s_w, warp, nloc, lane, yrow, it > 0, prow);
+                for (int ls = warp; ls < nloc; ls += 2 * NW) {
 #pragma unroll
-                        for (int k = 0; k < KPF2; ++k) {
-                            sx = fma(Bc.v[k], g[k].x, sx);
-                            sy = fma(Bc.v[k], g[k].y, sy);
+                    for (int half = 0; half < 2; ++half) {
+                        const int cur = ls + half * NW;
+                        SliceBufT<KPF2>& Bc = half ? B1 : B0;
+                        SliceBufT<KPF2>& Bn = half ? B0 : B1;
+                        slice_load(Bn, valc, encc, s_ent, s_w, cur + NW, nloc, lane, yrow, it > 0, prow);
+                        if (cur < nloc) {
+                            const int li = 32 * cur + lane;
+                            double2 pv = Bc.p, yv = Bc.y;
+                            if (it == 0) yv = make_double2(0.0, 0.0);
+                            row_body(Bc, cur, pv, yv);
+                            prow[li] = pv;
+                            if (it > 0) yrow[li] = yv;
                         }
-                        for (int k = KPF2; k < Bc.w; ++k) {
-                            const int e = Bc.off + ((k >> 1) << 6) + (k & 1);
-                            uint32_t c = __ldg(encc + e);
-                            double v = __ldg(valc + e);
-                            double2 rc = gather_enc(s_base, zl, c);
-                            sx = fma(v, rc.x, sx);
-                            sy = fma(v, rc.y, sy);
-                        }
-                        if (s_mask[cur] & (1u << lane)) {
-                            int2 nb = A.cpl[gr];
-                            double2 cc = A.cplc[gr];
-                            double2 zn = nb.x >= 0 ? gather(cl, zl, nb.x, rank, chunk, inv_chunk) : make_double2(0, 0);
-                            double2 zp = nb.y >= 0 ? gather(cl, zl, nb.y, rank, chunk, inv_chunk) : make_double2(0, 0);
-                            double ax = cc.x * zn.x - cc.y * zp.x, ay = cc.x * zn.y - cc.y * zp.y;
-                            sx -= ay;
-                            sy += ax;
-                        }
-                        double2 qi = ql[li];
-                        double2 pi = Bc.p;
-                        if (it > 0) {
-                            double2 yv = Bc.y;
-                            yv.x = fma(alpha, pi.x, yv.x);
-                            yv.y = fma(alpha, pi.y, yv.y);
-                            yrow[li] = yv;
-                        }
-                        qi.x = fma(beta, qi.x, sx);
-                        qi.y = fma(beta, qi.y, sy);
-                        pi.x = fma(beta, pi.x, zi.x);
-                        pi.y = fma(beta, pi.y, zi.y);
-                        ql[li] = qi;
-                        prow[li] = pi;
-                        l_pq += pi.x * qi.x + pi.y * qi.y;
                     }
                 }
             }
@@ -1661,12 +1672,14 @@ __global__ void __launch_bounds__(NT, 1) k_pcg2(PcgArgs A) {
         if (A.timing && threadIdx.x == 0)
             for (int q = 0; q < 6; ++q) A.timing[8 * blockIdx.x + q] = tm[q];
         // the last update y += alpha p
-        for (int i = threadIdx.x; i < 32 * nloc; i += NT) {
-            double2 pi = prow[i];
-            double2 yv = yrow[i];
-            yv.x = fma(alpha, pi.x, yv.x);
-            yv.y = fma(alpha, pi.y, yv.y);
-            yrow[i] = yv;
+        {
+            for (int i = threadIdx.x; i < 32 * nloc; i += NT) {
+                double2 pi = prow[i];
+                double2 yv = yrow[i];
+                yv.x = fma(alpha, pi.x, yv.x);
+                yv.y = fma(alpha, pi.y, yv.y);
+                yrow[i] = yv;
+            }
         }
     }
     if (rank == 0 && threadIdx.x == 0) {
@@ -2143,9 +2156,14 @@ int build_system(pgcp_batch* b, SolveSystem* S, bool dncp, const int32_t* d_pins
     PGCP_LAUNCH_CHECK();
     PGCP_TRY(exclusive_scan_i32_to_i64(flag.p, uscan.p, S->ne, s));
     std::vector<int64_t> hus(nslot + 1);
-    for (int j = 0; j <= nslot; ++j)
-        PGCP_TRY_CUDA(cudaMemcpyAsync(&hus[j], uscan.p + S->h_sv_off[j], sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-    PGCP_TRY_CUDA(cudaStreamSynchronize(s));
+    {
+        DevBuf<int64_t> g;
+        PGCP_TRY(g.alloc(nslot + 1, s));
+        k_gather_i64<<<grid_for(nslot + 1, 128), 128, 0, s>>>(uscan.p, S->sv_off.p, nslot + 1, g.p);
+        PGCP_LAUNCH_CHECK();
+        PGCP_TRY_CUDA(cudaMemcpyAsync(hus.data(), g.p, (nslot + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        PGCP_TRY_CUDA(cudaStreamSynchronize(s));
+    }
     S->h_nu.resize(nslot);
     S->h_sl_off.assign(nslot + 1, 0);
     for (int j = 0; j < nslot; ++j) {

@@ -609,18 +609,20 @@ __global__ void __launch_bounds__(NT, 1) k_phase1c(Phase1Args A) {
     }
     int parity = 0;
     // publish the listed global points into every CTA's slots, then barrier
+    // the thread that owns point g (the one that last wrote it) sends it, so
+    // no CTA barrier is needed before the cluster barrier
     auto publish = [&](const int* gidx, int np, double flag) {
-        __syncthreads();
-        for (int q = threadIdx.x; q < np * CS; q += NT) {
-            int which = q / CS, dst = q % CS;
+        for (int which = 0; which < np; ++which) {
             int g = gidx[which];
-            if (g >= lo && g < hi) {
+            if (g >= lo && g < hi && (g - lo) % NT == (int)threadIdx.x) {
                 PParam pp;
                 pp.z = pts[g - lo];
                 pp.s = sides[g - lo];
                 pp.pad = 0;
-                PParam* rs = cl.map_shared_rank(&s_param[parity][0], dst);
-                rs[which] = pp;
+                for (int dst = 0; dst < CS; ++dst) {
+                    PParam* rs = cl.map_shared_rank(&s_param[parity][0], dst);
+                    rs[which] = pp;
+                }
             }
         }
         if (threadIdx.x < CS) {
@@ -896,10 +898,14 @@ __global__ void k_replay_slots(ReplayArgs A) {
         double2 z = A.tv[slot];
         int8_t s = 0;
         double stage = 0;
+        Rec cur;
+        if (nrec > 0) cur = log[0];
         for (int r = 0; r < nrec; ++r) {
             if (r == sq) stage = c_fin(z) ? cabs_(z) : 0.0;
-            Rec rec = log[r];
-            apply_rec(rec, z, s);
+            Rec nxt;
+            if (r + 1 < nrec) nxt = log[r + 1];  // in flight while cur is applied
+            apply_rec(cur, z, s);
+            cur = nxt;
         }
         if (c_nan(z)) atomicExch(A.nan_flag, 1);
         A.tv[slot] = z;
