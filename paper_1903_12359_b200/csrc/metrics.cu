@@ -42,6 +42,7 @@ __global__ void k_stitch(int64_t n, const int64_t* __restrict__ lv_off, const in
                          const double2* __restrict__ z, double2* __restrict__ coords, int32_t* __restrict__ prov,
                          const int32_t* __restrict__ lv_comp, unsigned long long* spread_bits,
                          unsigned long long* scale_bits, int* missing) {
+    double tsp = 0, tsc = 0;  // this thread's maxima (reduced per warp: max is order-free)
     GRID_STRIDE(v, n) {
         int64_t lo = lv_off[v], hi = lv_off[v + 1];
         if (lo == hi) {
@@ -63,8 +64,14 @@ __global__ void k_stitch(int64_t n, const int64_t* __restrict__ lv_off, const in
         double cnt = (double)(hi - lo);
         coords[v] = cdiv_np(acc, make_double2(cnt, 0.0));
         prov[v] = lv_comp[lo];
-        atomic_max_pos(spread_bits, sp);
-        atomic_max_pos(scale_bits, sc);
+        tsp = fmax(tsp, sp);
+        tsc = fmax(tsc, sc);
+    }
+    tsp = warp_max(tsp);
+    tsc = warp_max(tsc);
+    if ((threadIdx.x & 31) == 0) {
+        atomic_max_pos(spread_bits, tsp);
+        atomic_max_pos(scale_bits, tsc);
     }
 }
 

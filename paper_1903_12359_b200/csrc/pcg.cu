@@ -535,10 +535,18 @@ __global__ void k_proj(int64_t ne, int32_t nslot, const int32_t* __restrict__ co
         pxy[u] = make_float2(px, py);
         key[u] = ((unsigned long long)j << 32) | f32_order(px);
         val[u] = (int32_t)e;
-        atomicMin(&bbox[4 * j], f32_order(px));
-        atomicMax(&bbox[4 * j + 1], f32_order(px));
-        atomicMin(&bbox[4 * j + 2], f32_order(py));
-        atomicMax(&bbox[4 * j + 3], f32_order(py));
+        // box of the slot: one atomic per distinct slot per warp
+        const unsigned act = __activemask();
+        const unsigned peers = __match_any_sync(act, j);
+        const uint32_t ox = f32_order(px), oy = f32_order(py);
+        const uint32_t x0 = __reduce_min_sync(peers, ox), x1 = __reduce_max_sync(peers, ox);
+        const uint32_t y0 = __reduce_min_sync(peers, oy), y1 = __reduce_max_sync(peers, oy);
+        if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) {
+            atomicMin(&bbox[4 * j], x0);
+            atomicMax(&bbox[4 * j + 1], x1);
+            atomicMin(&bbox[4 * j + 2], y0);
+            atomicMax(&bbox[4 * j + 3], y1);
+        }
     }
 }
 
@@ -925,29 +933,31 @@ __global__ void __launch_bounds__(INV_THREADS, 1) k_coarse_inv(const int64_t* __
         const bool drop = !(p > tol);
         for (int i = threadIdx.x; i < nr; i += INV_THREADS) colk[i] = Ml[(size_t)i * n + k];
         __syncthreads();
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        constexpr int NWI = INV_THREADS / 32;
         if (drop) {
-            for (int t = threadIdx.x; t < nr * n; t += INV_THREADS) {
-                const int i = t / n, c = t - i * n;
-                if (i0 + i == k || c == k) Ml[t] = make_double2(0.0, 0.0);
-            }
+            for (int i = warp; i < nr; i += NWI)
+                for (int c = lane; c < n; c += 32)
+                    if (i0 + i == k || c == k) Ml[(size_t)i * n + c] = make_double2(0.0, 0.0);
         } else {
             const double ip = 1.0 / p;
-            for (int t = threadIdx.x; t < nr * n; t += INV_THREADS) {
-                const int i = t / n, c = t - i * n;
+            for (int i = warp; i < nr; i += NWI) {
                 const int gi = i0 + i;
-                double2 v;
-                if (gi == k && c == k) {
-                    v = make_double2(ip, 0.0);
-                } else if (gi == k) {
-                    v = make_double2(rk[c].x * ip, rk[c].y * ip);
-                } else if (c == k) {
-                    v = make_double2(-colk[i].x * ip, -colk[i].y * ip);
-                } else {
-                    const double2 a = colk[i], b = rk[c];
-                    const double2 m = Ml[t];
-                    v = make_double2(m.x - (a.x * b.x - a.y * b.y) * ip, m.y - (a.x * b.y + a.y * b.x) * ip);
+                const double2 a = colk[i];
+                double2* row = Ml + (size_t)i * n;
+                for (int c = lane; c < n; c += 32) {
+                    const double2 b = rk[c];
+                    double2 v;
+                    if (gi == k) {
+                        v = (c == k) ? make_double2(ip, 0.0) : make_double2(b.x * ip, b.y * ip);
+                    } else if (c == k) {
+                        v = make_double2(-a.x * ip, -a.y * ip);
+                    } else {
+                        const double2 m = row[c];
+                        v = make_double2(m.x - (a.x * b.x - a.y * b.y) * ip, m.y - (a.x * b.y + a.y * b.x) * ip);
+                    }
+                    row[c] = v;
                 }
-                Ml[t] = v;
             }
         }
         __syncthreads();

@@ -159,6 +159,29 @@ def row_tree_schedule_order(kx, ky):
     return order
 
 
+def pairwise_tree_schedule_order(kx, ky):
+    """Fully balanced variant: blocks of a row are merged pairwise (spans
+    1, 2, 4, ...), then the rows pairwise as in `row_tree_schedule_order`.
+    log2(kx) + log2(ky) weld levels instead of (kx - 1) + log2(ky); every
+    merge still glues one contiguous arc (the edge between two adjacent
+    blocks, or the full row edge)."""
+    order = []
+    span = 1
+    while span < kx:
+        for r in range(ky):
+            for bx in range(0, kx, 2 * span):
+                if bx + span < kx:
+                    order.append((r * kx + bx, r * kx + bx + span))
+        span *= 2
+    span = 1
+    while span < ky:
+        for r in range(0, ky, 2 * span):
+            if r + span < ky:
+                order.append((r * kx, (r + span) * kx))
+        span *= 2
+    return order
+
+
 # ---------------------------------------------------------------------------
 # icosphere (vectorised edge-midpoint subdivision; `shapes.py:52-92` ordering
 # of new vertices is NOT reproduced -- only the geometry class)

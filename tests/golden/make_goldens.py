@@ -288,34 +288,65 @@ def weld_corpus(seed=0, count=12):
     print(f"weld_corpus: {count} welds")
 
 
+def _cases():
+    def c_cfg1():
+        V, F, cuts = gen.cfg1(seed=0)
+        pipeline_case("cfg1", V, F, cuts, "free")
+
+    def c_strips4():
+        V, F, cuts = gen.height_field_case(33, 4, layout="strips", seed=3)
+        pipeline_case("strips4", V, F, cuts, "free")
+
+    def c_blocks3x3():
+        V, F, cuts = gen.height_field_case(31, 3, seed=5)
+        pipeline_case("blocks3x3", V, F, cuts, "free")
+
+    def c_disk2x2():
+        V, F, cuts = gen.height_field_case(30, 2, seed=7)
+        pipeline_case("disk2x2", V, F, cuts, "disk")
+
+    def c_k1():
+        V, F = gen.height_field_grid(25, seed=11)
+        pipeline_case("k1free", V, F, None, "free")
+        pipeline_case("k1disk", V, F, None, "disk")
+
+    def c_flat2x2():
+        Vf, Ff = gen.flat_grid_arrays(20)
+        cf = gen.cuts_from_face_labels(Ff, gen.block_face_labels(21, 2))
+        pipeline_case("flat2x2", Vf, Ff, cf, "free")
+
+    def c_sphere():
+        sph = ref_shapes.icosphere(3)
+        lab = ref_shapes.hemisphere_labels(sph)
+        pipeline_case("sphere2", np.array(sph.vertices), np.array(sph.faces),
+                      ref_shapes.cuts_from_face_labels(sph, lab), "sphere")
+        lab = ref_shapes.azimuth_labels(sph, 4)
+        pipeline_case("sphere4", np.array(sph.vertices), np.array(sph.faces),
+                      ref_shapes.cuts_from_face_labels(sph, lab), "sphere")
+
+    def c_tree4x4():
+        # balanced rows->strips->tree schedule on 4x4 blocks (documented deviation)
+        V, F, cuts = gen.height_field_case(41, 4, seed=2)
+        pipeline_case("tree4x4", V, F, cuts, "free",
+                      schedule_pairs=gen.row_tree_schedule_order(4, 4))
+
+    def c_ptree4x4():
+        # fully pairwise tree (blocks -> pairs -> rows -> strips), the bench's order
+        V, F, cuts = gen.height_field_case(41, 4, seed=2)
+        pipeline_case("ptree4x4", V, F, cuts, "free",
+                      schedule_pairs=gen.pairwise_tree_schedule_order(4, 4))
+
+    return {"known_answers": known_answers, "weld_corpus": weld_corpus, "cfg1": c_cfg1, "strips4": c_strips4,
+            "blocks3x3": c_blocks3x3, "disk2x2": c_disk2x2, "k1": c_k1, "flat2x2": c_flat2x2,
+            "sphere": c_sphere, "tree4x4": c_tree4x4, "ptree4x4": c_ptree4x4}
+
+
 def main():
-    known_answers()
-    weld_corpus()
-    V, F, cuts = gen.cfg1(seed=0)
-    pipeline_case("cfg1", V, F, cuts, "free")
-    V, F, cuts = gen.height_field_case(33, 4, layout="strips", seed=3)
-    pipeline_case("strips4", V, F, cuts, "free")
-    V, F, cuts = gen.height_field_case(31, 3, seed=5)
-    pipeline_case("blocks3x3", V, F, cuts, "free")
-    V, F, cuts = gen.height_field_case(30, 2, seed=7)
-    pipeline_case("disk2x2", V, F, cuts, "disk")
-    V, F = gen.height_field_grid(25, seed=11)
-    pipeline_case("k1free", V, F, None, "free")
-    pipeline_case("k1disk", V, F, None, "disk")
-    Vf, Ff = gen.flat_grid_arrays(20)
-    cf = gen.cuts_from_face_labels(Ff, gen.block_face_labels(21, 2))
-    pipeline_case("flat2x2", Vf, Ff, cf, "free")
-    sph = ref_shapes.icosphere(3)
-    lab = ref_shapes.hemisphere_labels(sph)
-    pipeline_case("sphere2", np.array(sph.vertices), np.array(sph.faces),
-                  ref_shapes.cuts_from_face_labels(sph, lab), "sphere")
-    lab = ref_shapes.azimuth_labels(sph, 4)
-    pipeline_case("sphere4", np.array(sph.vertices), np.array(sph.faces),
-                  ref_shapes.cuts_from_face_labels(sph, lab), "sphere")
-    # balanced rows->strips->tree schedule on 4x4 blocks (documented deviation)
-    V, F, cuts = gen.height_field_case(41, 4, seed=2)
-    pipeline_case("tree4x4", V, F, cuts, "free",
-                  schedule_pairs=gen.row_tree_schedule_order(4, 4))
+    """python make_goldens.py [case ...]  (default: every case)"""
+    cases = _cases()
+    names = sys.argv[1:] or list(cases)
+    for n in names:
+        cases[n]()
 
 
 if __name__ == "__main__":

@@ -8,12 +8,12 @@ import json
 import numpy as np
 import pytest
 
-from conftest import load_golden, unpack
+from conftest import case_pairs, load_golden, unpack
 
 pytestmark = pytest.mark.gpu
 
 CASES = ["cfg1", "strips4", "blocks3x3", "disk2x2", "k1free", "k1disk", "flat2x2", "sphere2", "sphere4",
-         "tree4x4"]
+         "tree4x4", "ptree4x4"]
 
 
 def _diam(z):
@@ -25,7 +25,7 @@ def _diam(z):
     return 2 * np.max(np.abs(zz - c))
 
 
-@pytest.mark.parametrize("case", ["cfg1", "blocks3x3", "sphere4", "disk2x2", "tree4x4"])
+@pytest.mark.parametrize("case", ["cfg1", "blocks3x3", "sphere4", "disk2x2", "tree4x4", "ptree4x4"])
 def test_welds_match_reference(cuda, case):
     from paper_1903_12359_b200 import closed_weld, partial_weld
     z = load_golden(case)
@@ -66,13 +66,12 @@ def test_geodesic_matches_reference(cuda):
 @pytest.mark.parametrize("case", CASES)
 def test_pipeline_matches_reference(cuda, case):
     from paper_1903_12359_b200 import TriMesh, parameterize
-    from paper_1903_12359_b200.generators import row_tree_schedule_order
     z = load_golden(case)
     mesh = TriMesh(z["V"], z["F"])
     cuts = z["cuts"] if len(z["cuts"]) else None
     kw = {}
-    if case == "tree4x4":
-        kw["pairs"] = row_tree_schedule_order(4, 4)
+    if case_pairs(case) is not None:
+        kw["pairs"] = case_pairs(case)
     gp, rep = parameterize(mesh, cuts, str(z["mode"]), **kw)
     ref = z["coords"]
     got = np.asarray(gp.coords)

@@ -10,7 +10,7 @@ import re
 import numpy as np
 import pytest
 
-from conftest import ROOT, load_golden, unpack
+from conftest import ROOT, case_pairs, load_golden, unpack
 
 import oracle
 from paper_1903_12359_b200 import generators as gen
@@ -55,11 +55,11 @@ def _part(case):
 
 
 @pytest.mark.parametrize("case", ["cfg1", "strips4", "blocks3x3", "disk2x2", "flat2x2",
-                                  "sphere2", "sphere4", "tree4x4"])
+                                  "sphere2", "sphere4", "tree4x4", "ptree4x4"])
 def test_native_planner_matches_reference(case):
     from paper_1903_12359_b200.partition import plan_weld_schedule
     z, p = _part(case)
-    pairs = gen.row_tree_schedule_order(4, 4) if case == "tree4x4" else None
+    pairs = case_pairs(case)
     steps = plan_weld_schedule(p, str(z["mode"]), pairs=pairs)
     A, B, M = unpack(z, "step_a"), unpack(z, "step_b"), unpack(z, "step_merged")
     assert len(steps) == len(A)

@@ -12,7 +12,7 @@ import os
 import numpy as np
 import pytest
 
-from conftest import PIPELINE_CASES, load_golden, unpack, unpack_csr
+from conftest import PIPELINE_CASES, case_pairs, load_golden, unpack, unpack_csr
 
 import oracle
 from oracle import planner as opl
@@ -26,9 +26,8 @@ def test_oracle_pipeline_bitwise(case):
     mode = str(z["mode"])
     cuts = z["cuts"] if len(z["cuts"]) else None
     kw = {}
-    if case == "tree4x4":
-        from paper_1903_12359_b200.generators import row_tree_schedule_order
-        kw = dict(schedule="pairs", pairs=row_tree_schedule_order(4, 4))
+    if case_pairs(case) is not None:
+        kw = dict(schedule="pairs", pairs=case_pairs(case))
     out = oracle.run_parameterize(z["V"], z["F"], cuts, mode, **kw)
     coords = np.asarray(out["coords"])
     assert np.array_equal(coords, z["coords"])

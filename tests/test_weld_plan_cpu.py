@@ -5,7 +5,7 @@ reference's weld loop, pipeline.py:172-213, flattened to boundary slots)."""
 import numpy as np
 import pytest
 
-from conftest import load_golden, unpack
+from conftest import case_pairs, load_golden, unpack
 
 from paper_1903_12359_b200 import generators as gen
 
@@ -63,7 +63,7 @@ class _P:
 
 
 @pytest.mark.parametrize("case", ["cfg1", "strips4", "blocks3x3", "disk2x2", "flat2x2", "sphere2", "sphere4",
-                                  "tree4x4"])
+                                  "tree4x4", "ptree4x4"])
 def test_native_weld_plan_matches_numpy(case):
     from paper_1903_12359_b200.partition import plan_weld_schedule
     from paper_1903_12359_b200.pipeline import WeldPlan
@@ -71,7 +71,7 @@ def test_native_weld_plan_matches_numpy(case):
     p = _P()
     p.boundary_cycles = unpack(z, "cycles")
     p.cuts = np.sort(z["cuts"], axis=1) if len(z["cuts"]) else np.zeros((0, 2), np.int64)
-    pairs = gen.row_tree_schedule_order(4, 4) if case == "tree4x4" else None
+    pairs = case_pairs(case)
     steps = plan_weld_schedule(p, str(z["mode"]), pairs=pairs)
     n_parent = len(z["V"])
     plan = WeldPlan(p.boundary_cycles, steps, n_parent)
