@@ -272,10 +272,10 @@ def main():
     e2e = None
     if not args.no_e2e:
         Vp = torch.from_numpy(np.ascontiguousarray(V)).pin_memory()
-        Fp = torch.from_numpy(np.ascontiguousarray(F.astype(np.int64))).pin_memory()
+        Fp = torch.from_numpy(np.ascontiguousarray(F.astype(np.int32))).pin_memory()  # BASELINE: int32 faces
         Cp = torch.from_numpy(np.ascontiguousarray(cuts)).pin_memory()
         Vn, Fn, Cn = Vp.numpy(), Fp.numpy(), Cp.numpy()
-        h2d = Vn.nbytes + (Fn.nbytes // 2) + Cn.nbytes  # faces travel as int32
+        h2d = Vn.nbytes + Fn.nbytes + Cn.nbytes
         d2h = 0
         for i in range(args.warmup + args.steps):
             if i == args.warmup:

@@ -237,6 +237,11 @@ PGCP_API int pgcp_polygon_interior(const double* tv, const int32_t* src, int32_t
 PGCP_API int pgcp_inv_shift(double* z, const int32_t* idx, int64_t n, double add_re, double add_im,
                             double sub_re, double sub_im, void* stream);
 
+/* device int64 face indices -> int32 (values outside [0, 2^31) become -1,
+ * which pgcp_batch_create reports as "face index out of range"); lets
+ * TriMesh upload the reference's int64 faces without a host-side cast */
+PGCP_API int pgcp_faces_from_i64(const int64_t* src, int32_t* dst, int64_t count, void* stream);
+
 /* dst[i] = src[idx[i]] / dst[idx[i]] = src[i] for complex arrays */
 PGCP_API int pgcp_gather_complex(const double* src, const int32_t* idx, double* dst, int64_t n, void* stream);
 PGCP_API int pgcp_scatter_complex(const double* src, const int32_t* idx, double* dst, int64_t n, void* stream);

@@ -27,14 +27,25 @@ enum : int {
     ERR_VALENCE = 4,
 };
 
+// range errors outrank repeated-vertex errors (the reference checks the
+// whole index range first): repeats are recorded at index m + f
 __global__ void k_validate_faces(const int32_t* __restrict__ F, int64_t m, int64_t n, DevErr* err) {
     GRID_STRIDE(f, m) {
         int a = F[3 * f], b = F[3 * f + 1], c = F[3 * f + 2];
         if (a < 0 || b < 0 || c < 0 || a >= n || b >= n || c >= n) {
             dev_fail(err, ERR_FACE_RANGE, f);
         } else if (a == b || b == c || c == a) {
-            dev_fail(err, ERR_FACE_REPEAT, f);
+            dev_fail(err, ERR_FACE_REPEAT, m + f);
         }
+    }
+}
+
+// int64 face indices -> int32; values outside [0, 2^31) become -1 (reported
+// as out of range by the validation)
+__global__ void k_faces_i64(const int64_t* __restrict__ src, int32_t* __restrict__ dst, int64_t count) {
+    GRID_STRIDE(i, count) {
+        int64_t v = src[i];
+        dst[i] = (v >= 0 && v < 2147483647ll) ? (int32_t)v : -1;
     }
 }
 
@@ -617,7 +628,7 @@ int build_partition(pgcp_batch* b, const int64_t* cuts, int64_t ncuts, bool no_c
         if (herr.code == ERR_FACE_RANGE)
             set_error("face index out of range [0, %lld)", (long long)n);
         else
-            set_error("face %llu has repeated vertices", herr.index);
+            set_error("face %llu has repeated vertices", herr.index - (unsigned long long)m);
         return PGCP_E_MESH;
     }
 
@@ -911,3 +922,14 @@ int local_faces(pgcp_batch* b, int64_t* face_off, int32_t* faces, cudaStream_t s
 }
 
 }  // namespace pgcp
+
+extern "C" PGCP_API int pgcp_faces_from_i64(const int64_t* src, int32_t* dst, int64_t count, void* stream) {
+    if (count < 0 || (count > 0 && (!src || !dst))) {
+        pgcp::set_error("pgcp_faces_from_i64: invalid arguments");
+        return PGCP_E_INVALID;
+    }
+    if (count == 0) return PGCP_OK;
+    pgcp::k_faces_i64<<<pgcp::grid_for(count, 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(src, dst, count);
+    PGCP_LAUNCH_CHECK();
+    return PGCP_OK;
+}

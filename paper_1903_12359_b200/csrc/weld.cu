@@ -105,15 +105,18 @@ __device__ double2 csqrt_(double2 z) {
 __device__ __forceinline__ int rec_side(int flags, int k) { return (int)(int8_t)((flags >> (16 + 8 * k)) & 0xff); }
 
 // one record on one point (welding.py:251-509)
-__device__ void apply_rec(const Rec& r, double2& z, int8_t& s) {
+__device__ __forceinline__ void apply_rec(const Rec& r, double2& z, int8_t& s) {
     const double* p = r.p;
     switch (r.kind) {
         case R_MOB: {
             double2 a = C(p[0], p[1]), b = C(p[2], p[3]), c = C(p[4], p[5]), d = C(p[6], p[7]);
             bool axis = r.flags & 1;
             int npins = (r.flags >> 8) & 0xff;
-            for (int k = 0; k < npins; ++k) {
-                if (c_eq(z, C(p[8 + 4 * k], p[9 + 4 * k]))) {
+            // at most two pins (p[8..15]); static indices keep the record in
+            // registers (a dynamic index would put it on the local stack)
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                if (k < npins && c_eq(z, C(p[8 + 4 * k], p[9 + 4 * k]))) {
                     z = C(p[10 + 4 * k], p[11 + 4 * k]);
                     s = (int8_t)rec_side(r.flags, k);
                     return;
@@ -297,9 +300,13 @@ __device__ Rec mk_mob(double2 a, double2 b, double2 c, double2 d, bool axis = fa
     for (int i = 8; i < 16; ++i) r.p[i] = 0.0;
     return r;
 }
-__device__ void mob_pin(Rec& r, double2 pz, double2 pw, int side) {
-    int k = (r.flags >> 8) & 0xff;
-    r.p[8 + 4 * k] = pz.x; r.p[9 + 4 * k] = pz.y; r.p[10 + 4 * k] = pw.x; r.p[11 + 4 * k] = pw.y;
+__device__ __forceinline__ void mob_pin(Rec& r, double2 pz, double2 pw, int side) {
+    int k = (r.flags >> 8) & 0xff;  // 0 or 1 (two pins at most)
+    if (k == 0) {
+        r.p[8] = pz.x; r.p[9] = pz.y; r.p[10] = pw.x; r.p[11] = pw.y;
+    } else {
+        r.p[12] = pz.x; r.p[13] = pz.y; r.p[14] = pw.x; r.p[15] = pw.y;
+    }
     r.flags = (r.flags & ~(0xff << 8)) | ((k + 1) << 8);
     r.flags |= ((side & 0xff) << (16 + 8 * k));
 }
@@ -596,7 +603,10 @@ __global__ void __launch_bounds__(NT, 1) k_phase1c(Phase1Args A) {
         int8_t sd8 = 0;
         if (t <= k) {
             z = A.tv[(side ? sb : sa)[t]];
-            apply_rec(pre[side], z, sd8);
+            if (side)
+                apply_rec(pre[1], z, sd8);
+            else
+                apply_rec(pre[0], z, sd8);
         } else {
             z = (t == k + 1) ? C(0.0, 0.0) : cinf();
         }
@@ -637,7 +647,10 @@ __global__ void __launch_bounds__(NT, 1) k_phase1c(Phase1Args A) {
             if (side ? !ub : !ua) continue;
             double2 z = pts[g - lo];
             int8_t s8 = sides[g - lo];
-            apply_rec(side ? rb : ra, z, s8);
+            if (side)  // separate calls keep both records in registers
+                apply_rec(rb, z, s8);
+            else
+                apply_rec(ra, z, s8);
             pts[g - lo] = z;
             sides[g - lo] = s8;
         }
@@ -691,17 +704,20 @@ __global__ void __launch_bounds__(NT, 1) k_phase1c(Phase1Args A) {
         publish(gi, 2, 0.0);
         PParam* pp = s_param[parity];
         bool has[2] = {false, false};
-        Rec rr[2];
-        for (int side = 0; side < 2 && !err; ++side) {
+        Rec rr0, rr1;
+#pragma unroll
+        for (int side = 0; side < 2; ++side) {
+            if (err) break;
             double2 w0 = pp[side].z;
             if (!c_isinf(w0)) {
                 if (c_zero(w0)) {
                     err = WE_FAR0; eaux = side;
                 } else {
                     int br = side ? DOWN : UP;
-                    rr[side] = mk_mob(C(1, 0), C(0, 0), cdiv(C(-1.0, 0.0), w0), C(1, 0), true);
-                    mob_pin(rr[side], w0, cinf(), br);
-                    mob_pin(rr[side], C(0, 0), C(0, 0), br);
+                    Rec& rs = side ? rr1 : rr0;
+                    rs = mk_mob(C(1, 0), C(0, 0), cdiv(C(-1.0, 0.0), w0), C(1, 0), true);
+                    mob_pin(rs, w0, cinf(), br);
+                    mob_pin(rs, C(0, 0), C(0, 0), br);
                     has[side] = true;
                 }
             }
@@ -709,10 +725,10 @@ __global__ void __launch_bounds__(NT, 1) k_phase1c(Phase1Args A) {
         parity ^= 1;
         if (err) goto fail;
         if (logger) {
-            if (has[0]) log_a[na_rec++] = rr[0];
-            if (has[1]) log_b[nb_rec++] = rr[1];
+            if (has[0]) log_a[na_rec++] = rr0;
+            if (has[1]) log_b[nb_rec++] = rr1;
         }
-        apply_pair(rr[0], has[0], rr[1], has[1]);
+        apply_pair(rr0, has[0], rr1, has[1]);
     }
     // ---- closing loop (welding.py:673-687)
     for (int j = k - 1; j >= 1; --j) {
@@ -898,14 +914,9 @@ __global__ void k_replay_slots(ReplayArgs A) {
         double2 z = A.tv[slot];
         int8_t s = 0;
         double stage = 0;
-        Rec cur;
-        if (nrec > 0) cur = log[0];
         for (int r = 0; r < nrec; ++r) {
             if (r == sq) stage = c_fin(z) ? cabs_(z) : 0.0;
-            Rec nxt;
-            if (r + 1 < nrec) nxt = log[r + 1];  // in flight while cur is applied
-            apply_rec(cur, z, s);
-            cur = nxt;
+            apply_rec(log[r], z, s);  // fields read in place (L1 broadcast), no local copy
         }
         if (c_nan(z)) atomicExch(A.nan_flag, 1);
         A.tv[slot] = z;

@@ -156,9 +156,9 @@ def bench_distributed(args, V, F, cuts, pairs, metric, unit, workload):
         e2e = None
         if not args.no_e2e:
             Vn = torch.from_numpy(np.ascontiguousarray(V)).pin_memory().numpy()
-            Fn = torch.from_numpy(np.ascontiguousarray(F.astype(np.int64))).pin_memory().numpy()
+            Fn = torch.from_numpy(np.ascontiguousarray(F.astype(np.int32))).pin_memory().numpy()
             Cn = torch.from_numpy(np.ascontiguousarray(cuts)).pin_memory().numpy()
-            h2d = Vn.nbytes + Fn.nbytes // 2 + Cn.nbytes
+            h2d = Vn.nbytes + Fn.nbytes + Cn.nbytes
             d2h = 0
             et = []
             for i in range(args.warmup + args.steps):
