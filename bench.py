@@ -284,7 +284,7 @@ def main():
             mesh = pg.TriMesh(Vn, Fn)
             gp, rep = pg.parameterize(mesh, Cn, "free", pairs=pairs)
             coords = gp.coords
-            d2h = coords.nbytes + len(gp.provenance) * 4
+            d2h = coords.nbytes + gp.provenance.nbytes  # both arrays cross PCIe as returned
         torch.cuda.synchronize()
         et = (time.perf_counter() - t0) / args.steps
         e2e = {"value": n / et, "unit": UNIT, "ms_per_step": 1e3 * et, "h2d_bytes_per_step": int(h2d),

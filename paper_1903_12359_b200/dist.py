@@ -167,7 +167,7 @@ def bench_distributed(args, V, F, cuts, pairs, metric, unit, workload):
                 t0 = time.perf_counter()
                 mesh = pg.TriMesh(Vn, Fn)
                 gp, rep = parameterize_distributed(mesh, Cn, "free", pairs=pairs)
-                d2h = gp.coords.nbytes + len(gp.provenance) * 4
+                d2h = gp.coords.nbytes + gp.provenance.nbytes
                 torch.cuda.synchronize()
                 dt = _max_over_ranks(time.perf_counter() - t0, dev)
                 if i >= args.warmup:
