@@ -9,9 +9,9 @@ end, plus the batched-PCG HBM roofline).
 Workload (BASELINE configs[1], the largest single-GPU configuration the
 metric is quoted on): 1024 x 1024 height field, 8 seeded Gaussian bumps,
 8 x 8 cell-aligned subdomains, free-boundary global conformal map, with the
-documented balanced pairwise-tree weld schedule: blocks -> pairs -> rows ->
-strips (the reference's greedy schedule raises WeldError on this layout;
-SURVEY §7; 6 weld levels instead of 10 for the rows-as-chains order).
+documented quadtree weld schedule: horizontal and vertical pairwise merges
+alternate (the reference's greedy schedule raises WeldError on this layout;
+SURVEY §7; generators.quadtree_schedule_order, golden qtree4x4).
 
 One step = the whole pipeline (partition, plan, flatten, weld, harmonic,
 stitch, metrics):
@@ -48,7 +48,7 @@ sys.path.insert(0, ROOT)
 METRIC = "mesh_vertices_per_sec"
 UNIT = "vertices/s"
 WORKLOAD = ("cfg2: 1024x1024 height field (8 Gaussian bumps, seed 0), 8x8 cell-aligned subdomains, "
-            "free-boundary global conformal map, pairwise-tree weld schedule (blocks->rows->strips)")
+            "free-boundary global conformal map, quadtree weld schedule (alternating pairwise merges)")
 
 
 def parse():
@@ -75,7 +75,7 @@ def dist_env():
 def workload(grid, blocks):
     from paper_1903_12359_b200 import generators as gen
     V, F, cuts = gen.height_field_case(grid, blocks, n_bumps=8, seed=0)
-    pairs = gen.pairwise_tree_schedule_order(blocks, blocks)
+    pairs = gen.quadtree_schedule_order(blocks, blocks)
     return V, F, cuts, pairs
 
 

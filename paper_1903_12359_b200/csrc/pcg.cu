@@ -30,6 +30,7 @@
 // using A p_new = A z + beta A p_old, so only z is ever gathered.
 #include <cooperative_groups.h>
 #include <cub/device/device_radix_sort.cuh>
+#include <cuda_fp16.h>
 
 #include <algorithm>
 #include <cmath>
@@ -71,7 +72,7 @@ struct SolveSystem {
     int gmax = 8;
     DevBuf<int32_t> cell, aggr, aoff;
     DevBuf<float2> pxy_row;
-    DevBuf<float4> wr;
+    DevBuf<uint2> wr;
     DevBuf<int64_t> nu_d, abase, eoff;
     DevBuf<double2> einv, p;
     DevBuf<float2> einv32;
@@ -397,6 +398,21 @@ constexpr int NC_MAX = 3 * AGG_MAX;       // coarse dofs per slot
 constexpr int ITEMS_MAX = AGG_MAX;        // (aggregate, part) work items per CTA
 constexpr int COARSE_BYTES = 3 * NC_MAX * 16 + ITEMS_MAX * 6 * 8;
 
+// coarse weights of a row, (w0, w1, w2) as fp16 in 8 bytes: any fixed basis
+// serves, and E is assembled from the same rounded values
+__device__ __forceinline__ uint2 cw_make(double a, double b, double c) {
+    __half2 h0 = __floats2half2_rn((float)a, (float)b);
+    __half2 h1 = __floats2half2_rn((float)c, 0.0f);
+    return make_uint2(*reinterpret_cast<unsigned int*>(&h0), *reinterpret_cast<unsigned int*>(&h1));
+}
+__device__ __forceinline__ float4 cw_get(const uint2* __restrict__ w, int64_t r) {
+    uint2 u = w[r];
+    __half2 h0 = *reinterpret_cast<__half2*>(&u.x);
+    __half2 h1 = *reinterpret_cast<__half2*>(&u.y);
+    float2 a = __half22float2(h0), b = __half22float2(h1);
+    return make_float4(a.x, a.y, b.x, 0.0f);
+}
+
 __host__ __device__ inline int coarse_G(int64_t nu, int gmax) {
     int g = (int)sqrt((double)nu / 128.0);
     return g < 1 ? 1 : (g > gmax ? gmax : g);
@@ -670,7 +686,7 @@ __global__ void k_slot_abase(int32_t nslot, const int64_t* __restrict__ sl_off, 
 __global__ void k_agg_weights(int32_t nagg_total, const int32_t* __restrict__ aoff, int32_t nslot,
                               const int64_t* __restrict__ sl_off, const int64_t* __restrict__ nu_slot,
                               const float2* __restrict__ pxy_row, const double* __restrict__ Dsq,
-                              float4* __restrict__ wr) {
+                              uint2* __restrict__ wr) {
     __shared__ double red[3][32];
     __shared__ double s_c[3];
     const int A = blockIdx.x;
@@ -726,9 +742,9 @@ __global__ void k_agg_weights(int32_t nagg_total, const int32_t* __restrict__ ao
         if (r < rend) {
             float2 p = pxy_row[r];
             double d = Dsq[r];
-            wr[r] = make_float4((float)d, (float)(d * (p.x - cx) * sc), (float)(d * (p.y - cy) * sc), 0.0f);
+            wr[r] = cw_make(d, d * (p.x - cx) * sc, d * (p.y - cy) * sc);
         } else {
-            wr[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+            wr[r] = make_uint2(0u, 0u);
         }
     }
 }
@@ -747,7 +763,7 @@ __global__ void __launch_bounds__(32 * E_WARPS) k_coarse_E(
         int32_t nslot, const int64_t* __restrict__ sl_off, const int64_t* __restrict__ sl_ptr,
         const uint32_t* __restrict__ sl_mask, const int32_t* __restrict__ col, const double* __restrict__ val,
         const int2* __restrict__ cpl, const double2* __restrict__ cplc, const int32_t* __restrict__ aoff,
-        const int32_t* __restrict__ aggr, const int64_t* __restrict__ abase, const float4* __restrict__ wr,
+        const int32_t* __restrict__ aggr, const int64_t* __restrict__ abase, const uint2* __restrict__ wr,
         const int64_t* __restrict__ eoff, double2* __restrict__ E, int* __restrict__ overflow) {
     __shared__ int s_flag[AGG_MAX];
     __shared__ int s_nb[AGG_MAX];
@@ -804,7 +820,7 @@ __global__ void __launch_bounds__(32 * E_WARPS) k_coarse_E(
         int2 nb = make_int2(-1, -1);
         double2 cc = make_double2(0.0, 0.0);
         if (have) {
-            wi = wr[r];
+            wi = cw_get(wr, r);
             const int64_t s = r >> 5;
             ln = (int)(r & 31);
             e0 = sl_ptr[s];
@@ -829,7 +845,7 @@ __global__ void __launch_bounds__(32 * E_WARPS) k_coarse_E(
                     const int64_t q = sell_pos(e0, k, ln);
                     const int64_t rc = rbase + col[q];
                     if (aggr[rc] == b) {
-                        const float4 wc = wr[rc];
+                        const float4 wc = cw_get(wr, rc);
                         const double v = val[q];
                         yr[0] += v * wc.x;
                         yr[1] += v * wc.y;
@@ -838,13 +854,13 @@ __global__ void __launch_bounds__(32 * E_WARPS) k_coarse_E(
                 }
                 if (cp) {
                     if (nb.x >= 0 && aggr[rbase + nb.x] == b) {
-                        const float4 wc = wr[rbase + nb.x];
+                        const float4 wc = cw_get(wr, rbase + nb.x);
                         yi[0] += cc.x * wc.x;
                         yi[1] += cc.x * wc.y;
                         yi[2] += cc.x * wc.z;
                     }
                     if (nb.y >= 0 && aggr[rbase + nb.y] == b) {
-                        const float4 wc = wr[rbase + nb.y];
+                        const float4 wc = cw_get(wr, rbase + nb.y);
                         yi[0] -= cc.y * wc.x;
                         yi[1] -= cc.y * wc.y;
                         yi[2] -= cc.y * wc.z;
@@ -993,7 +1009,7 @@ __global__ void k_hermitize(const int64_t* __restrict__ abase, const int64_t* __
 struct CoarseArgs {
     const int64_t* abase;    // slot -> first aggregate (global id), nslot + 1
     const int32_t* aoff;     // aggregate -> first row (global padded row), NA + 1
-    const float4* wr;        // row -> scaled coarse weights (w0, w1, w2, 0)
+    const uint2* wr;         // row -> scaled coarse weights (w0, w1, w2) as fp16
     const float2* einv32;    // per slot E^-1, row-major, rows padded to a multiple of 8 columns
     const int64_t* eoff32;   // slot -> offset into einv32
     double2* p;              // search direction (rows)
@@ -1394,7 +1410,7 @@ __global__ void __launch_bounds__(NT, 1) k_pcg2(PcgArgs A) {
     const float2* Einv = A.C.einv32 + A.C.eoff32[slot];
     const int crow0 = 3 * (a_lo - a0);  // my first coarse row
     double2* pg = A.C.p;
-    const float4* wr = A.C.wr;
+    const uint2* wr = A.C.wr;
 
     auto item_range = [&](int t, int& a_rel, int64_t& rb, int64_t& re) {
         a_rel = t / npart;
@@ -1418,7 +1434,7 @@ __global__ void __launch_bounds__(NT, 1) k_pcg2(PcgArgs A) {
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     const int64_t r = rq + 32 * u;
-                    w[u] = r < re ? wr[r] : make_float4(0.f, 0.f, 0.f, 0.f);
+                    w[u] = r < re ? cw_get(wr, r) : make_float4(0.f, 0.f, 0.f, 0.f);
                 }
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
@@ -1513,7 +1529,7 @@ __global__ void __launch_bounds__(NT, 1) k_pcg2(PcgArgs A) {
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     const int64_t r = rq + 32 * u;
-                    w[u] = r < re ? wr[r] : make_float4(0.f, 0.f, 0.f, 0.f);
+                    w[u] = r < re ? cw_get(wr, r) : make_float4(0.f, 0.f, 0.f, 0.f);
                 }
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
@@ -2374,8 +2390,8 @@ int run_solve(pgcp_batch* b, SolveSystem* S, const pgcp_solve_opts* o, double* z
         // compulsory bytes per iteration of slot j: stored off-diagonal
         // values + cols (12 B per slice entry) and the y update (read +
         // write, 32 B per unknown row); CG vectors stay on chip. Two-level
-        // (k_pcg2) adds p read + write (32 B/row), the coarse weights read
-        // twice (2 x 16 B/row) and the float E^-1 (8 nc ncp B per slot).
+        // (k_pcg2) adds p read + write (32 B/row), the fp16 coarse weights
+        // read twice (2 x 8 B/row) and the float E^-1 (8 nc ncp B per slot).
         S->iters_sum = S->iters_max = S->bytes_iter_weighted = 0;
         for (int j = 0; j < nslot; ++j) {
             int64_t e = hptr[S->h_sl_off[j + 1]] - hptr[S->h_sl_off[j]];
@@ -2384,7 +2400,7 @@ int run_solve(pgcp_batch* b, SolveSystem* S, const pgcp_solve_opts* o, double* z
             if (S->coarse) {
                 double nc = 3.0 * (double)(S->h_abase[j + 1] - S->h_abase[j]);
                 double ncp = (double)(((int64_t)nc + 7) & ~7ll);
-                bytes += 64.0 * rows + 8.0 * nc * ncp;
+                bytes += 48.0 * rows + 8.0 * nc * ncp;
             }
             S->iters_sum += hit[j];
             S->iters_max = std::max<double>(S->iters_max, hit[j]);

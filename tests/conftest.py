@@ -10,7 +10,7 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 PIPELINE_CASES = ["cfg1", "strips4", "blocks3x3", "disk2x2", "k1free", "k1disk", "flat2x2",
-                  "sphere2", "sphere4", "tree4x4", "ptree4x4"]
+                  "sphere2", "sphere4", "tree4x4", "ptree4x4", "qtree4x4"]
 
 
 def case_pairs(case):
@@ -20,6 +20,8 @@ def case_pairs(case):
         return gen.row_tree_schedule_order(4, 4)
     if case == "ptree4x4":
         return gen.pairwise_tree_schedule_order(4, 4)
+    if case == "qtree4x4":
+        return gen.quadtree_schedule_order(4, 4)
     return None
 
 

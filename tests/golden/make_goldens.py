@@ -331,14 +331,21 @@ def _cases():
                       schedule_pairs=gen.row_tree_schedule_order(4, 4))
 
     def c_ptree4x4():
-        # fully pairwise tree (blocks -> pairs -> rows -> strips), the bench's order
+        # fully pairwise tree (blocks -> pairs -> rows -> strips)
         V, F, cuts = gen.height_field_case(41, 4, seed=2)
         pipeline_case("ptree4x4", V, F, cuts, "free",
                       schedule_pairs=gen.pairwise_tree_schedule_order(4, 4))
 
+    def c_qtree4x4():
+        # quadtree order (alternating horizontal / vertical pairwise merges), the bench's order
+        V, F, cuts = gen.height_field_case(41, 4, seed=2)
+        pipeline_case("qtree4x4", V, F, cuts, "free",
+                      schedule_pairs=gen.quadtree_schedule_order(4, 4))
+
     return {"known_answers": known_answers, "weld_corpus": weld_corpus, "cfg1": c_cfg1, "strips4": c_strips4,
             "blocks3x3": c_blocks3x3, "disk2x2": c_disk2x2, "k1": c_k1, "flat2x2": c_flat2x2,
-            "sphere": c_sphere, "tree4x4": c_tree4x4, "ptree4x4": c_ptree4x4}
+            "sphere": c_sphere, "tree4x4": c_tree4x4, "ptree4x4": c_ptree4x4,
+            "qtree4x4": c_qtree4x4}
 
 
 def main():

@@ -13,7 +13,7 @@ from conftest import case_pairs, load_golden, unpack
 pytestmark = pytest.mark.gpu
 
 CASES = ["cfg1", "strips4", "blocks3x3", "disk2x2", "k1free", "k1disk", "flat2x2", "sphere2", "sphere4",
-         "tree4x4", "ptree4x4"]
+         "tree4x4", "ptree4x4", "qtree4x4"]
 
 
 def _diam(z):
@@ -25,7 +25,7 @@ def _diam(z):
     return 2 * np.max(np.abs(zz - c))
 
 
-@pytest.mark.parametrize("case", ["cfg1", "blocks3x3", "sphere4", "disk2x2", "tree4x4", "ptree4x4"])
+@pytest.mark.parametrize("case", ["cfg1", "blocks3x3", "sphere4", "disk2x2", "tree4x4", "ptree4x4", "qtree4x4"])
 def test_welds_match_reference(cuda, case):
     from paper_1903_12359_b200 import closed_weld, partial_weld
     z = load_golden(case)

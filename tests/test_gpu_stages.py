@@ -9,7 +9,7 @@ from conftest import load_golden, unpack, unpack_csr
 
 pytestmark = pytest.mark.gpu
 
-CUT_CASES = ["cfg1", "strips4", "blocks3x3", "disk2x2", "flat2x2", "sphere2", "sphere4", "tree4x4", "ptree4x4"]
+CUT_CASES = ["cfg1", "strips4", "blocks3x3", "disk2x2", "flat2x2", "sphere2", "sphere4", "tree4x4", "ptree4x4", "qtree4x4"]
 ALL_CASES = CUT_CASES + ["k1free", "k1disk"]
 
 

@@ -55,7 +55,7 @@ def _part(case):
 
 
 @pytest.mark.parametrize("case", ["cfg1", "strips4", "blocks3x3", "disk2x2", "flat2x2",
-                                  "sphere2", "sphere4", "tree4x4", "ptree4x4"])
+                                  "sphere2", "sphere4", "tree4x4", "ptree4x4", "qtree4x4"])
 def test_native_planner_matches_reference(case):
     from paper_1903_12359_b200.partition import plan_weld_schedule
     z, p = _part(case)

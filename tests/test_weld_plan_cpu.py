@@ -63,7 +63,7 @@ class _P:
 
 
 @pytest.mark.parametrize("case", ["cfg1", "strips4", "blocks3x3", "disk2x2", "flat2x2", "sphere2", "sphere4",
-                                  "tree4x4", "ptree4x4"])
+                                  "tree4x4", "ptree4x4", "qtree4x4"])
 def test_native_weld_plan_matches_numpy(case):
     from paper_1903_12359_b200.partition import plan_weld_schedule
     from paper_1903_12359_b200.pipeline import WeldPlan

@@ -12,7 +12,7 @@ from paper_1903_12359_b200 import generators as gen
 grid = int(os.environ.get("GRID", "1024"))
 blocks = int(os.environ.get("BLOCKS", "8"))
 V, F, cuts = gen.height_field_case(grid, blocks)
-pairs = gen.pairwise_tree_schedule_order(blocks, blocks)
+pairs = gen.quadtree_schedule_order(blocks, blocks)
 t0 = time.perf_counter()
 ref = oracle.run_parameterize(V, F, cuts, "free", workers=os.cpu_count() or 1, schedule="pairs", pairs=pairs)
 print(f"oracle {time.perf_counter() - t0:.1f} s", flush=True)

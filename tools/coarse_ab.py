@@ -10,7 +10,7 @@ from paper_1903_12359_b200 import generators as gen
 grid = int(os.environ.get("GRID", "1024"))
 blocks = int(os.environ.get("BLOCKS", "8"))
 V, F, cuts = gen.height_field_case(grid, blocks)
-pairs = gen.pairwise_tree_schedule_order(blocks, blocks)
+pairs = gen.quadtree_schedule_order(blocks, blocks)
 mesh = pg.TriMesh(V, F)
 res = {}
 for mode in ["0", "1", "0", "1"]:

@@ -7,7 +7,7 @@ import paper_1903_12359_b200 as pg
 from paper_1903_12359_b200 import generators as gen
 
 V, F, cuts = gen.height_field_case(1024, 8)
-pairs = gen.pairwise_tree_schedule_order(8, 8)
+pairs = gen.quadtree_schedule_order(8, 8)
 mesh = pg.TriMesh(V, F)
 pg.parameterize(mesh, cuts, "free", pairs=pairs, keep_device=True)
 

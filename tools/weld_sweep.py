@@ -8,7 +8,7 @@ import paper_1903_12359_b200 as pg
 from paper_1903_12359_b200 import generators as gen
 
 V, F, cuts = gen.height_field_case(1024, 8)
-pairs = gen.pairwise_tree_schedule_order(8, 8)
+pairs = gen.quadtree_schedule_order(8, 8)
 mesh = pg.TriMesh(V, F)
 ref = None
 for nt, ppt in [(256, 1), (256, 2), (512, 1), (512, 2), (512, 4), (512, 8), (256, 4), (256, 16)]:
