@@ -33,6 +33,7 @@
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -2350,6 +2351,11 @@ int run_solve(pgcp_batch* b, SolveSystem* S, const pgcp_solve_opts* o, double* z
     PGCP_TRY(launch_pcg(S, A, csize, s));
     count_launch();
     PGCP_TRY_CUDA(cudaEventRecord(e1, s));
+    auto t_post = std::chrono::steady_clock::now();
+    if (want_timing) {
+        cudaEventSynchronize(e1);
+        t_post = std::chrono::steady_clock::now();
+    }
     k_true_residual<<<nslot, 512, 0, s>>>(A);
     PGCP_LAUNCH_CHECK();
     k_scatter<<<grid_for(S->ne, 256), 256, 0, s>>>(S->ne, nslot, S->d_comps.p, S->sv_off.p, b->vert_off.p, S->urow.p,
@@ -2367,6 +2373,9 @@ int run_solve(pgcp_batch* b, SolveSystem* S, const pgcp_solve_opts* o, double* z
     PGCP_TRY_CUDA(cudaMemcpyAsync(hit.data(), S->iters.p, nslot * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     PGCP_TRY_CUDA(cudaMemcpyAsync(hres.data(), S->res.p, 8 * nslot * sizeof(double), cudaMemcpyDeviceToHost, s));
     PGCP_TRY_CUDA(cudaStreamSynchronize(s));
+    if (want_timing)
+        fprintf(stderr, "[pcg timing] post-solve (true residual, scatter, checks, stats) %.2f ms\n",
+                1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - t_post).count());
     if (want_timing) {
         std::vector<long long> ht(8 * (size_t)nslot * csize);
         PGCP_TRY_CUDA(cudaMemcpy(ht.data(), tbuf.p, ht.size() * sizeof(long long), cudaMemcpyDeviceToHost));
@@ -2542,7 +2551,13 @@ int solve_flatten(pgcp_batch* b, const int32_t* comps, int32_t ncomp, const int3
     }
     PGCP_TRY_CUDA(cudaMemcpyAsync(dp.p, hp.data(), hp.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
     b->last_flat_pins = hp;
+    auto t0 = std::chrono::steady_clock::now();
     PGCP_TRY(build_system(b, S, true, dp.p, t, nullptr, nullptr, 0, s));
+    if (getenv("PGCP_PCG_TIMING")) {
+        cudaStreamSynchronize(s);
+        fprintf(stderr, "[pcg timing] flatten build_system %.2f ms (host, synchronised)\n",
+                1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+    }
     return run_solve(b, S, o, z, st, s);
 }
 
@@ -2555,7 +2570,13 @@ int solve_harmonic(pgcp_batch* b, const int32_t* comps, int32_t ncomp, const int
     SolveSystem* S = slot;
     PGCP_TRY(prepare_slots(b, S, comps, ncomp));
     if (S->nslot == 0) return PGCP_OK;
+    auto t0 = std::chrono::steady_clock::now();
     PGCP_TRY(build_system(b, S, false, nullptr, nullptr, fixed_gid, fixed_val, nfixed, s));
+    if (getenv("PGCP_PCG_TIMING")) {
+        cudaStreamSynchronize(s);
+        fprintf(stderr, "[pcg timing] harmonic build_system %.2f ms (host, synchronised)\n",
+                1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+    }
     return run_solve(b, S, o, z, st, s);
 }
 
