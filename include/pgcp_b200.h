@@ -161,9 +161,11 @@ PGCP_API int pgcp_batch_harmonic(pgcp_batch* b, const int32_t* comps, int32_t nc
 
 /* Summary of the last flatten (0) / harmonic (1) solve: out[0] PCG kernel
  * time in ms (CUDA events on the launch stream), [1] total iterations,
- * [2] max iterations, [3] sum over submeshes of iterations x compulsory bytes
- * per iteration (12 B per stored off-diagonal entry + 32 B per row), [4]
- * stored entries, [5] unknown rows, [6] CTAs per cluster, [7] submeshes. */
+ * [2] max iterations, [3] sum over submeshes of iterations x the device
+ * kernel's bytes per iteration, [4] stored entries, [5]
+ * unknown rows, [6] CTAs per cluster, [7] submeshes, [8] sum over
+ * submeshes of iterations x SURVEY §8(d)'s 12 z + 4 (r + 1) for the
+ * reference's CSR system (C_ff / L_II), [9] coarse-space setup ms. */
 PGCP_API int pgcp_batch_last_solve(const pgcp_batch* b, int which, double* out, int nout);
 
 /* Exported solver systems for pattern parity (flatten.py:160-166 C_ff and

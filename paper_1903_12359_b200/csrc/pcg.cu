@@ -56,6 +56,7 @@ struct SolveSystem {
     // last run: PCG kernel time (CUDA events on the launch stream), iteration
     // totals and the compulsory bytes of one iteration
     double kernel_ms = 0, iters_sum = 0, iters_max = 0, bytes_iter_weighted = 0, nnz_off = 0, nrows_u = 0;
+    double ref_bytes_weighted = 0;   // sum_j iters_j (12 z_j + 4 (r_j + 1)), reference CSR system
     DevBuf<int32_t> d_comps, slot_of_comp;
     DevBuf<int64_t> sl_off, sv_off, sl_ptr;
     DevBuf<uint32_t> sl_mask;
@@ -738,7 +739,9 @@ __global__ void k_agg_weights(int32_t nagg_total, const int32_t* __restrict__ ao
         s_c[2] = t;
     }
     __syncthreads();
-    const double sc = s_c[2] > 0 ? 1.0 / s_c[2] : 0.0;
+    // linear functions only on aggregates with enough rows to carry them
+    // (slivers cut off by a CTA boundary keep just the constant)
+    const double sc = (s_c[2] > 0 && rend - r0 >= 16) ? 1.0 / s_c[2] : 0.0;
     for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
         if (r < rend) {
             float2 p = pxy_row[r];
@@ -921,16 +924,11 @@ __global__ void __launch_bounds__(INV_THREADS, 1) k_coarse_inv(const int64_t* __
     double2* Ml = reinterpret_cast<double2*>(smem);    // [rpc][n] my rows
     double2* rowk = Ml + (size_t)rpc * n;              // [2][n] pivot row (broadcast)
     double2* colk = rowk + 2 * n;                      // [rpc]  my entries of the pivot column
-    double* s_misc = reinterpret_cast<double*>(colk + rpc);  // [0] dref
+    double* s_diag = reinterpret_cast<double*>(colk + rpc);  // [n] original diagonal
     double2* M = E + eoff[j];
     for (int t = threadIdx.x; t < nr * n; t += INV_THREADS) Ml[t] = M[(int64_t)i0 * n + t];
-    if (threadIdx.x == 0) {
-        double d = 0.0;
-        for (int i = 0; i < n; ++i) d = fmax(d, M[(int64_t)i * n + i].x);
-        s_misc[0] = d;
-    }
+    for (int i = threadIdx.x; i < n; i += INV_THREADS) s_diag[i] = M[(int64_t)i * n + i].x;
     __syncthreads();
-    const double tol = 1e-10 * s_misc[0];
     // pivot row 0 -> everyone
     int par = 0;
     auto publish = [&](int k, int pr) {
@@ -946,8 +944,10 @@ __global__ void __launch_bounds__(INV_THREADS, 1) k_coarse_inv(const int64_t* __
     cl.sync();
     for (int k = 0; k < n; ++k) {
         const double2* rk = rowk + par * n;
+        // a pivot that lost all but 1e-8 of its original diagonal means the
+        // coarse function is (numerically) dependent on the previous ones
         const double p = rk[k].x;
-        const bool drop = !(p > tol);
+        const bool drop = !(p > 1e-8 * s_diag[k]) || !(s_diag[k] > 0.0);
         for (int i = threadIdx.x; i < nr; i += INV_THREADS) colk[i] = Ml[(size_t)i * n + k];
         __syncthreads();
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1716,6 +1716,53 @@ __global__ void __launch_bounds__(NT, 1) k_pcg2(PcgArgs A) {
     }
 }
 
+// nnz of the reference's CSR system of every slot (SURVEY §8(d) bytes model).
+// DNCP C_ff (flatten.py:160-166): 2 x (diagonal + nonzero off-diagonals of
+// L_UU), plus, for a boundary row, one entry in the x-row and one in the
+// y-row per unknown loop neighbour (the -2M blocks); exact zeros are dropped
+// as scipy's csr_binop does. L_II (assemble.py:40): diagonal + every stored
+// off-diagonal (explicit zeros kept). Padding entries point to their own row
+// and are skipped.
+__global__ void k_ref_nnz(const int64_t* __restrict__ sl_off, const int64_t* __restrict__ sl_ptr,
+                          const int32_t* __restrict__ col, const double* __restrict__ val,
+                          const uint32_t* __restrict__ sl_mask, const int2* __restrict__ cpl,
+                          const int64_t* __restrict__ nu, int dncp, long long* __restrict__ out) {
+    __shared__ long long red[32];
+    const int j = blockIdx.x;
+    const int64_t rbase = 32 * sl_off[j];
+    long long cnt = 0;
+    for (int64_t r = rbase + threadIdx.x; r < rbase + nu[j]; r += blockDim.x) {
+        const int64_t s = r >> 5;
+        const int lane = (int)(r & 31);
+        const int64_t e0 = sl_ptr[s];
+        const int w = (int)((sl_ptr[s + 1] - e0) >> 5);
+        const int self = (int)(r - rbase);
+        long long c = 1;  // diagonal
+        for (int k = 0; k < w; ++k) {
+            const int64_t q = sell_pos(e0, k, lane);
+            if (col[q] == self) continue;
+            if (dncp && val[q] == 0.0) continue;
+            ++c;
+        }
+        if (dncp) {
+            c *= 2;
+            if (sl_mask[s] & (1u << lane)) {
+                const int2 nb = cpl[r];
+                c += 2 * ((nb.x >= 0) + (nb.y >= 0));
+            }
+        }
+        cnt += c;
+    }
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long t = 0;
+        for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += red[q];
+        out[j] = t;
+    }
+}
+
 // true residual of the unscaled system from the scaled arrays:
 //   ||b - H x||^2 = sum D |b^ - H^ y|^2, ||x||^2 = sum |y|^2 / D, ||b||^2 = sum D |b^|^2
 __global__ void k_true_residual(PcgArgs A) {
@@ -2083,7 +2130,7 @@ int build_coarse(SolveSystem* S, int csize, cudaStream_t s) {
         int CS = 1;
         auto inv_smem = [&](int cs) {
             int rpc = (nmax + cs - 1) / cs;
-            return (size_t)rpc * nmax * 16 + (size_t)2 * nmax * 16 + (size_t)rpc * 16 + 64;
+            return (size_t)rpc * nmax * 16 + (size_t)2 * nmax * 16 + (size_t)rpc * 16 + (size_t)nmax * 8 + 64;
         };
         while (CS < 16 && inv_smem(CS) > 200 * 1024) CS *= 2;
         const size_t smem = inv_smem(CS);
@@ -2366,6 +2413,20 @@ int run_solve(pgcp_batch* b, SolveSystem* S, const pgcp_solve_opts* o, double* z
                                             b->loop_off.p, b->loop.p, (const double2*)z, S->res.p);
         PGCP_LAUNCH_CHECK();
     }
+    DevBuf<long long> refnz;
+    PGCP_TRY(refnz.alloc(nslot, s));
+    {
+        DevBuf<int64_t> dnu;
+        std::vector<int64_t> hnu(S->h_nu.begin(), S->h_nu.end());
+        PGCP_TRY(dnu.alloc(nslot, s));
+        PGCP_TRY_CUDA(cudaMemcpyAsync(dnu.p, hnu.data(), nslot * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+        k_ref_nnz<<<nslot, 256, 0, s>>>(S->sl_off.p, S->sl_ptr.p, S->col.p, S->val.p, S->sl_mask.p, S->cpl.p, dnu.p,
+                                        S->dncp ? 1 : 0, refnz.p);
+        PGCP_LAUNCH_CHECK();
+        PGCP_TRY_CUDA(cudaStreamSynchronize(s));  // hnu is a local
+    }
+    std::vector<long long> hrefnz(nslot);
+    PGCP_TRY_CUDA(cudaMemcpyAsync(hrefnz.data(), refnz.p, nslot * sizeof(long long), cudaMemcpyDeviceToHost, s));
     std::vector<int32_t> hit(nslot);
     std::vector<double> hres(8 * nslot);
     std::vector<int64_t> hptr(S->nslices + 1);
@@ -2401,7 +2462,7 @@ int run_solve(pgcp_batch* b, SolveSystem* S, const pgcp_solve_opts* o, double* z
         // write, 32 B per unknown row); CG vectors stay on chip. Two-level
         // (k_pcg2) adds p read + write (32 B/row), the fp16 coarse weights
         // read twice (2 x 8 B/row) and the float E^-1 (8 nc ncp B per slot).
-        S->iters_sum = S->iters_max = S->bytes_iter_weighted = 0;
+        S->iters_sum = S->iters_max = S->bytes_iter_weighted = S->ref_bytes_weighted = 0;
         for (int j = 0; j < nslot; ++j) {
             int64_t e = hptr[S->h_sl_off[j + 1]] - hptr[S->h_sl_off[j]];
             double rows = (double)S->h_nu[j];
@@ -2414,6 +2475,8 @@ int run_solve(pgcp_batch* b, SolveSystem* S, const pgcp_solve_opts* o, double* z
             S->iters_sum += hit[j];
             S->iters_max = std::max<double>(S->iters_max, hit[j]);
             S->bytes_iter_weighted += bytes * hit[j];
+            const double rref = S->dncp ? 2.0 * rows : rows;
+            S->ref_bytes_weighted += (12.0 * (double)hrefnz[j] + 4.0 * (rref + 1.0)) * hit[j];
             S->nrows_u += rows;
             S->nnz_off += (double)e;
         }
@@ -2719,7 +2782,7 @@ int export_system(pgcp_batch* b, int which, int32_t comp, int64_t* dims, int32_t
 
 
 void solve_summary(const pgcp_batch* b, int which, double* out) {
-    for (int i = 0; i < 8; ++i) out[i] = 0;
+    for (int i = 0; i < 10; ++i) out[i] = 0;
     SolveSystem* S = static_cast<SolveSystem*>(b->sys[which]);
     if (!S) return;
     out[0] = S->kernel_ms;
@@ -2730,6 +2793,8 @@ void solve_summary(const pgcp_batch* b, int which, double* out) {
     out[5] = S->nrows_u;
     out[6] = S->csize;
     out[7] = S->nslot;
+    out[8] = S->ref_bytes_weighted;
+    out[9] = S->coarse_ms;
 }
 
 }  // namespace pgcp

@@ -226,10 +226,11 @@ class DeviceBatch:
     def last_solve(self, which):
         """PCG kernel time (CUDA events), iterations and compulsory bytes of
         the last flatten (0) / harmonic (1) solve."""
-        out = (ctypes.c_double * 8)()
-        nat.check(nat.lib().pgcp_batch_last_solve(self.h, which, out, 8))
+        out = (ctypes.c_double * 10)()
+        nat.check(nat.lib().pgcp_batch_last_solve(self.h, which, out, 10))
         return {"kernel_ms": out[0], "iters_sum": out[1], "iters_max": out[2], "bytes": out[3],
-                "stored_entries": out[4], "rows": out[5], "cluster": int(out[6]), "submeshes": int(out[7])}
+                "stored_entries": out[4], "rows": out[5], "cluster": int(out[6]), "submeshes": int(out[7]),
+                "ref_bytes": out[8], "coarse_ms": out[9]}
 
     def energy(self, z):
         out = (ctypes.c_double * self.K)()
