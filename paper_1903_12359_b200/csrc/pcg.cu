@@ -77,8 +77,10 @@ struct SolveSystem {
     DevBuf<uint2> wr;
     DevBuf<int64_t> nu_d, abase, eoff;
     DevBuf<double2> einv, p;
-    DevBuf<float2> einv32;
+    DevBuf<float2> einv32;        // Hermitian E^-1 copy read by k_pcg2 (fp32) ...
+    DevBuf<double2> einv64;       // ... or fp64 (PGCP_COARSE_FP64=1)
     DevBuf<int64_t> eoff32;
+    bool einv_fp64 = false;
     std::vector<int64_t> h_abase;
     double coarse_ms = 0;
 };
@@ -987,23 +989,37 @@ __global__ void __launch_bounds__(INV_THREADS, 1) k_coarse_inv(const int64_t* __
 
 // float copy of (E^-1 + E^-H) / 2: exactly Hermitian after rounding (the
 // preconditioner stays symmetric), rows padded to a multiple of 8 columns
+template <typename ET>
+__device__ __forceinline__ ET mk_et(double x, double y);
+template <>
+__device__ __forceinline__ float2 mk_et<float2>(double x, double y) { return make_float2((float)x, (float)y); }
+template <>
+__device__ __forceinline__ double2 mk_et<double2>(double x, double y) { return make_double2(x, y); }
+
+template <typename ET>
 __global__ void k_hermitize(const int64_t* __restrict__ abase, const int64_t* __restrict__ eoff,
                             const double2* __restrict__ E, const int64_t* __restrict__ eoff32,
-                            float2* __restrict__ E32) {
+                            ET* __restrict__ E32) {
     const int j = blockIdx.x;
     const int n = 3 * (int)(abase[j + 1] - abase[j]);
     const int np = (n + 7) & ~7;
     const double2* M = E + eoff[j];
-    float2* O = E32 + eoff32[j];
+    ET* O = E32 + eoff32[j];
     for (int64_t t = threadIdx.x; t < (int64_t)n * np; t += blockDim.x) {
         const int i = (int)(t / np), c = (int)(t % np);
         if (c >= n) {
-            O[t] = make_float2(0.f, 0.f);
+            O[t] = mk_et<ET>(0.0, 0.0);
             continue;
         }
+        // the upper triangle is the reference; the lower one is its exact
+        // conjugate after rounding
         const double2 a = M[(int64_t)i * n + c], b = M[(int64_t)c * n + i];
-        O[t] = (c < i) ? make_float2((float)(0.5 * (b.x + a.x)), -(float)(0.5 * (b.y - a.y)))
-                       : make_float2((float)(0.5 * (a.x + b.x)), (float)(0.5 * (a.y - b.y)));
+        if (c < i) {
+            const ET u = mk_et<ET>(0.5 * (b.x + a.x), 0.5 * (b.y - a.y));
+            O[t] = mk_et<ET>((double)u.x, -(double)u.y);
+        } else {
+            O[t] = mk_et<ET>(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));
+        }
     }
 }
 
@@ -1011,8 +1027,8 @@ struct CoarseArgs {
     const int64_t* abase;    // slot -> first aggregate (global id), nslot + 1
     const int32_t* aoff;     // aggregate -> first row (global padded row), NA + 1
     const uint2* wr;         // row -> scaled coarse weights (w0, w1, w2) as fp16
-    const float2* einv32;    // per slot E^-1, row-major, rows padded to a multiple of 8 columns
-    const int64_t* eoff32;   // slot -> offset into einv32
+    const void* einvh;       // per slot Hermitian E^-1 (float2 or double2), row-major, rows padded to 8 columns
+    const int64_t* eoff32;   // slot -> offset into einvh
     double2* p;              // search direction (rows)
 };
 
@@ -1342,7 +1358,7 @@ __global__ void __launch_bounds__(NT, 1) k_pcg(PcgArgs A) {
 //   A: q = A z + beta q; y += alpha p; p = z + beta p; <p,q>           [SYNC1]
 //   B: r -= alpha q; <r,r>; g = W^T r over my aggregates -> every CTA  [SYNC2]
 //   C: mu = E^-1 g on my aggregates; z = r + W^ mu; rho = <r,z>        [SYNC3]
-template <int NT>
+template <int NT, typename ET>
 __global__ void __launch_bounds__(NT, 1) k_pcg2(PcgArgs A) {
     constexpr int NW = NT / 32;
     extern __shared__ __align__(16) unsigned char smem[];
@@ -1408,7 +1424,7 @@ __global__ void __launch_bounds__(NT, 1) k_pcg2(PcgArgs A) {
     const int npart = max(1, NW / max(naggs, 1));
     const int nitems = naggs * npart;
     const int ncp = (nc + 7) & ~7;  // padded row stride of the float copy
-    const float2* Einv = A.C.einv32 + A.C.eoff32[slot];
+    const ET* Einv = reinterpret_cast<const ET*>(A.C.einvh) + A.C.eoff32[slot];
     const int crow0 = 3 * (a_lo - a0);  // my first coarse row
     double2* pg = A.C.p;
     const uint2* wr = A.C.wr;
@@ -1495,16 +1511,16 @@ __global__ void __launch_bounds__(NT, 1) k_pcg2(PcgArgs A) {
     auto prolong_z = [&](int par) -> double {
         const double2* g = gbuf + par * NC_MAX;
         for (int q = warp; q < 3 * naggs; q += NW) {
-            const float2* er = Einv + (int64_t)(crow0 + q) * ncp;
+            const ET* er = Einv + (int64_t)(crow0 + q) * ncp;
             double mx = 0.0, my = 0.0;
-            float2 e[NC_MAX / 32];
+            ET e[(NC_MAX + 31) / 32];
 #pragma unroll
-            for (int u = 0; u < NC_MAX / 32; ++u) {  // lane-strided columns: coalesced, conflict-free
+            for (int u = 0; u < (NC_MAX + 31) / 32; ++u) {  // lane-strided columns: coalesced, conflict-free
                 const int c = lane + 32 * u;
-                e[u] = c < nc ? er[c] : make_float2(0.f, 0.f);
+                e[u] = c < nc ? er[c] : mk_et<ET>(0.0, 0.0);
             }
 #pragma unroll
-            for (int u = 0; u < NC_MAX / 32; ++u) {
+            for (int u = 0; u < (NC_MAX + 31) / 32; ++u) {
                 const int c = lane + 32 * u;
                 if (c < nc) {
                     const double2 gg = g[c];
@@ -1955,9 +1971,9 @@ int launch_pcg_t(SolveSystem* S, const PcgArgs& args, int csize, size_t smem, cu
     return PGCP_OK;
 }
 
-template <int NT>
+template <int NT, typename ET>
 int launch_pcg2_t(SolveSystem* S, const PcgArgs& args, int csize, size_t smem, cudaStream_t s) {
-    auto kern = k_pcg2<NT>;
+    auto kern = k_pcg2<NT, ET>;
     PGCP_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (csize > 8) PGCP_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cudaLaunchConfig_t cfg = {};
@@ -1992,7 +2008,9 @@ int launch_pcg(SolveSystem* S, const PcgArgs& args, int csize, cudaStream_t s) {
         set_error("pcg: shared memory %zu exceeds limit", smem);
         return PGCP_E_INVALID;
     }
-    if (S->coarse) return launch_pcg2_t<512>(S, args, csize, smem, s);
+    if (S->coarse)
+        return S->einv_fp64 ? launch_pcg2_t<512, double2>(S, args, csize, smem, s)
+                            : launch_pcg2_t<512, float2>(S, args, csize, smem, s);
     const char* v = getenv("PGCP_PCG_VARIANT");
     int variant = v ? atoi(v) : 0;
     switch (variant) {
@@ -2124,6 +2142,27 @@ int build_coarse(SolveSystem* S, int csize, cudaStream_t s) {
                                                     S->val.p, S->cpl.p, S->cplc.p, S->aoff.p, S->aggr.p,
                                                     S->abase.p, S->wr.p, S->eoff.p, S->einv.p, ovf.p);
     PGCP_LAUNCH_CHECK();
+    if (const char* dump = getenv("PGCP_COARSE_DUMP")) {  // debugging aid: E of every slot before inversion
+        std::vector<double2> hE(heoff[nslot]);
+        std::vector<int32_t> haoff(NA + 1);
+        std::vector<uint2> hwr(S->rows);
+        PGCP_TRY_CUDA(cudaMemcpyAsync(hE.data(), S->einv.p, hE.size() * sizeof(double2), cudaMemcpyDeviceToHost, s));
+        PGCP_TRY_CUDA(cudaMemcpyAsync(haoff.data(), S->aoff.p, haoff.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        PGCP_TRY_CUDA(cudaMemcpyAsync(hwr.data(), S->wr.p, hwr.size() * sizeof(uint2), cudaMemcpyDeviceToHost, s));
+        PGCP_TRY_CUDA(cudaStreamSynchronize(s));
+        FILE* f = fopen(dump, "wb");
+        if (f) {
+            int64_t hdr[4] = {nslot, NA, S->rows, heoff[nslot]};
+            fwrite(hdr, sizeof(hdr), 1, f);
+            fwrite(S->h_abase.data(), sizeof(int64_t), nslot + 1, f);
+            fwrite(heoff.data(), sizeof(int64_t), nslot + 1, f);
+            fwrite(S->h_sl_off.data(), sizeof(int64_t), nslot + 1, f);
+            fwrite(haoff.data(), sizeof(int32_t), haoff.size(), f);
+            fwrite(hwr.data(), sizeof(uint2), hwr.size(), f);
+            fwrite(hE.data(), sizeof(double2), hE.size(), f);
+            fclose(f);
+        }
+    }
     {
         int nmax = 0;
         for (int j = 0; j < nslot; ++j) nmax = std::max<int>(nmax, 3 * (int)(S->h_abase[j + 1] - S->h_abase[j]));
@@ -2157,8 +2196,15 @@ int build_coarse(SolveSystem* S, int csize, cudaStream_t s) {
         }
         PGCP_TRY(S->eoff32.alloc(nslot + 1, s));
         PGCP_TRY_CUDA(cudaMemcpyAsync(S->eoff32.p, he32.data(), (nslot + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
-        PGCP_TRY(S->einv32.alloc(std::max<int64_t>(he32[nslot], 1), s));
-        k_hermitize<<<nslot, 512, 0, s>>>(S->abase.p, S->eoff.p, S->einv.p, S->eoff32.p, S->einv32.p);
+        const char* ef = getenv("PGCP_COARSE_FP64");
+        S->einv_fp64 = ef && atoi(ef) != 0;
+        if (S->einv_fp64) {
+            PGCP_TRY(S->einv64.alloc(std::max<int64_t>(he32[nslot], 1), s));
+            k_hermitize<double2><<<nslot, 512, 0, s>>>(S->abase.p, S->eoff.p, S->einv.p, S->eoff32.p, S->einv64.p);
+        } else {
+            PGCP_TRY(S->einv32.alloc(std::max<int64_t>(he32[nslot], 1), s));
+            k_hermitize<float2><<<nslot, 512, 0, s>>>(S->abase.p, S->eoff.p, S->einv.p, S->eoff32.p, S->einv32.p);
+        }
         PGCP_LAUNCH_CHECK();
         PGCP_TRY_CUDA(cudaStreamSynchronize(s));  // he32 is a local
     }
@@ -2380,7 +2426,7 @@ int run_solve(pgcp_batch* b, SolveSystem* S, const pgcp_solve_opts* o, double* z
     A.C.abase = S->abase.p;
     A.C.aoff = S->aoff.p;
     A.C.wr = S->wr.p;
-    A.C.einv32 = S->einv32.p;
+    A.C.einvh = S->einv_fp64 ? (const void*)S->einv64.p : (const void*)S->einv32.p;
     A.C.eoff32 = S->eoff32.p;
     A.C.p = S->p.p;
     DevBuf<long long> tbuf;

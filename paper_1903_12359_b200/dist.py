@@ -131,7 +131,7 @@ def bench_distributed(args, V, F, cuts, pairs, metric, unit, workload):
         if sampler:
             sampler.start()
         l0 = lib.pgcp_launch_count()
-        ms_steps, pcg_ms, pcg_bytes = [], [], []
+        ms_steps, pcg_ms, pcg_bytes = [], [], []  # pcg_bytes: SURVEY 8(d) algorithmic bytes
         for _ in range(args.steps):
             flush.zero_()
             dist.barrier()
@@ -145,7 +145,7 @@ def bench_distributed(args, V, F, cuts, pairs, metric, unit, workload):
             ms_steps.append(_max_over_ranks(e0.elapsed_time(e1), dev))
             fl = rep.solver["flatten"]
             pcg_ms.append(fl["kernel_ms"])
-            pcg_bytes.append(fl["bytes"])
+            pcg_bytes.append(fl["ref_bytes"])
         dist.barrier()
         torch.cuda.synchronize()
         launches = _sum_over_ranks(lib.pgcp_launch_count() - l0, dev)
@@ -181,7 +181,7 @@ def bench_distributed(args, V, F, cuts, pairs, metric, unit, workload):
         bytes_all = _sum_over_ranks(statistics.mean(pcg_bytes), dev)
         if rank == 0:
             achieved = bytes_all / world / (kernel_ms / 1e3) / 1e9
-            roof = {"bound": "hbm", "kernel": f"k_pcg (flatten, rank-local shard of 64 subdomains)",
+            roof = {"bound": "hbm", "kernel": "k_pcg2 (flatten, rank-local shard of the 64 subdomains)",
                     "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                     "traffic": B.ncu_traffic(), "peak_source": peak_src, "kernel_ms": kernel_ms,
                     "note": "per-GPU average of the flatten launch's algorithmic bytes over the slowest "
