@@ -221,7 +221,7 @@ def main():
     import paper_1903_12359_b200 as pg
     from paper_1903_12359_b200 import _native as nat
 
-    if world > 1:
+    if world > 1 or os.environ.get("PGCP_BENCH_DIST") == "1":  # the latter: exercise the NCCL path on 1 GPU
         return run_distributed(args, V, F, cuts, pairs)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
