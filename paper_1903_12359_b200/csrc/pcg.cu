@@ -71,6 +71,7 @@ struct SolveSystem {
     DevBuf<double> res;  // per slot: relres, bnorm^2, true_res^2, xnorm^2, pad
     // two-level preconditioner (see k_pcg2)
     bool coarse = false;
+    bool force_jacobi = false;   // set for the Jacobi re-solve of non-converged slots
     int gmax = 8;
     DevBuf<int32_t> cell, aggr, aoff;
     DevBuf<float2> pxy_row;
@@ -2302,7 +2303,7 @@ int build_system(pgcp_batch* b, SolveSystem* S, bool dncp, const int32_t* d_pins
     PGCP_TRY(S->rowsrc.fill_bytes(0xff, s));
     {
         const char* ev = getenv("PGCP_PCG_COARSE");
-        S->coarse = !(ev && atoi(ev) == 0);
+        S->coarse = !S->force_jacobi && !(ev && atoi(ev) == 0);
         const char* eg = getenv("PGCP_PCG_GMAX");
         S->gmax = eg ? std::max(1, std::min(COARSE_GMAX, atoi(eg))) : COARSE_GMAX;
     }
@@ -2421,7 +2422,11 @@ int run_solve(pgcp_batch* b, SolveSystem* S, const pgcp_solve_opts* o, double* z
     A.res = S->res.p;
     double rtol = (o && o->rtol > 0) ? o->rtol : 1e-10;
     A.tol2 = rtol * rtol;
-    A.maxit = (o && o->maxit > 0) ? o->maxit : 200000;
+    // two-level PCG needs ~3.5x fewer iterations than Jacobi; its default cap
+    // bounds the time lost before a slot falls back to Jacobi (solve_*)
+    int coarse_cap = 60000;
+    if (const char* ec = getenv("PGCP_PCG_COARSE_MAXIT")) coarse_cap = std::max(1, atoi(ec));  // tests
+    A.maxit = (o && o->maxit > 0) ? o->maxit : (S->coarse ? coarse_cap : 200000);
     A.chunk_cap = chunk;
     A.C.abase = S->abase.p;
     A.C.aoff = S->aoff.p;
@@ -2667,7 +2672,42 @@ int solve_flatten(pgcp_batch* b, const int32_t* comps, int32_t ncomp, const int3
         fprintf(stderr, "[pcg timing] flatten build_system %.2f ms (host, synchronised)\n",
                 1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
     }
-    return run_solve(b, S, o, z, st, s);
+    std::vector<pgcp_solve_stat> hst(S->nslot);
+    int rc = run_solve(b, S, o, z, hst.data(), s);
+    bool only_noconv = rc == PGCP_E_NOCONV;
+    for (int j = 0; j < S->nslot && only_noconv; ++j)
+        only_noconv = hst[j].status == PGCP_OK || hst[j].status == PGCP_E_NOCONV;
+    if (only_noconv && S->coarse && !(o && o->maxit > 0)) {
+        // safety net: re-solve the slots the two-level PCG did not finish with
+        // plain Jacobi-PCG (same kernels family, still on the device)
+        std::vector<int32_t> rc_comps, rc_pins;
+        std::vector<int> where;
+        for (int j = 0; j < S->nslot; ++j)
+            if (hst[j].status == PGCP_E_NOCONV) {
+                rc_comps.push_back(S->comps[j]);
+                rc_pins.push_back(hp[2 * j]);
+                rc_pins.push_back(hp[2 * j + 1]);
+                where.push_back(j);
+            }
+        SolveSystem R;
+        R.force_jacobi = true;
+        PGCP_TRY(prepare_slots(b, &R, rc_comps.data(), (int32_t)rc_comps.size()));
+        DevBuf<int32_t> dp2;
+        PGCP_TRY(dp2.alloc((int64_t)rc_pins.size(), s));
+        PGCP_TRY_CUDA(cudaMemcpyAsync(dp2.p, rc_pins.data(), rc_pins.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+        PGCP_TRY(build_system(b, &R, true, dp2.p, t, nullptr, nullptr, 0, s));
+        std::vector<pgcp_solve_stat> rst(R.nslot);
+        rc = run_solve(b, &R, o, z, rst.data(), s);
+        for (size_t q = 0; q < where.size(); ++q) hst[where[q]] = rst[q];
+        S->kernel_ms += R.kernel_ms;
+        S->iters_sum += R.iters_sum;
+        S->iters_max = std::max(S->iters_max, R.iters_max);
+        S->bytes_iter_weighted += R.bytes_iter_weighted;
+        S->ref_bytes_weighted += R.ref_bytes_weighted;
+    }
+    if (st)
+        for (int j = 0; j < S->nslot; ++j) st[j] = hst[j];
+    return rc;
 }
 
 int solve_harmonic(pgcp_batch* b, const int32_t* comps, int32_t ncomp, const int32_t* fixed_gid,
@@ -2686,7 +2726,35 @@ int solve_harmonic(pgcp_batch* b, const int32_t* comps, int32_t ncomp, const int
         fprintf(stderr, "[pcg timing] harmonic build_system %.2f ms (host, synchronised)\n",
                 1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
     }
-    return run_solve(b, S, o, z, st, s);
+    std::vector<pgcp_solve_stat> hst(S->nslot);
+    int rc = run_solve(b, S, o, z, hst.data(), s);
+    bool only_noconv = rc == PGCP_E_NOCONV;
+    for (int j = 0; j < S->nslot && only_noconv; ++j)
+        only_noconv = hst[j].status == PGCP_OK || hst[j].status == PGCP_E_NOCONV;
+    if (only_noconv && S->coarse && !(o && o->maxit > 0)) {  // Jacobi safety net (see solve_flatten)
+        std::vector<int32_t> rc_comps;
+        std::vector<int> where;
+        for (int j = 0; j < S->nslot; ++j)
+            if (hst[j].status == PGCP_E_NOCONV) {
+                rc_comps.push_back(S->comps[j]);
+                where.push_back(j);
+            }
+        SolveSystem R;
+        R.force_jacobi = true;
+        PGCP_TRY(prepare_slots(b, &R, rc_comps.data(), (int32_t)rc_comps.size()));
+        PGCP_TRY(build_system(b, &R, false, nullptr, nullptr, fixed_gid, fixed_val, nfixed, s));
+        std::vector<pgcp_solve_stat> rst(R.nslot);
+        rc = run_solve(b, &R, o, z, rst.data(), s);
+        for (size_t q = 0; q < where.size(); ++q) hst[where[q]] = rst[q];
+        S->kernel_ms += R.kernel_ms;
+        S->iters_sum += R.iters_sum;
+        S->iters_max = std::max(S->iters_max, R.iters_max);
+        S->bytes_iter_weighted += R.bytes_iter_weighted;
+        S->ref_bytes_weighted += R.ref_bytes_weighted;
+    }
+    if (st)
+        for (int j = 0; j < S->nslot; ++j) st[j] = hst[j];
+    return rc;
 }
 
 int system_dims(pgcp_batch* b, int which, int32_t* nslot_out) {

@@ -124,3 +124,15 @@ def test_weld_error_propagates(cuda):
         partial_weld(np.array([0, 0, 1 + 1j, 1j]), a, 2)
     with pytest.raises(WeldError, match="out of range"):
         partial_weld(a, a, 7)
+
+
+def test_two_level_falls_back_to_jacobi(cuda, monkeypatch):
+    """A slot the two-level PCG does not finish within its cap is re-solved
+    with Jacobi-PCG on the device; the result still matches the reference."""
+    from paper_1903_12359_b200 import TriMesh, parameterize
+    monkeypatch.setenv("PGCP_PCG_COARSE_MAXIT", "5")
+    z = load_golden("blocks3x3")
+    gp, rep = parameterize(TriMesh(z["V"], z["F"]), z["cuts"], str(z["mode"]))
+    ref = z["coords"]
+    assert np.max(np.abs(np.asarray(gp.coords) - ref)) <= 1e-6 * _diam(ref)
+    assert max(rep.solver["flatten_iters"]) > 5
