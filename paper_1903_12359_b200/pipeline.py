@@ -16,6 +16,7 @@ and the final device -> host copy of the coordinates.
 import ctypes
 import json
 import os
+import threading
 import time
 from dataclasses import dataclass, field
 
@@ -236,34 +237,59 @@ def parameterize(mesh, cuts=None, mode="free", workers=1, seed=0, mobius_area=Fa
                              "adjust the cut set")
     part = Partition(mesh, batch, norm)
     K = info[nat.INFO_K]
-    if have_cuts:
-        steps = plan_weld_schedule(part, mode, pairs=cfg.pairs if cfg.schedule == "pairs" else None)
-    else:
-        steps = []
-    clk.stop("partition")
     report.n_submeshes = K
     voff = batch.host(nat.ARR_VERT_OFF, torch.int64)
     report.submesh_sizes = [int(x) for x in np.diff(voff)]
+    welds = not (K == 1 and mode == "free")
+    if welds:  # host copies the planner needs, taken before the solve is queued
+        cycles = part.boundary_cycles
+        loop_local = batch.host(nat.ARR_LOOP, torch.int32).astype(np.int64)
+    clk.stop("partition")
 
     own = shard.comps(report.submesh_sizes) if (shard is not None and K > 1) else None
 
-    # ---- local free-boundary flattening (all submeshes, one launch) -----------
+    # ---- local free-boundary flattening (all submeshes, one launch), with the
+    # host-side weld planning (planner.cpp, weld plan) overlapped on this thread
     clk.start()
-    z0, fst = batch.flatten(comps=own, rtol=cfg.rtol, cluster=cfg.cluster)
+    fres = {}
+
+    def _flatten():
+        try:
+            torch.cuda.set_device(dev)  # the current device is per host thread
+            fres["out"] = batch.flatten(comps=own, rtol=cfg.rtol, cluster=cfg.cluster)
+        except BaseException as exc:  # re-raised on the caller's thread
+            fres["err"] = exc
+
+    worker = threading.Thread(target=_flatten, name="pgcp-flatten")
+    worker.start()
+    steps, plan, perr = [], None, None
+    t_plan = time.perf_counter()
+    try:
+        if have_cuts:
+            steps = plan_weld_schedule(part, mode, pairs=cfg.pairs if cfg.schedule == "pairs" else None)
+        if welds:
+            plan = WeldPlan(cycles, steps, mesh.n_vertices)
+            loop_gid_host = (voff[plan.slot_sub] + loop_local).astype(np.int32)
+    except BaseException as exc:
+        perr = exc
+    timings["plan (overlapped)"] = time.perf_counter() - t_plan
+    worker.join()
+    if "err" in fres:
+        raise fres["err"]
+    if perr is not None:
+        raise perr
+    z0, fst = fres["out"]
     clk.stop("flatten")
     report.solver = {"flatten_iters": [s["iters"] for s in fst], "flatten": batch.last_solve(0)}
     if own is not None:
         report.solver["shard"] = own
 
-    if K == 1 and mode == "free":
+    if not welds:
         embeddings = z0
     else:
         # ---- welding on tracked boundary values ---------------------------------
         clk.start()
-        cycles = part.boundary_cycles
-        plan = WeldPlan(cycles, steps, mesh.n_vertices)
-        loop_local = batch.host(nat.ARR_LOOP, torch.int32).astype(np.int64)
-        loop_gid = torch.as_tensor((voff[plan.slot_sub] + loop_local).astype(np.int32)).to(dev)
+        loop_gid = torch.as_tensor(loop_gid_host).to(dev)
         tv = torch.empty(len(plan.slot_parent), dtype=torch.complex128, device=dev)
         nat.check(nat.lib().pgcp_gather_complex(_ptr(z0), _ptr(loop_gid), _ptr(tv), tv.numel(), _stream()))
         if own is not None:
