@@ -159,6 +159,18 @@ PGCP_API int pgcp_batch_harmonic(pgcp_batch* b, const int32_t* comps, int32_t nc
                         const pgcp_solve_opts* opts, double* z,
                         pgcp_solve_stat* stats, void* stream);
 
+/* The harmonic solve in two calls: _prepare builds everything that does not
+ * depend on the fixed values (unknown numbering, sliced ELL, Jacobi scaling,
+ * coarse space; synchronises `stream`), _solve takes the values (same order
+ * as fixed_gid), forms the right-hand side and runs the PCG. Lets a caller
+ * overlap the preparation with the computation of the values (the weld).
+ * pgcp_batch_harmonic = _prepare + _solve. */
+PGCP_API int pgcp_batch_harmonic_prepare(pgcp_batch* b, const int32_t* comps, int32_t ncomp,
+                                         const int32_t* fixed_gid, int64_t nfixed, const pgcp_solve_opts* opts,
+                                         void* stream);
+PGCP_API int pgcp_batch_harmonic_solve(pgcp_batch* b, const double* fixed_val, int64_t nfixed,
+                                       const pgcp_solve_opts* opts, double* z, pgcp_solve_stat* stats, void* stream);
+
 /* Summary of the last flatten (0) / harmonic (1) solve: out[0] PCG kernel
  * time in ms (CUDA events on the launch stream), [1] total iterations,
  * [2] max iterations, [3] sum over submeshes of iterations x the device

@@ -64,6 +64,9 @@ _SIGS = {
                             ctypes.POINTER(SolveStat), _VP], ctypes.c_int),
     "pgcp_batch_harmonic": ([_VP, _VP, _I32, _VP, _VP, _I64, ctypes.POINTER(SolveOpts), _VP,
                              ctypes.POINTER(SolveStat), _VP], ctypes.c_int),
+    "pgcp_batch_harmonic_prepare": ([_VP, _VP, _I32, _VP, _I64, ctypes.POINTER(SolveOpts), _VP], ctypes.c_int),
+    "pgcp_batch_harmonic_solve": ([_VP, _VP, _I64, ctypes.POINTER(SolveOpts), _VP, ctypes.POINTER(SolveStat), _VP],
+                                  ctypes.c_int),
     "pgcp_batch_export_system": ([_VP, ctypes.c_int, _I32, _PI64, _VP, _VP, _VP, _VP, _VP], ctypes.c_int),
     "pgcp_batch_conformal_energy": ([_VP, _VP, _PD, _VP], ctypes.c_int),
     "pgcp_batch_stitch": ([_VP, _VP, ctypes.c_int, _D, _D, _VP, _VP, _VP, _VP, _VP, _VP], ctypes.c_int),

@@ -58,6 +58,10 @@ int conformal_energy(pgcp_batch* b, const double* z, double* energy, cudaStream_
 int solve_flatten(pgcp_batch* b, const int32_t* comps, int32_t ncomp, const int32_t* pins,
                   const double* targets, const pgcp_solve_opts* o, double* z, pgcp_solve_stat* st,
                   cudaStream_t s);
+int prepare_harmonic(pgcp_batch* b, const int32_t* comps, int32_t ncomp, const int32_t* fixed_gid, int64_t nfixed,
+                     const pgcp_solve_opts* o, cudaStream_t s);
+int finish_harmonic(pgcp_batch* b, const double* fixed_val, int64_t nfixed, const pgcp_solve_opts* o, double* z,
+                    pgcp_solve_stat* st, cudaStream_t s);
 int solve_harmonic(pgcp_batch* b, const int32_t* comps, int32_t ncomp, const int32_t* fixed_gid,
                    const double* fixed_val, int64_t nfixed, const pgcp_solve_opts* o, double* z,
                    pgcp_solve_stat* st, cudaStream_t s);

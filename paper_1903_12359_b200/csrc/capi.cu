@@ -201,6 +201,28 @@ int pgcp_batch_harmonic(pgcp_batch* b, const int32_t* comps, int32_t ncomp, cons
     return solve_harmonic(b, comps, ncomp, fixed_gid, fixed_val, nfixed, opts, z, stats, s);
 }
 
+int pgcp_batch_harmonic_prepare(pgcp_batch* b, const int32_t* comps, int32_t ncomp, const int32_t* fixed_gid,
+                                int64_t nfixed, const pgcp_solve_opts* opts, void* stream) {
+    if (!b || nfixed < 0 || (nfixed > 0 && !fixed_gid)) {
+        set_error("pgcp_batch_harmonic_prepare: invalid arguments");
+        return PGCP_E_INVALID;
+    }
+    PGCP_TRY_CUDA(cudaSetDevice(b->device));
+    cudaStream_t s = as_stream(stream);
+    if (!b->has_laplacian) PGCP_TRY(build_laplacian(b, nullptr, s));
+    return prepare_harmonic(b, comps, ncomp, fixed_gid, nfixed, opts, s);
+}
+
+int pgcp_batch_harmonic_solve(pgcp_batch* b, const double* fixed_val, int64_t nfixed, const pgcp_solve_opts* opts,
+                              double* z, pgcp_solve_stat* stats, void* stream) {
+    if (!b || !z || nfixed < 0 || (nfixed > 0 && !fixed_val)) {
+        set_error("pgcp_batch_harmonic_solve: invalid arguments");
+        return PGCP_E_INVALID;
+    }
+    PGCP_TRY_CUDA(cudaSetDevice(b->device));
+    return finish_harmonic(b, fixed_val, nfixed, opts, z, stats, as_stream(stream));
+}
+
 int pgcp_batch_export_system(pgcp_batch* b, int which, int32_t comp, int64_t* dims, int32_t* indptr,
                              int32_t* indices, double* data, double* rhs, void* stream) {
     if (!b || !dims) {

@@ -72,6 +72,11 @@ struct SolveSystem {
     // two-level preconditioner (see k_pcg2)
     bool coarse = false;
     bool force_jacobi = false;   // set for the Jacobi re-solve of non-converged slots
+    bool setup_done = false;     // cluster shape, coarse space and encoded columns built
+    bool prepared = false;       // harmonic: structure built, waiting for the fixed values
+    int chunk = 1;
+    DevBuf<int32_t> fixed_gid_copy;  // harmonic: fixed list (Jacobi re-solve)
+    int64_t nfixed = 0;
     int gmax = 8;
     DevBuf<int32_t> cell, aggr, aoff;
     DevBuf<float2> pxy_row;
@@ -248,6 +253,34 @@ __global__ void k_fill_rows(BuildArgs a, int64_t rows, const int64_t* __restrict
         bvec[r] = bb;
         cpl[r] = make_int2(-1, -1);
         x[r] = make_double2(0.0, 0.0);
+    }
+}
+
+// harmonic right-hand side from the fixed values (the part of k_fill_rows that
+// a prepared solve defers), already Jacobi-scaled: b = D^{-1/2} (-L_UF f)
+__global__ void k_rhs_fixed(BuildArgs a, int64_t rows, const double* __restrict__ Dsq, double2* __restrict__ bvec) {
+    GRID_STRIDE(r, rows) {
+        const int e = a.rowsrc[r];
+        double2 bb = make_double2(0.0, 0.0);
+        if (e >= 0) {
+            const int j = bsearch_off(a.sl_off, a.nslot + 1, r >> 5);
+            const int c = a.comps[j];
+            const int self = (int)(e - a.sv_off[j]);
+            const int64_t g = a.vert_off[c] + self;
+            for (int64_t q = a.row_ptr[g]; q < a.row_ptr[g + 1]; ++q) {
+                const int lc = a.col[q];
+                if (lc == self) continue;
+                const int64_t ee = a.sv_off[j] + lc;
+                if (a.urow[ee] < 0) {
+                    const double2 f = a.fv[a.fixed_ref[ee]];
+                    const double v = a.val[q];
+                    bb.x -= v * f.x;
+                    bb.y -= v * f.y;
+                }
+            }
+        }
+        const double d = Dsq[r];
+        bvec[r] = make_double2(bb.x / d, bb.y / d);
     }
 }
 
@@ -2261,7 +2294,10 @@ int build_system(pgcp_batch* b, SolveSystem* S, bool dncp, const int32_t* d_pins
     } else {
         PGCP_TRY(S->fv.alloc(nfixed, s));
         if (nfixed > 0) {
-            PGCP_TRY_CUDA(cudaMemcpyAsync(S->fv.p, fixed_val, nfixed * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+            if (fixed_val)
+                PGCP_TRY_CUDA(cudaMemcpyAsync(S->fv.p, fixed_val, nfixed * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+            else
+                PGCP_TRY(S->fv.zero(s));  // prepared solve: values (and the rhs) come later
             k_fixed_list<<<grid_for(nfixed, 256), 256, 0, s>>>(nfixed, fixed_gid, b->comp_of_gid.p,
                                                               S->slot_of_comp.p, b->vert_off.p, S->sv_off.p,
                                                               S->fixed_ref.p);
@@ -2374,14 +2410,16 @@ int build_system(pgcp_batch* b, SolveSystem* S, bool dncp, const int32_t* d_pins
     return PGCP_OK;
 }
 
-int run_solve(pgcp_batch* b, SolveSystem* S, const pgcp_solve_opts* o, double* z, pgcp_solve_stat* st,
-              cudaStream_t s) {
+// cluster shape, coarse space (two-level) and the per-shape column encoding:
+// everything of a solve that does not depend on the right-hand side
+int setup_solve(SolveSystem* S, const pgcp_solve_opts* o, cudaStream_t s) {
     const int32_t nslot = S->nslot;
     int64_t max_sl = 0;
     for (int j = 0; j < nslot; ++j) max_sl = std::max(max_sl, S->h_sl_off[j + 1] - S->h_sl_off[j]);
     int csize = 1, chunk = 1;
     PGCP_TRY(pick_cluster(max_sl, nslot, o ? o->cluster : 0, S->coarse, &csize, &chunk));
     S->csize = csize;
+    S->chunk = chunk;
     if (S->coarse) {
         cudaEvent_t c0, c1;
         PGCP_TRY_CUDA(cudaEventCreate(&c0));
@@ -2396,6 +2434,20 @@ int run_solve(pgcp_batch* b, SolveSystem* S, const pgcp_solve_opts* o, double* z
         cudaEventDestroy(c1);
         S->coarse_ms = cms;
     }
+    PGCP_TRY(S->enc.alloc(S->nnz, s));
+    PGCP_TRY(S->remote.alloc(S->nslices, s));
+    k_encode_cols<<<grid_for(S->nslices * 32, 256), 256, 0, s>>>(nslot, S->sl_off.p, S->nslices, S->sl_ptr.p, S->col.p,
+                                                               csize, S->enc.p, S->remote.p);
+    PGCP_LAUNCH_CHECK();
+    S->setup_done = true;
+    return PGCP_OK;
+}
+
+int run_solve(pgcp_batch* b, SolveSystem* S, const pgcp_solve_opts* o, double* z, pgcp_solve_stat* st,
+              cudaStream_t s) {
+    const int32_t nslot = S->nslot;
+    if (!S->setup_done) PGCP_TRY(setup_solve(S, o, s));
+    const int csize = S->csize, chunk = S->chunk;
     PGCP_TRY(S->iters.alloc(nslot, s));
     PGCP_TRY(S->res.alloc(8 * (int64_t)nslot, s));
     PGCP_TRY(S->res.zero(s));
@@ -2404,11 +2456,6 @@ int run_solve(pgcp_batch* b, SolveSystem* S, const pgcp_solve_opts* o, double* z
     A.sl_ptr = S->sl_ptr.p;
     A.sl_mask = S->sl_mask.p;
     A.col = S->col.p;
-    PGCP_TRY(S->enc.alloc(S->nnz, s));
-    PGCP_TRY(S->remote.alloc(S->nslices, s));
-    k_encode_cols<<<grid_for(S->nslices * 32, 256), 256, 0, s>>>(nslot, S->sl_off.p, S->nslices, S->sl_ptr.p, S->col.p,
-                                                               csize, S->enc.p, S->remote.p);
-    PGCP_LAUNCH_CHECK();
     A.enc = S->enc.p;
     A.remote = S->remote.p;
     A.val = S->val.p;
@@ -2710,21 +2757,65 @@ int solve_flatten(pgcp_batch* b, const int32_t* comps, int32_t ncomp, const int3
     return rc;
 }
 
-int solve_harmonic(pgcp_batch* b, const int32_t* comps, int32_t ncomp, const int32_t* fixed_gid,
-                   const double* fixed_val, int64_t nfixed, const pgcp_solve_opts* o, double* z,
-                   pgcp_solve_stat* st, cudaStream_t s) {
+// Harmonic solve in two parts so the structure (unknown numbering, sliced
+// ELL, Jacobi scaling, coarse space, column encoding) can be built while the
+// fixed values are still being computed (pipeline: during the weld).
+int prepare_harmonic(pgcp_batch* b, const int32_t* comps, int32_t ncomp, const int32_t* fixed_gid, int64_t nfixed,
+                     const pgcp_solve_opts* o, cudaStream_t s) {
     SolveSystem*& slot = system_slot(b, 1);
     delete slot;
     slot = new SolveSystem();
     SolveSystem* S = slot;
     PGCP_TRY(prepare_slots(b, S, comps, ncomp));
-    if (S->nslot == 0) return PGCP_OK;
+    S->nfixed = nfixed;
+    PGCP_TRY(S->fixed_gid_copy.alloc(std::max<int64_t>(nfixed, 1), s));
+    if (nfixed > 0)
+        PGCP_TRY_CUDA(cudaMemcpyAsync(S->fixed_gid_copy.p, fixed_gid, nfixed * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+    if (S->nslot == 0) {
+        S->prepared = true;
+        return PGCP_OK;
+    }
     auto t0 = std::chrono::steady_clock::now();
-    PGCP_TRY(build_system(b, S, false, nullptr, nullptr, fixed_gid, fixed_val, nfixed, s));
-    if (getenv("PGCP_PCG_TIMING")) {
-        cudaStreamSynchronize(s);
-        fprintf(stderr, "[pcg timing] harmonic build_system %.2f ms (host, synchronised)\n",
+    PGCP_TRY(build_system(b, S, false, nullptr, nullptr, S->fixed_gid_copy.p, nullptr, nfixed, s));
+    PGCP_TRY(setup_solve(S, o, s));
+    PGCP_TRY_CUDA(cudaStreamSynchronize(s));
+    if (getenv("PGCP_PCG_TIMING"))
+        fprintf(stderr, "[pcg timing] harmonic prepare (build + setup) %.2f ms (host, synchronised)\n",
                 1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+    S->prepared = true;
+    return PGCP_OK;
+}
+
+int finish_harmonic(pgcp_batch* b, const double* fixed_val, int64_t nfixed, const pgcp_solve_opts* o, double* z,
+                    pgcp_solve_stat* st, cudaStream_t s) {
+    SolveSystem* S = system_slot(b, 1);
+    if (!S || !S->prepared) {
+        set_error("harmonic solve: no prepared system (call pgcp_batch_harmonic_prepare first)");
+        return PGCP_E_INVALID;
+    }
+    if (nfixed != S->nfixed) {
+        set_error("harmonic solve: %lld fixed values for %lld fixed vertices", (long long)nfixed, (long long)S->nfixed);
+        return PGCP_E_INVALID;
+    }
+    S->prepared = false;
+    if (S->nslot == 0) return PGCP_OK;
+    if (nfixed > 0) {
+        PGCP_TRY_CUDA(cudaMemcpyAsync(S->fv.p, fixed_val, nfixed * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+        BuildArgs a;
+        a.nslot = S->nslot;
+        a.comps = S->d_comps.p;
+        a.sv_off = S->sv_off.p;
+        a.sl_off = S->sl_off.p;
+        a.vert_off = b->vert_off.p;
+        a.row_ptr = b->row_ptr.p;
+        a.col = b->col.p;
+        a.val = b->val.p;
+        a.rowsrc = S->rowsrc.p;
+        a.urow = S->urow.p;
+        a.fixed_ref = S->fixed_ref.p;
+        a.fv = S->fv.p;
+        k_rhs_fixed<<<grid_for(S->rows, 256), 256, 0, s>>>(a, S->rows, S->Dsq.p, S->b.p);
+        PGCP_LAUNCH_CHECK();
     }
     std::vector<pgcp_solve_stat> hst(S->nslot);
     int rc = run_solve(b, S, o, z, hst.data(), s);
@@ -2742,7 +2833,7 @@ int solve_harmonic(pgcp_batch* b, const int32_t* comps, int32_t ncomp, const int
         SolveSystem R;
         R.force_jacobi = true;
         PGCP_TRY(prepare_slots(b, &R, rc_comps.data(), (int32_t)rc_comps.size()));
-        PGCP_TRY(build_system(b, &R, false, nullptr, nullptr, fixed_gid, fixed_val, nfixed, s));
+        PGCP_TRY(build_system(b, &R, false, nullptr, nullptr, S->fixed_gid_copy.p, fixed_val, nfixed, s));
         std::vector<pgcp_solve_stat> rst(R.nslot);
         rc = run_solve(b, &R, o, z, rst.data(), s);
         for (size_t q = 0; q < where.size(); ++q) hst[where[q]] = rst[q];
@@ -2755,6 +2846,13 @@ int solve_harmonic(pgcp_batch* b, const int32_t* comps, int32_t ncomp, const int
     if (st)
         for (int j = 0; j < S->nslot; ++j) st[j] = hst[j];
     return rc;
+}
+
+int solve_harmonic(pgcp_batch* b, const int32_t* comps, int32_t ncomp, const int32_t* fixed_gid,
+                   const double* fixed_val, int64_t nfixed, const pgcp_solve_opts* o, double* z,
+                   pgcp_solve_stat* st, cudaStream_t s) {
+    PGCP_TRY(prepare_harmonic(b, comps, ncomp, fixed_gid, nfixed, o, s));
+    return finish_harmonic(b, fixed_val, nfixed, o, z, st, s);
 }
 
 int system_dims(pgcp_batch* b, int which, int32_t* nslot_out) {

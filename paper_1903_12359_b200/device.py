@@ -205,6 +205,40 @@ class DeviceBatch:
         nat.check(st)
         return z, self.last_stats
 
+    def harmonic_prepare(self, fixed_gid, comps=None, rtol=1e-10, contract_tol=1e-10, maxit=0, cluster=0,
+                         stream=None):
+        """First half of `harmonic`: everything that does not depend on the
+        fixed values (may run on another stream while those are computed)."""
+        self.laplacian()
+        carr, nc, nslot = self._comps(comps)
+        fg = to_dev(fixed_gid, torch.int32)
+        self._prep = (comps, nslot, int(fg.numel()))
+        if comps is not None and nc == 0:
+            return
+        nat.check(nat.lib().pgcp_batch_harmonic_prepare(
+            self.h, carr, nc, ptr(fg), int(fg.numel()),
+            ctypes.byref(self._opts(rtol, contract_tol, maxit, cluster)),
+            stream_handle(stream if stream is not None else self.stream)))
+
+    def harmonic_solve(self, fixed_val, rtol=1e-10, contract_tol=1e-10, maxit=0, cluster=0, out=None):
+        """Second half of `harmonic` (after `harmonic_prepare`)."""
+        comps, nslot, nfixed = self._prep
+        fv = to_dev(fixed_val, torch.complex128)
+        if int(fv.numel()) != nfixed:
+            raise ValueError(f"{fv.numel()} fixed values for {nfixed} fixed vertices")
+        z = out if out is not None else torch.zeros(self.info()[nat.INFO_SUM_N], dtype=torch.complex128,
+                                                    device=device())
+        if comps is not None and len(comps) == 0:
+            self.last_stats = []
+            return z, []
+        stats = (nat.SolveStat * max(nslot, 1))()
+        st = nat.lib().pgcp_batch_harmonic_solve(self.h, ptr(fv), nfixed,
+                                                 ctypes.byref(self._opts(rtol, contract_tol, maxit, cluster)),
+                                                 ptr(z), stats, stream_handle(self.stream))
+        self.last_stats = [_stat(s) for s in stats[:nslot]]
+        nat.check(st)
+        return z, self.last_stats
+
     def export_system(self, which, comp):
         """(scipy CSR, rhs) of the last flatten (0: C_ff) / harmonic (1: L_II) system."""
         from scipy import sparse

@@ -323,6 +323,8 @@ def parameterize(mesh, cuts=None, mode="free", workers=1, seed=0, mobius_area=Fa
             ext_slots = torch.as_tensor(plan.slots_of(exterior).astype(np.int32)).to(dev)
             nat.check(nat.lib().pgcp_inv_shift(_ptr(tv), _ptr(ext_slots), ext_slots.numel(), 0.0, 0.0,
                                                center.real, center.imag, _stream()))
+        # (building the harmonic system on a side stream during the weld was
+        # measured slower: its kernels and the weld's serial chain contend)
         z, hst = batch.harmonic(loop_gid, tv, comps=own, rtol=cfg.rtol, cluster=cfg.cluster)
         report.solver["harmonic_iters"] = [s["iters"] for s in hst]
         report.solver["harmonic"] = batch.last_solve(1)

@@ -186,3 +186,24 @@ def test_cfg2_stagewise(cuda):
         ref = oracle.dncp_flatten(sp.sub_V[c], sp.sub_F[c], sp.loops[c])
         got = zz[voff[c]:voff[c + 1]]
         assert np.max(np.abs(got - ref)) <= 1e-6 * 2 * np.max(np.abs(ref - ref.mean()))
+
+
+def test_harmonic_prepare_then_solve_equals_harmonic(cuda):
+    """The two-call harmonic API (structure first, values later) gives the
+    same embedding as the one-call solve, bit for bit."""
+    import torch
+    from paper_1903_12359_b200 import TriMesh, partition_mesh
+    from paper_1903_12359_b200 import _native as nat
+    z = load_golden("blocks3x3")
+    part = partition_mesh(TriMesh(z["V"], z["F"]), z["cuts"])
+    b = part.batch
+    voff = b.host(nat.ARR_VERT_OFF, torch.int64)
+    loff = b.host(nat.ARR_LOOP_OFF, torch.int64)
+    lp = b.host(nat.ARR_LOOP, torch.int32)
+    gid = np.concatenate([voff[c] + lp[loff[c]:loff[c + 1]] for c in range(b.K)]).astype(np.int32)
+    vals = np.exp(2j * np.pi * np.linspace(0, 1, len(gid), endpoint=False))
+    z1, _ = b.harmonic(gid, vals)
+    b.harmonic_prepare(gid)
+    z2, st = b.harmonic_solve(vals)
+    assert all(s["status"] == 0 for s in st)
+    assert torch.equal(z1, z2)
