@@ -55,6 +55,18 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
 }
 __device__ __forceinline__ double2 cscale(double s, double2 a) { return cmul(C(s, 0.0), a); }
 __device__ __forceinline__ double cabs_(double2 a) { return hypot(a.x, a.y); }
+// |a| > t and |a| < t without the hypot in the common case; same decisions:
+// max(|x|,|y|) <= |a| <= sqrt(2) max(|x|,|y|)
+__device__ __forceinline__ bool cabs_gt(double2 a, double t) {
+    const double m = fmax(fabs(a.x), fabs(a.y));
+    if (!(m * 1.5 > t)) return m != m ? (cabs_(a) > t) : false;  // 1.5 > sqrt(2) with margin
+    return m > t || cabs_(a) > t;
+}
+__device__ __forceinline__ bool cabs_lt(double2 a, double t) {
+    const double m = fmax(fabs(a.x), fabs(a.y));
+    if (m >= t) return false;
+    return cabs_(a) < t;
+}
 
 // numpy's complex division (Smith's method with a reciprocal)
 __device__ double2 cdiv(double2 a, double2 b) {
@@ -195,7 +207,7 @@ __device__ __forceinline__ void apply_rec(const Rec& r, double2& z, int8_t& s) {
             }
             if (!c_fin(L)) {
                 z = cinf();
-            } else if (cabs_(L) > 1e100) {
+            } else if (cabs_gt(L, 1e100)) {
                 z = (L.x >= 0) ? L : cneg(L);
             } else {
                 z = csqrt_(csub(cmul(L, L), C(1.0, 0.0)));
@@ -239,7 +251,7 @@ __device__ __forceinline__ void apply_rec(const Rec& r, double2& z, int8_t& s) {
             }
             if (!c_fin(T)) {
                 z = cinf();
-            } else if (cabs_(T) > 1e100) {
+            } else if (cabs_gt(T, 1e100)) {
                 z = (T.x >= 0) ? T : cneg(T);
             } else {
                 z = csqrt_(cadd(cmul(T, T), C(1.0, 0.0)));
@@ -684,7 +696,7 @@ __global__ void __launch_bounds__(NT, 1) k_phase1c(Phase1Args A) {
                 err = WE_ZIP_HALF; eidx = j; eaux = side;
             } else if (!(xi.x > 0)) {
                 err = WE_ZIP_AXIS; eidx = j; eaux = side;
-            } else if (cabs_(xi) < 1e-13) {
+            } else if (cabs_lt(xi, 1e-13)) {
                 err = WE_ZIP_COLL; eidx = j; eaux = side;
             }
         }
@@ -1079,7 +1091,7 @@ __global__ void __launch_bounds__(512) k_geodesic(GeoArgs A) {
             double2 xi = A.pts[j];
             if (A.sides[j] != 0 || c_isinf(xi)) block_fail(&s_err, WE_ZIP_HALF, j, 0, meta);
             else if (!(xi.x > 0)) block_fail(&s_err, WE_ZIP_AXIS, j, 0, meta);
-            else if (cabs_(xi) < 1e-13) block_fail(&s_err, WE_ZIP_COLL, j, 0, meta);
+            else if (cabs_lt(xi, 1e-13)) block_fail(&s_err, WE_ZIP_COLL, j, 0, meta);
             else {
                 s_rec = mk_open(xi, UP);
                 A.recs[nrec] = s_rec;
