@@ -247,3 +247,138 @@ def icosphere_arrays(subdiv):
                             np.stack([ca, bc, c], 1), np.stack([ab, bc, ca], 1)])
         V = np.concatenate([V, mid])
     return V, F.astype(np.int32)
+
+
+# ---------------------------------------------------------------------------
+# BASELINE cfg 3 (Delaunay disk) and cfg 4 (spherical-harmonic icosphere).
+# The construction details BASELINE leaves open are pinned here and listed in
+# the noise smoothing (mean over the 16 nearest neighbours), the
+# interior radius margin (interior points stay inside the 256-gon, so the
+# convex hull is exactly the boundary circle's polygon), the harmonic field
+# normalisation (max |f| = 1) and the k-means setup (scikit-learn, n_init=1).
+
+def _kmeans_labels(X, k, seed):
+    from sklearn.cluster import KMeans
+    km = KMeans(n_clusters=k, random_state=seed, n_init=1, max_iter=50).fit(X)
+    return km.cluster_centers_
+
+
+def _face_labels_nearest(centroids, centers):
+    from scipy.spatial import cKDTree
+    return cKDTree(centers).query(centroids)[1].astype(np.int64)
+
+
+def delaunay_disk(n_points=500_000, n_boundary=256, seed=0, noise=0.02):
+    """cfg 3 mesh: n_boundary points on the unit circle, the rest uniform in
+    the disk (r = sqrt(U)), Delaunay-triangulated (CCW), lifted to
+    z = 0.5 (1 - r^2) + noise * (N(0,1) averaged over 16 nearest points)."""
+    from scipy.spatial import Delaunay, cKDTree
+    rng = np.random.default_rng(seed)
+    nin = n_points - n_boundary
+    margin = np.cos(np.pi / n_boundary) * (1.0 - 1e-4)
+    r = np.sqrt(rng.uniform(0.0, 1.0, nin)) * margin
+    th = rng.uniform(0.0, 2.0 * np.pi, nin)
+    tb = 2.0 * np.pi * np.arange(n_boundary) / n_boundary
+    xy = np.concatenate([np.stack([np.cos(tb), np.sin(tb)], 1), np.stack([r * np.cos(th), r * np.sin(th)], 1)])
+    F = Delaunay(xy).simplices.astype(np.int64)
+    a, b, c = xy[F[:, 0]], xy[F[:, 1]], xy[F[:, 2]]
+    neg = ((b[:, 0] - a[:, 0]) * (c[:, 1] - a[:, 1]) - (b[:, 1] - a[:, 1]) * (c[:, 0] - a[:, 0])) < 0
+    F[neg] = F[neg][:, [0, 2, 1]]
+    rr = np.hypot(xy[:, 0], xy[:, 1])
+    eta = rng.standard_normal(len(xy))
+    nbr = cKDTree(xy).query(xy, k=16)[1]
+    z = 0.5 * (1.0 - rr * rr) + noise * eta[nbr].mean(axis=1)
+    V = np.column_stack([xy, z]).astype(np.float64)
+    return V, F.astype(np.int32)
+
+
+def repair_pinches(F, labels, n_vertices, max_rounds=20):
+    """Make every label region a manifold surface: a vertex where one label
+    touches in two or more separate fans (label changes around the vertex
+    exceed its distinct labels) takes the majority label for all its faces;
+    repeated until no such vertex is left."""
+    F = np.asarray(F, dtype=np.int64)
+    labels = np.asarray(labels, dtype=np.int64).copy()
+    m = len(F)
+    de = np.concatenate([F[:, [0, 1]], F[:, [1, 2]], F[:, [2, 0]]])
+    fid = np.tile(np.arange(m), 3)
+    key = np.minimum(de[:, 0], de[:, 1]) * n_vertices + np.maximum(de[:, 0], de[:, 1])
+    order = np.argsort(key, kind="stable")
+    ks = key[order]
+    pair = np.nonzero(ks[1:] == ks[:-1])[0]
+    f1, f2 = fid[order[pair]], fid[order[pair + 1]]      # interior edges: their two faces
+    ev = np.stack([ks[pair] // n_vertices, ks[pair] % n_vertices], 1)
+    vf = np.repeat(np.arange(m), 3)
+    vv = F.reshape(-1)
+    for _ in range(max_rounds):
+        chg = labels[f1] != labels[f2]
+        changes = np.bincount(ev[chg].ravel(), minlength=n_vertices)
+        pairs = np.unique(vv * (labels.max() + 1) + labels[vf])
+        distinct = np.bincount(pairs // (labels.max() + 1), minlength=n_vertices)
+        bnd = np.zeros(n_vertices, dtype=bool)
+        single = np.ones(len(key), dtype=bool)
+        single[order[pair]] = False
+        single[order[pair + 1]] = False
+        bnd[de[single].ravel()] = True
+        # interior vertex: changes == distinct (cyclic) when each label is one fan
+        # (one label: 0 changes); boundary vertex: changes == distinct - 1
+        expect = np.where(bnd, distinct - 1, np.where(distinct > 1, distinct, 0))
+        bad = np.nonzero(changes > expect)[0]
+        if len(bad) == 0:
+            return labels
+        for v in bad:
+            fs = vf[vv == v]
+            vals, cnt = np.unique(labels[fs], return_counts=True)
+            labels[fs] = vals[np.argmax(cnt)]
+    return labels
+
+
+def cfg3(seed=0, n_points=500_000, n_clusters=128):
+    """BASELINE cfg 3: Delaunay disk, 128 k-means subdomains on xy (face
+    centroid -> nearest centre, pinched regions repaired), disk mode."""
+    V, F = delaunay_disk(n_points, 256, seed)
+    cent = V[F].mean(axis=1)[:, :2]
+    centers = _kmeans_labels(V[:, :2], n_clusters, seed)
+    labels = repair_pinches(F, _face_labels_nearest(cent, centers), len(V))
+    return V, F, cuts_from_face_labels(F, labels)
+
+
+def real_sph_harm_field(P, degree=8, seed=0):
+    """sum_{l<=degree, m} c_lm Y_lm(P) with c_lm ~ N(0,1) (seeded), real
+    orthonormal harmonics, normalised to max |f| = 1 over the points P."""
+    from scipy.special import sph_harm_y
+    rng = np.random.default_rng(seed)
+    x, y, z = P[:, 0], P[:, 1], P[:, 2]
+    theta = np.arccos(np.clip(z / np.linalg.norm(P, axis=1), -1.0, 1.0))
+    phi = np.arctan2(y, x)
+    f = np.zeros(len(P))
+    for l in range(degree + 1):
+        for m in range(-l, l + 1):
+            Y = sph_harm_y(l, abs(m), theta, phi)
+            if m < 0:
+                Yr = np.sqrt(2.0) * (-1.0) ** m * Y.imag
+            elif m == 0:
+                Yr = Y.real
+            else:
+                Yr = np.sqrt(2.0) * (-1.0) ** m * Y.real
+            f += rng.standard_normal() * Yr
+    return f / np.max(np.abs(f))
+
+
+def harmonic_sphere(subdiv=9, amp=0.3, degree=8, seed=0):
+    """cfg 4 mesh: icosphere with radius 1 + amp * f(direction)."""
+    V, F = icosphere_arrays(subdiv)
+    f = real_sph_harm_field(V, degree, seed)
+    return V * (1.0 + amp * f)[:, None], F
+
+
+def cfg4(seed=0, subdiv=9, n_clusters=256):
+    """BASELINE cfg 4: spherical-harmonic icosphere (subdivision 9), 256
+    k-means subdomains on the unit directions, sphere mode."""
+    V, F = harmonic_sphere(subdiv, 0.3, 8, seed)
+    U = V / np.linalg.norm(V, axis=1, keepdims=True)
+    centers = _kmeans_labels(U, n_clusters, seed)
+    cent = U[F].mean(axis=1)
+    labels = repair_pinches(F, _face_labels_nearest(cent, centers), len(V))
+    return V, F, cuts_from_face_labels(F, labels)
+

@@ -113,3 +113,22 @@ def test_row_tree_order_covers_blocks():
     order = gen.row_tree_schedule_order(8, 8)
     assert len(order) == 63
     assert order[:2] == [(0, 1), (0, 2)] and order[-1] == (0, 32)
+
+
+def test_cfg3_cfg4_generators_shape():
+    """The irregular BASELINE meshes at test size: a disk whose boundary is
+    the 256-gon on the unit circle (cfg 3), a closed genus-0 surface (cfg 4);
+    both split into disk-type components by their k-means cuts."""
+    V, F, cuts = gen.cfg3(seed=0, n_points=20000, n_clusters=16)
+    chi, nl, cls = oracle.topology_class(len(V), F.astype(np.int64))
+    assert cls == "disk_type"
+    loop = oracle.boundary_loop_list(F.astype(np.int64))[0]
+    assert len(loop) == 256 and np.allclose(np.hypot(V[loop, 0], V[loop, 1]), 1.0)
+    sp = oracle.split_mesh(V, F, cuts)
+    assert sp.n_sub == 16
+    V, F, cuts = gen.cfg4(seed=0, subdiv=4, n_clusters=8)
+    chi, nl, cls = oracle.topology_class(len(V), F.astype(np.int64))
+    assert cls == "sphere_type"
+    r = np.linalg.norm(V, axis=1)
+    assert 0.69 <= r.min() and r.max() <= 1.31
+    assert oracle.split_mesh(V, F, cuts).n_sub == 8
