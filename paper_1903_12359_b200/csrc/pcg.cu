@@ -945,6 +945,10 @@ __global__ void __launch_bounds__(32 * E_WARPS) k_coarse_E(
 // (row/col zeroed). Output: E^-1, made exactly Hermitian.
 constexpr int INV_THREADS = 512;
 
+__device__ __forceinline__ double2 cm(double2 a, double2 b) {
+    return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+
 __global__ void __launch_bounds__(INV_THREADS, 1) k_coarse_inv(const int64_t* __restrict__ abase,
                                                                const int64_t* __restrict__ eoff,
                                                                double2* __restrict__ E) {
@@ -958,64 +962,121 @@ __global__ void __launch_bounds__(INV_THREADS, 1) k_coarse_inv(const int64_t* __
     const int i0 = min(n, rank * rpc), i1 = min(n, i0 + rpc);
     const int nr = i1 - i0;
     double2* Ml = reinterpret_cast<double2*>(smem);    // [rpc][n] my rows
-    double2* rowk = Ml + (size_t)rpc * n;              // [2][n] pivot row (broadcast)
-    double2* colk = rowk + 2 * n;                      // [rpc]  my entries of the pivot column
-    double* s_diag = reinterpret_cast<double*>(colk + rpc);  // [n] original diagonal
+    double2* rowk = Ml + (size_t)rpc * n;              // [2 parity][2 rows][n] pivot rows (broadcast)
+    double2* colk = rowk + 4 * n;                      // [rpc][2] my entries of the pivot columns
+    double* s_diag = reinterpret_cast<double*>(colk + 2 * rpc);  // [n] original diagonal
     double2* M = E + eoff[j];
     for (int t = threadIdx.x; t < nr * n; t += INV_THREADS) Ml[t] = M[(int64_t)i0 * n + t];
     for (int i = threadIdx.x; i < n; i += INV_THREADS) s_diag[i] = M[(int64_t)i * n + i].x;
     __syncthreads();
-    // pivot row 0 -> everyone
+    // pivot rows k, k+1 -> every CTA (owners write through DSMEM)
     int par = 0;
     auto publish = [&](int k, int pr) {
-        if (k < n && k >= i0 && k < i1) {
-            for (int q = threadIdx.x; q < n * CS; q += INV_THREADS) {
-                const int c = q / CS, dst = q - c * CS;
-                double2* rk = cl.map_shared_rank(rowk + pr * n, dst);
-                rk[c] = Ml[(size_t)(k - i0) * n + c];
-            }
+        for (int q = 0; q < 2; ++q) {
+            const int r = k + q;
+            if (r < n && r >= i0 && r < i1)
+                for (int t = threadIdx.x; t < n * CS; t += INV_THREADS) {
+                    const int c = t / CS, dst = t - c * CS;
+                    double2* rk = cl.map_shared_rank(rowk + (2 * pr + q) * n, dst);
+                    rk[c] = Ml[(size_t)(r - i0) * n + c];
+                }
         }
     };
     publish(0, par);
     cl.sync();
-    for (int k = 0; k < n; ++k) {
-        const double2* rk = rowk + par * n;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int NWI = INV_THREADS / 32;
+    for (int k = 0; k < n;) {
+        const double2* R0 = rowk + (2 * par) * n;
+        const double2* R1 = R0 + n;
         // a pivot that lost all but 1e-8 of its original diagonal means the
-        // coarse function is (numerically) dependent on the previous ones
-        const double p = rk[k].x;
-        const bool drop = !(p > 1e-8 * s_diag[k]) || !(s_diag[k] > 0.0);
-        for (int i = threadIdx.x; i < nr; i += INV_THREADS) colk[i] = Ml[(size_t)i * n + k];
+        // coarse function is (numerically) dependent on the previous ones;
+        // two pivots per cluster barrier when the 2x2 block is safe
+        const double a = R0[k].x;
+        const bool drop = !(a > 1e-8 * s_diag[k]) || !(s_diag[k] > 0.0);
+        bool two = false;
+        double2 bb = make_double2(0.0, 0.0);
+        double d = 0.0;
+        if (!drop && k + 1 < n) {
+            bb = R0[k + 1];
+            d = R1[k + 1].x;
+            const double schur = d - (bb.x * bb.x + bb.y * bb.y) / a;
+            two = schur > 1e-8 * s_diag[k + 1] && s_diag[k + 1] > 0.0;
+        }
+        for (int i = threadIdx.x; i < nr; i += INV_THREADS) {
+            colk[2 * i] = Ml[(size_t)i * n + k];
+            if (two) colk[2 * i + 1] = Ml[(size_t)i * n + k + 1];
+        }
         __syncthreads();
-        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-        constexpr int NWI = INV_THREADS / 32;
         if (drop) {
             for (int i = warp; i < nr; i += NWI)
                 for (int c = lane; c < n; c += 32)
                     if (i0 + i == k || c == k) Ml[(size_t)i * n + c] = make_double2(0.0, 0.0);
-        } else {
-            const double ip = 1.0 / p;
+        } else if (!two) {
+            const double ip = 1.0 / a;
             for (int i = warp; i < nr; i += NWI) {
                 const int gi = i0 + i;
-                const double2 a = colk[i];
+                const double2 ca = colk[2 * i];
                 double2* row = Ml + (size_t)i * n;
                 for (int c = lane; c < n; c += 32) {
-                    const double2 b = rk[c];
+                    const double2 b = R0[c];
                     double2 v;
                     if (gi == k) {
                         v = (c == k) ? make_double2(ip, 0.0) : make_double2(b.x * ip, b.y * ip);
                     } else if (c == k) {
-                        v = make_double2(-a.x * ip, -a.y * ip);
+                        v = make_double2(-ca.x * ip, -ca.y * ip);
                     } else {
                         const double2 m = row[c];
-                        v = make_double2(m.x - (a.x * b.x - a.y * b.y) * ip, m.y - (a.x * b.y + a.y * b.x) * ip);
+                        const double2 t = cm(ca, b);
+                        v = make_double2(m.x - t.x * ip, m.y - t.y * ip);
                     }
                     row[c] = v;
                 }
             }
+        } else {
+            // P = [[a, b], [conj(b), d]], P^-1 = [[d, -b], [-conj(b), a]] / det
+            const double det = a * d - (bb.x * bb.x + bb.y * bb.y);
+            const double id = 1.0 / det;
+            const double2 P00 = make_double2(d * id, 0.0), P11 = make_double2(a * id, 0.0);
+            const double2 P01 = make_double2(-bb.x * id, -bb.y * id), P10 = make_double2(-bb.x * id, bb.y * id);
+            for (int i = warp; i < nr; i += NWI) {
+                const int gi = i0 + i;
+                double2* row = Ml + (size_t)i * n;
+                if (gi == k || gi == k + 1) {
+                    const double2 Q0 = gi == k ? P00 : P10, Q1 = gi == k ? P01 : P11;
+                    for (int c = lane; c < n; c += 32) {
+                        double2 v;
+                        if (c == k) v = Q0;
+                        else if (c == k + 1) v = Q1;
+                        else {
+                            const double2 u0 = cm(Q0, R0[c]), u1 = cm(Q1, R1[c]);
+                            v = make_double2(u0.x + u1.x, u0.y + u1.y);
+                        }
+                        row[c] = v;
+                    }
+                } else {
+                    const double2 C0 = colk[2 * i], C1 = colk[2 * i + 1];
+                    const double2 a0 = cm(C0, P00), a1 = cm(C1, P10), b0 = cm(C0, P01), b1 = cm(C1, P11);
+                    const double2 T0 = make_double2(a0.x + a1.x, a0.y + a1.y);
+                    const double2 T1 = make_double2(b0.x + b1.x, b0.y + b1.y);
+                    for (int c = lane; c < n; c += 32) {
+                        double2 v;
+                        if (c == k) v = make_double2(-T0.x, -T0.y);
+                        else if (c == k + 1) v = make_double2(-T1.x, -T1.y);
+                        else {
+                            const double2 m = row[c];
+                            const double2 u0 = cm(T0, R0[c]), u1 = cm(T1, R1[c]);
+                            v = make_double2(m.x - u0.x - u1.x, m.y - u0.y - u1.y);
+                        }
+                        row[c] = v;
+                    }
+                }
+            }
         }
         __syncthreads();
+        k += two ? 2 : 1;
         par ^= 1;
-        publish(k + 1, par);
+        publish(k, par);
         cl.sync();
     }
     for (int t = threadIdx.x; t < nr * n; t += INV_THREADS) M[(int64_t)i0 * n + t] = Ml[t];
@@ -2203,7 +2264,7 @@ int build_coarse(SolveSystem* S, int csize, cudaStream_t s) {
         int CS = 1;
         auto inv_smem = [&](int cs) {
             int rpc = (nmax + cs - 1) / cs;
-            return (size_t)rpc * nmax * 16 + (size_t)2 * nmax * 16 + (size_t)rpc * 16 + (size_t)nmax * 8 + 64;
+            return (size_t)rpc * nmax * 16 + (size_t)4 * nmax * 16 + (size_t)2 * rpc * 16 + (size_t)nmax * 8 + 64;
         };
         while (CS < 16 && inv_smem(CS) > 200 * 1024) CS *= 2;
         const size_t smem = inv_smem(CS);
