@@ -252,11 +252,20 @@ def parameterize(mesh, cuts=None, mode="free", workers=1, seed=0, mobius_area=Fa
     # host-side weld planning (planner.cpp, weld plan) overlapped on this thread
     clk.start()
     fres = {}
+    # the flatten runs on a high-priority stream; the harmonic system (which
+    # depends only on which vertices are fixed) is prepared meanwhile on a
+    # normal-priority stream, on the SMs the flatten's cluster waves leave idle
+    hi, lo = _streams(dev)
+    cur = torch.cuda.current_stream()
+    hi.wait_stream(cur)
+    lo.wait_stream(cur)
+    overlap_prep = welds and os.environ.get("PGCP_OVERLAP_HPREP", "1") != "0"
 
     def _flatten():
         try:
             torch.cuda.set_device(dev)  # the current device is per host thread
-            fres["out"] = batch.flatten(comps=own, rtol=cfg.rtol, cluster=cfg.cluster)
+            with torch.cuda.stream(hi):
+                fres["out"] = batch.flatten(comps=own, rtol=cfg.rtol, cluster=cfg.cluster)
         except BaseException as exc:  # re-raised on the caller's thread
             fres["err"] = exc
 
@@ -270,10 +279,18 @@ def parameterize(mesh, cuts=None, mode="free", workers=1, seed=0, mobius_area=Fa
         if welds:
             plan = WeldPlan(cycles, steps, mesh.n_vertices)
             loop_gid_host = (voff[plan.slot_sub] + loop_local).astype(np.int32)
+        timings["plan (overlapped)"] = time.perf_counter() - t_plan
+        if overlap_prep:
+            t_h = time.perf_counter()
+            with torch.cuda.stream(lo):
+                loop_gid = torch.as_tensor(loop_gid_host).to(dev)
+                batch.harmonic_prepare(loop_gid, comps=own, rtol=cfg.rtol, cluster=cfg.cluster, stream=lo)
+            timings["harmonic prepare (overlapped)"] = time.perf_counter() - t_h
     except BaseException as exc:
         perr = exc
-    timings["plan (overlapped)"] = time.perf_counter() - t_plan
     worker.join()
+    cur.wait_stream(hi)
+    cur.wait_stream(lo)
     if "err" in fres:
         raise fres["err"]
     if perr is not None:
@@ -289,7 +306,8 @@ def parameterize(mesh, cuts=None, mode="free", workers=1, seed=0, mobius_area=Fa
     else:
         # ---- welding on tracked boundary values ---------------------------------
         clk.start()
-        loop_gid = torch.as_tensor(loop_gid_host).to(dev)
+        if not overlap_prep:
+            loop_gid = torch.as_tensor(loop_gid_host).to(dev)
         tv = torch.empty(len(plan.slot_parent), dtype=torch.complex128, device=dev)
         nat.check(nat.lib().pgcp_gather_complex(_ptr(z0), _ptr(loop_gid), _ptr(tv), tv.numel(), _stream()))
         if own is not None:
@@ -323,9 +341,10 @@ def parameterize(mesh, cuts=None, mode="free", workers=1, seed=0, mobius_area=Fa
             ext_slots = torch.as_tensor(plan.slots_of(exterior).astype(np.int32)).to(dev)
             nat.check(nat.lib().pgcp_inv_shift(_ptr(tv), _ptr(ext_slots), ext_slots.numel(), 0.0, 0.0,
                                                center.real, center.imag, _stream()))
-        # (building the harmonic system on a side stream during the weld was
-        # measured slower: its kernels and the weld's serial chain contend)
-        z, hst = batch.harmonic(loop_gid, tv, comps=own, rtol=cfg.rtol, cluster=cfg.cluster)
+        if overlap_prep:
+            z, hst = batch.harmonic_solve(tv, rtol=cfg.rtol, cluster=cfg.cluster)
+        else:
+            z, hst = batch.harmonic(loop_gid, tv, comps=own, rtol=cfg.rtol, cluster=cfg.cluster)
         report.solver["harmonic_iters"] = [s["iters"] for s in hst]
         report.solver["harmonic"] = batch.last_solve(1)
         if own is not None:
@@ -349,6 +368,19 @@ def parameterize(mesh, cuts=None, mode="free", workers=1, seed=0, mobius_area=Fa
         report.repairs = [{"flips_before": int(per[i]), "repair_iterations": 0, "cleared": bool(per[i] == 0),
                            "submesh": i} for i in range(K)]
     return _finish(mesh, batch, embeddings, gp, report, cfg, clk)
+
+
+_STREAMS = {}
+
+
+def _streams(dev):
+    """(high-priority, normal-priority) streams per device, kept for the life
+    of the process (scratch allocated on them is freed on them)."""
+    key = dev.index if dev.index is not None else torch.cuda.current_device()
+    if key not in _STREAMS:
+        lo_p, hi_p = torch.cuda.Stream.priority_range()
+        _STREAMS[key] = (torch.cuda.Stream(device=dev, priority=hi_p), torch.cuda.Stream(device=dev, priority=lo_p))
+    return _STREAMS[key]
 
 
 def _geodesic_boundary(plan, tv, gc):
