@@ -34,6 +34,8 @@
 
 #include <algorithm>
 #include <chrono>
+#include <climits>
+#include <cstring>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -92,6 +94,8 @@ struct SolveSystem {
 };
 
 void free_system(void* p) { delete static_cast<SolveSystem*>(p); }
+
+static std::vector<int32_t> g_prev_iters;  // PGCP_PCG_ORDER=prev (launch-order experiment)
 
 namespace {
 
@@ -1147,6 +1151,7 @@ struct PcgArgs {
     int32_t maxit;
     int32_t chunk_cap;       // slices per CTA the smem was sized for
     long long* timing;       // optional: per CTA [phaseA, red1, phaseB, red2] cycles (iterations 64..191)
+    const int32_t* order;    // k_pcg2: cluster -> slot launch order (nullptr: identity)
     CoarseArgs C;
 };
 
@@ -1460,8 +1465,10 @@ __global__ void __launch_bounds__(NT, 1) k_pcg2(PcgArgs A) {
     cg::cluster_group cl = cg::this_cluster();
     const int csize = (int)cl.num_blocks();
     const int rank = (int)cl.block_rank();
-    const int slot = blockIdx.x / csize;
+    const int slot = A.order ? A.order[blockIdx.x / csize] : (int)(blockIdx.x / csize);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned long long t_start = 0;
+    if (A.timing) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
 
     const int64_t s0 = A.sl_off[slot];
     const int S = (int)(A.sl_off[slot + 1] - s0);
@@ -1807,8 +1814,13 @@ __global__ void __launch_bounds__(NT, 1) k_pcg2(PcgArgs A) {
                 tm[5] += c6 - c5;
             }
         }
-        if (A.timing && threadIdx.x == 0)
+        if (A.timing && threadIdx.x == 0) {
             for (int q = 0; q < 6; ++q) A.timing[8 * blockIdx.x + q] = tm[q];
+            unsigned long long t_end;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+            A.timing[8 * blockIdx.x + 6] = (long long)t_start;
+            A.timing[8 * blockIdx.x + 7] = (long long)t_end;
+        }
         // the last update y += alpha p
         {
             for (int i = threadIdx.x; i < 32 * nloc; i += NT) {
@@ -2544,6 +2556,22 @@ int run_solve(pgcp_batch* b, SolveSystem* S, const pgcp_solve_opts* o, double* z
     A.C.p = S->p.p;
     DevBuf<long long> tbuf;
     A.timing = nullptr;
+    A.order = nullptr;
+    DevBuf<int32_t> dorder;
+    std::vector<int32_t> hord(nslot);
+    for (int j = 0; j < nslot; ++j) hord[j] = j;
+    if (S->coarse && !S->force_jacobi) {
+        const char* eo = getenv("PGCP_PCG_ORDER");
+        if (eo && !strcmp(eo, "prev") && (int)g_prev_iters.size() == nslot)
+            std::stable_sort(hord.begin(), hord.end(), [](int a, int b) { return g_prev_iters[a] > g_prev_iters[b]; });
+        else if (eo && !strcmp(eo, "rev"))
+            std::reverse(hord.begin(), hord.end());
+        if (eo) {
+            PGCP_TRY(dorder.alloc(nslot, s));
+            PGCP_TRY_CUDA(cudaMemcpyAsync(dorder.p, hord.data(), nslot * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+            A.order = dorder.p;
+        }
+    }
     const bool want_timing = getenv("PGCP_PCG_TIMING") != nullptr;
     if (want_timing) {
         PGCP_TRY(tbuf.alloc(8 * (int64_t)nslot * csize, s));
@@ -2593,6 +2621,7 @@ int run_solve(pgcp_batch* b, SolveSystem* S, const pgcp_solve_opts* o, double* z
     PGCP_TRY_CUDA(cudaMemcpyAsync(hit.data(), S->iters.p, nslot * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     PGCP_TRY_CUDA(cudaMemcpyAsync(hres.data(), S->res.p, 8 * nslot * sizeof(double), cudaMemcpyDeviceToHost, s));
     PGCP_TRY_CUDA(cudaStreamSynchronize(s));
+    if (S->coarse && !S->force_jacobi) g_prev_iters = hit;
     if (want_timing)
         fprintf(stderr, "[pcg timing] post-solve (true residual, scatter, checks, stats) %.2f ms\n",
                 1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - t_post).count());
@@ -2602,6 +2631,38 @@ int run_solve(pgcp_batch* b, SolveSystem* S, const pgcp_solve_opts* o, double* z
         double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         for (size_t i = 0; i < ht.size(); ++i) acc[i % 8] += (double)ht[i];
         double nct = (double)nslot * csize * 128.0;
+        if (S->coarse) {
+            // timeline: per cluster [first CTA start, last CTA end] (globaltimer ns)
+            long long t0 = LLONG_MAX, t1 = 0;
+            double busy = 0;
+            int late = -1;
+            long long late_end = 0;
+            for (int c = 0; c < nslot; ++c) {
+                long long cs = LLONG_MAX, ce = 0;
+                for (int r = 0; r < csize; ++r) {
+                    cs = std::min(cs, ht[8 * (size_t)(c * csize + r) + 6]);
+                    ce = std::max(ce, ht[8 * (size_t)(c * csize + r) + 7]);
+                }
+                t0 = std::min(t0, cs);
+                t1 = std::max(t1, ce);
+                busy += (double)(ce - cs);
+                if (ce > late_end) { late_end = ce; late = c; }
+            }
+            int first_wave = 0;
+            long long last_start = 0;
+            for (int c = 0; c < nslot; ++c) {
+                long long cs = LLONG_MAX;
+                for (int r = 0; r < csize; ++r) cs = std::min(cs, ht[8 * (size_t)(c * csize + r) + 6]);
+                if (cs - t0 < 50000) ++first_wave;
+                last_start = std::max(last_start, cs - t0);
+            }
+            long long ls = LLONG_MAX;
+            for (int r = 0; r < csize; ++r) ls = std::min(ls, ht[8 * (size_t)(late * csize + r) + 6]);
+            fprintf(stderr, "[pcg timing] timeline: makespan %.2f ms, cluster-busy sum %.1f ms (mean %.1f concurrent), "
+                    "%d clusters in the first wave, last start %.2f ms; last to finish: cluster %d (slot %d, %d iters) "
+                    "started %.2f ms\n", 1e-6 * (t1 - t0), 1e-6 * busy, busy / (double)(t1 - t0), first_wave,
+                    1e-6 * last_start, late, hord[late], hit[hord[late]], 1e-6 * (ls - t0));
+        }
         if (S->coarse)
             fprintf(stderr, "[pcg timing] cycles/iter per CTA: A %.0f sync1 %.0f B %.0f sync2 %.0f C %.0f sync3 %.0f "
                     "(csize %d, coarse setup %.2f ms)\n", acc[0] / nct, acc[1] / nct, acc[2] / nct, acc[3] / nct,

@@ -449,7 +449,33 @@ struct Phase1Args {
     Rec* recs;
     double* meta;
     int geodesic;           // unused here
+    int* prog;              // per step [2]: records published per log (streamed replay), or nullptr
+    int prog_every;         // publish the counters every this many logged steps
 };
+
+// Streamed replay (k_replay_stream): phase 1 publishes, per step and log, the
+// number of records written so far; the replay of the same level runs
+// concurrently (programmatic dependent launch) and applies records as they
+// appear. Counter word: bits 0..28 count, bit 30 = the step has finished
+// (its meta is final). The logger orders its record / meta stores before the
+// counter with a gpu-scope release fence.
+constexpr int PROG_DONE = 1 << 30;
+constexpr int PROG_TIMEOUT = 1 << 29;
+constexpr int PROG_COUNT = (1 << 29) - 1;
+
+__device__ __forceinline__ void prog_store(int* p, int v) {
+    asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int prog_load(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 __device__ void block_fail(int* s_err, int code, int idx, int aux, double* meta) {
     if (atomicCAS(s_err, 0, code) == 0) {
@@ -583,7 +609,18 @@ __global__ void __launch_bounds__(NT, 1) k_phase1c(Phase1Args A) {
     Rec* log_a = A.recs + sd.rec;
     Rec* log_b = log_a + sd.cap;
     const bool logger = rank == 0 && threadIdx.x == 0;
-    int na_rec = 0, nb_rec = 0;
+    int na_rec = 0, nb_rec = 0, nlogged = 0;
+    // every CTA of this grid is resident from here on: the streamed replay
+    // (secondary launch) may start and wait on the counters
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    int* prog = A.prog ? A.prog + 2 * step : nullptr;
+    auto progress = [&](bool fin) {
+        if (!logger || !prog) return;
+        if (!fin && (++nlogged % A.prog_every) != 0) return;
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        prog_store(prog, na_rec | (fin ? PROG_DONE : 0));
+        prog_store(prog + 1, nb_rec | (fin ? PROG_DONE : 0));
+    };
     if (logger)
         for (int i = 0; i < META; ++i) meta[i] = 0.0;
     if (k < 1 || k > sd.na - 1 || k > sd.nb - 1) {
@@ -591,6 +628,7 @@ __global__ void __launch_bounds__(NT, 1) k_phase1c(Phase1Args A) {
             meta[2] = WE_K;
             meta[3] = k;
         }
+        progress(true);
         return;
     }
     const int32_t* sa = A.src + sd.src;
@@ -606,6 +644,7 @@ __global__ void __launch_bounds__(NT, 1) k_phase1c(Phase1Args A) {
             meta[3] = okA ? 1 : 0;
             meta[4] = pcode;
         }
+        progress(true);
         return;
     }
     for (int g = lo + threadIdx.x; g < hi; g += NT) {
@@ -629,6 +668,7 @@ __global__ void __launch_bounds__(NT, 1) k_phase1c(Phase1Args A) {
         log_a[na_rec++] = pre[0];
         log_b[nb_rec++] = pre[1];
     }
+    progress(false);
     int parity = 0;
     // publish the listed global points into every CTA's slots, then barrier
     // the thread that owns point g (the one that last wrote it) sends it, so
@@ -684,6 +724,7 @@ __global__ void __launch_bounds__(NT, 1) k_phase1c(Phase1Args A) {
         log_a[na_rec++] = ra;
         log_b[nb_rec++] = rb;
     }
+    progress(false);
     apply_pair(ra, true, rb, true);
     // ---- zip steps j = 2..k: Open
     for (int j = 2; j <= k; ++j) {
@@ -708,6 +749,7 @@ __global__ void __launch_bounds__(NT, 1) k_phase1c(Phase1Args A) {
             log_a[na_rec++] = ra;
             log_b[nb_rec++] = rb;
         }
+        progress(false);
         apply_pair(ra, true, rb, true);
     }
     // ---- axis Mobius sending pts[0] to infinity (welding.py:593-600)
@@ -740,6 +782,7 @@ __global__ void __launch_bounds__(NT, 1) k_phase1c(Phase1Args A) {
             if (has[0]) log_a[na_rec++] = rr0;
             if (has[1]) log_b[nb_rec++] = rr1;
         }
+        progress(false);
         apply_pair(rr0, has[0], rr1, has[1]);
     }
     // ---- closing loop (welding.py:673-687)
@@ -762,6 +805,7 @@ __global__ void __launch_bounds__(NT, 1) k_phase1c(Phase1Args A) {
             log_a[na_rec++] = ra;
             log_b[nb_rec++] = ra;
         }
+        progress(false);
         apply_pair(ra, true, ra, true);
     }
     // ---- far ends: SquareMobius; stage max of |va| (arc + aux) for the deferred check
@@ -788,6 +832,7 @@ __global__ void __launch_bounds__(NT, 1) k_phase1c(Phase1Args A) {
             log_a[na_rec++] = ra;
             log_b[nb_rec++] = ra;
         }
+        progress(false);
         apply_pair(ra, true, ra, true);
     }
     // ---- normalisation (welding.py:699-717)
@@ -817,6 +862,7 @@ __global__ void __launch_bounds__(NT, 1) k_phase1c(Phase1Args A) {
             log_a[na_rec++] = ra;
             log_b[nb_rec++] = ra;
         }
+        progress(false);
         apply_pair(ra, true, ra, true);
     }
     // ---- closed welding: respread the seam (welding.py:751-763)
@@ -836,11 +882,13 @@ __global__ void __launch_bounds__(NT, 1) k_phase1c(Phase1Args A) {
             log_a[na_rec++] = ra;
             log_b[nb_rec++] = ra;
         }
+        progress(false);
         for (int g = lo + threadIdx.x; g < hi; g += NT) sides[g - lo] = 0;
         apply_pair(ra, true, ra, true);
     }
     // ---- outputs: all 2P points to arc_out; rank 0 finishes seam/maxima/area
     for (int g = lo + threadIdx.x; g < hi; g += NT) A.arc_out[sd.arc + g] = pts[g - lo];
+    if (prog) __threadfence();  // arc_out is read by the streamed replay after the final counter
     cl.sync();
     if (rank == 0) {
         const double2* o = A.arc_out + sd.arc;
@@ -880,6 +928,7 @@ __global__ void __launch_bounds__(NT, 1) k_phase1c(Phase1Args A) {
                 meta[4] = 3;
             }
         }
+        progress(true);
     }
     return;
 fail:
@@ -888,6 +937,7 @@ fail:
         meta[3] = eidx;
         meta[4] = eaux;
     }
+    progress(true);
 }
 
 // ---------------------------------------------------------------------------
@@ -940,6 +990,72 @@ __global__ void k_replay_slots(ReplayArgs A) {
         }
         if (cycB) atomicMax(&A.maxbits[3 * step + 2], (unsigned long long)__double_as_longlong(fin));
     }
+}
+
+// the same replay, streamed: launched as the programmatic dependent of the
+// level's phase 1, it applies each record as soon as the step's counter covers
+// it. A wait longer than 2 s (phase 1 of the largest level takes ~5 ms) flags
+// an internal error instead of hanging.
+__device__ int wait_prog(const int* p, int need, int* timeout_flag) {
+    int v = prog_load(p);
+    if ((v & PROG_COUNT) >= need || (v & PROG_DONE)) return v;
+    const unsigned long long t0 = gtimer();
+    for (;;) {
+        __nanosleep(256);
+        v = prog_load(p);
+        if ((v & PROG_COUNT) >= need || (v & PROG_DONE)) return v;
+        if (gtimer() - t0 > 2000000000ull) {
+            atomicExch(timeout_flag, 1);
+            return PROG_DONE | PROG_TIMEOUT;
+        }
+    }
+}
+
+__global__ void k_replay_stream(ReplayArgs A, const int* __restrict__ prog, int* timeout_flag) {
+    GRID_STRIDE(i, A.nwb) {
+        int slot = A.wb[3 * i], code = A.wb[3 * i + 1], step = A.wb[3 * i + 2];
+        const StepDesc sd = A.steps[step];
+        int arcpos = (code & 0xffffff) - 1;
+        bool sideB = (code >> 31) & 1;
+        const int* pg = prog + 2 * step + (sideB ? 1 : 0);
+        const double* meta = A.meta + META * (int64_t)step;
+        if (arcpos >= 0) {
+            int v = wait_prog(pg, PROG_COUNT, timeout_flag);
+            if ((v & PROG_TIMEOUT) || __ldcg(meta + 2) != 0.0) continue;
+            bool fromB = (code >> 24) & 1;
+            A.tv[slot] = __ldcg(A.arc_out + sd.arc + (fromB ? sd.k + 3 : 0) + arcpos);
+            continue;
+        }
+        const Rec* log = A.recs + sd.rec + (sideB ? sd.cap : 0);
+        double2 z = A.tv[slot];
+        int8_t s = 0;
+        double stage = 0;
+        int avail = 0, sq = 0, v = 0;
+        for (int r = 0;; ++r) {
+            if (r >= avail) {
+                if (v & PROG_DONE) break;
+                v = wait_prog(pg, r + 1, timeout_flag);
+                avail = v & PROG_COUNT;
+                if (r >= avail) break;  // finished (or failed / timed out) with fewer records
+            }
+            if (sq == 0) sq = (int)__ldcg(meta + (sideB ? 15 : 14));  // known before record sq is published
+            if (sq > 0 && r == sq) stage = c_fin(z) ? cabs_(z) : 0.0;
+            apply_rec(log[r], z, s);
+        }
+        if (!(v & PROG_DONE)) v = wait_prog(pg, PROG_COUNT, timeout_flag);
+        if ((v & PROG_TIMEOUT) || __ldcg(meta + 2) != 0.0) continue;  // failed step: leave values
+        if (c_nan(z)) atomicExch(A.nan_flag, 1);
+        A.tv[slot] = z;
+        bool cycA = (code >> 25) & 1, cycB = (code >> 26) & 1;
+        double fin = c_fin(z) ? cabs_(z) : 0.0;
+        if (cycA) {
+            atomicMax(&A.maxbits[3 * step + 0], (unsigned long long)__double_as_longlong(stage));
+            atomicMax(&A.maxbits[3 * step + 1], (unsigned long long)__double_as_longlong(fin));
+        }
+        if (cycB) atomicMax(&A.maxbits[3 * step + 2], (unsigned long long)__double_as_longlong(fin));
+    }
+    // completion of this grid implies completion of the level's phase 1
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 // generic replay: log on a point array (apply_log, welding.py:512-526)
@@ -1347,6 +1463,16 @@ int run_schedule(double2* tv, int32_t nsteps, const int32_t* info, const int32_t
     PGCP_TRY(d_max.zero(s));
     PGCP_TRY(d_nan.alloc(1, s));
     PGCP_TRY(d_nan.zero(s));
+    // streamed replay (default): each level's replay runs concurrently with
+    // its phase 1 (PGCP_WELD_STREAM=0: after it)
+    const bool streamed = env_int("PGCP_WELD_STREAM", 1) != 0;
+    DevBuf<int> d_prog, d_tmo;
+    if (streamed) {
+        PGCP_TRY(d_prog.alloc(2 * (int64_t)nsteps, s));
+        PGCP_TRY(d_prog.zero(s));
+        PGCP_TRY(d_tmo.alloc(1, s));
+        PGCP_TRY(d_tmo.zero(s));
+    }
     PGCP_TRY_CUDA(cudaMemcpyAsync(d_sd.p, sd.data(), nsteps * sizeof(StepDesc), cudaMemcpyHostToDevice, s));
     PGCP_TRY_CUDA(cudaMemcpyAsync(d_src.p, src, src_off[nsteps] * sizeof(int32_t), cudaMemcpyHostToDevice, s));
     PGCP_TRY_CUDA(cudaMemcpyAsync(d_wb.p, wb3.data(), 3 * nwb * sizeof(int32_t), cudaMemcpyHostToDevice, s));
@@ -1362,6 +1488,8 @@ int run_schedule(double2* tv, int32_t nsteps, const int32_t* info, const int32_t
         a.recs = d_recs.p;
         a.meta = d_meta.p + (int64_t)META * q0;
         a.geodesic = 0;
+        a.prog = streamed ? d_prog.p + 2 * q0 : nullptr;
+        a.prog_every = std::max(1, env_int("PGCP_WELD_PROG_EVERY", 8));
         int kmax = 0;
         for (int q = q0; q < q1; ++q) kmax = std::max(kmax, sd[q].k);
         const int NP = 2 * (kmax + 3);
@@ -1402,8 +1530,23 @@ int run_schedule(double2* tv, int32_t nsteps, const int32_t* info, const int32_t
             r.meta = d_meta.p;
             r.maxbits = d_max.p;
             r.nan_flag = d_nan.p;
-            k_replay_slots<<<grid_for(n, 128), 128, 0, s>>>(r);
-            PGCP_LAUNCH_CHECK();
+            if (streamed) {
+                cudaLaunchConfig_t rc = {};
+                rc.gridDim = dim3((unsigned)grid_for(n, 128), 1, 1);
+                rc.blockDim = dim3(128, 1, 1);
+                rc.dynamicSmemBytes = 0;
+                rc.stream = s;
+                cudaLaunchAttribute ra[1];
+                ra[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+                ra[0].val.programmaticStreamSerializationAllowed = 1;
+                rc.attrs = ra;
+                rc.numAttrs = 1;
+                PGCP_TRY_CUDA(cudaLaunchKernelEx(&rc, k_replay_stream, r, (const int*)d_prog.p, d_tmo.p));
+                count_launch();
+            } else {
+                k_replay_slots<<<grid_for(n, 128), 128, 0, s>>>(r);
+                PGCP_LAUNCH_CHECK();
+            }
         }
         q0 = q1;
     }
@@ -1413,6 +1556,8 @@ int run_schedule(double2* tv, int32_t nsteps, const int32_t* info, const int32_t
     PGCP_TRY_CUDA(cudaMemcpyAsync(meta.data(), d_meta.p, meta.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
     PGCP_TRY_CUDA(cudaMemcpyAsync(mx.data(), d_max.p, mx.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     PGCP_TRY_CUDA(cudaMemcpyAsync(&hnan, d_nan.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    int htmo = 0;
+    if (streamed) PGCP_TRY_CUDA(cudaMemcpyAsync(&htmo, d_tmo.p, sizeof(int), cudaMemcpyDeviceToHost, s));
     if (recs_host && recs_cap_total >= rec_tot)
         PGCP_TRY_CUDA(cudaMemcpyAsync(recs_host, d_recs.p, rec_tot * sizeof(Rec), cudaMemcpyDeviceToHost, s));
     PGCP_TRY_CUDA(cudaStreamSynchronize(s));
@@ -1457,6 +1602,10 @@ int run_schedule(double2* tv, int32_t nsteps, const int32_t* info, const int32_t
             status = PGCP_E_WELD;
             set_error("weld step %d: %s", i, msg.c_str());
         }
+    }
+    if (htmo) {
+        set_error("internal: streamed weld replay timed out waiting for phase 1");
+        return PGCP_E_CUDA;
     }
     if (status == PGCP_OK && hnan) {
         set_error("numerical breakdown (NaN) during apply_log");

@@ -136,3 +136,33 @@ def test_two_level_falls_back_to_jacobi(cuda, monkeypatch):
     ref = z["coords"]
     assert np.max(np.abs(np.asarray(gp.coords) - ref)) <= 1e-6 * _diam(ref)
     assert max(rep.solver["flatten_iters"]) > 5
+
+
+@pytest.mark.parametrize("every", ["1", "3", "64"])
+def test_streamed_replay_equals_serial_replay(cuda, monkeypatch, every):
+    """The streamed weld replay runs concurrently with phase 1 and applies
+    each record once its counter covers it. It must give the serial replay's
+    result bit for bit, whatever the counter publishing interval."""
+    from paper_1903_12359_b200 import TriMesh, parameterize
+    z = load_golden("qtree4x4")
+    mesh = TriMesh(z["V"], z["F"])
+    kw = {"pairs": case_pairs("qtree4x4")}
+    monkeypatch.setenv("PGCP_WELD_STREAM", "0")
+    g0, r0 = parameterize(mesh, z["cuts"], str(z["mode"]), **kw)
+    monkeypatch.setenv("PGCP_WELD_STREAM", "1")
+    monkeypatch.setenv("PGCP_WELD_PROG_EVERY", every)
+    g1, r1 = parameterize(mesh, z["cuts"], str(z["mode"]), **kw)
+    assert np.array_equal(g0.coords, g1.coords)
+    assert r0.seam_residuals == r1.seam_residuals
+
+
+def test_streamed_replay_failed_step(cuda, monkeypatch):
+    """A weld step that fails in phase 1 publishes its final counter; the
+    streamed replay leaves its points alone and the error surfaces as in
+    the serial replay."""
+    from paper_1903_12359_b200 import WeldError, partial_weld
+    a = np.array([0, 1, 1 + 1j, 1j], dtype=complex)
+    for mode in ("0", "1"):
+        monkeypatch.setenv("PGCP_WELD_STREAM", mode)
+        with pytest.raises(WeldError, match="zip points 0 and 1 coincide"):
+            partial_weld(np.array([0, 0, 1 + 1j, 1j]), a, 2)

@@ -21,6 +21,8 @@ for r in range(reps):
     z, st = b.flatten(cluster=int(os.environ.get("CLUSTER", "0")))
     torch.cuda.synchronize()
     print("flatten", round(1e3 * (time.perf_counter() - t0), 2), "ms", b.last_solve(0), flush=True)
+    if r == 0 and os.environ.get("ITERS"):
+        print("iters by slot", [s["iters"] for s in st], flush=True)
 if os.environ.get("HARMONIC"):
     loop_gid = []
     voff = b.host(nat.ARR_VERT_OFF, torch.int64)
