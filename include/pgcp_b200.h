@@ -194,6 +194,44 @@ PGCP_API int pgcp_batch_export_system(pgcp_batch* b, int which, int32_t comp, in
 PGCP_API int pgcp_batch_conformal_energy(pgcp_batch* b, const double* z, double* energy, void* stream);
 
 /* -------------------------------------------------------------------------
+ * Quasi-conformal fold-over repair (assemble.py:53-217)
+ */
+/* face_layout (assemble.py:53-67): isometric 2D corners of every face, corner
+ * 0 at the origin, corner 1 on the positive real axis.
+ *   V device f64 [3n]; F device int32 [3m]; layout device complex [3m]. */
+PGCP_API int pgcp_face_layout(const double* V, const int32_t* F, int64_t m, double* layout, void* stream);
+
+/* beltrami_per_face (assemble.py:74-92) of the piecewise-linear map src -> tgt.
+ * src/tgt are device complex per-vertex coordinates indexed through
+ * src_faces/tgt_faces (device int32 [3m]), or per-face corner arrays
+ * [3m] when the face pointer is NULL. mu device complex [m] (fz == 0 -> inf).
+ * A degenerate source triangle -> PGCP_E_SOLVE with its index in
+ * *first_degenerate (host, optional). Synchronises. */
+PGCP_API int pgcp_beltrami(const double* src, const int32_t* src_faces, const double* tgt, const int32_t* tgt_faces,
+                           int64_t m, double* mu, int64_t* first_degenerate, void* stream);
+
+/* qc_correct (assemble.py:174-217) of the listed submeshes, batched, in place:
+ * while a submesh has faces with signed area <= 0 (at most max_iter times):
+ * mu = capped Beltrami coefficient of embedding -> layout, K = linear
+ * Beltrami stiffness (lbs_stiffness, assemble.py:124-164, on the Laplacian's
+ * pattern), solve K_ff u = -K_f,fixed g with the held values g = z[fixed].
+ * The reference calls it per submesh after the harmonic solve
+ * (pipeline.py:88-102).
+ *   comps     host int32 [ncomp] (NULL: all submeshes)
+ *   layout    device complex [3m] per parent face, or NULL: face_layout of V
+ *   fixed_gid device int32 [nfixed] held local vertices (boundary loops)
+ *   z         device complex [sum_n] embeddings, updated in place
+ *   info      host int32 [4*ncomp]: flips before, iterations, cleared, flips after
+ *   flipped   device uint8 [m] (optional): parent faces of the listed
+ *             submeshes still folded at the end
+ * Synchronises. PGCP_E_SOLVE on a degenerate embedded triangle or a failed
+ * solve ("singular linear Beltrami system during repair"). */
+PGCP_API int pgcp_batch_qc_repair(pgcp_batch* b, const int32_t* comps, int32_t ncomp, const double* layout,
+                                  const int32_t* fixed_gid, int64_t nfixed, int32_t max_iter, double cap,
+                                  const pgcp_solve_opts* opts, double* z, int32_t* info, uint8_t* flipped,
+                                  void* stream);
+
+/* -------------------------------------------------------------------------
  * Boundary welding (welding.py:512-842), device resident.
  *
  * A map log is an array of records (welding.py:236-509):

@@ -15,6 +15,7 @@ import numpy as np
 from .assembly import distortion_summary, stitch
 from .laplace import conformal_energy, cotan_laplacian, dirichlet_extend, dncp_flatten
 from .planner import greedy_schedule, pair_schedule
+from .repair import isometric_layout, planar_flips, repair_folds
 from .surface import single_domain, split_mesh, topology_class
 from .zipper import closed_weld, geodesic_to_circle, interior_point, partial_weld, replay
 
@@ -29,12 +30,17 @@ def _flatten_job(args):
 
 
 def _harmonic_job(args):
-    V, F, loop, g = args
+    """`_harmonic_task` (pipeline.py:88-102): harmonic extension, flip check,
+    and the quasi-conformal repair of a folded submesh. Returns (z, info)."""
+    V, F, loop, g = args[:4]
+    repair_iters = args[4] if len(args) > 4 else 5
     z = dirichlet_extend(V, F, loop, g)
-    t = z[np.asarray(F)]
-    area = (t[:, 1] - t[:, 0]).real * (t[:, 2] - t[:, 0]).imag - \
-        (t[:, 1] - t[:, 0]).imag * (t[:, 2] - t[:, 0]).real
-    return z, int(np.sum(0.5 * area <= 0))
+    nf = len(planar_flips(z, F))
+    info = {"flips_before": nf, "repair_iterations": 0, "cleared": nf == 0}
+    if nf:
+        z, it, ok, left, n0 = repair_folds(isometric_layout(V, F), F, z, loop, max_iter=repair_iters)
+        info = {"flips_before": n0, "repair_iterations": it, "cleared": ok, "remaining": [int(x) for x in left]}
+    return z, info
 
 
 def _fan_out(fn, jobs, workers):
@@ -159,8 +165,12 @@ def run_parameterize(V, F, cuts=None, mode="free", workers=1, schedule="greedy",
                                         for i in range(part.n_sub)], workers)
         embeddings = []
         out["flips_before"] = []
-        for i, (z, nf) in enumerate(harm):
-            out["flips_before"].append(nf)
+        out["repairs"] = []
+        out["embeddings_local"] = []
+        for i, (z, info) in enumerate(harm):
+            out["flips_before"].append(info["flips_before"])
+            out["repairs"].append(info)
+            out["embeddings_local"].append(z)
             if i in ext:
                 z = center + 1.0 / z
             embeddings.append(z)

@@ -1,10 +1,13 @@
 """Interior reconstruction and global assembly (drop-in for `assemble.py`).
 
-`harmonic_solve` runs on the device (pcg.cu). The quasi-conformal repair
-(`assemble.py:105-217`) is out of scope: the pipeline reports
-flips instead of repairing them.
+`harmonic_solve` runs on the device (pcg.cu); the quasi-conformal fold-over
+repair (`face_layout`, `beltrami_per_face`, `qc_correct`,
+assemble.py:53-217) runs on the device as well (repair.cu), batched over
+every folded submesh by the pipeline; `stitch_global` is the device stitch
+(metrics.cu).
 """
 
+import ctypes
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -12,6 +15,8 @@ import torch
 
 from . import _native as nat
 from .errors import SolveError
+
+MU_CAP = 0.95  # assemble.py:20
 
 
 def harmonic_solve(mesh, boundary_idx, boundary_vals, residual_tol=1e-10, rtol=1e-10):
@@ -106,3 +111,138 @@ class GlobalParam:
     def uv(self):
         z = np.asarray(self.coords, dtype=np.complex128)
         return np.column_stack([z.real, z.imag])
+
+
+# ---------------------------------------------------------------------------
+# Fold-over repair (assemble.py:53-217), on the device
+
+
+def _stream():
+    from .device import stream_handle
+    return stream_handle()
+
+
+def _p(t):
+    from .device import ptr
+    return ptr(t)
+
+
+def face_layout(mesh):
+    """Isometric per-face 2D coordinates of a 3D mesh, (m, 3) complex: corner
+    0 at the origin, corner 1 on the positive real axis (assemble.py:53-67)."""
+    from .device import device, to_dev
+    V = to_dev(np.asarray(mesh.vertices, dtype=np.float64), torch.float64)
+    F = to_dev(np.asarray(mesh.faces), torch.int32)
+    m = int(F.shape[0])
+    out = torch.empty((m, 3), dtype=torch.complex128, device=device())
+    nat.check(nat.lib().pgcp_face_layout(_p(V), _p(F), m, _p(out), _stream()))
+    return out.cpu().numpy()
+
+
+def beltrami_per_face(source, target, faces=None):
+    """Per-face Beltrami coefficient of the piecewise-linear map source ->
+    target (assemble.py:74-92): per-vertex complex coordinates with `faces`,
+    or (m, 3) per-face corner arrays. SolveError on a degenerate source
+    triangle; fz == 0 gives inf."""
+    from .device import device, to_dev
+    src = to_dev(np.asarray(source, dtype=np.complex128).reshape(-1), torch.complex128)
+    tgt = to_dev(np.asarray(target, dtype=np.complex128).reshape(-1), torch.complex128)
+    if faces is not None:
+        fd = to_dev(np.asarray(faces), torch.int32).reshape(-1)
+        m = fd.numel() // 3
+        sf = tf = fd
+    else:
+        m = src.numel() // 3
+        sf = tf = None
+    mu = torch.empty(m, dtype=torch.complex128, device=device())
+    if m == 0:
+        return mu.cpu().numpy()
+    bad = ctypes.c_int64(-1)
+    nat.check(nat.lib().pgcp_beltrami(_p(src), _p(sf) if sf is not None else None, _p(tgt),
+                                      _p(tf) if tf is not None else None, m, _p(mu), ctypes.byref(bad), _stream()))
+    return mu.cpu().numpy()
+
+
+@dataclass
+class BijectivityReport:
+    bad_faces: np.ndarray
+    max_mu: float
+    threshold: float
+
+    @property
+    def ok(self):
+        return len(self.bad_faces) == 0
+
+
+def check_bijectivity(mu, threshold=0.99):
+    """Faces whose Beltrami magnitude reaches `threshold` (folded or nearly),
+    non-finite magnitudes counted as infinite (assemble.py:116-121)."""
+    mag = np.abs(np.asarray(mu))
+    mag[~np.isfinite(mag)] = np.inf
+    return BijectivityReport(np.flatnonzero(mag >= threshold), float(mag.max()) if mag.size else 0.0, threshold)
+
+
+@dataclass
+class RepairReport:
+    iterations: int
+    cleared: bool
+    remaining_faces: np.ndarray
+    initial_flips: int
+
+
+def qc_correct(layout, faces, embedding, fixed_idx, max_iter=5, cap=MU_CAP):
+    """Remove fold-overs from a planar embedding by quasi-conformal
+    composition (assemble.py:174-217), on the device: repeatedly solve the
+    linear Beltrami equation whose coefficient is the capped inverse Beltrami
+    coefficient (embedding -> layout), holding `fixed_idx` at the embedding's
+    values, until no face has signed area <= 0 or `max_iter` is reached.
+    Returns (embedding, RepairReport)."""
+    from .device import DeviceBatch, to_dev
+    emb = np.array(embedding, dtype=np.complex128)
+    F = np.asarray(faces)
+    fixed = np.asarray(fixed_idx, dtype=np.int64)
+    flips0 = int(np.count_nonzero(signed_areas(emb, F) <= 0))
+    if flips0 == 0:
+        return emb, RepairReport(0, True, np.array([], dtype=np.int64), 0)
+    lay = np.asarray(layout, dtype=np.complex128).reshape(-1, 3)
+    beltrami_per_face(emb[F], lay)  # the reference's first-iteration check: degenerate -> SolveError
+    n = len(emb)
+    V3 = np.column_stack([emb.real, emb.imag, np.zeros(n)])
+    b = DeviceBatch(V3, F, no_cuts=True)
+    if b.info()[nat.INFO_SUM_N] != n:
+        raise SolveError("singular linear Beltrami system during repair (unreferenced vertices)")
+    # single domain: local ids are parent ids (every vertex referenced)
+    z = to_dev(emb, torch.complex128)
+    rows, flipped = b.qc_repair(fixed.astype(np.int32), z, layout=lay, max_iter=max_iter, cap=cap,
+                                want_flipped=True)
+    _, iters, cleared, _ = rows[0]
+    remaining = np.flatnonzero(flipped.cpu().numpy()).astype(np.int64) if not cleared else \
+        np.array([], dtype=np.int64)
+    return z.cpu().numpy(), RepairReport(int(iters), bool(cleared), remaining, flips0)
+
+
+def stitch_global(partition, embeddings, mode, snap_tol=1e-8, hard_tol=1e-6, boundary_circle_tol=1e-9):
+    """Combine per-submesh embeddings into one coordinate per parent vertex
+    (assemble.py:286-337) with the device stitch: seam copies averaged and
+    checked against hard_tol x scale, disk boundary on the unit circle,
+    sphere finish, flips."""
+    from .device import device, to_dev
+    b = partition.batch
+    z = to_dev(np.concatenate([np.asarray(e, dtype=np.complex128) for e in embeddings]), torch.complex128)
+    dev = device()
+    n, m = b.n, b.m
+    coords = torch.empty(n, dtype=torch.complex128, device=dev)
+    sphere = torch.empty((n, 3), dtype=torch.float64, device=dev) if mode == "sphere" else None
+    prov = torch.empty(n, dtype=torch.int32, device=dev)
+    flip = torch.empty(m, dtype=torch.uint8, device=dev)
+    stats = np.zeros(8)
+    mcode = {"free": 0, "disk": 1, "sphere": 2}[mode]
+    nat.check(nat.lib().pgcp_batch_stitch(b.h, _p(z), mcode, hard_tol, boundary_circle_tol, _p(coords),
+                                          _p(sphere) if sphere is not None else None, _p(prov), _p(flip),
+                                          stats.ctypes.data, _stream()))
+    diag = {"seam_max_dev": float(stats[0]), "scale": float(stats[1])}
+    if mode == "disk":
+        diag["boundary_circle_dev"] = float(stats[2])
+    out = (sphere if mode == "sphere" else coords).cpu().numpy()
+    flipped = np.flatnonzero(flip.cpu().numpy()).astype(np.int64)
+    return GlobalParam(mode, out, flipped, prov.cpu().numpy().astype(np.int64), float(stats[0]), diag)

@@ -65,11 +65,21 @@ int finish_harmonic(pgcp_batch* b, const double* fixed_val, int64_t nfixed, cons
 int solve_harmonic(pgcp_batch* b, const int32_t* comps, int32_t ncomp, const int32_t* fixed_gid,
                    const double* fixed_val, int64_t nfixed, const pgcp_solve_opts* o, double* z,
                    pgcp_solve_stat* st, cudaStream_t s);
+int solve_values(pgcp_batch* b, const int32_t* comps, int32_t ncomp, const double* vals, const int32_t* fixed_gid,
+                 const double* fixed_val, int64_t nfixed, const pgcp_solve_opts* o, double* z, pgcp_solve_stat* st,
+                 cudaStream_t s);
 void free_system(void* p);
 void solve_summary(const pgcp_batch* b, int which, double* out8);
 unsigned long long launch_count();
 int export_system(pgcp_batch* b, int which, int32_t comp, int64_t* dims, int32_t* indptr,
                   int32_t* indices, double* data, double* rhs, cudaStream_t s);
+// repair.cu
+int face_layout(const double* V, const int32_t* F, int64_t m, double* out, cudaStream_t s);
+int beltrami_per_face(const double* src, const int32_t* sf, const double* tgt, const int32_t* tf, int64_t m,
+                      double* mu, int64_t* first_degenerate, cudaStream_t s);
+int qc_repair(pgcp_batch* b, const int32_t* comps, int32_t ncomp, const double* layout, const int32_t* fixed_gid,
+              int64_t nfixed, int32_t max_iter, double cap, const pgcp_solve_opts* o, double* z, int32_t* info,
+              uint8_t* flipped, cudaStream_t s);
 // metrics.cu
 int stitch(pgcp_batch* b, const double* z, double* coords, double* stats, cudaStream_t s);
 }  // namespace pgcp

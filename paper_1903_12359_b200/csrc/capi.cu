@@ -242,4 +242,36 @@ int pgcp_batch_conformal_energy(pgcp_batch* b, const double* z, double* energy, 
     return conformal_energy(b, z, energy, as_stream(stream));
 }
 
+int pgcp_face_layout(const double* V, const int32_t* F, int64_t m, double* layout, void* stream) {
+    if (m < 0 || (m > 0 && (!V || !F || !layout))) {
+        set_error("pgcp_face_layout: invalid arguments");
+        return PGCP_E_INVALID;
+    }
+    PGCP_TRY(set_device_of(V));
+    return face_layout(V, F, m, layout, as_stream(stream));
+}
+
+int pgcp_beltrami(const double* src, const int32_t* src_faces, const double* tgt, const int32_t* tgt_faces,
+                  int64_t m, double* mu, int64_t* first_degenerate, void* stream) {
+    if (m < 0 || (m > 0 && (!src || !tgt || !mu))) {
+        set_error("pgcp_beltrami: invalid arguments");
+        return PGCP_E_INVALID;
+    }
+    PGCP_TRY(set_device_of(src));
+    return beltrami_per_face(src, src_faces, tgt, tgt_faces, m, mu, first_degenerate, as_stream(stream));
+}
+
+int pgcp_batch_qc_repair(pgcp_batch* b, const int32_t* comps, int32_t ncomp, const double* layout,
+                         const int32_t* fixed_gid, int64_t nfixed, int32_t max_iter, double cap,
+                         const pgcp_solve_opts* opts, double* z, int32_t* info, uint8_t* flipped, void* stream) {
+    if (!b || !z || !info || ncomp < 0 || nfixed < 0 || (nfixed > 0 && !fixed_gid) || max_iter < 0 ||
+        !(cap > 0.0 && cap < 1.0)) {
+        set_error("pgcp_batch_qc_repair: invalid arguments");
+        return PGCP_E_INVALID;
+    }
+    PGCP_TRY_CUDA(cudaSetDevice(b->device));
+    return qc_repair(b, comps, ncomp, layout, fixed_gid, nfixed, max_iter, cap, opts, z, info, flipped,
+                     as_stream(stream));
+}
+
 }  // extern "C"

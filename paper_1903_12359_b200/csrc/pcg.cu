@@ -89,6 +89,8 @@ struct SolveSystem {
     DevBuf<double2> einv64;       // ... or fp64 (PGCP_COARSE_FP64=1)
     DevBuf<int64_t> eoff32;
     bool einv_fp64 = false;
+    int pcg_nt = 512;             // k_pcg2 threads per CTA (256: two CTAs per SM)
+    int ncb = 0, mu_cap = 0, items_cap = 0;  // k_pcg2 coarse shared layout (see PcgArgs)
     std::vector<int64_t> h_abase;
     double coarse_ms = 0;
 };
@@ -1152,6 +1154,9 @@ struct PcgArgs {
     int32_t chunk_cap;       // slices per CTA the smem was sized for
     long long* timing;       // optional: per CTA [phaseA, red1, phaseB, red2] cycles (iterations 64..191)
     const int32_t* order;    // k_pcg2: cluster -> slot launch order (nullptr: identity)
+    int32_t ncb;             // k_pcg2 shared layout: gbuf stride (>= every slot's nc)
+    int32_t mu_cap;          // ... own coarse rows per CTA
+    int32_t items_cap;       // ... (aggregate, part) work items per CTA
     CoarseArgs C;
 };
 
@@ -1459,7 +1464,7 @@ __global__ void __launch_bounds__(NT, 1) k_pcg(PcgArgs A) {
 //   B: r -= alpha q; <r,r>; g = W^T r over my aggregates -> every CTA  [SYNC2]
 //   C: mu = E^-1 g on my aggregates; z = r + W^ mu; rho = <r,z>        [SYNC3]
 template <int NT, typename ET>
-__global__ void __launch_bounds__(NT, 1) k_pcg2(PcgArgs A) {
+__global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) k_pcg2(PcgArgs A) {
     constexpr int NW = NT / 32;
     extern __shared__ __align__(16) unsigned char smem[];
     cg::cluster_group cl = cg::this_cluster();
@@ -1483,10 +1488,11 @@ __global__ void __launch_bounds__(NT, 1) k_pcg2(PcgArgs A) {
     double2* zl = s_slot + 2 * MAX_CLUSTER;
     double2* ql = zl + 32 * cap;
     double2* rl = ql + 32 * cap;
-    double2* gbuf = rl + 32 * cap;          // [2][NC_MAX]
-    double2* mu = gbuf + 2 * NC_MAX;        // [NC_MAX] (my aggregates)
-    double* part = reinterpret_cast<double*>(mu + NC_MAX);  // [ITEMS_MAX][6]
-    int* s_ent = reinterpret_cast<int*>(part + 6 * ITEMS_MAX);
+    const int ncb = A.ncb;
+    double2* gbuf = rl + 32 * cap;          // [2][ncb]
+    double2* mu = gbuf + 2 * ncb;           // [mu_cap] (my aggregates)
+    double* part = reinterpret_cast<double*>(mu + A.mu_cap);  // [items_cap][6]
+    int* s_ent = reinterpret_cast<int*>(part + 6 * A.items_cap);
     int* s_w = s_ent + cap;
     uint32_t* s_mask = reinterpret_cast<uint32_t*>(s_w + cap);
 
@@ -1604,14 +1610,14 @@ __global__ void __launch_bounds__(NT, 1) k_pcg2(PcgArgs A) {
                 gx += pp[2 * sidx];
                 gy += pp[2 * sidx + 1];
             }
-            double2* gb = cl.map_shared_rank(gbuf + par * NC_MAX, dst);
+            double2* gb = cl.map_shared_rank(gbuf + par * ncb, dst);
             gb[crow0 + cq] = make_double2(gx, gy);
         }
         return l_rr;
     };
     // C: mu = E^-1 g (my coarse rows), z = r + W^ mu, returns <r,z> share
     auto prolong_z = [&](int par) -> double {
-        const double2* g = gbuf + par * NC_MAX;
+        const double2* g = gbuf + par * ncb;
         for (int q = warp; q < 3 * naggs; q += NW) {
             const ET* er = Einv + (int64_t)(crow0 + q) * ncp;
             double mx = 0.0, my = 0.0;
@@ -1669,7 +1675,7 @@ __global__ void __launch_bounds__(NT, 1) k_pcg2(PcgArgs A) {
 
     // init: y = 0 (builder), r = b, p = q = 0; coarse buffers zero (columns
     // past nc meet zero padding of E^-1 and must not hold NaN garbage)
-    for (int i = threadIdx.x; i < 2 * NC_MAX; i += NT) gbuf[i] = make_double2(0.0, 0.0);
+    for (int i = threadIdx.x; i < 2 * ncb; i += NT) gbuf[i] = make_double2(0.0, 0.0);
     double l_rr = 0.0, l_bb = 0.0;
     for (int i = threadIdx.x; i < 32 * nloc; i += NT) {
         double2 bi = A.b[row0 + i];
@@ -2110,14 +2116,19 @@ int launch_pcg2_t(SolveSystem* S, const PcgArgs& args, int csize, size_t smem, c
 int launch_pcg(SolveSystem* S, const PcgArgs& args, int csize, cudaStream_t s) {
     int chunk = args.chunk_cap;
     size_t smem = (size_t)RED_BYTES + (size_t)3 * 32 * chunk * sizeof(double2) + (size_t)12 * chunk +
-                  (S->coarse ? (size_t)COARSE_BYTES : 0);
+                  (S->coarse ? (size_t)(2 * S->ncb + S->mu_cap) * 16 + (size_t)S->items_cap * 48
+                             : 0);
     if (smem > SMEM_LIMIT) {
         set_error("pcg: shared memory %zu exceeds limit", smem);
         return PGCP_E_INVALID;
     }
-    if (S->coarse)
+    if (S->coarse) {
+        if (S->pcg_nt == 256)
+            return S->einv_fp64 ? launch_pcg2_t<256, double2>(S, args, csize, smem, s)
+                                : launch_pcg2_t<256, float2>(S, args, csize, smem, s);
         return S->einv_fp64 ? launch_pcg2_t<512, double2>(S, args, csize, smem, s)
                             : launch_pcg2_t<512, float2>(S, args, csize, smem, s);
+    }
     const char* v = getenv("PGCP_PCG_VARIANT");
     int variant = v ? atoi(v) : 0;
     switch (variant) {
@@ -2315,6 +2326,33 @@ int build_coarse(SolveSystem* S, int csize, cudaStream_t s) {
         PGCP_LAUNCH_CHECK();
         PGCP_TRY_CUDA(cudaStreamSynchronize(s));  // he32 is a local
     }
+    {
+        // k_pcg2 shared layout: gbuf holds every coarse dof of a slot, mu and
+        // the partial sums only the CTA's own aggregates (k_pcg2 item_range)
+        std::vector<int32_t> haoff(NA + 1);
+        PGCP_TRY_CUDA(cudaMemcpyAsync(haoff.data(), S->aoff.p, haoff.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        PGCP_TRY_CUDA(cudaStreamSynchronize(s));
+        const int NW = S->pcg_nt / 32;
+        int ncmax = 0, own_max = 0, items_max = 1;
+        for (int j = 0; j < nslot; ++j) {
+            const int a0 = (int)S->h_abase[j], nag = (int)(S->h_abase[j + 1] - a0);
+            ncmax = std::max(ncmax, 3 * nag);
+            const int Sj = (int)(S->h_sl_off[j + 1] - S->h_sl_off[j]);
+            const int ch = (Sj + csize - 1) / csize;
+            for (int r = 0; r < csize; ++r) {
+                const int64_t row0 = 32 * (S->h_sl_off[j] + std::min(Sj, r * ch));
+                const int64_t rowN = 32 * (S->h_sl_off[j] + std::min(Sj, (r + 1) * ch));
+                int na = 0;
+                for (int a = a0; a < a0 + nag; ++a) na += haoff[a] >= row0 && haoff[a] < rowN;
+                own_max = std::max(own_max, na);
+                const int npart = std::max(1, NW / std::max(na, 1));
+                items_max = std::max(items_max, na * npart);
+            }
+        }
+        S->ncb = std::max(8, (ncmax + 7) & ~7);
+        S->mu_cap = std::max(2, (3 * own_max + 1) & ~1);
+        S->items_cap = items_max;
+    }
     PGCP_TRY(S->p.alloc(S->rows, s));
     int hovf = 0;
     PGCP_TRY_CUDA(cudaMemcpyAsync(&hovf, ovf.p, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -2329,8 +2367,12 @@ int build_coarse(SolveSystem* S, int csize, cudaStream_t s) {
 
 // Build the slot system. pins (device int32 [2*nslot]) for DNCP, or the fixed
 // list for harmonic. fv = fixed values (device complex).
+// val_override (device f64 [nnz of the batch Laplacian], optional): matrix
+// values on the Laplacian's CSR pattern to use instead of L (the linear
+// Beltrami stiffness of the fold-over repair, repair.cu).
 int build_system(pgcp_batch* b, SolveSystem* S, bool dncp, const int32_t* d_pins, const double2* targets_host,
-                 const int32_t* fixed_gid, const double* fixed_val, int64_t nfixed, cudaStream_t s) {
+                 const int32_t* fixed_gid, const double* fixed_val, int64_t nfixed, cudaStream_t s,
+                 const double* val_override = nullptr) {
     const int32_t nslot = S->nslot;
     S->dncp = dncp;
     // compact vertex enumeration over the slots
@@ -2432,7 +2474,7 @@ int build_system(pgcp_batch* b, SolveSystem* S, bool dncp, const int32_t* d_pins
     a.vert_off = b->vert_off.p;
     a.row_ptr = b->row_ptr.p;
     a.col = b->col.p;
-    a.val = b->val.p;
+    a.val = val_override ? val_override : b->val.p;
     a.rowsrc = S->rowsrc.p;
     a.urow = S->urow.p;
     a.fixed_ref = S->fixed_ref.p;
@@ -2493,6 +2535,7 @@ int setup_solve(SolveSystem* S, const pgcp_solve_opts* o, cudaStream_t s) {
     PGCP_TRY(pick_cluster(max_sl, nslot, o ? o->cluster : 0, S->coarse, &csize, &chunk));
     S->csize = csize;
     S->chunk = chunk;
+    if (const char* en = getenv("PGCP_PCG2_NT")) S->pcg_nt = atoi(en) == 256 ? 256 : 512;
     if (S->coarse) {
         cudaEvent_t c0, c1;
         PGCP_TRY_CUDA(cudaEventCreate(&c0));
@@ -2554,6 +2597,9 @@ int run_solve(pgcp_batch* b, SolveSystem* S, const pgcp_solve_opts* o, double* z
     A.C.einvh = S->einv_fp64 ? (const void*)S->einv64.p : (const void*)S->einv32.p;
     A.C.eoff32 = S->eoff32.p;
     A.C.p = S->p.p;
+    A.ncb = S->ncb;
+    A.mu_cap = S->mu_cap;
+    A.items_cap = S->items_cap;
     DevBuf<long long> tbuf;
     A.timing = nullptr;
     A.order = nullptr;
@@ -2975,6 +3021,43 @@ int solve_harmonic(pgcp_batch* b, const int32_t* comps, int32_t ncomp, const int
                    pgcp_solve_stat* st, cudaStream_t s) {
     PGCP_TRY(prepare_harmonic(b, comps, ncomp, fixed_gid, nfixed, o, s));
     return finish_harmonic(b, fixed_val, nfixed, o, z, st, s);
+}
+
+// Dirichlet solve of the listed submeshes with explicit matrix values on the
+// Laplacian pattern (repair.cu: assemble.py:205-213, K_ff u = -K_f,fixed g
+// for both coordinates). Same solver and safety net as the harmonic solve;
+// the system is not kept on the batch.
+int solve_values(pgcp_batch* b, const int32_t* comps, int32_t ncomp, const double* vals, const int32_t* fixed_gid,
+                 const double* fixed_val, int64_t nfixed, const pgcp_solve_opts* o, double* z, pgcp_solve_stat* st,
+                 cudaStream_t s) {
+    SolveSystem S;
+    PGCP_TRY(prepare_slots(b, &S, comps, ncomp));
+    if (S.nslot == 0) return PGCP_OK;
+    PGCP_TRY(build_system(b, &S, false, nullptr, nullptr, fixed_gid, fixed_val, nfixed, s, vals));
+    std::vector<pgcp_solve_stat> hst(S.nslot);
+    int rc = run_solve(b, &S, o, z, hst.data(), s);
+    bool only_noconv = rc == PGCP_E_NOCONV;
+    for (int j = 0; j < S.nslot && only_noconv; ++j)
+        only_noconv = hst[j].status == PGCP_OK || hst[j].status == PGCP_E_NOCONV;
+    if (only_noconv && S.coarse && !(o && o->maxit > 0)) {
+        std::vector<int32_t> rc_comps;
+        std::vector<int> where;
+        for (int j = 0; j < S.nslot; ++j)
+            if (hst[j].status == PGCP_E_NOCONV) {
+                rc_comps.push_back(S.comps[j]);
+                where.push_back(j);
+            }
+        SolveSystem R;
+        R.force_jacobi = true;
+        PGCP_TRY(prepare_slots(b, &R, rc_comps.data(), (int32_t)rc_comps.size()));
+        PGCP_TRY(build_system(b, &R, false, nullptr, nullptr, fixed_gid, fixed_val, nfixed, s, vals));
+        std::vector<pgcp_solve_stat> rst(R.nslot);
+        rc = run_solve(b, &R, o, z, rst.data(), s);
+        for (size_t q = 0; q < where.size(); ++q) hst[where[q]] = rst[q];
+    }
+    if (st)
+        for (int j = 0; j < S.nslot; ++j) st[j] = hst[j];
+    return rc;
 }
 
 int system_dims(pgcp_batch* b, int which, int32_t* nslot_out) {

@@ -239,6 +239,27 @@ class DeviceBatch:
         nat.check(st)
         return z, self.last_stats
 
+    def qc_repair(self, fixed_gid, z, comps=None, layout=None, max_iter=5, cap=0.95, rtol=1e-10,
+                  contract_tol=1e-10, cluster=0, want_flipped=False):
+        """Quasi-conformal fold-over repair (qc_correct, assemble.py:174-217)
+        of the listed submeshes, in place on the local-vertex embedding z.
+        Returns per submesh (flips_before, iterations, cleared, flips_after)
+        and, if asked, the per-parent-face flags of faces still folded."""
+        self.laplacian()
+        carr, nc, nslot = self._comps(comps)
+        fg = to_dev(fixed_gid, torch.int32)
+        lay = to_dev(layout, torch.complex128) if layout is not None else None
+        info = (ctypes.c_int32 * (4 * max(nslot, 1)))()
+        flipped = torch.zeros(self.m, dtype=torch.uint8, device=device()) if want_flipped else None
+        if comps is not None and nc == 0:
+            return [], flipped
+        nat.check(nat.lib().pgcp_batch_qc_repair(
+            self.h, carr, nc, ptr(lay) if lay is not None else None, ptr(fg), int(fg.numel()), int(max_iter),
+            float(cap), ctypes.byref(self._opts(rtol, contract_tol, 0, cluster)), ptr(z), info,
+            ptr(flipped) if flipped is not None else None, stream_handle(self.stream)))
+        rows = np.frombuffer(info, dtype=np.int32)[:4 * nslot].reshape(-1, 4)
+        return [tuple(int(v) for v in r) for r in rows], flipped
+
     def export_system(self, which, comp):
         """(scipy CSR, rhs) of the last flatten (0: C_ff) / harmonic (1: L_II) system."""
         from scipy import sparse

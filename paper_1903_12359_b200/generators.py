@@ -128,6 +128,27 @@ def height_field_case(n, k, n_bumps=8, seed=0, layout="blocks"):
     return V, F, cuts_from_face_labels(F, lab)
 
 
+def jittered_grid_case(n, jitter=0.45, amp=0.1, sigma=0.1, seed=0, n_bumps=3, strips=0):
+    """(V, F, cuts) of an n x n grid whose interior vertices are displaced in
+    the plane by up to `jitter` cells (uniform, seeded) and lifted by
+    `n_bumps` Gaussian bumps of amplitude `amp`, width `sigma`, centres in
+    [0.2, 0.8]^2. The obtuse triangles give negative cotangent weights, so
+    the harmonic maps fold and the pipeline's fold-over repair
+    (pipeline.py:88-102) runs. strips > 1: that many vertical strips
+    (cuts), else one domain (cuts = None)."""
+    V, F = flat_grid_arrays(n - 1)
+    rng = np.random.default_rng(seed)
+    h = 1.0 / (n - 1)
+    x, y = V[:, 0], V[:, 1]
+    inner = (x > 1e-9) & (x < 1 - 1e-9) & (y > 1e-9) & (y < 1 - 1e-9)
+    V[inner, :2] += rng.uniform(-jitter * h, jitter * h, (int(inner.sum()), 2))
+    for _ in range(n_bumps):
+        cx, cy = rng.uniform(0.2, 0.8, 2)
+        V[:, 2] += amp * np.exp(-((V[:, 0] - cx) ** 2 + (V[:, 1] - cy) ** 2) / (2 * sigma ** 2))
+    cuts = cuts_from_face_labels(F, strip_face_labels(n, strips)) if strips > 1 else None
+    return V, F, cuts
+
+
 def cfg1(seed=0):
     """BASELINE configs[0]: 100 x 100 height field, 8 bumps, 2 x 2 blocks."""
     return height_field_case(100, 2, n_bumps=8, seed=seed)

@@ -347,6 +347,10 @@ def parameterize(mesh, cuts=None, mode="free", workers=1, seed=0, mobius_area=Fa
             z, hst = batch.harmonic(loop_gid, tv, comps=own, rtol=cfg.rtol, cluster=cfg.cluster)
         report.solver["harmonic_iters"] = [s["iters"] for s in hst]
         report.solver["harmonic"] = batch.last_solve(1)
+        # fold-over repair of the submeshes whose harmonic map flipped faces
+        # (pipeline.py:88-102, per submesh before the exterior map-back),
+        # batched over every folded submesh on the device (repair.cu)
+        report.repairs = _repair(batch, loop_gid, z, own, K, cfg, shard)
         if own is not None:
             shard.sum_(z)
         if center is not None:
@@ -361,13 +365,43 @@ def parameterize(mesh, cuts=None, mode="free", workers=1, seed=0, mobius_area=Fa
     clk.start()
     gp, flip = _stitch(batch, embeddings, mode, cfg, mesh)
     clk.stop("stitch")
-    if not (K == 1 and mode == "free"):
-        fc = batch.array(nat.ARR_FACE_COMP, torch.int32)
-        per = torch.bincount(fc.long()[flip.bool()], minlength=K).cpu().numpy() if gp.flipped_faces.size else \
-            np.zeros(K, dtype=np.int64)
-        report.repairs = [{"flips_before": int(per[i]), "repair_iterations": 0, "cleared": bool(per[i] == 0),
-                           "submesh": i} for i in range(K)]
     return _finish(mesh, batch, embeddings, gp, report, cfg, clk)
+
+
+def _repair(batch, loop_gid, z, own, K, cfg, shard):
+    """Per-submesh flip check and qc_correct of the folded ones
+    (pipeline.py:88-102) -> the reference's report.repairs entries
+    (pipeline.py:258-260). Remaining faces are local face indices (faces of
+    a submesh in increasing parent-face order, partition.py:121-126)."""
+    from .assemble import MU_CAP
+    rows, _ = batch.qc_repair(loop_gid, z, comps=own, max_iter=cfg.repair_iters, cap=MU_CAP, rtol=cfg.rtol,
+                              cluster=cfg.cluster)
+    comps = list(range(K)) if own is None else list(own)
+    info = np.zeros((K, 4), dtype=np.int64)
+    for c, r in zip(comps, rows):
+        info[c] = r
+    if shard is not None and own is not None:  # every rank reports every submesh
+        t = torch.as_tensor(info, device=z.device)
+        shard.sum_(t)
+        info = t.cpu().numpy()
+    remaining = {}
+    stuck = [c for c in comps if info[c, 1] > 0 and not info[c, 2]]
+    if stuck:
+        _, flipped = batch.qc_repair(loop_gid, z, comps=stuck, max_iter=0, cap=MU_CAP, want_flipped=True)
+        fl = flipped.cpu().numpy().astype(bool)
+        fc = batch.host(nat.ARR_FACE_COMP, torch.int32)
+        for c in stuck:
+            pf = np.flatnonzero(fc == c)
+            remaining[c] = [int(x) for x in np.flatnonzero(fl[pf])]
+    out = []
+    for c in range(K):
+        before, iters, cleared = int(info[c, 0]), int(info[c, 1]), bool(info[c, 2])
+        e = {"flips_before": before, "repair_iterations": iters, "cleared": cleared}
+        if before:
+            e["remaining"] = remaining.get(c, [])
+        e["submesh"] = c
+        out.append(e)
+    return out
 
 
 _STREAMS = {}

@@ -11,6 +11,7 @@ if ROOT not in sys.path:
 
 PIPELINE_CASES = ["cfg1", "strips4", "blocks3x3", "disk2x2", "k1free", "k1disk", "flat2x2",
                   "sphere2", "sphere4", "tree4x4", "ptree4x4", "qtree4x4"]
+REPAIR_CASES = ["repair_k1disk", "repair_strips3", "repair_disk2"]
 
 
 def case_pairs(case):

@@ -199,6 +199,7 @@ def pipeline_case(name, V, F, cuts, mode, schedule_pairs=None, stagewise=True):
         pack_csr(out, "Lii", Liis, values=False)
         pack(out, "rhs_h", rh, np.complex128)
     out["coords"] = np.asarray(gp.coords)
+    out["repairs_json"] = np.array(json.dumps(rep.repairs))
     out["flips"] = np.array(rep.flips)
     out["seam_residuals"] = np.array(rep.seam_residuals, dtype=np.float64)
     out["distortion_json"] = np.array(json.dumps(rep.distortion))
@@ -241,6 +242,51 @@ def known_answers():
     out["stretch_distortion"] = d
     np.savez_compressed(os.path.join(HERE, "known_answers.npz"), **out)
     print("known_answers written")
+
+
+def qc_cases():
+    """Direct `qc_correct` calls of the reference (assemble.py:174-217):
+    (0) a grid embedding with one interior vertex dragged across a
+    neighbour (clears), (1)-(2) the folded harmonic maps of the repair
+    pipeline cases' submeshes as `_harmonic_task` hands them to qc_correct
+    (pipeline.py:90-97), (3) a degenerate embedded triangle (SolveError)."""
+    from pgcp.assemble import face_layout, qc_correct
+    out = {"count": 0}
+
+    def put(i, V, F, z, fixed, max_iter=5):
+        sub = pgcp.TriMesh(V, F, check=False)
+        lay = face_layout(sub)
+        try:
+            zo, rep = qc_correct(lay, F, z, fixed, max_iter=max_iter)
+            res = np.array([rep.iterations, int(rep.cleared), rep.initial_flips])
+            rem = np.asarray(rep.remaining_faces, np.int64)
+        except pgcp.SolveError as e:
+            zo, res, rem = np.zeros(0, complex), np.array([-1, 0, 0]), np.zeros(0, np.int64)
+            out[f"err{i}"] = np.array(str(e))
+        out[f"V{i}"], out[f"F{i}"], out[f"z{i}"] = V, np.asarray(F, np.int32), z
+        out[f"fixed{i}"], out[f"layout{i}"], out[f"max_iter{i}"] = np.asarray(fixed, np.int64), lay, np.array(max_iter)
+        out[f"out{i}"], out[f"res{i}"], out[f"remaining{i}"] = zo, res, rem
+        out["count"] = i + 1
+
+    Vg, Fg = gen.flat_grid_arrays(12)
+    Vg[:, 2] = 0.05 * np.sin(3 * Vg[:, 0]) * np.cos(2 * Vg[:, 1])
+    z = Vg[:, 0] + 1j * Vg[:, 1]
+    z[13 * 6 + 6] += (1.3 + 0.2j) / 12
+    put(0, Vg, Fg, z, pgcp.boundary_loops(pgcp.TriMesh(Vg, Fg))[0])
+    for i, (strips, mode, seed) in enumerate([(0, "disk", 1), (3, "free", 1)], start=1):
+        V, F, cuts = gen.jittered_grid_case(25, seed=seed, strips=strips)
+        _, _, _, cap = capture_run(V, F, cuts, mode)
+        hargs = [t for t in cap["tasks"] if t[0] == "_harmonic_task"][0][1]
+        j = 0 if strips == 0 else 2
+        sv, sf, bd, bv = hargs[j][:4]
+        z0 = pgcp.harmonic_solve(pgcp.TriMesh(sv, sf, check=False), bd, bv)
+        put(i, sv, sf, z0, bd)
+    zd = Vg[:, 0] + 1j * Vg[:, 1]
+    v00, v10, v11 = 13 * 6 + 6, 13 * 6 + 7, 13 * 7 + 7  # face [v00, v10, v11] made collinear
+    zd[v11] = zd[v10] + 0.5 * (zd[v10] - zd[v00])
+    put(3, Vg, Fg, zd, pgcp.boundary_loops(pgcp.TriMesh(Vg, Fg))[0])
+    np.savez_compressed(os.path.join(HERE, "qc_direct.npz"), **out)
+    print("qc_direct:", [tuple(out[f"res{i}"]) for i in range(out["count"])])
 
 
 def weld_corpus(seed=0, count=12):
@@ -342,7 +388,15 @@ def _cases():
         pipeline_case("qtree4x4", V, F, cuts, "free",
                       schedule_pairs=gen.quadtree_schedule_order(4, 4))
 
-    return {"known_answers": known_answers, "weld_corpus": weld_corpus, "cfg1": c_cfg1, "strips4": c_strips4,
+    def c_repair():
+        # jittered grids whose harmonic maps fold: the per-submesh repair of pipeline.py:88-102 runs
+        for name, strips, mode, seed in [("repair_k1disk", 0, "disk", 1), ("repair_strips3", 3, "free", 1),
+                                         ("repair_disk2", 2, "disk", 1)]:
+            V, F, cuts = gen.jittered_grid_case(25, seed=seed, strips=strips)
+            pipeline_case(name, V, F, cuts, mode)
+
+    return {"known_answers": known_answers, "weld_corpus": weld_corpus, "qc": qc_cases, "repair": c_repair,
+            "cfg1": c_cfg1, "strips4": c_strips4,
             "blocks3x3": c_blocks3x3, "disk2x2": c_disk2x2, "k1": c_k1, "flat2x2": c_flat2x2,
             "sphere": c_sphere, "tree4x4": c_tree4x4, "ptree4x4": c_ptree4x4,
             "qtree4x4": c_qtree4x4}

@@ -12,7 +12,7 @@ import os
 import numpy as np
 import pytest
 
-from conftest import PIPELINE_CASES, case_pairs, load_golden, unpack, unpack_csr
+from conftest import PIPELINE_CASES, REPAIR_CASES, case_pairs, load_golden, unpack, unpack_csr
 
 import oracle
 from oracle import planner as opl
@@ -20,7 +20,7 @@ from oracle import planner as opl
 REF = "/root/reference/pkg/src"
 
 
-@pytest.mark.parametrize("case", PIPELINE_CASES)
+@pytest.mark.parametrize("case", PIPELINE_CASES + REPAIR_CASES)
 def test_oracle_pipeline_bitwise(case):
     z = load_golden(case)
     mode = str(z["mode"])
@@ -47,6 +47,32 @@ def test_oracle_pipeline_bitwise(case):
         assert [st.comp_a, st.comp_b, st.k, int(st.closed)] == list(meta)
     for f, g in zip(out["flat"], unpack(z, "flat")):
         assert np.array_equal(f, g)
+    if "repairs_json" in z.files:
+        ref = json.loads(str(z["repairs_json"]))
+        assert [{k: v for k, v in r.items() if k != "submesh"} for r in ref] == out["repairs"]
+    if "harm" in z.files:
+        for a, b in zip(out["embeddings_local"], unpack(z, "harm")):
+            assert np.array_equal(a, b)
+
+
+def test_oracle_qc_correct_bitwise():
+    """oracle.repair restates assemble.py:53-217 call for call: the repaired
+    embeddings, iteration counts and remaining faces of the reference's
+    qc_correct (tests/golden/qc_direct.npz), the per-face layout, and the
+    degenerate-triangle error."""
+    from oracle.repair import OracleRepairError, isometric_layout, repair_folds
+    z = load_golden("qc_direct")
+    for i in range(int(z["count"])):
+        assert np.array_equal(isometric_layout(z[f"V{i}"], z[f"F{i}"]), z[f"layout{i}"])
+        args = (z[f"layout{i}"], z[f"F{i}"], z[f"z{i}"], z[f"fixed{i}"])
+        if f"err{i}" in z.files:
+            with pytest.raises(OracleRepairError, match="degenerate source triangle"):
+                repair_folds(*args, max_iter=int(z[f"max_iter{i}"]))
+            continue
+        out, it, ok, left, n0 = repair_folds(*args, max_iter=int(z[f"max_iter{i}"]))
+        assert [it, int(ok), n0] == list(z[f"res{i}"])
+        assert np.array_equal(left, z[f"remaining{i}"])
+        assert np.array_equal(out, z[f"out{i}"])
 
 
 @pytest.mark.parametrize("case", ["cfg1", "blocks3x3", "flat2x2", "sphere4"])
