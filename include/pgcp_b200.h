@@ -280,6 +280,14 @@ PGCP_API int pgcp_weld_replay(const pgcp_rec* recs, int32_t nrec, double* pts, i
 PGCP_API int pgcp_weld_geodesic(const double* tv, const int32_t* src, int32_t n, const double* interior,
                                 double* circ, pgcp_rec* recs, int32_t cap, double* meta, void* stream);
 
+/* intermediate_form (welding.py:578-602): zip points 0..k of the n device
+ * points (in place) onto the imaginary half-axis of `branch` (+1: +i,
+ * -1: -i), then send point 0 to infinity. sides device int8 [n] (out);
+ * recs host [cap >= k + 1], *nrec_out records. PGCP_E_WELD with the
+ * reference's message on a failed zip. Synchronises. */
+PGCP_API int pgcp_weld_intermediate(double* pts, int8_t* sides, int32_t n, int32_t k, int32_t branch,
+                                    pgcp_rec* recs, int32_t cap, int32_t* nrec_out, void* stream);
+
 /* polygon_interior_point of tv[src] (host src), optionally reversed. */
 PGCP_API int pgcp_polygon_interior(const double* tv, const int32_t* src, int32_t n, int reverse, double* out,
                                    void* stream);

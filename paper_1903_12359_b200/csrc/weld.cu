@@ -1271,6 +1271,100 @@ __global__ void __launch_bounds__(512) k_geodesic(GeoArgs A) {
     }
 }
 
+// intermediate_form (welding.py:578-602): zip points 0..k of one boundary
+// onto the branch's half of the imaginary axis (_zip_points,
+// welding.py:544-575), then the axis Mobius sending point 0 to infinity. One
+// block; every record is built by thread 0 and applied by all threads.
+__global__ void __launch_bounds__(512) k_zip_form(double2* pts, int8_t* sides, int n, int k, int br, Rec* recs,
+                                                   double* meta) {
+    __shared__ Rec s_rec;
+    __shared__ int s_err;
+    __shared__ double red[32];
+    if (threadIdx.x == 0) {
+        s_err = 0;
+        for (int i = 0; i < META; ++i) meta[i] = 0.0;
+    }
+    for (int i = threadIdx.x; i < n; i += blockDim.x) sides[i] = 0;
+    __syncthreads();
+    int nrec = 0;
+    auto apply_all = [&]() {
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            double2 z = pts[i];
+            int8_t sd = sides[i];
+            apply_rec(s_rec, z, sd);
+            pts[i] = z;
+            sides[i] = sd;
+        }
+    };
+    if (threadIdx.x == 0) {
+        if (c_eq(pts[0], pts[1])) block_fail(&s_err, WE_ZIP01, 0, 0, meta);
+        else s_rec = mk_sqr(pts[0], pts[1], br);
+        recs[nrec] = s_rec;
+    }
+    ++nrec;
+    __syncthreads();
+    if (s_err) return;
+    apply_all();
+    __syncthreads();
+    for (int j = 2; j <= k; ++j) {
+        if (threadIdx.x == 0) {
+            double2 xi = pts[j];
+            if (sides[j] != 0 || c_isinf(xi)) block_fail(&s_err, WE_ZIP_HALF, j, 0, meta);
+            else if (!(xi.x > 0)) block_fail(&s_err, WE_ZIP_AXIS, j, 0, meta);
+            else if (cabs_lt(xi, 1e-13)) block_fail(&s_err, WE_ZIP_COLL, j, 0, meta);
+            else {
+                s_rec = mk_open(xi, br);
+                recs[nrec] = s_rec;
+            }
+        }
+        ++nrec;
+        __syncthreads();
+        if (s_err) return;
+        apply_all();
+        __syncthreads();
+    }
+    double bad = 0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+        if (c_nan(pts[i])) bad = 1;
+    bad = block_max(bad, red);
+    if (bad > 0) {
+        if (threadIdx.x == 0) block_fail(&s_err, WE_NAN, 0, 1, meta);
+        return;
+    }
+    __shared__ int s_has;
+    if (threadIdx.x == 0) {
+        const double2 w0 = pts[0];
+        s_has = 0;
+        if (!c_isinf(w0)) {
+            if (c_zero(w0)) {
+                block_fail(&s_err, WE_FAR0, 0, 0, meta);
+            } else {
+                Rec r = mk_mob(C(1, 0), C(0, 0), cdiv(C(-1.0, 0.0), w0), C(1, 0), true);
+                mob_pin(r, w0, cinf(), br);
+                mob_pin(r, C(0, 0), C(0, 0), br);
+                s_rec = r;
+                recs[nrec] = r;
+                s_has = 1;
+            }
+        }
+    }
+    __syncthreads();
+    if (s_err) return;
+    if (s_has) {
+        ++nrec;
+        apply_all();
+        __syncthreads();
+    }
+    bad = 0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+        if (c_nan(pts[i])) bad = 1;
+    bad = block_max(bad, red);
+    if (threadIdx.x == 0) {
+        meta[0] = nrec;
+        if (bad > 0) block_fail(&s_err, WE_NAN, 0, 2, meta);
+    }
+}
+
 __global__ void k_interior(const double2* __restrict__ tv, const int32_t* __restrict__ src, int n, int reverse,
                            double2* scratch, double* out) {
     __shared__ double red[32];
@@ -1717,6 +1811,44 @@ PGCP_API int pgcp_weld_geodesic(const double* tv, const int32_t* src, int32_t n,
         set_error("%s", err_text((int)m[2], (int)m[3], (int)m[4], m[5]).c_str());
         return PGCP_E_WELD;
     }
+    return PGCP_OK;
+}
+
+// intermediate_form (welding.py:578-602) of n device points, in place
+PGCP_API int pgcp_weld_intermediate(double* pts, int8_t* sides, int32_t n, int32_t k, int32_t branch,
+                                    pgcp_rec* recs, int32_t cap, int32_t* nrec_out, void* stream) {
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (k < 1) {
+        set_error("zip count must be at least 1");
+        return PGCP_E_WELD;
+    }
+    if (n < k + 1) {
+        set_error("need at least k + 1 points");
+        return PGCP_E_WELD;
+    }
+    if (cap < k + 1 || (branch != UP && branch != DOWN)) {
+        set_error("pgcp_weld_intermediate: invalid arguments");
+        return PGCP_E_INVALID;
+    }
+    DevBuf<Rec> d_recs;
+    DevBuf<double> d_meta;
+    PGCP_TRY(d_recs.alloc(k + 1, s));
+    PGCP_TRY(d_meta.alloc(META, s));
+    k_zip_form<<<1, 512, 0, s>>>(reinterpret_cast<double2*>(pts), sides, n, k, branch, d_recs.p, d_meta.p);
+    PGCP_LAUNCH_CHECK();
+    double m[META];
+    PGCP_TRY_CUDA(cudaMemcpyAsync(m, d_meta.p, sizeof m, cudaMemcpyDeviceToHost, s));
+    PGCP_TRY_CUDA(cudaStreamSynchronize(s));
+    if (m[2] != 0) {
+        set_error("%s", err_text((int)m[2], (int)m[3], (int)m[4]).c_str());
+        return PGCP_E_WELD;
+    }
+    const int nrec = (int)m[0];
+    if (recs && nrec > 0) {
+        PGCP_TRY_CUDA(cudaMemcpyAsync(recs, d_recs.p, nrec * sizeof(Rec), cudaMemcpyDeviceToHost, s));
+        PGCP_TRY_CUDA(cudaStreamSynchronize(s));
+    }
+    if (nrec_out) *nrec_out = nrec;
     return PGCP_OK;
 }
 

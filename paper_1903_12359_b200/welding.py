@@ -28,6 +28,7 @@ nat.register("pgcp_weld_replay", [_VP, _I32, _VP, _VP, _I64, _VP])
 nat.register("pgcp_weld_geodesic", [_VP, _VP, _I32, _VP, _VP, _VP, _I32, _VP, _VP])
 nat.register("pgcp_polygon_interior", [_VP, _VP, _I32, ctypes.c_int, _VP, _VP])
 nat.register("pgcp_inv_shift", [_VP, _VP, _I64, _D, _D, _D, _D, _VP])
+nat.register("pgcp_weld_intermediate", [_VP, _VP, _I32, _I32, _I32, _VP, _I32, _VP, _VP])
 nat.register("pgcp_gather_complex", [_VP, _VP, _VP, _I64, _VP])
 nat.register("pgcp_scatter_complex", [_VP, _VP, _VP, _I64, _VP])
 
@@ -402,6 +403,32 @@ def closed_weld(a_points, b_points, hard_tol=1e-6):
     if len(a) < 3:
         raise WeldError("closed welding needs at least 3 boundary points")
     return _pair(a, b, len(a) - 1, True, hard_tol)
+
+
+@dataclass
+class IntermediateForm:
+    values: np.ndarray
+    sides: np.ndarray
+    zipped_count: int
+    log: list = field(default_factory=list)
+
+
+def intermediate_form(points, k, branch=UPPER):
+    """Half-unzip a boundary point sequence (welding.py:578-602) on the
+    device: points 0..k onto the branch's half of the imaginary axis (point
+    0 at infinity, point k at 0), the rest into the open right half-plane."""
+    from .device import device, ptr, require_cuda
+    require_cuda()
+    br = UPPER if branch in (UPPER, "plus_i") else LOWER
+    pts = torch.as_tensor(np.atleast_1d(np.asarray(points, dtype=np.complex128)).copy()).to(device())
+    sides = torch.zeros(pts.shape, dtype=torch.int8, device=pts.device)
+    cap = max(int(k), 1) + 1
+    recs = (nat.Rec * cap)()
+    nrec = ctypes.c_int32(0)
+    nat.check(nat.lib().pgcp_weld_intermediate(ptr(pts), ptr(sides), pts.numel(), int(k), br, recs, cap,
+                                               ctypes.byref(nrec), _stream()))
+    log = [_from_native(recs[i]) for i in range(nrec.value)]
+    return IntermediateForm(pts.cpu().numpy(), sides.cpu().numpy(), int(k), log)
 
 
 def geodesic_to_circle(points, interior=None):

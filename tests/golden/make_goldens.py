@@ -289,6 +289,41 @@ def qc_cases():
     print("qc_direct:", [tuple(out[f"res{i}"]) for i in range(out["count"])])
 
 
+def intermediate_cases():
+    """`intermediate_form` (welding.py:578-602) of the weld corpus boundaries
+    on both branches, plus its error paths."""
+    w = np.load(os.path.join(HERE, "weld_corpus.npz"))
+    a_off, b_off = w["a_off"], w["b_off"]
+    out = {"vals": [], "sides": [], "nrec": [], "k": [], "branch": [], "pts": []}
+    for i in range(len(w["k"])):
+        for pts, br in ((w["a"][a_off[i]:a_off[i + 1]], pgcp.welding.UPPER),
+                        (w["b"][b_off[i]:b_off[i + 1]], pgcp.welding.LOWER)):
+            k = int(w["k"][i])
+            r = pgcp.intermediate_form(pts, k, br)
+            out["pts"].append(pts)
+            out["vals"].append(r.values)
+            out["sides"].append(r.sides)
+            out["nrec"].append(len(r.log))
+            out["k"].append(k)
+            out["branch"].append(br)
+    res = {}
+    pack(res, "pts", out["pts"], np.complex128)
+    pack(res, "vals", out["vals"], np.complex128)
+    pack(res, "sides", out["sides"], np.int8)
+    for key in ("nrec", "k", "branch"):
+        res[key] = np.array(out[key], dtype=np.int64)
+    errs = []
+    for pts, k in (([0, 1, 2], 0), ([0, 1], 2), ([1, 1, 2, 3], 2), ([0, 1, 1j, 2], 3)):
+        try:
+            pgcp.intermediate_form(np.asarray(pts, np.complex128), k)
+            errs.append("")
+        except pgcp.WeldError as e:
+            errs.append(str(e))
+    res["errors"] = np.array(errs)
+    np.savez_compressed(os.path.join(HERE, "intermediate.npz"), **res)
+    print("intermediate:", len(out["k"]), "forms; errors", errs)
+
+
 def weld_corpus(seed=0, count=12):
     """Random Jordan polygon pairs welded by the reference `partial_weld`
     (SPEC acceptance criterion 1 shape): two star-shaped regions sharing an
@@ -395,7 +430,8 @@ def _cases():
             V, F, cuts = gen.jittered_grid_case(25, seed=seed, strips=strips)
             pipeline_case(name, V, F, cuts, mode)
 
-    return {"known_answers": known_answers, "weld_corpus": weld_corpus, "qc": qc_cases, "repair": c_repair,
+    return {"known_answers": known_answers, "weld_corpus": weld_corpus, "intermediate": intermediate_cases,
+            "qc": qc_cases, "repair": c_repair,
             "cfg1": c_cfg1, "strips4": c_strips4,
             "blocks3x3": c_blocks3x3, "disk2x2": c_disk2x2, "k1": c_k1, "flat2x2": c_flat2x2,
             "sphere": c_sphere, "tree4x4": c_tree4x4, "ptree4x4": c_ptree4x4,

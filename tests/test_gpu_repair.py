@@ -6,6 +6,7 @@ diameter; iteration counts, cleared flags, remaining faces and flip counts
 equal; angle-distortion mean/sd within 1e-3 degrees."""
 
 import json
+import re
 
 import numpy as np
 import pytest
@@ -112,3 +113,27 @@ def test_stitch_global_matches_reference(cuda):
     ref = z["coords"]
     assert np.max(np.abs(gp.coords - ref)) <= 1e-12 * _diam(ref)
     assert len(gp.flipped_faces) == int(z["flips"])
+
+
+def test_intermediate_form_matches_reference(cuda):
+    """intermediate_form (welding.py:578-602) on the weld corpus boundaries,
+    both branches: values within 1e-9 of the scale, side tags and record
+    counts equal; error paths with the reference's messages."""
+    from paper_1903_12359_b200 import WeldError, intermediate_form
+    z = load_golden("intermediate")
+    for pts, vals, sides, nrec, k, br in zip(unpack(z, "pts"), unpack(z, "vals"), unpack(z, "sides"), z["nrec"],
+                                             z["k"], z["branch"]):
+        r = intermediate_form(pts, int(k), int(br))
+        assert np.array_equal(r.sides, sides)
+        assert len(r.log) == nrec
+        fin = np.isfinite(vals)
+        assert np.array_equal(fin, np.isfinite(r.values))
+        sc = np.max(np.abs(vals[fin]))
+        assert np.max(np.abs(r.values[fin] - vals[fin])) <= 1e-9 * sc
+    cases = (([0, 1, 2], 0), ([0, 1], 2), ([1, 1, 2, 3], 2), ([0, 1, 1j, 2], 3))
+    for (pts, k), msg in zip(cases, z["errors"]):
+        if str(msg):
+            with pytest.raises(WeldError, match=re.escape(str(msg))):
+                intermediate_form(np.asarray(pts, np.complex128), k)
+        else:
+            intermediate_form(np.asarray(pts, np.complex128), k)
