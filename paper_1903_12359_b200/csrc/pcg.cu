@@ -1537,14 +1537,23 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) k_pcg2(PcgArgs A) {
     double2* pg = A.C.p;
     const uint2* wr = A.C.wr;
 
-    auto item_range = [&](int t, int& a_rel, int64_t& rb, int64_t& re) {
-        a_rel = t / npart;
-        const int pt = t - a_rel * npart;
+    // (aggregate, part) work items: row ranges kept in shared memory so the
+    // per-iteration loops do not wait on global aggregate offsets
+    int2* s_item = reinterpret_cast<int2*>((reinterpret_cast<uintptr_t>(s_mask + cap) + 7) & ~(uintptr_t)7);
+    for (int t = threadIdx.x; t < nitems; t += NT) {
+        const int a_rel = t / npart, pt = t - a_rel * npart;
         const int64_t r0 = A.C.aoff[a_lo + a_rel], r1 = A.C.aoff[a_lo + a_rel + 1];
         const int64_t per = (r1 - r0 + npart - 1) / npart;
-        rb = r0 + pt * per;
-        re = min(r1, rb + per);
+        const int64_t rb = r0 + pt * per;
+        s_item[t] = make_int2((int)(rb - row0), (int)(min(r1, rb + per) - row0));
+    }
+    auto item_range = [&](int t, int& a_rel, int64_t& rb, int64_t& re) {
+        a_rel = t / npart;
+        const int2 it2 = s_item[t];
+        rb = row0 + it2.x;
+        re = row0 + it2.y;
     };
+    constexpr int IU = 8;  // rows per lane in flight in the aggregate-order loops
     // B: (optionally r -= alpha q), <r,r>, g = W^T r for my aggregates, sent
     // to every CTA's gbuf[par]; returns this thread's <r,r> share
     auto restrict_r = [&](bool upd, double alpha, int par) -> double {
@@ -1554,15 +1563,15 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) k_pcg2(PcgArgs A) {
             int64_t rb, re;
             item_range(t, a_rel, rb, re);
             double g0x = 0, g0y = 0, g1x = 0, g1y = 0, g2x = 0, g2y = 0;
-            for (int64_t rq = rb + lane; rq < re; rq += 128) {
-                float4 w[4];
+            for (int64_t rq = rb + lane; rq < re; rq += 32 * IU) {
+                float4 w[IU];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
+                for (int u = 0; u < IU; ++u) {
                     const int64_t r = rq + 32 * u;
                     w[u] = r < re ? cw_get(wr, r) : make_float4(0.f, 0.f, 0.f, 0.f);
                 }
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
+                for (int u = 0; u < IU; ++u) {
                     const int64_t r = rq + 32 * u;
                     if (r >= re) break;
                     const int li = (int)(r - row0);
@@ -1649,15 +1658,15 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) k_pcg2(PcgArgs A) {
             int64_t rb, re;
             item_range(t, a_rel, rb, re);
             const double2 m0 = mu[3 * a_rel], m1 = mu[3 * a_rel + 1], m2 = mu[3 * a_rel + 2];
-            for (int64_t rq = rb + lane; rq < re; rq += 128) {
-                float4 w[4];
+            for (int64_t rq = rb + lane; rq < re; rq += 32 * IU) {
+                float4 w[IU];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
+                for (int u = 0; u < IU; ++u) {
                     const int64_t r = rq + 32 * u;
                     w[u] = r < re ? cw_get(wr, r) : make_float4(0.f, 0.f, 0.f, 0.f);
                 }
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
+                for (int u = 0; u < IU; ++u) {
                     const int64_t r = rq + 32 * u;
                     if (r >= re) break;
                     const int li = (int)(r - row0);
@@ -2116,7 +2125,7 @@ int launch_pcg2_t(SolveSystem* S, const PcgArgs& args, int csize, size_t smem, c
 int launch_pcg(SolveSystem* S, const PcgArgs& args, int csize, cudaStream_t s) {
     int chunk = args.chunk_cap;
     size_t smem = (size_t)RED_BYTES + (size_t)3 * 32 * chunk * sizeof(double2) + (size_t)12 * chunk +
-                  (S->coarse ? (size_t)(2 * S->ncb + S->mu_cap) * 16 + (size_t)S->items_cap * 48
+                  (S->coarse ? (size_t)(2 * S->ncb + S->mu_cap) * 16 + (size_t)S->items_cap * (48 + 8) + 8
                              : 0);
     if (smem > SMEM_LIMIT) {
         set_error("pcg: shared memory %zu exceeds limit", smem);
