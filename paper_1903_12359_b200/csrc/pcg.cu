@@ -1154,6 +1154,7 @@ struct PcgArgs {
     int32_t chunk_cap;       // slices per CTA the smem was sized for
     long long* timing;       // optional: per CTA [phaseA, red1, phaseB, red2] cycles (iterations 64..191)
     const int32_t* order;    // k_pcg2: cluster -> slot launch order (nullptr: identity)
+    double* hist;            // k_pcg2 (PGCP_PCG_HIST): per slot [HIST_K][3] alpha, rr, beta of the first iterations
     int32_t ncb;             // k_pcg2 shared layout: gbuf stride (>= every slot's nc)
     int32_t mu_cap;          // ... own coarse rows per CTA
     int32_t items_cap;       // ... (aggregate, part) work items per CTA
@@ -1189,6 +1190,7 @@ __device__ __forceinline__ double2 cluster_sum2(cg::cluster_group& cl, int csize
 }
 
 constexpr int KPF = 8;  // prefetched off-diagonal entries per row (4 pairs)
+constexpr int HIST_K = 128;  // PGCP_PCG_HIST: iterations recorded per slot
 constexpr int KPF2 = 6;  // k_pcg2 (register budget: p is prefetched as well)
 
 template <int KP>
@@ -1809,6 +1811,10 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) k_pcg2(PcgArgs A) {
             parity ^= 1;
             rr = tr.x;
             ++it;
+            if (A.hist && rank == 0 && threadIdx.x == 0 && it <= HIST_K) {
+                A.hist[(slot * HIST_K + it - 1) * 3 + 0] = alpha;
+                A.hist[(slot * HIST_K + it - 1) * 3 + 1] = rr;
+            }
             if (rr <= stop || !(rr == rr)) break;
             long long c4 = timed ? clock64() : 0;
             // ---- C: z = M r, rho = <r,z>
@@ -1819,6 +1825,7 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) k_pcg2(PcgArgs A) {
             parity ^= 1;
             beta = tz2.x / rho;
             rho = tz2.x;
+            if (A.hist && rank == 0 && threadIdx.x == 0 && it <= HIST_K) A.hist[(slot * HIST_K + it - 1) * 3 + 2] = beta;
             if (timed) {
                 long long c6 = clock64();
                 tm[0] += c1 - c0;
@@ -2042,6 +2049,34 @@ __global__ void k_flat_checks(const int32_t* __restrict__ comps, const int64_t* 
 // ---------------------------------------------------------------------------
 // host side
 
+// clusters of k_pcg2 that can be resident at once for a cluster shape
+int max_active_clusters(int csize, size_t smem) {
+    static std::vector<std::pair<long long, int>> cache;
+    const long long key = (long long)csize << 32 | (long long)smem;
+    for (auto& kv : cache)
+        if (kv.first == key) return kv.second;
+    auto kern = k_pcg2<512, float2>;
+    int n = 0;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess &&
+        (csize <= 8 || cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess)) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)csize, 1, 1);
+        cfg.blockDim = dim3(512, 1, 1);
+        cfg.dynamicSmemBytes = smem;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = csize;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) n = 0;
+    }
+    cudaGetLastError();
+    cache.emplace_back(key, n);
+    return n;
+}
+
 int pick_cluster(int64_t max_slices, int32_t nslot, int32_t forced, bool coarse, int* csize_out, int* chunk_out) {
     const int max_chunk = (SMEM_LIMIT - RED_BYTES - (coarse ? COARSE_BYTES : 0)) / (48 * 32 + 12);
     int cmin = 1;
@@ -2054,6 +2089,29 @@ int pick_cluster(int64_t max_slices, int32_t nslot, int32_t forced, bool coarse,
     int c = cmin;
     if (forced > 0) {
         c = std::max(cmin, forced);
+    } else if (coarse) {
+        // k_pcg2: choose the cluster shape by waves x per-iteration time.
+        // Waves come from the occupancy query (GPC packing: 33 four-CTA,
+        // 15 eight-CTA, 7 sixteen-CTA clusters fit on a B200); the
+        // per-iteration time per CTA was measured on cfg 2 as about
+        // 10.9K + 8.6 x (rows per CTA) cycles (46.7K / 28.8K / 21.9K at 4 / 8 /
+        // 16 CTAs per subdomain), barriers and coarse phases being the
+        // constant part. Spreading a few subdomains over wider clusters only
+        // pays while they still run in one wave.
+        double best = 0;
+        for (int cc = cmin; cc <= MAX_CLUSTER; cc *= 2) {
+            const int64_t ch = (max_slices + cc - 1) / cc;
+            if (cc > cmin && ch < 8) break;  // keep >= 256 rows per CTA
+            const size_t smem = (size_t)RED_BYTES + (size_t)3 * 32 * ch * 16 + (size_t)12 * ch + COARSE_BYTES;
+            const int nconc = max_active_clusters(cc, smem);
+            if (nconc < 1) continue;
+            const double waves = (double)((nslot + nconc - 1) / nconc);
+            const double cost = waves * (10900.0 + 8.6 * 32.0 * (double)ch);
+            if (best == 0 || cost < best * 0.98) {  // ties: the narrower cluster
+                best = cost;
+                c = cc;
+            }
+        }
     } else {
         // spread over the SMs when there are few subdomains, but keep >= 8
         // slices (256 rows) per CTA so DSMEM halo traffic stays small
@@ -2627,6 +2685,14 @@ int run_solve(pgcp_batch* b, SolveSystem* S, const pgcp_solve_opts* o, double* z
             A.order = dorder.p;
         }
     }
+    DevBuf<double> hbuf;
+    A.hist = nullptr;
+    const char* hist_path = getenv("PGCP_PCG_HIST");  // analysis aid: early CG coefficients per slot
+    if (hist_path && S->coarse && !S->force_jacobi) {
+        PGCP_TRY(hbuf.alloc((int64_t)nslot * HIST_K * 3, s));
+        PGCP_TRY(hbuf.zero(s));
+        A.hist = hbuf.p;
+    }
     const bool want_timing = getenv("PGCP_PCG_TIMING") != nullptr;
     if (want_timing) {
         PGCP_TRY(tbuf.alloc(8 * (int64_t)nslot * csize, s));
@@ -2677,6 +2743,17 @@ int run_solve(pgcp_batch* b, SolveSystem* S, const pgcp_solve_opts* o, double* z
     PGCP_TRY_CUDA(cudaMemcpyAsync(hres.data(), S->res.p, 8 * nslot * sizeof(double), cudaMemcpyDeviceToHost, s));
     PGCP_TRY_CUDA(cudaStreamSynchronize(s));
     if (S->coarse && !S->force_jacobi) g_prev_iters = hit;
+    if (A.hist) {
+        std::vector<double> hh((size_t)nslot * HIST_K * 3);
+        PGCP_TRY_CUDA(cudaMemcpy(hh.data(), hbuf.p, hh.size() * sizeof(double), cudaMemcpyDeviceToHost));
+        if (FILE* f = fopen(hist_path, "ab")) {
+            int32_t hdr[2] = {nslot, HIST_K};
+            fwrite(hdr, sizeof hdr, 1, f);
+            fwrite(hit.data(), sizeof(int32_t), nslot, f);
+            fwrite(hh.data(), sizeof(double), hh.size(), f);
+            fclose(f);
+        }
+    }
     if (want_timing)
         fprintf(stderr, "[pcg timing] post-solve (true residual, scatter, checks, stats) %.2f ms\n",
                 1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - t_post).count());

@@ -103,6 +103,13 @@ def bench_distributed(args, V, F, cuts, pairs, metric, unit, workload):
     from . import _native as nat
     import bench as B
 
+    if "RANK" not in os.environ:  # a single process outside torchrun (PGCP_BENCH_DIST=1)
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0", MASTER_ADDR="127.0.0.1",
+                          MASTER_PORT=str(port))
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", "0"))
