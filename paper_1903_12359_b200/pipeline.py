@@ -484,6 +484,10 @@ def _finish(mesh, batch, embeddings, gp, report, cfg, clk):
     if gp.mode in ("free", "disk"):
         energy = float(batch.energy(embeddings).sum())
     V, F = mesh.device_arrays()
+    pending = None
+    if not cfg.keep_device:
+        # the result's D2H runs on a copy stream while the metrics kernels run
+        pending = (_to_host_async(gp.coords), _to_host_async(gp.provenance.to(torch.int64)))
     dist = distortion_report(mesh, gp, energy=energy, V=V, F=F)
     clk.stop("metrics")
     if cfg.mobius_area:
@@ -497,18 +501,35 @@ def _finish(mesh, batch, embeddings, gp, report, cfg, clk):
         return gp, report
     # hand back host arrays, as the reference's GlobalParam holds numpy
     clk.start()
-    gp.coords = _to_host(gp.coords)
-    gp.provenance = _to_host(gp.provenance.to(torch.int64))  # widened on the device
+    gp.coords = _host_result(pending[0])
+    gp.provenance = _host_result(pending[1])  # widened on the device
     clk.stop("d2h")
     return gp, report
 
 
-def _to_host(t):
-    """Device tensor -> numpy through a pinned buffer (torch's caching host
-    allocator): one DMA at full PCIe rate instead of a pageable copy."""
+_COPY_STREAMS = {}
+
+
+def _to_host_async(t):
+    """Queue a device -> pinned-host copy of t on a per-device copy stream,
+    ordered after the work queued so far on the current stream."""
+    dev = t.device
+    if dev not in _COPY_STREAMS:
+        _COPY_STREAMS[dev] = torch.cuda.Stream(device=dev)
+    cs = _COPY_STREAMS[dev]
+    cs.wait_stream(torch.cuda.current_stream(dev))
     h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
-    h.copy_(t, non_blocking=True)
-    torch.cuda.current_stream().synchronize()
+    with torch.cuda.stream(cs):
+        h.copy_(t, non_blocking=True)
+        t.record_stream(cs)
+        ev = torch.cuda.Event()
+        ev.record(cs)
+    return h, ev
+
+
+def _host_result(pending):
+    h, ev = pending
+    ev.synchronize()
     return h.numpy()
 
 
