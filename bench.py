@@ -305,10 +305,11 @@ def main():
                            "CSR system C_ff (z nonzeros, r = 2|U| rows), summed over the iterations each subdomain ran",
             "device_bytes_per_launch": dev_launch,
             "device_achieved": dev_launch / (kernel_ms / 1e3) / 1e9,
-            "device_bytes_model": "what k_pcg2 moves per iteration: 12 B per stored sliced-ELL entry (complex-Hermitian "
-                                  "form: L streamed once for x and y), 32 B/row y, 32 B/row p, 16 B/row fp16 coarse "
+            "device_bytes_model": "what k_pcg2 moves per iteration: per stored sliced-ELL entry 8 B value + 2 B "
+                                  "column code (all-local slices) or 4 B (slices with remote columns) (complex-"
+                                  "Hermitian form: L streamed once for x and y), 32 B/row y, 32 B/row p, 16 B/row fp16 coarse "
                                   "weights, 8*nc*ncp B of fp32 E^-1; z, q, r stay in distributed shared memory",
-            "note": "the cfg-2 working set is L2-resident (96% L2 hit rate, traffic = DRAM bytes per launch from ncu)"}
+            "note": "the cfg-2 working set is L2-resident (97% L2 hit rate, traffic = DRAM bytes per launch from ncu)"}
     cpu = None
     if not args.no_cpu_baseline:
         cores = os.cpu_count() or 1

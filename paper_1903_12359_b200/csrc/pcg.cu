@@ -64,6 +64,7 @@ struct SolveSystem {
     DevBuf<uint32_t> sl_mask;
     DevBuf<int32_t> col, urow, rowsrc, fixed_ref;
     DevBuf<uint32_t> enc;
+    DevBuf<uint16_t> enc16;          // local row index of every entry of an all-local slice
     DevBuf<uint8_t> remote;
     DevBuf<int2> cpl;
     DevBuf<double> val, D, Dinv, Dsq, dmax;
@@ -390,9 +391,12 @@ __global__ void k_slot_dmax(const int64_t* __restrict__ sl_off, const double* __
 // offset of its vector entry in the CTA's shared block; a row owned by
 // another CTA of the cluster is (1 << 31) | (owner rank << 24) | byte offset.
 // remote[s] = 1 if slice s has any remote entry (the kernel's slow path).
+// enc16 holds the owner-local row index alone (rows per CTA < 2^16): the
+// all-local slices stream 2-byte column codes instead of 4-byte ones.
 __global__ void k_encode_cols(int32_t nslot, const int64_t* __restrict__ sl_off, int64_t nslices,
                               const int64_t* __restrict__ sl_ptr, const int32_t* __restrict__ col, int csize,
-                              uint32_t* __restrict__ enc, uint8_t* __restrict__ remote) {
+                              uint32_t* __restrict__ enc, uint16_t* __restrict__ enc16,
+                              uint8_t* __restrict__ remote) {
     int lane = threadIdx.x & 31;
     int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -408,8 +412,10 @@ __global__ void k_encode_cols(int32_t nslot, const int64_t* __restrict__ sl_off,
             int off = c - 32 * own * chunk;
             if (own == me) {
                 enc[e] = (uint32_t)(off * 16);
+                enc16[e] = (uint16_t)off;
             } else {
                 enc[e] = 0x80000000u | ((uint32_t)own << 24) | (uint32_t)(off * 16);
+                enc16[e] = 0;
                 rem = true;
             }
         }
@@ -1139,6 +1145,7 @@ struct PcgArgs {
     const uint32_t* sl_mask;
     const int32_t* col;
     const uint32_t* enc;     // encoded columns (see k_encode_cols)
+    const uint16_t* enc16;   // 16-bit local codes (all-local slices; k_pcg2)
     const uint8_t* remote;   // slice has entries owned by another CTA
     const double* val;       // scaled off-diagonal values
     const double* D;         // unscaled diagonal (norms of the unscaled residual)
@@ -1209,7 +1216,8 @@ template <int KP>
 __device__ __forceinline__ void slice_load(SliceBufT<KP>& B, const double* __restrict__ valc,
                                            const uint32_t* __restrict__ encc, const int* s_ent, const int* s_w,
                                            int ls, int nloc, int lane, const double2* yrow, bool need_y,
-                                           const double2* prow = nullptr) {
+                                           const double2* prow = nullptr,
+                                           const uint16_t* __restrict__ enc16c = nullptr) {
     // entries past the width become (own row, 0.0): the gathers below are
     // straight-line and issue back to back
     const uint32_t self = (uint32_t)((32 * ls + lane) * 16);
@@ -1227,6 +1235,20 @@ __device__ __forceinline__ void slice_load(SliceBufT<KP>& B, const double* __res
     B.w = s_w[ls] & 0xffff;
     B.remote = s_w[ls] >> 16;
     B.off = s_ent[ls] + (lane << 1);
+    if (enc16c && !B.remote) {  // all-local slice: two 16-bit codes per 4-byte load
+#pragma unroll
+        for (int p = 0; p < KP / 2; ++p) {
+            if (2 * p < B.w) {
+                double2 vv = __ldg(reinterpret_cast<const double2*>(valc + B.off + (p << 6)));
+                uint32_t cc = __ldg(reinterpret_cast<const unsigned int*>(enc16c + B.off + (p << 6)));
+                B.v[2 * p] = vv.x;
+                B.v[2 * p + 1] = vv.y;
+                B.c[2 * p] = (cc & 0xffffu) << 4;
+                B.c[2 * p + 1] = (cc >> 16) << 4;
+            }
+        }
+        return;
+    }
 #pragma unroll
     for (int p = 0; p < KP / 2; ++p) {
         if (2 * p < B.w) {
@@ -1722,6 +1744,7 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) k_pcg2(PcgArgs A) {
         rho = tz.x;
         const double* valc = A.val + ent0;
         const uint32_t* encc = A.enc + ent0;
+        const uint16_t* enc16c = A.enc16 + ent0;
         double2* yrow = A.x + row0;
         double2* prow = pg + row0;
         long long tm[6] = {0, 0, 0, 0, 0, 0};
@@ -1780,14 +1803,14 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) k_pcg2(PcgArgs A) {
                 l_pq += pi.x * qi.x + pi.y * qi.y;
             };
             {
-                slice_load(B0, valc, encc, s_ent, s_w, warp, nloc, lane, yrow, it > 0, prow);
+                slice_load(B0, valc, encc, s_ent, s_w, warp, nloc, lane, yrow, it > 0, prow, enc16c);
                 for (int ls = warp; ls < nloc; ls += 2 * NW) {
 #pragma unroll
                     for (int half = 0; half < 2; ++half) {
                         const int cur = ls + half * NW;
                         SliceBufT<KPF2>& Bc = half ? B1 : B0;
                         SliceBufT<KPF2>& Bn = half ? B0 : B1;
-                        slice_load(Bn, valc, encc, s_ent, s_w, cur + NW, nloc, lane, yrow, it > 0, prow);
+                        slice_load(Bn, valc, encc, s_ent, s_w, cur + NW, nloc, lane, yrow, it > 0, prow, enc16c);
                         if (cur < nloc) {
                             const int li = 32 * cur + lane;
                             double2 pv = Bc.p, yv = Bc.y;
@@ -2618,9 +2641,10 @@ int setup_solve(SolveSystem* S, const pgcp_solve_opts* o, cudaStream_t s) {
         S->coarse_ms = cms;
     }
     PGCP_TRY(S->enc.alloc(S->nnz, s));
+    PGCP_TRY(S->enc16.alloc(S->nnz, s));
     PGCP_TRY(S->remote.alloc(S->nslices, s));
     k_encode_cols<<<grid_for(S->nslices * 32, 256), 256, 0, s>>>(nslot, S->sl_off.p, S->nslices, S->sl_ptr.p, S->col.p,
-                                                               csize, S->enc.p, S->remote.p);
+                                                               csize, S->enc.p, S->enc16.p, S->remote.p);
     PGCP_LAUNCH_CHECK();
     S->setup_done = true;
     return PGCP_OK;
@@ -2640,6 +2664,7 @@ int run_solve(pgcp_batch* b, SolveSystem* S, const pgcp_solve_opts* o, double* z
     A.sl_mask = S->sl_mask.p;
     A.col = S->col.p;
     A.enc = S->enc.p;
+    A.enc16 = S->enc16.p;
     A.remote = S->remote.p;
     A.val = S->val.p;
     A.D = S->D.p;
@@ -2815,11 +2840,20 @@ int run_solve(pgcp_batch* b, SolveSystem* S, const pgcp_solve_opts* o, double* z
         // (k_pcg2) adds p read + write (32 B/row), the fp16 coarse weights
         // read twice (2 x 8 B/row) and the float E^-1 (8 nc ncp B per slot).
         S->iters_sum = S->iters_max = S->bytes_iter_weighted = S->ref_bytes_weighted = 0;
+        std::vector<uint8_t> hrem;
+        if (S->coarse) {  // all-local slices stream 16-bit codes in k_pcg2
+            hrem.resize(S->nslices);
+            PGCP_TRY_CUDA(cudaMemcpy(hrem.data(), S->remote.p, S->nslices, cudaMemcpyDeviceToHost));
+        }
         for (int j = 0; j < nslot; ++j) {
             int64_t e = hptr[S->h_sl_off[j + 1]] - hptr[S->h_sl_off[j]];
             double rows = (double)S->h_nu[j];
             double bytes = 12.0 * (double)e + 32.0 * rows;
             if (S->coarse) {
+                int64_t e_local = 0;
+                for (int64_t q = S->h_sl_off[j]; q < S->h_sl_off[j + 1]; ++q)
+                    if (!hrem[q]) e_local += hptr[q + 1] - hptr[q];
+                bytes -= 2.0 * (double)e_local;
                 double nc = 3.0 * (double)(S->h_abase[j + 1] - S->h_abase[j]);
                 double ncp = (double)(((int64_t)nc + 7) & ~7ll);
                 bytes += 48.0 * rows + 8.0 * nc * ncp;
