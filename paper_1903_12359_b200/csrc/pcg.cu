@@ -2820,10 +2820,20 @@ int run_solve(pgcp_batch* b, SolveSystem* S, const pgcp_solve_opts* o, double* z
                     "started %.2f ms\n", 1e-6 * (t1 - t0), 1e-6 * busy, busy / (double)(t1 - t0), first_wave,
                     1e-6 * last_start, late, hord[late], hit[hord[late]], 1e-6 * (ls - t0));
         }
-        if (S->coarse)
+        if (S->coarse) {
             fprintf(stderr, "[pcg timing] cycles/iter per CTA: A %.0f sync1 %.0f B %.0f sync2 %.0f C %.0f sync3 %.0f "
                     "(csize %d, coarse setup %.2f ms)\n", acc[0] / nct, acc[1] / nct, acc[2] / nct, acc[3] / nct,
                     acc[4] / nct, acc[5] / nct, csize, S->coarse_ms);
+            // per cluster rank: where the time of the slowest CTA goes
+            for (int r = 0; r < csize && r < 16; ++r) {
+                double pr[6] = {0, 0, 0, 0, 0, 0};
+                for (int c = 0; c < nslot; ++c)
+                    for (int q = 0; q < 6; ++q) pr[q] += (double)ht[8 * (size_t)(c * csize + r) + q];
+                const double d = (double)nslot * 128.0;
+                fprintf(stderr, "[pcg timing]   rank %d: A %.0f sync1 %.0f B %.0f sync2 %.0f C %.0f sync3 %.0f\n", r,
+                        pr[0] / d, pr[1] / d, pr[2] / d, pr[3] / d, pr[4] / d, pr[5] / d);
+            }
+        }
         else
             fprintf(stderr, "[pcg timing] cycles/iter per CTA: phaseA %.0f red1 %.0f phaseB %.0f red2 %.0f (csize %d)\n",
                     acc[0] / nct, acc[1] / nct, acc[2] / nct, acc[3] / nct, csize);

@@ -82,6 +82,16 @@ __device__ double2 cdiv(double2 a, double2 b) {
     return C((a.x * rat + a.y) * scl, (a.y * rat - a.x) * scl);
 }
 
+// |(x, y)|: sqrt(x^2 + y^2) with one rounding of the sum of squares when both
+// components are far from overflow and underflow (within an ulp of hypot);
+// hypot's scaled evaluation otherwise
+__device__ __forceinline__ double fast_hypot(double x, double y) {
+    const double ax = fabs(x), ay = fabs(y);
+    const double m = fmax(ax, ay), n = fmin(ax, ay);
+    if (m < 1e150 && (n > 1e-150 || n == 0.0) && m > 1e-150) return sqrt(fma(ax, ax, ay * ay));
+    return hypot(x, y);
+}
+
 // principal square root, glibc csqrt's case analysis
 __device__ double2 csqrt_(double2 z) {
     double re = z.x, im = z.y;
@@ -102,7 +112,7 @@ __device__ double2 csqrt_(double2 z) {
         double r = sqrt(0.5 * fabs(im));
         return C(r, copysign(r, im));
     }
-    double d = hypot(re, im);
+    double d = fast_hypot(re, im);
     double r, s;
     if (re > 0) {
         r = sqrt(0.5 * (d + re));
@@ -334,9 +344,16 @@ __device__ Rec mk_open(double2 xi, int br) {
     Rec r;
     r.kind = R_OPEN;
     r.flags = br & 0xff;
-    double s2 = hypot(xi.x, xi.y);
-    s2 = s2 * s2;
-    r.p[0] = xi.x; r.p[1] = xi.y; r.p[2] = xi.x / s2; r.p[3] = xi.y / s2;
+    const double ax = fabs(xi.x), ay = fabs(xi.y);
+    double s2;
+    if (fmax(ax, ay) < 1e150 && fmax(ax, ay) > 1e-150) {
+        s2 = fma(xi.x, xi.x, xi.y * xi.y);
+    } else {
+        s2 = hypot(xi.x, xi.y);
+        s2 = s2 * s2;
+    }
+    const double inv = 1.0 / s2;
+    r.p[0] = xi.x; r.p[1] = xi.y; r.p[2] = xi.x * inv; r.p[3] = xi.y * inv;
     for (int i = 4; i < 16; ++i) r.p[i] = 0.0;
     return r;
 }
@@ -344,7 +361,8 @@ __device__ Rec mk_close(double a, double b) {
     Rec r;
     r.kind = R_CLOSE;
     r.flags = 0;
-    r.p[0] = a; r.p[1] = b; r.p[2] = -2 * a * b / (a - b); r.p[3] = (a + b) / (a - b);
+    const double inv = 1.0 / (a - b);
+    r.p[0] = a; r.p[1] = b; r.p[2] = -2 * a * b * inv; r.p[3] = (a + b) * inv;
     for (int i = 4; i < 16; ++i) r.p[i] = 0.0;
     return r;
 }
@@ -451,6 +469,7 @@ struct Phase1Args {
     int geodesic;           // unused here
     int* prog;              // per step [2]: records published per log (streamed replay), or nullptr
     int prog_every;         // publish the counters every this many logged steps
+    long long* timing;      // optional (PGCP_WELD_TIMING): per step [publish+barrier, build, apply, zip steps] cycles
 };
 
 // Streamed replay (k_replay_stream): phase 1 publishes, per step and log, the
@@ -708,6 +727,7 @@ __global__ void __launch_bounds__(NT, 1) k_phase1c(Phase1Args A) {
         }
     };
     int err = 0, eidx = 0, eaux = 0;
+    long long tw[3] = {0, 0, 0};  // PGCP_WELD_TIMING
     Rec ra, rb;
     // ---- zip step 1: SqrtRatio
     {
@@ -728,8 +748,10 @@ __global__ void __launch_bounds__(NT, 1) k_phase1c(Phase1Args A) {
     apply_pair(ra, true, rb, true);
     // ---- zip steps j = 2..k: Open
     for (int j = 2; j <= k; ++j) {
+        const long long w0 = A.timing ? clock64() : 0;
         int gi[2] = {j, P + j};
         publish(gi, 2, 0.0);
+        const long long w1 = A.timing ? clock64() : 0;
         PParam* pp = s_param[parity];
         for (int side = 0; side < 2 && !err; ++side) {
             double2 xi = pp[side].z;
@@ -745,12 +767,25 @@ __global__ void __launch_bounds__(NT, 1) k_phase1c(Phase1Args A) {
         if (err) goto fail;
         ra = mk_open(pp[0].z, UP);
         rb = mk_open(pp[1].z, DOWN);
+        const long long w2 = A.timing ? clock64() : 0;
         if (logger) {
             log_a[na_rec++] = ra;
             log_b[nb_rec++] = rb;
         }
         progress(false);
         apply_pair(ra, true, rb, true);
+        if (A.timing) {
+            const long long w3 = clock64();
+            tw[0] += w1 - w0;
+            tw[1] += w2 - w1;
+            tw[2] += w3 - w2;
+        }
+    }
+    if (A.timing && rank == 0 && threadIdx.x == 0) {
+        A.timing[4 * step + 0] = tw[0];
+        A.timing[4 * step + 1] = tw[1];
+        A.timing[4 * step + 2] = tw[2];
+        A.timing[4 * step + 3] = k - 1;
     }
     // ---- axis Mobius sending pts[0] to infinity (welding.py:593-600)
     {
@@ -1560,6 +1595,12 @@ int run_schedule(double2* tv, int32_t nsteps, const int32_t* info, const int32_t
     // streamed replay (default): each level's replay runs concurrently with
     // its phase 1 (PGCP_WELD_STREAM=0: after it)
     const bool streamed = env_int("PGCP_WELD_STREAM", 1) != 0;
+    DevBuf<long long> d_wtime;  // PGCP_WELD_TIMING: phase-1 zip-loop cycle split per step
+    const bool wtiming = env_int("PGCP_WELD_TIMING", 0) != 0;
+    if (wtiming) {
+        PGCP_TRY(d_wtime.alloc(4 * (int64_t)nsteps, s));
+        PGCP_TRY(d_wtime.zero(s));
+    }
     DevBuf<int> d_prog, d_tmo;
     if (streamed) {
         PGCP_TRY(d_prog.alloc(2 * (int64_t)nsteps, s));
@@ -1584,6 +1625,7 @@ int run_schedule(double2* tv, int32_t nsteps, const int32_t* info, const int32_t
         a.geodesic = 0;
         a.prog = streamed ? d_prog.p + 2 * q0 : nullptr;
         a.prog_every = std::max(1, env_int("PGCP_WELD_PROG_EVERY", 8));
+        a.timing = d_wtime.p ? d_wtime.p + 4 * q0 : nullptr;
         int kmax = 0;
         for (int q = q0; q < q1; ++q) kmax = std::max(kmax, sd[q].k);
         const int NP = 2 * (kmax + 3);
@@ -1655,6 +1697,15 @@ int run_schedule(double2* tv, int32_t nsteps, const int32_t* info, const int32_t
     if (recs_host && recs_cap_total >= rec_tot)
         PGCP_TRY_CUDA(cudaMemcpyAsync(recs_host, d_recs.p, rec_tot * sizeof(Rec), cudaMemcpyDeviceToHost, s));
     PGCP_TRY_CUDA(cudaStreamSynchronize(s));
+    if (wtiming) {
+        std::vector<long long> wt(4 * (size_t)nsteps);
+        PGCP_TRY_CUDA(cudaMemcpy(wt.data(), d_wtime.p, wt.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+        for (int q = 0; q < nsteps; ++q) {
+            const double n = (double)std::max(1ll, wt[4 * q + 3]);
+            fprintf(stderr, "[weld timing] step %d k %d level %d: zip cycles/record publish+barrier %.0f build %.0f "
+                    "apply %.0f\n", q, sd[q].k, level[order[q]], wt[4 * q] / n, wt[4 * q + 1] / n, wt[4 * q + 2] / n);
+        }
+    }
     int status = PGCP_OK;
     for (int i = 0; i < nsteps; ++i) {
         int q = pos[i];
