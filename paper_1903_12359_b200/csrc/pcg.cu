@@ -2122,7 +2122,7 @@ int pick_cluster(int64_t max_slices, int32_t nslot, int32_t forced, bool coarse,
         // constant part. Spreading a few subdomains over wider clusters only
         // pays while they still run in one wave.
         double best = 0;
-        for (int cc = cmin; cc <= MAX_CLUSTER; cc *= 2) {
+        for (int cc = cmin; cc <= MAX_CLUSTER; ++cc) {  // any size: 6 / 10-CTA clusters pack GPCs well
             const int64_t ch = (max_slices + cc - 1) / cc;
             if (cc > cmin && ch < 8) break;  // keep >= 256 rows per CTA
             const size_t smem = (size_t)RED_BYTES + (size_t)3 * 32 * ch * 16 + (size_t)12 * ch + COARSE_BYTES;
