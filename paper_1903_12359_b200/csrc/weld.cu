@@ -126,6 +126,92 @@ __device__ double2 csqrt_(double2 z) {
 
 __device__ __forceinline__ int rec_side(int flags, int k) { return (int)(int8_t)((flags >> (16 + 8 * k)) & 0xff); }
 
+// Open record body (welding.py OpenRec.apply) on explicit parameters: the
+// zip loop keeps xi, Re/|xi|^2, Im/|xi|^2 in registers instead of a record
+__device__ __forceinline__ void apply_open(double2 xi, double pp, double qq, int br, double2& z, int8_t& s) {
+    if (c_eq(z, xi)) {
+        z = C(0.0, 0.0);
+        s = (int8_t)br;
+        return;
+    }
+    if (s != 0) {
+        double t = c_isinf(z) ? INFINITY : z.y;
+        double den = 1.0 - qq * t;
+        double t2 = (den == 0.0) ? INFINITY : pp * t / den;
+        if (isinf(t)) t2 = (qq != 0.0) ? -pp / qq : INFINITY;
+        if (!isfinite(t2)) {
+            z = cinf();
+            return;  // side kept
+        }
+        double sg = (t2 == 0.0) ? (double)br : (t2 > 0 ? 1.0 : -1.0);
+        double h = hypot(t2, 1.0);
+        z = C(0.0 * sg, sg * h);
+        s = (int8_t)sg;
+        return;
+    }
+    double2 L;
+    if (c_isinf(z)) {
+        L = (qq != 0.0) ? C(0.0, -(pp / qq)) : cinf();
+    } else {
+        double2 den = C(1.0 - qq * z.y, qq * z.x);
+        L = c_zero(den) ? cinf() : cdiv(C(pp * z.x, pp * z.y), den);
+    }
+    if (!c_fin(L)) {
+        z = cinf();
+    } else if (cabs_gt(L, 1e100)) {
+        z = (L.x >= 0) ? L : cneg(L);
+    } else {
+        z = csqrt_(csub(cmul(L, L), C(1.0, 0.0)));
+    }
+    s = 0;
+    return;
+}
+
+// Close record body (welding.py CloseRec.apply) on explicit parameters
+__device__ __forceinline__ void apply_close(double ai, double bi, double c, double d, double2& z, int8_t& s) {
+    if (c_eq(z, C(0.0, ai)) || c_eq(z, C(0.0, bi))) {
+        z = C(0.0, 0.0);
+        s = 0;
+        return;
+    }
+    if (s != 0) {
+        double t = c_isinf(z) ? INFINITY : z.y;
+        double den = c + d * t;
+        double t2 = (den == 0.0) ? INFINITY : t / den;
+        if (isinf(t)) t2 = (d != 0.0) ? 1.0 / d : INFINITY;
+        if (!isfinite(t2)) {
+            z = cinf();
+            return;  // side kept
+        }
+        if (fabs(t2) > 1.0) {
+            double mag = (fabs(t2) < 1e100) ? sqrt(fmax(t2 * t2 - 1.0, 0.0)) : fabs(t2);
+            double sg = t2 > 0 ? 1.0 : -1.0;
+            z = C(0.0 * sg, sg * mag);
+            s = t2 > 0 ? UP : DOWN;
+        } else {
+            z = C(sqrt(fmax(1.0 - t2 * t2, 0.0)), 0.0);
+            s = 0;
+        }
+        return;
+    }
+    double2 T;
+    if (c_isinf(z)) {
+        T = (d != 0.0) ? C(0.0, 1.0 / d) : cinf();
+    } else {
+        double2 den = C(c + d * z.y, -d * z.x);
+        T = c_zero(den) ? cinf() : cdiv(z, den);
+    }
+    if (!c_fin(T)) {
+        z = cinf();
+    } else if (cabs_gt(T, 1e100)) {
+        z = (T.x >= 0) ? T : cneg(T);
+    } else {
+        z = csqrt_(cadd(cmul(T, T), C(1.0, 0.0)));
+    }
+    s = 0;
+    return;
+}
+
 // one record on one point (welding.py:251-509)
 __device__ __forceinline__ void apply_rec(const Rec& r, double2& z, int8_t& s) {
     const double* p = r.p;
@@ -184,91 +270,12 @@ __device__ __forceinline__ void apply_rec(const Rec& r, double2& z, int8_t& s) {
             }
             return;
         }
-        case R_OPEN: {
-            double2 xi = C(p[0], p[1]);
-            double pp = p[2], qq = p[3];
-            int br = (int)(int8_t)(r.flags & 0xff);
-            if (c_eq(z, xi)) {
-                z = C(0.0, 0.0);
-                s = (int8_t)br;
-                return;
-            }
-            if (s != 0) {
-                double t = c_isinf(z) ? INFINITY : z.y;
-                double den = 1.0 - qq * t;
-                double t2 = (den == 0.0) ? INFINITY : pp * t / den;
-                if (isinf(t)) t2 = (qq != 0.0) ? -pp / qq : INFINITY;
-                if (!isfinite(t2)) {
-                    z = cinf();
-                    return;  // side kept
-                }
-                double sg = (t2 == 0.0) ? (double)br : (t2 > 0 ? 1.0 : -1.0);
-                double h = hypot(t2, 1.0);
-                z = C(0.0 * sg, sg * h);
-                s = (int8_t)sg;
-                return;
-            }
-            double2 L;
-            if (c_isinf(z)) {
-                L = (qq != 0.0) ? C(0.0, -(pp / qq)) : cinf();
-            } else {
-                double2 den = C(1.0 - qq * z.y, qq * z.x);
-                L = c_zero(den) ? cinf() : cdiv(C(pp * z.x, pp * z.y), den);
-            }
-            if (!c_fin(L)) {
-                z = cinf();
-            } else if (cabs_gt(L, 1e100)) {
-                z = (L.x >= 0) ? L : cneg(L);
-            } else {
-                z = csqrt_(csub(cmul(L, L), C(1.0, 0.0)));
-            }
-            s = 0;
+        case R_OPEN:
+            apply_open(C(p[0], p[1]), p[2], p[3], (int)(int8_t)(r.flags & 0xff), z, s);
             return;
-        }
-        case R_CLOSE: {
-            double ai = p[0], bi = p[1], c = p[2], d = p[3];
-            if (c_eq(z, C(0.0, ai)) || c_eq(z, C(0.0, bi))) {
-                z = C(0.0, 0.0);
-                s = 0;
-                return;
-            }
-            if (s != 0) {
-                double t = c_isinf(z) ? INFINITY : z.y;
-                double den = c + d * t;
-                double t2 = (den == 0.0) ? INFINITY : t / den;
-                if (isinf(t)) t2 = (d != 0.0) ? 1.0 / d : INFINITY;
-                if (!isfinite(t2)) {
-                    z = cinf();
-                    return;  // side kept
-                }
-                if (fabs(t2) > 1.0) {
-                    double mag = (fabs(t2) < 1e100) ? sqrt(fmax(t2 * t2 - 1.0, 0.0)) : fabs(t2);
-                    double sg = t2 > 0 ? 1.0 : -1.0;
-                    z = C(0.0 * sg, sg * mag);
-                    s = t2 > 0 ? UP : DOWN;
-                } else {
-                    z = C(sqrt(fmax(1.0 - t2 * t2, 0.0)), 0.0);
-                    s = 0;
-                }
-                return;
-            }
-            double2 T;
-            if (c_isinf(z)) {
-                T = (d != 0.0) ? C(0.0, 1.0 / d) : cinf();
-            } else {
-                double2 den = C(c + d * z.y, -d * z.x);
-                T = c_zero(den) ? cinf() : cdiv(z, den);
-            }
-            if (!c_fin(T)) {
-                z = cinf();
-            } else if (cabs_gt(T, 1e100)) {
-                z = (T.x >= 0) ? T : cneg(T);
-            } else {
-                z = csqrt_(cadd(cmul(T, T), C(1.0, 0.0)));
-            }
-            s = 0;
+        case R_CLOSE:
+            apply_close(p[0], p[1], p[2], p[3], z, s);
             return;
-        }
         case R_SQ: {
             double2 q = C(p[0], p[1]);
             bool qinf = c_isinf(q);
@@ -340,10 +347,8 @@ __device__ Rec mk_sqr(double2 z0, double2 z1, int br) {
     for (int i = 4; i < 16; ++i) r.p[i] = 0.0;
     return r;
 }
-__device__ Rec mk_open(double2 xi, int br) {
-    Rec r;
-    r.kind = R_OPEN;
-    r.flags = br & 0xff;
+// (Re, Im) / |xi|^2 of an Open record
+__device__ __forceinline__ void open_params(double2 xi, double& pp, double& qq) {
     const double ax = fabs(xi.x), ay = fabs(xi.y);
     double s2;
     if (fmax(ax, ay) < 1e150 && fmax(ax, ay) > 1e-150) {
@@ -353,18 +358,39 @@ __device__ Rec mk_open(double2 xi, int br) {
         s2 = s2 * s2;
     }
     const double inv = 1.0 / s2;
-    r.p[0] = xi.x; r.p[1] = xi.y; r.p[2] = xi.x * inv; r.p[3] = xi.y * inv;
+    pp = xi.x * inv;
+    qq = xi.y * inv;
+}
+__device__ Rec mk_open_p(double2 xi, double pp, double qq, int br) {
+    Rec r;
+    r.kind = R_OPEN;
+    r.flags = br & 0xff;
+    r.p[0] = xi.x; r.p[1] = xi.y; r.p[2] = pp; r.p[3] = qq;
+    for (int i = 4; i < 16; ++i) r.p[i] = 0.0;
+    return r;
+}
+__device__ Rec mk_open(double2 xi, int br) {
+    double pp, qq;
+    open_params(xi, pp, qq);
+    return mk_open_p(xi, pp, qq, br);
+}
+__device__ __forceinline__ void close_params(double a, double b, double& c, double& d) {
+    const double inv = 1.0 / (a - b);
+    c = -2 * a * b * inv;
+    d = (a + b) * inv;
+}
+__device__ Rec mk_close_p(double a, double b, double c, double d) {
+    Rec r;
+    r.kind = R_CLOSE;
+    r.flags = 0;
+    r.p[0] = a; r.p[1] = b; r.p[2] = c; r.p[3] = d;
     for (int i = 4; i < 16; ++i) r.p[i] = 0.0;
     return r;
 }
 __device__ Rec mk_close(double a, double b) {
-    Rec r;
-    r.kind = R_CLOSE;
-    r.flags = 0;
-    const double inv = 1.0 / (a - b);
-    r.p[0] = a; r.p[1] = b; r.p[2] = -2 * a * b * inv; r.p[3] = (a + b) * inv;
-    for (int i = 4; i < 16; ++i) r.p[i] = 0.0;
-    return r;
+    double c, d;
+    close_params(a, b, c, d);
+    return mk_close_p(a, b, c, d);
 }
 __device__ Rec mk_sq(double2 q) {
     Rec r;
@@ -765,15 +791,29 @@ __global__ void __launch_bounds__(NT, 1) k_phase1c(Phase1Args A) {
         }
         parity ^= 1;
         if (err) goto fail;
-        ra = mk_open(pp[0].z, UP);
-        rb = mk_open(pp[1].z, DOWN);
+        // the Open records as registers (xi, Re/|xi|^2, Im/|xi|^2), not as
+        // record structs: a struct the compiler keeps on the stack would be
+        // re-read from local memory by every point after every barrier
+        const double2 xa = pp[0].z, xb = pp[1].z;
+        double pa, qa, pb, qb;
+        open_params(xa, pa, qa);
+        open_params(xb, pb, qb);
         const long long w2 = A.timing ? clock64() : 0;
         if (logger) {
-            log_a[na_rec++] = ra;
-            log_b[nb_rec++] = rb;
+            log_a[na_rec++] = mk_open_p(xa, pa, qa, UP);
+            log_b[nb_rec++] = mk_open_p(xb, pb, qb, DOWN);
         }
         progress(false);
-        apply_pair(ra, true, rb, true);
+        for (int g = lo + threadIdx.x; g < hi; g += NT) {
+            double2 z = pts[g - lo];
+            int8_t s8 = sides[g - lo];
+            if (g >= P)
+                apply_open(xb, pb, qb, DOWN, z, s8);
+            else
+                apply_open(xa, pa, qa, UP, z, s8);
+            pts[g - lo] = z;
+            sides[g - lo] = s8;
+        }
         if (A.timing) {
             const long long w3 = clock64();
             tw[0] += w1 - w0;
@@ -835,13 +875,21 @@ __global__ void __launch_bounds__(NT, 1) k_phase1c(Phase1Args A) {
         }
         parity ^= 1;
         if (err) goto fail;
-        ra = mk_close(al.y, be.y);
+        double cc, dd;  // the Close record as registers (see the zip loop)
+        close_params(al.y, be.y, cc, dd);
         if (logger) {
-            log_a[na_rec++] = ra;
-            log_b[nb_rec++] = ra;
+            const Rec rc = mk_close_p(al.y, be.y, cc, dd);
+            log_a[na_rec++] = rc;
+            log_b[nb_rec++] = rc;
         }
         progress(false);
-        apply_pair(ra, true, ra, true);
+        for (int g = lo + threadIdx.x; g < hi; g += NT) {
+            double2 z = pts[g - lo];
+            int8_t s8 = sides[g - lo];
+            apply_close(al.y, be.y, cc, dd, z, s8);
+            pts[g - lo] = z;
+            sides[g - lo] = s8;
+        }
     }
     // ---- far ends: SquareMobius; stage max of |va| (arc + aux) for the deferred check
     {
