@@ -210,6 +210,14 @@ PGCP_API int pgcp_face_layout(const double* V, const int32_t* F, int64_t m, doub
 PGCP_API int pgcp_beltrami(const double* src, const int32_t* src_faces, const double* tgt, const int32_t* tgt_faces,
                            int64_t m, double* mu, int64_t* first_degenerate, void* stream);
 
+/* lbs_stiffness (assemble.py:124-164): linear-element stiffness of the
+ * operator with Beltrami coefficient mu on the embedding z (absolute face
+ * areas), for every submesh, on the batch Laplacian's CSR pattern
+ * (PGCP_ARR_L_ROWPTR / PGCP_ARR_L_COL).
+ *   z device complex [sum_n]; mu device complex [m] per parent face;
+ *   kval device f64 [nnz]. Synchronises. */
+PGCP_API int pgcp_batch_lbs_stiffness(pgcp_batch* b, const double* z, const double* mu, double* kval, void* stream);
+
 /* qc_correct (assemble.py:174-217) of the listed submeshes, batched, in place:
  * while a submesh has faces with signed area <= 0 (at most max_iter times):
  * mu = capped Beltrami coefficient of embedding -> layout, K = linear
@@ -334,6 +342,20 @@ PGCP_API int pgcp_batch_stitch(pgcp_batch* b, const double* z, int mode, double 
 PGCP_API int pgcp_distortion(const double* V, const int32_t* F, int64_t n, int64_t m, const double* coords,
                              int mode_sphere, double* d, uint8_t* valid, double* summary, uint64_t* hist,
                              int64_t hist_cap, void* stream);
+
+/* corner_angles / corner_angles_sphere (metrics.py:31-58): per-corner angle
+ * and degeneracy flag of every face.
+ *   points  device: kind 0 complex [n], 1 f64 [2n], 2 f64 [3n], 3 unit-sphere f64 [3n]
+ *           (edges projected on the corner's tangent plane)
+ *   ang     device f64 [3m]; bad device uint8 [3m] (a zero-length edge) */
+PGCP_API int pgcp_corner_angles(const double* points, int kind, const int32_t* F, int64_t m, double* ang,
+                                uint8_t* bad, void* stream);
+
+/* area_distortion (metrics.py:89-104): per face the log of the ratio of the
+ * normalised parametric and original areas; zero-area faces invalid (d = 0).
+ *   coords device complex [n] or f64 [3n] (mode_sphere); d f64 [m]; valid uint8 [m] */
+PGCP_API int pgcp_area_distortion(const double* V, const int32_t* F, int64_t n, int64_t m, const double* coords,
+                                  int mode_sphere, double* d, uint8_t* valid, void* stream);
 
 /* host-side weld-schedule planner (partition.py:236-324): see planner.cpp */
 PGCP_API int pgcp_plan_weld_schedule(const int64_t* cyc, const int64_t* cyc_off, int32_t K,

@@ -74,6 +74,9 @@ _SIGS = {
     "pgcp_launch_count": ([], ctypes.c_ulonglong),
     "pgcp_face_layout": ([_VP, _VP, _I64, _VP, _VP], ctypes.c_int),
     "pgcp_beltrami": ([_VP, _VP, _VP, _VP, _I64, _VP, _PI64, _VP], ctypes.c_int),
+    "pgcp_corner_angles": ([_VP, ctypes.c_int, _VP, _I64, _VP, _VP, _VP], ctypes.c_int),
+    "pgcp_area_distortion": ([_VP, _VP, _I64, _I64, _VP, ctypes.c_int, _VP, _VP, _VP], ctypes.c_int),
+    "pgcp_batch_lbs_stiffness": ([_VP, _VP, _VP, _VP, _VP], ctypes.c_int),
     "pgcp_batch_qc_repair": ([_VP, _VP, _I32, _VP, _VP, _I64, _I32, _D, ctypes.POINTER(SolveOpts), _VP, _VP, _VP,
                               _VP], ctypes.c_int),
 }

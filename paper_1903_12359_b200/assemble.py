@@ -182,6 +182,31 @@ def check_bijectivity(mu, threshold=0.99):
     return BijectivityReport(np.flatnonzero(mag >= threshold), float(mag.max()) if mag.size else 0.0, threshold)
 
 
+def lbs_stiffness(coords, faces, mu):
+    """Stiffness matrix (scipy CSR, n x n) of the divergence-form operator
+    whose solutions have Beltrami coefficient mu (per face) on the planar
+    mesh, linear elements, absolute face areas (assemble.py:124-164). The
+    element rows are assembled on the device on the mesh's own CSR pattern."""
+    from scipy import sparse
+    from .device import DeviceBatch, device, ptr, stream_handle, to_dev
+    z = np.atleast_1d(np.asarray(coords, dtype=np.complex128))
+    n = len(z)
+    F = np.asarray(faces)
+    b = DeviceBatch(np.column_stack([z.real, z.imag, np.zeros(n)]), F, no_cuts=True)
+    b.laplacian()
+    vmap = b.host(nat.ARR_VMAP, torch.int32).astype(np.int64)
+    zl = to_dev(z[vmap], torch.complex128)
+    mud = to_dev(np.asarray(mu, dtype=np.complex128), torch.complex128)
+    nnz = b.info()[nat.INFO_NNZ_L]
+    kval = torch.empty(nnz, dtype=torch.float64, device=device())
+    nat.check(nat.lib().pgcp_batch_lbs_stiffness(b.h, ptr(zl), ptr(mud), ptr(kval), stream_handle()))
+    rp = b.host(nat.ARR_L_ROWPTR, torch.int64)
+    col = b.host(nat.ARR_L_COL, torch.int32).astype(np.int64)
+    val = kval.cpu().numpy()
+    rows = np.repeat(vmap, np.diff(rp))
+    return sparse.csr_matrix((val, (rows, vmap[col])), shape=(n, n))
+
+
 @dataclass
 class RepairReport:
     iterations: int

@@ -77,6 +77,7 @@ int export_system(pgcp_batch* b, int which, int32_t comp, int64_t* dims, int32_t
 int face_layout(const double* V, const int32_t* F, int64_t m, double* out, cudaStream_t s);
 int beltrami_per_face(const double* src, const int32_t* sf, const double* tgt, const int32_t* tf, int64_t m,
                       double* mu, int64_t* first_degenerate, cudaStream_t s);
+int lbs_stiffness(pgcp_batch* b, const double* z, const double* mu, double* kval, cudaStream_t s);
 int qc_repair(pgcp_batch* b, const int32_t* comps, int32_t ncomp, const double* layout, const int32_t* fixed_gid,
               int64_t nfixed, int32_t max_iter, double cap, const pgcp_solve_opts* o, double* z, int32_t* info,
               uint8_t* flipped, cudaStream_t s);

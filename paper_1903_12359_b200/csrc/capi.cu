@@ -261,6 +261,15 @@ int pgcp_beltrami(const double* src, const int32_t* src_faces, const double* tgt
     return beltrami_per_face(src, src_faces, tgt, tgt_faces, m, mu, first_degenerate, as_stream(stream));
 }
 
+int pgcp_batch_lbs_stiffness(pgcp_batch* b, const double* z, const double* mu, double* kval, void* stream) {
+    if (!b || !z || !mu || !kval) {
+        set_error("pgcp_batch_lbs_stiffness: invalid arguments");
+        return PGCP_E_INVALID;
+    }
+    PGCP_TRY_CUDA(cudaSetDevice(b->device));
+    return lbs_stiffness(b, z, mu, kval, as_stream(stream));
+}
+
 int pgcp_batch_qc_repair(pgcp_batch* b, const int32_t* comps, int32_t ncomp, const double* layout,
                          const int32_t* fixed_gid, int64_t nfixed, int32_t max_iter, double cap,
                          const pgcp_solve_opts* opts, double* z, int32_t* info, uint8_t* flipped, void* stream) {

@@ -217,6 +217,45 @@ __global__ void k_distortion(const double* __restrict__ V, const int32_t* __rest
     }
 }
 
+// corner_angles / corner_angles_sphere (metrics.py:31-58): per corner the
+// angle between the two edges leaving it. kind 0: complex planar points,
+// 1: real 2D, 2: real 3D, 3: unit-sphere points (edges projected on the
+// tangent plane of the corner).
+__global__ void k_corner_angles(const double* __restrict__ P, int kind, const int32_t* __restrict__ F, int64_t m,
+                                double* __restrict__ ang, uint8_t* __restrict__ bad) {
+    GRID_STRIDE(f, m) {
+        const int id[3] = {F[3 * f], F[3 * f + 1], F[3 * f + 2]};
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const int i = id[c], j = id[(c + 1) % 3], k = id[(c + 2) % 3];
+            double a;
+            bool b;
+            if (kind == 0) {
+                const double2* Z = reinterpret_cast<const double2*>(P);
+                corner_angle2(Z[i], Z[j], Z[k], &a, &b);
+            } else if (kind == 1) {
+                corner_angle2(make_double2(P[2 * i], P[2 * i + 1]), make_double2(P[2 * j], P[2 * j + 1]),
+                              make_double2(P[2 * k], P[2 * k + 1]), &a, &b);
+            } else if (kind == 2) {
+                corner_angle3(P + 3 * i, P + 3 * j, P + 3 * k, &a, &b);
+            } else {
+                const double a0 = P[3 * i], a1 = P[3 * i + 1], a2 = P[3 * i + 2];
+                const double db = (P[3 * j] * a0 + P[3 * j + 2] * a2) + P[3 * j + 1] * a1;
+                const double dc = (P[3 * k] * a0 + P[3 * k + 2] * a2) + P[3 * k + 1] * a1;
+                double tb[3], tc[3];
+                for (int q = 0; q < 3; ++q) {
+                    tb[q] = P[3 * j + q] - db * P[3 * i + q];
+                    tc[q] = P[3 * k + q] - dc * P[3 * i + q];
+                }
+                const double o[3] = {0, 0, 0};
+                corner_angle3(o, tb, tc, &a, &b);
+            }
+            ang[3 * f + c] = a;
+            bad[3 * f + c] = b;
+        }
+    }
+}
+
 // deterministic block partial sums: out[block] = sum of f(i) over its range
 template <class Fn>
 __global__ void k_partial_sum(int64_t n, Fn fn, double* __restrict__ part) {
@@ -261,6 +300,18 @@ __global__ void k_area_logratio(int64_t m, const double* __restrict__ a_new, con
     GRID_STRIDE(f, m) {
         double an = a_new[f];
         absd[f] = an > 0 ? fabs(log((an / sum_new) / (a_ref[f] / sum_ref))) : -1.0;
+    }
+}
+
+// area_distortion (metrics.py:89-104): signed log of the normalised area
+// ratio per face; faces of zero parametric area flagged invalid (d = 0)
+__global__ void k_area_log_signed(int64_t m, const double* __restrict__ a_new, const double* __restrict__ a_ref,
+                                  double sum_new, double sum_ref, double* __restrict__ d, uint8_t* __restrict__ valid) {
+    GRID_STRIDE(f, m) {
+        const double an = a_new[f];
+        const bool ok = an > 0;
+        d[f] = ok ? log((an / sum_new) / (a_ref[f] / sum_ref)) : 0.0;
+        valid[f] = ok;
     }
 }
 
@@ -582,6 +633,44 @@ PGCP_API int pgcp_batch_stitch(pgcp_batch* b, const double* z, int mode, double 
         stats[4] = PGCP_E_SOLVE;
         return PGCP_E_SOLVE;
     }
+    return PGCP_OK;
+}
+
+PGCP_API int pgcp_corner_angles(const double* points, int kind, const int32_t* F, int64_t m, double* ang,
+                                uint8_t* bad, void* stream) {
+    if (m < 0 || kind < 0 || kind > 3 || (m > 0 && (!points || !F || !ang || !bad))) {
+        set_error("pgcp_corner_angles: invalid arguments");
+        return PGCP_E_INVALID;
+    }
+    if (m == 0) return PGCP_OK;
+    k_corner_angles<<<grid_for(m, 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(points, kind, F, m, ang,
+                                                                                          bad);
+    PGCP_LAUNCH_CHECK();
+    return PGCP_OK;
+}
+
+PGCP_API int pgcp_area_distortion(const double* V, const int32_t* F, int64_t n, int64_t m, const double* coords,
+                                  int mode_sphere, double* d, uint8_t* valid, void* stream) {
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (!V || !F || !coords || !d || !valid || m <= 0) {
+        set_error("pgcp_area_distortion: invalid arguments");
+        return PGCP_E_INVALID;
+    }
+    DevBuf<double> dc, absd, a_new, a_ref, part;
+    DevBuf<uint8_t> vc;
+    PGCP_TRY(dc.alloc(3 * m, s));
+    PGCP_TRY(vc.alloc(3 * m, s));
+    PGCP_TRY(absd.alloc(3 * m, s));
+    PGCP_TRY(a_new.alloc(m, s));
+    PGCP_TRY(a_ref.alloc(m, s));
+    PGCP_TRY(part.alloc(SUM_BLOCKS, s));
+    k_distortion<<<grid_for(m, 256), 256, 0, s>>>(V, F, m, coords, mode_sphere, dc.p, vc.p, absd.p, a_new.p, a_ref.p);
+    PGCP_LAUNCH_CHECK();
+    double sn = 0, sr = 0;
+    PGCP_TRY(dsum(m, Plain{a_new.p}, part, &sn, s));
+    PGCP_TRY(dsum(m, Plain{a_ref.p}, part, &sr, s));
+    k_area_log_signed<<<grid_for(m, 256), 256, 0, s>>>(m, a_new.p, a_ref.p, sn, sr, d, valid);
+    PGCP_LAUNCH_CHECK();
     return PGCP_OK;
 }
 

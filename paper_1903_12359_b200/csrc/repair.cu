@@ -115,6 +115,7 @@ struct RepairArgs {
     const uint8_t* active;  // per submesh
     const double2* z;
     double cap;
+    const double2* mu;      // per parent face: given coefficient (lbs_stiffness), or nullptr
 };
 
 // lbs_stiffness (assemble.py:124-164): the 3x3 element matrix row of corner i
@@ -125,15 +126,20 @@ __device__ bool face_row(const RepairArgs& A, int64_t f, int c, int i, int gids[
         gids[k] = lv_find(A.lv_off, A.lv_comp, A.lv_gid, A.F[3 * f + k], c);
         s[k] = A.z[gids[k]];
     }
-    if (A.layout) {
-#pragma unroll
-        for (int k = 0; k < 3; ++k) t[k] = A.layout[3 * f + k];
+    double2 mu;
+    if (A.mu) {
+        mu = A.mu[f];
     } else {
-        layout_of(A.V, A.F, f, t);
+        if (A.layout) {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) t[k] = A.layout[3 * f + k];
+        } else {
+            layout_of(A.V, A.F, f, t);
+        }
+        double2 mi;
+        if (!beltrami(s, t, &mi)) return false;
+        mu = cap_mu(mi, A.cap);
     }
-    double2 mi;
-    if (!beltrami(s, t, &mi)) return false;
-    const double2 mu = cap_mu(mi, A.cap);
     const double rho = mu.x, tau = mu.y;
     const double den = fmax(1.0 - rho * rho - tau * tau, 1e-12);
     const double a1 = ((rho - 1.0) * (rho - 1.0) + tau * tau) / den;
@@ -326,6 +332,7 @@ int qc_repair(pgcp_batch* b, const int32_t* comps, int32_t ncomp, const double* 
     A.active = d_act.p;
     A.z = reinterpret_cast<const double2*>(z);
     A.cap = cap;
+    A.mu = nullptr;
     std::vector<int32_t> hc(b->K);
     // flips of the active submeshes (and, on the last count, the face flags)
     auto count = [&](bool last) -> int {
@@ -399,6 +406,40 @@ int qc_repair(pgcp_batch* b, const int32_t* comps, int32_t ncomp, const double* 
         info[4 * q + 2] = after[c] == 0;
         info[4 * q + 3] = after[c];
     }
+    return PGCP_OK;
+}
+
+// lbs_stiffness (assemble.py:124-164) of every submesh for a given per-face
+// coefficient, on the Laplacian's CSR pattern
+int lbs_stiffness(pgcp_batch* b, const double* z, const double* mu, double* kval, cudaStream_t s) {
+    if (!b->has_laplacian) PGCP_TRY(build_laplacian(b, nullptr, s));
+    DevBuf<uint8_t> d_act;
+    PGCP_TRY(d_act.alloc(b->K, s));
+    PGCP_TRY(d_act.fill_bytes(1, s));
+    RepairArgs A;
+    A.V = b->V.p;
+    A.F = b->F.p;
+    A.layout = nullptr;
+    A.inc_off = b->inc_off.p;
+    A.inc = b->inc.p;
+    A.face_comp = b->face_comp.p;
+    A.vmap = b->vmap.p;
+    A.comp_of = b->comp_of_gid.p;
+    A.lv_off = b->lv_off.p;
+    A.lv_comp = b->lv_comp.p;
+    A.lv_gid = b->lv_gid.p;
+    A.vert_off = b->vert_off.p;
+    A.row_ptr = b->row_ptr.p;
+    A.col = b->col.p;
+    A.active = d_act.p;
+    A.z = reinterpret_cast<const double2*>(z);
+    A.cap = 1.0;
+    A.mu = reinterpret_cast<const double2*>(mu);
+    DevBuf<DevErr> err;
+    PGCP_TRY(init_err(err, s));
+    k_lbs_rows<<<grid_for(b->sum_n, 128), 128, 0, s>>>(A, b->sum_n, kval, err.p);
+    PGCP_LAUNCH_CHECK();
+    PGCP_TRY_CUDA(cudaStreamSynchronize(s));
     return PGCP_OK;
 }
 

@@ -1,5 +1,6 @@
 """Distortion measurement (drop-in for `metrics.py`), computed on the device
-(metrics.cu). The Mobius area post-optimisation (`metrics.py:183-270`) is out
+(metrics.cu): corner angles, angular and area distortion, the report's
+summaries. The Mobius area post-optimisation (`metrics.py:183-270`) is out
 of scope."""
 
 import ctypes
@@ -69,23 +70,48 @@ def angular_distortion(mesh, param):
 
 
 def area_distortion(mesh, param):
-    """Per-face log of the normalised area ratio (metrics.py:89-104). Host
-    form of the API helper; the report uses the device summary."""
+    """Per-face log of the normalised area ratio (metrics.py:89-104), on the
+    device; faces of zero parametric area are invalid (d = 0)."""
+    from .device import device, ptr, stream_handle, to_dev
     coords, mode = _param_coords(param)
-    coords = coords.cpu().numpy() if isinstance(coords, torch.Tensor) else np.asarray(coords)
-    F = np.asarray(mesh.faces)
-    if mode == "sphere":
-        p = coords[F]
-        a_new = 0.5 * np.linalg.norm(np.cross(p[:, 1] - p[:, 0], p[:, 2] - p[:, 0]), axis=1)
-    else:
-        z = np.asarray(coords, dtype=np.complex128)[F]
-        d1, d2 = z[:, 1] - z[:, 0], z[:, 2] - z[:, 0]
-        a_new = 0.5 * np.abs(d1.real * d2.imag - d1.imag * d2.real)
-    a_ref = mesh.face_areas()
-    valid = a_new > 0
-    d = np.zeros(len(a_ref))
-    d[valid] = np.log((a_new / a_new.sum())[valid] / (a_ref / a_ref.sum())[valid])
-    return d, valid
+    sphere = mode == "sphere"
+    Vd = to_dev(np.asarray(mesh.vertices, dtype=np.float64), torch.float64)
+    Fd = to_dev(np.asarray(mesh.faces), torch.int32)
+    cd = coords.to(device()).contiguous() if isinstance(coords, torch.Tensor) else \
+        to_dev(np.asarray(coords, dtype=np.float64 if sphere else np.complex128))
+    m = int(Fd.shape[0])
+    d = torch.empty(m, dtype=torch.float64, device=device())
+    valid = torch.empty(m, dtype=torch.uint8, device=device())
+    nat.check(nat.lib().pgcp_area_distortion(ptr(Vd), ptr(Fd), int(Vd.shape[0]), m, ptr(cd), int(sphere), ptr(d),
+                                             ptr(valid), stream_handle()))
+    return d.cpu().numpy(), valid.cpu().numpy().astype(bool)
+
+
+def _corner_angles(points, faces, kind):
+    from .device import device, ptr, stream_handle, to_dev
+    F = to_dev(np.asarray(faces), torch.int32)
+    P = to_dev(points)
+    m = int(F.shape[0])
+    ang = torch.empty((m, 3), dtype=torch.float64, device=device())
+    bad = torch.empty((m, 3), dtype=torch.uint8, device=device())
+    nat.check(nat.lib().pgcp_corner_angles(ptr(P), kind, ptr(F), m, ptr(ang), ptr(bad), stream_handle()))
+    return ang.cpu().numpy(), bad.cpu().numpy().astype(bool)
+
+
+def corner_angles(points, faces):
+    """(m, 3) corner angles of a planar (complex or 2D) or 3D vertex array and
+    the degeneracy mask (metrics.py:31-44), on the device."""
+    p = np.asarray(points)
+    if np.iscomplexobj(p) or p.ndim == 1:
+        return _corner_angles(np.asarray(p, dtype=np.complex128), faces, 0)
+    p = np.ascontiguousarray(p, dtype=np.float64)
+    return _corner_angles(p, faces, 1 if p.shape[1] == 2 else 2)
+
+
+def corner_angles_sphere(points, faces):
+    """Spherical corner angles through the tangent-plane projection of the
+    edges (metrics.py:47-58), on the device."""
+    return _corner_angles(np.ascontiguousarray(points, dtype=np.float64), faces, 3)
 
 
 def summarize(values):
