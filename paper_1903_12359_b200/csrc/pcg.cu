@@ -39,6 +39,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 
 #include "batch.cuh"
 
@@ -2072,16 +2073,39 @@ __global__ void k_flat_checks(const int32_t* __restrict__ comps, const int64_t* 
 // ---------------------------------------------------------------------------
 // host side
 
+// Kernel attributes are set to fixed values (the largest dynamic shared
+// memory the device allows next to the kernel's static shared memory, and
+// non-portable cluster sizes): the flatten's worker thread and the caller's
+// thread launch and query these kernels concurrently, so per-launch values
+// could race between a set and a launch.
+template <class K>
+int set_kernel_attrs(K kern) {
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lock(mu);
+    int dev = 0, optin = 0;
+    PGCP_TRY_CUDA(cudaGetDevice(&dev));
+    PGCP_TRY_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    cudaFuncAttributes fa;
+    PGCP_TRY_CUDA(cudaFuncGetAttributes(&fa, kern));
+    PGCP_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       optin - (int)fa.sharedSizeBytes));
+    PGCP_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    return PGCP_OK;
+}
+
 // clusters of k_pcg2 that can be resident at once for a cluster shape
 int max_active_clusters(int csize, size_t smem) {
+    // the flatten (worker thread) and the harmonic preparation (caller's
+    // thread) choose their shapes concurrently
+    static std::mutex mu;
     static std::vector<std::pair<long long, int>> cache;
+    std::lock_guard<std::mutex> lock(mu);
     const long long key = (long long)csize << 32 | (long long)smem;
     for (auto& kv : cache)
         if (kv.first == key) return kv.second;
     auto kern = k_pcg2<512, float2>;
     int n = 0;
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess &&
-        (csize <= 8 || cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess)) {
+    if (set_kernel_attrs(kern) == PGCP_OK) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)csize, 1, 1);
         cfg.blockDim = dim3(512, 1, 1);
@@ -2148,8 +2172,7 @@ int pick_cluster(int64_t max_slices, int32_t nslot, int32_t forced, bool coarse,
 template <int NT, bool PF>
 int launch_pcg_t(SolveSystem* S, const PcgArgs& args, int csize, size_t smem, cudaStream_t s) {
     auto kern = k_pcg<NT, PF>;
-    PGCP_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    if (csize > 8) PGCP_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    PGCP_TRY(set_kernel_attrs(kern));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(S->nslot * csize), 1, 1);
     cfg.blockDim = dim3(NT, 1, 1);
@@ -2177,8 +2200,7 @@ int launch_pcg_t(SolveSystem* S, const PcgArgs& args, int csize, size_t smem, cu
 template <int NT, typename ET>
 int launch_pcg2_t(SolveSystem* S, const PcgArgs& args, int csize, size_t smem, cudaStream_t s) {
     auto kern = k_pcg2<NT, ET>;
-    PGCP_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    if (csize > 8) PGCP_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    PGCP_TRY(set_kernel_attrs(kern));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(S->nslot * csize), 1, 1);
     cfg.blockDim = dim3(NT, 1, 1);
@@ -2381,8 +2403,7 @@ int build_coarse(SolveSystem* S, int csize, cudaStream_t s) {
         };
         while (CS < 16 && inv_smem(CS) > 200 * 1024) CS *= 2;
         const size_t smem = inv_smem(CS);
-        PGCP_TRY_CUDA(cudaFuncSetAttribute(k_coarse_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        if (CS > 8) PGCP_TRY_CUDA(cudaFuncSetAttribute(k_coarse_inv, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        PGCP_TRY(set_kernel_attrs(k_coarse_inv));
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)(nslot * CS), 1, 1);
         cfg.blockDim = dim3(INV_THREADS, 1, 1);

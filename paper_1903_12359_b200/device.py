@@ -5,6 +5,7 @@ torch.distributed; every computation is a libpgcp_b200 kernel.
 """
 
 import ctypes
+import threading
 import warnings
 
 import numpy as np
@@ -94,6 +95,7 @@ class DeviceBatch:
         self.h = h
         self._info = None
         self._cache = {}
+        self._lock = threading.Lock()
 
     # -- lifetime
     def close(self):
@@ -137,11 +139,14 @@ class DeviceBatch:
 
     # -- compute
     def laplacian(self):
-        if "lap" not in self._cache:
-            cl = ctypes.c_int64()
-            nat.check(nat.lib().pgcp_batch_laplacian(self.h, ctypes.byref(cl), stream_handle(self.stream)))
-            self._cache["lap"] = int(cl.value)
-        return self._cache["lap"]
+        """Build (once) the cotangent Laplacians of every submesh. Guarded: a
+        rebuild replaces device arrays other streams may be reading."""
+        with self._lock:
+            if "lap" not in self._cache:
+                cl = ctypes.c_int64()
+                nat.check(nat.lib().pgcp_batch_laplacian(self.h, ctypes.byref(cl), stream_handle(self.stream)))
+                self._cache["lap"] = int(cl.value)
+            return self._cache["lap"]
 
     def default_pins(self):
         nat.check(nat.lib().pgcp_batch_default_pins(self.h, stream_handle(self.stream)))

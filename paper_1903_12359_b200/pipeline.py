@@ -257,6 +257,9 @@ def parameterize(mesh, cuts=None, mode="free", workers=1, seed=0, mobius_area=Fa
     # normal-priority stream, on the SMs the flatten's cluster waves leave idle
     hi, lo = _streams(dev)
     cur = torch.cuda.current_stream()
+    # the Laplacian both streams read is built once, here, before the flatten
+    # worker thread and the harmonic preparation start using the batch
+    batch.laplacian()
     hi.wait_stream(cur)
     lo.wait_stream(cur)
     overlap_prep = welds and os.environ.get("PGCP_OVERLAP_HPREP", "1") != "0"
