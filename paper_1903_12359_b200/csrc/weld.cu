@@ -653,7 +653,10 @@ __global__ void __launch_bounds__(NT, 1) k_phase1c(Phase1Args A) {
     int8_t* sides = reinterpret_cast<int8_t*>(pts + chunk);
     Rec* log_a = A.recs + sd.rec;
     Rec* log_b = log_a + sd.cap;
-    const bool logger = rank == 0 && threadIdx.x == 0;
+    // the logger writes both logs and the progress counters; a thread that
+    // owns no point does it, so the record writes stay off the points' path
+    const int logger_tid = (hi - lo < NT) ? NT - 1 : 0;
+    const bool logger = rank == 0 && (int)threadIdx.x == logger_tid;
     int na_rec = 0, nb_rec = 0, nlogged = 0;
     // every CTA of this grid is resident from here on: the streamed replay
     // (secondary launch) may start and wait on the counters
@@ -998,7 +1001,7 @@ __global__ void __launch_bounds__(NT, 1) k_phase1c(Phase1Args A) {
         mx = block_max(mx, red);
         area = block_sum(area, red);
         bad = block_max(bad, red);
-        if (threadIdx.x == 0) {
+        if (logger) {  // every thread holds the reductions; the logger owns the record counts
             meta[0] = na_rec;
             meta[1] = nb_rec;
             meta[5] = seam;
