@@ -70,9 +70,20 @@ PGCP_API unsigned long long pgcp_launch_count(void);
  * (duplicate/non-edge cuts, non-disk component).
  */
 #define PGCP_BATCH_NO_CUTS 1u
+/* PGCP_BATCH_VALIDATE_ONLY: validate the parent mesh (mesh.py:91-111: face
+ * indices, repeated vertices, degenerate faces, repeated directed edges) and
+ * build its incidence and half-edge twins only; no submeshes (K = 0). The
+ * TriMesh constructor's check; partitions start from it with
+ * pgcp_batch_create_from. */
+#define PGCP_BATCH_VALIDATE_ONLY 2u
 PGCP_API int pgcp_batch_create(const double* V, const int32_t* F, int64_t n, int64_t m,
                       const int64_t* cuts, int64_t ncuts, uint32_t flags,
                       void* stream, pgcp_batch** out);
+/* A partition of base's mesh (pgcp_batch_create without re-validating the
+ * mesh and without rebuilding its incidence and twins). flags as above
+ * (PGCP_BATCH_NO_CUTS). */
+PGCP_API int pgcp_batch_create_from(const pgcp_batch* base, const int64_t* cuts, int64_t ncuts, uint32_t flags,
+                                    void* stream, pgcp_batch** out);
 PGCP_API int pgcp_batch_destroy(pgcp_batch* b);
 
 /* host int64 info[PGCP_INFO_COUNT] */

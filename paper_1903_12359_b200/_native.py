@@ -23,6 +23,7 @@ INFO_K, INFO_SUM_N, INFO_SUM_NB, INFO_NNZ_L, INFO_PARENT_CHI, INFO_PARENT_LOOPS,
     INFO_M, INFO_BAD_COMP = range(9)
 INFO_COUNT = 16
 BATCH_NO_CUTS = 1
+BATCH_VALIDATE_ONLY = 2
 
 
 class SolveOpts(ctypes.Structure):
@@ -55,6 +56,7 @@ _SIGS = {
     "pgcp_last_error": ([], ctypes.c_char_p),
     "pgcp_batch_create": ([_VP, _VP, _I64, _I64, _VP, _I64, _U32, _VP, ctypes.POINTER(_VP)], ctypes.c_int),
     "pgcp_batch_destroy": ([_VP], ctypes.c_int),
+    "pgcp_batch_create_from": ([_VP, _VP, _I64, _U32, _VP, ctypes.POINTER(_VP)], ctypes.c_int),
     "pgcp_batch_info": ([_VP, _PI64, ctypes.c_int], ctypes.c_int),
     "pgcp_batch_array": ([_VP, ctypes.c_int, ctypes.POINTER(_VP), _PI64], ctypes.c_int),
     "pgcp_batch_local_faces": ([_VP, _PI64, _VP, _VP], ctypes.c_int),

@@ -23,6 +23,7 @@ struct pgcp_batch {
     int64_t sum_n = 0, sum_nb = 0, nnz = 0;
     int64_t parent_chi = 0, parent_loops = 0, bad_comp = -1;
     bool has_laplacian = false;
+    bool has_topology = false;  // incidence and twins built (validation passed)
 
     pgcp::DevBuf<double> V;
     pgcp::DevBuf<int32_t> F;
@@ -49,6 +50,8 @@ struct pgcp_batch {
 namespace pgcp {
 // topology.cu
 int build_partition(pgcp_batch* b, const int64_t* cuts, int64_t ncuts, bool no_cuts, cudaStream_t s);
+int build_topology(pgcp_batch* b, cudaStream_t s);
+int build_components(pgcp_batch* b, const int64_t* cuts, int64_t ncuts, bool no_cuts, cudaStream_t s);
 int local_faces(pgcp_batch* b, int64_t* face_off, int32_t* faces, cudaStream_t s);
 // laplace.cu
 int build_laplacian(pgcp_batch* b, int64_t* clamped, cudaStream_t s);

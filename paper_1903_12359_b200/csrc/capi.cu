@@ -81,10 +81,57 @@ int pgcp_batch_create(const double* V, const int32_t* F, int64_t n, int64_t m, c
             st = PGCP_E_CUDA;
         }
     }
-    if (st == PGCP_OK) st = build_partition(b, cuts, ncuts, (flags & PGCP_BATCH_NO_CUTS) != 0, s);
+    if (st == PGCP_OK)
+        st = (flags & PGCP_BATCH_VALIDATE_ONLY)
+                 ? build_topology(b, s)
+                 : build_partition(b, cuts, ncuts, (flags & PGCP_BATCH_NO_CUTS) != 0, s);
     if (st != PGCP_OK) {
         free_system(b->sys[0]);
         free_system(b->sys[1]);
+        delete b;
+        return st;
+    }
+    *out = b;
+    return PGCP_OK;
+}
+
+int pgcp_batch_create_from(const pgcp_batch* base, const int64_t* cuts, int64_t ncuts, uint32_t flags, void* stream,
+                           pgcp_batch** out) {
+    if (!out || !base || !base->has_topology || ncuts < 0 || (ncuts > 0 && !cuts)) {
+        set_error("pgcp_batch_create_from: invalid arguments");
+        return PGCP_E_INVALID;
+    }
+    *out = nullptr;
+    PGCP_TRY_CUDA(cudaSetDevice(base->device));
+    cudaStream_t s = as_stream(stream);
+    pgcp_batch* b = new pgcp_batch();
+    b->device = base->device;
+    b->n = base->n;
+    b->m = base->m;
+    const int64_t n = b->n, m = b->m;
+    auto copy = [&](void* dst, const void* src, size_t bytes) -> int {
+        cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, s);
+        if (e != cudaSuccess) {
+            set_error("pgcp_batch_create_from: copy failed: %s", cudaGetErrorString(e));
+            return PGCP_E_CUDA;
+        }
+        return PGCP_OK;
+    };
+    int st = b->V.alloc(3 * n, s);
+    if (st == PGCP_OK) st = b->F.alloc(3 * m, s);
+    if (st == PGCP_OK) st = b->inc_off.alloc(n + 1, s);
+    if (st == PGCP_OK) st = b->inc.alloc(3 * m, s);
+    if (st == PGCP_OK) st = b->twin.alloc(3 * m, s);
+    if (st == PGCP_OK) st = copy(b->V.p, base->V.p, 3 * n * sizeof(double));
+    if (st == PGCP_OK) st = copy(b->F.p, base->F.p, 3 * m * sizeof(int32_t));
+    if (st == PGCP_OK) st = copy(b->inc_off.p, base->inc_off.p, (n + 1) * sizeof(int64_t));
+    if (st == PGCP_OK) st = copy(b->inc.p, base->inc.p, 3 * m * sizeof(int32_t));
+    if (st == PGCP_OK) st = copy(b->twin.p, base->twin.p, 3 * m * sizeof(int32_t));
+    if (st == PGCP_OK) {
+        b->has_topology = true;
+        st = build_components(b, cuts, ncuts, (flags & PGCP_BATCH_NO_CUTS) != 0, s);
+    }
+    if (st != PGCP_OK) {
         delete b;
         return st;
     }

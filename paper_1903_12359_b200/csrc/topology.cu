@@ -612,7 +612,11 @@ int reset_err(DevBuf<DevErr>& e, cudaStream_t s) {
 
 }  // namespace
 
-int build_partition(pgcp_batch* b, const int64_t* cuts, int64_t ncuts, bool no_cuts, cudaStream_t s) {
+// Parent topology (mesh.py:91-111 validation, vertex -> face incidence,
+// half-edge twins): everything that does not depend on the cut set. A batch
+// created with PGCP_BATCH_VALIDATE_ONLY stops here; pgcp_batch_create_from
+// starts a partition from another batch's topology.
+int build_topology(pgcp_batch* b, cudaStream_t s) {
     const int64_t n = b->n, m = b->m;
     const int BT = 256;
     DevBuf<DevErr> err;
@@ -675,6 +679,18 @@ int build_partition(pgcp_batch* b, const int64_t* cuts, int64_t ncuts, bool no_c
         set_error("%s", face_err_text(herr.code));
         return PGCP_E_MESH;
     }
+
+    b->has_topology = true;
+    return PGCP_OK;
+}
+
+int build_components(pgcp_batch* b, const int64_t* cuts, int64_t ncuts, bool no_cuts, cudaStream_t s) {
+    const int64_t n = b->n, m = b->m;
+    const int BT = 256;
+    DevBuf<DevErr> err;
+    PGCP_TRY(err.alloc(1, s));
+    PGCP_TRY(reset_err(err, s));
+    DevErr herr;
 
     // --- cut edges (partition.py:48-59)
     PGCP_TRY(b->he_cut.alloc(3 * m, s));
@@ -919,6 +935,11 @@ int local_faces(pgcp_batch* b, int64_t* face_off, int32_t* faces, cudaStream_t s
     PGCP_TRY_CUDA(cudaMemcpyAsync(face_off, off.p, (b->K + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     PGCP_TRY_CUDA(cudaStreamSynchronize(s));
     return PGCP_OK;
+}
+
+int build_partition(pgcp_batch* b, const int64_t* cuts, int64_t ncuts, bool no_cuts, cudaStream_t s) {
+    PGCP_TRY(build_topology(b, s));
+    return build_components(b, cuts, ncuts, no_cuts, s);
 }
 
 }  // namespace pgcp

@@ -74,7 +74,11 @@ class DeviceBatch:
     """A device-resident partition of one mesh into disk-type submeshes plus
     everything derived from it (Laplacians, solver systems)."""
 
-    def __init__(self, V, F, cuts=None, no_cuts=False, stream=None):
+    def __init__(self, V, F, cuts=None, no_cuts=False, stream=None, validate_only=False, base=None):
+        """A partition of (V, F) along `cuts` (or the whole mesh). With
+        `validate_only` only the parent mesh is validated and its topology
+        built (TriMesh's check); with `base` (such a batch, or any other of
+        the same mesh) the partition starts from base's topology."""
         require_cuda()
         self.stream = stream
         self.V = to_dev(V, torch.float64)
@@ -87,11 +91,16 @@ class DeviceBatch:
         else:
             self.cuts = None
             ncuts = 0
+        flags = nat.BATCH_NO_CUTS if (no_cuts or ncuts == 0) else 0
+        if validate_only:
+            flags |= nat.BATCH_VALIDATE_ONLY
         h = ctypes.c_void_p()
-        nat.check(nat.lib().pgcp_batch_create(ptr(self.V), ptr(self.F), self.n, self.m,
-                                              ptr(self.cuts), ncuts,
-                                              nat.BATCH_NO_CUTS if (no_cuts or ncuts == 0) else 0,
-                                              stream_handle(stream), ctypes.byref(h)))
+        if base is not None:
+            nat.check(nat.lib().pgcp_batch_create_from(base.h, ptr(self.cuts), ncuts, flags, stream_handle(stream),
+                                                       ctypes.byref(h)))
+        else:
+            nat.check(nat.lib().pgcp_batch_create(ptr(self.V), ptr(self.F), self.n, self.m, ptr(self.cuts), ncuts,
+                                                  flags, stream_handle(stream), ctypes.byref(h)))
         self.h = h
         self._info = None
         self._cache = {}

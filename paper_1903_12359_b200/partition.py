@@ -145,10 +145,8 @@ class Partition:
 def partition_mesh(mesh, cuts):
     """Split along cut edges into disk-type submeshes (partition.py:94-137),
     on the device."""
-    from .device import DeviceBatch
     norm = validate_cuts(mesh, cuts)
-    V, F = mesh.device_arrays()
-    batch = DeviceBatch(V, F, cuts=norm)
+    batch = mesh.partition_batch(norm)
     info = batch.info()
     bad = info[nat.INFO_BAD_COMP]
     if bad >= 0:

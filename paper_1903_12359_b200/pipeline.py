@@ -194,7 +194,7 @@ def parameterize(mesh, cuts=None, mode="free", workers=1, seed=0, mobius_area=Fa
     (dist.Shard) splits the flatten/harmonic solves across ranks: each rank
     solves its own subdomains and one sum-all-reduce per stage assembles the
     boundary values / embeddings (dist.py)."""
-    from .device import DeviceBatch, device, require_cuda
+    from .device import device, require_cuda
     require_cuda()
     cfg = config or RunConfig(mode=mode, workers=workers, seed=seed, mobius_area=mobius_area)
     if schedule is not None:
@@ -217,7 +217,7 @@ def parameterize(mesh, cuts=None, mode="free", workers=1, seed=0, mobius_area=Fa
     have_cuts = cuts is not None and len(cuts) > 0
     if have_cuts:
         norm = validate_cuts(mesh, cuts)
-        batch = DeviceBatch(V, F, cuts=norm)
+        batch = mesh.partition_batch(norm)
     else:
         norm = np.zeros((0, 2), np.int64)
         batch = mesh.batch()
