@@ -1163,6 +1163,7 @@ struct PcgArgs {
     long long* timing;       // optional: per CTA [phaseA, red1, phaseB, red2] cycles (iterations 64..191)
     const int32_t* order;    // k_pcg2: cluster -> slot launch order (nullptr: identity)
     double* hist;            // k_pcg2 (PGCP_PCG_HIST): per slot [HIST_K][3] alpha, rr, beta of the first iterations
+    int32_t x0;              // k_pcg2: start from the coarse solution x0 = Q b (PGCP_PCG_X0)
     int32_t ncb;             // k_pcg2 shared layout: gbuf stride (>= every slot's nc)
     int32_t mu_cap;          // ... own coarse rows per CTA
     int32_t items_cap;       // ... (aggregate, part) work items per CTA
@@ -1740,9 +1741,41 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) k_pcg2(PcgArgs A) {
         parity ^= 1;
         double l_rz = prolong_z(gpar);
         gpar ^= 1;
-        double2 tz = cluster_sum2<NW>(cl, csize, rank, l_rz, 0.0, s_warp, s_slot, parity);
+        // coarse start: the first search direction is Q b = z0 - r0 (step
+        // length 1 in exact arithmetic, so x1 = Q b, r1 = b - A Q b); CG
+        // restarts from there (beta = 0 after the first iteration)
+        double l_bq = 0.0;
+        if (A.x0) {
+            __syncthreads();
+            for (int i = threadIdx.x; i < 32 * nloc; i += NT) {
+                const double2 ri = rl[i];
+                double2 zi = zl[i];
+                zi.x -= ri.x;
+                zi.y -= ri.y;
+                zl[i] = zi;
+                l_bq += ri.x * zi.x + ri.y * zi.y;
+            }
+        }
+        double2 tz = cluster_sum2<NW>(cl, csize, rank, l_rz, l_bq, s_warp, s_slot, parity);
         parity ^= 1;
         rho = tz.x;
+        bool x0_start = A.x0 != 0;
+        if (x0_start) {
+            if (tz.y > 1e-24 * tz.x) {
+                rho = tz.y;
+            } else {  // no coarse component: back to z0 = M r0
+                x0_start = false;
+                for (int i = threadIdx.x; i < 32 * nloc; i += NT) {
+                    const double2 ri = rl[i];
+                    double2 zi = zl[i];
+                    zi.x += ri.x;
+                    zi.y += ri.y;
+                    zl[i] = zi;
+                }
+                cluster_sum2<NW>(cl, csize, rank, 0.0, 0.0, s_warp, s_slot, parity);
+                parity ^= 1;
+            }
+        }
         const double* valc = A.val + ent0;
         const uint32_t* encc = A.enc + ent0;
         const uint16_t* enc16c = A.enc16 + ent0;
@@ -1847,7 +1880,7 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) k_pcg2(PcgArgs A) {
             long long c5 = timed ? clock64() : 0;
             double2 tz2 = cluster_sum2<NW>(cl, csize, rank, l_rz2, 0.0, s_warp, s_slot, parity);
             parity ^= 1;
-            beta = tz2.x / rho;
+            beta = (x0_start && it == 1) ? 0.0 : tz2.x / rho;
             rho = tz2.x;
             if (A.hist && rank == 0 && threadIdx.x == 0 && it <= HIST_K) A.hist[(slot * HIST_K + it - 1) * 3 + 2] = beta;
             if (timed) {
@@ -2733,6 +2766,10 @@ int run_solve(pgcp_batch* b, SolveSystem* S, const pgcp_solve_opts* o, double* z
     }
     DevBuf<double> hbuf;
     A.hist = nullptr;
+    {
+        const char* ex = getenv("PGCP_PCG_X0");
+        A.x0 = ex ? atoi(ex) : 1;
+    }
     const char* hist_path = getenv("PGCP_PCG_HIST");  // analysis aid: early CG coefficients per slot
     if (hist_path && S->coarse && !S->force_jacobi) {
         PGCP_TRY(hbuf.alloc((int64_t)nslot * HIST_K * 3, s));
