@@ -309,7 +309,7 @@ def main():
                                   "column code (all-local slices) or 4 B (slices with remote columns) (complex-"
                                   "Hermitian form: L streamed once for x and y), 32 B/row y, 32 B/row p, 16 B/row fp16 coarse "
                                   "weights, 8*nc*ncp B of fp32 E^-1; z, q, r stay in distributed shared memory",
-            "note": "the cfg-2 working set is L2-resident (97% L2 hit rate, traffic = DRAM bytes per launch from ncu)"}
+            "note": "the cfg-2 working set is L2-resident (95-97% L2 hit rate, traffic = DRAM bytes per launch from ncu)"}
     cpu = None
     if not args.no_cpu_baseline:
         cores = os.cpu_count() or 1

@@ -63,3 +63,26 @@ def test_sphere_unit_norm(cuda):
     z = load_golden("sphere4")
     gp, rep = parameterize(TriMesh(z["V"], z["F"]), z["cuts"], "sphere")
     assert np.max(np.abs(np.linalg.norm(gp.coords, axis=1) - 1.0)) <= 1e-9
+
+def test_coarse_start_same_solution_fewer_iterations(cuda, monkeypatch):
+    """The coarse start (x0 = Q b) changes the CG path,
+    not the answer: flatten from x = 0 and from x0 agree to 1e-7 x diameter
+    per subdomain, and the coarse start needs fewer iterations in total."""
+    import torch
+    from paper_1903_12359_b200 import TriMesh, partition_mesh
+    from paper_1903_12359_b200 import _native as nat
+    from paper_1903_12359_b200 import generators as gen
+    V, F, cuts = gen.height_field_case(257, 4)
+    b = partition_mesh(TriMesh(V, F, check=False), cuts).batch
+    out = {}
+    for x0 in ("0", "1"):
+        monkeypatch.setenv("PGCP_PCG_X0", x0)
+        z, st = b.flatten()
+        assert all(s["status"] == 0 for s in st)
+        out[x0] = (z.cpu().numpy(), b.last_solve(0)["iters_sum"])
+    voff = b.host(nat.ARR_VERT_OFF, torch.int64)
+    for c in range(b.K):
+        a, e = out["0"][0][voff[c]:voff[c + 1]], out["1"][0][voff[c]:voff[c + 1]]
+        diam = 2 * np.max(np.abs(a - a.mean()))
+        assert np.max(np.abs(a - e)) <= 1e-7 * diam, c
+    assert out["1"][1] < out["0"][1]
