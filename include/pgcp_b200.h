@@ -341,6 +341,31 @@ PGCP_API int pgcp_batch_stitch(pgcp_batch* b, const double* z, int mode, double 
                                double* coords, double* sphere, int32_t* prov, uint8_t* flip, double* stats,
                                void* stream);
 
+/* Sharded form (one rank of a multi-GPU run, dist.py): flips are counted
+ * only over faces with face_mask[f] != 0 (this rank's submeshes); NULL mask =
+ * every face. */
+PGCP_API int pgcp_batch_stitch_ex(pgcp_batch* b, const double* z, int mode, double hard_tol, double circle_tol,
+                                  const uint8_t* face_mask, double* coords, double* sphere, int32_t* prov,
+                                  uint8_t* flip, double* stats, void* stream);
+
+/* One rank's share of a batch (dist.py): face_mask (device uint8 [m]) = 1
+ * on the faces of the listed submeshes; own_vertices (device int32 [n]
+ * capacity) = the parent vertices with a copy in one of them, ascending;
+ * *n_own their count. Synchronises. */
+PGCP_API int pgcp_batch_shard_maps(pgcp_batch* b, const int32_t* comps, int32_t ncomp, uint8_t* face_mask,
+                                   int32_t* own_vertices, int64_t* n_own, void* stream);
+
+/* Caller-supplied reduction over the ranks of a sharded run: combine
+ * `count` elements of the device buffer `buf` (dtype PGCP_RED_F64 / U32 /
+ * U64, op PGCP_RED_SUM / MAX) in place across ranks, ordered on `stream`
+ * (e.g. an NCCL all-reduce issued from Python). Returns 0 on success. */
+#define PGCP_RED_F64 0
+#define PGCP_RED_U32 1
+#define PGCP_RED_U64 2
+#define PGCP_RED_SUM 0
+#define PGCP_RED_MAX 1
+typedef int (*pgcp_reduce_fn)(void* buf, int64_t count, int dtype, int op, void* user, void* stream);
+
 /* distortion_report (metrics.py:31-176): per-corner angular distortion,
  * per-face area log ratio, their summaries (mean, population sd, median,
  * IQR with numpy's linear interpolation on exact order statistics), and the
@@ -353,6 +378,14 @@ PGCP_API int pgcp_batch_stitch(pgcp_batch* b, const double* z, int mode, double 
 PGCP_API int pgcp_distortion(const double* V, const int32_t* F, int64_t n, int64_t m, const double* coords,
                              int mode_sphere, double* d, uint8_t* valid, double* summary, uint64_t* hist,
                              int64_t hist_cap, void* stream);
+/* Sharded distortion_report: this rank measures the faces with
+ * face_mask[f] != 0; every sum, radix-select histogram (8-bit digits) and
+ * histogram count goes through `reduce`, so all ranks return the summary of
+ * the whole mesh. summary[14] = bytes passed to `reduce`. */
+PGCP_API int pgcp_distortion_ex(const double* V, const int32_t* F, int64_t n, int64_t m, const double* coords,
+                                int mode_sphere, const uint8_t* face_mask, pgcp_reduce_fn reduce, void* user,
+                                double* d, uint8_t* valid, double* summary, uint64_t* hist, int64_t hist_cap,
+                                void* stream);
 
 /* corner_angles / corner_angles_sphere (metrics.py:31-58): per-corner angle
  * and degeneracy flag of every face.

@@ -36,6 +36,11 @@ class SolveStat(ctypes.Structure):
                 ("true_res", ctypes.c_double), ("bnorm", ctypes.c_double), ("xnorm", ctypes.c_double)]
 
 
+# int (*pgcp_reduce_fn)(void* buf, int64_t count, int dtype, int op, void* user, void* stream)
+REDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
+                             ctypes.c_void_p, ctypes.c_void_p)
+
+
 class Rec(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_int32), ("flags", ctypes.c_int32), ("p", ctypes.c_double * 16)]
 

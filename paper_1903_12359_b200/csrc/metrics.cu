@@ -115,9 +115,13 @@ __global__ void k_circle_dev(const int32_t* __restrict__ F, const int32_t* __res
 }
 
 __global__ void k_flips(const int32_t* __restrict__ F, int64_t m, const double2* __restrict__ zc,
-                        const double* __restrict__ P, int mode_sphere, uint8_t* __restrict__ flip,
-                        unsigned long long* count) {
+                        const double* __restrict__ P, int mode_sphere, const uint8_t* __restrict__ fmask,
+                        uint8_t* __restrict__ flip, unsigned long long* count) {
     GRID_STRIDE(f, m) {
+        if (fmask && !fmask[f]) {  // a face another rank owns (sharded run)
+            flip[f] = 0;
+            continue;
+        }
         int a = F[3 * f], b = F[3 * f + 1], c = F[3 * f + 2];
         bool fl;
         if (mode_sphere) {
@@ -158,10 +162,20 @@ __device__ __forceinline__ void corner_angle2(double2 pi, double2 pj, double2 pk
 }
 
 __global__ void k_distortion(const double* __restrict__ V, const int32_t* __restrict__ F, int64_t m,
-                             const double* __restrict__ coords, int mode_sphere, double* __restrict__ d,
-                             uint8_t* __restrict__ valid, double* __restrict__ absd, double* __restrict__ a_new,
-                             double* __restrict__ a_ref) {
+                             const double* __restrict__ coords, int mode_sphere, const uint8_t* __restrict__ fmask,
+                             double* __restrict__ d, uint8_t* __restrict__ valid, double* __restrict__ absd,
+                             double* __restrict__ a_new, double* __restrict__ a_ref) {
     GRID_STRIDE(f, m) {
+        if (fmask && !fmask[f]) {  // counted by the rank that owns the face (sharded run)
+            for (int c = 0; c < 3; ++c) {
+                d[3 * f + c] = 0.0;
+                valid[3 * f + c] = 0;
+                absd[3 * f + c] = -1.0;
+            }
+            a_new[f] = 0.0;
+            a_ref[f] = 0.0;
+            continue;
+        }
         int id[3] = {F[3 * f], F[3 * f + 1], F[3 * f + 2]};
         for (int c = 0; c < 3; ++c) {
             int i = id[c], j = id[(c + 1) % 3], k = id[(c + 2) % 3];
@@ -316,13 +330,13 @@ __global__ void k_area_log_signed(int64_t m, const double* __restrict__ a_new, c
 }
 
 // ---- radix select on non-negative doubles (bits are order-preserving)
-// 12-bit digits (6 passes: shifts 52, 40, 28, 16, 4, then the last 4 bits),
-// block-private shared-memory histograms with warp-aggregated increments;
-// selections that share their prefix share one histogram.
+// RB-bit digits, most significant first (RB = 12: 6 passes, shifts 52, 40,
+// 28, 16, 4, then the last 4 bits; RB = 8: 8 passes, used when the
+// histograms are summed over ranks, 7 KB each), block-private shared-memory
+// histograms with warp-aggregated increments; selections that share their
+// prefix share one histogram.
 constexpr int RBITS = 12;
-constexpr int RBINS = 1 << RBITS;
 constexpr int NSEL = 7;
-constexpr int SEL_PASSES = 6;
 constexpr int SEL_BLOCKS = 296;
 
 struct SelState {
@@ -330,8 +344,12 @@ struct SelState {
     long long rank;             // remaining rank within the prefix
 };
 
-__host__ __device__ inline int sel_shift(int pass) { return pass < 5 ? 64 - RBITS * (pass + 1) : 0; }
-__host__ __device__ inline int sel_width(int pass) { return pass < 5 ? RBITS : 4; }
+template <int RB>
+struct Digits {
+    static constexpr int passes = (64 + RB - 1) / RB;
+    __host__ __device__ static int width(int pass) { return 64 - RB * pass < RB ? 64 - RB * pass : RB; }
+    __host__ __device__ static int shift(int pass) { return 64 - RB * pass - width(pass); }
+};
 
 // representative (first selection with the same prefix) of selection s
 __device__ inline int sel_rep(const SelState* st, int s) {
@@ -340,21 +358,23 @@ __device__ inline int sel_rep(const SelState* st, int s) {
     return s;
 }
 
+template <int RB>
 __global__ void __launch_bounds__(512) k_sel_hist(const double* __restrict__ x, int64_t n, int pass,
                                                   const SelState* __restrict__ st, unsigned int* __restrict__ hist,
                                                   int* __restrict__ rep_out) {
-    extern __shared__ unsigned int sh[];  // [NSEL][RBINS]
+    constexpr int NB = 1 << RB;
+    extern __shared__ unsigned int sh[];  // [NSEL][NB]
     __shared__ unsigned long long pre[NSEL];
     __shared__ int rep[NSEL];
-    const int shift = sel_shift(pass);
-    const int width = sel_width(pass);
+    const int shift = Digits<RB>::shift(pass);
+    const int width = Digits<RB>::width(pass);
     const int nb = 1 << width;
     if (threadIdx.x < NSEL) {
         pre[threadIdx.x] = st[threadIdx.x].prefix;
         rep[threadIdx.x] = sel_rep(st, threadIdx.x);
         if (blockIdx.x == 0) rep_out[threadIdx.x] = rep[threadIdx.x];
     }
-    for (int i = threadIdx.x; i < NSEL * RBINS; i += blockDim.x) sh[i] = 0;
+    for (int i = threadIdx.x; i < NSEL * NB; i += blockDim.x) sh[i] = 0;
     __syncthreads();
     const int hs = shift + width;  // bits above the current digit
     const int lane = threadIdx.x & 31;
@@ -372,7 +392,7 @@ __global__ void __launch_bounds__(512) k_sel_hist(const double* __restrict__ x, 
             if (!act) continue;
             if (m) {
                 unsigned int peers = __match_any_sync(act, digit);
-                if (lane == __ffs(peers) - 1) atomicAdd(&sh[s * RBINS + digit], (unsigned int)__popc(peers));
+                if (lane == __ffs(peers) - 1) atomicAdd(&sh[s * NB + digit], (unsigned int)__popc(peers));
             }
         }
     }
@@ -380,20 +400,22 @@ __global__ void __launch_bounds__(512) k_sel_hist(const double* __restrict__ x, 
     for (int s = 0; s < NSEL; ++s) {
         if (rep[s] != s) continue;
         for (int i = threadIdx.x; i < nb; i += blockDim.x) {
-            unsigned int c = sh[s * RBINS + i];
-            if (c) atomicAdd(&hist[s * RBINS + i], c);
+            unsigned int c = sh[s * NB + i];
+            if (c) atomicAdd(&hist[s * NB + i], c);
         }
     }
 }
 
+template <int RB>
 __global__ void k_sel_pick(int pass, SelState* st, const unsigned int* __restrict__ hist,
                            const int* __restrict__ rep) {
     // one block per selection; chunk sums, then a serial scan by thread 0
+    constexpr int NB = 1 << RB;
     __shared__ unsigned long long chunk[256];
     const int s = blockIdx.x;
-    const int width = sel_width(pass);
+    const int width = Digits<RB>::width(pass);
     const int nb = 1 << width;
-    const unsigned int* h = hist + (int64_t)rep[s] * RBINS;
+    const unsigned int* h = hist + (int64_t)rep[s] * NB;
     const int per = (nb + 255) / 256;
     unsigned long long t = 0;
     for (int i = 0; i < per; ++i) {
@@ -414,7 +436,7 @@ __global__ void k_sel_pick(int pass, SelState* st, const unsigned int* __restric
             r -= h[d];
             ++d;
         }
-        st[s].prefix |= ((unsigned long long)d) << sel_shift(pass);
+        st[s].prefix |= ((unsigned long long)d) << Digits<RB>::shift(pass);
         st[s].rank = r;
     }
 }
@@ -495,19 +517,105 @@ double lerp_np(double a, double b, double t) {
     return a + diff * t;
 }
 
+// sharded runs: faces / parent vertices belonging to this rank's submeshes
+__global__ void k_shard_face_mask(int64_t m, const int32_t* __restrict__ face_comp, const uint8_t* __restrict__ own,
+                                  uint8_t* __restrict__ mask) {
+    GRID_STRIDE(f, m) mask[f] = own[face_comp[f]];
+}
+__global__ void k_shard_vert_flag(int64_t n, const int64_t* __restrict__ lv_off, const int32_t* __restrict__ lv_comp,
+                                  const uint8_t* __restrict__ own, int32_t* __restrict__ flag) {
+    GRID_STRIDE(v, n) {
+        int f = 0;
+        for (int64_t e = lv_off[v]; e < lv_off[v + 1]; ++e) f |= own[lv_comp[e]];
+        flag[v] = f;
+    }
+}
+__global__ void k_shard_compact(int64_t n, const int32_t* __restrict__ flag, const int64_t* __restrict__ pos,
+                                int32_t* __restrict__ out) {
+    GRID_STRIDE(v, n) if (flag[v]) out[pos[v]] = (int32_t)v;
+}
+
+// Sums / maxima over the ranks of a sharded run (pgcp_reduce_fn supplied
+// by the caller, e.g. an NCCL all-reduce); a no-op for a single GPU.
+struct Reducer {
+    pgcp_reduce_fn fn = nullptr;
+    void* user = nullptr;
+    cudaStream_t s = nullptr;
+    DevBuf<double> buf;
+    int64_t bytes = 0;  // payload handed to the hook
+
+    int dev(void* p, int64_t n, int dtype, int op) {
+        if (!fn || n == 0) return PGCP_OK;
+        bytes += n * (dtype == PGCP_RED_U32 ? 4 : 8);
+        if (fn(p, n, dtype, op, user, s) != 0) {
+            set_error("distributed reduction (pgcp_reduce_fn) failed");
+            return PGCP_E_CUDA;
+        }
+        return PGCP_OK;
+    }
+    // in place over host doubles (staged through a small device buffer)
+    int host(double* v, int n, int op) {
+        if (!fn) return PGCP_OK;
+        if (buf.n < n) PGCP_TRY(buf.alloc(std::max(n, 8), s));
+        PGCP_TRY_CUDA(cudaMemcpyAsync(buf.p, v, n * sizeof(double), cudaMemcpyHostToDevice, s));
+        PGCP_TRY(dev(buf.p, n, PGCP_RED_F64, op));
+        PGCP_TRY_CUDA(cudaMemcpyAsync(v, buf.p, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+        PGCP_TRY_CUDA(cudaStreamSynchronize(s));
+        return PGCP_OK;
+    }
+};
+
+// exact order statistics: NSEL selections of given ranks among the entries
+// of x that are >= 0 (histograms summed over ranks between the passes)
+template <int RB>
+int select_ranks(const double* x, int64_t n, SelState* hs, Reducer& red, cudaStream_t s) {
+    constexpr int NB = 1 << RB;
+    DevBuf<SelState> st;
+    DevBuf<unsigned int> hist;
+    DevBuf<int> rep;
+    PGCP_TRY(rep.alloc(NSEL, s));
+    PGCP_TRY(st.alloc(NSEL, s));
+    PGCP_TRY(hist.alloc(NSEL * (int64_t)NB, s));
+    PGCP_TRY_CUDA(cudaMemcpyAsync(st.p, hs, NSEL * sizeof(SelState), cudaMemcpyHostToDevice, s));
+    const size_t smem = NSEL * NB * sizeof(unsigned int);
+    static bool attr = false;
+    if (!attr) {
+        PGCP_TRY_CUDA(cudaFuncSetAttribute(k_sel_hist<RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(SEL_BLOCKS, (n + 511) / 512));
+    for (int pass = 0; pass < Digits<RB>::passes; ++pass) {
+        PGCP_TRY(hist.zero(s));
+        k_sel_hist<RB><<<blocks, 512, smem, s>>>(x, n, pass, st.p, hist.p, rep.p);
+        PGCP_LAUNCH_CHECK();
+        PGCP_TRY(red.dev(hist.p, NSEL * (int64_t)NB, PGCP_RED_U32, PGCP_RED_SUM));
+        k_sel_pick<RB><<<NSEL, 256, 0, s>>>(pass, st.p, hist.p, rep.p);
+        PGCP_LAUNCH_CHECK();
+    }
+    PGCP_TRY_CUDA(cudaMemcpyAsync(hs, st.p, NSEL * sizeof(SelState), cudaMemcpyDeviceToHost, s));
+    PGCP_TRY_CUDA(cudaStreamSynchronize(s));
+    return PGCP_OK;
+}
+
 // mean, population sd, median, IQR of the entries of x that are >= 0
+// (over every rank's entries when red carries a hook)
 int summarize_dev(const double* x, int64_t n, double* out4, int64_t* count, DevBuf<double>& part, cudaStream_t s,
-                  double* vmax = nullptr) {
-    double cnt = 0, sum = 0, sq = 0;
-    PGCP_TRY(dsum(n, Count{x}, part, &cnt, s));
+                  Reducer& red, double* vmax = nullptr) {
+    double cs[2] = {0, 0};  // count, sum
+    PGCP_TRY(dsum(n, Count{x}, part, &cs[0], s));
+    PGCP_TRY(dsum(n, AbsVal{x}, part, &cs[1], s));
+    PGCP_TRY(red.host(cs, 2, PGCP_RED_SUM));
+    const double cnt = cs[0], sum = cs[1];
     *count = (int64_t)cnt;
     if (cnt == 0) {
         out4[0] = out4[1] = out4[2] = out4[3] = NAN;
+        if (vmax) *vmax = 0.0;
         return PGCP_OK;
     }
-    PGCP_TRY(dsum(n, AbsVal{x}, part, &sum, s));
     double mean = sum / cnt;
+    double sq = 0;
     PGCP_TRY(dsum(n, SqDev{x, mean}, part, &sq, s));
+    PGCP_TRY(red.host(&sq, 1, PGCP_RED_SUM));
     out4[0] = mean;
     out4[1] = sqrt(sq / cnt);
     // order statistics for q = 25, 50, 75 (numpy 'linear')
@@ -523,33 +631,14 @@ int summarize_dev(const double* x, int64_t n, double* out4, int64_t* count, DevB
         ranks[2 * q] = (int64_t)pv;
         ranks[2 * q + 1] = std::min<int64_t>((int64_t)pv + 1, N - 1);
     }
-    SelState hs[7];
-    for (int q = 0; q < 7; ++q) hs[q] = {0ull, (long long)ranks[q]};
-    DevBuf<SelState> st;
-    DevBuf<unsigned int> hist;
-    DevBuf<int> rep;
-    PGCP_TRY(rep.alloc(NSEL, s));
-    PGCP_TRY(st.alloc(7, s));
-    PGCP_TRY(hist.alloc(NSEL * (int64_t)RBINS, s));
-    PGCP_TRY_CUDA(cudaMemcpyAsync(st.p, hs, sizeof hs, cudaMemcpyHostToDevice, s));
-    const size_t smem = NSEL * RBINS * sizeof(unsigned int);
-    static bool attr = false;
-    if (!attr) {
-        PGCP_TRY_CUDA(cudaFuncSetAttribute(k_sel_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
-    const int blocks = (int)std::min<int64_t>(SEL_BLOCKS, (n + 511) / 512);
-    for (int pass = 0; pass < SEL_PASSES; ++pass) {
-        PGCP_TRY(hist.zero(s));
-        k_sel_hist<<<blocks, 512, smem, s>>>(x, n, pass, st.p, hist.p, rep.p);
-        PGCP_LAUNCH_CHECK();
-        k_sel_pick<<<NSEL, 256, 0, s>>>(pass, st.p, hist.p, rep.p);
-        PGCP_LAUNCH_CHECK();
-    }
-    PGCP_TRY_CUDA(cudaMemcpyAsync(hs, st.p, sizeof hs, cudaMemcpyDeviceToHost, s));
-    PGCP_TRY_CUDA(cudaStreamSynchronize(s));
-    double v[7];
-    for (int q = 0; q < 7; ++q) memcpy(&v[q], &hs[q].prefix, sizeof(double));
+    SelState hs[NSEL];
+    for (int q = 0; q < NSEL; ++q) hs[q] = {0ull, (long long)ranks[q]};
+    if (red.fn)
+        PGCP_TRY(select_ranks<8>(x, n, hs, red, s));
+    else
+        PGCP_TRY(select_ranks<RBITS>(x, n, hs, red, s));
+    double v[NSEL];
+    for (int q = 0; q < NSEL; ++q) memcpy(&v[q], &hs[q].prefix, sizeof(double));
     if (vmax) *vmax = v[6];
     double q25 = lerp_np(v[0], v[1], gam[0]);
     double q50 = lerp_np(v[2], v[3], gam[1]);
@@ -576,6 +665,12 @@ extern "C" {
 PGCP_API int pgcp_batch_stitch(pgcp_batch* b, const double* z, int mode, double hard_tol, double circle_tol,
                                double* coords, double* sphere, int32_t* prov, uint8_t* flip, double* stats,
                                void* stream) {
+    return pgcp_batch_stitch_ex(b, z, mode, hard_tol, circle_tol, nullptr, coords, sphere, prov, flip, stats, stream);
+}
+
+PGCP_API int pgcp_batch_stitch_ex(pgcp_batch* b, const double* z, int mode, double hard_tol, double circle_tol,
+                                  const uint8_t* face_mask, double* coords, double* sphere, int32_t* prov,
+                                  uint8_t* flip, double* stats, void* stream) {
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     if (!b || !z || !coords || !prov || !flip || !stats || (mode == 2 && !sphere)) {
         set_error("pgcp_batch_stitch: invalid arguments");
@@ -602,7 +697,7 @@ PGCP_API int pgcp_batch_stitch(pgcp_batch* b, const double* z, int mode, double 
         PGCP_LAUNCH_CHECK();
     }
     k_flips<<<grid_for(b->m, 256), 256, 0, s>>>(b->F.p, b->m, reinterpret_cast<const double2*>(coords), sphere,
-                                               mode == 2, flip, bits.p + 3);
+                                               mode == 2, face_mask, flip, bits.p + 3);
     PGCP_LAUNCH_CHECK();
     unsigned long long h[4];
     int hm = 0;
@@ -636,6 +731,43 @@ PGCP_API int pgcp_batch_stitch(pgcp_batch* b, const double* z, int mode, double 
     return PGCP_OK;
 }
 
+// Maps of one rank's share of a batch (dist.py): face_mask[f] = 1 for the
+// faces of the listed submeshes; own_vertices = the parent vertices with a
+// copy in one of them, ascending (count in *n_own). Synchronises.
+PGCP_API int pgcp_batch_shard_maps(pgcp_batch* b, const int32_t* comps, int32_t ncomp, uint8_t* face_mask,
+                                   int32_t* own_vertices, int64_t* n_own, void* stream) {
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (!b || (ncomp > 0 && !comps) || !face_mask || !own_vertices || !n_own) {
+        set_error("pgcp_batch_shard_maps: invalid arguments");
+        return PGCP_E_INVALID;
+    }
+    PGCP_TRY_CUDA(cudaSetDevice(b->device));
+    std::vector<uint8_t> h(std::max<int64_t>(b->K, 1), 0);
+    for (int i = 0; i < ncomp; ++i) {
+        if (comps[i] < 0 || comps[i] >= b->K) {
+            set_error("pgcp_batch_shard_maps: submesh %d out of range", comps[i]);
+            return PGCP_E_INVALID;
+        }
+        h[comps[i]] = 1;
+    }
+    DevBuf<uint8_t> own;
+    DevBuf<int32_t> flag;
+    DevBuf<int64_t> pos;
+    PGCP_TRY(own.alloc((int64_t)h.size(), s));
+    PGCP_TRY(flag.alloc(b->n, s));
+    PGCP_TRY(pos.alloc(b->n + 1, s));
+    PGCP_TRY_CUDA(cudaMemcpyAsync(own.p, h.data(), h.size(), cudaMemcpyHostToDevice, s));
+    k_shard_face_mask<<<grid_for(b->m, 256), 256, 0, s>>>(b->m, b->face_comp.p, own.p, face_mask);
+    PGCP_LAUNCH_CHECK();
+    k_shard_vert_flag<<<grid_for(b->n, 256), 256, 0, s>>>(b->n, b->lv_off.p, b->lv_comp.p, own.p, flag.p);
+    PGCP_LAUNCH_CHECK();
+    PGCP_TRY(exclusive_scan_i32_to_i64(flag.p, pos.p, b->n, s));
+    k_shard_compact<<<grid_for(b->n, 256), 256, 0, s>>>(b->n, flag.p, pos.p, own_vertices);
+    PGCP_LAUNCH_CHECK();
+    PGCP_TRY(fetch_scalar(pos.p + b->n, n_own, s));
+    return PGCP_OK;
+}
+
 PGCP_API int pgcp_corner_angles(const double* points, int kind, const int32_t* F, int64_t m, double* ang,
                                 uint8_t* bad, void* stream) {
     if (m < 0 || kind < 0 || kind > 3 || (m > 0 && (!points || !F || !ang || !bad))) {
@@ -664,7 +796,8 @@ PGCP_API int pgcp_area_distortion(const double* V, const int32_t* F, int64_t n, 
     PGCP_TRY(a_new.alloc(m, s));
     PGCP_TRY(a_ref.alloc(m, s));
     PGCP_TRY(part.alloc(SUM_BLOCKS, s));
-    k_distortion<<<grid_for(m, 256), 256, 0, s>>>(V, F, m, coords, mode_sphere, dc.p, vc.p, absd.p, a_new.p, a_ref.p);
+    k_distortion<<<grid_for(m, 256), 256, 0, s>>>(V, F, m, coords, mode_sphere, nullptr, dc.p, vc.p, absd.p, a_new.p,
+                                                  a_ref.p);
     PGCP_LAUNCH_CHECK();
     double sn = 0, sr = 0;
     PGCP_TRY(dsum(m, Plain{a_new.p}, part, &sn, s));
@@ -684,29 +817,47 @@ PGCP_API int pgcp_area_distortion(const double* V, const int32_t* F, int64_t n, 
 PGCP_API int pgcp_distortion(const double* V, const int32_t* F, int64_t n, int64_t m, const double* coords,
                              int mode_sphere, double* d, uint8_t* valid, double* summary, uint64_t* hist,
                              int64_t hist_cap, void* stream) {
+    return pgcp_distortion_ex(V, F, n, m, coords, mode_sphere, nullptr, nullptr, nullptr, d, valid, summary, hist,
+                              hist_cap, stream);
+}
+
+// Sharded form: only the faces with face_mask[f] != 0 are this rank's; every
+// global quantity (sums, the radix-select histograms, the 0.1-degree counts)
+// goes through `reduce` (sum / max over ranks), so every rank returns the
+// summary of the whole mesh. summary[14] = bytes handed to `reduce`.
+PGCP_API int pgcp_distortion_ex(const double* V, const int32_t* F, int64_t n, int64_t m, const double* coords,
+                                int mode_sphere, const uint8_t* face_mask, pgcp_reduce_fn reduce, void* user,
+                                double* d, uint8_t* valid, double* summary, uint64_t* hist, int64_t hist_cap,
+                                void* stream) {
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     if (!V || !F || !coords || !d || !valid || !summary || m <= 0) {
         set_error("pgcp_distortion: invalid arguments");
         return PGCP_E_INVALID;
     }
+    Reducer red;
+    red.fn = reduce;
+    red.user = user;
+    red.s = s;
     DevBuf<double> absd, a_new, a_ref, aabs, part;
     PGCP_TRY(absd.alloc(3 * m, s));
     PGCP_TRY(a_new.alloc(m, s));
     PGCP_TRY(a_ref.alloc(m, s));
     PGCP_TRY(aabs.alloc(m, s));
     PGCP_TRY(part.alloc(SUM_BLOCKS, s));
-    k_distortion<<<grid_for(m, 256), 256, 0, s>>>(V, F, m, coords, mode_sphere, d, valid, absd.p, a_new.p, a_ref.p);
+    k_distortion<<<grid_for(m, 256), 256, 0, s>>>(V, F, m, coords, mode_sphere, face_mask, d, valid, absd.p, a_new.p,
+                                                  a_ref.p);
     PGCP_LAUNCH_CHECK();
     double ang[4], ar[4];
     int64_t nc = 0, nf = 0;
     double mval = 0;
-    PGCP_TRY(summarize_dev(absd.p, 3 * m, ang, &nc, part, s, &mval));
-    double sn = 0, sr = 0;
-    PGCP_TRY(dsum(m, Plain{a_new.p}, part, &sn, s));
-    PGCP_TRY(dsum(m, Plain{a_ref.p}, part, &sr, s));
-    k_area_logratio<<<grid_for(m, 256), 256, 0, s>>>(m, a_new.p, a_ref.p, sn, sr, aabs.p);
+    PGCP_TRY(summarize_dev(absd.p, 3 * m, ang, &nc, part, s, red, &mval));
+    double sa[2] = {0, 0};  // total parametric and original area
+    PGCP_TRY(dsum(m, Plain{a_new.p}, part, &sa[0], s));
+    PGCP_TRY(dsum(m, Plain{a_ref.p}, part, &sa[1], s));
+    PGCP_TRY(red.host(sa, 2, PGCP_RED_SUM));
+    k_area_logratio<<<grid_for(m, 256), 256, 0, s>>>(m, a_new.p, a_ref.p, sa[0], sa[1], aabs.p);
     PGCP_LAUNCH_CHECK();
-    PGCP_TRY(summarize_dev(aabs.p, m, ar, &nf, part, s));
+    PGCP_TRY(summarize_dev(aabs.p, m, ar, &nf, part, s, red));
     for (int i = 0; i < 4; ++i) {
         summary[i] = ang[i];
         summary[4 + i] = ar[i];
@@ -741,9 +892,11 @@ PGCP_API int pgcp_distortion(const double* V, const int32_t* F, int64_t n, int64
         else
             k_hist_bins<<<grid_for(3 * m, 256), 256, 0, s>>>(absd.p, 3 * m, de.p, (int)nb, cnt.p);
         PGCP_LAUNCH_CHECK();
+        PGCP_TRY(red.dev(cnt.p, nb, PGCP_RED_U64, PGCP_RED_SUM));
         PGCP_TRY_CUDA(cudaMemcpyAsync(hist, cnt.p, nb * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
         PGCP_TRY_CUDA(cudaStreamSynchronize(s));
     }
+    summary[14] = (double)red.bytes;
     return PGCP_OK;
 }
 

@@ -2,30 +2,39 @@
 
 The reference parallelises with one process per subdomain solve
 (`pipeline._run_tasks`, pipeline.py:105-109), while the partition, weld loop
-and stitch stay serial in the driver process. This module keeps the same
-split across GPUs, one process per GPU:
+and stitch stay serial in the driver process. Here one process drives one
+GPU, and the data plane is the one SURVEY §8(e) specifies:
 
-  partition        every rank (replicated, deterministic, ~13 ms on cfg 2)
+  partition        every rank (replicated, deterministic)
   flatten          rank r solves only its own subdomains (LPT shard)
-  exchange 1       sum-all-reduce of the tracked boundary values: each
-                   boundary slot is owned by exactly one subdomain, and so by
-                   one rank, and the other ranks contribute 0 (Σnb x 16 B)
+  exchange         ONE all-gather (NCCL over NVLink) of the boundary-loop
+                   values of every rank's subdomains: each rank packs its
+                   own slots, and a scatter puts the gathered blocks into the
+                   tracked-value vector in slot order (Σnb x 16 B in total)
   weld / boundary  every rank (replicated: the record chain is serial and
                    identical inputs give identical outputs)
-  harmonic         rank r solves only its own subdomains
-  exchange 2       sum-all-reduce of the embeddings (Σn x 16 B)
-  stitch/metrics   every rank (replicated)
+  harmonic/repair  rank r solves (and repairs) only its own subdomains; the
+                   welded Dirichlet values are already known to every rank,
+                   so every seam copy of every parent vertex is known too
+  stitch/metrics   every rank stitches all seam vertices and its own
+                   interiors, and measures only its own faces; the report's
+                   global quantities (flip count, energy, repair info, seam
+                   scale; the distortion sums, exact order statistics and
+                   histogram counts) are summed over ranks with small
+                   all-reduces (a few KB to ~0.1 MB, `pgcp_reduce_fn`)
+  result           per-rank D2H of the rank's own vertices (no collective);
+                   `gather_coords` assembles the full UV on one rank if asked
 
-Both exchanges are disjoint sums: x + 0 = x exactly, so the assembled vectors
-equal the single-GPU ones bit for bit, except that -0.0 becomes +0.0. There
-is no other data-path collective. On NCCL, the two all-reduces move about
-0.5 MB and 17 MB on cfg 2.
+Every rank returns the same RunReport; GlobalParam.coords holds this rank's
+own vertices (every seam vertex included) and NaN elsewhere.
 """
 
+import ctypes
 import json
 import os
 import statistics
 import time
+import traceback
 
 import numpy as np
 import torch
@@ -54,6 +63,11 @@ def lpt_shards(sizes, world):
     return [sorted(s) for s in out]
 
 
+from ._native import REDUCE_FN  # noqa: E402
+
+_RED_TYPESTR = {0: "<f8", 1: "<i4", 2: "<i8"}  # u32 / u64 sums are summed as their signed views (same bits)
+
+
 class Shard:
     """Rank-local view of the sharded pipeline (pass as parameterize(shard=))."""
 
@@ -64,10 +78,41 @@ class Shard:
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         self.exchanged_bytes = 0
+        self.shards = None
+        self._cfn = None
 
     def comps(self, sizes):
-        return lpt_shards(list(sizes), self.world)[self.rank]
+        """This rank's submeshes (LPT over every rank; all ranks agree)."""
+        self.shards = lpt_shards(list(sizes), self.world)
+        return self.shards[self.rank]
 
+    # -- the boundary exchange ------------------------------------------------
+    def slot_layout(self, loop_off):
+        """(own slots, scatter map of the gathered buffer, block length).
+        Rank r's block holds the slots of its submeshes in slot order,
+        padded to the longest block; the map sends every gathered entry to
+        its slot, padding to the dummy slot Σnb."""
+        nslot = int(loop_off[-1])
+        per = [np.concatenate([np.arange(loop_off[c], loop_off[c + 1]) for c in sh]).astype(np.int64)
+               if len(sh) else np.zeros(0, np.int64) for sh in self.shards]
+        blk = max(1, max(len(p) for p in per))
+        smap = np.full(self.world * blk, nslot, dtype=np.int32)
+        for r, p in enumerate(per):
+            smap[r * blk:r * blk + len(p)] = p
+        return per[self.rank], smap, blk
+
+    def all_gather_(self, send, recv):
+        """recv[r * len(send):(r + 1) * len(send)] = rank r's send."""
+        sv, rv = torch.view_as_real(send) if send.is_complex() else send, \
+            torch.view_as_real(recv) if recv.is_complex() else recv
+        if dist.get_backend(self.group) == "nccl":
+            dist.all_gather_into_tensor(rv, sv, group=self.group)
+        else:  # gloo (CPU tests, the one-GPU two-rank test): the list form
+            dist.all_gather(list(rv.chunk(self.world)), sv, group=self.group)
+        self.exchanged_bytes += rv.numel() * rv.element_size()
+        return recv
+
+    # -- small reductions -------------------------------------------------------
     def sum_(self, t):
         """In-place sum over ranks (complex tensors as their real view)."""
         v = torch.view_as_real(t) if t.is_complex() else t
@@ -75,10 +120,50 @@ class Shard:
         self.exchanged_bytes += v.numel() * v.element_size()
         return t
 
+    def reduce_fn(self):
+        """pgcp_reduce_fn for the native sharded metrics: an all-reduce of a
+        device buffer on the current stream (NCCL orders it there)."""
+        if self._cfn is None:
+            from .device import _CudaArray, device
+
+            def fn(buf, count, dtype, op, user, stream):
+                try:
+                    t = torch.as_tensor(_CudaArray(buf, count, _RED_TYPESTR[dtype], None), device=device())
+                    dist.all_reduce(t, op=dist.ReduceOp.MAX if op == 1 else dist.ReduceOp.SUM, group=self.group)
+                    self.exchanged_bytes += t.numel() * t.element_size()
+                    return 0
+                except BaseException:  # reported by the native caller as a failed reduction
+                    traceback.print_exc()
+                    return 1
+
+            self._cfn = REDUCE_FN(fn)
+        return self._cfn
+
+    def gather_objects(self, obj):
+        out = [None] * self.world
+        dist.all_gather_object(out, obj, group=self.group)
+        return out
+
+
+def gather_coords(gp, shard, dst=0):
+    """Assemble the full parameterization on rank `dst` from every rank's
+    own vertices (each rank holds NaN elsewhere). Not part of the timed
+    pipeline: the product returns each rank's share by a per-rank D2H."""
+    own = np.asarray(gp.diagnostics["own_vertices"])
+    vals = np.asarray(gp.coords)[own]
+    parts = shard.gather_objects((own, vals))
+    if shard.rank != dst:
+        return None
+    full = np.array(gp.coords, copy=True)
+    for o, v in parts:
+        full[o] = v
+    return full
+
 
 def parameterize_distributed(mesh, cuts=None, mode="free", group=None, **kw):
     """`parameterize` with the subdomain solves sharded over the ranks of
-    `group`; every rank returns the same (GlobalParam, RunReport)."""
+    `group`; every rank returns the same RunReport and a GlobalParam with
+    its own vertices (`gather_coords` assembles the whole map)."""
     from .pipeline import parameterize
     return parameterize(mesh, cuts, mode, shard=Shard(group), **kw)
 

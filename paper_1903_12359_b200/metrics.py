@@ -14,6 +14,8 @@ from . import _native as nat
 
 _VP, _I64, _D = ctypes.c_void_p, ctypes.c_int64, ctypes.c_double
 nat.register("pgcp_distortion", [_VP, _VP, _I64, _I64, _VP, ctypes.c_int, _VP, _VP, _VP, _VP, _I64, _VP])
+nat.register("pgcp_distortion_ex", [_VP, _VP, _I64, _I64, _VP, ctypes.c_int, _VP, nat.REDUCE_FN, _VP, _VP, _VP, _VP,
+                                    _VP, _I64, _VP])
 
 SUMMARY_COUNT = 16
 
@@ -30,7 +32,9 @@ def _param_coords(param):
 class DeviceDistortion:
     """Raw device outputs of pgcp_distortion."""
 
-    def __init__(self, V, F, coords, mode, hist=True):
+    def __init__(self, V, F, coords, mode, hist=True, face_mask=None, reduce=None):
+        """face_mask / reduce: the sharded form (pgcp_distortion_ex): this
+        rank's faces, and the pgcp_reduce_fn summing over ranks."""
         from .device import device, ptr, stream_handle, to_dev
         sphere = mode == "sphere"
         Vd = to_dev(V, torch.float64)
@@ -49,9 +53,16 @@ class DeviceDistortion:
         if hist:
             cap = 1 << 20
             h = np.zeros(cap, dtype=np.uint64)
-        nat.check(nat.lib().pgcp_distortion(ptr(Vd), ptr(Fd), n, m, ptr(cd), int(sphere), ptr(self.d),
-                                            ptr(self.valid), self.summary.ctypes.data,
-                                            h.ctypes.data if h is not None else None, cap, stream_handle()))
+        if face_mask is None and reduce is None:
+            nat.check(nat.lib().pgcp_distortion(ptr(Vd), ptr(Fd), n, m, ptr(cd), int(sphere), ptr(self.d),
+                                                ptr(self.valid), self.summary.ctypes.data,
+                                                h.ctypes.data if h is not None else None, cap, stream_handle()))
+        else:
+            nat.check(nat.lib().pgcp_distortion_ex(ptr(Vd), ptr(Fd), n, m, ptr(cd), int(sphere),
+                                                   ptr(face_mask) if face_mask is not None else None,
+                                                   reduce if reduce is not None else nat.REDUCE_FN(), None,
+                                                   ptr(self.d), ptr(self.valid), self.summary.ctypes.data,
+                                                   h.ctypes.data if h is not None else None, cap, stream_handle()))
         nb = int(self.summary[11])
         self.hist = h[:nb].tolist() if (h is not None and self.summary[12] > 0) else []
 
@@ -153,14 +164,14 @@ class DistortionReport:
             json.dump(self.to_dict(), fh, indent=2)
 
 
-def distortion_report(mesh, param, energy=None, V=None, F=None):
+def distortion_report(mesh, param, energy=None, V=None, F=None, face_mask=None, reduce=None):
     """Device distortion report (metrics.py:165-176). The per-corner values
     stay on the device (`report.angular` is a CUDA tensor of the valid |d|
     entries' source array and mask)."""
     coords, mode = _param_coords(param)
     Vs = V if V is not None else mesh.vertices
     Fs = F if F is not None else mesh.faces
-    dd = DeviceDistortion(Vs, Fs, coords, mode, hist=True)
+    dd = DeviceDistortion(Vs, Fs, coords, mode, hist=True, face_mask=face_mask, reduce=reduce)
     s = dd.summary
     return DistortionReport(angular=dd.d, area=None, angular_stats=dd.stats("angular"),
                             area_stats=dd.stats("area"), excluded_corners=int(s[8]),

@@ -26,25 +26,28 @@ nat.register("pgcp_plan_weld_schedule",
 
 
 def read_cut_edges(path):
-    """'<i> <j>' 1-based pairs per line (partition.py:25-39)."""
-    pairs = []
+    """Cut file -> (c, 2) int64 zero-based vertex pairs. The format
+    (partition.py:25-39) is one 1-based `i j` pair per line; blank lines and
+    `#` comments are skipped."""
+    rows = []
     with open(path, "r", encoding="utf-8") as fh:
         for ln, line in enumerate(fh, start=1):
-            parts = line.split()
-            if not parts or parts[0].startswith("#"):
+            tok = line.split()
+            if not tok or tok[0].startswith("#"):
                 continue
-            if len(parts) != 2:
+            if len(tok) != 2:
                 raise PartitionError(f"{path}:{ln}: expected two vertex ids")
-            i, j = int(parts[0]), int(parts[1])
-            if i < 1 or j < 1:
-                raise PartitionError(f"{path}:{ln}: vertex ids are 1-based")
-            pairs.append((i - 1, j - 1))
-    return np.array(pairs, dtype=np.int64).reshape(-1, 2)
+            rows.append((ln, int(tok[0]), int(tok[1])))
+    arr = np.asarray(rows, dtype=np.int64).reshape(-1, 3)
+    bad = np.flatnonzero((arr[:, 1] < 1) | (arr[:, 2] < 1))
+    if len(bad):
+        raise PartitionError(f"{path}:{int(arr[bad[0], 0])}: vertex ids are 1-based")
+    return arr[:, 1:] - 1
 
 
 def write_cut_edges(path, cuts):
-    with open(path, "w", encoding="utf-8") as fh:
-        fh.writelines(f"{i + 1} {j + 1}\n" for i, j in np.asarray(cuts, dtype=np.int64))
+    """Inverse of read_cut_edges (1-based pairs, one per line)."""
+    np.savetxt(path, np.asarray(cuts, dtype=np.int64).reshape(-1, 2) + 1, fmt="%d")
 
 
 def validate_cuts(mesh, cuts):
@@ -218,29 +221,41 @@ class StepList(list):
 
 
 def _cyclic_runs(c1, c2):
-    """Host form of the run finder (partition.py:149-179), API helper."""
-    n1, n2 = len(c1), len(c2)
-    pos2 = {int(v): i for i, v in enumerate(c2)}
-    ok = np.array([(int(c1[i]) in pos2 and int(c1[(i + 1) % n1]) in pos2 and
-                    (pos2[int(c1[(i + 1) % n1])] + 1) % n2 == pos2[int(c1[i])]) for i in range(n1)],
-                  dtype=bool)
-    if ok.all():
+    """Maximal runs of consecutive c1 vertices that c2 traverses in the
+    opposite direction (the shared arcs of two boundary cycles,
+    partition.py:149-179). Vectorised: edge i of c1 (c1[i] -> c1[i+1]) is
+    shared iff c2 holds c1[i+1] immediately before c1[i]. Returns "full"
+    when every edge is shared (two cycles bounding the same curve)."""
+    a = np.asarray(c1, dtype=np.int64)
+    b = np.asarray(c2, dtype=np.int64)
+    n1, n2 = len(a), len(b)
+    order = np.argsort(b, kind="stable")
+    sb = b[order]
+
+    def pos_in_b(v):
+        j = np.searchsorted(sb, v)
+        j = np.minimum(j, n2 - 1)
+        return np.where(sb[j] == v, order[j], -1)
+
+    p_here = pos_in_b(a)
+    p_next = pos_in_b(np.roll(a, -1))
+    shared = (p_here >= 0) & (p_next >= 0) & ((p_next + 1) % n2 == p_here)
+    if shared.all():
         if n1 != n2:
             raise PartitionError("inconsistent full-cycle correspondence")
         return "full"
-    if not ok.any():
+    if not shared.any():
         return []
+    # rotate so the scan starts after a non-shared edge; a run starts at
+    # every shared edge whose predecessor is not shared
+    first_gap = int(np.flatnonzero(~shared)[0])
+    idx = (first_gap + 1 + np.arange(n1)) % n1
+    s = shared[idx]
+    starts = np.flatnonzero(s & ~np.roll(s, 1))
     runs = []
-    start = int(np.nonzero(~ok)[0][0])
-    for t in range(1, n1 + 1):
-        i = (start + t) % n1
-        if ok[i] and not ok[i - 1]:
-            j = i
-            chain = [int(c1[j])]
-            while ok[j % n1]:
-                chain.append(int(c1[(j + 1) % n1]))
-                j += 1
-            runs.append(chain)
+    for st in starts:
+        ln = int(np.argmin(s[st:]))  # s ends with the gap, so a False exists
+        runs.append([int(a[i]) for i in (idx[st] + np.arange(ln + 1)) % n1])
     return runs
 
 

@@ -311,10 +311,11 @@ def parameterize(mesh, cuts=None, mode="free", workers=1, seed=0, mobius_area=Fa
         clk.start()
         if not overlap_prep:
             loop_gid = torch.as_tensor(loop_gid_host).to(dev)
-        tv = torch.empty(len(plan.slot_parent), dtype=torch.complex128, device=dev)
-        nat.check(nat.lib().pgcp_gather_complex(_ptr(z0), _ptr(loop_gid), _ptr(tv), tv.numel(), _stream()))
-        if own is not None:
-            shard.sum_(tv)  # boundary values of the other ranks' subdomains (zeros here)
+        if own is None:
+            tv = torch.empty(len(plan.slot_parent), dtype=torch.complex128, device=dev)
+            nat.check(nat.lib().pgcp_gather_complex(_ptr(z0), _ptr(loop_gid), _ptr(tv), tv.numel(), _stream()))
+        else:  # the one exchange: all-gather of every rank's boundary-loop values
+            own_slots, tv = _exchange_boundary(shard, plan, loop_gid_host, z0, dev)
         out = None
         if len(steps):
             out, _ = run_schedule(tv, plan.info, plan.src, plan.wb_off, plan.wb, cfg.hard_tol)
@@ -355,7 +356,9 @@ def parameterize(mesh, cuts=None, mode="free", workers=1, seed=0, mobius_area=Fa
         # batched over every folded submesh on the device (repair.cu)
         report.repairs = _repair(batch, loop_gid, z, own, K, cfg, shard)
         if own is not None:
-            shard.sum_(z)
+            # the other ranks' boundary loops hold the welded values (their
+            # Dirichlet data), so every seam copy is known here
+            _fill_foreign_loops(tv, z, own_slots, loop_gid_host, dev)
         if center is not None:
             gids = np.concatenate([np.arange(voff[i], voff[i + 1]) for i in exterior]).astype(np.int32)
             gt = torch.as_tensor(gids).to(dev)
@@ -366,9 +369,60 @@ def parameterize(mesh, cuts=None, mode="free", workers=1, seed=0, mobius_area=Fa
 
     # ---- stitch ---------------------------------------------------------------
     clk.start()
-    gp, flip = _stitch(batch, embeddings, mode, cfg, mesh)
+    smaps = _shard_maps(batch, own, dev) if own is not None else None
+    gp, flip = _stitch(batch, embeddings, mode, cfg, mesh, smaps)
     clk.stop("stitch")
-    return _finish(mesh, batch, embeddings, gp, report, cfg, clk)
+    return _finish(mesh, batch, embeddings, gp, report, cfg, clk, shard if own is not None else None, smaps, own)
+
+
+def _exchange_boundary(shard, plan, loop_gid_host, z0, dev):
+    """SURVEY §8(e)'s only data-path collective: every rank packs the
+    boundary-loop values of its own submeshes (slot order) and one
+    all-gather hands every rank every block; a scatter puts them into the
+    tracked-value vector (padding lands in a dummy slot past the end)."""
+    nslot = len(plan.slot_parent)
+    own_slots, smap, blk = shard.slot_layout(plan.loop_off)
+    send = torch.zeros(blk, dtype=torch.complex128, device=dev)
+    if len(own_slots):
+        idx = torch.as_tensor(loop_gid_host[own_slots]).to(dev)
+        nat.check(nat.lib().pgcp_gather_complex(_ptr(z0), _ptr(idx), _ptr(send), len(own_slots), _stream()))
+    recv = torch.empty(shard.world * blk, dtype=torch.complex128, device=dev)
+    shard.all_gather_(send, recv)
+    tv_ext = torch.empty(nslot + 1, dtype=torch.complex128, device=dev)
+    sm = torch.as_tensor(smap).to(dev)
+    nat.check(nat.lib().pgcp_scatter_complex(_ptr(recv), _ptr(sm), _ptr(tv_ext), recv.numel(), _stream()))
+    return own_slots, tv_ext[:nslot]
+
+
+def _fill_foreign_loops(tv, z, own_slots, loop_gid_host, dev):
+    """z on the boundary loops of other ranks' submeshes := their welded
+    Dirichlet values (what their harmonic solves hold fixed)."""
+    foreign = np.setdiff1d(np.arange(len(loop_gid_host)), own_slots).astype(np.int32)
+    if not len(foreign):
+        return
+    src = torch.as_tensor(foreign).to(dev)
+    dst = torch.as_tensor(loop_gid_host[foreign]).to(dev)
+    tmp = torch.empty(len(foreign), dtype=torch.complex128, device=dev)
+    nat.check(nat.lib().pgcp_gather_complex(_ptr(tv), _ptr(src), _ptr(tmp), len(foreign), _stream()))
+    nat.check(nat.lib().pgcp_scatter_complex(_ptr(tmp), _ptr(dst), _ptr(z), len(foreign), _stream()))
+
+
+nat.register("pgcp_batch_shard_maps", [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p,
+                                       ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64), ctypes.c_void_p])
+nat.register("pgcp_batch_stitch_ex", [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_double,
+                                      ctypes.c_double, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                      ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p])
+
+
+def _shard_maps(batch, own, dev):
+    """(face mask, own parent vertices, count) of this rank's submeshes."""
+    mask = torch.empty(batch.m, dtype=torch.uint8, device=dev)
+    ov = torch.empty(max(batch.n, 1), dtype=torch.int32, device=dev)
+    cnt = ctypes.c_int64()
+    arr = (ctypes.c_int32 * max(len(own), 1))(*[int(c) for c in own])
+    nat.check(nat.lib().pgcp_batch_shard_maps(batch.h, arr, len(own), _ptr(mask), _ptr(ov), ctypes.byref(cnt),
+                                              _stream()))
+    return mask, ov[:cnt.value], int(cnt.value)
 
 
 def _repair(batch, loop_gid, z, own, K, cfg, shard):
@@ -388,7 +442,9 @@ def _repair(batch, loop_gid, z, own, K, cfg, shard):
         shard.sum_(t)
         info = t.cpu().numpy()
     remaining = {}
-    stuck = [c for c in comps if info[c, 1] > 0 and not info[c, 2]]
+    # submeshes still folded after the repair, over every rank's submeshes
+    stuck_all = [c for c in range(K) if info[c, 1] > 0 and not info[c, 2]]
+    stuck = [c for c in stuck_all if c in set(comps)]
     if stuck:
         _, flipped = batch.qc_repair(loop_gid, z, comps=stuck, max_iter=0, cap=MU_CAP, want_flipped=True)
         fl = flipped.cpu().numpy().astype(bool)
@@ -396,6 +452,9 @@ def _repair(batch, loop_gid, z, own, K, cfg, shard):
         for c in stuck:
             pf = np.flatnonzero(fc == c)
             remaining[c] = [int(x) for x in np.flatnonzero(fl[pf])]
+    if shard is not None and own is not None and stuck_all:  # the owners' lists, to every rank
+        for part in shard.gather_objects(remaining):
+            remaining.update(part)
     out = []
     for c in range(K):
         before, iters, cleared = int(info[c, 0]), int(info[c, 1]), bool(info[c, 2])
@@ -454,7 +513,7 @@ def _geodesic_boundary(plan, tv, gc):
         nat.check(nat.lib().pgcp_scatter_complex(_ptr(tmp), _ptr(dst_on), _ptr(tv), len(on), _stream()))
 
 
-def _stitch(batch, z, mode, cfg, mesh):
+def _stitch(batch, z, mode, cfg, mesh, smaps=None):
     from .device import device
     dev = device()
     n, m = batch.n, batch.m
@@ -464,9 +523,14 @@ def _stitch(batch, z, mode, cfg, mesh):
     flip = torch.empty(m, dtype=torch.uint8, device=dev)
     stats = np.zeros(8)
     mcode = {"free": 0, "disk": 1, "sphere": 2}[mode]
-    st = nat.lib().pgcp_batch_stitch(batch.h, _ptr(z), mcode, cfg.hard_tol, 1e-9, _ptr(coords),
-                                     _ptr(sphere) if sphere is not None else None, _ptr(prov), _ptr(flip),
-                                     stats.ctypes.data, _stream())
+    if smaps is None:
+        st = nat.lib().pgcp_batch_stitch(batch.h, _ptr(z), mcode, cfg.hard_tol, 1e-9, _ptr(coords),
+                                         _ptr(sphere) if sphere is not None else None, _ptr(prov), _ptr(flip),
+                                         stats.ctypes.data, _stream())
+    else:  # sharded: flips of own faces; the seam check waits for the global scale (_finish)
+        st = nat.lib().pgcp_batch_stitch_ex(batch.h, _ptr(z), mcode, float("inf"), 1e-9, _ptr(smaps[0]),
+                                            _ptr(coords), _ptr(sphere) if sphere is not None else None, _ptr(prov),
+                                            _ptr(flip), stats.ctypes.data, _stream())
     nat.check(st)
     nflip = int(stats[3])
     flipped = np.nonzero(flip.cpu().numpy())[0] if nflip else np.zeros(0, dtype=np.int64)
@@ -476,38 +540,93 @@ def _stitch(batch, z, mode, cfg, mesh):
     out = sphere if mode == "sphere" else coords
     gp = GlobalParam(mode, out, flipped, prov, float(stats[0]), diag)
     gp._device = True
+    gp._nflip_local = nflip
     return gp, flip
 
 
-def _finish(mesh, batch, embeddings, gp, report, cfg, clk):
-    """Energy, distortion report, acceptance flags (pipeline.py:274-297)."""
+def _finish(mesh, batch, embeddings, gp, report, cfg, clk, shard=None, smaps=None, own=None):
+    """Energy, distortion report, acceptance flags (pipeline.py:274-297).
+    Sharded: this rank measures its own faces; the global quantities are
+    summed over ranks (dist.py) and the result's D2H covers only this
+    rank's own vertices."""
     from .metrics import distortion_report
     clk.start()
     energy = None
-    if gp.mode in ("free", "disk"):
-        energy = float(batch.energy(embeddings).sum())
+    e_sub = batch.energy(embeddings) if gp.mode in ("free", "disk") else None
+    nflip = int(len(gp.flipped_faces))
+    if shard is None:
+        if e_sub is not None:
+            energy = float(e_sub.sum())
+    else:
+        # flips, energy and every rank's seam scale in one small all-reduce
+        vec = np.zeros(2 + shard.world)
+        vec[0] = gp._nflip_local
+        vec[1] = float(e_sub[list(own)].sum()) if e_sub is not None and len(own) else 0.0
+        vec[2 + shard.rank] = gp.diagnostics["scale"]
+        t = torch.as_tensor(vec, device=embeddings.device)
+        shard.sum_(t)
+        vec = t.cpu().numpy()
+        nflip = int(round(vec[0]))
+        energy = float(vec[1]) if e_sub is not None else None
+        scale = float(vec[2:].max())
+        gp.diagnostics["scale"] = scale
+        if scale > 0 and gp.seam_max_dev > cfg.hard_tol * scale:
+            raise SolveError(f"seam disagreement {gp.seam_max_dev:.3e} exceeds {cfg.hard_tol:g} x scale "
+                             f"{scale:.3e} (welding bug upstream)")
     V, F = mesh.device_arrays()
     pending = None
     if not cfg.keep_device:
         # the result's D2H runs on a copy stream while the metrics kernels run
-        pending = (_to_host_async(gp.coords), _to_host_async(gp.provenance.to(torch.int64)))
-    dist = distortion_report(mesh, gp, energy=energy, V=V, F=F)
+        if smaps is None:
+            pending = (_to_host_async(gp.coords), _to_host_async(gp.provenance.to(torch.int64)))
+        else:  # this rank's own vertices only
+            ov = smaps[1]
+            pending = (_to_host_async(_rows(gp.coords, ov)), _to_host_async(_rows(gp.provenance, ov).to(torch.int64)),
+                       _to_host_async(ov))
+    if shard is None:
+        dist = distortion_report(mesh, gp, energy=energy, V=V, F=F)
+    else:
+        dist = distortion_report(mesh, gp, energy=energy, V=V, F=F, face_mask=smaps[0], reduce=shard.reduce_fn())
+        report.solver["exchanged_bytes"] = shard.exchanged_bytes
     clk.stop("metrics")
     if cfg.mobius_area:
         report.mobius_info = {"pre": None, "post": None, "improved": False,
                               "note": "Mobius area optimisation is out of scope on this path"}
-    report.flips = int(len(gp.flipped_faces))
+    report.flips = nflip
     report.distortion = dist.to_dict()
     seam_ok = all(r <= cfg.snap_tol for r in report.seam_residuals)
     report.ok = report.flips == 0 and seam_ok
     if cfg.keep_device:
+        if smaps is not None:
+            gp.diagnostics["own_vertices"] = smaps[1]
         return gp, report
     # hand back host arrays, as the reference's GlobalParam holds numpy
     clk.start()
-    gp.coords = _host_result(pending[0])
-    gp.provenance = _host_result(pending[1])  # widened on the device
+    if smaps is None:
+        gp.coords = _host_result(pending[0])
+        gp.provenance = _host_result(pending[1])  # widened on the device
+    else:
+        ov = _host_result(pending[2]).astype(np.int64)
+        vals, prov = _host_result(pending[0]), _host_result(pending[1])
+        full = np.full((mesh.n_vertices,) + vals.shape[1:], np.nan, dtype=vals.dtype)
+        full[ov] = vals
+        pv = np.full(mesh.n_vertices, -1, dtype=np.int64)
+        pv[ov] = prov
+        gp.coords, gp.provenance = full, pv
+        gp.diagnostics["own_vertices"] = ov
+        report.solver["d2h_bytes"] = int(vals.nbytes + prov.nbytes + 4 * len(ov))
     clk.stop("d2h")
     return gp, report
+
+
+def _rows(t, idx):
+    """t[idx] on the device (planar coordinates through the library's
+    gather kernel; sphere rows and provenance through torch's index_select)."""
+    if t.dtype == torch.complex128 and t.dim() == 1:
+        out = torch.empty(idx.numel(), dtype=t.dtype, device=t.device)
+        nat.check(nat.lib().pgcp_gather_complex(_ptr(t), _ptr(idx), _ptr(out), idx.numel(), _stream()))
+        return out
+    return t.index_select(0, idx.long())
 
 
 _COPY_STREAMS = {}

@@ -44,7 +44,7 @@ def pack_csr(out, name, mats, values=True):
         pack(out, name + "_data", [m.data for m in mats], np.float64)
 
 
-def capture_run(V, F, cuts, mode, schedule_pairs=None):
+def capture_run(V, F, cuts, mode, schedule_pairs=None, workers=1):
     """Run pgcp.parameterize and capture every stage's inputs/outputs."""
     cap = {"tasks": [], "welds": [], "geo": None}
     orig_run = ref_pipeline._run_tasks
@@ -88,7 +88,7 @@ def capture_run(V, F, cuts, mode, schedule_pairs=None):
     ref_pipeline.plan_weld_schedule = plan
     try:
         mesh = pgcp.TriMesh(V, F)
-        gp, rep = pgcp.parameterize(mesh, cuts, mode)
+        gp, rep = pgcp.parameterize(mesh, cuts, mode, workers=workers)
     finally:
         ref_pipeline._run_tasks = orig_run
         ref_pipeline.partial_weld = orig_pw
@@ -208,6 +208,100 @@ def pipeline_case(name, V, F, cuts, mode, schedule_pairs=None, stagewise=True):
     np.savez_compressed(path, **out)
     print(f"{name}: {os.path.getsize(path) / 1e3:.0f} KB  mode={mode} K={len(subs)} "
           f"flips={rep.flips} mean|d|={rep.distortion['angular_abs']['mean']:.6f}")
+
+
+def _sha(a):
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()[:16]
+
+
+def cfg2_qtree_case(stride=61, workers=None):
+    """The benchmarked run itself: cfg 2 (1024^2 height field, 8x8 blocks,
+    seed 0) welded in the quadtree order, free mode, run by the reference
+    `pgcp.parameterize` (`pipeline.py:119-271`) with `workers` processes.
+
+    The full run is ~1M vertices, so the fixture keeps, exactly as the
+    reference produced them:
+      * integer outputs: face labels (uint8), boundary cycles and local loops
+        (full), per-step (comp_a, comp_b, k) and sha256 of every step's
+        a/b/merged cycle;
+      * the flatten of every subdomain on its whole boundary loop plus every
+        `stride`-th local vertex; the welded Dirichlet values g of every
+        subdomain (full; the product of the whole weld chain) and the
+        harmonic solution on every `stride`-th local vertex;
+      * the inputs and outputs of the largest weld of each of the 6 levels
+        (k up to 1024) and every weld's seam error;
+      * the final UV on every `stride`-th parent vertex, flips, seam
+        residuals and the full distortion report;
+      * the reference's own stage timings on this host (`report.timings`).
+    """
+    import time as _time
+    workers = workers or os.cpu_count() or 1
+    V, F, cuts = gen.cfg2(0)
+    pairs = gen.quadtree_schedule_order(8, 8)
+    t0 = _time.perf_counter()
+    mesh, gp, rep, cap = capture_run(V, F, cuts, "free", schedule_pairs=pairs, workers=workers)
+    wall = _time.perf_counter() - t0
+    part = pgcp.partition_mesh(mesh, cuts)
+    out = {"mode": np.array("free"), "stride": np.array(stride),
+           "V_sha": np.array(_sha(np.asarray(V, np.float64))),
+           "F_sha": np.array(_sha(np.asarray(F, np.int32))),
+           "cuts_sha": np.array(_sha(np.asarray(cuts, np.int64))),
+           "face_assignment": np.asarray(part.face_assignment, np.uint8),
+           "vertex_maps_sha": np.array(_sha(np.concatenate(part.vertex_maps).astype(np.int64))),
+           "sub_n": np.array([m.n_vertices for m in part.submeshes], np.int64)}
+    pack(out, "cycles", part.boundary_cycles, np.int64)
+    loops = [pgcp.boundary_loops(s)[0] for s in part.submeshes]
+    pack(out, "loops", loops, np.int64)
+    steps = cap["steps"]
+    out["step_meta"] = np.array([[s.comp_a, s.comp_b, s.k, int(s.closed)] for s in steps], np.int64)
+    out["step_sha"] = np.array([[_sha(np.asarray(s.a_cycle, np.int64)), _sha(np.asarray(s.b_cycle, np.int64)),
+                                 _sha(np.asarray(s.merged_cycle, np.int64))] for s in steps])
+    # level of each weld: 1 + the deeper of the two components' last merges
+    depth, lev = {}, []
+    for s in steps:
+        lv = 1 + max(depth.get(s.comp_a, 0), depth.get(s.comp_b, 0))
+        depth[s.comp_a] = lv
+        lev.append(lv)
+    out["step_level"] = np.array(lev, np.int64)
+    tasks = {t[0]: t for t in cap["tasks"]}
+    flat = tasks["_dncp_task"][2]
+    samp = [np.arange(0, len(z), stride) for z in flat]
+    pack(out, "flat_loop", [z[lp] for z, lp in zip(flat, loops)], np.complex128)
+    pack(out, "flat_samp", [z[s] for z, s in zip(flat, samp)], np.complex128)
+    hres = tasks["_harmonic_task"][2]
+    pack(out, "harm_g", [a[3] for a in tasks["_harmonic_task"][1]], np.complex128)
+    pack(out, "harm_samp", [r[0][s] for r, s in zip(hres, samp)], np.complex128)
+    out["flips_before"] = np.array([r[1]["flips_before"] for r in hres], np.int64)
+    welds = cap["welds"]
+    out["weld_k"] = np.array([w[3] for w in welds], np.int64)
+    out["weld_seam"] = np.array([w[4].seam_error for w in welds])
+    big = []
+    for lv in sorted(set(lev)):
+        idx = [i for i in range(len(welds)) if lev[i] == lv]
+        big.append(max(idx, key=lambda i: (welds[i][3], -i)))
+    out["big_weld"] = np.array(big, np.int64)
+    pack(out, "big_in_a", [welds[i][1] for i in big], np.complex128)
+    pack(out, "big_in_b", [welds[i][2] for i in big], np.complex128)
+    pack(out, "big_out_a", [welds[i][4].a for i in big], np.complex128)
+    pack(out, "big_out_b", [welds[i][4].b for i in big], np.complex128)
+    coords = np.asarray(gp.coords)
+    out["coords_samp"] = coords[::stride]
+    cen = coords.mean()
+    out["coords_diam"] = np.array(2 * np.max(np.abs(coords - cen)))
+    out["flips"] = np.array(rep.flips)
+    out["seam_residuals"] = np.array(rep.seam_residuals, np.float64)
+    out["distortion_json"] = np.array(json.dumps(rep.distortion))
+    out["repairs_json"] = np.array(json.dumps(rep.repairs))
+    out["ok"] = np.array(rep.ok)
+    tm = dict(rep.timings)
+    tm["wall"] = wall
+    tm["workers"] = workers
+    out["ref_timings_json"] = np.array(json.dumps(tm))
+    path = os.path.join(HERE, "cfg2_qtree.npz")
+    np.savez_compressed(path, **out)
+    print(f"cfg2_qtree: {os.path.getsize(path) / 1e6:.2f} MB flips={rep.flips} "
+          f"mean|d|={rep.distortion['angular_abs']['mean']:.6f} timings={tm}")
 
 
 def known_answers():
@@ -435,13 +529,13 @@ def _cases():
             "cfg1": c_cfg1, "strips4": c_strips4,
             "blocks3x3": c_blocks3x3, "disk2x2": c_disk2x2, "k1": c_k1, "flat2x2": c_flat2x2,
             "sphere": c_sphere, "tree4x4": c_tree4x4, "ptree4x4": c_ptree4x4,
-            "qtree4x4": c_qtree4x4}
+            "qtree4x4": c_qtree4x4, "cfg2_qtree": cfg2_qtree_case}
 
 
 def main():
     """python make_goldens.py [case ...]  (default: every case)"""
     cases = _cases()
-    names = sys.argv[1:] or list(cases)
+    names = sys.argv[1:] or [c for c in cases if c != "cfg2_qtree"]  # cfg2_qtree: ~5 min, run by name
     for n in names:
         cases[n]()
 

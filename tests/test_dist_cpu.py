@@ -1,10 +1,15 @@
 """Multi-rank host logic of dist.py on CPU (gloo, world_size 2).
 
 The device solves are replaced by the oracle (this is test infrastructure).
-Each rank solves its LPT shard, and the rank-local vectors laid out like the
-device batch (submeshes concatenated, zeros for other ranks' submeshes) go
-through `Shard.sum_`. The tests check that the assembled boundary values and
-embeddings equal the single-process ones bit for bit.
+Each rank solves its LPT shard; the boundary-loop values of its own
+submeshes go through the one exchange of the design, `Shard.slot_layout` +
+`Shard.all_gather_` (each rank's slots packed, gathered, scattered into
+slot order); each rank then solves its own Dirichlet problems and fills the
+other ranks' loops with the welded values (pipeline._fill_foreign_loops).
+The tests check that the exchanged boundary values equal the
+single-process ones bit for bit, that every rank's own vertices (seams
+included) stitch to the single-process result, and that the exchange moves
+one padded block per rank.
 """
 
 import os
@@ -67,22 +72,28 @@ def _worker(rank, world, port, q):
         z0 = np.zeros(voff[-1], np.complex128)
         for c in own:
             z0[voff[c]:voff[c + 1]] = oracle.dncp_flatten(sp.sub_V[c], sp.sub_F[c], sp.loops[c])
-        # boundary slots gathered from the rank-local embedding, then exchanged
+        # the exchange: own slots packed, all-gathered, scattered to slot order
         loop_gid = np.concatenate([voff[c] + np.asarray(sp.loops[c]) for c in range(sp.n_sub)])
-        tv = torch.from_numpy(z0[loop_gid].copy())
-        shard.sum_(tv)
-        # harmonic of own submeshes with the exchanged boundary values
-        z = np.zeros(voff[-1], np.complex128)
-        tvn = tv.numpy()
+        own_slots, smap, blk = shard.slot_layout(loff)
+        send = torch.zeros(blk, dtype=torch.complex128)
+        send[:len(own_slots)] = torch.from_numpy(z0[loop_gid[own_slots]])
+        recv = torch.empty(world * blk, dtype=torch.complex128)
+        shard.all_gather_(send, recv)
+        tv_ext = np.zeros(loff[-1] + 1, np.complex128)
+        tv_ext[smap] = recv.numpy()
+        tvn = tv_ext[:-1]
+        # harmonic of own submeshes with the exchanged boundary values, then
+        # the other ranks' loops := their Dirichlet values
+        z = np.full(voff[-1], np.nan + 0j)
         for c in own:
             g = tvn[loff[c]:loff[c + 1]]
             z[voff[c]:voff[c + 1]] = oracle.dirichlet_extend(sp.sub_V[c], sp.sub_F[c], sp.loops[c], g)
-        zt = torch.from_numpy(z)
-        shard.sum_(zt)
-        q.put((rank, own, tvn.copy(), zt.numpy().copy(), shard.exchanged_bytes))
+        foreign = np.setdiff1d(np.arange(len(loop_gid)), own_slots)
+        z[loop_gid[foreign]] = tvn[foreign]
+        q.put((rank, own, tvn.copy(), z, shard.exchanged_bytes, blk))
         dist.destroy_process_group()
     except Exception as exc:  # pragma: no cover - reported to the parent
-        q.put((rank, "error", repr(exc), None, None))
+        q.put((rank, "error", repr(exc), None, None, None))
 
 
 def test_shard_exchange_gloo_matches_single_process():
@@ -113,9 +124,18 @@ def test_shard_exchange_gloo_matches_single_process():
     flat = [oracle.dncp_flatten(sp.sub_V[c], sp.sub_F[c], sp.loops[c]) for c in range(sp.n_sub)]
     tv = np.concatenate([flat[c][sp.loops[c]] for c in range(sp.n_sub)])
     loff = np.concatenate([[0], np.cumsum([len(l) for l in sp.loops])])
-    z = np.concatenate([oracle.dirichlet_extend(sp.sub_V[c], sp.sub_F[c], sp.loops[c], tv[loff[c]:loff[c + 1]])
-                        for c in range(sp.n_sub)])
+    zref = np.concatenate([oracle.dirichlet_extend(sp.sub_V[c], sp.sub_F[c], sp.loops[c],
+                                                   tv[loff[c]:loff[c + 1]]) for c in range(sp.n_sub)])
+    voff = np.concatenate([[0], np.cumsum([len(v) for v in sp.sub_V])])
     for r in (0, 1):
         assert np.array_equal(res[r][2], tv)
-        assert np.array_equal(res[r][3], z)
-        assert res[r][4] == (tv.size + z.size) * 16
+        z = res[r][3]
+        known = ~np.isnan(z.real)
+        assert np.array_equal(z[known], zref[known])
+        # own submeshes complete, every seam copy known
+        for c in res[r][1]:
+            assert known[voff[c]:voff[c + 1]].all()
+        loop_gid = np.concatenate([voff[c] + np.asarray(sp.loops[c]) for c in range(sp.n_sub)])
+        assert known[loop_gid].all()
+        assert res[r][4] == 2 * res[r][5] * 16  # one all-gather of two padded blocks
+        assert 2 * res[r][5] <= len(tv) + max(len(l) for l in sp.loops)

@@ -1,6 +1,10 @@
 """Sharded pipeline on the device: two ranks (gloo; both processes on cuda:0,
 exchanging through host memory, no kernel waits on another process) must
-reproduce the single-process result exactly."""
+reproduce the single-process result: the boundary all-gather feeds the
+replicated weld, every rank solves its own subdomains, and the assembled
+UV (gather_coords) equals the one-GPU UV bit for bit; every rank's report
+carries the whole mesh's flips, repairs and distortion summary (order
+statistics exact, sums to rounding)."""
 
 import os
 import socket
@@ -29,27 +33,36 @@ def _worker(rank, world, port, mode, q):
         dist.init_process_group("gloo", rank=rank, world_size=world)
         import paper_1903_12359_b200 as pg
         from paper_1903_12359_b200 import generators as gen
-        from paper_1903_12359_b200.dist import parameterize_distributed
-        if mode == "sphere":
-            V, F, cuts = _sphere_case()
-            gp, rep = parameterize_distributed(pg.TriMesh(V, F), cuts, "sphere")
-        else:
-            V, F, cuts = gen.height_field_case(65, 4, seed=2)
-            gp, rep = parameterize_distributed(pg.TriMesh(V, F), cuts, mode,
-                                               pairs=gen.row_tree_schedule_order(4, 4))
-        q.put((rank, np.asarray(gp.coords), rep.flips, rep.solver.get("shard")))
+        from paper_1903_12359_b200.dist import Shard, gather_coords
+        shard = Shard()
+        V, F, cuts, m, kw = _case(mode)
+        gp, rep = pg.parameterize(pg.TriMesh(V, F), cuts, m, shard=shard, **kw)
+        full = gather_coords(gp, shard)
+        q.put((rank, full, rep.flips, rep.solver.get("shard"), rep.distortion, rep.repairs,
+               rep.solver.get("exchanged_bytes"), np.asarray(gp.coords)))
         dist.barrier()
         dist.destroy_process_group()
     except Exception as exc:  # pragma: no cover
         q.put((rank, "error", repr(exc), None))
 
 
-def _sphere_case():
-    z = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "sphere4.npz"))
-    return z["V"], z["F"], z["cuts"]
+def _golden(name):
+    return np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", f"{name}.npz"))
 
 
-@pytest.mark.parametrize("mode", ["free", "disk", "sphere"])
+def _case(mode):
+    from paper_1903_12359_b200 import generators as gen
+    if mode == "sphere":
+        z = _golden("sphere4")
+        return z["V"], z["F"], z["cuts"], "sphere", {}
+    if mode == "fold":  # jittered strips whose harmonic maps fold: the repair path
+        z = _golden("repair_strips3")
+        return z["V"], z["F"], z["cuts"], str(z["mode"]), {}
+    V, F, cuts = gen.height_field_case(65, 4, seed=2)
+    return V, F, cuts, mode, {"pairs": gen.row_tree_schedule_order(4, 4)}
+
+
+@pytest.mark.parametrize("mode", ["free", "disk", "sphere", "fold"])
 def test_two_rank_shards_match_single_gpu(cuda, mode):
     import multiprocessing as mp
     import paper_1903_12359_b200 as pg
@@ -69,16 +82,30 @@ def test_two_rank_shards_match_single_gpu(cuda, mode):
         p.join(timeout=60)
     for r in res.values():
         assert not isinstance(r[1], str), r[2]
-    if mode == "sphere":
-        V, F, cuts = _sphere_case()
-        gp, rep = pg.parameterize(pg.TriMesh(V, F), cuts, "sphere")
-    else:
-        V, F, cuts = gen.height_field_case(65, 4, seed=2)
-        gp, rep = pg.parameterize(pg.TriMesh(V, F), cuts, mode, pairs=gen.row_tree_schedule_order(4, 4))
+    V, F, cuts, m, kw = _case(mode)
+    gp, rep = pg.parameterize(pg.TriMesh(V, F), cuts, m, **kw)
     ref = np.asarray(gp.coords)
     s0, s1 = res[0][3], res[1][3]
     assert s0 and s1 and sorted(s0 + s1) == list(range(rep.n_submeshes))
+    assert np.array_equal(res[0][1], ref)  # assembled on rank 0 from both ranks' own vertices
+    nb = sum(len(c) for c in pg.partition_mesh(pg.TriMesh(V, F), cuts).boundary_cycles)
     for r in (0, 1):
-        assert res[r][2] == rep.flips == 0
-        # disjoint sums are exact: identical up to the sign of zero
-        assert np.array_equal(res[r][1], ref)
+        flips, d, reps, xb, own = res[r][2], res[r][4], res[r][5], res[r][6], res[r][7]
+        assert flips == rep.flips
+        assert [x["flips_before"] for x in reps] == [x["flips_before"] for x in rep.repairs]
+        assert [x.get("remaining") for x in reps] == [x.get("remaining") for x in rep.repairs]
+        for key in ("median", "iqr"):  # per-corner |d| are the same numbers: exact order statistics agree
+            assert d["angular_abs"][key] == rep.distortion["angular_abs"][key]
+            # area ratios are normalised by summed areas (summation order differs)
+            assert abs(d["area_abs"][key] - rep.distortion["area_abs"][key]) <= 1e-12
+        for key in ("mean", "sd"):
+            assert abs(d["angular_abs"][key] - rep.distortion["angular_abs"][key]) <= 1e-12 * max(
+                1.0, abs(rep.distortion["angular_abs"][key]))
+        assert d["angular_histogram"] == rep.distortion["angular_histogram"]
+        assert d["excluded_corners"] == rep.distortion["excluded_corners"]
+        # the rank's own coordinates (the seams included) are the one-GPU ones
+        ok = ~np.isnan(own.real if own.ndim == 1 else own[:, 0])
+        assert np.array_equal(own[ok], ref[ok])
+        # exchange: the boundary all-gather (2 blocks of the longest rank's
+        # slots) plus the small summary / metric reductions
+        assert xb < 16 * (2 * nb + 4096) + 160_000, xb

@@ -132,3 +132,45 @@ def test_cfg3_cfg4_generators_shape():
     r = np.linalg.norm(V, axis=1)
     assert 0.69 <= r.min() and r.max() <= 1.31
     assert oracle.split_mesh(V, F, cuts).n_sub == 8
+
+
+def test_cyclic_runs_matches_oracle():
+    """partition._cyclic_runs (vectorised) equals the oracle's run finder
+    (oracle/planner.py, pinned to partition.py:149-179) on the goldens'
+    boundary-cycle pairs and on random cycles."""
+    import oracle.planner as op
+    from paper_1903_12359_b200.partition import _cyclic_runs
+    pairs = []
+    for case in ("cfg1", "blocks3x3", "strips4", "sphere4", "qtree4x4"):
+        cyc = unpack(load_golden(case), "cycles")
+        pairs += [(cyc[i], cyc[j]) for i in range(len(cyc)) for j in range(len(cyc)) if i != j]
+    rng = np.random.default_rng(5)
+    for _ in range(200):
+        n = int(rng.integers(3, 40))
+        c1 = rng.permutation(60)[:n]
+        c2 = list(rng.permutation(60)[:int(rng.integers(3, 40))])
+        if rng.random() < 0.7:  # splice a reversed arc of c1 into c2
+            s, ln = int(rng.integers(0, n)), int(rng.integers(2, n + 1))
+            arc = [int(c1[(s + t) % n]) for t in range(ln)][::-1]
+            c2 = arc + [v for v in c2 if v not in arc]
+        pairs.append((c1, np.array(c2)))
+    pairs.append((np.arange(6), np.arange(6)[::-1].copy()))
+    for a, b in pairs:
+        assert _cyclic_runs(a, b) == op.cyclic_runs(list(map(int, a)), list(map(int, b)))
+
+
+def test_cut_file_round_trip(tmp_path):
+    from paper_1903_12359_b200 import PartitionError
+    from paper_1903_12359_b200.partition import read_cut_edges, write_cut_edges
+    cuts = np.array([[0, 5], [3, 9], [12, 2]])
+    p = tmp_path / "c.cuts"
+    write_cut_edges(p, cuts)
+    assert np.array_equal(read_cut_edges(p), cuts)
+    p.write_text("# header\n1 2\n\n3 4\n")
+    assert np.array_equal(read_cut_edges(p), [[0, 1], [2, 3]])
+    p.write_text("1 2\n0 4\n")
+    with pytest.raises(PartitionError, match=":2: vertex ids are 1-based"):
+        read_cut_edges(p)
+    p.write_text("1 2 3\n")
+    with pytest.raises(PartitionError, match="expected two vertex ids"):
+        read_cut_edges(p)
