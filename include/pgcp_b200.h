@@ -401,6 +401,10 @@ PGCP_API int pgcp_corner_angles(const double* points, int kind, const int32_t* F
 PGCP_API int pgcp_area_distortion(const double* V, const int32_t* F, int64_t n, int64_t m, const double* coords,
                                   int mode_sphere, double* d, uint8_t* valid, void* stream);
 
+/* Measurement kernel (bench.py): stream buf[0, bytes) `reps` times with
+ * L2-only 16-byte loads; bytes x reps / time = attainable L2 read bandwidth. */
+PGCP_API int pgcp_l2_probe(const void* buf, int64_t bytes, int32_t reps, unsigned long long* sink, void* stream);
+
 /* host-side weld-schedule planner (partition.py:236-324): see planner.cpp */
 PGCP_API int pgcp_plan_weld_schedule(const int64_t* cyc, const int64_t* cyc_off, int32_t K,
                             const int64_t* cuts, int64_t ncuts, int mode_sphere,
