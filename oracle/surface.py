@@ -154,12 +154,16 @@ def split_mesh(V, F, cuts):
     ncomp, labels = face_components(F, cut_norm)
     sub_V, sub_F, vmaps, loops, cycles = [], [], [], [], []
     nvert = len(V)
+    # faces grouped by label, each group in increasing face order (= F[labels == ci])
+    order = np.argsort(labels, kind="stable")
+    bounds = np.searchsorted(labels[order], np.arange(ncomp + 1))
+    remap = np.full(nvert, -1, dtype=np.int64)
     for ci in range(ncomp):
-        f = F[labels == ci]
+        f = F[order[bounds[ci]:bounds[ci + 1]]]
         used = np.unique(f)
-        remap = np.full(nvert, -1, dtype=np.int64)
         remap[used] = np.arange(len(used))
         lf = remap[f]
+        remap[used] = -1
         chi, nl, cls = topology_class(len(used), lf)
         if cls != "disk_type":
             raise OraclePartitionError(

@@ -1,5 +1,5 @@
-// pcg.cu -- K3: batched fp64 Jacobi-preconditioned CG, one thread-block
-// cluster per subdomain, CG vectors resident in distributed shared memory.
+// pcg.cu -- K3: batched fp64 preconditioned CG, one thread-block cluster per
+// subdomain, CG vectors resident in distributed shared memory.
 //
 // Replaces the two `spsolve` calls of the hot path:
 //   flatten.py:157-173  DNCP: C_ff x = -C_f,fixed t with C = blockdiag(L,L) - 2M
@@ -8,31 +8,39 @@
 //     H = L_UU + 2i M_xy[U,U]      (flatten; M_xy[p,next]=+1/4, [p,prev]=-1/4)
 //     H = L_UU                      (harmonic; complex RHS)
 // which is exactly the real 2|U| system of the reference (pinned by
-// tests/test_oracle_pins.py::test_hermitian_form). CG on an HPD system with a
-// real diagonal preconditioner has real alpha/beta, so one recurrence serves
-// both halves and L is streamed once per iteration for both.
+// tests/test_oracle_pins.py::test_hermitian_form). CG on an HPD system with
+// an HPD preconditioner has real alpha/beta, so one recurrence serves both
+// halves and L is streamed once per iteration for both.
 //
 // Layout (per solve, over the listed subdomains = "slots"):
 //   rows      unknowns of slot j padded to 32*S_j rows (S_j slices); slot row
 //             base 32*sl_off[j]; padding rows are inert (D=1, b=0, val=0)
-//   matrix    sliced ELL, one 32-row slice per warp: entry k of row `lane` of
-//             slice s at sl_ptr[s] + 32k + lane, so every load of val/col is a
-//             coalesced 256 B / 128 B transaction; col = slot-local padded row
+//   matrix    paired sliced ELL (sell_pos): one 32-row slice per warp, two
+//             values per 16-byte lane load, Jacobi-scaled D^-1/2 H D^-1/2;
+//             columns re-encoded per launch as 16-bit CTA-local rows
+//             (all-local slices) or (owner CTA, byte offset) codes (slices
+//             that reach into another CTA's rows: DSMEM gathers)
 //   coupling  flatten boundary rows carry (next, prev) rows in cpl[] and a bit
 //             in the slice mask: (H z)_u += i/2 (z_next - z_prev)
-//   vectors   z, p, q (complex) live in the shared memory of the cluster's
-//             CTAs (48 B/row); x and the diagonal stay in global memory
 //
-// Iteration (2 cluster barriers, both inside the reductions):
-//   A: s = A z; q = s + beta q; p = z + beta p; pq = Re<p,q>        [gathers z]
-//   B: alpha = rz/pq; x += alpha p; z -= alpha Dinv q;
-//      rz = sum D|z|^2, rr = sum D^2|z|^2   (residual r = D z)
-// using A p_new = A z + beta A p_old, so only z is ever gathered.
+// Kernels:
+//   k_pcg2 (default) two-level PCG: M^-1 = I + W E^-1 W^T with W the linear
+//             functions (1, u, v) of geometric aggregates that never straddle
+//             a CTA; z, q, r in distributed shared memory, p and y in global
+//             memory (row-local); three cluster reductions per iteration
+//             (see the comment above k_pcg2); coarse start x0 = Q b.
+//   k_pcg     plain Jacobi-PCG (PGCP_PCG_COARSE=0, and the safety net that
+//             re-solves any slot the two-level solve did not finish), two
+//             cluster reductions per iteration, using A p_new = A z + beta A p
+//             so only z is ever gathered.
+// Every reduction is a fixed-order warp / CTA / cluster sum: results are
+// bitwise reproducible run to run.
 #include <cooperative_groups.h>
 #include <cub/device/device_radix_sort.cuh>
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <climits>
 #include <cstring>
@@ -95,11 +103,38 @@ struct SolveSystem {
     int ncb = 0, mu_cap = 0, items_cap = 0;  // k_pcg2 coarse shared layout (see PcgArgs)
     std::vector<int64_t> h_abase;
     double coarse_ms = 0;
+    std::vector<int32_t> h_iters;  // last run's iterations per slot
+    // Every buffer above is allocated (and later freed, cudaFreeAsync) on
+    // `home`, the stream of the call that built the system. A call that reads
+    // the system on another stream (the harmonic solve after a prepare on a
+    // side stream, export_system) makes `home` wait for its work, so the
+    // frees of a later rebuild or of pgcp_batch_destroy are ordered after it.
+    cudaStream_t home = nullptr;
+    bool has_home = false;
+    cudaEvent_t use_ev = nullptr;
+    void built_on(cudaStream_t s) {
+        home = s;
+        has_home = true;
+    }
+    int used_on(cudaStream_t s) {
+        if (!has_home || s == home) return PGCP_OK;
+        if (!use_ev) PGCP_TRY_CUDA(cudaEventCreateWithFlags(&use_ev, cudaEventDisableTiming));
+        PGCP_TRY_CUDA(cudaEventRecord(use_ev, s));
+        PGCP_TRY_CUDA(cudaStreamWaitEvent(home, use_ev, 0));
+        return PGCP_OK;
+    }
+    ~SolveSystem() {
+        if (use_ev) cudaEventDestroy(use_ev);
+    }
 };
 
 void free_system(void* p) { delete static_cast<SolveSystem*>(p); }
 
-static std::vector<int32_t> g_prev_iters;  // PGCP_PCG_ORDER=prev (launch-order experiment)
+// PGCP_PCG_ORDER=prev (launch-order experiment): the last two-level solve's
+// iteration counts; written and read by concurrent solves (flatten worker
+// thread, harmonic on the caller's thread), hence the lock
+static std::vector<int32_t> g_prev_iters;
+static std::mutex g_prev_mu;
 
 namespace {
 
@@ -2126,22 +2161,17 @@ int set_kernel_attrs(K kern) {
     return PGCP_OK;
 }
 
-// clusters of k_pcg2 that can be resident at once for a cluster shape
-int max_active_clusters(int csize, size_t smem) {
-    // the flatten (worker thread) and the harmonic preparation (caller's
-    // thread) choose their shapes concurrently
-    static std::mutex mu;
-    static std::vector<std::pair<long long, int>> cache;
-    std::lock_guard<std::mutex> lock(mu);
-    const long long key = (long long)csize << 32 | (long long)smem;
-    for (auto& kv : cache)
-        if (kv.first == key) return kv.second;
-    auto kern = k_pcg2<512, float2>;
+// clusters of k_pcg2 that can be resident at once for a cluster shape, for
+// the instantiation that will be launched (threads per CTA, E^-1 precision),
+// cached per device
+template <int NT, typename ET>
+int query_active_clusters(int csize, size_t smem) {
+    auto kern = k_pcg2<NT, ET>;
     int n = 0;
     if (set_kernel_attrs(kern) == PGCP_OK) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)csize, 1, 1);
-        cfg.blockDim = dim3(512, 1, 1);
+        cfg.blockDim = dim3(NT, 1, 1);
         cfg.dynamicSmemBytes = smem;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -2153,11 +2183,31 @@ int max_active_clusters(int csize, size_t smem) {
         if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) n = 0;
     }
     cudaGetLastError();
+    return n;
+}
+
+int max_active_clusters(int csize, size_t smem, int nt, bool einv_fp64) {
+    // the flatten (worker thread) and the harmonic preparation (caller's
+    // thread) choose their shapes concurrently
+    static std::mutex mu;
+    static std::vector<std::pair<std::array<long long, 5>, int>> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const std::array<long long, 5> key = {dev, nt, einv_fp64 ? 1 : 0, csize, (long long)smem};
+    std::lock_guard<std::mutex> lock(mu);
+    for (auto& kv : cache)
+        if (kv.first == key) return kv.second;
+    int n;
+    if (nt == 256)
+        n = einv_fp64 ? query_active_clusters<256, double2>(csize, smem) : query_active_clusters<256, float2>(csize, smem);
+    else
+        n = einv_fp64 ? query_active_clusters<512, double2>(csize, smem) : query_active_clusters<512, float2>(csize, smem);
     cache.emplace_back(key, n);
     return n;
 }
 
-int pick_cluster(int64_t max_slices, int32_t nslot, int32_t forced, bool coarse, int* csize_out, int* chunk_out) {
+int pick_cluster(int64_t max_slices, int32_t nslot, int32_t forced, bool coarse, int nt, bool einv_fp64,
+                 int* csize_out, int* chunk_out) {
     const int max_chunk = (SMEM_LIMIT - RED_BYTES - (coarse ? COARSE_BYTES : 0)) / (48 * 32 + 12);
     int cmin = 1;
     while (cmin <= MAX_CLUSTER && (max_slices + cmin - 1) / cmin > max_chunk) cmin *= 2;
@@ -2183,7 +2233,7 @@ int pick_cluster(int64_t max_slices, int32_t nslot, int32_t forced, bool coarse,
             const int64_t ch = (max_slices + cc - 1) / cc;
             if (cc > cmin && ch < 8) break;  // keep >= 256 rows per CTA
             const size_t smem = (size_t)RED_BYTES + (size_t)3 * 32 * ch * 16 + (size_t)12 * ch + COARSE_BYTES;
-            const int nconc = max_active_clusters(cc, smem);
+            const int nconc = max_active_clusters(cc, smem, nt, einv_fp64);
             if (nconc < 1) continue;
             const double waves = (double)((nslot + nconc - 1) / nconc);
             const double cost = waves * (10900.0 + 8.6 * 32.0 * (double)ch);
@@ -2458,9 +2508,7 @@ int build_coarse(SolveSystem* S, int csize, cudaStream_t s) {
         }
         PGCP_TRY(S->eoff32.alloc(nslot + 1, s));
         PGCP_TRY_CUDA(cudaMemcpyAsync(S->eoff32.p, he32.data(), (nslot + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
-        const char* ef = getenv("PGCP_COARSE_FP64");
-        S->einv_fp64 = ef && atoi(ef) != 0;
-        if (S->einv_fp64) {
+        if (S->einv_fp64) {  // PGCP_COARSE_FP64=1 (read in setup_solve)
             PGCP_TRY(S->einv64.alloc(std::max<int64_t>(he32[nslot], 1), s));
             k_hermitize<double2><<<nslot, 512, 0, s>>>(S->abase.p, S->eoff.p, S->einv.p, S->eoff32.p, S->einv64.p);
         } else {
@@ -2676,10 +2724,14 @@ int setup_solve(SolveSystem* S, const pgcp_solve_opts* o, cudaStream_t s) {
     int64_t max_sl = 0;
     for (int j = 0; j < nslot; ++j) max_sl = std::max(max_sl, S->h_sl_off[j + 1] - S->h_sl_off[j]);
     int csize = 1, chunk = 1;
-    PGCP_TRY(pick_cluster(max_sl, nslot, o ? o->cluster : 0, S->coarse, &csize, &chunk));
+    if (const char* en = getenv("PGCP_PCG2_NT")) S->pcg_nt = atoi(en) == 256 ? 256 : 512;
+    {
+        const char* ef = getenv("PGCP_COARSE_FP64");
+        S->einv_fp64 = ef && atoi(ef) != 0;
+    }
+    PGCP_TRY(pick_cluster(max_sl, nslot, o ? o->cluster : 0, S->coarse, S->pcg_nt, S->einv_fp64, &csize, &chunk));
     S->csize = csize;
     S->chunk = chunk;
-    if (const char* en = getenv("PGCP_PCG2_NT")) S->pcg_nt = atoi(en) == 256 ? 256 : 512;
     if (S->coarse) {
         cudaEvent_t c0, c1;
         PGCP_TRY_CUDA(cudaEventCreate(&c0));
@@ -2754,11 +2806,33 @@ int run_solve(pgcp_batch* b, SolveSystem* S, const pgcp_solve_opts* o, double* z
     for (int j = 0; j < nslot; ++j) hord[j] = j;
     if (S->coarse && !S->force_jacobi) {
         const char* eo = getenv("PGCP_PCG_ORDER");
-        if (eo && !strcmp(eo, "prev") && (int)g_prev_iters.size() == nslot)
-            std::stable_sort(hord.begin(), hord.end(), [](int a, int b) { return g_prev_iters[a] > g_prev_iters[b]; });
+        std::vector<int32_t> prev;
+        if (eo && !strcmp(eo, "prev")) {
+            std::lock_guard<std::mutex> lock(g_prev_mu);
+            prev = g_prev_iters;
+        }
+        // the harmonic solve launches its clusters heaviest first, predicted
+        // by the same subdomains' iteration counts in the batch's last
+        // flatten (longest-processing-time order shortens the last wave);
+        // PGCP_HARM_ORDER=0 keeps the slot order
+        std::vector<int32_t> pred;
+        const char* eh = getenv("PGCP_HARM_ORDER");
+        const SolveSystem* FS = static_cast<const SolveSystem*>(b->sys[0]);
+        if (!eo && !S->dncp && !(eh && atoi(eh) == 0) && FS && FS != S && (int)FS->h_iters.size() == FS->nslot) {
+            std::vector<int32_t> by_comp(b->K, -1);
+            for (int j = 0; j < FS->nslot; ++j) by_comp[FS->comps[j]] = FS->h_iters[j];
+            pred.resize(nslot);
+            bool all = true;
+            for (int j = 0; j < nslot; ++j) all &= (pred[j] = by_comp[S->comps[j]]) >= 0;
+            if (!all) pred.clear();
+        }
+        if (eo && !strcmp(eo, "prev") && (int)prev.size() == nslot)
+            std::stable_sort(hord.begin(), hord.end(), [&](int a, int b) { return prev[a] > prev[b]; });
         else if (eo && !strcmp(eo, "rev"))
             std::reverse(hord.begin(), hord.end());
-        if (eo) {
+        else if (!pred.empty())
+            std::stable_sort(hord.begin(), hord.end(), [&](int a, int b) { return pred[a] > pred[b]; });
+        if (eo || !pred.empty()) {
             PGCP_TRY(dorder.alloc(nslot, s));
             PGCP_TRY_CUDA(cudaMemcpyAsync(dorder.p, hord.data(), nslot * sizeof(int32_t), cudaMemcpyHostToDevice, s));
             A.order = dorder.p;
@@ -2825,7 +2899,11 @@ int run_solve(pgcp_batch* b, SolveSystem* S, const pgcp_solve_opts* o, double* z
     PGCP_TRY_CUDA(cudaMemcpyAsync(hit.data(), S->iters.p, nslot * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     PGCP_TRY_CUDA(cudaMemcpyAsync(hres.data(), S->res.p, 8 * nslot * sizeof(double), cudaMemcpyDeviceToHost, s));
     PGCP_TRY_CUDA(cudaStreamSynchronize(s));
-    if (S->coarse && !S->force_jacobi) g_prev_iters = hit;
+    S->h_iters = hit;
+    if (S->coarse && !S->force_jacobi) {
+        std::lock_guard<std::mutex> lock(g_prev_mu);
+        g_prev_iters = hit;
+    }
     if (A.hist) {
         std::vector<double> hh((size_t)nslot * HIST_K * 3);
         PGCP_TRY_CUDA(cudaMemcpy(hh.data(), hbuf.p, hh.size() * sizeof(double), cudaMemcpyDeviceToHost));
@@ -3013,6 +3091,7 @@ int solve_flatten(pgcp_batch* b, const int32_t* comps, int32_t ncomp, const int3
     delete slot;
     slot = new SolveSystem();
     SolveSystem* S = slot;
+    S->built_on(s);
     PGCP_TRY(prepare_slots(b, S, comps, ncomp));
     if (S->nslot == 0) return PGCP_OK;
     double2 t[2] = {make_double2(0.0, 0.0), make_double2(1.0, 0.0)};
@@ -3110,6 +3189,7 @@ int solve_flatten(pgcp_batch* b, const int32_t* comps, int32_t ncomp, const int3
     }
     if (st)
         for (int j = 0; j < S->nslot; ++j) st[j] = hst[j];
+    PGCP_TRY(S->used_on(s));
     return rc;
 }
 
@@ -3122,6 +3202,7 @@ int prepare_harmonic(pgcp_batch* b, const int32_t* comps, int32_t ncomp, const i
     delete slot;
     slot = new SolveSystem();
     SolveSystem* S = slot;
+    S->built_on(s);
     PGCP_TRY(prepare_slots(b, S, comps, ncomp));
     S->nfixed = nfixed;
     PGCP_TRY(S->fixed_gid_copy.alloc(std::max<int64_t>(nfixed, 1), s));
@@ -3201,6 +3282,7 @@ int finish_harmonic(pgcp_batch* b, const double* fixed_val, int64_t nfixed, cons
     }
     if (st)
         for (int j = 0; j < S->nslot; ++j) st[j] = hst[j];
+    PGCP_TRY(S->used_on(s));
     return rc;
 }
 

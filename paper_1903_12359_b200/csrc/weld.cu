@@ -6,22 +6,30 @@
 //   SqrtRatio(pts[0], pts[1]); Open(pts[j]) j = 2..k; axis-Mobius(pts[0]);
 //   Close(va[j], vb[j]) j = k-1..1; SquareMobius(va[0]); 3-point Mobius(aux).
 // So a weld runs in two phases:
-//   phase 1  one CTA per weld holds only the 2(k+3) arc + tracking points in
-//            shared memory and builds both logs record by record (a block
-//            barrier per record; the records are the serial critical path);
+//   phase 1  k_phase1c: one thread-block cluster per weld (up to 16 CTAs)
+//            holds the 2(k+3) arc + tracking points in the CTAs' shared
+//            memory; per record step the owners of the next parameter points
+//            publish them into every CTA through DSMEM, one cluster barrier,
+//            then every thread rebuilds the record and applies it to its
+//            points (the records are the serial critical path);
 //   phase 2  every other tracked point of the two components (non-arc cycle
 //            points and interior seam points: the reference's `apply_log` on
 //            "others", pipeline.py:200-204) replays its side's log
-//            independently -- one thread per point over the whole GPU.
+//            independently. k_replay_stream runs concurrently with phase 1
+//            as its programmatic dependent launch, applying records as soon
+//            as phase 1's published per-log record counter covers them
+//            (PGCP_WELD_STREAM=0: the serial k_replay_slots after phase 1).
 // Welds of one schedule level touch disjoint components and run as one
-// launch (one CTA each); checks whose inputs span all points (the far-end
-// and seam scale tests, welding.py:689-692 and 721-729) are finished after
-// phase 2 from per-step maxima.
+// launch (one cluster each); checks whose inputs span all points (the
+// far-end and seam scale tests, welding.py:689-692 and 721-729) are finished
+// after phase 2 from per-step maxima.
 //
 // Numerics: complex division follows numpy's algorithm, the square root
 // glibc's csqrt; record semantics (pins, side tags, infinity handling) follow
 // the reference record by record. Results agree with the reference to
-// rounding (tests/test_gpu_weld.py), not bit for bit.
+// rounding (<= 1e-9 relative: tests/test_gpu_pipeline.py
+// test_welds_match_reference / test_weld_corpus, and the k >= 1000 welds of
+// cfg 2 in tests/test_gpu_cfg2.py), not bit for bit.
 #include <algorithm>
 #include <cmath>
 #include <cstring>

@@ -166,3 +166,23 @@ def test_streamed_replay_failed_step(cuda, monkeypatch):
         monkeypatch.setenv("PGCP_WELD_STREAM", mode)
         with pytest.raises(WeldError, match="zip points 0 and 1 coincide"):
             partial_weld(np.array([0, 0, 1 + 1j, 1j]), a, 2)
+
+
+@pytest.mark.parametrize("env", [{"PGCP_PCG_COARSE": "0"}, {"PGCP_COARSE_FP64": "1"}, {"PGCP_PCG2_NT": "256"},
+                                 {"PGCP_PCG_GMAX": "4"}, {"PGCP_PCG_ORDER": "rev"}, {"PGCP_PCG_ORDER": "prev"},
+                                 {"PGCP_PCG_X0": "0"}, {"PGCP_OVERLAP_HPREP": "0"}])
+def test_solver_switches_match_reference(cuda, monkeypatch, env):
+    """Every A/B switch of the PCG: plain Jacobi-PCG,
+    fp64 E^-1, 256-thread CTAs, a coarser coarse grid, both launch orders,
+    the start from zero, the non-overlapped harmonic preparation -- each
+    must still give the reference's UV."""
+    from paper_1903_12359_b200 import TriMesh, parameterize
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    for case in ("qtree4x4", "disk2x2"):
+        z = load_golden(case)
+        kw = {"pairs": case_pairs(case)} if case_pairs(case) is not None else {}
+        gp, rep = parameterize(TriMesh(z["V"], z["F"]), z["cuts"], str(z["mode"]), **kw)
+        ref = z["coords"]
+        assert np.max(np.abs(np.asarray(gp.coords) - ref)) <= 1e-6 * _diam(ref), (case, env)
+        assert rep.flips == 0
