@@ -1,6 +1,11 @@
 import os
 import sys
 
+# the oracle's SuperLU solves run in worker processes in several tests: one
+# BLAS thread each (unset, every worker spins up a thread per core)
+for _var in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
+    os.environ.setdefault(_var, "1")
+
 import numpy as np
 import pytest
 

@@ -109,3 +109,49 @@ def test_two_rank_shards_match_single_gpu(cuda, mode):
         # exchange: the boundary all-gather (2 blocks of the longest rank's
         # slots) plus the small summary / metric reductions
         assert xb < 16 * (2 * nb + 4096) + 160_000, xb
+
+
+def _nccl_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        torch.cuda.set_device(rank)
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+        import paper_1903_12359_b200 as pg
+        from paper_1903_12359_b200.dist import Shard, gather_coords
+        shard = Shard()
+        V, F, cuts, m, kw = _case("free")
+        gp, rep = pg.parameterize(pg.TriMesh(V, F), cuts, m, shard=shard, **kw)
+        q.put((rank, gather_coords(gp, shard), rep.flips, rep.distortion["angular_abs"]["median"]))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as exc:  # pragma: no cover
+        q.put((rank, "error", repr(exc), None))
+
+
+def test_two_gpu_nccl_matches_single_gpu(cuda):
+    """The production transport: two ranks on two GPUs over NCCL (one
+    all-gather + the small reductions). Runs where two GPUs are visible."""
+    import multiprocessing as mp
+    import torch
+    import paper_1903_12359_b200 as pg
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two GPUs")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_nccl_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict((r[0], r) for r in (q.get(timeout=300) for _ in range(2)))
+    for p in procs:
+        p.join(timeout=60)
+    for r in res.values():
+        assert not isinstance(r[1], str), r[2]
+    V, F, cuts, m, kw = _case("free")
+    gp, rep = pg.parameterize(pg.TriMesh(V, F), cuts, m, **kw)
+    assert np.array_equal(res[0][1], np.asarray(gp.coords))
+    assert res[0][2] == res[1][2] == rep.flips == 0
+    assert res[0][3] == res[1][3] == rep.distortion["angular_abs"]["median"]
