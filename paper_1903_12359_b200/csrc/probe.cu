@@ -1,6 +1,6 @@
 // probe.cu -- bandwidth probe for bench.py's roofline denominators.
 //
-// k_l2_probe streams a buffer that fits in L2 (bench.py uses 48 MiB of the
+// k_l2_probe streams a buffer that fits in L2 (bench.py uses 64 MiB of the
 // 126 MB) `reps` times with 16-byte L2-only loads (ld.global.cg: no L1
 // allocation), eight loads in flight per thread, a persistent grid of 4
 // CTAs x 512 threads per SM. bytes x reps / time is the L2 -> SM read
@@ -16,21 +16,24 @@ namespace {
 template <int U>
 __global__ void __launch_bounds__(512) k_l2_probe(const int4* __restrict__ buf, int64_t n16, int reps,
                                                   unsigned long long* __restrict__ sink) {
+    // one continuous stream of reps x n16 loads per grid (the index wraps at
+    // the buffer end), U independent loads in flight per thread
     int acc = 0;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    for (int r = 0; r < reps; ++r) {
-        int64_t i = t0;
-        for (; i + (U - 1) * stride < n16; i += U * stride) {
-            int4 v[U];
+    const int64_t total = (int64_t)reps * n16;
+    int64_t idx[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u) v[u] = __ldcg(buf + i + u * stride);
+    for (int u = 0; u < U; ++u) idx[u] = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x + u * stride) % n16;
+    const int64_t step = (U * stride) % n16;
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v + (U - 1) * stride < total; v += U * stride) {
+        int4 x[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u) acc ^= v[u].x ^ v[u].w ^ v[u].y ^ v[u].z;
-        }
-        for (; i < n16; i += stride) {
-            int4 a = __ldcg(buf + i);
-            acc ^= a.x ^ a.w;
+        for (int u = 0; u < U; ++u) x[u] = __ldcg(buf + idx[u]);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            acc ^= x[u].x ^ x[u].w ^ x[u].y ^ x[u].z;
+            idx[u] += step;
+            if (idx[u] >= n16) idx[u] -= n16;
         }
     }
     if (acc == 0x7f3a5c11) atomicAdd(sink, 1ull);  // keeps the loads live

@@ -9,5 +9,5 @@ from paper_1903_12359_b200 import _native as nat
 dev = torch.device("cuda", 0)
 for u in ("4", "8"):
     os.environ["PGCP_L2_PROBE_U"] = u
-    for mib in (16, 32, 48, 64, 96):
+    for mib in (16, 32, 48, 64, 80, 96):
         print(f"U={u} {mib:3d} MiB: {B.l2_probe_gbs(dev, mib=mib):8.0f} GB/s", flush=True)
