@@ -105,7 +105,7 @@ def ncu_traffic(name="pcg_ncu_summary.json"):
     return ncu_summary(name).get("dram_bytes_per_launch")
 
 
-def l2_probe_gbs(dev, mib=64, reps=40):
+def l2_probe_gbs(dev, mib=48, reps=40):
     """Attainable L2 -> SM read bandwidth, measured here: pgcp_l2_probe
     streams an L2-resident buffer with 16-byte L2-only loads (probe.cu),
     timed with CUDA events on the launch stream (best of 3)."""
@@ -402,7 +402,7 @@ def main():
     roof = {"bound": "l2", "kernel": "k_pcg2 (two-level PCG, DNCP flatten of the 64 subdomains, one launch)",
             "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": ncu_traffic(),
             "lts_bytes_per_launch": ncu.get("lts_bytes_per_launch"),
-            "l2_peak": l2_peak, "l2_peak_source": "measured here: pgcp_l2_probe (64 MiB resident, L2-only 16-B loads, best of 3)",
+            "l2_peak": l2_peak, "l2_peak_source": "measured here: pgcp_l2_probe (48 MiB resident, L2-only 16-B loads, best of 3)",
             "l2_frac": dev_ach / l2_peak if l2_peak else None,
             "peak_source": peak_src, "kernel_ms": kernel_ms, "iterations_per_launch": statistics.mean(pcg_iters),
             "bytes_per_launch": ref_launch,

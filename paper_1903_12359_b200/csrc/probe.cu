@@ -1,8 +1,8 @@
 // probe.cu -- bandwidth probe for bench.py's roofline denominators.
 //
-// k_l2_probe streams a buffer that fits in L2 (bench.py uses 64 MiB of the
+// k_l2_probe streams a buffer that fits in L2 (bench.py uses 48 MiB of the
 // 126 MB) `reps` times with 16-byte L2-only loads (ld.global.cg: no L1
-// allocation), eight loads in flight per thread, a persistent grid of 4
+// allocation), four loads in flight per thread, a persistent grid of 4
 // CTAs x 512 threads per SM. bytes x reps / time is the L2 -> SM read
 // bandwidth a streaming kernel can reach on this part; the PCG kernel's
 // working set is served from there.
@@ -56,9 +56,10 @@ PGCP_API int pgcp_l2_probe(const void* buf, int64_t bytes, int32_t reps, unsigne
     int dev = 0, sms = 148;
     PGCP_TRY_CUDA(cudaGetDevice(&dev));
     PGCP_TRY_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    // 8 independent 16-byte loads per thread in flight (4 with PGCP_L2_PROBE_U=4)
+    // 4 independent 16-byte loads per thread in flight (8 with PGCP_L2_PROBE_U=8;
+    // tools/l2_probe_sweep.py: 4 reaches the higher rate)
     const char* eu = getenv("PGCP_L2_PROBE_U");
-    if (eu && atoi(eu) == 4)
+    if (!(eu && atoi(eu) == 8))
         k_l2_probe<4><<<4 * sms, 512, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
             reinterpret_cast<const int4*>(buf), bytes / 16, reps, sink);
     else

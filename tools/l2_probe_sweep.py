@@ -7,7 +7,7 @@ import bench as B
 from paper_1903_12359_b200 import _native as nat
 
 dev = torch.device("cuda", 0)
-for u in ("4", "8"):
+for u in ("4", "8"):  # default kernel: 4
     os.environ["PGCP_L2_PROBE_U"] = u
     for mib in (16, 32, 48, 64, 80, 96):
         print(f"U={u} {mib:3d} MiB: {B.l2_probe_gbs(dev, mib=mib):8.0f} GB/s", flush=True)
