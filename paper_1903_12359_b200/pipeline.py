@@ -345,10 +345,17 @@ def parameterize(mesh, cuts=None, mode="free", workers=1, seed=0, mobius_area=Fa
             ext_slots = torch.as_tensor(plan.slots_of(exterior).astype(np.int32)).to(dev)
             nat.check(nat.lib().pgcp_inv_shift(_ptr(tv), _ptr(ext_slots), ext_slots.numel(), 0.0, 0.0,
                                                center.real, center.imag, _stream()))
+        # sharded: the other ranks' subdomains stay NaN here (never solved on
+        # this rank; stitch and metrics skip them) except their boundary
+        # loops, filled below with the welded values
+        zout = None
+        if own is not None:
+            zout = torch.full((int(voff[-1]),), complex(float("nan"), float("nan")), dtype=torch.complex128,
+                              device=dev)
         if overlap_prep:
-            z, hst = batch.harmonic_solve(tv, rtol=cfg.rtol, cluster=cfg.cluster)
+            z, hst = batch.harmonic_solve(tv, rtol=cfg.rtol, cluster=cfg.cluster, out=zout)
         else:
-            z, hst = batch.harmonic(loop_gid, tv, comps=own, rtol=cfg.rtol, cluster=cfg.cluster)
+            z, hst = batch.harmonic(loop_gid, tv, comps=own, rtol=cfg.rtol, cluster=cfg.cluster, out=zout)
         report.solver["harmonic_iters"] = [s["iters"] for s in hst]
         report.solver["harmonic"] = batch.last_solve(1)
         # fold-over repair of the submeshes whose harmonic map flipped faces
