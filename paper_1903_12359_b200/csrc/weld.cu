@@ -563,9 +563,14 @@ __device__ double block_max(double v, double* red) {
 }
 
 // Prenormalizer (welding.py:609-625) over the n points src[0..n) of tv.
-__device__ bool prenormalize(const double2* tv, const int32_t* src, int n, double* red, Rec* out, int* code) {
+// Every thread below `nth` takes points threadIdx.x, + nth, ... (the others
+// add zeros), so the sums do not depend on blockDim beyond nth.
+__device__ bool prenormalize(const double2* tv, const int32_t* src, int n, double* red, Rec* out, int* code,
+                             int nth = 0) {
+    if (nth <= 0) nth = blockDim.x;
+    const int i0 = threadIdx.x < nth ? (int)threadIdx.x : n;
     double sx = 0, sy = 0, cnt = 0;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    for (int i = i0; i < n; i += nth) {
         double2 z = tv[src[i]];
         if (c_fin(z)) {
             sx += z.x;
@@ -582,7 +587,7 @@ __device__ bool prenormalize(const double2* tv, const int32_t* src, int n, doubl
     }
     double2 c = C(sx / cnt, sy / cnt);
     double m = 0;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    for (int i = i0; i < n; i += nth) {
         double2 z = tv[src[i]];
         if (c_fin(z)) m = fmax(m, cabs_(csub(z, c)));
     }
@@ -594,7 +599,7 @@ __device__ bool prenormalize(const double2* tv, const int32_t* src, int n, doubl
     int tries = 0;
     for (; tries < 4; ++tries) {
         double hit = 0;
-        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        for (int i = i0; i < n; i += nth) {
             double2 z = tv[src[i]];
             if (c_fin(z) && c_eq(z, c)) hit = 1;
         }
@@ -1010,6 +1015,658 @@ __global__ void __launch_bounds__(NT, 1) k_phase1c(Phase1Args A) {
         area = block_sum(area, red);
         bad = block_max(bad, red);
         if (logger) {  // every thread holds the reductions; the logger owns the record counts
+            meta[0] = na_rec;
+            meta[1] = nb_rec;
+            meta[5] = seam;
+            meta[11] = ma;
+            meta[12] = mb;
+            meta[13] = mx;
+            meta[16] = area;
+            if (bad > 0) {
+                meta[2] = WE_NAN;
+                meta[4] = 3;
+            }
+        }
+        progress(true);
+    }
+    return;
+fail:
+    if (logger) {
+        meta[2] = err;
+        meta[3] = eidx;
+        meta[4] = eaux;
+    }
+    progress(true);
+}
+
+// ---------------------------------------------------------------------------
+// phase 1, wavefront form (default; PGCP_WELD_WAVE=0 selects k_phase1c).
+//
+// The zip (Open) and alignment (Close) loops are 2(k-1) of the weld's 2k+3
+// records, and record j's parameter is a single point (a_j, b_j) after all
+// earlier records. k_phase1c pays a cluster barrier per record so that every
+// CTA can rebuild it. Here the chain instead runs inside the warp that holds
+// the parameter points: points are interleaved by index (point id
+// q = 2 t + side, so a_t and b_t sit in adjacent lanes and both sides of an
+// index in one warp), and the owning warp takes the parameters by shuffle,
+// builds the record, applies it to its own points and moves on to the next
+// index -- no memory operation and no barrier on the chain. It publishes each
+// record into a ring in its CTA's shared memory (a CTA-scope release of a
+// per-producer counter); the other warps of the CTA apply records from the
+// ring as they appear (they lag behind, off the chain); a forwarder warp per
+// CTA copies the CTA's own records into every other CTA's ring (DSMEM,
+// cluster-scope release of that CTA's counter), writes the logs for the
+// replay and publishes the replay's progress counter. The chain moves to the
+// next warp every 16 indices and to the next CTA every PT / 2.
+// Every point applies the same records in the same order as in k_phase1c,
+// with the same arithmetic, so the results are bit-identical
+// (tests/test_gpu_pipeline.py::test_wave_weld_equals_barrier_weld).
+// Errors (the checks of welding.py:655-687) abort the chain through a flag
+// bit in the counters; every spin has a 2 s timeout that reports an internal
+// error instead of hanging.
+
+constexpr int WAVE_ABORT = 1 << 30;
+constexpr int WAVE_COUNT = (1 << 30) - 1;
+constexpr int WE_TIMEOUT = 19;
+constexpr unsigned long long WAVE_TIMEOUT_NS = 2000000000ull;
+
+struct WaveRec {
+    double x0, x1, x2, x3;  // Open: xi.re, xi.im, pp, qq; Close: a, b, c, d
+};
+
+__device__ __forceinline__ int ld_vol_i(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
+__device__ __forceinline__ void st_vol_i(int* p, int v) { *reinterpret_cast<volatile int*>(p) = v; }
+__device__ __forceinline__ void fence_cluster() { asm volatile("fence.acq_rel.cluster;" ::: "memory"); }
+__device__ __forceinline__ void fence_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
+// wait until *cnt (this CTA's shared memory) reaches need or carries the abort
+// bit; returns the observed value (WAVE_ABORT set on abort / timeout)
+__device__ __forceinline__ int wave_wait(const int* cnt, int need, unsigned long long& t0) {
+    int v = ld_vol_i(cnt);
+    int spins = 0;
+    while ((v & WAVE_COUNT) < need && !(v & WAVE_ABORT)) {
+        if (++spins == 256) {
+            spins = 0;
+            const unsigned long long now = gtimer();
+            if (t0 == 0) {
+                t0 = now;
+            } else if (now - t0 > WAVE_TIMEOUT_NS) {
+                return WAVE_ABORT | WAVE_COUNT;  // reported as WE_TIMEOUT by the caller
+            }
+        }
+        v = ld_vol_i(cnt);
+    }
+    return v;
+}
+
+template <int PT>
+__global__ void __launch_bounds__(PT + 32, 1) k_phase1w(Phase1Args A) {
+    constexpr int NT = PT + 32;
+    constexpr unsigned FULL = 0xffffffffu;
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ PParam s_param[2][NPARAM];
+    __shared__ double s_flag[2][NFLAG];
+    __shared__ double red[32];
+    __shared__ int s_cnt[2][PC_MAXCS];  // [open, close][producer CTA] records available from that CTA
+    __shared__ int s_err[4];            // rank 0's copy: code, index, aux, taken
+    cgw::cluster_group cl = cgw::this_cluster();
+    const int CS = (int)cl.num_blocks();
+    const int rank = (int)cl.block_rank();
+    const int step = blockIdx.x / CS;
+    const StepDesc sd = A.steps[step];
+    double* meta = A.meta + META * (int64_t)step;
+    const int k = sd.k;
+    const int P = k + 3;
+    const int NP = 2 * P;
+    const int chunk = (((NP + CS - 1) / CS) + 1) & ~1;  // even: a_t and b_t in one CTA, one warp
+    const int lo = min(NP, rank * chunk), hi = min(NP, lo + chunk);
+    WaveRec* ringO = reinterpret_cast<WaveRec*>(smem);  // [k + 1][2]
+    WaveRec* ringC = ringO + 2 * (k + 1);              // [k + 1]
+    const int lane = threadIdx.x & 31;
+    const bool fwd = threadIdx.x >= PT;                 // the forwarder warp
+    const int q = lo + (int)threadIdx.x;
+    const bool have = !fwd && q < hi;
+    const int side = q & 1, t = q >> 1;
+    const int wq0 = lo + (int)(threadIdx.x & ~31u);     // first point id of my warp
+    Rec* log_a = A.recs + sd.rec;
+    Rec* log_b = log_a + sd.cap;
+    const bool logger = rank == 0 && (int)threadIdx.x == PT;
+    int na_rec = 0, nb_rec = 0, nlogged = 0;
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    int* prog = A.prog ? A.prog + 2 * step : nullptr;
+    auto progress = [&](bool fin) {
+        if (!logger || !prog) return;
+        if (!fin && (++nlogged % A.prog_every) != 0) return;
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        prog_store(prog, na_rec | (fin ? PROG_DONE : 0));
+        prog_store(prog + 1, nb_rec | (fin ? PROG_DONE : 0));
+    };
+    if (threadIdx.x < 2 * PC_MAXCS) (&s_cnt[0][0])[threadIdx.x] = 0;
+    if (threadIdx.x < 4) s_err[threadIdx.x] = 0;
+    if (logger)
+        for (int i = 0; i < META; ++i) meta[i] = 0.0;
+    if (k < 1 || k > sd.na - 1 || k > sd.nb - 1) {
+        if (logger) {
+            meta[2] = WE_K;
+            meta[3] = k;
+        }
+        progress(true);
+        return;
+    }
+    const int32_t* sa = A.src + sd.src;
+    const int32_t* sb = sa + sd.na;
+    Rec pre[2];
+    int pcode = 0;
+    // the point threads' reduction order, as k_phase1c<PT> (bit-identical prenormalizer)
+    bool okA = prenormalize(A.tv, sa, sd.na, red, &pre[0], &pcode, PT);
+    bool okB = okA && prenormalize(A.tv, sb, sd.nb, red, &pre[1], &pcode, PT);
+    if (!okA || !okB) {
+        if (logger) {
+            meta[2] = WE_PRE;
+            meta[3] = okA ? 1 : 0;
+            meta[4] = pcode;
+        }
+        progress(true);
+        return;
+    }
+    const bool timed = A.timing && rank == 0 && threadIdx.x == 0;
+    const long long tk0 = timed ? clock64() : 0;
+    long long tk1 = tk0, tk2 = tk0;
+    double2 z = C(0.0, 0.0);
+    int8_t s8 = 0;
+    if (have) {
+        if (t <= k) {
+            z = A.tv[(side ? sb : sa)[t]];
+            int8_t tmp = 0;
+            apply_rec(pre[side], z, tmp);
+        } else {
+            z = (t == k + 1) ? C(0.0, 0.0) : cinf();
+        }
+    }
+    if (logger) {
+        log_a[na_rec++] = pre[0];
+        log_b[nb_rec++] = pre[1];
+    }
+    progress(false);
+    int parity = 0;
+    // point ids -> every CTA's parameter slots, then the cluster barrier
+    auto publish = [&](const int* qidx, int np, double flag) {
+        for (int which = 0; which < np; ++which) {
+            if (have && q == qidx[which]) {
+                PParam pp;
+                pp.z = z;
+                pp.s = s8;
+                pp.pad = 0;
+                for (int dst = 0; dst < CS; ++dst) cl.map_shared_rank(&s_param[parity][0], dst)[which] = pp;
+            }
+        }
+        if (threadIdx.x < CS) cl.map_shared_rank(&s_flag[parity][0], threadIdx.x)[rank] = flag;
+        cl.sync();
+    };
+    // the first error of a wavefront loop, kept in rank 0's s_err
+    auto raise = [&](int code, int idx, int aux) {
+        int* e = cl.map_shared_rank(s_err, 0);
+        if (atomicCAS(e + 3, 0, 1) == 0) {
+            e[0] = code;
+            e[1] = idx;
+            e[2] = aux;
+        }
+    };
+    // abort a wavefront loop everywhere: the abort bit into every counter of every CTA
+    auto abort_all = [&](int loop) {
+        for (int x = 0; x < CS; ++x)
+            for (int r = 0; r < CS; ++r) atomicOr(cl.map_shared_rank(&s_cnt[loop][r], x), WAVE_ABORT);
+    };
+    auto take_error = [&](int& err, int& eidx, int& eaux) {  // after a cluster barrier
+        const int* e = cl.map_shared_rank(s_err, 0);
+        if (e[3]) {
+            err = e[0];
+            eidx = e[1];
+            eaux = e[2];
+        }
+    };
+    int err = 0, eidx = 0, eaux = 0;
+    Rec ra, rb;
+    bool has[2] = {false, false};  // axis Mobius records logged (below)
+    // ---- zip step 1: SqrtRatio
+    {
+        int gi[4] = {0, 2, 1, 3};  // a0, a1, b0, b1
+        publish(gi, 4, 0.0);
+        PParam* pp = s_param[parity];
+        if (c_eq(pp[0].z, pp[1].z) || c_eq(pp[2].z, pp[3].z)) err = WE_ZIP01;
+        ra = mk_sqr(pp[0].z, pp[1].z, UP);
+        rb = mk_sqr(pp[2].z, pp[3].z, DOWN);
+        parity ^= 1;
+    }
+    if (err) goto fail;
+    if (logger) {
+        log_a[na_rec++] = ra;
+        log_b[nb_rec++] = rb;
+    }
+    progress(false);
+    if (have) apply_rec(side ? rb : ra, z, s8);
+    // ---- zip steps j = 2..k: Open, as a wavefront
+    if (k >= 2) {
+        unsigned long long t0 = 0;
+        if (!fwd) {
+            int j = 2;
+            while (j <= k) {
+                const int lp = 2 * j - wq0;
+                if (lp >= 0 && lp < 32 && 2 * j < hi) {
+                    // my warp holds a_j .. a_j1 and b_j .. b_j1 (lanes 2(j - t0) + side):
+                    // produce the whole segment. Only the lanes whose own index is
+                    // still ahead apply each record at once (all unzipped: one branch
+                    // of apply_open, no divergence on the chain); the others catch
+                    // up from the ring after the segment.
+                    const int j1 = min(k, min((hi - 1) / 2, (wq0 + 31) / 2));
+                    const int j0 = j;
+                    bool bad = false;
+                    for (; j <= j1; ++j) {
+                        const int lq = 2 * j - wq0;
+                        const double2 xs = C(__shfl_sync(FULL, z.x, lq + side), __shfl_sync(FULL, z.y, lq + side));
+                        const int ss = __shfl_sync(FULL, (int)s8, lq + side);
+                        int e = 0;
+                        if (ss != 0 || c_isinf(xs)) {
+                            e = WE_ZIP_HALF;
+                        } else if (!(xs.x > 0)) {
+                            e = WE_ZIP_AXIS;
+                        } else if (cabs_lt(xs, 1e-13)) {
+                            e = WE_ZIP_COLL;
+                        }
+                        const int ea = __shfl_sync(FULL, e, lq), eb = __shfl_sync(FULL, e, lq + 1);
+                        if (ea || eb) {
+                            if (lane == 0) {
+                                raise(ea ? ea : eb, j, ea ? 0 : 1);
+                                fence_cluster();
+                                abort_all(0);
+                            }
+                            bad = true;
+                            break;
+                        }
+                        double pp, qq;
+                        open_params(xs, pp, qq);
+                        if (lane == lq || lane == lq + 1) {
+                            WaveRec w;
+                            w.x0 = xs.x;
+                            w.x1 = xs.y;
+                            w.x2 = pp;
+                            w.x3 = qq;
+                            ringO[2 * j + side] = w;
+                        }
+                        __syncwarp();
+                        if (lane == lq) {
+                            __threadfence_block();
+                            st_vol_i(&s_cnt[0][rank], j);
+                        }
+                        if (have && t > j) apply_open(xs, pp, qq, side ? DOWN : UP, z, s8);
+                    }
+                    if (bad) break;
+                    // catch-up: my own record and the rest of the segment, in order
+                    if (have)
+                        for (int jj = max(t, j0); jj <= j1; ++jj) {
+                            const WaveRec w = ringO[2 * jj + side];
+                            apply_open(C(w.x0, w.x1), w.x2, w.x3, side ? DOWN : UP, z, s8);
+                        }
+                    __syncwarp();
+                } else {
+                    // records of other warps / CTAs: apply them as they appear
+                    const int r = (2 * j) / chunk;
+                    int v = 0;
+                    if (lane == 0) {  // one lane acquires; the warp stays converged
+                        v = wave_wait(&s_cnt[0][r], j, t0);
+                        if (r == rank) __threadfence_block(); else fence_cluster();
+                    }
+                    v = __shfl_sync(FULL, v, 0);
+                    __syncwarp();
+                    if (v & WAVE_ABORT) {
+                        if ((v & WAVE_COUNT) == WAVE_COUNT && lane == 0) {
+                            raise(WE_TIMEOUT, j, 0);
+                            fence_cluster();
+                            abort_all(0);
+                        }
+                        break;
+                    }
+                    const int upto = min(v & WAVE_COUNT, k);
+                    for (; j <= upto; ++j) {
+                        if (2 * j >= wq0 && 2 * j < wq0 + 32 && 2 * j < hi) break;  // mine to build
+                        const WaveRec w = ringO[2 * j + side];
+                        if (have) apply_open(C(w.x0, w.x1), w.x2, w.x3, side ? DOWN : UP, z, s8);
+                    }
+                }
+            }
+        } else {
+            // forwarder: this CTA's records j in [jlo, jhi] -> logs, other CTAs, replay progress
+            const int jlo = max(2, lo / 2), jhi = min(k, (hi - 1) / 2);
+            for (int jf = jlo; jf <= jhi;) {
+                int v = 0;
+                if (lane == 0) {
+                    v = wave_wait(&s_cnt[0][rank], jf, t0);
+                    __threadfence_block();
+                }
+                v = __shfl_sync(FULL, v, 0);
+                __syncwarp();
+                const bool ab = (v & WAVE_ABORT) != 0;
+                if ((v & WAVE_COUNT) == WAVE_COUNT && lane == 0) {
+                    raise(WE_TIMEOUT, jf, 2);
+                    fence_cluster();
+                    abort_all(0);
+                }
+                const int upto = ab ? jf - 1 : min(v & WAVE_COUNT, jhi);
+                for (int jj = jf + lane; jj <= upto; jj += 32) {
+                    const WaveRec wa = ringO[2 * jj], wb = ringO[2 * jj + 1];
+                    log_a[jj] = mk_open_p(C(wa.x0, wa.x1), wa.x2, wa.x3, UP);
+                    log_b[jj] = mk_open_p(C(wb.x0, wb.x1), wb.x2, wb.x3, DOWN);
+                }
+                fence_gpu();  // the logs before the records leave this CTA (replay progress causality)
+                __syncwarp();
+                for (int x = lane; x < CS; x += 32) {
+                    if (x == rank) continue;
+                    WaveRec* rr = cl.map_shared_rank(ringO, x);
+                    for (int jj = jf; jj <= upto; ++jj) {
+                        rr[2 * jj] = ringO[2 * jj];
+                        rr[2 * jj + 1] = ringO[2 * jj + 1];
+                    }
+                    fence_cluster();
+                    st_vol_i(cl.map_shared_rank(&s_cnt[0][rank], x), (ab ? WAVE_ABORT : 0) | upto);
+                }
+                if (prog && lane == 0 && upto >= jf) {
+                    prog_store(prog, upto + 1);
+                    prog_store(prog + 1, upto + 1);
+                }
+                if (ab) break;
+                jf = upto + 1;
+            }
+        }
+        cl.sync();
+        take_error(err, eidx, eaux);
+        if (err) goto fail;
+    }
+    if (timed) tk1 = clock64();
+    if (logger) {
+        na_rec = k + 1;
+        nb_rec = k + 1;
+    }
+    // ---- axis Mobius sending pts[0] to infinity (welding.py:593-600)
+    {
+        int gi[2] = {0, 1};
+        publish(gi, 2, 0.0);
+        PParam* pp = s_param[parity];
+        Rec rr0, rr1;
+#pragma unroll
+        for (int sdx = 0; sdx < 2; ++sdx) {
+            if (err) break;
+            double2 w0 = pp[sdx].z;
+            if (!c_isinf(w0)) {
+                if (c_zero(w0)) {
+                    err = WE_FAR0;
+                    eaux = sdx;
+                } else {
+                    int br = sdx ? DOWN : UP;
+                    Rec& rs = sdx ? rr1 : rr0;
+                    rs = mk_mob(C(1, 0), C(0, 0), cdiv(C(-1.0, 0.0), w0), C(1, 0), true);
+                    mob_pin(rs, w0, cinf(), br);
+                    mob_pin(rs, C(0, 0), C(0, 0), br);
+                    has[sdx] = true;
+                }
+            }
+        }
+        parity ^= 1;
+        if (err) goto fail;
+        if (logger) {
+            if (has[0]) log_a[na_rec++] = rr0;
+            if (has[1]) log_b[nb_rec++] = rr1;
+        }
+        progress(false);
+        if (have && has[side]) apply_rec(side ? rr1 : rr0, z, s8);
+    }
+    // ---- closing loop j = k-1 .. 1 (welding.py:673-687), as a wavefront
+    if (k >= 2) {
+        const int base_a = k + 1 + (has[0] ? 1 : 0), base_b = k + 1 + (has[1] ? 1 : 0);
+        unsigned long long t0 = 0;
+        if (!fwd) {
+            int j = k - 1;
+            while (j >= 1) {
+                const int lp = 2 * j - wq0;
+                if (lp >= 0 && lp < 32 && 2 * j < hi) {
+                    // produce records j .. jbot (descending); lanes whose own index is
+                    // below the record apply it at once (all still on the axis: one
+                    // branch of apply_close), the others catch up afterwards
+                    const int jtop = j;
+                    const int jbot = max(1, wq0 / 2);
+                    bool bad = false;
+                    for (; j >= jbot; --j) {
+                        const int lq = 2 * j - wq0;
+                        const double2 al = C(__shfl_sync(FULL, z.x, lq), __shfl_sync(FULL, z.y, lq));
+                        const double2 be = C(__shfl_sync(FULL, z.x, lq + 1), __shfl_sync(FULL, z.y, lq + 1));
+                        const int sa_ = __shfl_sync(FULL, (int)s8, lq), sb_ = __shfl_sync(FULL, (int)s8, lq + 1);
+                        int e = 0;
+                        if (sa_ == 0 || c_isinf(al) || al.y == 0.0) {
+                            e = WE_ALIGN_A;
+                        } else if (sb_ == 0 || c_isinf(be) || be.y == 0.0) {
+                            e = WE_ALIGN_B;
+                        } else if (!walk_less(al.y, be.y)) {
+                            e = WE_ORDER;
+                        }
+                        if (e) {
+                            if (lane == 0) {
+                                raise(e, j, 0);
+                                fence_cluster();
+                                abort_all(1);
+                            }
+                            bad = true;
+                            break;
+                        }
+                        double cc, dd;
+                        close_params(al.y, be.y, cc, dd);
+                        if (lane == lq) {
+                            WaveRec w;
+                            w.x0 = al.y;
+                            w.x1 = be.y;
+                            w.x2 = cc;
+                            w.x3 = dd;
+                            ringC[j] = w;
+                        }
+                        __syncwarp();
+                        if (lane == lq) {
+                            __threadfence_block();
+                            st_vol_i(&s_cnt[1][rank], k - j);
+                        }
+                        if (have && t < j) apply_close(al.y, be.y, cc, dd, z, s8);
+                    }
+                    if (bad) break;
+                    if (have)
+                        for (int jj = min(t, jtop); jj >= jbot; --jj) {
+                            const WaveRec w = ringC[jj];
+                            apply_close(w.x0, w.x1, w.x2, w.x3, z, s8);
+                        }
+                    __syncwarp();
+                } else {
+                    const int r = (2 * j) / chunk;
+                    int v = 0;
+                    if (lane == 0) {
+                        v = wave_wait(&s_cnt[1][r], k - j, t0);
+                        if (r == rank) __threadfence_block(); else fence_cluster();
+                    }
+                    v = __shfl_sync(FULL, v, 0);
+                    __syncwarp();
+                    if (v & WAVE_ABORT) {
+                        if ((v & WAVE_COUNT) == WAVE_COUNT && lane == 0) {
+                            raise(WE_TIMEOUT, j, 1);
+                            fence_cluster();
+                            abort_all(1);
+                        }
+                        break;
+                    }
+                    const int lowest = max(1, k - (v & WAVE_COUNT));
+                    for (; j >= lowest; --j) {
+                        if (2 * j >= wq0 && 2 * j < wq0 + 32 && 2 * j < hi) break;
+                        const WaveRec w = ringC[j];
+                        if (have) apply_close(w.x0, w.x1, w.x2, w.x3, z, s8);
+                    }
+                }
+            }
+        } else {
+            // forwarder: this CTA's records, high index first
+            const int jtop = min(k - 1, (hi - 1) / 2), jbot = max(1, lo / 2);
+            for (int jf = jtop; jf >= jbot;) {
+                int v = 0;
+                if (lane == 0) {
+                    v = wave_wait(&s_cnt[1][rank], k - jf, t0);
+                    __threadfence_block();
+                }
+                v = __shfl_sync(FULL, v, 0);
+                __syncwarp();
+                const bool ab = (v & WAVE_ABORT) != 0;
+                if ((v & WAVE_COUNT) == WAVE_COUNT && lane == 0) {
+                    raise(WE_TIMEOUT, jf, 3);
+                    fence_cluster();
+                    abort_all(1);
+                }
+                const int lowest = ab ? jf + 1 : max(jbot, k - (v & WAVE_COUNT));
+                for (int jj = jf - lane; jj >= lowest; jj -= 32) {
+                    const WaveRec w = ringC[jj];
+                    const Rec rc = mk_close_p(w.x0, w.x1, w.x2, w.x3);
+                    log_a[base_a + (k - 1 - jj)] = rc;
+                    log_b[base_b + (k - 1 - jj)] = rc;
+                }
+                fence_gpu();
+                __syncwarp();
+                for (int x = lane; x < CS; x += 32) {
+                    if (x == rank) continue;
+                    WaveRec* rr = cl.map_shared_rank(ringC, x);
+                    for (int jj = jf; jj >= lowest; --jj) rr[jj] = ringC[jj];
+                    fence_cluster();
+                    st_vol_i(cl.map_shared_rank(&s_cnt[1][rank], x), (ab ? WAVE_ABORT : 0) | (k - lowest));
+                }
+                if (prog && lane == 0 && lowest <= jf) {
+                    prog_store(prog, base_a + (k - lowest));
+                    prog_store(prog + 1, base_b + (k - lowest));
+                }
+                if (ab) break;
+                jf = lowest - 1;
+            }
+        }
+        cl.sync();
+        take_error(err, eidx, eaux);
+        if (err) goto fail;
+    }
+    if (timed) {
+        tk2 = clock64();
+        A.timing[4 * step + 0] = tk1 - tk0;  // init + SqrtRatio + open loop
+        A.timing[4 * step + 1] = tk2 - tk1;  // axis Mobius + closing loop
+        A.timing[4 * step + 3] = -(k - 1);   // negative: wavefront layout of the split
+    }
+    if (logger) {  // the close records the forwarders logged
+        na_rec += k - 1;
+        nb_rec += k - 1;
+    }
+    // ---- far ends: SquareMobius; stage max of |va| (arc + aux) for the deferred check
+    {
+        double m = 0;
+        if (have && side == 0 && c_fin(z)) m = cabs_(z);
+        m = block_max(m, red);
+        int gi[2] = {0, 1};
+        publish(gi, 2, m);
+        PParam* pp = s_param[parity];
+        double2 qa = pp[0].z, qb = pp[1].z;
+        double stage = 0;
+        for (int r = 0; r < CS; ++r) stage = fmax(stage, s_flag[parity][r]);
+        parity ^= 1;
+        if (logger) {
+            meta[6] = qa.x; meta[7] = qa.y; meta[8] = qb.x; meta[9] = qb.y;
+            meta[10] = stage;
+            meta[14] = na_rec;
+            meta[15] = nb_rec;
+        }
+        ra = mk_sq(c_isinf(qa) ? cinf() : qa);
+        if (logger) {
+            log_a[na_rec++] = ra;
+            log_b[nb_rec++] = ra;
+        }
+        progress(false);
+        if (have) apply_rec(ra, z, s8);
+    }
+    // ---- normalisation (welding.py:699-717)
+    {
+        int gi[4] = {2 * (k + 1), 2 * (k + 1) + 1, 2 * (k + 2), 2 * (k + 2) + 1};
+        publish(gi, 4, 0.0);
+        PParam* pp = s_param[parity];
+        double2 za = pp[0].z, zb = pp[1].z, ia = pp[2].z, ib = pp[3].z;
+        double2 co[4];
+        if (c_isinf(za) || c_isinf(zb) || c_isinf(ia) || c_isinf(ib)) {
+            err = WE_TRACK;
+        } else {
+            double2 zmid = C(0.5 * (ia.x + ib.x), 0.5 * (ia.y + ib.y));
+            if (!c_eq(za, zb) && !c_eq(za, zmid) && !c_eq(zb, zmid)) {
+                double2 zs[3] = {za, zb, zmid}, ws[3] = {C(-1, 0), C(1, 0), cinf()};
+                if (!three_point(zs, ws, co)) err = WE_THREE;
+            } else if (!c_zero(za)) {
+                co[0] = cdiv(C(-1.0, 0.0), za); co[1] = C(0, 0); co[2] = C(0, 0); co[3] = C(1, 0);
+            } else {
+                co[0] = C(1, 0); co[1] = C(0, 0); co[2] = C(0, 0); co[3] = C(1, 0);
+            }
+        }
+        parity ^= 1;
+        if (err) goto fail;
+        ra = mk_mob(co[0], co[1], co[2], co[3]);
+        if (logger) {
+            log_a[na_rec++] = ra;
+            log_b[nb_rec++] = ra;
+        }
+        progress(false);
+        if (have) apply_rec(ra, z, s8);
+    }
+    // ---- closed welding: respread the seam (welding.py:751-763)
+    if (sd.closed) {
+        int n = k + 1;
+        int gi[3] = {0, 2 * (n / 3), 2 * ((2 * n) / 3)};
+        publish(gi, 3, 0.0);
+        PParam* pp = s_param[parity];
+        double2 an[3] = {pp[0].z, pp[1].z, pp[2].z};
+        double2 tg[3] = {C(1.0, 0.0), C(cos(2 * M_PI / 3), sin(2 * M_PI / 3)), C(cos(4 * M_PI / 3), sin(4 * M_PI / 3))};
+        double2 co[4];
+        if (!three_point(an, tg, co)) err = WE_THREE, eidx = 1;
+        parity ^= 1;
+        if (err) goto fail;
+        ra = mk_mob(co[0], co[1], co[2], co[3]);
+        if (logger) {
+            log_a[na_rec++] = ra;
+            log_b[nb_rec++] = ra;
+        }
+        progress(false);
+        s8 = 0;
+        if (have) apply_rec(ra, z, s8);
+    }
+    // ---- outputs: all 2P points to arc_out (side a then side b); rank 0 finishes seam/maxima/area
+    if (have) A.arc_out[sd.arc + side * P + t] = z;
+    if (prog) __threadfence();  // arc_out is read by the streamed replay after the final counter
+    cl.sync();
+    if (rank == 0) {
+        const double2* o = A.arc_out + sd.arc;
+        double seam = 0, ma = 0, mb = 0, mx = 0, area = 0, bad = 0;
+        for (int i = threadIdx.x; i <= k; i += NT) {
+            double2 a = o[i], b = o[P + i];
+            double gg = (c_isinf(a) && c_isinf(b)) ? 0.0 : cabs_(csub(a, b));
+            if (!isnan(gg)) seam = fmax(seam, gg);
+            if (c_fin(a)) ma = fmax(ma, cabs_(a));
+            if (c_fin(b)) mb = fmax(mb, cabs_(b));
+            double2 nx = o[(i + 1) % (k + 1)];
+            area += 0.5 * (a.x * nx.y - a.y * nx.x);
+        }
+        for (int g = threadIdx.x; g < NP; g += NT)
+            if (c_nan(o[g])) bad = 1;
+        for (int i = threadIdx.x; i < 2; i += NT) {
+            double2 a = o[k + 1 + i], b = o[P + k + 1 + i];
+            if (c_fin(a)) mx = fmax(mx, cabs_(a));
+            if (c_fin(b)) mx = fmax(mx, cabs_(b));
+        }
+        seam = block_max(seam, red);
+        ma = block_max(ma, red);
+        mb = block_max(mb, red);
+        mx = block_max(mx, red);
+        area = block_sum(area, red);
+        bad = block_max(bad, red);
+        if (logger) {
             meta[0] = na_rec;
             meta[1] = nb_rec;
             meta[5] = seam;
@@ -1535,6 +2192,9 @@ std::string err_text(int code, int idx, int aux, double a = 0, double b = 0, dou
         case WE_GEO_DISK: return "interior point left the unit disk during the geodesic mapping";
         case WE_GEO_CIRCLE: snprintf(buf, sizeof buf, "boundary point left the unit circle by %.3e", a); return buf;
         case WE_INTERIOR: return "could not locate a point inside the polygon";
+        case WE_TIMEOUT:
+            snprintf(buf, sizeof buf, "internal error: weld wavefront stalled at record %d (loop %d)", idx, aux);
+            return buf;
         default: return "weld failure";
     }
 }
@@ -1550,6 +2210,16 @@ int prep_phase1(int CS, size_t smem) {
     if (CS > 8) PGCP_TRY_CUDA(cudaFuncSetAttribute(k_phase1c<NT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     if (smem > 48 * 1024)
         PGCP_TRY_CUDA(cudaFuncSetAttribute(k_phase1c<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    return PGCP_OK;
+}
+
+constexpr int WAVE_PT = 256;  // point threads per CTA of k_phase1w (+ one forwarder warp)
+
+int prep_phase1w(int CS, size_t smem) {
+    if (CS > 8)
+        PGCP_TRY_CUDA(cudaFuncSetAttribute(k_phase1w<WAVE_PT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    if (smem > 48 * 1024)
+        PGCP_TRY_CUDA(cudaFuncSetAttribute(k_phase1w<WAVE_PT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     return PGCP_OK;
 }
 
@@ -1688,11 +2358,13 @@ int run_schedule(double2* tv, int32_t nsteps, const int32_t* info, const int32_t
         int kmax = 0;
         for (int q = q0; q < q1; ++q) kmax = std::max(kmax, sd[q].k);
         const int NP = 2 * (kmax + 3);
+        // wavefront phase 1 (default) while every point has its own thread
+        const bool wave = env_int("PGCP_WELD_WAVE", 1) != 0 && NP <= PC_MAXCS * WAVE_PT;
         const int ppt = std::max(1, env_int("PGCP_WELD_PPT", 1));
-        const int NT = env_int("PGCP_WELD_NT", 256) >= 512 ? 512 : 256;
-        int CS = std::min(PC_MAXCS, (NP + NT * ppt - 1) / (NT * ppt));
+        const int NT = wave ? WAVE_PT + 32 : (env_int("PGCP_WELD_NT", 256) >= 512 ? 512 : 256);
+        int CS = wave ? (NP + WAVE_PT - 1) / WAVE_PT : std::min(PC_MAXCS, (NP + NT * ppt - 1) / (NT * ppt));
         const int chunk = (NP + CS - 1) / CS;
-        size_t smem = (size_t)chunk * (sizeof(double2) + 1) + 16;
+        size_t smem = wave ? (size_t)96 * (kmax + 1) + 16 : (size_t)chunk * (sizeof(double2) + 1) + 16;
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)((q1 - q0) * CS), 1, 1);
         cfg.blockDim = dim3(NT, 1, 1);
@@ -1705,7 +2377,10 @@ int run_schedule(double2* tv, int32_t nsteps, const int32_t* info, const int32_t
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        if (NT == 512) {
+        if (wave) {
+            PGCP_TRY(prep_phase1w(CS, smem));
+            PGCP_TRY_CUDA(cudaLaunchKernelEx(&cfg, k_phase1w<WAVE_PT>, a));
+        } else if (NT == 512) {
             PGCP_TRY(prep_phase1<512>(CS, smem));
             PGCP_TRY_CUDA(cudaLaunchKernelEx(&cfg, k_phase1c<512>, a));
         } else {
@@ -1760,6 +2435,12 @@ int run_schedule(double2* tv, int32_t nsteps, const int32_t* info, const int32_t
         std::vector<long long> wt(4 * (size_t)nsteps);
         PGCP_TRY_CUDA(cudaMemcpy(wt.data(), d_wtime.p, wt.size() * sizeof(long long), cudaMemcpyDeviceToHost));
         for (int q = 0; q < nsteps; ++q) {
+            if (wt[4 * q + 3] < 0) {  // k_phase1w: [open part, close part] cycles
+                const double n = (double)std::max(1ll, -wt[4 * q + 3]);
+                fprintf(stderr, "[weld timing] step %d k %d level %d (wavefront): open %.0f cycles/record, close %.0f\n",
+                        q, sd[q].k, level[order[q]], wt[4 * q] / n, wt[4 * q + 1] / n);
+                continue;
+            }
             const double n = (double)std::max(1ll, wt[4 * q + 3]);
             fprintf(stderr, "[weld timing] step %d k %d level %d: zip cycles/record publish+barrier %.0f build %.0f "
                     "apply %.0f\n", q, sd[q].k, level[order[q]], wt[4 * q] / n, wt[4 * q + 1] / n, wt[4 * q + 2] / n);

@@ -186,3 +186,38 @@ def test_solver_switches_match_reference(cuda, monkeypatch, env):
         ref = z["coords"]
         assert np.max(np.abs(np.asarray(gp.coords) - ref)) <= 1e-6 * _diam(ref), (case, env)
         assert rep.flips == 0
+
+
+@pytest.mark.parametrize("case", ["qtree4x4", "cfg1", "sphere4", "disk2x2", "tree4x4"])
+def test_wave_weld_equals_barrier_weld(cuda, monkeypatch, case):
+    """The wavefront phase 1 (k_phase1w, default) applies the same records in
+    the same order as the per-record-barrier kernel (PGCP_WELD_WAVE=0): the
+    welded map is bit-identical, and so are the seam residuals."""
+    from paper_1903_12359_b200 import TriMesh, parameterize
+    z = load_golden(case)
+    mesh = TriMesh(z["V"], z["F"])
+    kw = {"pairs": case_pairs(case)} if case_pairs(case) is not None else {}
+    cuts = z["cuts"] if len(z["cuts"]) else None
+    monkeypatch.setenv("PGCP_WELD_WAVE", "0")
+    g0, r0 = parameterize(mesh, cuts, str(z["mode"]), **kw)
+    monkeypatch.setenv("PGCP_WELD_WAVE", "1")
+    g1, r1 = parameterize(mesh, cuts, str(z["mode"]), **kw)
+    assert np.array_equal(np.asarray(g0.coords), np.asarray(g1.coords))
+    assert r0.seam_residuals == r1.seam_residuals
+
+
+def test_wave_weld_errors(cuda, monkeypatch):
+    """Weld failures inside the wavefront loops surface as the same
+    WeldError as with the barrier kernel, on every weld size."""
+    from paper_1903_12359_b200 import WeldError, partial_weld
+    z = load_golden("weld_corpus")
+    a, b, k = unpack(z, "a")[0], unpack(z, "b")[0], int(z["k"][0])
+    bad = a.copy()
+    bad[3] = bad[2]  # two zip points coincide -> the Open chain fails
+    msgs = []
+    for mode in ("0", "1"):
+        monkeypatch.setenv("PGCP_WELD_WAVE", mode)
+        with pytest.raises(WeldError) as ei:
+            partial_weld(bad, b, k)
+        msgs.append(str(ei.value))
+    assert msgs[0] == msgs[1]
