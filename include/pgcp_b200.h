@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define PGCP_ABI_VERSION 1
+#define PGCP_ABI_VERSION 2
 
 /* status codes -> Python exceptions (paper_1903_12359_b200/_native.py) */
 #define PGCP_OK 0
@@ -132,9 +132,16 @@ PGCP_API int pgcp_batch_default_pins(pgcp_batch* b, void* stream);
 typedef struct {
     double rtol;        /* stop when ||r|| <= rtol ||b|| (recurrence residual)   */
     double contract_tol;/* residual contract of flatten.py:170-173 (1e-10)        */
-    int32_t maxit;      /* per-submesh iteration cap                             */
-    int32_t cluster;    /* CTAs per submesh (0 = auto)                           */
+    int32_t maxit;      /* per-submesh iteration cap (PCG)                       */
+    int32_t cluster;    /* CTAs per submesh (0 = auto; PCG)                      */
+    int32_t solver;     /* PGCP_SOLVER_*: 0 = default (direct unless maxit > 0
+                           or PGCP_SOLVER=pcg), 1 = direct, 2 = PCG            */
+    int32_t reserved;
 } pgcp_solve_opts;
+
+#define PGCP_SOLVER_DEFAULT 0
+#define PGCP_SOLVER_DIRECT 1  /* batched multifrontal Cholesky (direct.cu)       */
+#define PGCP_SOLVER_PCG 2     /* batched two-level PCG, one cluster per submesh  */
 
 typedef struct {
     int32_t iters;      /* PCG iterations                                        */

@@ -29,6 +29,13 @@ def _flatten_job(args):
     return dncp_flatten(V, F, loop)
 
 
+def _dirichlet_job(args):
+    """The Dirichlet solve alone (`assemble.py:23-50`) of one submesh:
+    (V, F, loop, boundary values) -> complex embedding."""
+    V, F, loop, g = args
+    return dirichlet_extend(V, F, loop, g)
+
+
 def _harmonic_job(args):
     """`_harmonic_task` (pipeline.py:88-102): harmonic extension, flip check,
     and the quasi-conformal repair of a folded submesh. Returns (z, info)."""

@@ -28,7 +28,11 @@ BATCH_VALIDATE_ONLY = 2
 
 class SolveOpts(ctypes.Structure):
     _fields_ = [("rtol", ctypes.c_double), ("contract_tol", ctypes.c_double),
-                ("maxit", ctypes.c_int32), ("cluster", ctypes.c_int32)]
+                ("maxit", ctypes.c_int32), ("cluster", ctypes.c_int32),
+                ("solver", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
+SOLVERS = {"default": 0, "direct": 1, "pcg": 2}
 
 
 class SolveStat(ctypes.Structure):
@@ -113,7 +117,7 @@ def lib():
                 fn = getattr(L, name)
                 fn.argtypes = args
                 fn.restype = res
-        if L.pgcp_abi_version() != 1:
+        if L.pgcp_abi_version() != 2:
             raise RuntimeError("libpgcp_b200.so ABI version mismatch")
         _lib = L
         return L

@@ -1,0 +1,1562 @@
+// direct.cu -- K3d: batched multifrontal Cholesky of the per-subdomain
+// systems (the DNCP flatten H = L_UU + 2i M_xy, complex Hermitian, and the
+// Dirichlet system L_II, real symmetric), all subdomains of a solve at once.
+//
+// Replaces the two `spsolve` calls of the hot path (flatten.py:167,
+// assemble.py:42) with what SuperLU does on the CPU -- a sparse direct
+// factorization -- laid out for the GPU:
+//
+//   ordering   geometric nested dissection of every subdomain, level by level
+//              over all subdomains: a region is split at the midpoint of the
+//              longest axis of its bounding box; its separator is the set of
+//              near-side vertices with an edge to the far side. Per-vertex
+//              kernels with warp-aggregated atomics, one host sync per level.
+//   symbolic   update sets U(N) = (adj(pivots) u U(children)) beyond N's
+//              pivots, one CTA per front (shared-memory sort + unique),
+//              level by level from the leaves.
+//   numeric    one CTA per front, level by level from the leaves: assemble
+//              the matrix entries of the pivots, extend-add the children's
+//              update blocks, blocked partial Cholesky of the pivot columns
+//              (warp-factored 16x16 diagonal blocks, per-row TRSM, 64x64
+//              tiled updates staged in shared memory), then one tiled
+//              Schur update of the U block that the parent reads in place.
+//   solve      forward (leaves -> roots) and backward (roots -> leaves)
+//              substitution, one CTA per front, deterministic extend-add of
+//              the children's partial sums.
+//
+// Everything is fixed-order (no floating-point atomics): results are bitwise
+// reproducible. The system is the Jacobi-scaled one pcg.cu builds (unit
+// diagonal), so the PCG path's post-processing (true residual, scatter,
+// flatten checks) applies unchanged.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+#include <chrono>
+#include <climits>
+#include <cmath>
+#include <memory>
+#include <cstdlib>
+#include <vector>
+
+#include "direct.cuh"
+
+namespace pgcp {
+
+namespace {
+
+constexpr int DNT = 128;        // threads per CTA of the per-front kernels (4 CTAs per SM)
+constexpr int NB = 16;          // diagonal block of the partial factorization
+constexpr int TR = 32;          // update tiles: TR rows x TC columns, 4x4 outputs per thread
+constexpr int TC = 64;
+constexpr int KC = 16;          // k-chunk staged per update tile
+constexpr int CAND_MAX = 8192;  // symbolic: candidates per front (shared memory)
+constexpr unsigned FULL = 0xffffffffu;
+
+// ---------------------------------------------------------------------------
+// scalar helpers: T = double (real symmetric) or double2 (complex Hermitian)
+
+__device__ __forceinline__ double re(double a) { return a; }
+__device__ __forceinline__ double re(double2 a) { return a.x; }
+template <class T> __device__ __forceinline__ T zero_t();
+template <> __device__ __forceinline__ double zero_t<double>() { return 0.0; }
+template <> __device__ __forceinline__ double2 zero_t<double2>() { return make_double2(0.0, 0.0); }
+template <class T> __device__ __forceinline__ T from_c(double2 v);
+template <> __device__ __forceinline__ double from_c<double>(double2 v) { return v.x; }
+template <> __device__ __forceinline__ double2 from_c<double2>(double2 v) { return v; }
+__device__ __forceinline__ double cj(double a) { return a; }
+__device__ __forceinline__ double2 cj(double2 a) { return make_double2(a.x, -a.y); }
+__device__ __forceinline__ double scale(double a, double s) { return a * s; }
+__device__ __forceinline__ double2 scale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+__device__ __forceinline__ double add(double a, double b) { return a + b; }
+__device__ __forceinline__ double2 add(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double sub(double a, double b) { return a - b; }
+__device__ __forceinline__ double2 sub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+// acc += a * conj(b)
+__device__ __forceinline__ void fma_cj(double& acc, double a, double b) { acc = fma(a, b, acc); }
+__device__ __forceinline__ void fma_cj(double2& acc, double2 a, double2 b) {
+    acc.x = fma(a.x, b.x, fma(a.y, b.y, acc.x));
+    acc.y = fma(a.y, b.x, fma(-a.x, b.y, acc.y));
+}
+// complex vector entry times a matrix entry: v * a, and v * conj(a)
+__device__ __forceinline__ double2 vmul(double a, double2 v) { return make_double2(a * v.x, a * v.y); }
+__device__ __forceinline__ double2 vmul(double2 a, double2 v) {
+    return make_double2(a.x * v.x - a.y * v.y, a.x * v.y + a.y * v.x);
+}
+__device__ __forceinline__ double2 vmul_cj(double a, double2 v) { return make_double2(a * v.x, a * v.y); }
+__device__ __forceinline__ double2 vmul_cj(double2 a, double2 v) {
+    return make_double2(a.x * v.x + a.y * v.y, a.x * v.y - a.y * v.x);
+}
+
+__device__ __forceinline__ int dbsearch(const int64_t* __restrict__ off, int n, int64_t e) {
+    int lo = 0, hi = n - 1;  // largest j with off[j] <= e
+    while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if (off[mid] <= e) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ int lower_bound_i32(const int32_t* a, int n, int32_t x) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (a[mid] < x) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ uint32_t ford(float f) {
+    uint32_t u = __float_as_uint(f);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float funord(uint32_t u) {
+    return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
+}
+
+// warp-aggregated atomics keyed by a node id: every lane of the warp must
+// call (active or not)
+__device__ __forceinline__ void agg_min_max(uint32_t* bb, int key, bool active, uint32_t v, int which) {
+    unsigned act = __ballot_sync(FULL, active);
+    const int lane = threadIdx.x & 31;
+    while (act) {
+        const int leader = __ffs(act) - 1;
+        const int k = __shfl_sync(FULL, key, leader);
+        const bool mine = active && key == k;
+        const unsigned m = __ballot_sync(FULL, mine);
+        if (mine) {
+            const uint32_t lo = __reduce_min_sync(m, v), hi = __reduce_max_sync(m, v);
+            if (lane == leader) {
+                atomicMin(bb + 6 * (int64_t)k + which, lo);
+                atomicMax(bb + 6 * (int64_t)k + 3 + which, hi);
+            }
+        }
+        act &= ~m;
+    }
+}
+__device__ __forceinline__ void agg_count(int32_t* cnt, int key, bool active, int g) {
+    unsigned act = __ballot_sync(FULL, active);
+    const int lane = threadIdx.x & 31;
+    while (act) {
+        const int leader = __ffs(act) - 1;
+        const int k = __shfl_sync(FULL, key, leader);
+        const int gg = __shfl_sync(FULL, g, leader);
+        const bool mine = active && key == k && g == gg;
+        const unsigned m = __ballot_sync(FULL, mine);
+        if (lane == leader) atomicAdd(cnt + 3 * (int64_t)k + gg, __popc(m));
+        act &= ~m;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// unknowns, coordinates, adjacency
+
+__global__ void k_d_urow(int64_t NU, int32_t nslot, const int64_t* __restrict__ uoff,
+                         const int64_t* __restrict__ sl_off, int32_t* __restrict__ urow,
+                         int32_t* __restrict__ uslot) {
+    GRID_STRIDE(u, NU) {
+        const int j = dbsearch(uoff, nslot + 1, u);
+        urow[u] = (int32_t)(32 * sl_off[j] + (u - uoff[j]));
+        uslot[u] = j;
+    }
+}
+
+__global__ void k_d_pos(int64_t NU, const int32_t* __restrict__ urow, const int32_t* __restrict__ uslot,
+                        const int32_t* __restrict__ rowsrc, const int64_t* __restrict__ sv_off,
+                        const int32_t* __restrict__ comps, const int64_t* __restrict__ vert_off,
+                        const int32_t* __restrict__ vmap, const double* __restrict__ V, float4* __restrict__ pos) {
+    GRID_STRIDE(u, NU) {
+        const int j = uslot[u];
+        const int e = rowsrc[urow[u]];
+        const int64_t gid = vert_off[comps[j]] + (e - sv_off[j]);
+        const int64_t pv = vmap[gid];
+        pos[u] = make_float4((float)V[3 * pv], (float)V[3 * pv + 1], (float)V[3 * pv + 2], 0.f);
+    }
+}
+
+struct AdjArgs {
+    const int32_t* urow;
+    const int32_t* uslot;
+    const int64_t* uoff;
+    const int64_t* sl_off;
+    const int64_t* sl_ptr;
+    const int32_t* col;
+    const double* val;
+    const uint32_t* sl_mask;
+    const int2* cpl;
+    const double2* cplc;
+};
+
+__device__ __forceinline__ int64_t sp_pos(int64_t e0, int k, int lane) {
+    return e0 + ((int64_t)(k >> 1) << 6) + (lane << 1) + (k & 1);
+}
+
+// row u's off-diagonal entries: the ELL entries (column != own row) and the
+// coupling partners not already among them; fill=false only counts
+template <bool FILL>
+__device__ __forceinline__ int adj_row(const AdjArgs& a, int64_t u, int32_t* oc, double2* ov) {
+    const int r = a.urow[u];
+    const int j = a.uslot[u];
+    const int64_t rbase = 32 * a.sl_off[j];
+    const int self = (int)(r - rbase);
+    const int64_t s = r >> 5;
+    const int lane = r & 31;
+    const int64_t e0 = a.sl_ptr[s];
+    const int w = (int)((a.sl_ptr[s + 1] - e0) >> 5);
+    int2 cp = make_int2(-1, -1);
+    double2 cc = make_double2(0.0, 0.0);
+    const bool has_c = a.sl_mask && ((a.sl_mask[s] >> lane) & 1u);
+    if (has_c) {
+        cp = a.cpl[r];
+        cc = a.cplc[r];
+    }
+    bool seen_n = false, seen_p = false;
+    int k = 0;
+    for (int q = 0; q < w; ++q) {
+        const int64_t e = sp_pos(e0, q, lane);
+        const int c = a.col[e];
+        if (c == self) continue;
+        if (FILL) {
+            double im = 0.0;
+            if (c == cp.x) im += cc.x;
+            if (c == cp.y) im -= cc.y;
+            oc[k] = (int32_t)(a.uoff[j] + c);
+            ov[k] = make_double2(a.val[e], im);
+        }
+        seen_n |= c == cp.x;
+        seen_p |= c == cp.y;
+        ++k;
+    }
+    if (cp.x >= 0 && !seen_n) {
+        if (FILL) {
+            oc[k] = (int32_t)(a.uoff[j] + cp.x);
+            ov[k] = make_double2(0.0, cp.x == cp.y ? cc.x - cc.y : cc.x);
+        }
+        ++k;
+    }
+    if (cp.y >= 0 && !seen_p && cp.y != cp.x) {
+        if (FILL) {
+            oc[k] = (int32_t)(a.uoff[j] + cp.y);
+            ov[k] = make_double2(0.0, -cc.y);
+        }
+        ++k;
+    }
+    return k;
+}
+
+__global__ void k_d_adj_count(int64_t NU, AdjArgs a, int64_t* __restrict__ cnt) {
+    GRID_STRIDE(u, NU) cnt[u] = adj_row<false>(a, u, nullptr, nullptr);
+}
+__global__ void k_d_adj_fill(int64_t NU, AdjArgs a, const int64_t* __restrict__ ptr, int32_t* __restrict__ oc,
+                             double2* __restrict__ ov) {
+    GRID_STRIDE(u, NU) adj_row<true>(a, u, oc + ptr[u], ov + ptr[u]);
+}
+
+// ---------------------------------------------------------------------------
+// nested dissection
+
+struct NodeArrays {
+    int32_t* parent;
+    int32_t* chA;
+    int32_t* chB;
+    int32_t* cnt;     // unknowns in the region when it was created
+    int32_t* npiv;    // pivots (separator, or all of a leaf)
+    int32_t* slot;
+    int8_t* leaf;
+    uint32_t* bbox;   // [6] ordered floats, min xyz then max xyz
+    int32_t* gcnt;    // [3] near side / far side / separator
+    float2* split;    // (axis, mid)
+    int32_t* nchild;
+};
+
+__global__ void k_nd_roots(int32_t nslot, const int64_t* __restrict__ uoff, int leafmax, NodeArrays nd) {
+    GRID_STRIDE(j, nslot) {
+        const int32_t c = (int32_t)(uoff[j + 1] - uoff[j]);
+        nd.parent[j] = -1;
+        nd.chA[j] = nd.chB[j] = -1;
+        nd.cnt[j] = c;
+        nd.slot[j] = (int32_t)j;
+        nd.leaf[j] = c <= leafmax;
+        nd.npiv[j] = c <= leafmax ? c : 0;
+    }
+}
+
+__global__ void k_nd_init_u(int64_t NU, const int32_t* __restrict__ uslot, const int8_t* __restrict__ leaf,
+                            int32_t* __restrict__ reg, int32_t* __restrict__ node_of) {
+    GRID_STRIDE(u, NU) {
+        const int j = uslot[u];
+        if (leaf[j]) {
+            node_of[u] = j;
+            reg[u] = -1;
+        } else {
+            reg[u] = j;
+            node_of[u] = -1;
+        }
+    }
+}
+
+__global__ void k_nd_reset(int32_t lb, int32_t le, NodeArrays nd) {
+    GRID_STRIDE(i, (int64_t)(le - lb)) {
+        const int64_t N = lb + i;
+        for (int q = 0; q < 3; ++q) {
+            nd.bbox[6 * N + q] = 0xffffffffu;
+            nd.bbox[6 * N + 3 + q] = 0u;
+            nd.gcnt[3 * N + q] = 0;
+        }
+    }
+}
+
+__global__ void k_nd_bbox(int64_t NU, const int32_t* __restrict__ reg, const float4* __restrict__ pos, NodeArrays nd) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < NU; base += stride) {
+        const int64_t u = base + threadIdx.x;
+        const int r = u < NU ? reg[u] : -1;
+        const bool act = r >= 0;
+        const float4 p = act ? pos[u] : make_float4(0.f, 0.f, 0.f, 0.f);
+        agg_min_max(nd.bbox, r, act, ford(p.x), 0);
+        agg_min_max(nd.bbox, r, act, ford(p.y), 1);
+        agg_min_max(nd.bbox, r, act, ford(p.z), 2);
+    }
+}
+
+__global__ void k_nd_split(int32_t lb, int32_t le, NodeArrays nd) {
+    GRID_STRIDE(i, (int64_t)(le - lb)) {
+        const int64_t N = lb + i;
+        if (nd.leaf[N]) continue;
+        float lo[3], hi[3];
+        int ax = 0;
+        float best = -1.f;
+        for (int q = 0; q < 3; ++q) {
+            lo[q] = funord(nd.bbox[6 * N + q]);
+            hi[q] = funord(nd.bbox[6 * N + 3 + q]);
+            if (hi[q] - lo[q] > best) {
+                best = hi[q] - lo[q];
+                ax = q;
+            }
+        }
+        float mid = 0.5f * (lo[ax] + hi[ax]);
+        if (!(mid > lo[ax])) mid = hi[ax];  // ties: the far side is the maximum
+        if (!(best > 0.f)) {                 // all points coincide: a dense leaf
+            nd.leaf[N] = 2;
+            nd.npiv[N] = nd.cnt[N];
+        }
+        nd.split[N] = make_float2((float)ax, mid);
+    }
+}
+
+__global__ void k_nd_side(int64_t NU, const int32_t* __restrict__ reg, const float4* __restrict__ pos, NodeArrays nd,
+                          int8_t* __restrict__ side) {
+    GRID_STRIDE(u, NU) {
+        const int r = reg[u];
+        if (r < 0) continue;
+        const float2 sp = nd.split[r];
+        const float4 p = pos[u];
+        const float c = sp.x == 0.f ? p.x : (sp.x == 1.f ? p.y : p.z);
+        side[u] = c >= sp.y ? 1 : 0;
+    }
+}
+
+__global__ void k_nd_sep(int64_t NU, const int32_t* __restrict__ reg, const int8_t* __restrict__ side,
+                         const int64_t* __restrict__ aptr, const int32_t* __restrict__ acol, NodeArrays nd,
+                         int8_t* __restrict__ grp) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < NU; base += stride) {
+        const int64_t u = base + threadIdx.x;
+        const int r = u < NU ? reg[u] : -1;
+        const bool act = r >= 0 && nd.leaf[r] == 0;
+        int g = 0;
+        if (act) {
+            if (side[u]) {
+                g = 1;
+            } else {
+                for (int64_t q = aptr[u]; q < aptr[u + 1]; ++q) {
+                    const int w = acol[q];
+                    if (reg[w] == r && side[w]) {
+                        g = 2;
+                        break;
+                    }
+                }
+            }
+            grp[u] = (int8_t)g;
+        }
+        agg_count(nd.gcnt, r, act, g);
+    }
+}
+
+__global__ void k_nd_count_children(int32_t lb, int32_t le, NodeArrays nd) {
+    GRID_STRIDE(i, (int64_t)(le - lb)) {
+        const int64_t N = lb + i;
+        int nc = 0;
+        if (!nd.leaf[N]) {
+            const int nA = nd.gcnt[3 * N], nB = nd.gcnt[3 * N + 1], nS = nd.gcnt[3 * N + 2];
+            if (nB == 0 || nA + nS == 0) {  // no split: a dense leaf
+                nd.leaf[N] = 2;
+                nd.npiv[N] = nd.cnt[N];
+            } else {
+                nd.npiv[N] = nS;
+                nc = (nA > 0) + 1;
+            }
+        }
+        nd.nchild[i] = nc;
+    }
+}
+
+__global__ void k_nd_link(int32_t lb, int32_t le, const int32_t* __restrict__ scan, int32_t next, int leafmax,
+                          NodeArrays nd) {
+    GRID_STRIDE(i, (int64_t)(le - lb)) {
+        const int64_t N = lb + i;
+        if (nd.nchild[i] == 0) continue;
+        const int nA = nd.gcnt[3 * N], nB = nd.gcnt[3 * N + 1];
+        int id = next + scan[i];
+        int c[2] = {-1, -1}, n[2] = {nA, nB};
+        if (nA > 0) c[0] = id++;
+        c[1] = id;
+        nd.chA[N] = c[0];
+        nd.chB[N] = c[1];
+        for (int q = 0; q < 2; ++q) {
+            if (c[q] < 0) continue;
+            const int C = c[q];
+            nd.parent[C] = (int32_t)N;
+            nd.chA[C] = nd.chB[C] = -1;
+            nd.cnt[C] = n[q];
+            nd.slot[C] = nd.slot[N];
+            nd.leaf[C] = n[q] <= leafmax;
+            nd.npiv[C] = n[q] <= leafmax ? n[q] : 0;
+        }
+    }
+}
+
+__global__ void k_nd_assign(int64_t NU, int32_t* __restrict__ reg, const int8_t* __restrict__ grp, NodeArrays nd,
+                            int32_t* __restrict__ node_of) {
+    GRID_STRIDE(u, NU) {
+        const int r = reg[u];
+        if (r < 0) continue;
+        if (nd.leaf[r]) {  // dense leaf (no split possible)
+            node_of[u] = r;
+            reg[u] = -1;
+            continue;
+        }
+        const int g = grp[u];
+        if (g == 2) {
+            node_of[u] = r;
+            reg[u] = -1;
+            continue;
+        }
+        const int C = g == 0 ? nd.chA[r] : nd.chB[r];
+        if (nd.leaf[C]) {
+            node_of[u] = C;
+            reg[u] = -1;
+        } else {
+            reg[u] = C;
+        }
+    }
+}
+
+// postorder numbering: subtree sizes bottom-up, then starts top-down
+__global__ void k_nd_subtree(int32_t lb, int32_t le, NodeArrays nd, int64_t* __restrict__ tsz) {
+    GRID_STRIDE(i, (int64_t)(le - lb)) {
+        const int64_t N = lb + i;
+        int64_t t = nd.npiv[N];
+        if (nd.chA[N] >= 0) t += tsz[nd.chA[N]];
+        if (nd.chB[N] >= 0) t += tsz[nd.chB[N]];
+        tsz[N] = t;
+    }
+}
+__global__ void k_nd_start(int32_t lb, int32_t le, NodeArrays nd, const int64_t* __restrict__ tsz,
+                           const int64_t* __restrict__ uoff, int64_t* __restrict__ start, int64_t* __restrict__ pfirst) {
+    GRID_STRIDE(i, (int64_t)(le - lb)) {
+        const int64_t N = lb + i;
+        if (nd.parent[N] < 0) start[N] = uoff[nd.slot[N]];
+        const int64_t s0 = start[N];
+        int64_t off = s0;
+        if (nd.chA[N] >= 0) {
+            start[nd.chA[N]] = off;
+            off += tsz[nd.chA[N]];
+        }
+        if (nd.chB[N] >= 0) start[nd.chB[N]] = off;
+        pfirst[N] = s0 + tsz[N] - nd.npiv[N];
+    }
+}
+__global__ void k_iota(int64_t n, int32_t* __restrict__ v) {
+    GRID_STRIDE(i, n) v[i] = (int32_t)i;
+}
+__global__ void k_nd_elim(int64_t NU, const int32_t* __restrict__ skey, const int32_t* __restrict__ sval,
+                          const int64_t* __restrict__ gstart, const int64_t* __restrict__ pfirst,
+                          int32_t* __restrict__ elim, int32_t* __restrict__ perm) {
+    GRID_STRIDE(i, NU) {
+        const int N = skey[i];
+        const int u = sval[i];
+        const int64_t e = pfirst[N] + (i - gstart[N]);
+        elim[u] = (int32_t)e;
+        perm[e] = u;
+    }
+}
+__global__ void k_nd_npiv64(int32_t n, const int32_t* __restrict__ a, int64_t* __restrict__ b) {
+    GRID_STRIDE(i, (int64_t)n) b[i] = a[i];
+}
+
+// ---------------------------------------------------------------------------
+// symbolic: update sets
+
+struct SymArgs {
+    NodeArrays nd;
+    const int64_t* pfirst;
+    const int32_t* perm;
+    const int32_t* elim;
+    const int64_t* aptr;
+    const int32_t* acol;
+    int32_t* ucnt;
+    int64_t* ustart;
+    int32_t* upool;
+    unsigned long long* bump;
+    int64_t ucap;
+    int32_t* overflow;
+};
+
+__global__ void __launch_bounds__(DNT) k_sym(int32_t lb, SymArgs a) {
+    __shared__ int32_t cand[CAND_MAX];
+    __shared__ int32_t ncand;
+    __shared__ int32_t wsum[DNT / 32 + 1];
+    __shared__ unsigned long long base;
+    const int N = lb + blockIdx.x;
+    const int64_t pf = a.pfirst[N];
+    const int s = a.nd.npiv[N];
+    const int64_t pend = pf + s;
+    if (threadIdx.x == 0) ncand = 0;
+    __syncthreads();
+    for (int k = threadIdx.x; k < s; k += DNT) {
+        const int u = a.perm[pf + k];
+        for (int64_t q = a.aptr[u]; q < a.aptr[u + 1]; ++q) {
+            const int e = a.elim[a.acol[q]];
+            if (e >= pend) {
+                const int i = atomicAdd(&ncand, 1);
+                if (i < CAND_MAX) cand[i] = e;
+            }
+        }
+    }
+    const int ch[2] = {a.nd.chA[N], a.nd.chB[N]};
+    for (int c = 0; c < 2; ++c) {
+        if (ch[c] < 0) continue;
+        const int n = a.ucnt[ch[c]];
+        const int32_t* U = a.upool + a.ustart[ch[c]];
+        for (int t = threadIdx.x; t < n; t += DNT) {
+            const int e = U[t];
+            if (e >= pend) {
+                const int i = atomicAdd(&ncand, 1);
+                if (i < CAND_MAX) cand[i] = e;
+            }
+        }
+    }
+    __syncthreads();
+    const int n = ncand;
+    if (n > CAND_MAX) {
+        if (threadIdx.x == 0) {
+            atomicExch(a.overflow, 1);
+            a.ucnt[N] = 0;
+            a.ustart[N] = 0;
+        }
+        return;
+    }
+    int p2 = 1;
+    while (p2 < n) p2 <<= 1;
+    for (int i = n + threadIdx.x; i < p2; i += DNT) cand[i] = INT_MAX;
+    __syncthreads();
+    // bitonic sort (ascending)
+    for (int k = 2; k <= p2; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < p2; i += DNT) {
+                const int l = i ^ j;
+                if (l > i) {
+                    const int x = cand[i], y = cand[l];
+                    const bool up = (i & k) == 0;
+                    if ((x > y) == up) {
+                        cand[i] = y;
+                        cand[l] = x;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    // unique: contiguous chunks per thread, block scan of the kept counts
+    const int per = (n + DNT - 1) / DNT;
+    const int i0 = min(n, (int)threadIdx.x * per), i1 = min(n, i0 + per);
+    int keep = 0;
+    for (int i = i0; i < i1; ++i) keep += (i == 0 || cand[i] != cand[i - 1]);
+    // inclusive warp scan, then warp offsets
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int inc = keep;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(FULL, inc, o);
+        if (lane >= o) inc += v;
+    }
+    if (lane == 31) wsum[w] = inc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int acc = 0;
+        for (int q = 0; q < DNT / 32; ++q) {
+            const int v = wsum[q];
+            wsum[q] = acc;
+            acc += v;
+        }
+        wsum[DNT / 32] = acc;
+        const unsigned long long b = atomicAdd(a.bump, (unsigned long long)acc);
+        base = b;
+        if ((int64_t)(b + acc) > a.ucap) atomicExch(a.overflow, 1);
+        a.ucnt[N] = acc;
+        a.ustart[N] = (int64_t)b;
+    }
+    __syncthreads();
+    const int total = wsum[DNT / 32];
+    if ((int64_t)(base + total) > a.ucap) return;
+    int o = wsum[w] + inc - keep;
+    int32_t* out = a.upool + base;
+    for (int i = i0; i < i1; ++i)
+        if (i == 0 || cand[i] != cand[i - 1]) out[o++] = cand[i];
+}
+
+__global__ void k_front_sizes(int32_t n, const int32_t* __restrict__ npiv, const int32_t* __restrict__ ucnt,
+                              int32_t* __restrict__ fsz, int64_t* __restrict__ f2, int64_t* __restrict__ f1) {
+    GRID_STRIDE(i, (int64_t)n) {
+        const int64_t f = (int64_t)npiv[i] + ucnt[i];
+        fsz[i] = (int32_t)f;
+        f2[i] = f * f;
+        f1[i] = f;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// numeric factorization
+
+struct FacArgs {
+    NodeArrays nd;
+    const int64_t* pfirst;
+    const int32_t* perm;
+    const int32_t* elim;
+    const int64_t* aptr;
+    const int32_t* acol;
+    const double2* aval;
+    const int32_t* ucnt;
+    const int64_t* ustart;
+    const int32_t* upool;
+    const int32_t* fsz;
+    const int64_t* foff;
+    void* fpool;
+    int32_t* err;  // per slot: nonpositive pivot
+};
+
+// position of elimination index x in front N's row list (pivots, then U)
+__device__ __forceinline__ int front_pos(int64_t x, int64_t pf, int s, const int32_t* U, int nu) {
+    if (x < pf + s) return (int)(x - pf);
+    return s + lower_bound_i32(U, nu, (int32_t)x);
+}
+
+// One TR x TC tile (rows [ti, ti+TR) below rlim, columns [tj, tj+TC) below
+// clim, lower part r >= c only): F[r][c] -= sum_{k in [kb, ke)} F[r][k]
+// conj(F[c][k]), k staged in chunks of KC through shared memory; 4x4
+// outputs per thread.
+template <class T>
+__device__ __forceinline__ void tile_one(T* F, int f, int ti, int tj, int rlim, int clim, int kb, int ke, T* As,
+                                         T* Bs) {
+    const int t = threadIdx.x;
+    const int ty = t >> 4, tx = t & 15;
+    T acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = zero_t<T>();
+    for (int kc = kb; kc < ke; kc += KC) {
+#pragma unroll
+        for (int q = 0; q < (TR * KC) / DNT; ++q) {
+            const int idx = t + q * DNT;
+            const int r = idx % TR, kk = idx / TR;
+            const int k = kc + kk;
+            As[kk * TR + r] = (k < ke && ti + r < rlim) ? F[(int64_t)(ti + r) + (int64_t)k * f] : zero_t<T>();
+        }
+#pragma unroll
+        for (int q = 0; q < (TC * KC) / DNT; ++q) {
+            const int idx = t + q * DNT;
+            const int r = idx % TC, kk = idx / TC;
+            const int k = kc + kk;
+            Bs[kk * TC + r] = (k < ke && tj + r < clim) ? F[(int64_t)(tj + r) + (int64_t)k * f] : zero_t<T>();
+        }
+        __syncthreads();
+#pragma unroll 4
+        for (int kk = 0; kk < KC; ++kk) {
+            T av[4], bv[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) av[i] = As[kk * TR + ty * 4 + i];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) bv[j] = Bs[kk * TC + tx * 4 + j];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) fma_cj(acc[i][j], av[i], bv[j]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int r = ti + ty * 4 + i;
+        if (r >= rlim) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int c = tj + tx * 4 + j;
+            if (c >= clim || r < c) continue;
+            T& dst = F[(int64_t)r + (int64_t)c * f];
+            dst = sub(dst, acc[i][j]);
+        }
+    }
+}
+
+// F[i][j] -= sum_{k in [kb, ke)} F[i][k] conj(F[j][k]) for j in [c0, c1),
+// i in [j, f): every lower tile in turn (one CTA)
+template <class T>
+__device__ void tile_update(T* F, int f, int c0, int c1, int kb, int ke, T* As, T* Bs) {
+    for (int tj = c0; tj < c1; tj += TC)
+        for (int ti = tj; ti < f; ti += TR) tile_one<T>(F, f, ti, tj, f, c1, kb, ke, As, Bs);
+    __syncthreads();
+}
+
+// lower tiles of an n x n block: column tile j (TC wide) has ceil((n - TC j) / TR) row tiles
+__host__ __device__ inline int schur_tiles(int n) {
+    int t = 0;
+    for (int c = 0; c < n; c += TC) t += (n - c + TR - 1) / TR;
+    return t;
+}
+
+template <class T>
+__global__ void __launch_bounds__(DNT, 4) k_factor(int32_t lb, FacArgs a, int schur_inline) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    T* As = reinterpret_cast<T*>(dsm);
+    T* Bs = As + KC * TR;
+    T* Ld = Bs + KC * TC;                                // NB x NB, column-major
+    int32_t* Us = reinterpret_cast<int32_t*>(Ld + NB * NB);  // my U list, then a child's rel map
+    __shared__ int bad;
+    const int N = lb + blockIdx.x;
+    const int s = a.nd.npiv[N];
+    const int nu = a.ucnt[N];
+    const int f = s + nu;
+    const int64_t pf = a.pfirst[N];
+    T* F = reinterpret_cast<T*>(a.fpool) + a.foff[N];
+    int32_t* rel = Us + nu;
+    if (threadIdx.x == 0) bad = 0;
+    for (int i = threadIdx.x; i < nu; i += DNT) Us[i] = a.upool[a.ustart[N] + i];
+    {   // zero the front (16-byte stores)
+        const int64_t nd2 = (int64_t)f * f * (int64_t)(sizeof(T) / 8);
+        double2* z2 = reinterpret_cast<double2*>(F);
+        const bool al = (reinterpret_cast<uintptr_t>(F) & 15) == 0;
+        if (al) {
+            for (int64_t i = threadIdx.x; i < nd2 / 2; i += DNT) z2[i] = make_double2(0.0, 0.0);
+            if ((nd2 & 1) && threadIdx.x == 0) reinterpret_cast<double*>(F)[nd2 - 1] = 0.0;
+        } else {
+            for (int64_t i = threadIdx.x; i < nd2; i += DNT) reinterpret_cast<double*>(F)[i] = 0.0;
+        }
+    }
+    __syncthreads();
+    // matrix entries of my pivot columns (lower part): F[pos(w)][k] = A(w, u) = conj(A(u, w))
+    for (int k = threadIdx.x; k < s; k += DNT) {
+        const int u = a.perm[pf + k];
+        F[(int64_t)k + (int64_t)k * f] = from_c<T>(make_double2(1.0, 0.0));
+        for (int64_t q = a.aptr[u]; q < a.aptr[u + 1]; ++q) {
+            const int64_t e = a.elim[a.acol[q]];
+            if (e <= pf + k) continue;  // eliminated earlier, or the upper part
+            const int i = front_pos(e, pf, s, Us, nu);
+            F[(int64_t)i + (int64_t)k * f] = cj(from_c<T>(a.aval[q]));
+        }
+    }
+    __syncthreads();
+    // extend-add the children's update blocks (fixed order: A, then B; every
+    // entry of one child's block lands on a distinct position)
+    const int ch[2] = {a.nd.chA[N], a.nd.chB[N]};
+    for (int c = 0; c < 2; ++c) {
+        const int C = ch[c];
+        if (C < 0) continue;
+        const int sc = a.nd.npiv[C], uc = a.ucnt[C], fc = sc + uc;
+        const int32_t* UC = a.upool + a.ustart[C];
+        for (int i = threadIdx.x; i < uc; i += DNT) rel[i] = front_pos(UC[i], pf, s, Us, nu);
+        __syncthreads();
+        const T* __restrict__ FC = reinterpret_cast<const T*>(a.fpool) + a.foff[C] + (int64_t)sc * fc + sc;
+        const int tot = uc * uc;
+        for (int t0 = threadIdx.x; t0 < tot; t0 += 4 * DNT) {
+            T v[4];
+            int pos[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int t = t0 + q * DNT;
+                const int bcol = t / max(uc, 1), i = t - bcol * uc;
+                const bool ok = t < tot && i >= bcol;
+                pos[q] = ok ? rel[i] + rel[bcol] * f : -1;
+                v[q] = ok ? FC[(int64_t)bcol * fc + i] : zero_t<T>();
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (pos[q] >= 0) F[pos[q]] = add(F[pos[q]], v[q]);
+        }
+        __syncthreads();
+    }
+    // partial factorization of the pivot columns
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int k0 = 0; k0 < s; k0 += NB) {
+        const int nb = min(NB, s - k0);
+        // diagonal block: one warp, unblocked
+        if (warp == 0) {
+            for (int idx = lane; idx < NB * NB; idx += 32) {
+                const int i = idx % NB, j = idx / NB;
+                Ld[idx] = (i < nb && j < nb && i >= j) ? F[(int64_t)(k0 + i) + (int64_t)(k0 + j) * f] : zero_t<T>();
+            }
+            __syncwarp();
+            for (int k = 0; k < nb; ++k) {
+                double d = re(Ld[k + k * NB]);
+                if (!(d > 0.0) || !isfinite(d)) {
+                    if (lane == 0) bad = 1;
+                    d = 1.0;
+                }
+                d = sqrt(d);
+                __syncwarp();
+                if (lane == 0) Ld[k + k * NB] = from_c<T>(make_double2(d, 0.0));
+                if (lane > k && lane < nb) Ld[lane + k * NB] = scale(Ld[lane + k * NB], 1.0 / d);
+                __syncwarp();
+                // trailing part of the block: column j > k, rows i >= j
+                if (lane > k && lane < nb) {
+                    const T lik = Ld[lane + k * NB];
+                    for (int j = k + 1; j <= lane; ++j) {
+                        T v = Ld[lane + j * NB];
+                        fma_cj(v, scale(lik, -1.0), Ld[j + k * NB]);
+                        Ld[lane + j * NB] = v;
+                    }
+                }
+                __syncwarp();
+            }
+            for (int idx = lane; idx < NB * NB; idx += 32) {
+                const int i = idx % NB, j = idx / NB;
+                if (i < nb && j < nb && i >= j) F[(int64_t)(k0 + i) + (int64_t)(k0 + j) * f] = Ld[idx];
+            }
+        }
+        __syncthreads();
+        // rows below the block: x L^H = row -> forward substitution per row
+        for (int r = k0 + nb + threadIdx.x; r < f; r += DNT) {
+            T x[NB];
+#pragma unroll
+            for (int k = 0; k < NB; ++k) x[k] = k < nb ? F[(int64_t)r + (int64_t)(k0 + k) * f] : zero_t<T>();
+#pragma unroll
+            for (int k = 0; k < NB; ++k) {
+                if (k < nb) {
+                    T v = x[k];
+#pragma unroll
+                    for (int j = 0; j < NB; ++j)
+                        if (j < k) fma_cj(v, scale(x[j], -1.0), Ld[k + j * NB]);
+                    x[k] = scale(v, 1.0 / re(Ld[k + k * NB]));
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < NB; ++k)
+                if (k < nb) F[(int64_t)r + (int64_t)(k0 + k) * f] = x[k];
+        }
+        __syncthreads();
+        // the remaining pivot columns
+        if (k0 + nb < s) tile_update<T>(F, f, k0 + nb, s, k0, k0 + nb, As, Bs);
+    }
+    // Schur complement of the update block (read in place by the parent):
+    // here, or by k_schur's tiles spread over CTAs
+    if (schur_inline && nu > 0 && s > 0) tile_update<T>(F, f, s, f, 0, s, As, Bs);
+    if (threadIdx.x == 0 && bad) atomicExch(a.err + a.nd.slot[N], 1);
+}
+
+// Schur update of the U block of every front of a level, one CTA per lower
+// 64x64 tile (blockIdx.y = tile index within the front)
+template <class T>
+__global__ void __launch_bounds__(DNT, 4) k_schur(int32_t lb, FacArgs a) {
+    __shared__ __align__(16) T As[KC * TR];
+    __shared__ __align__(16) T Bs[KC * TC];
+    const int N = lb + blockIdx.x;
+    const int s = a.nd.npiv[N];
+    const int nu = a.ucnt[N];
+    if (s == 0 || nu == 0) return;
+    int p = blockIdx.y;
+    int tj = 0;
+    for (; tj < nu; tj += TC) {
+        const int nr = (nu - tj + TR - 1) / TR;
+        if (p < nr) break;
+        p -= nr;
+    }
+    if (tj >= nu) return;
+    const int f = s + nu;
+    T* F = reinterpret_cast<T*>(a.fpool) + a.foff[N];
+    tile_one<T>(F, f, s + tj + TR * p, s + tj, f, f, 0, s, As, Bs);
+}
+
+// ---------------------------------------------------------------------------
+// solves
+
+struct SolArgs {
+    NodeArrays nd;
+    const int64_t* pfirst;
+    const int32_t* perm;
+    const int32_t* urow;
+    const int32_t* ucnt;
+    const int64_t* ustart;
+    const int32_t* upool;
+    const int64_t* foff;
+    const int64_t* woff;
+    const void* fpool;
+    double2* W;   // per front partial sums (forward)
+    double2* X;   // elimination order: y after the forward sweep, x after the backward one
+    const double2* b;
+};
+
+constexpr int SB = 32;  // pivots per block of the blocked substitutions
+
+template <class T>
+__global__ void __launch_bounds__(DNT) k_fwd(int32_t lb, SolArgs a) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    __shared__ __align__(16) T Lb[SB * SB];   // diagonal block, column-major
+    double2* w = reinterpret_cast<double2*>(dsm);
+    const int N = lb + blockIdx.x;
+    const int s = a.nd.npiv[N];
+    const int nu = a.ucnt[N];
+    const int f = s + nu;
+    const int64_t pf = a.pfirst[N];
+    int32_t* Us = reinterpret_cast<int32_t*>(w + f);
+    for (int i = threadIdx.x; i < nu; i += DNT) Us[i] = a.upool[a.ustart[N] + i];
+    for (int k = threadIdx.x; k < f; k += DNT)
+        w[k] = k < s ? a.b[a.urow[a.perm[pf + k]]] : make_double2(0.0, 0.0);
+    __syncthreads();
+    const int ch[2] = {a.nd.chA[N], a.nd.chB[N]};
+    for (int c = 0; c < 2; ++c) {
+        const int C = ch[c];
+        if (C < 0) continue;
+        const int sc = a.nd.npiv[C], uc = a.ucnt[C];
+        const int32_t* UC = a.upool + a.ustart[C];
+        const double2* WC = a.W + a.woff[C] + sc;
+        for (int i = threadIdx.x; i < uc; i += DNT) {
+            const int p = front_pos(UC[i], pf, s, Us, nu);
+            const double2 v = WC[i];
+            w[p].x += v.x;
+            w[p].y += v.y;
+        }
+        __syncthreads();
+    }
+    const T* F = reinterpret_cast<const T*>(a.fpool) + a.foff[N];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int k0 = 0; k0 < s; k0 += SB) {
+        const int nb = min(SB, s - k0);
+        for (int idx = threadIdx.x; idx < SB * SB; idx += DNT) {
+            const int i = idx % SB, j = idx / SB;
+            Lb[idx] = (i < nb && j < nb && i >= j) ? F[(int64_t)(k0 + i) + (int64_t)(k0 + j) * f] : zero_t<T>();
+        }
+        __syncthreads();
+        if (warp == 0) {  // lane i holds w[k0 + i]
+            double2 wi = lane < nb ? w[k0 + lane] : make_double2(0.0, 0.0);
+            for (int k = 0; k < nb; ++k) {
+                const double2 wk = make_double2(__shfl_sync(FULL, wi.x, k), __shfl_sync(FULL, wi.y, k));
+                const double d = re(Lb[k + k * SB]);
+                const double2 yk = make_double2(wk.x / d, wk.y / d);
+                if (lane == k) {
+                    wi = yk;
+                } else if (lane > k && lane < nb) {
+                    const double2 t = vmul(Lb[lane + k * SB], yk);
+                    wi.x -= t.x;
+                    wi.y -= t.y;
+                }
+            }
+            if (lane < nb) w[k0 + lane] = wi;
+        }
+        __syncthreads();
+        for (int i = k0 + nb + threadIdx.x; i < f; i += DNT) {
+            double2 acc = w[i];
+            for (int k = 0; k < nb; ++k) {
+                const double2 t = vmul(F[(int64_t)i + (int64_t)(k0 + k) * f], w[k0 + k]);
+                acc.x -= t.x;
+                acc.y -= t.y;
+            }
+            w[i] = acc;
+        }
+        __syncthreads();
+    }
+    double2* WN = a.W + a.woff[N];
+    for (int i = threadIdx.x; i < f; i += DNT) {
+        WN[i] = w[i];
+        if (i < s) a.X[pf + i] = w[i];
+    }
+}
+
+template <class T>
+__global__ void __launch_bounds__(DNT) k_bwd(int32_t lb, SolArgs a) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    __shared__ __align__(16) T Lb[SB * SB];
+    double2* t = reinterpret_cast<double2*>(dsm);   // [s] right-hand sides, then x
+    const int N = lb + blockIdx.x;
+    const int s = a.nd.npiv[N];
+    const int nu = a.ucnt[N];
+    const int f = s + nu;
+    if (s == 0) return;
+    const int64_t pf = a.pfirst[N];
+    double2* xu = t + s;                            // [nu] ancestors' x
+    const int32_t* U = a.upool + a.ustart[N];
+    for (int i = threadIdx.x; i < nu; i += DNT) xu[i] = a.X[U[i]];
+    __syncthreads();
+    const T* F = reinterpret_cast<const T*>(a.fpool) + a.foff[N];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // t_k = y_k - sum_a conj(L[s+a][k]) x_U[a]   (one warp per pivot column)
+    for (int k = warp; k < s; k += DNT / 32) {
+        const T* colk = F + (int64_t)k * f + s;
+        double sx = 0.0, sy = 0.0;
+        for (int q = lane; q < nu; q += 32) {
+            const double2 v = vmul_cj(colk[q], xu[q]);
+            sx += v.x;
+            sy += v.y;
+        }
+        sx = warp_sum(sx);
+        sy = warp_sum(sy);
+        if (lane == 0) {
+            const double2 y = a.X[pf + k];
+            t[k] = make_double2(y.x - sx, y.y - sy);
+        }
+    }
+    __syncthreads();
+    // blocked back substitution with L_PP^H, last block first
+    for (int k1 = s; k1 > 0; k1 -= SB) {
+        const int k0 = max(0, k1 - SB), nb = k1 - k0;
+        for (int idx = threadIdx.x; idx < SB * SB; idx += DNT) {
+            const int i = idx % SB, j = idx / SB;
+            Lb[idx] = (i < nb && j < nb && i >= j) ? F[(int64_t)(k0 + i) + (int64_t)(k0 + j) * f] : zero_t<T>();
+        }
+        __syncthreads();
+        if (warp == 0) {  // lane i holds t[k0 + i]
+            double2 ti = lane < nb ? t[k0 + lane] : make_double2(0.0, 0.0);
+            for (int k = nb - 1; k >= 0; --k) {
+                const double2 tk = make_double2(__shfl_sync(FULL, ti.x, k), __shfl_sync(FULL, ti.y, k));
+                const double d = re(Lb[k + k * SB]);
+                const double2 xk = make_double2(tk.x / d, tk.y / d);
+                if (lane == k) {
+                    ti = xk;
+                } else if (lane < k) {  // t_i -= conj(L[k][i]) x_k
+                    const double2 v = vmul_cj(Lb[k + lane * SB], xk);
+                    ti.x -= v.x;
+                    ti.y -= v.y;
+                }
+            }
+            if (lane < nb) t[k0 + lane] = ti;
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < k0; i += DNT) {
+            double2 acc = t[i];
+            const T* rowi = F + (int64_t)i * f;  // column i of L: entries L[k][i], k in the block
+            for (int k = 0; k < nb; ++k) {
+                const double2 v = vmul_cj(rowi[k0 + k], t[k0 + k]);
+                acc.x -= v.x;
+                acc.y -= v.y;
+            }
+            t[i] = acc;
+        }
+        __syncthreads();
+    }
+    for (int k = threadIdx.x; k < s; k += DNT) a.X[pf + k] = t[k];
+}
+
+__global__ void k_d_scatter(int64_t NU, const int32_t* __restrict__ urow, const int32_t* __restrict__ elim,
+                            const double2* __restrict__ X, double2* __restrict__ x) {
+    GRID_STRIDE(u, NU) x[urow[u]] = X[elim[u]];
+}
+
+int env_int(const char* name, int dflt) {
+    const char* e = getenv(name);
+    return e ? atoi(e) : dflt;
+}
+
+// PGCP_DIRECT_TIMING=1: CUDA-event split of the phases, printed to stderr
+struct PhaseTimer {
+    bool on = false;
+    cudaStream_t s = nullptr;
+    std::vector<std::pair<const char*, cudaEvent_t>> ev;
+    explicit PhaseTimer(cudaStream_t st) : on(getenv("PGCP_DIRECT_TIMING") != nullptr), s(st) { mark("start"); }
+    void mark(const char* name) {
+        if (!on) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, s);
+        ev.push_back({name, e});
+    }
+    ~PhaseTimer() {
+        if (!on) return;
+        cudaEventSynchronize(ev.back().second);
+        fprintf(stderr, "[direct timing]");
+        for (size_t i = 1; i < ev.size(); ++i) {
+            float ms = 0;
+            cudaEventElapsedTime(&ms, ev[i - 1].second, ev[i].second);
+            fprintf(stderr, " %s %.3f", ev[i].first, ms);
+        }
+        fprintf(stderr, " (ms)\n");
+        for (auto& p : ev) cudaEventDestroy(p.second);
+    }
+};
+
+}  // namespace
+
+struct DirectFactor {
+    bool cplx = false;
+    int32_t nslot = 0;
+    int64_t NU = 0, rows = 0;
+    std::vector<int64_t> h_uoff;
+    DevBuf<int64_t> uoff;
+    DevBuf<int32_t> urow, uslot;
+    DevBuf<int64_t> aptr;
+    DevBuf<int32_t> acol;
+    DevBuf<double2> aval;
+    DevBuf<int32_t> elim, perm;
+    // tree
+    int32_t nnodes = 0;
+    std::vector<std::pair<int32_t, int32_t>> levels;  // node id ranges, level 0 = roots
+    DevBuf<int32_t> parent, chA, chB, cnt, npiv, slot, nchild;
+    DevBuf<int8_t> leaf;
+    DevBuf<uint32_t> bbox;
+    DevBuf<int32_t> gcnt;
+    DevBuf<float2> split;
+    DevBuf<int64_t> pfirst;
+    DevBuf<int32_t> ucnt, upool, fsz;
+    DevBuf<int64_t> ustart, foff, woff;
+    DevBuf<unsigned char> fpool;
+    DevBuf<double2> W, X;
+    DevBuf<int32_t> err;
+    std::vector<int> lvl_maxf, lvl_maxu;
+    std::vector<int32_t> h_err;
+    double fmas = 0, factor_ms = 0, solve_ms = 0, front_bytes = 0;
+    int maxf = 0;
+
+    NodeArrays na() {
+        NodeArrays n;
+        n.parent = parent.p;
+        n.chA = chA.p;
+        n.chB = chB.p;
+        n.cnt = cnt.p;
+        n.npiv = npiv.p;
+        n.slot = slot.p;
+        n.leaf = leaf.p;
+        n.bbox = bbox.p;
+        n.gcnt = gcnt.p;
+        n.split = split.p;
+        n.nchild = nchild.p;
+        return n;
+    }
+};
+
+void direct_free(DirectFactor* F) { delete F; }
+
+void direct_stats(const DirectFactor* F, double* o) {
+    for (int i = 0; i < 8; ++i) o[i] = 0;
+    if (!F) return;
+    o[0] = F->nnodes;
+    o[1] = (double)F->levels.size();
+    o[2] = F->maxf;
+    o[3] = F->fmas;
+    o[4] = F->factor_ms;
+    o[5] = F->solve_ms;
+    o[6] = F->front_bytes;
+    o[7] = (double)F->NU;
+}
+
+const std::vector<int32_t>& direct_slot_status(const DirectFactor* F) { return F->h_err; }
+
+namespace {
+
+template <class K>
+int set_smem(K kern, size_t bytes) {
+    PGCP_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    return PGCP_OK;
+}
+
+template <class T>
+int factor_levels(DirectFactor* D, FacArgs& fa, cudaStream_t s, PhaseTimer& pt) {
+    const size_t tsz = sizeof(T);
+    static const char* names[] = {"L0", "L1", "L2", "L3", "L4", "L5", "L6", "L7", "L8", "L9", "L10", "L11",
+                                  "L12", "L13", "L14", "L15", "L16", "L17", "L18", "L19", "L20+"};
+    for (int l = (int)D->levels.size() - 1; l >= 0; --l) {
+        const int lb = D->levels[l].first, le = D->levels[l].second;
+        if (le <= lb) continue;
+        const int maxu_child = (l + 1 < (int)D->levels.size()) ? D->lvl_maxu[l + 1] : 0;
+        const size_t smem = (KC * (TR + TC) + NB * NB) * tsz + (size_t)(D->lvl_maxu[l] + maxu_child) * 4 + 16;
+        if (smem > 227 * 1024) {
+            set_error("direct solver: front update set too large (%d)", D->lvl_maxu[l]);
+            return DIRECT_FALLBACK;
+        }
+        PGCP_TRY(set_smem(k_factor<T>, smem));
+        const int nt = schur_tiles(D->lvl_maxu[l]);
+        const bool inl = nt <= 1;
+        k_factor<T><<<le - lb, DNT, smem, s>>>(lb, fa, inl ? 1 : 0);
+        PGCP_LAUNCH_CHECK();
+        if (!inl) {
+            k_schur<T><<<dim3(le - lb, nt), DNT, 0, s>>>(lb, fa);
+            PGCP_LAUNCH_CHECK();
+        }
+        pt.mark(names[std::min(l, 20)]);
+    }
+    return PGCP_OK;
+}
+
+}  // namespace
+
+int direct_factor(pgcp_batch* b, const DirectInput& in, DirectFactor** out, cudaStream_t s) {
+    *out = nullptr;
+    auto* D = new DirectFactor();
+    std::unique_ptr<DirectFactor> guard(D);
+    D->cplx = in.cplx;
+    D->nslot = in.nslot;
+    const int32_t nslot = in.nslot;
+    D->h_uoff.assign(nslot + 1, 0);
+    for (int j = 0; j < nslot; ++j) D->h_uoff[j + 1] = D->h_uoff[j] + in.h_nu[j];
+    const int64_t NU = D->h_uoff[nslot];
+    D->NU = NU;
+    D->rows = 32 * in.h_sl_off[nslot];
+    const int leafmax = std::max(4, env_int("PGCP_DIRECT_LEAF", 48));
+    cudaEvent_t e0, e1;
+    PGCP_TRY_CUDA(cudaEventCreate(&e0));
+    PGCP_TRY_CUDA(cudaEventCreate(&e1));
+    PGCP_TRY_CUDA(cudaEventRecord(e0, s));
+    PhaseTimer pt(s);
+    PGCP_TRY(D->err.alloc(std::max(nslot, 1), s));
+    PGCP_TRY(D->err.zero(s));
+    D->h_err.assign(nslot, 0);
+    if (NU == 0) {
+        *out = guard.release();
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        return PGCP_OK;
+    }
+    PGCP_TRY(D->uoff.alloc(nslot + 1, s));
+    PGCP_TRY_CUDA(cudaMemcpyAsync(D->uoff.p, D->h_uoff.data(), (nslot + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    PGCP_TRY(D->urow.alloc(NU, s));
+    PGCP_TRY(D->uslot.alloc(NU, s));
+    k_d_urow<<<grid_for(NU, 256), 256, 0, s>>>(NU, nslot, D->uoff.p, in.sl_off, D->urow.p, D->uslot.p);
+    PGCP_LAUNCH_CHECK();
+    DevBuf<float4> pos;
+    PGCP_TRY(pos.alloc(NU, s));
+    k_d_pos<<<grid_for(NU, 256), 256, 0, s>>>(NU, D->urow.p, D->uslot.p, in.rowsrc, in.sv_off, in.comps,
+                                            b->vert_off.p, b->vmap.p, b->V.p, pos.p);
+    PGCP_LAUNCH_CHECK();
+    // adjacency (the system's rows in unknown space)
+    AdjArgs aa;
+    aa.urow = D->urow.p;
+    aa.uslot = D->uslot.p;
+    aa.uoff = D->uoff.p;
+    aa.sl_off = in.sl_off;
+    aa.sl_ptr = in.sl_ptr;
+    aa.col = in.col;
+    aa.val = in.val;
+    aa.sl_mask = in.cplx ? in.sl_mask : nullptr;
+    aa.cpl = in.cpl;
+    aa.cplc = in.cplc;
+    {
+        DevBuf<int64_t> cntb;
+        PGCP_TRY(cntb.alloc(NU, s));
+        k_d_adj_count<<<grid_for(NU, 256), 256, 0, s>>>(NU, aa, cntb.p);
+        PGCP_LAUNCH_CHECK();
+        PGCP_TRY(D->aptr.alloc(NU + 1, s));
+        PGCP_TRY(exclusive_scan_i64(cntb.p, D->aptr.p, NU, s));
+    }
+    int64_t annz = 0;
+    PGCP_TRY(fetch_scalar(D->aptr.p + NU, &annz, s));
+    PGCP_TRY(D->acol.alloc(annz, s));
+    PGCP_TRY(D->aval.alloc(annz, s));
+    k_d_adj_fill<<<grid_for(NU, 256), 256, 0, s>>>(NU, aa, D->aptr.p, D->acol.p, D->aval.p);
+    PGCP_LAUNCH_CHECK();
+    pt.mark("adjacency");
+
+    // ---- nested dissection, level by level
+    const int64_t ncap = NU / 4 + 4 * (int64_t)nslot + 4096;
+    PGCP_TRY(D->parent.alloc(ncap, s));
+    PGCP_TRY(D->chA.alloc(ncap, s));
+    PGCP_TRY(D->chB.alloc(ncap, s));
+    PGCP_TRY(D->cnt.alloc(ncap, s));
+    PGCP_TRY(D->npiv.alloc(ncap, s));
+    PGCP_TRY(D->slot.alloc(ncap, s));
+    PGCP_TRY(D->nchild.alloc(ncap, s));
+    PGCP_TRY(D->leaf.alloc(ncap, s));
+    PGCP_TRY(D->bbox.alloc(6 * ncap, s));
+    PGCP_TRY(D->gcnt.alloc(3 * ncap, s));
+    PGCP_TRY(D->split.alloc(ncap, s));
+    NodeArrays nd = D->na();
+    DevBuf<int32_t> reg, node_of;
+    DevBuf<int8_t> side, grp;
+    PGCP_TRY(reg.alloc(NU, s));
+    PGCP_TRY(node_of.alloc(NU, s));
+    PGCP_TRY(side.alloc(NU, s));
+    PGCP_TRY(grp.alloc(NU, s));
+    k_nd_roots<<<grid_for(nslot, 128), 128, 0, s>>>(nslot, D->uoff.p, leafmax, nd);
+    PGCP_LAUNCH_CHECK();
+    k_nd_init_u<<<grid_for(NU, 256), 256, 0, s>>>(NU, D->uslot.p, D->leaf.p, reg.p, node_of.p);
+    PGCP_LAUNCH_CHECK();
+    DevBuf<int32_t> scan;
+    PGCP_TRY(scan.alloc(ncap + 1, s));
+    DevBuf<unsigned char> cub_tmp;
+    size_t cub_bytes = 0;
+    int32_t lb = 0, le = nslot;
+    D->levels.clear();
+    const int ugrid = grid_for(NU, 256);
+    while (le > lb) {
+        D->levels.push_back({lb, le});
+        if ((int)D->levels.size() > 200) {
+            set_error("direct solver: nested dissection did not terminate");
+            return DIRECT_FALLBACK;
+        }
+        const int64_t nl = le - lb;
+        k_nd_reset<<<grid_for(nl, 256), 256, 0, s>>>(lb, le, nd);
+        PGCP_LAUNCH_CHECK();
+        k_nd_bbox<<<ugrid, 256, 0, s>>>(NU, reg.p, pos.p, nd);
+        PGCP_LAUNCH_CHECK();
+        k_nd_split<<<grid_for(nl, 256), 256, 0, s>>>(lb, le, nd);
+        PGCP_LAUNCH_CHECK();
+        k_nd_side<<<ugrid, 256, 0, s>>>(NU, reg.p, pos.p, nd, side.p);
+        PGCP_LAUNCH_CHECK();
+        k_nd_sep<<<ugrid, 256, 0, s>>>(NU, reg.p, side.p, D->aptr.p, D->acol.p, nd, grp.p);
+        PGCP_LAUNCH_CHECK();
+        k_nd_count_children<<<grid_for(nl, 256), 256, 0, s>>>(lb, le, nd);
+        PGCP_LAUNCH_CHECK();
+        size_t need = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, need, D->nchild.p, scan.p, (int)nl + 1, s);
+        if (need > cub_bytes) {
+            PGCP_TRY(cub_tmp.alloc((int64_t)need, s));
+            cub_bytes = need;
+        }
+        // nchild[nl] is a sentinel 0 so scan[nl] is the level total
+        PGCP_TRY_CUDA(cudaMemsetAsync(D->nchild.p + nl, 0, sizeof(int32_t), s));
+        PGCP_TRY_CUDA(cub::DeviceScan::ExclusiveSum(cub_tmp.p, need, D->nchild.p, scan.p, (int)nl + 1, s));
+        int32_t total = 0;
+        PGCP_TRY(fetch_scalar(scan.p + nl, &total, s));
+        if ((int64_t)le + total > ncap) {
+            set_error("direct solver: nested dissection node capacity exceeded");
+            return DIRECT_FALLBACK;
+        }
+        k_nd_link<<<grid_for(nl, 256), 256, 0, s>>>(lb, le, scan.p, le, leafmax, nd);
+        PGCP_LAUNCH_CHECK();
+        k_nd_assign<<<ugrid, 256, 0, s>>>(NU, reg.p, grp.p, nd, node_of.p);
+        PGCP_LAUNCH_CHECK();
+        lb = le;
+        le = le + total;
+    }
+    D->nnodes = le;
+    const int32_t nn = D->nnodes;
+    pt.mark("nd");
+    // ---- postorder: elimination indices
+    DevBuf<int64_t> tsz, start, npiv64, gstart;
+    PGCP_TRY(tsz.alloc(nn, s));
+    PGCP_TRY(start.alloc(nn, s));
+    PGCP_TRY(D->pfirst.alloc(nn, s));
+    for (int l = (int)D->levels.size() - 1; l >= 0; --l) {
+        const int a0 = D->levels[l].first, a1 = D->levels[l].second;
+        k_nd_subtree<<<grid_for(a1 - a0, 256), 256, 0, s>>>(a0, a1, nd, tsz.p);
+        PGCP_LAUNCH_CHECK();
+    }
+    for (size_t l = 0; l < D->levels.size(); ++l) {
+        const int a0 = D->levels[l].first, a1 = D->levels[l].second;
+        k_nd_start<<<grid_for(a1 - a0, 256), 256, 0, s>>>(a0, a1, nd, tsz.p, D->uoff.p, start.p, D->pfirst.p);
+        PGCP_LAUNCH_CHECK();
+    }
+    PGCP_TRY(npiv64.alloc(nn, s));
+    PGCP_TRY(gstart.alloc(nn + 1, s));
+    k_nd_npiv64<<<grid_for(nn, 256), 256, 0, s>>>(nn, D->npiv.p, npiv64.p);
+    PGCP_LAUNCH_CHECK();
+    PGCP_TRY(exclusive_scan_i64(npiv64.p, gstart.p, nn, s));
+    {
+        DevBuf<int32_t> kin, vin, kout, vout;
+        PGCP_TRY(vin.alloc(NU, s));
+        PGCP_TRY(kout.alloc(NU, s));
+        PGCP_TRY(vout.alloc(NU, s));
+        k_iota<<<grid_for(NU, 256), 256, 0, s>>>(NU, vin.p);
+        PGCP_LAUNCH_CHECK();
+        int bits = 1;
+        while ((1ll << bits) < nn) ++bits;
+        size_t need = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, need, node_of.p, kout.p, vin.p, vout.p, (int)NU, 0, bits, s);
+        DevBuf<unsigned char> tmp;
+        PGCP_TRY(tmp.alloc((int64_t)need, s));
+        PGCP_TRY_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, need, node_of.p, kout.p, vin.p, vout.p, (int)NU, 0, bits, s));
+        PGCP_TRY(D->elim.alloc(NU, s));
+        PGCP_TRY(D->perm.alloc(NU, s));
+        k_nd_elim<<<grid_for(NU, 256), 256, 0, s>>>(NU, kout.p, vout.p, gstart.p, D->pfirst.p, D->elim.p, D->perm.p);
+        PGCP_LAUNCH_CHECK();
+    }
+    pt.mark("postorder");
+    // ---- symbolic: update sets, leaves first
+    PGCP_TRY(D->ucnt.alloc(nn, s));
+    PGCP_TRY(D->ustart.alloc(nn, s));
+    const int64_t ucap = 24 * NU + 65536;
+    PGCP_TRY(D->upool.alloc(ucap, s));
+    DevBuf<unsigned long long> bump;
+    DevBuf<int32_t> ovf;
+    PGCP_TRY(bump.alloc(1, s));
+    PGCP_TRY(bump.zero(s));
+    PGCP_TRY(ovf.alloc(1, s));
+    PGCP_TRY(ovf.zero(s));
+    SymArgs sa;
+    sa.nd = nd;
+    sa.pfirst = D->pfirst.p;
+    sa.perm = D->perm.p;
+    sa.elim = D->elim.p;
+    sa.aptr = D->aptr.p;
+    sa.acol = D->acol.p;
+    sa.ucnt = D->ucnt.p;
+    sa.ustart = D->ustart.p;
+    sa.upool = D->upool.p;
+    sa.bump = bump.p;
+    sa.ucap = ucap;
+    sa.overflow = ovf.p;
+    for (int l = (int)D->levels.size() - 1; l >= 0; --l) {
+        const int a0 = D->levels[l].first, a1 = D->levels[l].second;
+        k_sym<<<a1 - a0, DNT, 0, s>>>(a0, sa);
+        PGCP_LAUNCH_CHECK();
+    }
+    pt.mark("symbolic");
+    int32_t hov = 0;
+    PGCP_TRY(fetch_scalar(ovf.p, &hov, s));
+    if (hov) {
+        set_error("direct solver: symbolic capacity exceeded");
+        return DIRECT_FALLBACK;
+    }
+    // ---- front layout
+    PGCP_TRY(D->fsz.alloc(nn, s));
+    PGCP_TRY(D->foff.alloc(nn + 1, s));
+    PGCP_TRY(D->woff.alloc(nn + 1, s));
+    {
+        DevBuf<int64_t> f2, f1;
+        PGCP_TRY(f2.alloc(nn, s));
+        PGCP_TRY(f1.alloc(nn, s));
+        k_front_sizes<<<grid_for(nn, 256), 256, 0, s>>>(nn, D->npiv.p, D->ucnt.p, D->fsz.p, f2.p, f1.p);
+        PGCP_LAUNCH_CHECK();
+        PGCP_TRY(exclusive_scan_i64(f2.p, D->foff.p, nn, s));
+        PGCP_TRY(exclusive_scan_i64(f1.p, D->woff.p, nn, s));
+    }
+    std::vector<int32_t> hf(nn), hp(nn);
+    int64_t ftot = 0, wtot = 0;
+    PGCP_TRY_CUDA(cudaMemcpyAsync(hf.data(), D->fsz.p, nn * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    PGCP_TRY_CUDA(cudaMemcpyAsync(hp.data(), D->npiv.p, nn * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    PGCP_TRY_CUDA(cudaMemcpyAsync(&ftot, D->foff.p + nn, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    PGCP_TRY_CUDA(cudaMemcpyAsync(&wtot, D->woff.p + nn, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    PGCP_TRY_CUDA(cudaStreamSynchronize(s));
+    D->lvl_maxf.assign(D->levels.size(), 0);
+    D->lvl_maxu.assign(D->levels.size(), 0);
+    D->fmas = 0;
+    D->maxf = 0;
+    const double cmul = D->cplx ? 4.0 : 1.0;
+    for (size_t l = 0; l < D->levels.size(); ++l)
+        for (int N = D->levels[l].first; N < D->levels[l].second; ++N) {
+            const double f = hf[N], sp = hp[N], u = f - sp;
+            D->lvl_maxf[l] = std::max(D->lvl_maxf[l], hf[N]);
+            D->lvl_maxu[l] = std::max(D->lvl_maxu[l], hf[N] - hp[N]);
+            D->maxf = std::max(D->maxf, hf[N]);
+            D->fmas += cmul * (sp * sp * sp / 6.0 + u * sp * sp / 2.0 + u * u * sp / 2.0);
+        }
+    if (pt.on) {
+        for (size_t l = 0; l < D->levels.size(); ++l) {
+            double lf = 0;
+            int maxp = 0;
+            for (int N = D->levels[l].first; N < D->levels[l].second; ++N) {
+                const double f = hf[N], sp = hp[N], u = f - sp;
+                lf += cmul * (sp * sp * sp / 6.0 + u * sp * sp / 2.0 + u * u * sp / 2.0);
+                maxp = std::max(maxp, hp[N]);
+            }
+            fprintf(stderr, "[direct levels] L%zu nodes %d max front %d max pivots %d max update %d FMAs %.3g\n", l,
+                    D->levels[l].second - D->levels[l].first, D->lvl_maxf[l], maxp, D->lvl_maxu[l], lf);
+        }
+    }
+    const size_t tsz_b = D->cplx ? sizeof(double2) : sizeof(double);
+    D->front_bytes = (double)ftot * (double)tsz_b;
+    PGCP_TRY(D->fpool.alloc(ftot * (int64_t)tsz_b, s));  // every front zeroes itself
+    PGCP_TRY(D->W.alloc(wtot, s));
+    PGCP_TRY(D->X.alloc(NU, s));
+    pt.mark("layout");
+    // ---- numeric
+    FacArgs fa;
+    fa.nd = nd;
+    fa.pfirst = D->pfirst.p;
+    fa.perm = D->perm.p;
+    fa.elim = D->elim.p;
+    fa.aptr = D->aptr.p;
+    fa.acol = D->acol.p;
+    fa.aval = D->aval.p;
+    fa.ucnt = D->ucnt.p;
+    fa.ustart = D->ustart.p;
+    fa.upool = D->upool.p;
+    fa.fsz = D->fsz.p;
+    fa.foff = D->foff.p;
+    fa.fpool = D->fpool.p;
+    fa.err = D->err.p;
+    if (D->cplx)
+        PGCP_TRY(factor_levels<double2>(D, fa, s, pt));
+    else
+        PGCP_TRY(factor_levels<double>(D, fa, s, pt));
+    PGCP_TRY_CUDA(cudaEventRecord(e1, s));
+    PGCP_TRY_CUDA(cudaMemcpyAsync(D->h_err.data(), D->err.p, nslot * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    PGCP_TRY_CUDA(cudaStreamSynchronize(s));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    D->factor_ms = ms;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *out = guard.release();
+    return PGCP_OK;
+}
+
+int direct_solve(DirectFactor* D, const double2* b_rows, double2* x_rows, cudaStream_t s) {
+    PGCP_TRY_CUDA(cudaMemsetAsync(x_rows, 0, (size_t)D->rows * sizeof(double2), s));
+    if (D->NU == 0) return PGCP_OK;
+    cudaEvent_t e0, e1;
+    PGCP_TRY_CUDA(cudaEventCreate(&e0));
+    PGCP_TRY_CUDA(cudaEventCreate(&e1));
+    PGCP_TRY_CUDA(cudaEventRecord(e0, s));
+    PhaseTimer pt(s);
+    SolArgs a;
+    a.nd = D->na();
+    a.pfirst = D->pfirst.p;
+    a.perm = D->perm.p;
+    a.urow = D->urow.p;
+    a.ucnt = D->ucnt.p;
+    a.ustart = D->ustart.p;
+    a.upool = D->upool.p;
+    a.foff = D->foff.p;
+    a.woff = D->woff.p;
+    a.fpool = D->fpool.p;
+    a.W = D->W.p;
+    a.X = D->X.p;
+    a.b = b_rows;
+    const int L = (int)D->levels.size();
+    for (int l = L - 1; l >= 0; --l) {
+        const int lb = D->levels[l].first, le = D->levels[l].second;
+        const int maxu_child = (l + 1 < L) ? D->lvl_maxu[l + 1] : 0;
+        const size_t smem = (size_t)D->lvl_maxf[l] * sizeof(double2) + (size_t)(D->lvl_maxu[l] + maxu_child) * 4 + 16;
+        if (D->cplx) {
+            PGCP_TRY(set_smem(k_fwd<double2>, smem));
+            k_fwd<double2><<<le - lb, DNT, smem, s>>>(lb, a);
+        } else {
+            PGCP_TRY(set_smem(k_fwd<double>, smem));
+            k_fwd<double><<<le - lb, DNT, smem, s>>>(lb, a);
+        }
+        PGCP_LAUNCH_CHECK();
+    }
+    pt.mark("forward");
+    for (int l = 0; l < L; ++l) {
+        const int lb = D->levels[l].first, le = D->levels[l].second;
+        const size_t smem = (size_t)D->lvl_maxf[l] * sizeof(double2) + 16;
+        if (D->cplx) {
+            PGCP_TRY(set_smem(k_bwd<double2>, smem));
+            k_bwd<double2><<<le - lb, DNT, smem, s>>>(lb, a);
+        } else {
+            PGCP_TRY(set_smem(k_bwd<double>, smem));
+            k_bwd<double><<<le - lb, DNT, smem, s>>>(lb, a);
+        }
+        PGCP_LAUNCH_CHECK();
+    }
+    pt.mark("backward");
+    k_d_scatter<<<grid_for(D->NU, 256), 256, 0, s>>>(D->NU, D->urow.p, D->elim.p, D->X.p, x_rows);
+    PGCP_LAUNCH_CHECK();
+    PGCP_TRY_CUDA(cudaEventRecord(e1, s));
+    PGCP_TRY_CUDA(cudaEventSynchronize(e1));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    D->solve_ms = ms;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return PGCP_OK;
+}
+
+}  // namespace pgcp

@@ -50,6 +50,7 @@
 #include <mutex>
 
 #include "batch.cuh"
+#include "direct.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -109,6 +110,9 @@ struct SolveSystem {
     // the system on another stream (the harmonic solve after a prepare on a
     // side stream, export_system) makes `home` wait for its work, so the
     // frees of a later rebuild or of pgcp_batch_destroy are ordered after it.
+    // direct solver (direct.cu): multifrontal Cholesky instead of PCG
+    bool use_direct = false;
+    DirectFactor* direct = nullptr;
     cudaStream_t home = nullptr;
     bool has_home = false;
     cudaEvent_t use_ev = nullptr;
@@ -125,6 +129,7 @@ struct SolveSystem {
     }
     ~SolveSystem() {
         if (use_ev) cudaEventDestroy(use_ev);
+        direct_free(direct);
     }
 };
 
@@ -378,6 +383,10 @@ __global__ void k_coupling(int32_t nslot, const int32_t* __restrict__ comps, con
 // Jacobi scaling: the solver iterates on D^{-1/2} H D^{-1/2} (unit diagonal),
 // which is Jacobi-PCG in exact arithmetic and needs no diagonal loads per
 // iteration. x = D^{-1/2} y.
+
+__global__ void k_fill_i32(int32_t* __restrict__ p, int32_t n, int32_t v) {
+    GRID_STRIDE(i, (int64_t)n) p[i] = v;
+}
 
 __global__ void k_dsq(int64_t rows, const double* __restrict__ D, double* __restrict__ Dsq) {
     GRID_STRIDE(r, rows) Dsq[r] = sqrt(D[r]);
@@ -2646,7 +2655,7 @@ int build_system(pgcp_batch* b, SolveSystem* S, bool dncp, const int32_t* d_pins
     PGCP_TRY(S->rowsrc.fill_bytes(0xff, s));
     {
         const char* ev = getenv("PGCP_PCG_COARSE");
-        S->coarse = !S->force_jacobi && !(ev && atoi(ev) == 0);
+        S->coarse = !S->force_jacobi && !S->use_direct && !(ev && atoi(ev) == 0);
         const char* eg = getenv("PGCP_PCG_GMAX");
         S->gmax = eg ? std::max(1, std::min(COARSE_GMAX, atoi(eg))) : COARSE_GMAX;
     }
@@ -2719,8 +2728,41 @@ int build_system(pgcp_batch* b, SolveSystem* S, bool dncp, const int32_t* d_pins
 
 // cluster shape, coarse space (two-level) and the per-shape column encoding:
 // everything of a solve that does not depend on the right-hand side
-int setup_solve(SolveSystem* S, const pgcp_solve_opts* o, cudaStream_t s) {
+int setup_direct(pgcp_batch* b, SolveSystem* S, cudaStream_t s) {
+    DirectInput in;
+    in.nslot = S->nslot;
+    in.comps = S->d_comps.p;
+    in.sv_off = S->sv_off.p;
+    in.sl_off = S->sl_off.p;
+    in.h_sl_off = S->h_sl_off;
+    in.h_nu = S->h_nu;
+    in.rowsrc = S->rowsrc.p;
+    in.sl_ptr = S->sl_ptr.p;
+    in.col = S->col.p;
+    in.val = S->val.p;
+    in.sl_mask = S->sl_mask.p;
+    in.cpl = S->cpl.p;
+    in.cplc = S->cplc.p;
+    in.cplx = S->dncp;
+    DirectFactor* F = nullptr;
+    const int rc = direct_factor(b, in, &F, s);
+    if (rc == DIRECT_FALLBACK) {  // a front outgrew the kernels' bounds: plain PCG on the device
+        S->use_direct = false;
+        return PGCP_OK;
+    }
+    PGCP_TRY(rc);
+    direct_free(S->direct);
+    S->direct = F;
+    S->setup_done = true;
+    return PGCP_OK;
+}
+
+int setup_solve(pgcp_batch* b, SolveSystem* S, const pgcp_solve_opts* o, cudaStream_t s) {
     const int32_t nslot = S->nslot;
+    if (S->use_direct) {
+        PGCP_TRY(setup_direct(b, S, s));
+        if (S->use_direct) return PGCP_OK;
+    }
     int64_t max_sl = 0;
     for (int j = 0; j < nslot; ++j) max_sl = std::max(max_sl, S->h_sl_off[j + 1] - S->h_sl_off[j]);
     int csize = 1, chunk = 1;
@@ -2759,7 +2801,7 @@ int setup_solve(SolveSystem* S, const pgcp_solve_opts* o, cudaStream_t s) {
 int run_solve(pgcp_batch* b, SolveSystem* S, const pgcp_solve_opts* o, double* z, pgcp_solve_stat* st,
               cudaStream_t s) {
     const int32_t nslot = S->nslot;
-    if (!S->setup_done) PGCP_TRY(setup_solve(S, o, s));
+    if (!S->setup_done) PGCP_TRY(setup_solve(b, S, o, s));
     const int csize = S->csize, chunk = S->chunk;
     PGCP_TRY(S->iters.alloc(nslot, s));
     PGCP_TRY(S->res.alloc(8 * (int64_t)nslot, s));
@@ -2860,8 +2902,14 @@ int run_solve(pgcp_batch* b, SolveSystem* S, const pgcp_solve_opts* o, double* z
     PGCP_TRY_CUDA(cudaEventCreate(&e0));
     PGCP_TRY_CUDA(cudaEventCreate(&e1));
     PGCP_TRY_CUDA(cudaEventRecord(e0, s));
-    PGCP_TRY(launch_pcg(S, A, csize, s));
-    count_launch();
+    if (S->use_direct) {
+        PGCP_TRY(direct_solve(S->direct, S->b.p, S->x.p, s));
+        k_fill_i32<<<grid_for(nslot, 128), 128, 0, s>>>(S->iters.p, nslot, 1);
+        PGCP_LAUNCH_CHECK();
+    } else {
+        PGCP_TRY(launch_pcg(S, A, csize, s));
+        count_launch();
+    }
     PGCP_TRY_CUDA(cudaEventRecord(e1, s));
     auto t_post = std::chrono::steady_clock::now();
     if (want_timing) {
@@ -3024,6 +3072,7 @@ int run_solve(pgcp_batch* b, SolveSystem* S, const pgcp_solve_opts* o, double* z
         t.bnorm = hres[8 * j + 4];
         t.status = PGCP_OK;
         bool finite = std::isfinite(t.true_res) && std::isfinite(t.xnorm);
+        if (S->use_direct && S->direct && direct_slot_status(S->direct)[j]) finite = false;  // pivot <= 0
         if (!finite) {
             t.status = PGCP_E_SOLVE;
         } else if (t.relres > rtol && t.iters >= A.maxit) {
@@ -3059,6 +3108,17 @@ int run_solve(pgcp_batch* b, SolveSystem* S, const pgcp_solve_opts* o, double* z
     return worst;
 }
 
+// solver choice: the direct solver unless the caller asks for PCG (explicitly,
+// by an iteration cap, or PGCP_SOLVER=pcg)
+bool want_direct(const pgcp_solve_opts* o) {
+    const int k = o ? o->solver : PGCP_SOLVER_DEFAULT;
+    if (k == PGCP_SOLVER_DIRECT) return true;
+    if (k == PGCP_SOLVER_PCG) return false;
+    if (o && o->maxit > 0) return false;
+    const char* e = getenv("PGCP_SOLVER");
+    return !(e && !strcmp(e, "pcg"));
+}
+
 int prepare_slots(pgcp_batch* b, SolveSystem* S, const int32_t* comps, int32_t ncomp) {
     if (!b->has_laplacian) {
         set_error("laplacian not built");
@@ -3092,6 +3152,7 @@ int solve_flatten(pgcp_batch* b, const int32_t* comps, int32_t ncomp, const int3
     slot = new SolveSystem();
     SolveSystem* S = slot;
     S->built_on(s);
+    S->use_direct = want_direct(o);
     PGCP_TRY(prepare_slots(b, S, comps, ncomp));
     if (S->nslot == 0) return PGCP_OK;
     double2 t[2] = {make_double2(0.0, 0.0), make_double2(1.0, 0.0)};
@@ -3203,6 +3264,7 @@ int prepare_harmonic(pgcp_batch* b, const int32_t* comps, int32_t ncomp, const i
     slot = new SolveSystem();
     SolveSystem* S = slot;
     S->built_on(s);
+    S->use_direct = want_direct(o);
     PGCP_TRY(prepare_slots(b, S, comps, ncomp));
     S->nfixed = nfixed;
     PGCP_TRY(S->fixed_gid_copy.alloc(std::max<int64_t>(nfixed, 1), s));
@@ -3214,7 +3276,7 @@ int prepare_harmonic(pgcp_batch* b, const int32_t* comps, int32_t ncomp, const i
     }
     auto t0 = std::chrono::steady_clock::now();
     PGCP_TRY(build_system(b, S, false, nullptr, nullptr, S->fixed_gid_copy.p, nullptr, nfixed, s));
-    PGCP_TRY(setup_solve(S, o, s));
+    PGCP_TRY(setup_solve(b, S, o, s));
     PGCP_TRY_CUDA(cudaStreamSynchronize(s));
     if (getenv("PGCP_PCG_TIMING"))
         fprintf(stderr, "[pcg timing] harmonic prepare (build + setup) %.2f ms (host, synchronised)\n",
@@ -3469,7 +3531,7 @@ int export_system(pgcp_batch* b, int which, int32_t comp, int64_t* dims, int32_t
 
 
 void solve_summary(const pgcp_batch* b, int which, double* out) {
-    for (int i = 0; i < 10; ++i) out[i] = 0;
+    for (int i = 0; i < 18; ++i) out[i] = 0;
     SolveSystem* S = static_cast<SolveSystem*>(b->sys[which]);
     if (!S) return;
     out[0] = S->kernel_ms;
@@ -3482,6 +3544,21 @@ void solve_summary(const pgcp_batch* b, int which, double* out) {
     out[7] = S->nslot;
     out[8] = S->ref_bytes_weighted;
     out[9] = S->coarse_ms;
+    // direct solver: [10] 1, [11] real FMAs of the factorization, [12] factor
+    // ms, [13] solve ms (forward + backward), [14] largest front, [15] front
+    // storage bytes, [16] tree nodes, [17] tree levels
+    if (S->use_direct && S->direct) {
+        double d[8];
+        direct_stats(S->direct, d);
+        out[10] = 1;
+        out[11] = d[3];
+        out[12] = d[4];
+        out[13] = d[5];
+        out[14] = d[2];
+        out[15] = d[6];
+        out[16] = d[0];
+        out[17] = d[1];
+    }
 }
 
 }  // namespace pgcp

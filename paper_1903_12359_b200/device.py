@@ -162,12 +162,15 @@ class DeviceBatch:
         return self.host(nat.ARR_PINS, torch.int32).reshape(-1, 2)
 
     @staticmethod
-    def _opts(rtol, contract_tol, maxit, cluster):
+    def _opts(rtol, contract_tol, maxit, cluster, solver="default"):
+        """solver: "default" (the multifrontal direct solver unless maxit > 0
+        or PGCP_SOLVER=pcg), "direct" or "pcg"."""
         o = nat.SolveOpts()
         o.rtol = rtol
         o.contract_tol = contract_tol
         o.maxit = maxit
         o.cluster = cluster
+        o.solver = nat.SOLVERS[solver] if isinstance(solver, str) else int(solver)
         return o
 
     def _comps(self, comps):
@@ -177,7 +180,7 @@ class DeviceBatch:
         return arr, len(comps), len(comps)
 
     def flatten(self, comps=None, pins=None, targets=(0j, 1 + 0j), rtol=1e-10, contract_tol=1e-10,
-                maxit=0, cluster=0, out=None):
+                maxit=0, cluster=0, out=None, solver="default"):
         """DNCP flattening of the listed submeshes -> complex tensor over all
         local vertices (sum_n), plus per-submesh solve stats."""
         self.laplacian()
@@ -194,14 +197,14 @@ class DeviceBatch:
         t = (ctypes.c_double * 4)(complex(targets[0]).real, complex(targets[0]).imag,
                                   complex(targets[1]).real, complex(targets[1]).imag)
         stats = (nat.SolveStat * max(nslot, 1))()
-        st = nat.lib().pgcp_batch_flatten(self.h, carr, nc, parr, t, ctypes.byref(self._opts(rtol, contract_tol, maxit, cluster)),
+        st = nat.lib().pgcp_batch_flatten(self.h, carr, nc, parr, t, ctypes.byref(self._opts(rtol, contract_tol, maxit, cluster, solver)),
                                           ptr(z), stats, stream_handle(self.stream))
         self.last_stats = [_stat(s) for s in stats[:nslot]]
         nat.check(st)
         return z, self.last_stats
 
     def harmonic(self, fixed_gid, fixed_val, comps=None, rtol=1e-10, contract_tol=1e-10, maxit=0,
-                 cluster=0, out=None):
+                 cluster=0, out=None, solver="default"):
         self.laplacian()
         carr, nc, nslot = self._comps(comps)
         fg = to_dev(fixed_gid, torch.int32)
@@ -213,14 +216,14 @@ class DeviceBatch:
             return z, []
         stats = (nat.SolveStat * max(nslot, 1))()
         st = nat.lib().pgcp_batch_harmonic(self.h, carr, nc, ptr(fg), ptr(fv), int(fg.numel()),
-                                           ctypes.byref(self._opts(rtol, contract_tol, maxit, cluster)), ptr(z),
+                                           ctypes.byref(self._opts(rtol, contract_tol, maxit, cluster, solver)), ptr(z),
                                            stats, stream_handle(self.stream))
         self.last_stats = [_stat(s) for s in stats[:nslot]]
         nat.check(st)
         return z, self.last_stats
 
     def harmonic_prepare(self, fixed_gid, comps=None, rtol=1e-10, contract_tol=1e-10, maxit=0, cluster=0,
-                         stream=None):
+                         stream=None, solver="default"):
         """First half of `harmonic`: everything that does not depend on the
         fixed values (may run on another stream while those are computed)."""
         self.laplacian()
@@ -231,10 +234,11 @@ class DeviceBatch:
             return
         nat.check(nat.lib().pgcp_batch_harmonic_prepare(
             self.h, carr, nc, ptr(fg), int(fg.numel()),
-            ctypes.byref(self._opts(rtol, contract_tol, maxit, cluster)),
+            ctypes.byref(self._opts(rtol, contract_tol, maxit, cluster, solver)),
             stream_handle(stream if stream is not None else self.stream)))
 
-    def harmonic_solve(self, fixed_val, rtol=1e-10, contract_tol=1e-10, maxit=0, cluster=0, out=None):
+    def harmonic_solve(self, fixed_val, rtol=1e-10, contract_tol=1e-10, maxit=0, cluster=0, out=None,
+                       solver="default"):
         """Second half of `harmonic` (after `harmonic_prepare`)."""
         comps, nslot, nfixed = self._prep
         fv = to_dev(fixed_val, torch.complex128)
@@ -247,7 +251,7 @@ class DeviceBatch:
             return z, []
         stats = (nat.SolveStat * max(nslot, 1))()
         st = nat.lib().pgcp_batch_harmonic_solve(self.h, ptr(fv), nfixed,
-                                                 ctypes.byref(self._opts(rtol, contract_tol, maxit, cluster)),
+                                                 ctypes.byref(self._opts(rtol, contract_tol, maxit, cluster, solver)),
                                                  ptr(z), stats, stream_handle(self.stream))
         self.last_stats = [_stat(s) for s in stats[:nslot]]
         nat.check(st)
@@ -295,11 +299,15 @@ class DeviceBatch:
     def last_solve(self, which):
         """PCG kernel time (CUDA events), iterations and compulsory bytes of
         the last flatten (0) / harmonic (1) solve."""
-        out = (ctypes.c_double * 10)()
-        nat.check(nat.lib().pgcp_batch_last_solve(self.h, which, out, 10))
-        return {"kernel_ms": out[0], "iters_sum": out[1], "iters_max": out[2], "bytes": out[3],
-                "stored_entries": out[4], "rows": out[5], "cluster": int(out[6]), "submeshes": int(out[7]),
-                "ref_bytes": out[8], "coarse_ms": out[9]}
+        out = (ctypes.c_double * 18)()
+        nat.check(nat.lib().pgcp_batch_last_solve(self.h, which, out, 18))
+        r = {"kernel_ms": out[0], "iters_sum": out[1], "iters_max": out[2], "bytes": out[3],
+             "stored_entries": out[4], "rows": out[5], "cluster": int(out[6]), "submeshes": int(out[7]),
+             "ref_bytes": out[8], "coarse_ms": out[9], "solver": "direct" if out[10] else "pcg"}
+        if out[10]:
+            r.update({"fmas": out[11], "factor_ms": out[12], "solve_ms": out[13], "max_front": int(out[14]),
+                      "front_bytes": out[15], "nodes": int(out[16]), "levels": int(out[17])})
+        return r
 
     def energy(self, z):
         out = (ctypes.c_double * self.K)()

@@ -130,6 +130,7 @@ def test_two_level_falls_back_to_jacobi(cuda, monkeypatch):
     """A slot the two-level PCG does not finish within its cap is re-solved
     with Jacobi-PCG on the device; the result still matches the reference."""
     from paper_1903_12359_b200 import TriMesh, parameterize
+    monkeypatch.setenv("PGCP_SOLVER", "pcg")
     monkeypatch.setenv("PGCP_PCG_COARSE_MAXIT", "5")
     z = load_golden("blocks3x3")
     gp, rep = parameterize(TriMesh(z["V"], z["F"]), z["cuts"], str(z["mode"]))
@@ -172,11 +173,12 @@ def test_streamed_replay_failed_step(cuda, monkeypatch):
                                  {"PGCP_PCG_GMAX": "4"}, {"PGCP_PCG_ORDER": "rev"}, {"PGCP_PCG_ORDER": "prev"},
                                  {"PGCP_PCG_X0": "0"}, {"PGCP_OVERLAP_HPREP": "0"}])
 def test_solver_switches_match_reference(cuda, monkeypatch, env):
-    """Every A/B switch of the PCG: plain Jacobi-PCG,
+    """Every A/B switch of the PCG solver (PGCP_SOLVER=pcg): plain Jacobi-PCG,
     fp64 E^-1, 256-thread CTAs, a coarser coarse grid, both launch orders,
     the start from zero, the non-overlapped harmonic preparation -- each
     must still give the reference's UV."""
     from paper_1903_12359_b200 import TriMesh, parameterize
+    monkeypatch.setenv("PGCP_SOLVER", "pcg")
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     for case in ("qtree4x4", "disk2x2"):

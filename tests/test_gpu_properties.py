@@ -74,6 +74,7 @@ def test_coarse_start_same_solution_fewer_iterations(cuda, monkeypatch):
     from paper_1903_12359_b200 import generators as gen
     V, F, cuts = gen.height_field_case(257, 4)
     b = partition_mesh(TriMesh(V, F, check=False), cuts).batch
+    monkeypatch.setenv("PGCP_SOLVER", "pcg")
     out = {}
     for x0 in ("0", "1"):
         monkeypatch.setenv("PGCP_PCG_X0", x0)
