@@ -615,13 +615,29 @@ __global__ void __launch_bounds__(DNT) k_sym(int32_t lb, SymArgs a) {
         if (i == 0 || cand[i] != cand[i - 1]) out[o++] = cand[i];
 }
 
+// front sizes; storage in doubles (complex: 2 per entry; real: padded to
+// an even count so every complex front stays 16-byte aligned)
 __global__ void k_front_sizes(int32_t n, const int32_t* __restrict__ npiv, const int32_t* __restrict__ ucnt,
-                              int32_t* __restrict__ fsz, int64_t* __restrict__ f2, int64_t* __restrict__ f1) {
+                              const int8_t* __restrict__ ntype, int32_t* __restrict__ fsz, int64_t* __restrict__ f2,
+                              int64_t* __restrict__ f1) {
     GRID_STRIDE(i, (int64_t)n) {
         const int64_t f = (int64_t)npiv[i] + ucnt[i];
         fsz[i] = (int32_t)f;
-        f2[i] = f * f;
+        f2[i] = ntype[i] ? 2 * f * f : ((f * f + 1) & ~1ll);
         f1[i] = f;
+    }
+}
+
+// a front is complex when its subtree holds a row with DNCP coupling
+// (imaginary entries); marks walk up from the row's node (idempotent stores)
+__global__ void k_mark_cplx(int64_t NU, const int64_t* __restrict__ aptr, const double2* __restrict__ aval,
+                            const int32_t* __restrict__ node_of, const int32_t* __restrict__ parent,
+                            int8_t* __restrict__ ntype) {
+    GRID_STRIDE(u, NU) {
+        bool c = false;
+        for (int64_t q = aptr[u]; q < aptr[u + 1]; ++q) c |= aval[q].y != 0.0;
+        if (!c) continue;
+        for (int N = node_of[u]; N >= 0; N = parent[N]) ntype[N] = 1;
     }
 }
 
@@ -640,10 +656,24 @@ struct FacArgs {
     const int64_t* ustart;
     const int32_t* upool;
     const int32_t* fsz;
-    const int64_t* foff;
+    const int64_t* foff;     // front offsets in doubles (complex fronts: 16-byte aligned)
     void* fpool;
+    const int8_t* ntype;     // 1: complex front (its subtree holds DNCP coupling entries)
+    const int32_t* list;     // the fronts of one launch (one level, one type)
     int32_t* err;  // per slot: nonpositive pivot
 };
+
+template <class T>
+__device__ __forceinline__ T* front_ptr(void* pool, int64_t off) {
+    return reinterpret_cast<T*>(reinterpret_cast<double*>(pool) + off);
+}
+template <class T>
+__device__ __forceinline__ const T* front_ptr(const void* pool, int64_t off) {
+    return reinterpret_cast<const T*>(reinterpret_cast<const double*>(pool) + off);
+}
+template <class T> __device__ __forceinline__ T narrow(double2 v);
+template <> __device__ __forceinline__ double narrow<double>(double2 v) { return v.x; }
+template <> __device__ __forceinline__ double2 narrow<double2>(double2 v) { return v; }
 
 // position of elimination index x in front N's row list (pivots, then U)
 __device__ __forceinline__ int front_pos(int64_t x, int64_t pf, int s, const int32_t* U, int nu) {
@@ -725,20 +755,63 @@ __host__ __device__ inline int schur_tiles(int n) {
     return t;
 }
 
+__device__ __forceinline__ double shfl_t(double v, int src) { return __shfl_sync(FULL, v, src); }
+__device__ __forceinline__ double2 shfl_t(double2 v, int src) {
+    return make_double2(__shfl_sync(FULL, v.x, src), __shfl_sync(FULL, v.y, src));
+}
+
+// Cholesky of the nb x nb lower block Ld (leading dimension LDB <= 32) by
+// one warp: lane i keeps row i in registers, column k's entries travel by
+// shuffles; a nonpositive pivot sets *bad and continues with 1
+template <class T, int LDB>
+__device__ __forceinline__ void diag_factor(T* Ld, int nb, int* bad) {
+    const int lane = threadIdx.x & 31;
+    T r[LDB];
+#pragma unroll
+    for (int j = 0; j < LDB; ++j) r[j] = (lane < nb && j < nb) ? Ld[lane + j * LDB] : zero_t<T>();
+#pragma unroll
+    for (int k = 0; k < LDB; ++k) {
+        if (k < nb) {
+            double d = re(shfl_t(r[k], k));
+            if (!(d > 0.0) || !isfinite(d)) {
+                if (lane == 0) *bad = 1;
+                d = 1.0;
+            }
+            d = sqrt(d);
+            if (lane == k) r[k] = from_c<T>(make_double2(d, 0.0));
+            else if (lane > k) r[k] = scale(r[k], 1.0 / d);
+#pragma unroll
+            for (int j = k + 1; j < LDB; ++j) {
+                const T ljk = shfl_t(r[k], j);
+                if (lane >= j && j < nb) fma_cj(r[j], scale(r[k], -1.0), ljk);
+            }
+        }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < LDB; ++j)
+        if (lane < nb && j <= lane) Ld[lane + j * LDB] = r[j];
+    __syncwarp();
+}
+
+constexpr int FAC_SCHUR_INLINE = 1;  // k_factor: Schur update of the U block in this CTA
+constexpr int FAC_ASSEMBLE_ONLY = 2; // k_factor: assembly only (the level-synchronous panel follows)
+
+// real fronts: 8 CTAs per SM (64 registers); complex: 4
 template <class T>
-__global__ void __launch_bounds__(DNT, 4) k_factor(int32_t lb, FacArgs a, int schur_inline) {
+__global__ void __launch_bounds__(DNT, sizeof(T) == 8 ? 8 : 4) k_factor(FacArgs a, int mode) {
     extern __shared__ __align__(16) unsigned char dsm[];
     T* As = reinterpret_cast<T*>(dsm);
     T* Bs = As + KC * TR;
     T* Ld = Bs + KC * TC;                                // NB x NB, column-major
     int32_t* Us = reinterpret_cast<int32_t*>(Ld + NB * NB);  // my U list, then a child's rel map
     __shared__ int bad;
-    const int N = lb + blockIdx.x;
+    const int N = a.list[blockIdx.x];
     const int s = a.nd.npiv[N];
     const int nu = a.ucnt[N];
     const int f = s + nu;
     const int64_t pf = a.pfirst[N];
-    T* F = reinterpret_cast<T*>(a.fpool) + a.foff[N];
+    T* F = front_ptr<T>(a.fpool, a.foff[N]);
     int32_t* rel = Us + nu;
     if (threadIdx.x == 0) bad = 0;
     for (int i = threadIdx.x; i < nu; i += DNT) Us[i] = a.upool[a.ustart[N] + i];
@@ -776,10 +849,11 @@ __global__ void __launch_bounds__(DNT, 4) k_factor(int32_t lb, FacArgs a, int sc
         const int32_t* UC = a.upool + a.ustart[C];
         for (int i = threadIdx.x; i < uc; i += DNT) rel[i] = front_pos(UC[i], pf, s, Us, nu);
         __syncthreads();
-        const T* __restrict__ FC = reinterpret_cast<const T*>(a.fpool) + a.foff[C] + (int64_t)sc * fc + sc;
+        const bool ccx = a.ntype[C] != 0;  // a real child may feed a complex front
+        const double* __restrict__ FC = reinterpret_cast<const double*>(a.fpool) + a.foff[C];
         const int tot = uc * uc;
         for (int t0 = threadIdx.x; t0 < tot; t0 += 4 * DNT) {
-            T v[4];
+            double2 v[4];
             int pos[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
@@ -787,14 +861,17 @@ __global__ void __launch_bounds__(DNT, 4) k_factor(int32_t lb, FacArgs a, int sc
                 const int bcol = t / max(uc, 1), i = t - bcol * uc;
                 const bool ok = t < tot && i >= bcol;
                 pos[q] = ok ? rel[i] + rel[bcol] * f : -1;
-                v[q] = ok ? FC[(int64_t)bcol * fc + i] : zero_t<T>();
+                const int64_t e = (int64_t)(sc + bcol) * fc + sc + i;
+                v[q] = !ok ? make_double2(0.0, 0.0)
+                           : (ccx ? reinterpret_cast<const double2*>(FC)[e] : make_double2(FC[e], 0.0));
             }
 #pragma unroll
             for (int q = 0; q < 4; ++q)
-                if (pos[q] >= 0) F[pos[q]] = add(F[pos[q]], v[q]);
+                if (pos[q] >= 0) F[pos[q]] = add(F[pos[q]], narrow<T>(v[q]));
         }
         __syncthreads();
     }
+    if (mode & FAC_ASSEMBLE_ONLY) return;
     // partial factorization of the pivot columns
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int k0 = 0; k0 < s; k0 += NB) {
@@ -806,28 +883,7 @@ __global__ void __launch_bounds__(DNT, 4) k_factor(int32_t lb, FacArgs a, int sc
                 Ld[idx] = (i < nb && j < nb && i >= j) ? F[(int64_t)(k0 + i) + (int64_t)(k0 + j) * f] : zero_t<T>();
             }
             __syncwarp();
-            for (int k = 0; k < nb; ++k) {
-                double d = re(Ld[k + k * NB]);
-                if (!(d > 0.0) || !isfinite(d)) {
-                    if (lane == 0) bad = 1;
-                    d = 1.0;
-                }
-                d = sqrt(d);
-                __syncwarp();
-                if (lane == 0) Ld[k + k * NB] = from_c<T>(make_double2(d, 0.0));
-                if (lane > k && lane < nb) Ld[lane + k * NB] = scale(Ld[lane + k * NB], 1.0 / d);
-                __syncwarp();
-                // trailing part of the block: column j > k, rows i >= j
-                if (lane > k && lane < nb) {
-                    const T lik = Ld[lane + k * NB];
-                    for (int j = k + 1; j <= lane; ++j) {
-                        T v = Ld[lane + j * NB];
-                        fma_cj(v, scale(lik, -1.0), Ld[j + k * NB]);
-                        Ld[lane + j * NB] = v;
-                    }
-                }
-                __syncwarp();
-            }
+            diag_factor<T, NB>(Ld, nb, &bad);
             for (int idx = lane; idx < NB * NB; idx += 32) {
                 const int i = idx % NB, j = idx / NB;
                 if (i < nb && j < nb && i >= j) F[(int64_t)(k0 + i) + (int64_t)(k0 + j) * f] = Ld[idx];
@@ -859,17 +915,194 @@ __global__ void __launch_bounds__(DNT, 4) k_factor(int32_t lb, FacArgs a, int sc
     }
     // Schur complement of the update block (read in place by the parent):
     // here, or by k_schur's tiles spread over CTAs
-    if (schur_inline && nu > 0 && s > 0) tile_update<T>(F, f, s, f, 0, s, As, Bs);
+    if ((mode & FAC_SCHUR_INLINE) && nu > 0 && s > 0) tile_update<T>(F, f, s, f, 0, s, As, Bs);
     if (threadIdx.x == 0 && bad) atomicExch(a.err + a.nd.slot[N], 1);
+}
+
+// Level-synchronous blocked panel for the large fronts of a level: all
+// fronts advance through their pivot columns in blocks of PB together.
+// k_pdiag: the diagonal block (redundantly per CTA, written by row chunk 0)
+// and the TRSM of DNT rows below it per CTA; k_pupd: the update of the
+// remaining pivot columns, one CTA per TR x TC tile.
+constexpr int PB = 32;
+constexpr int FUSED_MAXS = 48;  // levels whose fronts all have <= this many pivots stay fused
+
+// phase 0 (one CTA per front): factor the diagonal block in place;
+// phase 1 (CTAs over row chunks): TRSM of the rows below it
+template <class T>
+__global__ void __launch_bounds__(DNT) k_pdiag(FacArgs a, int k0, int phase) {
+    __shared__ __align__(16) T Ld[PB * PB];
+    __shared__ int bad;
+    const int N = a.list[blockIdx.x];
+    const int s = a.nd.npiv[N];
+    if (k0 >= s) return;
+    const int f = s + a.ucnt[N];
+    const int nb = min(PB, s - k0);
+    const int r0 = k0 + nb + blockIdx.y * DNT;
+    if (blockIdx.y > 0 && r0 >= f) return;
+    T* F = front_ptr<T>(a.fpool, a.foff[N]);
+    if (threadIdx.x == 0) bad = 0;
+    for (int idx = threadIdx.x; idx < PB * PB; idx += DNT) {
+        const int i = idx % PB, j = idx / PB;
+        Ld[idx] = (i < nb && j < nb && i >= j) ? F[(int64_t)(k0 + i) + (int64_t)(k0 + j) * f] : zero_t<T>();
+    }
+    if (phase == 0) {
+        __syncthreads();
+        if (threadIdx.x < 32) diag_factor<T, PB>(Ld, nb, &bad);
+        __syncthreads();
+        for (int idx = threadIdx.x; idx < PB * PB; idx += DNT) {
+            const int i = idx % PB, j = idx / PB;
+            if (i < nb && j < nb && i >= j) F[(int64_t)(k0 + i) + (int64_t)(k0 + j) * f] = Ld[idx];
+        }
+        if (threadIdx.x == 0 && bad) atomicExch(a.err + a.nd.slot[N], 1);
+        return;
+    }
+    __syncthreads();
+    // TRSM of my row in two halves of 16: a dependency chain per half, the
+    // coupling between the halves as independent multiply-adds
+    const int r = r0 + threadIdx.x;
+    if (r < f) {
+        T* row = F + r;
+        T x[16], y[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) x[k] = k < nb ? row[(int64_t)(k0 + k) * f] : zero_t<T>();
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            T v = x[k];
+#pragma unroll
+            for (int j = 0; j < k; ++j) fma_cj(v, scale(x[j], -1.0), Ld[k + j * PB]);
+            x[k] = k < nb ? scale(v, 1.0 / re(Ld[k + k * PB])) : zero_t<T>();
+        }
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+            if (k < nb) row[(int64_t)(k0 + k) * f] = x[k];
+        if (nb > 16) {
+#pragma unroll
+            for (int k = 0; k < 16; ++k) y[k] = 16 + k < nb ? row[(int64_t)(k0 + 16 + k) * f] : zero_t<T>();
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+#pragma unroll
+                for (int k = 0; k < 16; ++k) fma_cj(y[k], scale(x[j], -1.0), Ld[(16 + k) + j * PB]);
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                T v = y[k];
+#pragma unroll
+                for (int j = 0; j < k; ++j) fma_cj(v, scale(y[j], -1.0), Ld[(16 + k) + (16 + j) * PB]);
+                y[k] = 16 + k < nb ? scale(v, 1.0 / re(Ld[(16 + k) + (16 + k) * PB])) : zero_t<T>();
+            }
+#pragma unroll
+            for (int k = 0; k < 16; ++k)
+                if (16 + k < nb) row[(int64_t)(k0 + 16 + k) * f] = y[k];
+        }
+    }
+}
+
+// Multi-CTA assembly of the large fronts of a level. k_asm_cols: CTA y owns
+// columns [y cw, (y+1) cw): zeroes them and writes the matrix entries of the
+// pivots among them. k_asm_child: one child's update block, CTA y adding
+// columns [y cw, (y+1) cw) of it. Launched zero, child A, child B: every
+// position's sum is formed in a fixed order.
+template <class T>
+__global__ void __launch_bounds__(DNT) k_asm_cols(FacArgs a, int cw) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    int32_t* Us = reinterpret_cast<int32_t*>(dsm);
+    const int N = a.list[blockIdx.x];
+    const int s = a.nd.npiv[N];
+    const int nu = a.ucnt[N];
+    const int f = s + nu;
+    const int c0 = blockIdx.y * cw;
+    if (c0 >= f) return;
+    const int c1 = min(f, c0 + cw);
+    const int64_t pf = a.pfirst[N];
+    T* F = front_ptr<T>(a.fpool, a.foff[N]);
+    const int kb = c0, ke = min(c1, s);
+    if (ke > kb)
+        for (int i = threadIdx.x; i < nu; i += DNT) Us[i] = a.upool[a.ustart[N] + i];
+    for (int64_t i = (int64_t)c0 * f + threadIdx.x; i < (int64_t)c1 * f; i += DNT) F[i] = zero_t<T>();
+    __syncthreads();
+    for (int k = kb + threadIdx.x; k < ke; k += DNT) {
+        const int u = a.perm[pf + k];
+        F[(int64_t)k + (int64_t)k * f] = from_c<T>(make_double2(1.0, 0.0));
+        for (int64_t q = a.aptr[u]; q < a.aptr[u + 1]; ++q) {
+            const int64_t e = a.elim[a.acol[q]];
+            if (e <= pf + k) continue;
+            const int i = front_pos(e, pf, s, Us, nu);
+            F[(int64_t)i + (int64_t)k * f] = cj(from_c<T>(a.aval[q]));
+        }
+    }
+}
+
+template <class T>
+__global__ void __launch_bounds__(DNT) k_asm_child(FacArgs a, int which, int cw) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    int32_t* Us = reinterpret_cast<int32_t*>(dsm);
+    const int N = a.list[blockIdx.x];
+    const int C = which ? a.nd.chB[N] : a.nd.chA[N];
+    if (C < 0) return;
+    const int sc = a.nd.npiv[C], uc = a.ucnt[C], fc = sc + uc;
+    const int b0 = blockIdx.y * cw;
+    if (b0 >= uc) return;
+    const int b1 = min(uc, b0 + cw);
+    const int s = a.nd.npiv[N];
+    const int nu = a.ucnt[N];
+    const int f = s + nu;
+    const int64_t pf = a.pfirst[N];
+    int32_t* rel = Us + nu;
+    for (int i = threadIdx.x; i < nu; i += DNT) Us[i] = a.upool[a.ustart[N] + i];
+    __syncthreads();
+    const int32_t* UC = a.upool + a.ustart[C];
+    for (int i = b0 + threadIdx.x; i < uc; i += DNT) rel[i] = front_pos(UC[i], pf, s, Us, nu);
+    __syncthreads();
+    T* F = front_ptr<T>(a.fpool, a.foff[N]);
+    const bool ccx = a.ntype[C] != 0;
+    const double* FC = reinterpret_cast<const double*>(a.fpool) + a.foff[C];
+    for (int b = b0; b < b1; ++b) {
+        const int cb = rel[b];
+        for (int i = b + threadIdx.x; i < uc; i += DNT) {
+            const int64_t e = (int64_t)(sc + b) * fc + sc + i;
+            const double2 v = ccx ? reinterpret_cast<const double2*>(FC)[e] : make_double2(FC[e], 0.0);
+            T& d = F[(int64_t)rel[i] + (int64_t)cb * f];
+            d = add(d, narrow<T>(v));
+        }
+    }
+}
+
+// tiles of the pivot-column update after block k0: columns [c0, s), rows [tj, f)
+__host__ __device__ inline int pupd_tiles(int s, int f, int c0) {
+    int t = 0;
+    for (int tj = c0; tj < s; tj += TC) t += (f - tj + TR - 1) / TR;
+    return t;
+}
+
+template <class T>
+__global__ void __launch_bounds__(DNT, 4) k_pupd(FacArgs a, int k0) {
+    __shared__ __align__(16) T As[KC * TR];
+    __shared__ __align__(16) T Bs[KC * TC];
+    const int N = a.list[blockIdx.x];
+    const int s = a.nd.npiv[N];
+    const int nb = min(PB, s - k0);
+    const int c0 = k0 + nb;
+    if (k0 >= s || c0 >= s) return;
+    const int f = s + a.ucnt[N];
+    int p = blockIdx.y;
+    int tj = c0;
+    for (; tj < s; tj += TC) {
+        const int nr = (f - tj + TR - 1) / TR;
+        if (p < nr) break;
+        p -= nr;
+    }
+    if (tj >= s) return;
+    T* F = front_ptr<T>(a.fpool, a.foff[N]);
+    tile_one<T>(F, f, tj + TR * p, tj, f, s, k0, k0 + nb, As, Bs);
 }
 
 // Schur update of the U block of every front of a level, one CTA per lower
 // 64x64 tile (blockIdx.y = tile index within the front)
 template <class T>
-__global__ void __launch_bounds__(DNT, 4) k_schur(int32_t lb, FacArgs a) {
+__global__ void __launch_bounds__(DNT, sizeof(T) == 8 ? 8 : 4) k_schur(FacArgs a) {
     __shared__ __align__(16) T As[KC * TR];
     __shared__ __align__(16) T Bs[KC * TC];
-    const int N = lb + blockIdx.x;
+    const int N = a.list[blockIdx.x];
     const int s = a.nd.npiv[N];
     const int nu = a.ucnt[N];
     if (s == 0 || nu == 0) return;
@@ -882,7 +1115,7 @@ __global__ void __launch_bounds__(DNT, 4) k_schur(int32_t lb, FacArgs a) {
     }
     if (tj >= nu) return;
     const int f = s + nu;
-    T* F = reinterpret_cast<T*>(a.fpool) + a.foff[N];
+    T* F = front_ptr<T>(a.fpool, a.foff[N]);
     tile_one<T>(F, f, s + tj + TR * p, s + tj, f, f, 0, s, As, Bs);
 }
 
@@ -900,6 +1133,7 @@ struct SolArgs {
     const int64_t* foff;
     const int64_t* woff;
     const void* fpool;
+    const int32_t* list;  // the fronts of one launch (one level, one type)
     double2* W;   // per front partial sums (forward)
     double2* X;   // elimination order: y after the forward sweep, x after the backward one
     const double2* b;
@@ -908,11 +1142,11 @@ struct SolArgs {
 constexpr int SB = 32;  // pivots per block of the blocked substitutions
 
 template <class T>
-__global__ void __launch_bounds__(DNT) k_fwd(int32_t lb, SolArgs a) {
+__global__ void __launch_bounds__(DNT) k_fwd(SolArgs a) {
     extern __shared__ __align__(16) unsigned char dsm[];
     __shared__ __align__(16) T Lb[SB * SB];   // diagonal block, column-major
     double2* w = reinterpret_cast<double2*>(dsm);
-    const int N = lb + blockIdx.x;
+    const int N = a.list[blockIdx.x];
     const int s = a.nd.npiv[N];
     const int nu = a.ucnt[N];
     const int f = s + nu;
@@ -937,7 +1171,7 @@ __global__ void __launch_bounds__(DNT) k_fwd(int32_t lb, SolArgs a) {
         }
         __syncthreads();
     }
-    const T* F = reinterpret_cast<const T*>(a.fpool) + a.foff[N];
+    const T* F = front_ptr<T>(a.fpool, a.foff[N]);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int k0 = 0; k0 < s; k0 += SB) {
         const int nb = min(SB, s - k0);
@@ -982,11 +1216,11 @@ __global__ void __launch_bounds__(DNT) k_fwd(int32_t lb, SolArgs a) {
 }
 
 template <class T>
-__global__ void __launch_bounds__(DNT) k_bwd(int32_t lb, SolArgs a) {
+__global__ void __launch_bounds__(DNT) k_bwd(SolArgs a) {
     extern __shared__ __align__(16) unsigned char dsm[];
     __shared__ __align__(16) T Lb[SB * SB];
     double2* t = reinterpret_cast<double2*>(dsm);   // [s] right-hand sides, then x
-    const int N = lb + blockIdx.x;
+    const int N = a.list[blockIdx.x];
     const int s = a.nd.npiv[N];
     const int nu = a.ucnt[N];
     const int f = s + nu;
@@ -996,7 +1230,7 @@ __global__ void __launch_bounds__(DNT) k_bwd(int32_t lb, SolArgs a) {
     const int32_t* U = a.upool + a.ustart[N];
     for (int i = threadIdx.x; i < nu; i += DNT) xu[i] = a.X[U[i]];
     __syncthreads();
-    const T* F = reinterpret_cast<const T*>(a.fpool) + a.foff[N];
+    const T* F = front_ptr<T>(a.fpool, a.foff[N]);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // t_k = y_k - sum_a conj(L[s+a][k]) x_U[a]   (one warp per pivot column)
     for (int k = warp; k < s; k += DNT / 32) {
@@ -1119,7 +1353,14 @@ struct DirectFactor {
     DevBuf<unsigned char> fpool;
     DevBuf<double2> W, X;
     DevBuf<int32_t> err;
+    DevBuf<int8_t> ntype;
+    // fronts per (level, type): nlist[lst_off[2 l + t], lst_off[2 l + t + 1])
+    DevBuf<int32_t> nlist;
+    std::vector<int64_t> lst_off;
+    std::vector<int> lst_maxs;               // per (level, type): largest pivot count
+    std::vector<int32_t> h_nlist, h_npiv, h_fsz;
     std::vector<int> lvl_maxf, lvl_maxu;
+    int ncplx = 0;
     std::vector<int32_t> h_err;
     double fmas = 0, factor_ms = 0, solve_ms = 0, front_bytes = 0;
     int maxf = 0;
@@ -1167,28 +1408,74 @@ int set_smem(K kern, size_t bytes) {
 }
 
 template <class T>
-int factor_levels(DirectFactor* D, FacArgs& fa, cudaStream_t s, PhaseTimer& pt) {
+int factor_level(DirectFactor* D, FacArgs fa, int l, int type, cudaStream_t s) {
+    const int64_t o0 = D->lst_off[2 * l + type], o1 = D->lst_off[2 * l + type + 1];
+    if (o1 <= o0) return PGCP_OK;
+    const int n = (int)(o1 - o0);
+    fa.list = D->nlist.p + o0;
     const size_t tsz = sizeof(T);
+    const int maxu_child = (l + 1 < (int)D->levels.size()) ? D->lvl_maxu[l + 1] : 0;
+    const size_t smem = (KC * (TR + TC) + NB * NB) * tsz + (size_t)(D->lvl_maxu[l] + maxu_child) * 4 + 16;
+    if (smem > 227 * 1024) {
+        set_error("direct solver: front update set too large (%d)", D->lvl_maxu[l]);
+        return DIRECT_FALLBACK;
+    }
+    PGCP_TRY(set_smem(k_factor<T>, smem));
+    const int nt = schur_tiles(D->lvl_maxu[l]);
+    const int maxs = D->lst_maxs[2 * l + type];
+    if (maxs <= FUSED_MAXS) {
+        const bool inl = nt <= 1;
+        k_factor<T><<<n, DNT, smem, s>>>(fa, inl ? FAC_SCHUR_INLINE : 0);
+        PGCP_LAUNCH_CHECK();
+    } else {
+        {
+            constexpr int CW = 8;
+            const int maxf = D->lvl_maxf[l];
+            const size_t sm1 = (size_t)D->lvl_maxu[l] * 4 + 16;
+            const size_t sm2 = (size_t)(D->lvl_maxu[l] + maxu_child) * 4 + 16;
+            PGCP_TRY(set_smem(k_asm_cols<T>, sm1));
+            PGCP_TRY(set_smem(k_asm_child<T>, sm2));
+            k_asm_cols<T><<<dim3(n, (maxf + CW - 1) / CW), DNT, sm1, s>>>(fa, CW);
+            PGCP_LAUNCH_CHECK();
+            for (int w = 0; w < 2; ++w) {
+                k_asm_child<T><<<dim3(n, (std::max(maxu_child, 1) + CW - 1) / CW), DNT, sm2, s>>>(fa, w, CW);
+                PGCP_LAUNCH_CHECK();
+            }
+        }
+        const size_t xs = 0;
+        for (int k0 = 0; k0 < maxs; k0 += PB) {
+            int chunks = 1, tiles = 0;
+            for (int64_t q = o0; q < o1; ++q) {
+                const int N = D->h_nlist[q];
+                const int sp = D->h_npiv[N], f = D->h_fsz[N];
+                if (k0 >= sp) continue;
+                const int nb = std::min(PB, sp - k0);
+                chunks = std::max(chunks, (f - k0 - nb + DNT - 1) / DNT);
+                tiles = std::max(tiles, pupd_tiles(sp, f, k0 + nb));
+            }
+            k_pdiag<T><<<dim3(n, 1), DNT, xs, s>>>(fa, k0, 0);
+            PGCP_LAUNCH_CHECK();
+            k_pdiag<T><<<dim3(n, chunks), DNT, xs, s>>>(fa, k0, 1);
+            PGCP_LAUNCH_CHECK();
+            if (tiles > 0) {
+                k_pupd<T><<<dim3(n, tiles), DNT, 0, s>>>(fa, k0);
+                PGCP_LAUNCH_CHECK();
+            }
+        }
+    }
+    if (nt > 1 || (maxs > FUSED_MAXS && nt > 0)) {
+        k_schur<T><<<dim3(n, nt), DNT, 0, s>>>(fa);
+        PGCP_LAUNCH_CHECK();
+    }
+    return PGCP_OK;
+}
+
+int factor_levels(DirectFactor* D, FacArgs& fa, cudaStream_t s, PhaseTimer& pt) {
     static const char* names[] = {"L0", "L1", "L2", "L3", "L4", "L5", "L6", "L7", "L8", "L9", "L10", "L11",
                                   "L12", "L13", "L14", "L15", "L16", "L17", "L18", "L19", "L20+"};
     for (int l = (int)D->levels.size() - 1; l >= 0; --l) {
-        const int lb = D->levels[l].first, le = D->levels[l].second;
-        if (le <= lb) continue;
-        const int maxu_child = (l + 1 < (int)D->levels.size()) ? D->lvl_maxu[l + 1] : 0;
-        const size_t smem = (KC * (TR + TC) + NB * NB) * tsz + (size_t)(D->lvl_maxu[l] + maxu_child) * 4 + 16;
-        if (smem > 227 * 1024) {
-            set_error("direct solver: front update set too large (%d)", D->lvl_maxu[l]);
-            return DIRECT_FALLBACK;
-        }
-        PGCP_TRY(set_smem(k_factor<T>, smem));
-        const int nt = schur_tiles(D->lvl_maxu[l]);
-        const bool inl = nt <= 1;
-        k_factor<T><<<le - lb, DNT, smem, s>>>(lb, fa, inl ? 1 : 0);
-        PGCP_LAUNCH_CHECK();
-        if (!inl) {
-            k_schur<T><<<dim3(le - lb, nt), DNT, 0, s>>>(lb, fa);
-            PGCP_LAUNCH_CHECK();
-        }
+        PGCP_TRY(factor_level<double>(D, fa, l, 0, s));
+        PGCP_TRY(factor_level<double2>(D, fa, l, 1, s));
         pt.mark(names[std::min(l, 20)]);
     }
     return PGCP_OK;
@@ -1413,6 +1700,13 @@ int direct_factor(pgcp_batch* b, const DirectInput& in, DirectFactor** out, cuda
         set_error("direct solver: symbolic capacity exceeded");
         return DIRECT_FALLBACK;
     }
+    // ---- front types: complex where the subtree holds coupling entries
+    PGCP_TRY(D->ntype.alloc(nn, s));
+    PGCP_TRY(D->ntype.zero(s));
+    if (D->cplx) {
+        k_mark_cplx<<<grid_for(NU, 256), 256, 0, s>>>(NU, D->aptr.p, D->aval.p, node_of.p, D->parent.p, D->ntype.p);
+        PGCP_LAUNCH_CHECK();
+    }
     // ---- front layout
     PGCP_TRY(D->fsz.alloc(nn, s));
     PGCP_TRY(D->foff.alloc(nn + 1, s));
@@ -1421,13 +1715,15 @@ int direct_factor(pgcp_batch* b, const DirectInput& in, DirectFactor** out, cuda
         DevBuf<int64_t> f2, f1;
         PGCP_TRY(f2.alloc(nn, s));
         PGCP_TRY(f1.alloc(nn, s));
-        k_front_sizes<<<grid_for(nn, 256), 256, 0, s>>>(nn, D->npiv.p, D->ucnt.p, D->fsz.p, f2.p, f1.p);
+        k_front_sizes<<<grid_for(nn, 256), 256, 0, s>>>(nn, D->npiv.p, D->ucnt.p, D->ntype.p, D->fsz.p, f2.p, f1.p);
         PGCP_LAUNCH_CHECK();
         PGCP_TRY(exclusive_scan_i64(f2.p, D->foff.p, nn, s));
         PGCP_TRY(exclusive_scan_i64(f1.p, D->woff.p, nn, s));
     }
     std::vector<int32_t> hf(nn), hp(nn);
+    std::vector<int8_t> ht(nn);
     int64_t ftot = 0, wtot = 0;
+    PGCP_TRY_CUDA(cudaMemcpyAsync(ht.data(), D->ntype.p, nn * sizeof(int8_t), cudaMemcpyDeviceToHost, s));
     PGCP_TRY_CUDA(cudaMemcpyAsync(hf.data(), D->fsz.p, nn * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     PGCP_TRY_CUDA(cudaMemcpyAsync(hp.data(), D->npiv.p, nn * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     PGCP_TRY_CUDA(cudaMemcpyAsync(&ftot, D->foff.p + nn, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
@@ -1437,33 +1733,56 @@ int direct_factor(pgcp_batch* b, const DirectInput& in, DirectFactor** out, cuda
     D->lvl_maxu.assign(D->levels.size(), 0);
     D->fmas = 0;
     D->maxf = 0;
-    const double cmul = D->cplx ? 4.0 : 1.0;
-    for (size_t l = 0; l < D->levels.size(); ++l)
+    D->ncplx = 0;
+    std::vector<int32_t> hl;
+    hl.reserve(nn);
+    D->lst_off.assign(2 * D->levels.size() + 1, 0);
+    for (size_t l = 0; l < D->levels.size(); ++l) {
+        for (int t = 0; t < 2; ++t) {
+            D->lst_off[2 * l + t] = (int64_t)hl.size();
+            for (int N = D->levels[l].first; N < D->levels[l].second; ++N)
+                if (ht[N] == t) hl.push_back(N);
+        }
         for (int N = D->levels[l].first; N < D->levels[l].second; ++N) {
             const double f = hf[N], sp = hp[N], u = f - sp;
             D->lvl_maxf[l] = std::max(D->lvl_maxf[l], hf[N]);
             D->lvl_maxu[l] = std::max(D->lvl_maxu[l], hf[N] - hp[N]);
             D->maxf = std::max(D->maxf, hf[N]);
-            D->fmas += cmul * (sp * sp * sp / 6.0 + u * sp * sp / 2.0 + u * u * sp / 2.0);
+            D->fmas += (ht[N] ? 4.0 : 1.0) * (sp * sp * sp / 6.0 + u * sp * sp / 2.0 + u * u * sp / 2.0);
+            D->ncplx += ht[N] != 0;
         }
+    }
+    D->lst_off[2 * D->levels.size()] = (int64_t)hl.size();
+    D->lst_maxs.assign(2 * D->levels.size(), 0);
+    for (size_t q = 0; q < 2 * D->levels.size(); ++q)
+        for (int64_t i = D->lst_off[q]; i < D->lst_off[q + 1]; ++i)
+            D->lst_maxs[q] = std::max(D->lst_maxs[q], hp[hl[i]]);
+    D->h_nlist = hl;
+    D->h_npiv = hp;
+    D->h_fsz = hf;
+    PGCP_TRY(D->nlist.alloc(nn, s));
+    PGCP_TRY_CUDA(cudaMemcpyAsync(D->nlist.p, hl.data(), nn * sizeof(int32_t), cudaMemcpyHostToDevice, s));
     if (pt.on) {
         for (size_t l = 0; l < D->levels.size(); ++l) {
             double lf = 0;
             int maxp = 0;
             for (int N = D->levels[l].first; N < D->levels[l].second; ++N) {
                 const double f = hf[N], sp = hp[N], u = f - sp;
-                lf += cmul * (sp * sp * sp / 6.0 + u * sp * sp / 2.0 + u * u * sp / 2.0);
+                lf += (ht[N] ? 4.0 : 1.0) * (sp * sp * sp / 6.0 + u * sp * sp / 2.0 + u * u * sp / 2.0);
                 maxp = std::max(maxp, hp[N]);
             }
             fprintf(stderr, "[direct levels] L%zu nodes %d max front %d max pivots %d max update %d FMAs %.3g\n", l,
                     D->levels[l].second - D->levels[l].first, D->lvl_maxf[l], maxp, D->lvl_maxu[l], lf);
         }
     }
-    const size_t tsz_b = D->cplx ? sizeof(double2) : sizeof(double);
-    D->front_bytes = (double)ftot * (double)tsz_b;
-    PGCP_TRY(D->fpool.alloc(ftot * (int64_t)tsz_b, s));  // every front zeroes itself
+    D->front_bytes = 8.0 * (double)ftot;
+    auto ta = std::chrono::steady_clock::now();
+    PGCP_TRY(D->fpool.alloc(8 * ftot, s));  // every front zeroes itself
     PGCP_TRY(D->W.alloc(wtot, s));
     PGCP_TRY(D->X.alloc(NU, s));
+    if (pt.on)
+        fprintf(stderr, "[direct timing] front storage %.3f GB, allocation %.3f ms (host)\n", 8e-9 * (double)ftot,
+                1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - ta).count());
     pt.mark("layout");
     // ---- numeric
     FacArgs fa;
@@ -1480,11 +1799,10 @@ int direct_factor(pgcp_batch* b, const DirectInput& in, DirectFactor** out, cuda
     fa.fsz = D->fsz.p;
     fa.foff = D->foff.p;
     fa.fpool = D->fpool.p;
+    fa.ntype = D->ntype.p;
+    fa.list = nullptr;
     fa.err = D->err.p;
-    if (D->cplx)
-        PGCP_TRY(factor_levels<double2>(D, fa, s, pt));
-    else
-        PGCP_TRY(factor_levels<double>(D, fa, s, pt));
+    PGCP_TRY(factor_levels(D, fa, s, pt));
     PGCP_TRY_CUDA(cudaEventRecord(e1, s));
     PGCP_TRY_CUDA(cudaMemcpyAsync(D->h_err.data(), D->err.p, nslot * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     PGCP_TRY_CUDA(cudaStreamSynchronize(s));
@@ -1516,35 +1834,44 @@ int direct_solve(DirectFactor* D, const double2* b_rows, double2* x_rows, cudaSt
     a.foff = D->foff.p;
     a.woff = D->woff.p;
     a.fpool = D->fpool.p;
+    a.list = nullptr;
     a.W = D->W.p;
     a.X = D->X.p;
     a.b = b_rows;
     const int L = (int)D->levels.size();
-    for (int l = L - 1; l >= 0; --l) {
-        const int lb = D->levels[l].first, le = D->levels[l].second;
+    auto launch = [&](bool fwd, int l, int t) -> int {
+        const int64_t o0 = D->lst_off[2 * l + t], o1 = D->lst_off[2 * l + t + 1];
+        if (o1 <= o0) return PGCP_OK;
+        SolArgs aa = a;
+        aa.list = D->nlist.p + o0;
+        const int n = (int)(o1 - o0);
         const int maxu_child = (l + 1 < L) ? D->lvl_maxu[l + 1] : 0;
-        const size_t smem = (size_t)D->lvl_maxf[l] * sizeof(double2) + (size_t)(D->lvl_maxu[l] + maxu_child) * 4 + 16;
-        if (D->cplx) {
+        const size_t smem = fwd ? (size_t)D->lvl_maxf[l] * sizeof(double2) + (size_t)(D->lvl_maxu[l] + maxu_child) * 4 + 16
+                                : (size_t)D->lvl_maxf[l] * sizeof(double2) + 16;
+        if (fwd && t) {
             PGCP_TRY(set_smem(k_fwd<double2>, smem));
-            k_fwd<double2><<<le - lb, DNT, smem, s>>>(lb, a);
-        } else {
+            k_fwd<double2><<<n, DNT, smem, s>>>(aa);
+        } else if (fwd) {
             PGCP_TRY(set_smem(k_fwd<double>, smem));
-            k_fwd<double><<<le - lb, DNT, smem, s>>>(lb, a);
+            k_fwd<double><<<n, DNT, smem, s>>>(aa);
+        } else if (t) {
+            PGCP_TRY(set_smem(k_bwd<double2>, smem));
+            k_bwd<double2><<<n, DNT, smem, s>>>(aa);
+        } else {
+            PGCP_TRY(set_smem(k_bwd<double>, smem));
+            k_bwd<double><<<n, DNT, smem, s>>>(aa);
         }
         PGCP_LAUNCH_CHECK();
+        return PGCP_OK;
+    };
+    for (int l = L - 1; l >= 0; --l) {
+        PGCP_TRY(launch(true, l, 0));
+        PGCP_TRY(launch(true, l, 1));
     }
     pt.mark("forward");
     for (int l = 0; l < L; ++l) {
-        const int lb = D->levels[l].first, le = D->levels[l].second;
-        const size_t smem = (size_t)D->lvl_maxf[l] * sizeof(double2) + 16;
-        if (D->cplx) {
-            PGCP_TRY(set_smem(k_bwd<double2>, smem));
-            k_bwd<double2><<<le - lb, DNT, smem, s>>>(lb, a);
-        } else {
-            PGCP_TRY(set_smem(k_bwd<double>, smem));
-            k_bwd<double><<<le - lb, DNT, smem, s>>>(lb, a);
-        }
-        PGCP_LAUNCH_CHECK();
+        PGCP_TRY(launch(false, l, 0));
+        PGCP_TRY(launch(false, l, 1));
     }
     pt.mark("backward");
     k_d_scatter<<<grid_for(D->NU, 256), 256, 0, s>>>(D->NU, D->urow.p, D->elim.p, D->X.p, x_rows);
