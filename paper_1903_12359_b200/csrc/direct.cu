@@ -36,6 +36,7 @@
 #include <climits>
 #include <cmath>
 #include <memory>
+#include <mutex>
 #include <cstdlib>
 #include <vector>
 
@@ -495,6 +496,37 @@ __global__ void k_nd_npiv64(int32_t n, const int32_t* __restrict__ a, int64_t* _
     GRID_STRIDE(i, (int64_t)n) b[i] = a[i];
 }
 
+// the adjacency in elimination order, entries above the row only (w > e):
+// what assembly and the symbolic pass read, contiguous per front
+__global__ void k_eadj_count(int64_t NU, const int32_t* __restrict__ perm, const int32_t* __restrict__ elim,
+                             const int64_t* __restrict__ aptr, const int32_t* __restrict__ acol,
+                             int64_t* __restrict__ cnt) {
+    GRID_STRIDE(e, NU) {
+        const int u = perm[e];
+        int c = 0;
+        for (int64_t q = aptr[u]; q < aptr[u + 1]; ++q) c += elim[acol[q]] > e;
+        cnt[e] = c;
+    }
+}
+__global__ void k_eadj_fill(int64_t NU, const int32_t* __restrict__ perm, const int32_t* __restrict__ elim,
+                            const int64_t* __restrict__ aptr, const int32_t* __restrict__ acol,
+                            const double2* __restrict__ aval, const int64_t* __restrict__ eptr,
+                            int32_t* __restrict__ erow, int32_t* __restrict__ ecol, double2* __restrict__ eval) {
+    GRID_STRIDE(e, NU) {
+        const int u = perm[e];
+        int64_t o = eptr[e];
+        for (int64_t q = aptr[u]; q < aptr[u + 1]; ++q) {
+            const int w = elim[acol[q]];
+            if (w > e) {
+                erow[o] = (int32_t)e;
+                ecol[o] = w;
+                eval[o] = aval[q];
+                ++o;
+            }
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // symbolic: update sets
 
@@ -503,8 +535,8 @@ struct SymArgs {
     const int64_t* pfirst;
     const int32_t* perm;
     const int32_t* elim;
-    const int64_t* aptr;
-    const int32_t* acol;
+    const int64_t* eptr;     // adjacency in elimination order (entries above the row only)
+    const int32_t* ecol;
     int32_t* ucnt;
     int64_t* ustart;
     int32_t* upool;
@@ -524,14 +556,11 @@ __global__ void __launch_bounds__(DNT) k_sym(int32_t lb, SymArgs a) {
     const int64_t pend = pf + s;
     if (threadIdx.x == 0) ncand = 0;
     __syncthreads();
-    for (int k = threadIdx.x; k < s; k += DNT) {
-        const int u = a.perm[pf + k];
-        for (int64_t q = a.aptr[u]; q < a.aptr[u + 1]; ++q) {
-            const int e = a.elim[a.acol[q]];
-            if (e >= pend) {
-                const int i = atomicAdd(&ncand, 1);
-                if (i < CAND_MAX) cand[i] = e;
-            }
+    for (int64_t q = a.eptr[pf] + threadIdx.x; q < a.eptr[pend]; q += DNT) {
+        const int e = a.ecol[q];
+        if (e >= pend) {
+            const int i = atomicAdd(&ncand, 1);
+            if (i < CAND_MAX) cand[i] = e;
         }
     }
     const int ch[2] = {a.nd.chA[N], a.nd.chB[N]};
@@ -649,9 +678,10 @@ struct FacArgs {
     const int64_t* pfirst;
     const int32_t* perm;
     const int32_t* elim;
-    const int64_t* aptr;
-    const int32_t* acol;
-    const double2* aval;
+    const int64_t* eptr;     // adjacency in elimination order: row e's entries w > e
+    const int32_t* erow;
+    const int32_t* ecol;
+    const double2* eval;     // A(row, col)
     const int32_t* ucnt;
     const int64_t* ustart;
     const int32_t* upool;
@@ -679,6 +709,21 @@ template <> __device__ __forceinline__ double2 narrow<double2>(double2 v) { retu
 __device__ __forceinline__ int front_pos(int64_t x, int64_t pf, int s, const int32_t* U, int nu) {
     if (x < pf + s) return (int)(x - pf);
     return s + lower_bound_i32(U, nu, (int32_t)x);
+}
+
+// matrix entries of pivots [kb, ke) of a front (lower part, column-major,
+// leading dimension f): S[pos(w)][k] = A(w, u) = conj(A(u, w)), unit diagonal.
+// One thread per stored entry: independent, coalesced loads.
+template <class T>
+__device__ __forceinline__ void assemble_entries(T* S, int f, int64_t pf, int s, const int32_t* Us, int nu, int kb,
+                                                 int ke, const FacArgs& a) {
+    for (int k = kb + threadIdx.x; k < ke; k += DNT) S[(int64_t)k + (int64_t)k * f] = from_c<T>(make_double2(1.0, 0.0));
+    const int64_t q1 = a.eptr[pf + ke];
+    for (int64_t q = a.eptr[pf + kb] + threadIdx.x; q < q1; q += DNT) {
+        const int k = (int)(a.erow[q] - pf);
+        const int i = front_pos(a.ecol[q], pf, s, Us, nu);
+        S[(int64_t)i + (int64_t)k * f] = cj(from_c<T>(a.eval[q]));
+    }
 }
 
 // One TR x TC tile (rows [ti, ti+TR) below rlim, columns [tj, tj+TC) below
@@ -827,17 +872,7 @@ __global__ void __launch_bounds__(DNT, sizeof(T) == 8 ? 8 : 4) k_factor(FacArgs 
         }
     }
     __syncthreads();
-    // matrix entries of my pivot columns (lower part): F[pos(w)][k] = A(w, u) = conj(A(u, w))
-    for (int k = threadIdx.x; k < s; k += DNT) {
-        const int u = a.perm[pf + k];
-        F[(int64_t)k + (int64_t)k * f] = from_c<T>(make_double2(1.0, 0.0));
-        for (int64_t q = a.aptr[u]; q < a.aptr[u + 1]; ++q) {
-            const int64_t e = a.elim[a.acol[q]];
-            if (e <= pf + k) continue;  // eliminated earlier, or the upper part
-            const int i = front_pos(e, pf, s, Us, nu);
-            F[(int64_t)i + (int64_t)k * f] = cj(from_c<T>(a.aval[q]));
-        }
-    }
+    assemble_entries<T>(F, f, pf, s, Us, nu, 0, s, a);
     __syncthreads();
     // extend-add the children's update blocks (fixed order: A, then B; every
     // entry of one child's block lands on a distinct position)
@@ -925,7 +960,8 @@ __global__ void __launch_bounds__(DNT, sizeof(T) == 8 ? 8 : 4) k_factor(FacArgs 
 // and the TRSM of DNT rows below it per CTA; k_pupd: the update of the
 // remaining pivot columns, one CTA per TR x TC tile.
 constexpr int PB = 32;
-constexpr int FUSED_MAXS = 48;  // levels whose fronts all have <= this many pivots stay fused
+constexpr int FUSED_MAXS = 48;
+constexpr size_t SM_FRONT_BYTES = 112 * 1024;  // k_factor_sm: two CTAs per SM  // levels whose fronts all have <= this many pivots stay fused
 
 // phase 0 (one CTA per front): factor the diagonal block in place;
 // phase 1 (CTAs over row chunks): TRSM of the rows below it
@@ -1020,16 +1056,7 @@ __global__ void __launch_bounds__(DNT) k_asm_cols(FacArgs a, int cw) {
         for (int i = threadIdx.x; i < nu; i += DNT) Us[i] = a.upool[a.ustart[N] + i];
     for (int64_t i = (int64_t)c0 * f + threadIdx.x; i < (int64_t)c1 * f; i += DNT) F[i] = zero_t<T>();
     __syncthreads();
-    for (int k = kb + threadIdx.x; k < ke; k += DNT) {
-        const int u = a.perm[pf + k];
-        F[(int64_t)k + (int64_t)k * f] = from_c<T>(make_double2(1.0, 0.0));
-        for (int64_t q = a.aptr[u]; q < a.aptr[u + 1]; ++q) {
-            const int64_t e = a.elim[a.acol[q]];
-            if (e <= pf + k) continue;
-            const int i = front_pos(e, pf, s, Us, nu);
-            F[(int64_t)i + (int64_t)k * f] = cj(from_c<T>(a.aval[q]));
-        }
-    }
+    if (ke > kb) assemble_entries<T>(F, f, pf, s, Us, nu, kb, ke, a);
 }
 
 template <class T>
@@ -1094,6 +1121,154 @@ __global__ void __launch_bounds__(DNT, 4) k_pupd(FacArgs a, int k0) {
     if (tj >= s) return;
     T* F = front_ptr<T>(a.fpool, a.foff[N]);
     tile_one<T>(F, f, tj + TR * p, tj, f, s, k0, k0 + nb, As, Bs);
+}
+
+// Small fronts, resident in shared memory for the whole factorization:
+// zero, matrix entries, children's update blocks (fixed order), then per
+// 16-column block: the diagonal block by one warp (registers + shuffles),
+// the rows below by one thread each, and the trailing lower triangle
+// (pivot columns and the update block alike) in 4x4 register tiles read
+// straight from shared memory. One coalesced write-back at the end.
+template <class T>
+__global__ void __launch_bounds__(DNT) k_factor_sm(FacArgs a) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    __shared__ int bad;
+    const int N = a.list[blockIdx.x];
+    const int s = a.nd.npiv[N];
+    const int nu = a.ucnt[N];
+    const int f = s + nu;
+    const int64_t pf = a.pfirst[N];
+    T* S = reinterpret_cast<T*>(dsm);
+    int32_t* Us = reinterpret_cast<int32_t*>(S + (int64_t)f * f);
+    int32_t* rel = Us + nu;
+    if (threadIdx.x == 0) bad = 0;
+    for (int i = threadIdx.x; i < f * f; i += DNT) S[i] = zero_t<T>();
+    for (int i = threadIdx.x; i < nu; i += DNT) Us[i] = a.upool[a.ustart[N] + i];
+    __syncthreads();
+    assemble_entries<T>(S, f, pf, s, Us, nu, 0, s, a);
+    __syncthreads();
+    const int ch[2] = {a.nd.chA[N], a.nd.chB[N]};
+    for (int c = 0; c < 2; ++c) {
+        const int C = ch[c];
+        if (C < 0) continue;
+        const int sc = a.nd.npiv[C], uc = a.ucnt[C], fc = sc + uc;
+        const int32_t* UC = a.upool + a.ustart[C];
+        for (int i = threadIdx.x; i < uc; i += DNT) rel[i] = front_pos(UC[i], pf, s, Us, nu);
+        __syncthreads();
+        const bool ccx = a.ntype[C] != 0;
+        const double* FC = reinterpret_cast<const double*>(a.fpool) + a.foff[C];
+        const int tot = uc * uc;
+        for (int t0 = threadIdx.x; t0 < tot; t0 += 4 * DNT) {
+            double2 v[4];
+            int pos[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int t = t0 + q * DNT;
+                const int bcol = t / uc, i = t - bcol * uc;
+                const bool ok = t < tot && i >= bcol;
+                pos[q] = ok ? rel[i] + rel[bcol] * f : -1;
+                const int64_t e = (int64_t)(sc + bcol) * fc + sc + i;
+                v[q] = !ok ? make_double2(0.0, 0.0)
+                           : (ccx ? reinterpret_cast<const double2*>(FC)[e] : make_double2(FC[e], 0.0));
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (pos[q] >= 0) S[pos[q]] = add(S[pos[q]], narrow<T>(v[q]));
+        }
+        __syncthreads();
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int k0 = 0; k0 < s; k0 += NB) {
+        const int nb = min(NB, s - k0);
+        if (warp == 0) {  // diagonal block: lane i keeps row i
+            T r[NB];
+#pragma unroll
+            for (int j = 0; j < NB; ++j) r[j] = (lane < nb && j < nb) ? S[(k0 + lane) + (k0 + j) * f] : zero_t<T>();
+#pragma unroll
+            for (int k = 0; k < NB; ++k) {
+                if (k < nb) {
+                    double d = re(shfl_t(r[k], k));
+                    if (!(d > 0.0) || !isfinite(d)) {
+                        if (lane == 0) bad = 1;
+                        d = 1.0;
+                    }
+                    d = sqrt(d);
+                    if (lane == k) r[k] = from_c<T>(make_double2(d, 0.0));
+                    else if (lane > k) r[k] = scale(r[k], 1.0 / d);
+#pragma unroll
+                    for (int j = k + 1; j < NB; ++j) {
+                        const T ljk = shfl_t(r[k], j);
+                        if (lane >= j && j < nb) fma_cj(r[j], scale(r[k], -1.0), ljk);
+                    }
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < NB; ++j)
+                if (lane < nb && j <= lane) S[(k0 + lane) + (k0 + j) * f] = r[j];
+        }
+        __syncthreads();
+        for (int rr = k0 + nb + threadIdx.x; rr < f; rr += DNT) {
+            T x[NB];
+#pragma unroll
+            for (int k = 0; k < NB; ++k) x[k] = k < nb ? S[rr + (k0 + k) * f] : zero_t<T>();
+#pragma unroll
+            for (int k = 0; k < NB; ++k) {
+                if (k < nb) {
+                    T v = x[k];
+#pragma unroll
+                    for (int j = 0; j < NB; ++j)
+                        if (j < k) fma_cj(v, scale(x[j], -1.0), S[(k0 + k) + (k0 + j) * f]);
+                    x[k] = scale(v, 1.0 / re(S[(k0 + k) + (k0 + k) * f]));
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < NB; ++k)
+                if (k < nb) S[rr + (k0 + k) * f] = x[k];
+        }
+        __syncthreads();
+        // trailing lower triangle, 4x4 tiles (tile row ti >= tile column tj)
+        const int c0 = k0 + nb, m = f - c0;
+        if (m > 0) {
+            const int nt = (m + 3) >> 2;
+            const int ntiles = nt * (nt + 1) / 2;
+            for (int t = threadIdx.x; t < ntiles; t += DNT) {
+                // t -> (ti, tj), ti >= tj, row-major over the lower tiles
+                int ti = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
+                while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+                while (ti * (ti + 1) / 2 > t) --ti;
+                const int tj = t - ti * (ti + 1) / 2;
+                const int rb = c0 + 4 * ti, cb = c0 + 4 * tj;
+                T acc[4][4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) acc[i][j] = zero_t<T>();
+                for (int k = 0; k < nb; ++k) {
+                    const T* colk = S + (k0 + k) * f;
+                    T av[4], bv[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) av[i] = rb + i < f ? colk[rb + i] : zero_t<T>();
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) bv[j] = cb + j < f ? colk[cb + j] : zero_t<T>();
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) fma_cj(acc[i][j], av[i], bv[j]);
+                }
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int r = rb + i, c = cb + j;
+                        if (r < f && c < f && r >= c) S[r + c * f] = sub(S[r + c * f], acc[i][j]);
+                    }
+            }
+        }
+        __syncthreads();
+    }
+    T* F = front_ptr<T>(a.fpool, a.foff[N]);
+    for (int i = threadIdx.x; i < f * f; i += DNT) F[i] = S[i];
+    if (threadIdx.x == 0 && bad) atomicExch(a.err + a.nd.slot[N], 1);
 }
 
 // Schur update of the U block of every front of a level, one CTA per lower
@@ -1328,6 +1503,92 @@ struct PhaseTimer {
 
 }  // namespace
 
+// ---------------------------------------------------------------------------
+// Workspace cache for the large per-factorization buffers (front storage,
+// update sets, forward partial sums: GBs at cfg 2). Stream-ordered pool
+// allocations of that size sometimes make the pool map new memory (ms of
+// host time); these blocks are instead kept per process, grow-only, and
+// handed out again after an event on the releasing stream (the acquiring
+// stream waits on it).
+struct WsSlot {
+    int dev = -1;
+    void* p = nullptr;
+    size_t bytes = 0;
+    bool busy = false;
+    cudaEvent_t ready = nullptr;
+};
+static std::mutex g_ws_mu;
+static std::vector<WsSlot> g_ws;
+
+static int ws_acquire(size_t bytes, cudaStream_t s, int* slot_out, void** p_out) {
+    int dev = 0;
+    PGCP_TRY_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(g_ws_mu);
+    int best = -1;
+    for (int i = 0; i < (int)g_ws.size(); ++i) {
+        const WsSlot& w = g_ws[i];
+        if (w.dev != dev || w.busy || w.bytes < bytes) continue;
+        if (best < 0 || w.bytes < g_ws[best].bytes) best = i;
+    }
+    if (best < 0) {  // grow: reuse an idle slot of this device, else add one
+        for (int i = 0; i < (int)g_ws.size() && best < 0; ++i)
+            if (g_ws[i].dev == dev && !g_ws[i].busy) best = i;
+        if (best < 0) {
+            g_ws.push_back(WsSlot());
+            best = (int)g_ws.size() - 1;
+            g_ws[best].dev = dev;
+        }
+        WsSlot& w = g_ws[best];
+        if (w.p) {
+            if (w.ready) PGCP_TRY_CUDA(cudaEventSynchronize(w.ready));
+            PGCP_TRY_CUDA(cudaFree(w.p));
+            w.p = nullptr;
+            w.bytes = 0;
+        }
+        const size_t want = std::max<size_t>(bytes + bytes / 8, 1 << 20);
+        PGCP_TRY_CUDA(cudaMalloc(&w.p, want));
+        w.bytes = want;
+    }
+    WsSlot& w = g_ws[best];
+    if (w.ready) PGCP_TRY_CUDA(cudaStreamWaitEvent(s, w.ready, 0));
+    w.busy = true;
+    *slot_out = best;
+    *p_out = w.p;
+    return PGCP_OK;
+}
+
+static void ws_release(int slot, cudaStream_t s) {
+    std::lock_guard<std::mutex> lock(g_ws_mu);
+    WsSlot& w = g_ws[slot];
+    if (!w.ready) cudaEventCreateWithFlags(&w.ready, cudaEventDisableTiming);
+    cudaEventRecord(w.ready, s);
+    w.busy = false;
+}
+
+template <class T>
+struct WsBuf {
+    T* p = nullptr;
+    int slot = -1;
+    cudaStream_t s = nullptr;
+    WsBuf() = default;
+    WsBuf(const WsBuf&) = delete;
+    WsBuf& operator=(const WsBuf&) = delete;
+    ~WsBuf() { release(); }
+    int alloc(int64_t n, cudaStream_t st) {
+        release();
+        void* q = nullptr;
+        PGCP_TRY(ws_acquire((size_t)std::max<int64_t>(n, 1) * sizeof(T), st, &slot, &q));
+        p = static_cast<T*>(q);
+        s = st;
+        return PGCP_OK;
+    }
+    void release() {
+        if (slot >= 0) ws_release(slot, s);
+        slot = -1;
+        p = nullptr;
+    }
+};
+
 struct DirectFactor {
     bool cplx = false;
     int32_t nslot = 0;
@@ -1339,6 +1600,9 @@ struct DirectFactor {
     DevBuf<int32_t> acol;
     DevBuf<double2> aval;
     DevBuf<int32_t> elim, perm;
+    DevBuf<int64_t> eptr;
+    DevBuf<int32_t> erow, ecol;
+    DevBuf<double2> eval;
     // tree
     int32_t nnodes = 0;
     std::vector<std::pair<int32_t, int32_t>> levels;  // node id ranges, level 0 = roots
@@ -1348,16 +1612,19 @@ struct DirectFactor {
     DevBuf<int32_t> gcnt;
     DevBuf<float2> split;
     DevBuf<int64_t> pfirst;
-    DevBuf<int32_t> ucnt, upool, fsz;
+    DevBuf<int32_t> ucnt, fsz;
+    WsBuf<int32_t> upool;
     DevBuf<int64_t> ustart, foff, woff;
-    DevBuf<unsigned char> fpool;
-    DevBuf<double2> W, X;
+    WsBuf<unsigned char> fpool;
+    WsBuf<double2> W;
+    DevBuf<double2> X;
     DevBuf<int32_t> err;
     DevBuf<int8_t> ntype;
     // fronts per (level, type): nlist[lst_off[2 l + t], lst_off[2 l + t + 1])
     DevBuf<int32_t> nlist;
     std::vector<int64_t> lst_off;
     std::vector<int> lst_maxs;               // per (level, type): largest pivot count
+    std::vector<int> lst_maxf;               // ... largest front
     std::vector<int32_t> h_nlist, h_npiv, h_fsz;
     std::vector<int> lvl_maxf, lvl_maxu;
     int ncplx = 0;
@@ -1419,6 +1686,16 @@ int factor_level(DirectFactor* D, FacArgs fa, int l, int type, cudaStream_t s) {
     if (smem > 227 * 1024) {
         set_error("direct solver: front update set too large (%d)", D->lvl_maxu[l]);
         return DIRECT_FALLBACK;
+    }
+    {   // fronts that fit in shared memory: the resident kernel
+        const int maxf_t = D->lst_maxf[2 * l + type];
+        const size_t sm = (size_t)maxf_t * maxf_t * tsz + (size_t)(D->lvl_maxu[l] + maxu_child) * 4 + 16;
+        if (sm <= SM_FRONT_BYTES && !getenv("PGCP_DIRECT_NO_SMEM")) {
+            PGCP_TRY(set_smem(k_factor_sm<T>, sm));
+            k_factor_sm<T><<<n, DNT, sm, s>>>(fa);
+            PGCP_LAUNCH_CHECK();
+            return PGCP_OK;
+        }
     }
     PGCP_TRY(set_smem(k_factor<T>, smem));
     const int nt = schur_tiles(D->lvl_maxu[l]);
@@ -1664,6 +1941,22 @@ int direct_factor(pgcp_batch* b, const DirectInput& in, DirectFactor** out, cuda
         PGCP_LAUNCH_CHECK();
     }
     pt.mark("postorder");
+    // ---- adjacency in elimination order
+    {
+        DevBuf<int64_t> ecnt;
+        PGCP_TRY(ecnt.alloc(NU, s));
+        k_eadj_count<<<grid_for(NU, 256), 256, 0, s>>>(NU, D->perm.p, D->elim.p, D->aptr.p, D->acol.p, ecnt.p);
+        PGCP_LAUNCH_CHECK();
+        PGCP_TRY(D->eptr.alloc(NU + 1, s));
+        PGCP_TRY(exclusive_scan_i64(ecnt.p, D->eptr.p, NU, s));
+        const int64_t ne = annz;  // upper bound (each stored entry once per direction)
+        PGCP_TRY(D->erow.alloc(ne, s));
+        PGCP_TRY(D->ecol.alloc(ne, s));
+        PGCP_TRY(D->eval.alloc(ne, s));
+        k_eadj_fill<<<grid_for(NU, 256), 256, 0, s>>>(NU, D->perm.p, D->elim.p, D->aptr.p, D->acol.p, D->aval.p,
+                                                    D->eptr.p, D->erow.p, D->ecol.p, D->eval.p);
+        PGCP_LAUNCH_CHECK();
+    }
     // ---- symbolic: update sets, leaves first
     PGCP_TRY(D->ucnt.alloc(nn, s));
     PGCP_TRY(D->ustart.alloc(nn, s));
@@ -1680,8 +1973,8 @@ int direct_factor(pgcp_batch* b, const DirectInput& in, DirectFactor** out, cuda
     sa.pfirst = D->pfirst.p;
     sa.perm = D->perm.p;
     sa.elim = D->elim.p;
-    sa.aptr = D->aptr.p;
-    sa.acol = D->acol.p;
+    sa.eptr = D->eptr.p;
+    sa.ecol = D->ecol.p;
     sa.ucnt = D->ucnt.p;
     sa.ustart = D->ustart.p;
     sa.upool = D->upool.p;
@@ -1754,9 +2047,12 @@ int direct_factor(pgcp_batch* b, const DirectInput& in, DirectFactor** out, cuda
     }
     D->lst_off[2 * D->levels.size()] = (int64_t)hl.size();
     D->lst_maxs.assign(2 * D->levels.size(), 0);
+    D->lst_maxf.assign(2 * D->levels.size(), 0);
     for (size_t q = 0; q < 2 * D->levels.size(); ++q)
-        for (int64_t i = D->lst_off[q]; i < D->lst_off[q + 1]; ++i)
+        for (int64_t i = D->lst_off[q]; i < D->lst_off[q + 1]; ++i) {
             D->lst_maxs[q] = std::max(D->lst_maxs[q], hp[hl[i]]);
+            D->lst_maxf[q] = std::max(D->lst_maxf[q], hf[hl[i]]);
+        }
     D->h_nlist = hl;
     D->h_npiv = hp;
     D->h_fsz = hf;
@@ -1790,9 +2086,10 @@ int direct_factor(pgcp_batch* b, const DirectInput& in, DirectFactor** out, cuda
     fa.pfirst = D->pfirst.p;
     fa.perm = D->perm.p;
     fa.elim = D->elim.p;
-    fa.aptr = D->aptr.p;
-    fa.acol = D->acol.p;
-    fa.aval = D->aval.p;
+    fa.eptr = D->eptr.p;
+    fa.erow = D->erow.p;
+    fa.ecol = D->ecol.p;
+    fa.eval = D->eval.p;
     fa.ucnt = D->ucnt.p;
     fa.ustart = D->ustart.p;
     fa.upool = D->upool.p;
