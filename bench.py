@@ -1,6 +1,6 @@
 #!/usr/bin/env python
 """PGCP hot-path benchmark (BASELINE.json metric: mesh vertices/sec end to
-end, plus the batched-PCG HBM roofline).
+end; the direct solver's FP64 roofline, plus the batched-PCG HBM/L2 roofline).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
     python -m torch.distributed.run --nnodes=1 --nproc-per-node N \
@@ -62,6 +62,7 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cfg5", action="store_true", help="skip the cfg-5 (4096^2, 256 subdomains) solve leg")
+    p.add_argument("--no-pcg", action="store_true", help="skip the cfg-2 PCG (solver='pcg') roofline leg")
     p.add_argument("--cpu-sample", type=int, default=0, help="subdomains in the CPU sample (0 = cores)")
     p.add_argument("--cpu-seconds", type=float, default=10.0, help="minimum CPU-baseline sample time")
     return p.parse_args()
@@ -130,6 +131,59 @@ def l2_probe_gbs(dev, mib=48, reps=40):
     return best
 
 
+def fp64_probe_tflops(iters=20000):
+    """Attainable FP64 FMA rate, measured here: pgcp_fp64_probe (8 CTAs x 256
+    threads per SM, 8 independent FMA chains per thread), CUDA events on the
+    launch stream, best of 3 after a warm-up."""
+    import ctypes
+    import torch
+    from paper_1903_12359_b200 import _native as nat
+    L = nat.lib()
+    L.pgcp_fp64_probe.argtypes = [ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+    sink = torch.zeros(1, dtype=torch.float64, device="cuda")
+    thr = ctypes.c_int64(0)
+    st = torch.cuda.current_stream()
+    best = 0.0
+    for i in range(4):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        nat.check(L.pgcp_fp64_probe(iters, sink.data_ptr(), ctypes.byref(thr), ctypes.c_void_p(st.cuda_stream)))
+        e1.record(st)
+        torch.cuda.synchronize()
+        if i:
+            best = max(best, 16.0 * iters * thr.value / (e0.elapsed_time(e1) / 1e3) / 1e12)
+    return best
+
+
+def pcg_leg(part_batch, peak, l2_peak, runs=2):
+    """The batched two-level PCG (solver="pcg", the north_star's kernel) on the
+    same cfg-2 systems: its HBM/L2 roofline, CUDA events on its stream."""
+    b = part_batch
+    b.flatten(solver="pcg")
+    res = []
+    for _ in range(runs):
+        _, st = b.flatten(solver="pcg")
+        assert all(x["status"] == 0 for x in st)
+        res.append(b.last_solve(0))
+    kernel_ms = statistics.mean(r["kernel_ms"] for r in res)
+    ref_launch = statistics.mean(r["ref_bytes"] for r in res)
+    dev_launch = statistics.mean(r["bytes"] for r in res)
+    achieved = ref_launch / (kernel_ms / 1e3) / 1e9
+    dev_ach = dev_launch / (kernel_ms / 1e3) / 1e9
+    ncu = ncu_summary()
+    return {"bound": "l2", "kernel": "k_pcg2 (two-level PCG, DNCP flatten of the 64 cfg-2 subdomains, one launch; "
+                                     "solver='pcg')",
+            "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": ncu_traffic(),
+            "lts_bytes_per_launch": ncu.get("lts_bytes_per_launch"), "l2_peak": l2_peak,
+            "l2_frac": dev_ach / l2_peak if l2_peak else None, "kernel_ms": kernel_ms,
+            "iterations_per_launch": statistics.mean(r["iters_sum"] for r in res), "bytes_per_launch": ref_launch,
+            "bytes_model": "SURVEY 8(d): per PCG iteration of a subdomain 12*z + 4*(r+1) bytes of the reference's "
+                           "CSR system C_ff (z nonzeros, r = 2|U| rows), summed over the iterations each subdomain ran",
+            "device_bytes_per_launch": dev_launch, "device_achieved": dev_ach,
+            "note": "L2-resident working set (DRAM ~2% of the algorithmic bytes): bounded by L2 latency; the default "
+                    "solver is the multifrontal direct one (`roofline`), 10x faster on this workload"}
+
+
 def physical_cores():
     try:
         import psutil
@@ -166,13 +220,43 @@ def cfg5_leg(dev, peak, l2_peak, runs=2):
     part = pg.partition_mesh(pg.TriMesh(V, F), cuts)
     b = part.batch
     b.laplacian()
-    b.flatten()  # warm-up (coarse-space setup paths, allocator)
+    # the default (direct) solver: flatten + Dirichlet solve of all 256 subdomains
+    from paper_1903_12359_b200 import _native as nat
+    voff = b.host(nat.ARR_VERT_OFF, torch.int64)
+    loff = b.host(nat.ARR_LOOP_OFF, torch.int64)
+    lp = b.host(nat.ARR_LOOP, torch.int32)
+    gid = torch.tensor(np.concatenate([voff[c] + lp[loff[c]:loff[c + 1]] for c in range(b.K)]).astype(np.int32),
+                       device=dev)
+    direct = []
+    for i in range(3):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        z, st = b.flatten(solver="direct")
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        zh, sth = b.harmonic(gid, z[gid.long()], solver="direct")
+        torch.cuda.synchronize()
+        t2 = time.perf_counter()
+        assert all(x["status"] == 0 for x in st) and all(x["status"] == 0 for x in sth), "cfg-5 direct solve failed"
+        if i:
+            fl, hm = b.last_solve(0), b.last_solve(1)
+            direct.append((1e3 * (t1 - t0), 1e3 * (t2 - t1), fl, hm))
+    del z, zh
+    direct_leg = {"flatten_ms": statistics.mean(d[0] for d in direct),
+                  "harmonic_ms": statistics.mean(d[1] for d in direct),
+                  "flatten_numeric_ms": statistics.mean(d[2]["numeric_ms"] for d in direct),
+                  "flatten_fmas": direct[-1][2]["fmas"], "harmonic_fmas": direct[-1][3]["fmas"],
+                  "front_gb": (direct[-1][2]["front_bytes"] + direct[-1][3]["front_bytes"]) / 1e9,
+                  "max_front": direct[-1][2]["max_front"],
+                  "note": "wall time of batch.flatten / batch.harmonic (ordering, symbolic, numeric, solves, "
+                          "checks), host-synchronised"}
+    b.flatten(solver="pcg")  # warm-up (coarse-space setup paths, allocator)
     torch.cuda.synchronize()
     sampler = ClockSampler(dev.index or 0)
     sampler.start()
     res = []
     for _ in range(runs):
-        _, st = b.flatten()
+        _, st = b.flatten(solver="pcg")
         res.append(b.last_solve(0))
         assert all(x["status"] == 0 for x in st), "cfg-5 flatten failed"
     clocks = sampler.stop()
@@ -183,7 +267,8 @@ def cfg5_leg(dev, peak, l2_peak, runs=2):
     ncu = ncu_summary("r2_cfg5_ncu_summary.json")
     del part, b
     torch.cuda.empty_cache()
-    return {"bound": "l2", "kernel": "k_pcg2 (DNCP flatten of the 256 cfg-5 subdomains, one launch, 16-CTA clusters)",
+    return {"bound": "l2", "kernel": "k_pcg2 (solver='pcg': DNCP flatten of the 256 cfg-5 subdomains, one launch, "
+                                     "16-CTA clusters); `direct`: the default multifrontal solver on the same systems",
             "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak, "kernel_ms": ms,
             "bytes_per_launch": ref_b, "device_bytes_per_launch": dev_b,
             "device_achieved": dev_b / (ms / 1e3) / 1e9, "l2_peak": l2_peak,
@@ -191,7 +276,7 @@ def cfg5_leg(dev, peak, l2_peak, runs=2):
             "iterations_per_launch": statistics.mean(r["iters_sum"] for r in res),
             "iterations_max": max(r["iters_max"] for r in res),
             "traffic": ncu.get("dram_bytes_per_launch"), "lts_bytes_per_launch": ncu.get("lts_bytes_per_launch"),
-            "ncu": "profiles/r2_cfg5_ncu_summary.json", "clocks": clocks, "generate_s": t_gen,
+            "ncu": "profiles/r2_cfg5_ncu_summary.json", "clocks": clocks, "generate_s": t_gen, "direct": direct_leg,
             "note": "1.2 GB of matrices in total, but the ~7 concurrent clusters' working sets stay in L2 for their "
                     "thousands of iterations: DRAM sees ~19 GB per launch against ~10 TB of L2 traffic, so the "
                     "bound is L2 latency, and frac is the algorithmic bytes over the HBM peak (the rate an HBM-"
@@ -345,7 +430,7 @@ def main():
     sampler.start()
     l0 = lib.pgcp_launch_count()
     total_ms = 0.0
-    pcg_ms, pcg_bytes, pcg_iters, pcg_ref = [], [], [], []
+    flat_stats, harm_stats = [], []
     stages = {}
     for _ in range(args.steps):
         flush.zero_()
@@ -357,11 +442,8 @@ def main():
         e1.record(stream)
         torch.cuda.synchronize()
         total_ms += e0.elapsed_time(e1)
-        fl = rep.solver["flatten"]
-        pcg_ms.append(fl["kernel_ms"])
-        pcg_bytes.append(fl["bytes"])
-        pcg_ref.append(fl["ref_bytes"])
-        pcg_iters.append(fl["iters_sum"])
+        flat_stats.append(rep.solver["flatten"])
+        harm_stats.append(rep.solver.get("harmonic", {}))
         for k, v in rep.timings.items():
             stages[k] = stages.get(k, 0.0) + 1e3 * v
     launches = lib.pgcp_launch_count() - l0
@@ -392,32 +474,43 @@ def main():
                "d2h_bytes_per_step": int(d2h)}
 
     peak, peak_src = measured_peak()
-    kernel_ms = statistics.mean(pcg_ms)
-    ref_launch = statistics.mean(pcg_ref)
-    dev_launch = statistics.mean(pcg_bytes)
-    achieved = ref_launch / (kernel_ms / 1e3) / 1e9
     l2_peak = l2_probe_gbs(dev)
-    ncu = ncu_summary()
-    dev_ach = dev_launch / (kernel_ms / 1e3) / 1e9
-    roof = {"bound": "l2", "kernel": "k_pcg2 (two-level PCG, DNCP flatten of the 64 subdomains, one launch)",
-            "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": ncu_traffic(),
-            "lts_bytes_per_launch": ncu.get("lts_bytes_per_launch"),
-            "l2_peak": l2_peak, "l2_peak_source": "measured here: pgcp_l2_probe (48 MiB resident, L2-only 16-B loads, best of 3)",
-            "l2_frac": dev_ach / l2_peak if l2_peak else None,
-            "peak_source": peak_src, "kernel_ms": kernel_ms, "iterations_per_launch": statistics.mean(pcg_iters),
-            "bytes_per_launch": ref_launch,
-            "bytes_model": "SURVEY 8(d): per PCG iteration of a subdomain 12*z + 4*(r+1) bytes of the reference's "
-                           "CSR system C_ff (z nonzeros, r = 2|U| rows), summed over the iterations each subdomain ran",
-            "device_bytes_per_launch": dev_launch,
-            "device_achieved": dev_ach,
-            "device_bytes_model": "what k_pcg2 moves per iteration: per stored sliced-ELL entry 8 B value + 2 B "
-                                  "column code (all-local slices) or 4 B (slices with remote columns) (complex-"
-                                  "Hermitian form: L streamed once for x and y), 32 B/row y, 32 B/row p, 16 B/row fp16 coarse "
-                                  "weights, 8*nc*ncp B of fp32 E^-1; z, q, r stay in distributed shared memory",
-            "note": "the cfg-2 working set (~90 MB) is L2-resident: DRAM traffic (ncu, `traffic`) is ~2% of the "
-                    "algorithmic bytes, so the kernel is bounded by L2 latency, not HBM; `frac` is the algorithmic "
-                    "bytes over the measured HBM peak (the contract's denominator), `l2_frac` the device bytes over "
-                    "the L2 bandwidth measured in this run"}
+    fp64 = fp64_probe_tflops()
+    fl = flat_stats
+    assert all(x.get("solver") == "direct" for x in fl), "the bench measures the default (direct) solver"
+    num_ms = statistics.mean(x["numeric_ms"] for x in fl)
+    fmas = statistics.mean(x["fmas"] for x in fl)
+    achieved = 2.0 * fmas / (num_ms / 1e3) / 1e12
+    dncp = ncu_summary("r2_direct_ncu_summary.json")
+    roof = {"bound": "fp64",
+            "kernel": "multifrontal numeric factorization of the 64 cfg-2 DNCP systems (k_factor_warp / "
+                      "k_factor_sm / k_factor / k_asm_* / k_pdiag / k_pupd / k_schur: 13 dissection levels x "
+                      "{real, complex} fronts, one stream; `launch` = the whole numeric phase)",
+            "achieved": achieved, "peak": fp64, "unit": "TFLOP/s", "frac": achieved / fp64 if fp64 else None,
+            "traffic": dncp.get("dram_bytes_per_factorization"),
+            "peak_source": "measured here: pgcp_fp64_probe (8 independent FMA chains per thread, 8 x 256 threads "
+                           "per SM, best of 3)",
+            "flops_per_launch": 2.0 * fmas,
+            "flops_model": "per front with s pivots and u update rows: s^3/6 + u s^2/2 + u^2 s/2 multiply-adds, x4 "
+                           "for complex fronts (subtree holds DNCP coupling), x2 flops",
+            "numeric_ms": num_ms,
+            "factor_ms_with_ordering": statistics.mean(x["factor_ms"] for x in fl),
+            "solve_ms": statistics.mean(x["solve_ms"] for x in fl),
+            "front_bytes": statistics.mean(x["front_bytes"] for x in fl),
+            "harmonic": {"numeric_ms": statistics.mean(x["numeric_ms"] for x in harm_stats if x),
+                         "fmas": statistics.mean(x["fmas"] for x in harm_stats if x),
+                         "solve_ms": statistics.mean(x["solve_ms"] for x in harm_stats if x)},
+            "hbm_view": {"front_bytes_written_per_launch": statistics.mean(x["front_bytes"] for x in fl),
+                         "gbs": statistics.mean(x["front_bytes"] for x in fl) / (num_ms / 1e3) / 1e9,
+                         "hbm_peak": peak, "hbm_peak_source": peak_src},
+            "note": "thousands of small dense fronts per level: the phase is latency-bound (per-front dependency "
+                    "chains, level barriers), neither FP64- nor HBM-bound; DESIGN.md section 4b"}
+    roof_pcg = None
+    if not args.no_pcg:
+        part = pg.partition_mesh(mesh_dev, cuts)
+        part.batch.laplacian()
+        roof_pcg = pcg_leg(part.batch, peak, l2_peak)
+        del part
     cfg5 = None
     if not args.no_cfg5:
         cfg5 = cfg5_leg(dev, peak, l2_peak)
@@ -442,7 +535,7 @@ def main():
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": WORKLOAD, "n_vertices": n, "n_faces": int(len(F)), "n_subdomains": 64,
                        "l2": "flushed before every timed step (256 MiB write)", "parallelism": "1 GPU"},
-            "roofline": roof, "roofline_cfg5": cfg5, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+            "roofline": roof, "roofline_pcg": roof_pcg, "roofline_cfg5": cfg5, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
             "gpu_launches": int(launches),
             "stages_ms_per_step": {k: v / args.steps for k, v in stages.items()},
             "quality": {"flips": rep.flips, "angular_mean_deg": rep.distortion["angular_abs"]["mean"],

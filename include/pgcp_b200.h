@@ -412,6 +412,10 @@ PGCP_API int pgcp_area_distortion(const double* V, const int32_t* F, int64_t n, 
  * L2-only 16-byte loads; bytes x reps / time = attainable L2 read bandwidth. */
 PGCP_API int pgcp_l2_probe(const void* buf, int64_t bytes, int32_t reps, unsigned long long* sink, void* stream);
 
+/* Measurement kernel (bench.py): FP64 FMA throughput, 8 independent chains
+ * per thread over `iters` steps; flops = 16 x iters x *threads_out. */
+PGCP_API int pgcp_fp64_probe(int32_t iters, double* sink, int64_t* threads_out, void* stream);
+
 /* host-side weld-schedule planner (partition.py:236-324): see planner.cpp */
 PGCP_API int pgcp_plan_weld_schedule(const int64_t* cyc, const int64_t* cyc_off, int32_t K,
                             const int64_t* cuts, int64_t ncuts, int mode_sphere,

@@ -52,9 +52,9 @@ int pgcp_batch_last_solve(const pgcp_batch* b, int which, double* out, int nout)
         set_error("pgcp_batch_last_solve: invalid arguments");
         return PGCP_E_INVALID;
     }
-    double v[18];
+    double v[19];
     pgcp::solve_summary(b, which, v);
-    for (int i = 0; i < nout && i < 18; ++i) out[i] = v[i];
+    for (int i = 0; i < nout && i < 19; ++i) out[i] = v[i];
     return PGCP_OK;
 }
 

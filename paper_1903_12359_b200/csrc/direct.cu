@@ -961,7 +961,8 @@ __global__ void __launch_bounds__(DNT, sizeof(T) == 8 ? 8 : 4) k_factor(FacArgs 
 // remaining pivot columns, one CTA per TR x TC tile.
 constexpr int PB = 32;
 constexpr int FUSED_MAXS = 48;
-constexpr size_t SM_FRONT_BYTES = 112 * 1024;  // k_factor_sm: two CTAs per SM  // levels whose fronts all have <= this many pivots stay fused
+constexpr size_t SM_FRONT_BYTES = 112 * 1024;  // k_factor_sm: two CTAs per SM
+constexpr size_t WARP_FRONT_BYTES = 40 * 1024; // k_factor_warp: per warp (packed lower triangle)  // levels whose fronts all have <= this many pivots stay fused
 
 // phase 0 (one CTA per front): factor the diagonal block in place;
 // phase 1 (CTAs over row chunks): TRSM of the rows below it
@@ -1083,14 +1084,24 @@ __global__ void __launch_bounds__(DNT) k_asm_child(FacArgs a, int which, int cw)
     T* F = front_ptr<T>(a.fpool, a.foff[N]);
     const bool ccx = a.ntype[C] != 0;
     const double* FC = reinterpret_cast<const double*>(a.fpool) + a.foff[C];
-    for (int b = b0; b < b1; ++b) {
-        const int cb = rel[b];
-        for (int i = b + threadIdx.x; i < uc; i += DNT) {
+    const int tot = (b1 - b0) * uc;
+    constexpr int BAT = 4;
+    for (int t0 = threadIdx.x; t0 < tot; t0 += DNT * BAT) {
+        double2 v[BAT];
+        int64_t pos[BAT];
+#pragma unroll
+        for (int q = 0; q < BAT; ++q) {
+            const int t = t0 + DNT * q;
+            const int b = b0 + t / uc, i = t % uc;
+            const bool ok = t < tot && i >= b;
+            pos[q] = ok ? (int64_t)rel[i] + (int64_t)rel[b] * f : -1;
             const int64_t e = (int64_t)(sc + b) * fc + sc + i;
-            const double2 v = ccx ? reinterpret_cast<const double2*>(FC)[e] : make_double2(FC[e], 0.0);
-            T& d = F[(int64_t)rel[i] + (int64_t)cb * f];
-            d = add(d, narrow<T>(v));
+            v[q] = !ok ? make_double2(0.0, 0.0)
+                       : (ccx ? reinterpret_cast<const double2*>(FC)[e] : make_double2(FC[e], 0.0));
         }
+#pragma unroll
+        for (int q = 0; q < BAT; ++q)
+            if (pos[q] >= 0) F[pos[q]] = add(F[pos[q]], narrow<T>(v[q]));
     }
 }
 
@@ -1269,6 +1280,173 @@ __global__ void __launch_bounds__(DNT) k_factor_sm(FacArgs a) {
     T* F = front_ptr<T>(a.fpool, a.foff[N]);
     for (int i = threadIdx.x; i < f * f; i += DNT) F[i] = S[i];
     if (threadIdx.x == 0 && bad) atomicExch(a.err + a.nd.slot[N], 1);
+}
+
+// Warp-per-front factorization of the smallest fronts: each warp of the CTA
+// owns one front, stored as a packed lower triangle (column-major) in its
+// own slice of shared memory, and runs the whole partial factorization with
+// __syncwarp only: diagonal blocks in registers (lane = row), TRSM with one
+// lane per row, trailing updates in 4x4 register tiles. The result goes to
+// the front's full-square storage (lower part) for the parent and the solves.
+__device__ __forceinline__ int pk(int i, int j, int f) { return j * (2 * f - j - 1) / 2 + i; }
+
+template <class T>
+__global__ void __launch_bounds__(256) k_factor_warp(FacArgs a, int nfront, int wbytes) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int idx = blockIdx.x * (blockDim.x >> 5) + warp;
+    if (idx >= nfront) return;
+    const int N = a.list[idx];
+    const int s = a.nd.npiv[N];
+    const int nu = a.ucnt[N];
+    const int f = s + nu;
+    const int64_t pf = a.pfirst[N];
+    unsigned char* base = dsm + (size_t)warp * wbytes;
+    T* S = reinterpret_cast<T*>(base);
+    const int np = f * (f + 1) / 2;
+    int32_t* Us = reinterpret_cast<int32_t*>(S + np);
+    int32_t* rel = Us + nu;
+    for (int i = lane; i < np; i += 32) S[i] = zero_t<T>();
+    for (int i = lane; i < nu; i += 32) Us[i] = a.upool[a.ustart[N] + i];
+    __syncwarp();
+    for (int k = lane; k < s; k += 32) S[pk(k, k, f)] = from_c<T>(make_double2(1.0, 0.0));
+    {
+        const int64_t q1 = a.eptr[pf + s];
+        for (int64_t q = a.eptr[pf] + lane; q < q1; q += 32) {
+            const int k = (int)(a.erow[q] - pf);
+            const int i = front_pos(a.ecol[q], pf, s, Us, nu);
+            S[pk(i, k, f)] = cj(from_c<T>(a.eval[q]));
+        }
+    }
+    __syncwarp();
+    const int ch[2] = {a.nd.chA[N], a.nd.chB[N]};
+    for (int c = 0; c < 2; ++c) {
+        const int C = ch[c];
+        if (C < 0) continue;
+        const int sc = a.nd.npiv[C], uc = a.ucnt[C], fc = sc + uc;
+        const int32_t* UC = a.upool + a.ustart[C];
+        for (int i = lane; i < uc; i += 32) rel[i] = front_pos(UC[i], pf, s, Us, nu);
+        __syncwarp();
+        const bool ccx = a.ntype[C] != 0;
+        const double* FC = reinterpret_cast<const double*>(a.fpool) + a.foff[C];
+        const int tot = uc * uc;
+        constexpr int BAT = 8;  // independent loads in flight per lane
+        for (int t0 = lane; t0 < tot; t0 += 32 * BAT) {
+            double2 v[BAT];
+            int pos[BAT];
+#pragma unroll
+            for (int q = 0; q < BAT; ++q) {
+                const int t = t0 + 32 * q;
+                const int bcol = t / uc, i = t - bcol * uc;
+                const bool ok = t < tot && i >= bcol;
+                pos[q] = ok ? pk(rel[i], rel[bcol], f) : -1;
+                const int64_t e = (int64_t)(sc + bcol) * fc + sc + i;
+                v[q] = !ok ? make_double2(0.0, 0.0)
+                           : (ccx ? reinterpret_cast<const double2*>(FC)[e] : make_double2(FC[e], 0.0));
+            }
+#pragma unroll
+            for (int q = 0; q < BAT; ++q)
+                if (pos[q] >= 0) S[pos[q]] = add(S[pos[q]], narrow<T>(v[q]));
+        }
+        __syncwarp();
+    }
+    int bad = 0;
+    for (int k0 = 0; k0 < s; k0 += NB) {
+        const int nb = min(NB, s - k0);
+        {   // diagonal block: lane i keeps row i
+            T r[NB];
+#pragma unroll
+            for (int j = 0; j < NB; ++j) r[j] = (lane < nb && j < nb && j <= lane) ? S[pk(k0 + lane, k0 + j, f)] : zero_t<T>();
+#pragma unroll
+            for (int k = 0; k < NB; ++k) {
+                if (k < nb) {
+                    double d = re(shfl_t(r[k], k));
+                    if (!(d > 0.0) || !isfinite(d)) {
+                        bad = 1;
+                        d = 1.0;
+                    }
+                    d = sqrt(d);
+                    if (lane == k) r[k] = from_c<T>(make_double2(d, 0.0));
+                    else if (lane > k) r[k] = scale(r[k], 1.0 / d);
+#pragma unroll
+                    for (int j = k + 1; j < NB; ++j) {
+                        const T ljk = shfl_t(r[k], j);
+                        if (lane >= j && j < nb) fma_cj(r[j], scale(r[k], -1.0), ljk);
+                    }
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < NB; ++j)
+                if (lane < nb && j <= lane) S[pk(k0 + lane, k0 + j, f)] = r[j];
+        }
+        __syncwarp();
+        for (int rr = k0 + nb + lane; rr < f; rr += 32) {
+            T x[NB];
+#pragma unroll
+            for (int k = 0; k < NB; ++k) x[k] = k < nb ? S[pk(rr, k0 + k, f)] : zero_t<T>();
+#pragma unroll
+            for (int k = 0; k < NB; ++k) {
+                if (k < nb) {
+                    T v = x[k];
+#pragma unroll
+                    for (int j = 0; j < NB; ++j)
+                        if (j < k) fma_cj(v, scale(x[j], -1.0), S[pk(k0 + k, k0 + j, f)]);
+                    x[k] = scale(v, 1.0 / re(S[pk(k0 + k, k0 + k, f)]));
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < NB; ++k)
+                if (k < nb) S[pk(rr, k0 + k, f)] = x[k];
+        }
+        __syncwarp();
+        const int c0 = k0 + nb, m = f - c0;
+        if (m > 0) {
+            const int nt = (m + 3) >> 2;
+            const int ntiles = nt * (nt + 1) / 2;
+            for (int t = lane; t < ntiles; t += 32) {
+                int ti = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
+                while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+                while (ti * (ti + 1) / 2 > t) --ti;
+                const int tj = t - ti * (ti + 1) / 2;
+                const int rb = c0 + 4 * ti, cb = c0 + 4 * tj;
+                T acc[4][4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) acc[i][j] = zero_t<T>();
+                for (int k = 0; k < nb; ++k) {
+                    const T* colk = S + pk(0, k0 + k, f);
+                    T av[4], bv[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) av[i] = rb + i < f ? colk[rb + i] : zero_t<T>();
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) bv[j] = cb + j < f ? colk[cb + j] : zero_t<T>();
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) fma_cj(acc[i][j], av[i], bv[j]);
+                }
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int r = rb + i, c = cb + j;
+                        if (r < f && c < f && r >= c) {
+                            T& d = S[pk(r, c, f)];
+                            d = sub(d, acc[i][j]);
+                        }
+                    }
+            }
+        }
+        __syncwarp();
+    }
+    T* F = front_ptr<T>(a.fpool, a.foff[N]);
+    for (int j = 0; j < f; ++j) {
+        const T* cs = S + pk(0, j, f);
+        for (int i = j + lane; i < f; i += 32) F[(int64_t)i + (int64_t)j * f] = cs[i];
+    }
+    bad = __any_sync(FULL, bad);
+    if (lane == 0 && bad) atomicExch(a.err + a.nd.slot[N], 1);
 }
 
 // Schur update of the U block of every front of a level, one CTA per lower
@@ -1629,7 +1807,7 @@ struct DirectFactor {
     std::vector<int> lvl_maxf, lvl_maxu;
     int ncplx = 0;
     std::vector<int32_t> h_err;
-    double fmas = 0, factor_ms = 0, solve_ms = 0, front_bytes = 0;
+    double fmas = 0, factor_ms = 0, solve_ms = 0, front_bytes = 0, numeric_ms = 0;
     int maxf = 0;
 
     NodeArrays na() {
@@ -1652,7 +1830,7 @@ struct DirectFactor {
 void direct_free(DirectFactor* F) { delete F; }
 
 void direct_stats(const DirectFactor* F, double* o) {
-    for (int i = 0; i < 8; ++i) o[i] = 0;
+    for (int i = 0; i < 9; ++i) o[i] = 0;
     if (!F) return;
     o[0] = F->nnodes;
     o[1] = (double)F->levels.size();
@@ -1662,6 +1840,7 @@ void direct_stats(const DirectFactor* F, double* o) {
     o[5] = F->solve_ms;
     o[6] = F->front_bytes;
     o[7] = (double)F->NU;
+    o[8] = F->numeric_ms;
 }
 
 const std::vector<int32_t>& direct_slot_status(const DirectFactor* F) { return F->h_err; }
@@ -1686,6 +1865,18 @@ int factor_level(DirectFactor* D, FacArgs fa, int l, int type, cudaStream_t s) {
     if (smem > 227 * 1024) {
         set_error("direct solver: front update set too large (%d)", D->lvl_maxu[l]);
         return DIRECT_FALLBACK;
+    }
+    {   // the smallest fronts: one warp each
+        const int maxf_t = D->lst_maxf[2 * l + type];
+        size_t wb = (size_t)maxf_t * (maxf_t + 1) / 2 * tsz + (size_t)(D->lvl_maxu[l] + maxu_child) * 4 + 16;
+        wb = (wb + 15) & ~(size_t)15;
+        if (wb <= WARP_FRONT_BYTES && !getenv("PGCP_DIRECT_NO_WARP")) {
+            const int wpc = (int)std::max<size_t>(1, std::min<size_t>(8, (96 * 1024) / wb));
+            PGCP_TRY(set_smem(k_factor_warp<T>, wb * wpc));
+            k_factor_warp<T><<<(n + wpc - 1) / wpc, 32 * wpc, wb * wpc, s>>>(fa, n, (int)wb);
+            PGCP_LAUNCH_CHECK();
+            return PGCP_OK;
+        }
     }
     {   // fronts that fit in shared memory: the resident kernel
         const int maxf_t = D->lst_maxf[2 * l + type];
@@ -2099,13 +2290,22 @@ int direct_factor(pgcp_batch* b, const DirectInput& in, DirectFactor** out, cuda
     fa.ntype = D->ntype.p;
     fa.list = nullptr;
     fa.err = D->err.p;
+    cudaEvent_t n0, n1;
+    PGCP_TRY_CUDA(cudaEventCreate(&n0));
+    PGCP_TRY_CUDA(cudaEventCreate(&n1));
+    PGCP_TRY_CUDA(cudaEventRecord(n0, s));
     PGCP_TRY(factor_levels(D, fa, s, pt));
+    PGCP_TRY_CUDA(cudaEventRecord(n1, s));
     PGCP_TRY_CUDA(cudaEventRecord(e1, s));
     PGCP_TRY_CUDA(cudaMemcpyAsync(D->h_err.data(), D->err.p, nslot * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     PGCP_TRY_CUDA(cudaStreamSynchronize(s));
     float ms = 0;
     cudaEventElapsedTime(&ms, e0, e1);
     D->factor_ms = ms;
+    cudaEventElapsedTime(&ms, n0, n1);
+    D->numeric_ms = ms;
+    cudaEventDestroy(n0);
+    cudaEventDestroy(n1);
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     *out = guard.release();

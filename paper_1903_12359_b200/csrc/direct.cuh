@@ -42,8 +42,9 @@ int direct_factor(pgcp_batch* b, const DirectInput& in, DirectFactor** out, cuda
 int direct_solve(DirectFactor* F, const double2* b_rows, double2* x_rows, cudaStream_t s);
 void direct_free(DirectFactor* F);
 // last factorization: [nodes, levels, max front, real FMAs of the factorization,
-// factor ms, last solve ms, front storage bytes, unknowns]
-void direct_stats(const DirectFactor* F, double* out8);
+// factor ms (ordering + symbolic + numeric), last solve ms, front storage
+// bytes, unknowns, numeric-phase ms]
+void direct_stats(const DirectFactor* F, double* out9);
 // per-slot pivot failure flags of the last factorization (host copy)
 const std::vector<int32_t>& direct_slot_status(const DirectFactor* F);
 

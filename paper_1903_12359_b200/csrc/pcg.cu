@@ -3531,7 +3531,7 @@ int export_system(pgcp_batch* b, int which, int32_t comp, int64_t* dims, int32_t
 
 
 void solve_summary(const pgcp_batch* b, int which, double* out) {
-    for (int i = 0; i < 18; ++i) out[i] = 0;
+    for (int i = 0; i < 19; ++i) out[i] = 0;
     SolveSystem* S = static_cast<SolveSystem*>(b->sys[which]);
     if (!S) return;
     out[0] = S->kernel_ms;
@@ -3546,9 +3546,9 @@ void solve_summary(const pgcp_batch* b, int which, double* out) {
     out[9] = S->coarse_ms;
     // direct solver: [10] 1, [11] real FMAs of the factorization, [12] factor
     // ms, [13] solve ms (forward + backward), [14] largest front, [15] front
-    // storage bytes, [16] tree nodes, [17] tree levels
+    // storage bytes, [16] tree nodes, [17] tree levels, [18] numeric-phase ms
     if (S->use_direct && S->direct) {
-        double d[8];
+        double d[9];
         direct_stats(S->direct, d);
         out[10] = 1;
         out[11] = d[3];
@@ -3558,6 +3558,7 @@ void solve_summary(const pgcp_batch* b, int which, double* out) {
         out[15] = d[6];
         out[16] = d[0];
         out[17] = d[1];
+        out[18] = d[8];
     }
 }
 

@@ -39,6 +39,22 @@ __global__ void __launch_bounds__(512) k_l2_probe(const int4* __restrict__ buf, 
     if (acc == 0x7f3a5c11) atomicAdd(sink, 1ull);  // keeps the loads live
 }
 
+// FP64 FMA throughput: 8 independent chains per thread, no memory traffic
+__global__ void __launch_bounds__(256) k_fp64_probe(int iters, double seed, double* __restrict__ sink) {
+    double a[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) a[u] = seed + 1e-3 * (threadIdx.x + u);
+    const double m = 0.999999, c = 1e-9;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) a[u] = fma(a[u], m, c);
+    }
+    double t = 0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) t += a[u];
+    if (t == 12345.678) sink[0] = t;  // keeps the chains live
+}
+
 }  // namespace
 }  // namespace pgcp
 
@@ -66,6 +82,22 @@ PGCP_API int pgcp_l2_probe(const void* buf, int64_t bytes, int32_t reps, unsigne
         k_l2_probe<8><<<4 * sms, 512, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
             reinterpret_cast<const int4*>(buf), bytes / 16, reps, sink);
     PGCP_LAUNCH_CHECK();
+    return PGCP_OK;
+}
+
+// FP64 peak probe for the direct solver's roofline: grid 8 CTAs x 256
+// threads per SM, 8 FMA chains per thread; flops = 2 * 8 * iters * threads.
+PGCP_API int pgcp_fp64_probe(int32_t iters, double* sink, int64_t* threads_out, void* stream) {
+    if (iters < 1 || !sink || !threads_out) {
+        set_error("pgcp_fp64_probe: invalid arguments");
+        return PGCP_E_INVALID;
+    }
+    int dev = 0, sms = 148;
+    PGCP_TRY_CUDA(cudaGetDevice(&dev));
+    PGCP_TRY_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    k_fp64_probe<<<8 * sms, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(iters, 1.0, sink);
+    PGCP_LAUNCH_CHECK();
+    *threads_out = (int64_t)8 * sms * 256;
     return PGCP_OK;
 }
 

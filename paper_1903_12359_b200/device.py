@@ -299,14 +299,15 @@ class DeviceBatch:
     def last_solve(self, which):
         """PCG kernel time (CUDA events), iterations and compulsory bytes of
         the last flatten (0) / harmonic (1) solve."""
-        out = (ctypes.c_double * 18)()
-        nat.check(nat.lib().pgcp_batch_last_solve(self.h, which, out, 18))
+        out = (ctypes.c_double * 19)()
+        nat.check(nat.lib().pgcp_batch_last_solve(self.h, which, out, 19))
         r = {"kernel_ms": out[0], "iters_sum": out[1], "iters_max": out[2], "bytes": out[3],
              "stored_entries": out[4], "rows": out[5], "cluster": int(out[6]), "submeshes": int(out[7]),
              "ref_bytes": out[8], "coarse_ms": out[9], "solver": "direct" if out[10] else "pcg"}
         if out[10]:
             r.update({"fmas": out[11], "factor_ms": out[12], "solve_ms": out[13], "max_front": int(out[14]),
-                      "front_bytes": out[15], "nodes": int(out[16]), "levels": int(out[17])})
+                      "front_bytes": out[15], "nodes": int(out[16]), "levels": int(out[17]),
+                      "numeric_ms": out[18]})
         return r
 
     def energy(self, z):

@@ -31,7 +31,7 @@ def test_library_exports_every_declared_symbol():
     assert len(names) >= 10
     missing = [n for n in names if not hasattr(lib, n)]
     assert not missing, missing
-    assert lib.pgcp_abi_version() == 1
+    assert lib.pgcp_abi_version() == 2
 
 
 def test_product_never_imports_oracle():
