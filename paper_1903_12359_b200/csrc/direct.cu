@@ -822,9 +822,9 @@ __device__ __forceinline__ void diag_factor(T* Ld, int nb, int* bad) {
                 if (lane == 0) *bad = 1;
                 d = 1.0;
             }
-            d = sqrt(d);
-            if (lane == k) r[k] = from_c<T>(make_double2(d, 0.0));
-            else if (lane > k) r[k] = scale(r[k], 1.0 / d);
+            const double inv = rsqrt(d);  // one reciprocal square root per pivot
+            if (lane == k) r[k] = from_c<T>(make_double2(d * inv, 0.0));
+            else if (lane > k) r[k] = scale(r[k], inv);
 #pragma unroll
             for (int j = k + 1; j < LDB; ++j) {
                 const T ljk = shfl_t(r[k], j);
@@ -839,6 +839,34 @@ __device__ __forceinline__ void diag_factor(T* Ld, int nb, int* bad) {
     __syncwarp();
 }
 
+// the same by the whole CTA in shared memory (no register arrays: for
+// kernels whose register budget is set by other work)
+template <class T, int LDB, int NTH>
+__device__ __forceinline__ void diag_factor_cta(T* Ld, int nb, int* bad) {
+    __shared__ double sinv;
+    for (int k = 0; k < nb; ++k) {
+        if (threadIdx.x == 0) {
+            double d = re(Ld[k + k * LDB]);
+            if (!(d > 0.0) || !isfinite(d)) {
+                *bad = 1;
+                d = 1.0;
+            }
+            const double inv = rsqrt(d);
+            Ld[k + k * LDB] = from_c<T>(make_double2(d * inv, 0.0));
+            sinv = inv;
+        }
+        __syncthreads();
+        for (int i = k + 1 + threadIdx.x; i < nb; i += NTH) Ld[i + k * LDB] = scale(Ld[i + k * LDB], sinv);
+        __syncthreads();
+        const int m = nb - k - 1;
+        for (int t = threadIdx.x; t < m * m; t += NTH) {
+            const int j = k + 1 + t / m, i = k + 1 + t % m;
+            if (i >= j) fma_cj(Ld[i + j * LDB], scale(Ld[i + k * LDB], -1.0), Ld[j + k * LDB]);
+        }
+        __syncthreads();
+    }
+}
+
 constexpr int FAC_SCHUR_INLINE = 1;  // k_factor: Schur update of the U block in this CTA
 constexpr int FAC_ASSEMBLE_ONLY = 2; // k_factor: assembly only (the level-synchronous panel follows)
 
@@ -851,6 +879,7 @@ __global__ void __launch_bounds__(DNT, sizeof(T) == 8 ? 8 : 4) k_factor(FacArgs 
     T* Ld = Bs + KC * TC;                                // NB x NB, column-major
     int32_t* Us = reinterpret_cast<int32_t*>(Ld + NB * NB);  // my U list, then a child's rel map
     __shared__ int bad;
+    __shared__ double dinv[NB];
     const int N = a.list[blockIdx.x];
     const int s = a.nd.npiv[N];
     const int nu = a.ucnt[N];
@@ -924,6 +953,7 @@ __global__ void __launch_bounds__(DNT, sizeof(T) == 8 ? 8 : 4) k_factor(FacArgs 
                 if (i < nb && j < nb && i >= j) F[(int64_t)(k0 + i) + (int64_t)(k0 + j) * f] = Ld[idx];
             }
         }
+        if (threadIdx.x < nb) dinv[threadIdx.x] = 1.0 / re(Ld[threadIdx.x + threadIdx.x * NB]);
         __syncthreads();
         // rows below the block: x L^H = row -> forward substitution per row
         for (int r = k0 + nb + threadIdx.x; r < f; r += DNT) {
@@ -937,7 +967,7 @@ __global__ void __launch_bounds__(DNT, sizeof(T) == 8 ? 8 : 4) k_factor(FacArgs 
 #pragma unroll
                     for (int j = 0; j < NB; ++j)
                         if (j < k) fma_cj(v, scale(x[j], -1.0), Ld[k + j * NB]);
-                    x[k] = scale(v, 1.0 / re(Ld[k + k * NB]));
+                    x[k] = scale(v, dinv[k]);
                 }
             }
 #pragma unroll
@@ -969,6 +999,7 @@ constexpr size_t WARP_FRONT_BYTES = 40 * 1024; // k_factor_warp: per warp (packe
 template <class T>
 __global__ void __launch_bounds__(DNT) k_pdiag(FacArgs a, int k0, int phase) {
     __shared__ __align__(16) T Ld[PB * PB];
+    __shared__ double dinvp[PB];
     __shared__ int bad;
     const int N = a.list[blockIdx.x];
     const int s = a.nd.npiv[N];
@@ -995,6 +1026,8 @@ __global__ void __launch_bounds__(DNT) k_pdiag(FacArgs a, int k0, int phase) {
         return;
     }
     __syncthreads();
+    if (threadIdx.x < nb) dinvp[threadIdx.x] = 1.0 / re(Ld[threadIdx.x + threadIdx.x * PB]);
+    __syncthreads();
     // TRSM of my row in two halves of 16: a dependency chain per half, the
     // coupling between the halves as independent multiply-adds
     const int r = r0 + threadIdx.x;
@@ -1008,7 +1041,7 @@ __global__ void __launch_bounds__(DNT) k_pdiag(FacArgs a, int k0, int phase) {
             T v = x[k];
 #pragma unroll
             for (int j = 0; j < k; ++j) fma_cj(v, scale(x[j], -1.0), Ld[k + j * PB]);
-            x[k] = k < nb ? scale(v, 1.0 / re(Ld[k + k * PB])) : zero_t<T>();
+            x[k] = k < nb ? scale(v, dinvp[k]) : zero_t<T>();
         }
 #pragma unroll
         for (int k = 0; k < 16; ++k)
@@ -1025,7 +1058,7 @@ __global__ void __launch_bounds__(DNT) k_pdiag(FacArgs a, int k0, int phase) {
                 T v = y[k];
 #pragma unroll
                 for (int j = 0; j < k; ++j) fma_cj(v, scale(y[j], -1.0), Ld[(16 + k) + (16 + j) * PB]);
-                y[k] = 16 + k < nb ? scale(v, 1.0 / re(Ld[(16 + k) + (16 + k) * PB])) : zero_t<T>();
+                y[k] = 16 + k < nb ? scale(v, dinvp[16 + k]) : zero_t<T>();
             }
 #pragma unroll
             for (int k = 0; k < 16; ++k)
@@ -1115,7 +1148,8 @@ __host__ __device__ inline int pupd_tiles(int s, int f, int c0) {
 template <class T>
 __global__ void __launch_bounds__(DNT, 4) k_pupd(FacArgs a, int k0) {
     __shared__ __align__(16) T As[KC * TR];
-    __shared__ __align__(16) T Bs[KC * TC];
+    __shared__ __align__(16) T Bs[KC * TC];  // then the next diagonal block (PB x PB <= KC x TC)
+    __shared__ int bad;
     const int N = a.list[blockIdx.x];
     const int s = a.nd.npiv[N];
     const int nb = min(PB, s - k0);
@@ -1132,6 +1166,24 @@ __global__ void __launch_bounds__(DNT, 4) k_pupd(FacArgs a, int k0) {
     if (tj >= s) return;
     T* F = front_ptr<T>(a.fpool, a.foff[N]);
     tile_one<T>(F, f, tj + TR * p, tj, f, s, k0, k0 + nb, As, Bs);
+    if (tj != c0 || p != 0) return;
+    // this tile holds the next diagonal block: factor it now (the next
+    // step's TRSM reads it; no other CTA of this launch touches it)
+    __syncthreads();
+    const int nb2 = min(PB, s - c0);
+    T* Ld = Bs;
+    if (threadIdx.x == 0) bad = 0;
+    for (int idx = threadIdx.x; idx < PB * PB; idx += DNT) {
+        const int i = idx % PB, j = idx / PB;
+        Ld[idx] = (i < nb2 && j < nb2 && i >= j) ? F[(int64_t)(c0 + i) + (int64_t)(c0 + j) * f] : zero_t<T>();
+    }
+    __syncthreads();
+    diag_factor_cta<T, PB, DNT>(Ld, nb2, &bad);
+    for (int idx = threadIdx.x; idx < PB * PB; idx += DNT) {
+        const int i = idx % PB, j = idx / PB;
+        if (i < nb2 && j < nb2 && i >= j) F[(int64_t)(c0 + i) + (int64_t)(c0 + j) * f] = Ld[idx];
+    }
+    if (threadIdx.x == 0 && bad) atomicExch(a.err + a.nd.slot[N], 1);
 }
 
 // Small fronts, resident in shared memory for the whole factorization:
@@ -1144,6 +1196,7 @@ template <class T>
 __global__ void __launch_bounds__(DNT) k_factor_sm(FacArgs a) {
     extern __shared__ __align__(16) unsigned char dsm[];
     __shared__ int bad;
+    __shared__ double dsm_inv[NB];
     const int N = a.list[blockIdx.x];
     const int s = a.nd.npiv[N];
     const int nu = a.ucnt[N];
@@ -1203,9 +1256,9 @@ __global__ void __launch_bounds__(DNT) k_factor_sm(FacArgs a) {
                         if (lane == 0) bad = 1;
                         d = 1.0;
                     }
-                    d = sqrt(d);
-                    if (lane == k) r[k] = from_c<T>(make_double2(d, 0.0));
-                    else if (lane > k) r[k] = scale(r[k], 1.0 / d);
+                    const double inv = rsqrt(d);
+                    if (lane == k) r[k] = from_c<T>(make_double2(d * inv, 0.0));
+                    else if (lane > k) r[k] = scale(r[k], inv);
 #pragma unroll
                     for (int j = k + 1; j < NB; ++j) {
                         const T ljk = shfl_t(r[k], j);
@@ -1217,6 +1270,7 @@ __global__ void __launch_bounds__(DNT) k_factor_sm(FacArgs a) {
             for (int j = 0; j < NB; ++j)
                 if (lane < nb && j <= lane) S[(k0 + lane) + (k0 + j) * f] = r[j];
         }
+        if (threadIdx.x < nb) dsm_inv[threadIdx.x] = 1.0 / re(S[(k0 + threadIdx.x) + (k0 + threadIdx.x) * f]);
         __syncthreads();
         for (int rr = k0 + nb + threadIdx.x; rr < f; rr += DNT) {
             T x[NB];
@@ -1229,7 +1283,7 @@ __global__ void __launch_bounds__(DNT) k_factor_sm(FacArgs a) {
 #pragma unroll
                     for (int j = 0; j < NB; ++j)
                         if (j < k) fma_cj(v, scale(x[j], -1.0), S[(k0 + k) + (k0 + j) * f]);
-                    x[k] = scale(v, 1.0 / re(S[(k0 + k) + (k0 + k) * f]));
+                    x[k] = scale(v, dsm_inv[k]);
                 }
             }
 #pragma unroll
@@ -1365,9 +1419,9 @@ __global__ void __launch_bounds__(256) k_factor_warp(FacArgs a, int nfront, int 
                         bad = 1;
                         d = 1.0;
                     }
-                    d = sqrt(d);
-                    if (lane == k) r[k] = from_c<T>(make_double2(d, 0.0));
-                    else if (lane > k) r[k] = scale(r[k], 1.0 / d);
+                    const double inv = rsqrt(d);
+                    if (lane == k) r[k] = from_c<T>(make_double2(d * inv, 0.0));
+                    else if (lane > k) r[k] = scale(r[k], inv);
 #pragma unroll
                     for (int j = k + 1; j < NB; ++j) {
                         const T ljk = shfl_t(r[k], j);
@@ -1380,6 +1434,9 @@ __global__ void __launch_bounds__(256) k_factor_warp(FacArgs a, int nfront, int 
                 if (lane < nb && j <= lane) S[pk(k0 + lane, k0 + j, f)] = r[j];
         }
         __syncwarp();
+        double di[NB];
+#pragma unroll
+        for (int k = 0; k < NB; ++k) di[k] = k < nb ? 1.0 / re(S[pk(k0 + k, k0 + k, f)]) : 0.0;
         for (int rr = k0 + nb + lane; rr < f; rr += 32) {
             T x[NB];
 #pragma unroll
@@ -1391,7 +1448,7 @@ __global__ void __launch_bounds__(256) k_factor_warp(FacArgs a, int nfront, int 
 #pragma unroll
                     for (int j = 0; j < NB; ++j)
                         if (j < k) fma_cj(v, scale(x[j], -1.0), S[pk(k0 + k, k0 + j, f)]);
-                    x[k] = scale(v, 1.0 / re(S[pk(k0 + k, k0 + k, f)]));
+                    x[k] = scale(v, di[k]);
                 }
             }
 #pragma unroll
@@ -1921,8 +1978,10 @@ int factor_level(DirectFactor* D, FacArgs fa, int l, int type, cudaStream_t s) {
                 chunks = std::max(chunks, (f - k0 - nb + DNT - 1) / DNT);
                 tiles = std::max(tiles, pupd_tiles(sp, f, k0 + nb));
             }
-            k_pdiag<T><<<dim3(n, 1), DNT, xs, s>>>(fa, k0, 0);
-            PGCP_LAUNCH_CHECK();
+            if (k0 == 0) {  // later diagonal blocks are factored by the previous k_pupd
+                k_pdiag<T><<<dim3(n, 1), DNT, xs, s>>>(fa, k0, 0);
+                PGCP_LAUNCH_CHECK();
+            }
             k_pdiag<T><<<dim3(n, chunks), DNT, xs, s>>>(fa, k0, 1);
             PGCP_LAUNCH_CHECK();
             if (tiles > 0) {

@@ -263,6 +263,11 @@ def parameterize(mesh, cuts=None, mode="free", workers=1, seed=0, mobius_area=Fa
     hi.wait_stream(cur)
     lo.wait_stream(cur)
     overlap_prep = welds and os.environ.get("PGCP_OVERLAP_HPREP", "1") != "0"
+    # where the harmonic preparation overlaps: the flatten (default) or, with
+    # PGCP_HPREP_AT=weld, the weld (measured slower: the preparation's
+    # per-level host synchronisations queue behind the weld's kernels)
+    prep_at_weld = overlap_prep and os.environ.get("PGCP_HPREP_AT", "flatten") == "weld"
+    hprep = {}
 
     def _flatten():
         try:
@@ -283,7 +288,7 @@ def parameterize(mesh, cuts=None, mode="free", workers=1, seed=0, mobius_area=Fa
             plan = WeldPlan(cycles, steps, mesh.n_vertices)
             loop_gid_host = (voff[plan.slot_sub] + loop_local).astype(np.int32)
         timings["plan (overlapped)"] = time.perf_counter() - t_plan
-        if overlap_prep:
+        if overlap_prep and not prep_at_weld:
             t_h = time.perf_counter()
             with torch.cuda.stream(lo):
                 loop_gid = torch.as_tensor(loop_gid_host).to(dev)
@@ -309,22 +314,49 @@ def parameterize(mesh, cuts=None, mode="free", workers=1, seed=0, mobius_area=Fa
     else:
         # ---- welding on tracked boundary values ---------------------------------
         clk.start()
-        if not overlap_prep:
+        if not overlap_prep or prep_at_weld:
             loop_gid = torch.as_tensor(loop_gid_host).to(dev)
-        if own is None:
-            tv = torch.empty(len(plan.slot_parent), dtype=torch.complex128, device=dev)
-            nat.check(nat.lib().pgcp_gather_complex(_ptr(z0), _ptr(loop_gid), _ptr(tv), tv.numel(), _stream()))
-        else:  # the one exchange: all-gather of every rank's boundary-loop values
-            own_slots, tv = _exchange_boundary(shard, plan, loop_gid_host, z0, dev)
-        out = None
-        if len(steps):
-            out, _ = run_schedule(tv, plan.info, plan.src, plan.wb_off, plan.wb, cfg.hard_tol)
-            report.seam_residuals = [float(x) for x in out[:, 1]]
+        hworker = None
+        if prep_at_weld:
+            lo.wait_stream(cur)
+
+            def _hprep():
+                try:
+                    torch.cuda.set_device(dev)
+                    t_h = time.perf_counter()
+                    with torch.cuda.stream(lo):
+                        batch.harmonic_prepare(loop_gid, comps=own, rtol=cfg.rtol, cluster=cfg.cluster, stream=lo)
+                    hprep["t"] = time.perf_counter() - t_h
+                except BaseException as exc:
+                    hprep["err"] = exc
+
+            hworker = threading.Thread(target=_hprep, name="pgcp-harmonic-prepare")
+            hworker.start()
+        try:
+            if own is None:
+                tv = torch.empty(len(plan.slot_parent), dtype=torch.complex128, device=dev)
+                nat.check(nat.lib().pgcp_gather_complex(_ptr(z0), _ptr(loop_gid), _ptr(tv), tv.numel(), _stream()))
+            else:  # the one exchange: all-gather of every rank's boundary-loop values
+                own_slots, tv = _exchange_boundary(shard, plan, loop_gid_host, z0, dev)
+            out = None
+            if len(steps):
+                out, _ = run_schedule(tv, plan.info, plan.src, plan.wb_off, plan.wb, cfg.hard_tol)
+                report.seam_residuals = [float(x) for x in out[:, 1]]
+        except BaseException:
+            if hworker is not None:  # never leave the preparation running on the batch
+                hworker.join()
+            raise
         exterior = []
         if len(steps) and steps[-1].closed:
             A, B = plan.exterior_candidates
             exterior = B if out[-1, 2] > 0 else A
         clk.stop("weld")
+        if hworker is not None:
+            hworker.join()
+            cur.wait_stream(lo)
+            if "err" in hprep:
+                raise hprep["err"]
+            timings["harmonic prepare (overlapped)"] = hprep["t"]
 
         if mode == "disk":
             clk.start()
