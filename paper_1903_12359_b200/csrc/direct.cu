@@ -728,41 +728,51 @@ __device__ __forceinline__ void assemble_entries(T* S, int f, int64_t pf, int s,
 
 // One TR x TC tile (rows [ti, ti+TR) below rlim, columns [tj, tj+TC) below
 // clim, lower part r >= c only): F[r][c] -= sum_{k in [kb, ke)} F[r][k]
-// conj(F[c][k]), k staged in chunks of KC through shared memory; 4x4
-// outputs per thread.
+// conj(F[c][k]), k staged in chunks of KC through shared memory (the next
+// chunk's global loads issued before the current chunk's multiply-adds).
+// Thread (ty, tx) owns rows ty + 8 i and columns tx + 16 j: for a fixed
+// (i, j) a warp reads consecutive shared-memory entries (no bank conflicts).
 template <class T>
 __device__ __forceinline__ void tile_one(T* F, int f, int ti, int tj, int rlim, int clim, int kb, int ke, T* As,
                                          T* Bs) {
     const int t = threadIdx.x;
     const int ty = t >> 4, tx = t & 15;
+    constexpr int QA = (TR * KC) / DNT, QB = (TC * KC) / DNT;
     T acc[4][4];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j] = zero_t<T>();
+    T ra[QA], rb[QB];
+    auto fetch = [&](int kc) {
+#pragma unroll
+        for (int q = 0; q < QA; ++q) {
+            const int idx = t + q * DNT;
+            const int r = idx % TR, k = kc + idx / TR;
+            ra[q] = (k < ke && ti + r < rlim) ? F[(int64_t)(ti + r) + (int64_t)k * f] : zero_t<T>();
+        }
+#pragma unroll
+        for (int q = 0; q < QB; ++q) {
+            const int idx = t + q * DNT;
+            const int r = idx % TC, k = kc + idx / TC;
+            rb[q] = (k < ke && tj + r < clim) ? F[(int64_t)(tj + r) + (int64_t)k * f] : zero_t<T>();
+        }
+    };
+    if (kb < ke) fetch(kb);
     for (int kc = kb; kc < ke; kc += KC) {
 #pragma unroll
-        for (int q = 0; q < (TR * KC) / DNT; ++q) {
-            const int idx = t + q * DNT;
-            const int r = idx % TR, kk = idx / TR;
-            const int k = kc + kk;
-            As[kk * TR + r] = (k < ke && ti + r < rlim) ? F[(int64_t)(ti + r) + (int64_t)k * f] : zero_t<T>();
-        }
+        for (int q = 0; q < QA; ++q) As[t + q * DNT] = ra[q];
 #pragma unroll
-        for (int q = 0; q < (TC * KC) / DNT; ++q) {
-            const int idx = t + q * DNT;
-            const int r = idx % TC, kk = idx / TC;
-            const int k = kc + kk;
-            Bs[kk * TC + r] = (k < ke && tj + r < clim) ? F[(int64_t)(tj + r) + (int64_t)k * f] : zero_t<T>();
-        }
+        for (int q = 0; q < QB; ++q) Bs[t + q * DNT] = rb[q];
         __syncthreads();
+        if (kc + KC < ke) fetch(kc + KC);
 #pragma unroll 4
         for (int kk = 0; kk < KC; ++kk) {
             T av[4], bv[4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) av[i] = As[kk * TR + ty * 4 + i];
+            for (int i = 0; i < 4; ++i) av[i] = As[kk * TR + ty + 8 * i];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) bv[j] = Bs[kk * TC + tx * 4 + j];
+            for (int j = 0; j < 4; ++j) bv[j] = Bs[kk * TC + tx + 16 * j];
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -772,11 +782,11 @@ __device__ __forceinline__ void tile_one(T* F, int f, int ti, int tj, int rlim, 
     }
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-        const int r = ti + ty * 4 + i;
+        const int r = ti + ty + 8 * i;
         if (r >= rlim) continue;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            const int c = tj + tx * 4 + j;
+            const int c = tj + tx + 16 * j;
             if (c >= clim || r < c) continue;
             T& dst = F[(int64_t)r + (int64_t)c * f];
             dst = sub(dst, acc[i][j]);
