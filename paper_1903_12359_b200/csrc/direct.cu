@@ -1561,12 +1561,15 @@ struct SolArgs {
 
 constexpr int SB = 32;  // pivots per block of the blocked substitutions
 
+// Forward step of front N (CTA-wide): gather the pivots' right-hand side and
+// the children's partial sums (fixed order; L2 loads: written by other CTAs
+// of the same persistent launch), blocked substitution with L_PP (one warp
+// per 32-pivot diagonal block, shuffles), GEMV for the rows below; W[N] and
+// the pivots' y in X.
 template <class T>
-__global__ void __launch_bounds__(DNT) k_fwd(SolArgs a) {
-    extern __shared__ __align__(16) unsigned char dsm[];
-    __shared__ __align__(16) T Lb[SB * SB];   // diagonal block, column-major
+__device__ void fwd_front(const SolArgs& a, int N, unsigned char* dsm, T* Lb) {
     double2* w = reinterpret_cast<double2*>(dsm);
-    const int N = a.list[blockIdx.x];
+    __shared__ double dvi[SB];
     const int s = a.nd.npiv[N];
     const int nu = a.ucnt[N];
     const int f = s + nu;
@@ -1585,7 +1588,7 @@ __global__ void __launch_bounds__(DNT) k_fwd(SolArgs a) {
         const double2* WC = a.W + a.woff[C] + sc;
         for (int i = threadIdx.x; i < uc; i += DNT) {
             const int p = front_pos(UC[i], pf, s, Us, nu);
-            const double2 v = WC[i];
+            const double2 v = __ldcg(WC + i);
             w[p].x += v.x;
             w[p].y += v.y;
         }
@@ -1600,12 +1603,13 @@ __global__ void __launch_bounds__(DNT) k_fwd(SolArgs a) {
             Lb[idx] = (i < nb && j < nb && i >= j) ? F[(int64_t)(k0 + i) + (int64_t)(k0 + j) * f] : zero_t<T>();
         }
         __syncthreads();
+        if (threadIdx.x < nb) dvi[threadIdx.x] = 1.0 / re(Lb[threadIdx.x + threadIdx.x * SB]);
+        __syncthreads();
         if (warp == 0) {  // lane i holds w[k0 + i]
             double2 wi = lane < nb ? w[k0 + lane] : make_double2(0.0, 0.0);
             for (int k = 0; k < nb; ++k) {
                 const double2 wk = make_double2(__shfl_sync(FULL, wi.x, k), __shfl_sync(FULL, wi.y, k));
-                const double d = re(Lb[k + k * SB]);
-                const double2 yk = make_double2(wk.x / d, wk.y / d);
+                const double2 yk = make_double2(wk.x * dvi[k], wk.y * dvi[k]);
                 if (lane == k) {
                     wi = yk;
                 } else if (lane > k && lane < nb) {
@@ -1635,12 +1639,12 @@ __global__ void __launch_bounds__(DNT) k_fwd(SolArgs a) {
     }
 }
 
+// Backward step of front N: t = y_P - L_UP^H x_U (one warp per pivot column;
+// the ancestors' x through L2), then the blocked back substitution with L_PP^H.
 template <class T>
-__global__ void __launch_bounds__(DNT) k_bwd(SolArgs a) {
-    extern __shared__ __align__(16) unsigned char dsm[];
-    __shared__ __align__(16) T Lb[SB * SB];
+__device__ void bwd_front(const SolArgs& a, int N, unsigned char* dsm, T* Lb) {
     double2* t = reinterpret_cast<double2*>(dsm);   // [s] right-hand sides, then x
-    const int N = a.list[blockIdx.x];
+    __shared__ double dvi[SB];
     const int s = a.nd.npiv[N];
     const int nu = a.ucnt[N];
     const int f = s + nu;
@@ -1648,11 +1652,10 @@ __global__ void __launch_bounds__(DNT) k_bwd(SolArgs a) {
     const int64_t pf = a.pfirst[N];
     double2* xu = t + s;                            // [nu] ancestors' x
     const int32_t* U = a.upool + a.ustart[N];
-    for (int i = threadIdx.x; i < nu; i += DNT) xu[i] = a.X[U[i]];
+    for (int i = threadIdx.x; i < nu; i += DNT) xu[i] = __ldcg(a.X + U[i]);
     __syncthreads();
     const T* F = front_ptr<T>(a.fpool, a.foff[N]);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    // t_k = y_k - sum_a conj(L[s+a][k]) x_U[a]   (one warp per pivot column)
     for (int k = warp; k < s; k += DNT / 32) {
         const T* colk = F + (int64_t)k * f + s;
         double sx = 0.0, sy = 0.0;
@@ -1669,7 +1672,6 @@ __global__ void __launch_bounds__(DNT) k_bwd(SolArgs a) {
         }
     }
     __syncthreads();
-    // blocked back substitution with L_PP^H, last block first
     for (int k1 = s; k1 > 0; k1 -= SB) {
         const int k0 = max(0, k1 - SB), nb = k1 - k0;
         for (int idx = threadIdx.x; idx < SB * SB; idx += DNT) {
@@ -1677,12 +1679,13 @@ __global__ void __launch_bounds__(DNT) k_bwd(SolArgs a) {
             Lb[idx] = (i < nb && j < nb && i >= j) ? F[(int64_t)(k0 + i) + (int64_t)(k0 + j) * f] : zero_t<T>();
         }
         __syncthreads();
+        if (threadIdx.x < nb) dvi[threadIdx.x] = 1.0 / re(Lb[threadIdx.x + threadIdx.x * SB]);
+        __syncthreads();
         if (warp == 0) {  // lane i holds t[k0 + i]
             double2 ti = lane < nb ? t[k0 + lane] : make_double2(0.0, 0.0);
             for (int k = nb - 1; k >= 0; --k) {
                 const double2 tk = make_double2(__shfl_sync(FULL, ti.x, k), __shfl_sync(FULL, ti.y, k));
-                const double d = re(Lb[k + k * SB]);
-                const double2 xk = make_double2(tk.x / d, tk.y / d);
+                const double2 xk = make_double2(tk.x * dvi[k], tk.y * dvi[k]);
                 if (lane == k) {
                     ti = xk;
                 } else if (lane < k) {  // t_i -= conj(L[k][i]) x_k
@@ -1707,6 +1710,88 @@ __global__ void __launch_bounds__(DNT) k_bwd(SolArgs a) {
         __syncthreads();
     }
     for (int k = threadIdx.x; k < s; k += DNT) a.X[pf + k] = t[k];
+}
+
+// per-level launches (PGCP_DIRECT_PERSIST=0)
+template <class T>
+__global__ void __launch_bounds__(DNT) k_fwd(SolArgs a) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    __shared__ __align__(16) T Lb[SB * SB];
+    fwd_front<T>(a, a.list[blockIdx.x], dsm, Lb);
+}
+template <class T>
+__global__ void __launch_bounds__(DNT) k_bwd(SolArgs a) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    __shared__ __align__(16) T Lb[SB * SB];
+    bwd_front<T>(a, a.list[blockIdx.x], dsm, Lb);
+}
+
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_gpu(int* p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+// spin until *flag != 0; gives up after 2 s (flags the solve instead of hanging)
+__device__ __forceinline__ void wait_flag(const int* flag, int* err) {
+    if (ld_acquire_gpu(flag)) return;
+    const unsigned long long t0 = gtimer();
+    while (!ld_acquire_gpu(flag)) {
+        __nanosleep(64);
+        if (gtimer() - t0 > 2000000000ull) {
+            atomicExch(err, 1);
+            return;
+        }
+    }
+}
+
+// One persistent launch per sweep. CTAs draw fronts from a ticket counter in
+// `order` (leaves first for the forward sweep, read backwards for the
+// backward one) and wait for the fronts they depend on (children / parent),
+// whose tickets are smaller and so held by CTAs already running: no level
+// barriers, no per-level launches, real and complex fronts in one launch.
+__global__ void __launch_bounds__(DNT) k_solve_pers(SolArgs a, const int32_t* __restrict__ order, int nn,
+                                                    int* __restrict__ done, int* ticket,
+                                                    const int8_t* __restrict__ ntype, int backward) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    __shared__ __align__(16) double2 Lb[SB * SB];
+    __shared__ int sq;
+    for (;;) {
+        if (threadIdx.x == 0) sq = atomicAdd(ticket, 1);
+        __syncthreads();
+        const int q = sq;
+        __syncthreads();
+        if (q >= nn) return;
+        const int N = backward ? order[nn - 1 - q] : order[q];
+        if (threadIdx.x == 0) {
+            if (backward) {
+                const int P = a.nd.parent[N];
+                if (P >= 0) wait_flag(done + P, ticket - 1);
+            } else {
+                const int A = a.nd.chA[N], B = a.nd.chB[N];
+                if (A >= 0) wait_flag(done + A, ticket - 1);
+                if (B >= 0) wait_flag(done + B, ticket - 1);
+            }
+        }
+        __syncthreads();
+        if (backward) {
+            if (ntype[N]) bwd_front<double2>(a, N, dsm, Lb);
+            else bwd_front<double>(a, N, dsm, reinterpret_cast<double*>(Lb));
+        } else {
+            if (ntype[N]) fwd_front<double2>(a, N, dsm, Lb);
+            else fwd_front<double>(a, N, dsm, reinterpret_cast<double*>(Lb));
+        }
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) st_release_gpu(done + N, 1);
+    }
 }
 
 __global__ void k_d_scatter(int64_t NU, const int32_t* __restrict__ urow, const int32_t* __restrict__ elim,
@@ -1865,6 +1950,8 @@ struct DirectFactor {
     DevBuf<double2> X;
     DevBuf<int32_t> err;
     DevBuf<int8_t> ntype;
+    DevBuf<int32_t> order;   // fronts deepest level first (the persistent solves' ticket order)
+    DevBuf<int32_t> sync;    // [0] ticket counter, [1 + N] front N done
     // fronts per (level, type): nlist[lst_off[2 l + t], lst_off[2 l + t + 1])
     DevBuf<int32_t> nlist;
     std::vector<int64_t> lst_off;
@@ -2318,6 +2405,17 @@ int direct_factor(pgcp_batch* b, const DirectInput& in, DirectFactor** out, cuda
     D->h_fsz = hf;
     PGCP_TRY(D->nlist.alloc(nn, s));
     PGCP_TRY_CUDA(cudaMemcpyAsync(D->nlist.p, hl.data(), nn * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    {   // deepest level first: every front after its children
+        std::vector<int32_t> ord;
+        ord.reserve(nn);
+        for (int l = (int)D->levels.size() - 1; l >= 0; --l)
+            for (int N = D->levels[l].first; N < D->levels[l].second; ++N) ord.push_back(N);
+        PGCP_TRY(D->order.alloc(nn, s));
+        PGCP_TRY_CUDA(cudaMemcpyAsync(D->order.p, ord.data(), nn * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+        PGCP_TRY(D->sync.alloc(nn + 2, s));
+        PGCP_TRY(D->sync.zero(s));
+        PGCP_TRY_CUDA(cudaStreamSynchronize(s));  // ord is a local
+    }
     if (pt.on) {
         for (size_t l = 0; l < D->levels.size(); ++l) {
             double lf = 0;
@@ -2430,20 +2528,50 @@ int direct_solve(DirectFactor* D, const double2* b_rows, double2* x_rows, cudaSt
         PGCP_LAUNCH_CHECK();
         return PGCP_OK;
     };
-    for (int l = L - 1; l >= 0; --l) {
-        PGCP_TRY(launch(true, l, 0));
-        PGCP_TRY(launch(true, l, 1));
+    const char* ep = getenv("PGCP_DIRECT_PERSIST");
+    if (!(ep && atoi(ep) == 0)) {  // one persistent, dependency-driven launch per sweep
+        int maxf = 0, maxu = 0;
+        for (int l = 0; l < L; ++l) {
+            maxf = std::max(maxf, D->lvl_maxf[l]);
+            maxu = std::max(maxu, D->lvl_maxu[l]);
+        }
+        const size_t smem = (size_t)maxf * sizeof(double2) + (size_t)maxu * 4 + 16;
+        PGCP_TRY(set_smem(k_solve_pers, smem));
+        int per_sm = 1, dev = 0, sms = 148;
+        PGCP_TRY_CUDA(cudaGetDevice(&dev));
+        PGCP_TRY_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        PGCP_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve_pers, DNT, smem));
+        const int grid = std::max(1, std::min(per_sm * sms, D->nnodes));
+        for (int bwd = 0; bwd < 2; ++bwd) {
+            PGCP_TRY_CUDA(cudaMemsetAsync(D->sync.p + 1, 0, (size_t)(D->nnodes + 1) * sizeof(int), s));
+            k_solve_pers<<<grid, DNT, smem, s>>>(a, D->order.p, D->nnodes, D->sync.p + 2, D->sync.p + 1, D->ntype.p, bwd);
+            PGCP_LAUNCH_CHECK();
+            pt.mark(bwd ? "backward" : "forward");
+        }
+    } else {
+        for (int l = L - 1; l >= 0; --l) {
+            PGCP_TRY(launch(true, l, 0));
+            PGCP_TRY(launch(true, l, 1));
+        }
+        pt.mark("forward");
+        for (int l = 0; l < L; ++l) {
+            PGCP_TRY(launch(false, l, 0));
+            PGCP_TRY(launch(false, l, 1));
+        }
+        pt.mark("backward");
     }
-    pt.mark("forward");
-    for (int l = 0; l < L; ++l) {
-        PGCP_TRY(launch(false, l, 0));
-        PGCP_TRY(launch(false, l, 1));
-    }
-    pt.mark("backward");
     k_d_scatter<<<grid_for(D->NU, 256), 256, 0, s>>>(D->NU, D->urow.p, D->elim.p, D->X.p, x_rows);
     PGCP_LAUNCH_CHECK();
     PGCP_TRY_CUDA(cudaEventRecord(e1, s));
     PGCP_TRY_CUDA(cudaEventSynchronize(e1));
+    {
+        int timeout_flag = 0;
+        PGCP_TRY_CUDA(cudaMemcpy(&timeout_flag, D->sync.p, sizeof(int), cudaMemcpyDeviceToHost));
+        if (timeout_flag) {
+            set_error("direct solver: substitution dependency wait timed out");
+            return PGCP_E_CUDA;
+        }
+    }
     float ms = 0;
     cudaEventElapsedTime(&ms, e0, e1);
     D->solve_ms = ms;
