@@ -85,6 +85,10 @@ PGCP_API int pgcp_batch_create(const double* V, const int32_t* F, int64_t n, int
 PGCP_API int pgcp_batch_create_from(const pgcp_batch* base, const int64_t* cuts, int64_t ncuts, uint32_t flags,
                                     void* stream, pgcp_batch** out);
 PGCP_API int pgcp_batch_destroy(pgcp_batch* b);
+/* Free the batch's last flatten (bit 0 of which) and/or harmonic (bit 1)
+ * solver systems -- factors, fronts, workspaces -- once their results are
+ * consumed (stream-ordered; pgcp_batch_last_solve then reports zeros). */
+PGCP_API int pgcp_batch_release_solvers(pgcp_batch* b, int which);
 
 /* host int64 info[PGCP_INFO_COUNT] */
 #define PGCP_INFO_K 0            /* number of submeshes                          */

@@ -65,6 +65,7 @@ _SIGS = {
     "pgcp_last_error": ([], ctypes.c_char_p),
     "pgcp_batch_create": ([_VP, _VP, _I64, _I64, _VP, _I64, _U32, _VP, ctypes.POINTER(_VP)], ctypes.c_int),
     "pgcp_batch_destroy": ([_VP], ctypes.c_int),
+    "pgcp_batch_release_solvers": ([_VP, ctypes.c_int], ctypes.c_int),
     "pgcp_batch_create_from": ([_VP, _VP, _I64, _U32, _VP, ctypes.POINTER(_VP)], ctypes.c_int),
     "pgcp_batch_info": ([_VP, _PI64, ctypes.c_int], ctypes.c_int),
     "pgcp_batch_array": ([_VP, ctypes.c_int, ctypes.POINTER(_VP), _PI64], ctypes.c_int),

@@ -148,6 +148,20 @@ int pgcp_batch_destroy(pgcp_batch* b) {
     return PGCP_OK;
 }
 
+int pgcp_batch_release_solvers(pgcp_batch* b, int which) {
+    if (!b) {
+        set_error("pgcp_batch_release_solvers: null batch");
+        return PGCP_E_INVALID;
+    }
+    PGCP_TRY_CUDA(cudaSetDevice(b->device));
+    for (int k = 0; k < 2; ++k)
+        if (which & (1 << k)) {
+            free_system(b->sys[k]);
+            b->sys[k] = nullptr;
+        }
+    return PGCP_OK;
+}
+
 int pgcp_batch_info(const pgcp_batch* b, int64_t* info, int ninfo) {
     if (!b || !info) {
         set_error("pgcp_batch_info: null argument");

@@ -3,6 +3,9 @@
 
 #include "common.cuh"
 
+#include <cstring>
+#include <vector>
+
 namespace pgcp {
 
 static thread_local std::string g_err;
@@ -206,6 +209,52 @@ int stable_counting_sort(const int32_t* keys, int64_t n, int32_t nkeys, int32_t*
         k_csort_scatter<<<grid, block, 0, s>>>(keys, n, tile, ntiles, cur.p, perm);
         PGCP_LAUNCH_CHECK();
     }
+    return PGCP_OK;
+}
+
+namespace {
+struct PinStage {
+    unsigned char* buf = nullptr;
+    size_t cap = 0, used = 0;
+    struct Pending {
+        void* host;
+        size_t off, bytes;
+    };
+    std::vector<Pending> pend;
+    ~PinStage() {
+        if (buf) cudaFreeHost(buf);
+    }
+};
+thread_local PinStage g_pin;
+}  // namespace
+
+int d2h_async(void* host, const void* dev, size_t bytes, cudaStream_t s) {
+    PinStage& p = g_pin;
+    const size_t off = (p.used + 15) & ~(size_t)15;
+    if (off + bytes > p.cap) {
+        if (!p.pend.empty()) PGCP_TRY(d2h_flush(s));  // queued copies go out first
+        if (bytes > p.cap) {
+            if (p.buf) PGCP_TRY_CUDA(cudaFreeHost(p.buf));
+            p.buf = nullptr;
+            p.cap = 0;
+            const size_t want = bytes < (1u << 20) ? (1u << 20) : bytes + bytes / 4;
+            PGCP_TRY_CUDA(cudaMallocHost((void**)&p.buf, want));
+            p.cap = want;
+        }
+        return d2h_async(host, dev, bytes, s);
+    }
+    PGCP_TRY_CUDA(cudaMemcpyAsync(p.buf + off, dev, bytes, cudaMemcpyDeviceToHost, s));
+    p.pend.push_back({host, off, bytes});
+    p.used = off + bytes;
+    return PGCP_OK;
+}
+
+int d2h_flush(cudaStream_t s) {
+    PinStage& p = g_pin;
+    PGCP_TRY_CUDA(cudaStreamSynchronize(s));
+    for (const auto& q : p.pend) memcpy(q.host, p.buf + q.off, q.bytes);
+    p.pend.clear();
+    p.used = 0;
     return PGCP_OK;
 }
 

@@ -155,12 +155,20 @@ int exclusive_scan_i32_to_i64(const int32_t* in, int64_t* out, int64_t n, cudaSt
 int stable_counting_sort(const int32_t* keys, int64_t n, int32_t nkeys, int32_t* perm,
                          int64_t* key_off, cudaStream_t s);
 
+// Device -> host reads through a per-thread pinned staging buffer. A copy
+// into pageable memory is staged by the driver synchronously and can wait
+// for unrelated work (e.g. a weld running on the legacy default stream while
+// the Dirichlet systems are prepared on another thread); a pinned
+// destination is a plain DMA on `s`. d2h_async queues a copy, d2h_flush
+// synchronises `s` and delivers every queued copy to its destination.
+int d2h_async(void* host, const void* dev, size_t bytes, cudaStream_t s);
+int d2h_flush(cudaStream_t s);
+
 // copy one scalar back (synchronises the stream)
 template <class T>
 int fetch_scalar(const T* dptr, T* host, cudaStream_t s) {
-    PGCP_TRY_CUDA(cudaMemcpyAsync(host, dptr, sizeof(T), cudaMemcpyDeviceToHost, s));
-    PGCP_TRY_CUDA(cudaStreamSynchronize(s));
-    return PGCP_OK;
+    PGCP_TRY(d2h_async(host, dptr, sizeof(T), s));
+    return d2h_flush(s);
 }
 
 }  // namespace pgcp

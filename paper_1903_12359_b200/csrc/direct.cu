@@ -296,9 +296,14 @@ __global__ void k_nd_init_u(int64_t NU, const int32_t* __restrict__ uslot, const
     }
 }
 
-__global__ void k_nd_reset(int32_t lb, int32_t le, NodeArrays nd) {
-    GRID_STRIDE(i, (int64_t)(le - lb)) {
-        const int64_t N = lb + i;
+// region kernels read the level's node range [rng[0], rng[1]) from device
+// memory (no host round trip per level) and stride over it
+#define RANGE_LOOP(N, rng)                                                                  \
+    for (int64_t N = (rng)[0] + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; N < (rng)[1]; \
+         N += (int64_t)gridDim.x * blockDim.x)
+
+__global__ void k_nd_reset(const int32_t* __restrict__ rng, NodeArrays nd) {
+    RANGE_LOOP(N, rng) {
         for (int q = 0; q < 3; ++q) {
             nd.bbox[6 * N + q] = 0xffffffffu;
             nd.bbox[6 * N + 3 + q] = 0u;
@@ -320,9 +325,8 @@ __global__ void k_nd_bbox(int64_t NU, const int32_t* __restrict__ reg, const flo
     }
 }
 
-__global__ void k_nd_split(int32_t lb, int32_t le, NodeArrays nd) {
-    GRID_STRIDE(i, (int64_t)(le - lb)) {
-        const int64_t N = lb + i;
+__global__ void k_nd_split(const int32_t* __restrict__ rng, NodeArrays nd) {
+    RANGE_LOOP(N, rng) {
         if (nd.leaf[N]) continue;
         float lo[3], hi[3];
         int ax = 0;
@@ -384,9 +388,9 @@ __global__ void k_nd_sep(int64_t NU, const int32_t* __restrict__ reg, const int8
     }
 }
 
-__global__ void k_nd_count_children(int32_t lb, int32_t le, NodeArrays nd) {
-    GRID_STRIDE(i, (int64_t)(le - lb)) {
-        const int64_t N = lb + i;
+__global__ void k_nd_count_children(const int32_t* __restrict__ rng, NodeArrays nd) {
+    RANGE_LOOP(N, rng) {
+        const int64_t i = N - rng[0];
         int nc = 0;
         if (!nd.leaf[N]) {
             const int nA = nd.gcnt[3 * N], nB = nd.gcnt[3 * N + 1], nS = nd.gcnt[3 * N + 2];
@@ -402,10 +406,13 @@ __global__ void k_nd_count_children(int32_t lb, int32_t le, NodeArrays nd) {
     }
 }
 
-__global__ void k_nd_link(int32_t lb, int32_t le, const int32_t* __restrict__ scan, int32_t next, int leafmax,
+// `cur` = this level's recorded range (the live range already points at the
+// next level); children ids start at cur[1]
+__global__ void k_nd_link(const int32_t* __restrict__ cur, const int32_t* __restrict__ scan, int leafmax,
                           NodeArrays nd) {
-    GRID_STRIDE(i, (int64_t)(le - lb)) {
-        const int64_t N = lb + i;
+    const int32_t next = cur[1];
+    RANGE_LOOP(N, cur) {
+        const int64_t i = N - cur[0];
         if (nd.nchild[i] == 0) continue;
         const int nA = nd.gcnt[3 * N], nB = nd.gcnt[3 * N + 1];
         int id = next + scan[i];
@@ -423,6 +430,54 @@ __global__ void k_nd_link(int32_t lb, int32_t le, const int32_t* __restrict__ sc
             nd.slot[C] = nd.slot[N];
             nd.leaf[C] = n[q] <= leafmax;
             nd.npiv[C] = n[q] <= leafmax ? n[q] : 0;
+        }
+    }
+}
+
+// exclusive scan of the level's child counts (one CTA), the level recorded in
+// hist[2 level..], the live range advanced to the children
+__global__ void __launch_bounds__(1024) k_nd_scan(int32_t* __restrict__ rng, const int32_t* __restrict__ nchild,
+                                                  int32_t* __restrict__ scan, int32_t* __restrict__ hist, int level,
+                                                  int64_t ncap, int32_t* __restrict__ ovf) {
+    __shared__ int32_t wsum[33];
+    const int lb = rng[0], le = rng[1], n = le - lb;
+    const int per = (n + 1023) / 1024;
+    const int i0 = min(n, (int)threadIdx.x * per), i1 = min(n, i0 + per);
+    int loc = 0;
+    for (int i = i0; i < i1; ++i) loc += nchild[i];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int inc = loc;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(FULL, inc, o);
+        if (lane >= o) inc += v;
+    }
+    if (lane == 31) wsum[w] = inc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int acc = 0;
+        for (int q = 0; q < 32; ++q) {
+            const int v = wsum[q];
+            wsum[q] = acc;
+            acc += v;
+        }
+        wsum[32] = acc;
+    }
+    __syncthreads();
+    int off = wsum[w] + inc - loc;
+    for (int i = i0; i < i1; ++i) {
+        scan[i] = off;
+        off += nchild[i];
+    }
+    if (threadIdx.x == 0) {
+        const int total = wsum[32];
+        hist[2 * level] = lb;
+        hist[2 * level + 1] = le;
+        if ((int64_t)le + total > ncap) {
+            *ovf = 1;
+            rng[0] = rng[1] = le;
+        } else {
+            rng[0] = le;
+            rng[1] = le + total;
         }
     }
 }
@@ -1804,11 +1859,13 @@ int env_int(const char* name, int dflt) {
     return e ? atoi(e) : dflt;
 }
 
-// PGCP_DIRECT_TIMING=1: CUDA-event split of the phases, printed to stderr
+// PGCP_DIRECT_TIMING=1: CUDA-event split of the phases (and the host time
+// between the marks), printed to stderr
 struct PhaseTimer {
     bool on = false;
     cudaStream_t s = nullptr;
     std::vector<std::pair<const char*, cudaEvent_t>> ev;
+    std::vector<double> host;
     explicit PhaseTimer(cudaStream_t st) : on(getenv("PGCP_DIRECT_TIMING") != nullptr), s(st) { mark("start"); }
     void mark(const char* name) {
         if (!on) return;
@@ -1816,6 +1873,7 @@ struct PhaseTimer {
         cudaEventCreate(&e);
         cudaEventRecord(e, s);
         ev.push_back({name, e});
+        host.push_back(1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count());
     }
     ~PhaseTimer() {
         if (!on) return;
@@ -1826,10 +1884,13 @@ struct PhaseTimer {
             cudaEventElapsedTime(&ms, ev[i - 1].second, ev[i].second);
             fprintf(stderr, " %s %.3f", ev[i].first, ms);
         }
+        fprintf(stderr, " (ms)\n[direct host]  ");
+        for (size_t i = 1; i < ev.size(); ++i) fprintf(stderr, " %s %.3f", ev[i].first, host[i] - host[i - 1]);
         fprintf(stderr, " (ms)\n");
         for (auto& p : ev) cudaEventDestroy(p.second);
     }
 };
+
 
 }  // namespace
 
@@ -1860,8 +1921,13 @@ static int ws_acquire(size_t bytes, cudaStream_t s, int* slot_out, void** p_out)
         if (w.dev != dev || w.busy || w.bytes < bytes) continue;
         if (best < 0 || w.bytes < g_ws[best].bytes) best = i;
     }
-    if (best < 0) {  // grow: reuse an idle slot of this device, else add one
-        for (int i = 0; i < (int)g_ws.size() && best < 0; ++i)
+    if (best < 0) {  // grow: a new slot while the cache stays under half the device memory, else evict an idle one
+        size_t cached = 0, free_b = 0, total_b = 0;
+        for (const WsSlot& w : g_ws)
+            if (w.dev == dev) cached += w.bytes;
+        PGCP_TRY_CUDA(cudaMemGetInfo(&free_b, &total_b));
+        const bool room = cached + bytes + bytes / 8 <= total_b / 2;
+        for (int i = 0; i < (int)g_ws.size() && best < 0 && !room; ++i)
             if (g_ws[i].dev == dev && !g_ws[i].busy) best = i;
         if (best < 0) {
             g_ws.push_back(WsSlot());
@@ -1957,7 +2023,7 @@ struct DirectFactor {
     std::vector<int64_t> lst_off;
     std::vector<int> lst_maxs;               // per (level, type): largest pivot count
     std::vector<int> lst_maxf;               // ... largest front
-    std::vector<int32_t> h_nlist, h_npiv, h_fsz;
+    std::vector<int32_t> h_nlist, h_npiv, h_fsz, h_order;  // host copies (uploads stay async)
     std::vector<int> lvl_maxf, lvl_maxu;
     int ncplx = 0;
     std::vector<int32_t> h_err;
@@ -2001,9 +2067,28 @@ const std::vector<int32_t>& direct_slot_status(const DirectFactor* F) { return F
 
 namespace {
 
+// Dynamic shared-memory limit of a kernel: raised once to the most the
+// kernel can take and never lowered. Concurrent solves (the flatten worker
+// and the Dirichlet preparation) launch the same kernels with different
+// sizes; a per-launch attribute could be lowered by one thread between the
+// other's set and launch.
+std::mutex g_smem_mu;
+std::vector<const void*> g_smem_done;  // kernels whose limit is raised (keyed by entry point)
 template <class K>
 int set_smem(K kern, size_t bytes) {
-    PGCP_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    std::lock_guard<std::mutex> lock(g_smem_mu);
+    const void* key = reinterpret_cast<const void*>(kern);
+    if (std::find(g_smem_done.begin(), g_smem_done.end(), key) == g_smem_done.end()) {
+        cudaFuncAttributes fa;
+        PGCP_TRY_CUDA(cudaFuncGetAttributes(&fa, kern));
+        const int cap = 227 * 1024 - (int)fa.sharedSizeBytes;
+        PGCP_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, cap));
+        g_smem_done.push_back(key);
+    }
+    if (bytes + 0 > (size_t)(227 * 1024)) {
+        set_error("direct solver: %zu bytes of shared memory requested", bytes);
+        return DIRECT_FALLBACK;
+    }
     return PGCP_OK;
 }
 
@@ -2165,8 +2250,9 @@ int direct_factor(pgcp_batch* b, const DirectInput& in, DirectFactor** out, cuda
         PGCP_TRY(D->aptr.alloc(NU + 1, s));
         PGCP_TRY(exclusive_scan_i64(cntb.p, D->aptr.p, NU, s));
     }
-    int64_t annz = 0;
-    PGCP_TRY(fetch_scalar(D->aptr.p + NU, &annz, s));
+    // upper bound of the stored entries (no host round trip): every ELL slot
+    // (padding included) plus the two coupling partners of a row
+    const int64_t annz = in.nnz_ell + 2 * NU;
     PGCP_TRY(D->acol.alloc(annz, s));
     PGCP_TRY(D->aval.alloc(annz, s));
     k_d_adj_fill<<<grid_for(NU, 256), 256, 0, s>>>(NU, aa, D->aptr.p, D->acol.p, D->aval.p);
@@ -2197,53 +2283,69 @@ int direct_factor(pgcp_batch* b, const DirectInput& in, DirectFactor** out, cuda
     PGCP_LAUNCH_CHECK();
     k_nd_init_u<<<grid_for(NU, 256), 256, 0, s>>>(NU, D->uslot.p, D->leaf.p, reg.p, node_of.p);
     PGCP_LAUNCH_CHECK();
-    DevBuf<int32_t> scan;
+    DevBuf<int32_t> scan, ndst;  // ndst: [0..1] live level range, [2] overflow, [4..] per-level ranges
     PGCP_TRY(scan.alloc(ncap + 1, s));
-    DevBuf<unsigned char> cub_tmp;
-    size_t cub_bytes = 0;
-    int32_t lb = 0, le = nslot;
+    constexpr int MAXL = 96;
+    PGCP_TRY(ndst.alloc(4 + 2 * MAXL, s));
+    PGCP_TRY(ndst.zero(s));
+    {
+        const int32_t r0[2] = {0, nslot};
+        PGCP_TRY_CUDA(cudaMemcpyAsync(ndst.p, r0, sizeof(r0), cudaMemcpyHostToDevice, s));
+    }
+    int32_t* rng = ndst.p;
+    int32_t* hist = ndst.p + 4;
     D->levels.clear();
     const int ugrid = grid_for(NU, 256);
-    while (le > lb) {
-        D->levels.push_back({lb, le});
-        if ((int)D->levels.size() > 200) {
+    const int rgrid = 4 * 148;
+    int nlev = 0;
+    const bool nd_detail = env_int("PGCP_DIRECT_TIMING", 0) >= 2;
+    for (int level = 0;; ++level) {
+        if (level >= MAXL) {
             set_error("direct solver: nested dissection did not terminate");
             return DIRECT_FALLBACK;
         }
-        const int64_t nl = le - lb;
-        k_nd_reset<<<grid_for(nl, 256), 256, 0, s>>>(lb, le, nd);
+        k_nd_reset<<<rgrid, 256, 0, s>>>(rng, nd);
         PGCP_LAUNCH_CHECK();
         k_nd_bbox<<<ugrid, 256, 0, s>>>(NU, reg.p, pos.p, nd);
         PGCP_LAUNCH_CHECK();
-        k_nd_split<<<grid_for(nl, 256), 256, 0, s>>>(lb, le, nd);
+        k_nd_split<<<rgrid, 256, 0, s>>>(rng, nd);
         PGCP_LAUNCH_CHECK();
         k_nd_side<<<ugrid, 256, 0, s>>>(NU, reg.p, pos.p, nd, side.p);
         PGCP_LAUNCH_CHECK();
         k_nd_sep<<<ugrid, 256, 0, s>>>(NU, reg.p, side.p, D->aptr.p, D->acol.p, nd, grp.p);
         PGCP_LAUNCH_CHECK();
-        k_nd_count_children<<<grid_for(nl, 256), 256, 0, s>>>(lb, le, nd);
+        k_nd_count_children<<<rgrid, 256, 0, s>>>(rng, nd);
         PGCP_LAUNCH_CHECK();
-        size_t need = 0;
-        cub::DeviceScan::ExclusiveSum(nullptr, need, D->nchild.p, scan.p, (int)nl + 1, s);
-        if (need > cub_bytes) {
-            PGCP_TRY(cub_tmp.alloc((int64_t)need, s));
-            cub_bytes = need;
-        }
-        // nchild[nl] is a sentinel 0 so scan[nl] is the level total
-        PGCP_TRY_CUDA(cudaMemsetAsync(D->nchild.p + nl, 0, sizeof(int32_t), s));
-        PGCP_TRY_CUDA(cub::DeviceScan::ExclusiveSum(cub_tmp.p, need, D->nchild.p, scan.p, (int)nl + 1, s));
-        int32_t total = 0;
-        PGCP_TRY(fetch_scalar(scan.p + nl, &total, s));
-        if ((int64_t)le + total > ncap) {
-            set_error("direct solver: nested dissection node capacity exceeded");
-            return DIRECT_FALLBACK;
-        }
-        k_nd_link<<<grid_for(nl, 256), 256, 0, s>>>(lb, le, scan.p, le, leafmax, nd);
+        k_nd_scan<<<1, 1024, 0, s>>>(rng, D->nchild.p, scan.p, hist, level, ncap, ndst.p + 2);
+        PGCP_LAUNCH_CHECK();
+        k_nd_link<<<rgrid, 256, 0, s>>>(hist + 2 * level, scan.p, leafmax, nd);
         PGCP_LAUNCH_CHECK();
         k_nd_assign<<<ugrid, 256, 0, s>>>(NU, reg.p, grp.p, nd, node_of.p);
         PGCP_LAUNCH_CHECK();
-        lb = le;
-        le = le + total;
+        if (nd_detail) pt.mark("ndlvl");
+        // termination: checked on the host every other level past the 9th
+        if (level >= 8 && (level & 1)) {
+            int32_t h[4];
+            PGCP_TRY(d2h_async(h, ndst.p, sizeof(h), s));
+            PGCP_TRY(d2h_flush(s));
+            if (h[2]) {
+                set_error("direct solver: nested dissection node capacity exceeded");
+                return DIRECT_FALLBACK;
+            }
+            if (h[0] >= h[1]) {
+                nlev = level + 1;
+                break;
+            }
+        }
+    }
+    std::vector<int32_t> hh(2 * nlev);
+    PGCP_TRY(d2h_async(hh.data(), hist, hh.size() * sizeof(int32_t), s));
+    PGCP_TRY(d2h_flush(s));
+    int32_t le = nslot;
+    for (int l = 0; l < nlev; ++l) {
+        if (hh[2 * l + 1] <= hh[2 * l]) break;  // trailing empty levels
+        D->levels.push_back({hh[2 * l], hh[2 * l + 1]});
+        le = hh[2 * l + 1];
     }
     D->nnodes = le;
     const int32_t nn = D->nnodes;
@@ -2333,13 +2435,7 @@ int direct_factor(pgcp_batch* b, const DirectInput& in, DirectFactor** out, cuda
         k_sym<<<a1 - a0, DNT, 0, s>>>(a0, sa);
         PGCP_LAUNCH_CHECK();
     }
-    pt.mark("symbolic");
-    int32_t hov = 0;
-    PGCP_TRY(fetch_scalar(ovf.p, &hov, s));
-    if (hov) {
-        set_error("direct solver: symbolic capacity exceeded");
-        return DIRECT_FALLBACK;
-    }
+    pt.mark("symbolic");  // the overflow flag is read with the layout below
     // ---- front types: complex where the subtree holds coupling entries
     PGCP_TRY(D->ntype.alloc(nn, s));
     PGCP_TRY(D->ntype.zero(s));
@@ -2363,12 +2459,18 @@ int direct_factor(pgcp_batch* b, const DirectInput& in, DirectFactor** out, cuda
     std::vector<int32_t> hf(nn), hp(nn);
     std::vector<int8_t> ht(nn);
     int64_t ftot = 0, wtot = 0;
-    PGCP_TRY_CUDA(cudaMemcpyAsync(ht.data(), D->ntype.p, nn * sizeof(int8_t), cudaMemcpyDeviceToHost, s));
-    PGCP_TRY_CUDA(cudaMemcpyAsync(hf.data(), D->fsz.p, nn * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    PGCP_TRY_CUDA(cudaMemcpyAsync(hp.data(), D->npiv.p, nn * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    PGCP_TRY_CUDA(cudaMemcpyAsync(&ftot, D->foff.p + nn, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-    PGCP_TRY_CUDA(cudaMemcpyAsync(&wtot, D->woff.p + nn, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-    PGCP_TRY_CUDA(cudaStreamSynchronize(s));
+    PGCP_TRY(d2h_async(ht.data(), D->ntype.p, nn * sizeof(int8_t), s));
+    PGCP_TRY(d2h_async(hf.data(), D->fsz.p, nn * sizeof(int32_t), s));
+    PGCP_TRY(d2h_async(hp.data(), D->npiv.p, nn * sizeof(int32_t), s));
+    PGCP_TRY(d2h_async(&ftot, D->foff.p + nn, sizeof(int64_t), s));
+    PGCP_TRY(d2h_async(&wtot, D->woff.p + nn, sizeof(int64_t), s));
+    int32_t hov = 0;
+    PGCP_TRY(d2h_async(&hov, ovf.p, sizeof(int32_t), s));
+    PGCP_TRY(d2h_flush(s));
+    if (hov) {  // some update set was cut short: nothing after it is valid
+        set_error("direct solver: symbolic capacity exceeded");
+        return DIRECT_FALLBACK;
+    }
     D->lvl_maxf.assign(D->levels.size(), 0);
     D->lvl_maxu.assign(D->levels.size(), 0);
     D->fmas = 0;
@@ -2405,8 +2507,9 @@ int direct_factor(pgcp_batch* b, const DirectInput& in, DirectFactor** out, cuda
     D->h_fsz = hf;
     PGCP_TRY(D->nlist.alloc(nn, s));
     PGCP_TRY_CUDA(cudaMemcpyAsync(D->nlist.p, hl.data(), nn * sizeof(int32_t), cudaMemcpyHostToDevice, s));
-    {   // deepest level first: every front after its children
-        std::vector<int32_t> ord;
+    {   // deepest level first: every front after its children (host copy kept: async upload)
+        std::vector<int32_t>& ord = D->h_order;
+        ord.clear();
         ord.reserve(nn);
         for (int l = (int)D->levels.size() - 1; l >= 0; --l)
             for (int N = D->levels[l].first; N < D->levels[l].second; ++N) ord.push_back(N);
@@ -2414,7 +2517,6 @@ int direct_factor(pgcp_batch* b, const DirectInput& in, DirectFactor** out, cuda
         PGCP_TRY_CUDA(cudaMemcpyAsync(D->order.p, ord.data(), nn * sizeof(int32_t), cudaMemcpyHostToDevice, s));
         PGCP_TRY(D->sync.alloc(nn + 2, s));
         PGCP_TRY(D->sync.zero(s));
-        PGCP_TRY_CUDA(cudaStreamSynchronize(s));  // ord is a local
     }
     if (pt.on) {
         for (size_t l = 0; l < D->levels.size(); ++l) {
@@ -2464,8 +2566,8 @@ int direct_factor(pgcp_batch* b, const DirectInput& in, DirectFactor** out, cuda
     PGCP_TRY(factor_levels(D, fa, s, pt));
     PGCP_TRY_CUDA(cudaEventRecord(n1, s));
     PGCP_TRY_CUDA(cudaEventRecord(e1, s));
-    PGCP_TRY_CUDA(cudaMemcpyAsync(D->h_err.data(), D->err.p, nslot * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    PGCP_TRY_CUDA(cudaStreamSynchronize(s));
+    PGCP_TRY(d2h_async(D->h_err.data(), D->err.p, nslot * sizeof(int32_t), s));
+    PGCP_TRY(d2h_flush(s));
     float ms = 0;
     cudaEventElapsedTime(&ms, e0, e1);
     D->factor_ms = ms;

@@ -20,6 +20,7 @@ struct DirectInput {
     std::vector<int64_t> h_nu;        // unknowns per slot
     const int32_t* rowsrc = nullptr;  // row -> compact vertex (-1: padding)
     const int64_t* sl_ptr = nullptr;  // paired sliced ELL (off-diagonals, unit diagonal implied)
+    int64_t nnz_ell = 0;              // stored ELL entries (padding included)
     const int32_t* col = nullptr;
     const double* val = nullptr;
     const uint32_t* sl_mask = nullptr;  // coupling rows (DNCP)

@@ -2634,8 +2634,8 @@ int build_system(pgcp_batch* b, SolveSystem* S, bool dncp, const int32_t* d_pins
         PGCP_TRY(g.alloc(nslot + 1, s));
         k_gather_i64<<<grid_for(nslot + 1, 128), 128, 0, s>>>(uscan.p, S->sv_off.p, nslot + 1, g.p);
         PGCP_LAUNCH_CHECK();
-        PGCP_TRY_CUDA(cudaMemcpyAsync(hus.data(), g.p, (nslot + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-        PGCP_TRY_CUDA(cudaStreamSynchronize(s));
+        PGCP_TRY(d2h_async(hus.data(), g.p, (nslot + 1) * sizeof(int64_t), s));
+        PGCP_TRY(d2h_flush(s));
     }
     S->h_nu.resize(nslot);
     S->h_sl_off.assign(nslot + 1, 0);
@@ -2738,6 +2738,7 @@ int setup_direct(pgcp_batch* b, SolveSystem* S, cudaStream_t s) {
     in.h_nu = S->h_nu;
     in.rowsrc = S->rowsrc.p;
     in.sl_ptr = S->sl_ptr.p;
+    in.nnz_ell = S->nnz;
     in.col = S->col.p;
     in.val = S->val.p;
     in.sl_mask = S->sl_mask.p;

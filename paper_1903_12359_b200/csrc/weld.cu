@@ -2423,14 +2423,15 @@ int run_schedule(double2* tv, int32_t nsteps, const int32_t* info, const int32_t
     std::vector<double> meta((size_t)META * nsteps);
     std::vector<unsigned long long> mx(3 * (size_t)nsteps);
     int hnan = 0;
-    PGCP_TRY_CUDA(cudaMemcpyAsync(meta.data(), d_meta.p, meta.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
-    PGCP_TRY_CUDA(cudaMemcpyAsync(mx.data(), d_max.p, mx.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-    PGCP_TRY_CUDA(cudaMemcpyAsync(&hnan, d_nan.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    // pinned staging (common.cuh): a pageable read would hold the driver
+    // while the whole weld drains, stalling other host threads' launches
+    PGCP_TRY(d2h_async(meta.data(), d_meta.p, meta.size() * sizeof(double), s));
+    PGCP_TRY(d2h_async(mx.data(), d_max.p, mx.size() * sizeof(unsigned long long), s));
+    PGCP_TRY(d2h_async(&hnan, d_nan.p, sizeof(int), s));
     int htmo = 0;
-    if (streamed) PGCP_TRY_CUDA(cudaMemcpyAsync(&htmo, d_tmo.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-    if (recs_host && recs_cap_total >= rec_tot)
-        PGCP_TRY_CUDA(cudaMemcpyAsync(recs_host, d_recs.p, rec_tot * sizeof(Rec), cudaMemcpyDeviceToHost, s));
-    PGCP_TRY_CUDA(cudaStreamSynchronize(s));
+    if (streamed) PGCP_TRY(d2h_async(&htmo, d_tmo.p, sizeof(int), s));
+    if (recs_host && recs_cap_total >= rec_tot) PGCP_TRY(d2h_async(recs_host, d_recs.p, rec_tot * sizeof(Rec), s));
+    PGCP_TRY(d2h_flush(s));
     if (wtiming) {
         std::vector<long long> wt(4 * (size_t)nsteps);
         PGCP_TRY_CUDA(cudaMemcpy(wt.data(), d_wtime.p, wt.size() * sizeof(long long), cudaMemcpyDeviceToHost));

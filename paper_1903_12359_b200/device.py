@@ -107,6 +107,12 @@ class DeviceBatch:
         self._lock = threading.Lock()
 
     # -- lifetime
+    def release_solvers(self, which=3):
+        """Free the last flatten (bit 0) / harmonic (bit 1) solver systems
+        (factors and workspaces) once their results are consumed."""
+        if getattr(self, "h", None) is not None and self.h.value:
+            nat.check(nat.lib().pgcp_batch_release_solvers(self.h, which))
+
     def close(self):
         if getattr(self, "h", None) is not None and self.h.value:
             nat.lib().pgcp_batch_destroy(self.h)

@@ -263,9 +263,11 @@ def parameterize(mesh, cuts=None, mode="free", workers=1, seed=0, mobius_area=Fa
     hi.wait_stream(cur)
     lo.wait_stream(cur)
     overlap_prep = welds and os.environ.get("PGCP_OVERLAP_HPREP", "1") != "0"
-    # where the harmonic preparation overlaps: the flatten (default) or, with
-    # PGCP_HPREP_AT=weld, the weld (measured slower: the preparation's
-    # per-level host synchronisations queue behind the weld's kernels)
+    # where the harmonic preparation (the Dirichlet factorization) overlaps:
+    # the flatten (default) or, with PGCP_HPREP_AT=weld, the weld (the weld
+    # then runs on the high-priority stream). cfg 2: the weld placement is
+    # ~1.5 ms faster with device-resident inputs but 2-8 ms slower and
+    # erratic end to end (host-array inputs), so the default stays here.
     prep_at_weld = overlap_prep and os.environ.get("PGCP_HPREP_AT", "flatten") == "weld"
     hprep = {}
 
@@ -332,20 +334,29 @@ def parameterize(mesh, cuts=None, mode="free", workers=1, seed=0, mobius_area=Fa
 
             hworker = threading.Thread(target=_hprep, name="pgcp-harmonic-prepare")
             hworker.start()
+        # with the preparation beside it, the weld runs on the high-priority
+        # stream: its cluster launches get the SMs the factorization frees
+        wstream = hi if (hworker is not None and os.environ.get("PGCP_WELD_HI", "1") != "0") else cur
+        if wstream is not cur:
+            wstream.wait_stream(cur)
         try:
-            if own is None:
-                tv = torch.empty(len(plan.slot_parent), dtype=torch.complex128, device=dev)
-                nat.check(nat.lib().pgcp_gather_complex(_ptr(z0), _ptr(loop_gid), _ptr(tv), tv.numel(), _stream()))
-            else:  # the one exchange: all-gather of every rank's boundary-loop values
-                own_slots, tv = _exchange_boundary(shard, plan, loop_gid_host, z0, dev)
-            out = None
-            if len(steps):
-                out, _ = run_schedule(tv, plan.info, plan.src, plan.wb_off, plan.wb, cfg.hard_tol)
-                report.seam_residuals = [float(x) for x in out[:, 1]]
+            with torch.cuda.stream(wstream):
+                if own is None:
+                    tv = torch.empty(len(plan.slot_parent), dtype=torch.complex128, device=dev)
+                    nat.check(nat.lib().pgcp_gather_complex(_ptr(z0), _ptr(loop_gid), _ptr(tv), tv.numel(),
+                                                            _stream()))
+                else:  # the one exchange: all-gather of every rank's boundary-loop values
+                    own_slots, tv = _exchange_boundary(shard, plan, loop_gid_host, z0, dev)
+                out = None
+                if len(steps):
+                    out, _ = run_schedule(tv, plan.info, plan.src, plan.wb_off, plan.wb, cfg.hard_tol)
+                    report.seam_residuals = [float(x) for x in out[:, 1]]
         except BaseException:
             if hworker is not None:  # never leave the preparation running on the batch
                 hworker.join()
             raise
+        if wstream is not cur:
+            cur.wait_stream(wstream)
         exterior = []
         if len(steps) and steps[-1].closed:
             A, B = plan.exterior_candidates
@@ -394,6 +405,11 @@ def parameterize(mesh, cuts=None, mode="free", workers=1, seed=0, mobius_area=Fa
         # (pipeline.py:88-102, per submesh before the exterior map-back),
         # batched over every folded submesh on the device (repair.cu)
         report.repairs = _repair(batch, loop_gid, z, own, K, cfg, shard)
+        # the factors (GBs at cfg 2/5) are not needed past this point;
+        # PGCP_RELEASE_SOLVERS=1 frees them here (measured: e2e steps become
+        # erratic, so by default they go with the batch)
+        if os.environ.get("PGCP_RELEASE_SOLVERS", "0") == "1":
+            batch.release_solvers()
         if own is not None:
             # the other ranks' boundary loops hold the welded values (their
             # Dirichlet data), so every seam copy is known here
