@@ -707,7 +707,8 @@ __global__ void k_front_sizes(int32_t n, const int32_t* __restrict__ npiv, const
     GRID_STRIDE(i, (int64_t)n) {
         const int64_t f = (int64_t)npiv[i] + ucnt[i];
         fsz[i] = (int32_t)f;
-        f2[i] = ntype[i] ? 2 * f * f : ((f * f + 1) & ~1ll);
+        const int64_t np = f * (f + 1) / 2;  // packed lower triangle
+        f2[i] = ntype[i] ? 2 * np : ((np + 1) & ~1ll);
         f1[i] = f;
     }
 }
@@ -756,6 +757,10 @@ template <class T>
 __device__ __forceinline__ const T* front_ptr(const void* pool, int64_t off) {
     return reinterpret_cast<const T*>(reinterpret_cast<const double*>(pool) + off);
 }
+// fronts live in global memory as packed lower triangles, column-major:
+// column j holds rows j..f-1 and starts at j (2f - j - 1) / 2
+__device__ __forceinline__ int64_t pk64(int i, int j, int f) { return (int64_t)j * (2 * f - j - 1) / 2 + i; }
+__device__ __forceinline__ int64_t npk(int f) { return (int64_t)f * (f + 1) / 2; }
 template <class T> __device__ __forceinline__ T narrow(double2 v);
 template <> __device__ __forceinline__ double narrow<double>(double2 v) { return v.x; }
 template <> __device__ __forceinline__ double2 narrow<double2>(double2 v) { return v; }
@@ -769,15 +774,16 @@ __device__ __forceinline__ int front_pos(int64_t x, int64_t pf, int s, const int
 // matrix entries of pivots [kb, ke) of a front (lower part, column-major,
 // leading dimension f): S[pos(w)][k] = A(w, u) = conj(A(u, w)), unit diagonal.
 // One thread per stored entry: independent, coalesced loads.
-template <class T>
+template <class T, bool PACKED>
 __device__ __forceinline__ void assemble_entries(T* S, int f, int64_t pf, int s, const int32_t* Us, int nu, int kb,
                                                  int ke, const FacArgs& a) {
-    for (int k = kb + threadIdx.x; k < ke; k += DNT) S[(int64_t)k + (int64_t)k * f] = from_c<T>(make_double2(1.0, 0.0));
+    auto at = [&](int i, int j) -> int64_t { return PACKED ? pk64(i, j, f) : (int64_t)i + (int64_t)j * f; };
+    for (int k = kb + threadIdx.x; k < ke; k += DNT) S[at(k, k)] = from_c<T>(make_double2(1.0, 0.0));
     const int64_t q1 = a.eptr[pf + ke];
     for (int64_t q = a.eptr[pf + kb] + threadIdx.x; q < q1; q += DNT) {
         const int k = (int)(a.erow[q] - pf);
         const int i = front_pos(a.ecol[q], pf, s, Us, nu);
-        S[(int64_t)i + (int64_t)k * f] = cj(from_c<T>(a.eval[q]));
+        S[at(i, k)] = cj(from_c<T>(a.eval[q]));
     }
 }
 
@@ -804,13 +810,13 @@ __device__ __forceinline__ void tile_one(T* F, int f, int ti, int tj, int rlim, 
         for (int q = 0; q < QA; ++q) {
             const int idx = t + q * DNT;
             const int r = idx % TR, k = kc + idx / TR;
-            ra[q] = (k < ke && ti + r < rlim) ? F[(int64_t)(ti + r) + (int64_t)k * f] : zero_t<T>();
+            ra[q] = (k < ke && ti + r < rlim) ? F[pk64(ti + r, k, f)] : zero_t<T>();
         }
 #pragma unroll
         for (int q = 0; q < QB; ++q) {
             const int idx = t + q * DNT;
             const int r = idx % TC, k = kc + idx / TC;
-            rb[q] = (k < ke && tj + r < clim) ? F[(int64_t)(tj + r) + (int64_t)k * f] : zero_t<T>();
+            rb[q] = (k < ke && tj + r < clim) ? F[pk64(tj + r, k, f)] : zero_t<T>();
         }
     };
     if (kb < ke) fetch(kb);
@@ -843,7 +849,7 @@ __device__ __forceinline__ void tile_one(T* F, int f, int ti, int tj, int rlim, 
         for (int j = 0; j < 4; ++j) {
             const int c = tj + tx + 16 * j;
             if (c >= clim || r < c) continue;
-            T& dst = F[(int64_t)r + (int64_t)c * f];
+            T& dst = F[pk64(r, c, f)];
             dst = sub(dst, acc[i][j]);
         }
     }
@@ -955,7 +961,7 @@ __global__ void __launch_bounds__(DNT, sizeof(T) == 8 ? 8 : 4) k_factor(FacArgs 
     if (threadIdx.x == 0) bad = 0;
     for (int i = threadIdx.x; i < nu; i += DNT) Us[i] = a.upool[a.ustart[N] + i];
     {   // zero the front (16-byte stores)
-        const int64_t nd2 = (int64_t)f * f * (int64_t)(sizeof(T) / 8);
+        const int64_t nd2 = npk(f) * (int64_t)(sizeof(T) / 8);
         double2* z2 = reinterpret_cast<double2*>(F);
         const bool al = (reinterpret_cast<uintptr_t>(F) & 15) == 0;
         if (al) {
@@ -966,7 +972,7 @@ __global__ void __launch_bounds__(DNT, sizeof(T) == 8 ? 8 : 4) k_factor(FacArgs 
         }
     }
     __syncthreads();
-    assemble_entries<T>(F, f, pf, s, Us, nu, 0, s, a);
+    assemble_entries<T, true>(F, f, pf, s, Us, nu, 0, s, a);
     __syncthreads();
     // extend-add the children's update blocks (fixed order: A, then B; every
     // entry of one child's block lands on a distinct position)
@@ -989,8 +995,8 @@ __global__ void __launch_bounds__(DNT, sizeof(T) == 8 ? 8 : 4) k_factor(FacArgs 
                 const int t = t0 + q * DNT;
                 const int bcol = t / max(uc, 1), i = t - bcol * uc;
                 const bool ok = t < tot && i >= bcol;
-                pos[q] = ok ? rel[i] + rel[bcol] * f : -1;
-                const int64_t e = (int64_t)(sc + bcol) * fc + sc + i;
+                pos[q] = ok ? pk64(rel[i], rel[bcol], f) : -1;
+                const int64_t e = pk64(sc + i, sc + bcol, fc);
                 v[q] = !ok ? make_double2(0.0, 0.0)
                            : (ccx ? reinterpret_cast<const double2*>(FC)[e] : make_double2(FC[e], 0.0));
             }
@@ -1009,13 +1015,13 @@ __global__ void __launch_bounds__(DNT, sizeof(T) == 8 ? 8 : 4) k_factor(FacArgs 
         if (warp == 0) {
             for (int idx = lane; idx < NB * NB; idx += 32) {
                 const int i = idx % NB, j = idx / NB;
-                Ld[idx] = (i < nb && j < nb && i >= j) ? F[(int64_t)(k0 + i) + (int64_t)(k0 + j) * f] : zero_t<T>();
+                Ld[idx] = (i < nb && j < nb && i >= j) ? F[pk64(k0 + i, k0 + j, f)] : zero_t<T>();
             }
             __syncwarp();
             diag_factor<T, NB>(Ld, nb, &bad);
             for (int idx = lane; idx < NB * NB; idx += 32) {
                 const int i = idx % NB, j = idx / NB;
-                if (i < nb && j < nb && i >= j) F[(int64_t)(k0 + i) + (int64_t)(k0 + j) * f] = Ld[idx];
+                if (i < nb && j < nb && i >= j) F[pk64(k0 + i, k0 + j, f)] = Ld[idx];
             }
         }
         if (threadIdx.x < nb) dinv[threadIdx.x] = 1.0 / re(Ld[threadIdx.x + threadIdx.x * NB]);
@@ -1024,7 +1030,7 @@ __global__ void __launch_bounds__(DNT, sizeof(T) == 8 ? 8 : 4) k_factor(FacArgs 
         for (int r = k0 + nb + threadIdx.x; r < f; r += DNT) {
             T x[NB];
 #pragma unroll
-            for (int k = 0; k < NB; ++k) x[k] = k < nb ? F[(int64_t)r + (int64_t)(k0 + k) * f] : zero_t<T>();
+            for (int k = 0; k < NB; ++k) x[k] = k < nb ? F[pk64(r, k0 + k, f)] : zero_t<T>();
 #pragma unroll
             for (int k = 0; k < NB; ++k) {
                 if (k < nb) {
@@ -1037,7 +1043,7 @@ __global__ void __launch_bounds__(DNT, sizeof(T) == 8 ? 8 : 4) k_factor(FacArgs 
             }
 #pragma unroll
             for (int k = 0; k < NB; ++k)
-                if (k < nb) F[(int64_t)r + (int64_t)(k0 + k) * f] = x[k];
+                if (k < nb) F[pk64(r, k0 + k, f)] = x[k];
         }
         __syncthreads();
         // the remaining pivot columns
@@ -1077,7 +1083,7 @@ __global__ void __launch_bounds__(DNT) k_pdiag(FacArgs a, int k0, int phase) {
     if (threadIdx.x == 0) bad = 0;
     for (int idx = threadIdx.x; idx < PB * PB; idx += DNT) {
         const int i = idx % PB, j = idx / PB;
-        Ld[idx] = (i < nb && j < nb && i >= j) ? F[(int64_t)(k0 + i) + (int64_t)(k0 + j) * f] : zero_t<T>();
+        Ld[idx] = (i < nb && j < nb && i >= j) ? F[pk64(k0 + i, k0 + j, f)] : zero_t<T>();
     }
     if (phase == 0) {
         __syncthreads();
@@ -1085,7 +1091,7 @@ __global__ void __launch_bounds__(DNT) k_pdiag(FacArgs a, int k0, int phase) {
         __syncthreads();
         for (int idx = threadIdx.x; idx < PB * PB; idx += DNT) {
             const int i = idx % PB, j = idx / PB;
-            if (i < nb && j < nb && i >= j) F[(int64_t)(k0 + i) + (int64_t)(k0 + j) * f] = Ld[idx];
+            if (i < nb && j < nb && i >= j) F[pk64(k0 + i, k0 + j, f)] = Ld[idx];
         }
         if (threadIdx.x == 0 && bad) atomicExch(a.err + a.nd.slot[N], 1);
         return;
@@ -1097,10 +1103,9 @@ __global__ void __launch_bounds__(DNT) k_pdiag(FacArgs a, int k0, int phase) {
     // coupling between the halves as independent multiply-adds
     const int r = r0 + threadIdx.x;
     if (r < f) {
-        T* row = F + r;
         T x[16], y[16];
 #pragma unroll
-        for (int k = 0; k < 16; ++k) x[k] = k < nb ? row[(int64_t)(k0 + k) * f] : zero_t<T>();
+        for (int k = 0; k < 16; ++k) x[k] = k < nb ? F[pk64(r, k0 + k, f)] : zero_t<T>();
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
             T v = x[k];
@@ -1110,10 +1115,10 @@ __global__ void __launch_bounds__(DNT) k_pdiag(FacArgs a, int k0, int phase) {
         }
 #pragma unroll
         for (int k = 0; k < 16; ++k)
-            if (k < nb) row[(int64_t)(k0 + k) * f] = x[k];
+            if (k < nb) F[pk64(r, k0 + k, f)] = x[k];
         if (nb > 16) {
 #pragma unroll
-            for (int k = 0; k < 16; ++k) y[k] = 16 + k < nb ? row[(int64_t)(k0 + 16 + k) * f] : zero_t<T>();
+            for (int k = 0; k < 16; ++k) y[k] = 16 + k < nb ? F[pk64(r, k0 + 16 + k, f)] : zero_t<T>();
 #pragma unroll
             for (int j = 0; j < 16; ++j)
 #pragma unroll
@@ -1127,7 +1132,7 @@ __global__ void __launch_bounds__(DNT) k_pdiag(FacArgs a, int k0, int phase) {
             }
 #pragma unroll
             for (int k = 0; k < 16; ++k)
-                if (16 + k < nb) row[(int64_t)(k0 + 16 + k) * f] = y[k];
+                if (16 + k < nb) F[pk64(r, k0 + 16 + k, f)] = y[k];
         }
     }
 }
@@ -1153,9 +1158,9 @@ __global__ void __launch_bounds__(DNT) k_asm_cols(FacArgs a, int cw) {
     const int kb = c0, ke = min(c1, s);
     if (ke > kb)
         for (int i = threadIdx.x; i < nu; i += DNT) Us[i] = a.upool[a.ustart[N] + i];
-    for (int64_t i = (int64_t)c0 * f + threadIdx.x; i < (int64_t)c1 * f; i += DNT) F[i] = zero_t<T>();
+    for (int64_t i = pk64(c0, c0, f) + threadIdx.x; i < pk64(c1, c1, f); i += DNT) F[i] = zero_t<T>();
     __syncthreads();
-    if (ke > kb) assemble_entries<T>(F, f, pf, s, Us, nu, kb, ke, a);
+    if (ke > kb) assemble_entries<T, true>(F, f, pf, s, Us, nu, kb, ke, a);
 }
 
 template <class T>
@@ -1192,8 +1197,8 @@ __global__ void __launch_bounds__(DNT) k_asm_child(FacArgs a, int which, int cw)
             const int t = t0 + DNT * q;
             const int b = b0 + t / uc, i = t % uc;
             const bool ok = t < tot && i >= b;
-            pos[q] = ok ? (int64_t)rel[i] + (int64_t)rel[b] * f : -1;
-            const int64_t e = (int64_t)(sc + b) * fc + sc + i;
+            pos[q] = ok ? pk64(rel[i], rel[b], f) : -1;
+            const int64_t e = pk64(sc + i, sc + b, fc);
             v[q] = !ok ? make_double2(0.0, 0.0)
                        : (ccx ? reinterpret_cast<const double2*>(FC)[e] : make_double2(FC[e], 0.0));
         }
@@ -1240,13 +1245,13 @@ __global__ void __launch_bounds__(DNT, 4) k_pupd(FacArgs a, int k0) {
     if (threadIdx.x == 0) bad = 0;
     for (int idx = threadIdx.x; idx < PB * PB; idx += DNT) {
         const int i = idx % PB, j = idx / PB;
-        Ld[idx] = (i < nb2 && j < nb2 && i >= j) ? F[(int64_t)(c0 + i) + (int64_t)(c0 + j) * f] : zero_t<T>();
+        Ld[idx] = (i < nb2 && j < nb2 && i >= j) ? F[pk64(c0 + i, c0 + j, f)] : zero_t<T>();
     }
     __syncthreads();
     diag_factor_cta<T, PB, DNT>(Ld, nb2, &bad);
     for (int idx = threadIdx.x; idx < PB * PB; idx += DNT) {
         const int i = idx % PB, j = idx / PB;
-        if (i < nb2 && j < nb2 && i >= j) F[(int64_t)(c0 + i) + (int64_t)(c0 + j) * f] = Ld[idx];
+        if (i < nb2 && j < nb2 && i >= j) F[pk64(c0 + i, c0 + j, f)] = Ld[idx];
     }
     if (threadIdx.x == 0 && bad) atomicExch(a.err + a.nd.slot[N], 1);
 }
@@ -1274,7 +1279,7 @@ __global__ void __launch_bounds__(DNT) k_factor_sm(FacArgs a) {
     for (int i = threadIdx.x; i < f * f; i += DNT) S[i] = zero_t<T>();
     for (int i = threadIdx.x; i < nu; i += DNT) Us[i] = a.upool[a.ustart[N] + i];
     __syncthreads();
-    assemble_entries<T>(S, f, pf, s, Us, nu, 0, s, a);
+    assemble_entries<T, false>(S, f, pf, s, Us, nu, 0, s, a);
     __syncthreads();
     const int ch[2] = {a.nd.chA[N], a.nd.chB[N]};
     for (int c = 0; c < 2; ++c) {
@@ -1296,7 +1301,7 @@ __global__ void __launch_bounds__(DNT) k_factor_sm(FacArgs a) {
                 const int bcol = t / uc, i = t - bcol * uc;
                 const bool ok = t < tot && i >= bcol;
                 pos[q] = ok ? rel[i] + rel[bcol] * f : -1;
-                const int64_t e = (int64_t)(sc + bcol) * fc + sc + i;
+                const int64_t e = pk64(sc + i, sc + bcol, fc);
                 v[q] = !ok ? make_double2(0.0, 0.0)
                            : (ccx ? reinterpret_cast<const double2*>(FC)[e] : make_double2(FC[e], 0.0));
             }
@@ -1397,7 +1402,10 @@ __global__ void __launch_bounds__(DNT) k_factor_sm(FacArgs a) {
         __syncthreads();
     }
     T* F = front_ptr<T>(a.fpool, a.foff[N]);
-    for (int i = threadIdx.x; i < f * f; i += DNT) F[i] = S[i];
+    for (int j = 0; j < f; ++j) {  // square (shared) -> packed lower triangle (global)
+        const int64_t b = pk64(0, j, f);
+        for (int i = j + threadIdx.x; i < f; i += DNT) F[b + i] = S[i + j * f];
+    }
     if (threadIdx.x == 0 && bad) atomicExch(a.err + a.nd.slot[N], 1);
 }
 
@@ -1459,7 +1467,7 @@ __global__ void __launch_bounds__(256) k_factor_warp(FacArgs a, int nfront, int 
                 const int bcol = t / uc, i = t - bcol * uc;
                 const bool ok = t < tot && i >= bcol;
                 pos[q] = ok ? pk(rel[i], rel[bcol], f) : -1;
-                const int64_t e = (int64_t)(sc + bcol) * fc + sc + i;
+                const int64_t e = pk64(sc + i, sc + bcol, fc);
                 v[q] = !ok ? make_double2(0.0, 0.0)
                            : (ccx ? reinterpret_cast<const double2*>(FC)[e] : make_double2(FC[e], 0.0));
             }
@@ -1563,10 +1571,7 @@ __global__ void __launch_bounds__(256) k_factor_warp(FacArgs a, int nfront, int 
         __syncwarp();
     }
     T* F = front_ptr<T>(a.fpool, a.foff[N]);
-    for (int j = 0; j < f; ++j) {
-        const T* cs = S + pk(0, j, f);
-        for (int i = j + lane; i < f; i += 32) F[(int64_t)i + (int64_t)j * f] = cs[i];
-    }
+    for (int t = lane; t < np; t += 32) F[t] = S[t];  // same packed layout
     bad = __any_sync(FULL, bad);
     if (lane == 0 && bad) atomicExch(a.err + a.nd.slot[N], 1);
 }
@@ -1655,7 +1660,7 @@ __device__ void fwd_front(const SolArgs& a, int N, unsigned char* dsm, T* Lb) {
         const int nb = min(SB, s - k0);
         for (int idx = threadIdx.x; idx < SB * SB; idx += DNT) {
             const int i = idx % SB, j = idx / SB;
-            Lb[idx] = (i < nb && j < nb && i >= j) ? F[(int64_t)(k0 + i) + (int64_t)(k0 + j) * f] : zero_t<T>();
+            Lb[idx] = (i < nb && j < nb && i >= j) ? F[pk64(k0 + i, k0 + j, f)] : zero_t<T>();
         }
         __syncthreads();
         if (threadIdx.x < nb) dvi[threadIdx.x] = 1.0 / re(Lb[threadIdx.x + threadIdx.x * SB]);
@@ -1679,7 +1684,7 @@ __device__ void fwd_front(const SolArgs& a, int N, unsigned char* dsm, T* Lb) {
         for (int i = k0 + nb + threadIdx.x; i < f; i += DNT) {
             double2 acc = w[i];
             for (int k = 0; k < nb; ++k) {
-                const double2 t = vmul(F[(int64_t)i + (int64_t)(k0 + k) * f], w[k0 + k]);
+                const double2 t = vmul(F[pk64(i, k0 + k, f)], w[k0 + k]);
                 acc.x -= t.x;
                 acc.y -= t.y;
             }
@@ -1712,7 +1717,7 @@ __device__ void bwd_front(const SolArgs& a, int N, unsigned char* dsm, T* Lb) {
     const T* F = front_ptr<T>(a.fpool, a.foff[N]);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int k = warp; k < s; k += DNT / 32) {
-        const T* colk = F + (int64_t)k * f + s;
+        const T* colk = F + pk64(0, k, f) + s;  // column k, rows s..f-1
         double sx = 0.0, sy = 0.0;
         for (int q = lane; q < nu; q += 32) {
             const double2 v = vmul_cj(colk[q], xu[q]);
@@ -1731,7 +1736,7 @@ __device__ void bwd_front(const SolArgs& a, int N, unsigned char* dsm, T* Lb) {
         const int k0 = max(0, k1 - SB), nb = k1 - k0;
         for (int idx = threadIdx.x; idx < SB * SB; idx += DNT) {
             const int i = idx % SB, j = idx / SB;
-            Lb[idx] = (i < nb && j < nb && i >= j) ? F[(int64_t)(k0 + i) + (int64_t)(k0 + j) * f] : zero_t<T>();
+            Lb[idx] = (i < nb && j < nb && i >= j) ? F[pk64(k0 + i, k0 + j, f)] : zero_t<T>();
         }
         __syncthreads();
         if (threadIdx.x < nb) dvi[threadIdx.x] = 1.0 / re(Lb[threadIdx.x + threadIdx.x * SB]);
@@ -1754,7 +1759,7 @@ __device__ void bwd_front(const SolArgs& a, int N, unsigned char* dsm, T* Lb) {
         __syncthreads();
         for (int i = threadIdx.x; i < k0; i += DNT) {
             double2 acc = t[i];
-            const T* rowi = F + (int64_t)i * f;  // column i of L: entries L[k][i], k in the block
+            const T* rowi = F + pk64(0, i, f);  // column i of L: entries L[k][i], k in the block
             for (int k = 0; k < nb; ++k) {
                 const double2 v = vmul_cj(rowi[k0 + k], t[k0 + k]);
                 acc.x -= v.x;
