@@ -1262,11 +1262,11 @@ __global__ void __launch_bounds__(DNT, 4) k_pupd(FacArgs a, int k0) {
 // the rows below by one thread each, and the trailing lower triangle
 // (pivot columns and the update block alike) in 4x4 register tiles read
 // straight from shared memory. One coalesced write-back at the end.
-template <class T>
+template <class T, int SBK>
 __global__ void __launch_bounds__(DNT) k_factor_sm(FacArgs a) {
     extern __shared__ __align__(16) unsigned char dsm[];
     __shared__ int bad;
-    __shared__ double dsm_inv[NB];
+    __shared__ double dsm_inv[SBK];
     const int N = a.list[blockIdx.x];
     const int s = a.nd.npiv[N];
     const int nu = a.ucnt[N];
@@ -1312,14 +1312,14 @@ __global__ void __launch_bounds__(DNT) k_factor_sm(FacArgs a) {
         __syncthreads();
     }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int k0 = 0; k0 < s; k0 += NB) {
-        const int nb = min(NB, s - k0);
+    for (int k0 = 0; k0 < s; k0 += SBK) {
+        const int nb = min(SBK, s - k0);
         if (warp == 0) {  // diagonal block: lane i keeps row i
-            T r[NB];
+            T r[SBK];
 #pragma unroll
-            for (int j = 0; j < NB; ++j) r[j] = (lane < nb && j < nb) ? S[(k0 + lane) + (k0 + j) * f] : zero_t<T>();
+            for (int j = 0; j < SBK; ++j) r[j] = (lane < nb && j < nb) ? S[(k0 + lane) + (k0 + j) * f] : zero_t<T>();
 #pragma unroll
-            for (int k = 0; k < NB; ++k) {
+            for (int k = 0; k < SBK; ++k) {
                 if (k < nb) {
                     double d = re(shfl_t(r[k], k));
                     if (!(d > 0.0) || !isfinite(d)) {
@@ -1330,34 +1330,34 @@ __global__ void __launch_bounds__(DNT) k_factor_sm(FacArgs a) {
                     if (lane == k) r[k] = from_c<T>(make_double2(d * inv, 0.0));
                     else if (lane > k) r[k] = scale(r[k], inv);
 #pragma unroll
-                    for (int j = k + 1; j < NB; ++j) {
+                    for (int j = k + 1; j < SBK; ++j) {
                         const T ljk = shfl_t(r[k], j);
                         if (lane >= j && j < nb) fma_cj(r[j], scale(r[k], -1.0), ljk);
                     }
                 }
             }
 #pragma unroll
-            for (int j = 0; j < NB; ++j)
+            for (int j = 0; j < SBK; ++j)
                 if (lane < nb && j <= lane) S[(k0 + lane) + (k0 + j) * f] = r[j];
         }
         if (threadIdx.x < nb) dsm_inv[threadIdx.x] = 1.0 / re(S[(k0 + threadIdx.x) + (k0 + threadIdx.x) * f]);
         __syncthreads();
         for (int rr = k0 + nb + threadIdx.x; rr < f; rr += DNT) {
-            T x[NB];
+            T x[SBK];
 #pragma unroll
-            for (int k = 0; k < NB; ++k) x[k] = k < nb ? S[rr + (k0 + k) * f] : zero_t<T>();
+            for (int k = 0; k < SBK; ++k) x[k] = k < nb ? S[rr + (k0 + k) * f] : zero_t<T>();
 #pragma unroll
-            for (int k = 0; k < NB; ++k) {
+            for (int k = 0; k < SBK; ++k) {
                 if (k < nb) {
                     T v = x[k];
 #pragma unroll
-                    for (int j = 0; j < NB; ++j)
+                    for (int j = 0; j < SBK; ++j)
                         if (j < k) fma_cj(v, scale(x[j], -1.0), S[(k0 + k) + (k0 + j) * f]);
                     x[k] = scale(v, dsm_inv[k]);
                 }
             }
 #pragma unroll
-            for (int k = 0; k < NB; ++k)
+            for (int k = 0; k < SBK; ++k)
                 if (k < nb) S[rr + (k0 + k) * f] = x[k];
         }
         __syncthreads();
@@ -1417,7 +1417,7 @@ __global__ void __launch_bounds__(DNT) k_factor_sm(FacArgs a) {
 // the front's full-square storage (lower part) for the parent and the solves.
 __device__ __forceinline__ int pk(int i, int j, int f) { return j * (2 * f - j - 1) / 2 + i; }
 
-template <class T>
+template <class T, int WB>
 __global__ void __launch_bounds__(256) k_factor_warp(FacArgs a, int nfront, int wbytes) {
     extern __shared__ __align__(16) unsigned char dsm[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1478,14 +1478,14 @@ __global__ void __launch_bounds__(256) k_factor_warp(FacArgs a, int nfront, int 
         __syncwarp();
     }
     int bad = 0;
-    for (int k0 = 0; k0 < s; k0 += NB) {
-        const int nb = min(NB, s - k0);
+    for (int k0 = 0; k0 < s; k0 += WB) {
+        const int nb = min(WB, s - k0);
         {   // diagonal block: lane i keeps row i
-            T r[NB];
+            T r[WB];
 #pragma unroll
-            for (int j = 0; j < NB; ++j) r[j] = (lane < nb && j < nb && j <= lane) ? S[pk(k0 + lane, k0 + j, f)] : zero_t<T>();
+            for (int j = 0; j < WB; ++j) r[j] = (lane < nb && j < nb && j <= lane) ? S[pk(k0 + lane, k0 + j, f)] : zero_t<T>();
 #pragma unroll
-            for (int k = 0; k < NB; ++k) {
+            for (int k = 0; k < WB; ++k) {
                 if (k < nb) {
                     double d = re(shfl_t(r[k], k));
                     if (!(d > 0.0) || !isfinite(d)) {
@@ -1496,36 +1496,36 @@ __global__ void __launch_bounds__(256) k_factor_warp(FacArgs a, int nfront, int 
                     if (lane == k) r[k] = from_c<T>(make_double2(d * inv, 0.0));
                     else if (lane > k) r[k] = scale(r[k], inv);
 #pragma unroll
-                    for (int j = k + 1; j < NB; ++j) {
+                    for (int j = k + 1; j < WB; ++j) {
                         const T ljk = shfl_t(r[k], j);
                         if (lane >= j && j < nb) fma_cj(r[j], scale(r[k], -1.0), ljk);
                     }
                 }
             }
 #pragma unroll
-            for (int j = 0; j < NB; ++j)
+            for (int j = 0; j < WB; ++j)
                 if (lane < nb && j <= lane) S[pk(k0 + lane, k0 + j, f)] = r[j];
         }
         __syncwarp();
-        double di[NB];
+        double di[WB];
 #pragma unroll
-        for (int k = 0; k < NB; ++k) di[k] = k < nb ? 1.0 / re(S[pk(k0 + k, k0 + k, f)]) : 0.0;
+        for (int k = 0; k < WB; ++k) di[k] = k < nb ? 1.0 / re(S[pk(k0 + k, k0 + k, f)]) : 0.0;
         for (int rr = k0 + nb + lane; rr < f; rr += 32) {
-            T x[NB];
+            T x[WB];
 #pragma unroll
-            for (int k = 0; k < NB; ++k) x[k] = k < nb ? S[pk(rr, k0 + k, f)] : zero_t<T>();
+            for (int k = 0; k < WB; ++k) x[k] = k < nb ? S[pk(rr, k0 + k, f)] : zero_t<T>();
 #pragma unroll
-            for (int k = 0; k < NB; ++k) {
+            for (int k = 0; k < WB; ++k) {
                 if (k < nb) {
                     T v = x[k];
 #pragma unroll
-                    for (int j = 0; j < NB; ++j)
+                    for (int j = 0; j < WB; ++j)
                         if (j < k) fma_cj(v, scale(x[j], -1.0), S[pk(k0 + k, k0 + j, f)]);
                     x[k] = scale(v, di[k]);
                 }
             }
 #pragma unroll
-            for (int k = 0; k < NB; ++k)
+            for (int k = 0; k < WB; ++k)
                 if (k < nb) S[pk(rr, k0 + k, f)] = x[k];
         }
         __syncwarp();
@@ -2116,8 +2116,17 @@ int factor_level(DirectFactor* D, FacArgs fa, int l, int type, cudaStream_t s) {
         wb = (wb + 15) & ~(size_t)15;
         if (wb <= WARP_FRONT_BYTES && !getenv("PGCP_DIRECT_NO_WARP")) {
             const int wpc = (int)std::max<size_t>(1, std::min<size_t>(8, (96 * 1024) / wb));
-            PGCP_TRY(set_smem(k_factor_warp<T>, wb * wpc));
-            k_factor_warp<T><<<(n + wpc - 1) / wpc, 32 * wpc, wb * wpc, s>>>(fa, n, (int)wb);
+            const int wbk = env_int("PGCP_DIRECT_WB", 8);
+            if (wbk == 4) {
+                PGCP_TRY(set_smem(k_factor_warp<T, 4>, wb * wpc));
+                k_factor_warp<T, 4><<<(n + wpc - 1) / wpc, 32 * wpc, wb * wpc, s>>>(fa, n, (int)wb);
+            } else if (wbk == 8) {
+                PGCP_TRY(set_smem(k_factor_warp<T, 8>, wb * wpc));
+                k_factor_warp<T, 8><<<(n + wpc - 1) / wpc, 32 * wpc, wb * wpc, s>>>(fa, n, (int)wb);
+            } else {
+                PGCP_TRY(set_smem(k_factor_warp<T, 16>, wb * wpc));
+                k_factor_warp<T, 16><<<(n + wpc - 1) / wpc, 32 * wpc, wb * wpc, s>>>(fa, n, (int)wb);
+            }
             PGCP_LAUNCH_CHECK();
             return PGCP_OK;
         }
@@ -2126,8 +2135,13 @@ int factor_level(DirectFactor* D, FacArgs fa, int l, int type, cudaStream_t s) {
         const int maxf_t = D->lst_maxf[2 * l + type];
         const size_t sm = (size_t)maxf_t * maxf_t * tsz + (size_t)(D->lvl_maxu[l] + maxu_child) * 4 + 16;
         if (sm <= SM_FRONT_BYTES && !getenv("PGCP_DIRECT_NO_SMEM")) {
-            PGCP_TRY(set_smem(k_factor_sm<T>, sm));
-            k_factor_sm<T><<<n, DNT, sm, s>>>(fa);
+            if (env_int("PGCP_DIRECT_SB", 8) == 8) {
+                PGCP_TRY(set_smem(k_factor_sm<T, 8>, sm));
+                k_factor_sm<T, 8><<<n, DNT, sm, s>>>(fa);
+            } else {
+                PGCP_TRY(set_smem(k_factor_sm<T, 16>, sm));
+                k_factor_sm<T, 16><<<n, DNT, sm, s>>>(fa);
+            }
             PGCP_LAUNCH_CHECK();
             return PGCP_OK;
         }
