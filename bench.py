@@ -464,10 +464,15 @@ def main():
             if i == args.warmup:
                 torch.cuda.synchronize()
                 t0 = time.perf_counter()
+            ts = time.perf_counter()
             mesh = pg.TriMesh(Vn, Fn)
             gp, rep = pg.parameterize(mesh, Cn, "free", pairs=pairs)
             coords = gp.coords
             d2h = coords.nbytes + gp.provenance.nbytes  # both arrays cross PCIe as returned
+            if os.environ.get("PGCP_BENCH_VERBOSE"):
+                torch.cuda.synchronize()
+                print(f"e2e step {i}: {1e3 * (time.perf_counter() - ts):.2f} ms",
+                      {k: round(1e3 * v, 2) for k, v in rep.timings.items()}, file=sys.stderr, flush=True)
         torch.cuda.synchronize()
         et = (time.perf_counter() - t0) / args.steps
         e2e = {"value": n / et, "unit": UNIT, "ms_per_step": 1e3 * et, "h2d_bytes_per_step": int(h2d),

@@ -1949,6 +1949,14 @@ static int ws_acquire(size_t bytes, cudaStream_t s, int* slot_out, void** p_out)
         const size_t want = std::max<size_t>(bytes + bytes / 8, 1 << 20);
         PGCP_TRY_CUDA(cudaMalloc(&w.p, want));
         w.bytes = want;
+        if (getenv("PGCP_DIRECT_TIMING")) {
+            size_t cached = 0;
+            int nsl = 0;
+            for (const WsSlot& q : g_ws)
+                if (q.dev == dev) cached += q.bytes, ++nsl;
+            fprintf(stderr, "[direct workspace] slot %d sized %.3f GB (%d slots, %.2f GB cached)\n", best, 1e-9 * want,
+                    nsl, 1e-9 * cached);
+        }
     }
     WsSlot& w = g_ws[best];
     if (w.ready) PGCP_TRY_CUDA(cudaStreamWaitEvent(s, w.ready, 0));
