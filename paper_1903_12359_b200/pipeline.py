@@ -16,6 +16,7 @@ and the final device -> host copy of the coordinates.
 import ctypes
 import json
 import os
+import sys
 import threading
 import time
 from dataclasses import dataclass, field
@@ -269,7 +270,6 @@ def parameterize(mesh, cuts=None, mode="free", workers=1, seed=0, mobius_area=Fa
     # ~1.5 ms faster with device-resident inputs but 2-8 ms slower and
     # erratic end to end (host-array inputs), so the default stays here.
     prep_at_weld = overlap_prep and os.environ.get("PGCP_HPREP_AT", "flatten") == "weld"
-    hprep = {}
 
     def _flatten():
         try:
@@ -279,8 +279,37 @@ def parameterize(mesh, cuts=None, mode="free", workers=1, seed=0, mobius_area=Fa
         except BaseException as exc:  # re-raised on the caller's thread
             fres["err"] = exc
 
+    # three host threads hand the GIL back and forth around their native
+    # calls (flatten, Dirichlet preparation, planning): with the default 5 ms
+    # switch interval a thread returning from a call can wait that long
+    swi = sys.getswitchinterval()
+    if os.environ.get("PGCP_SWITCH_INTERVAL", "1") != "0":
+        sys.setswitchinterval(1e-4)
     worker = threading.Thread(target=_flatten, name="pgcp-flatten")
     worker.start()
+    # the Dirichlet preparation needs only the fixed vertices (every loop
+    # vertex, in slot order = submesh order, loop order): it starts now, in
+    # its own thread, beside the flatten and the host-side planning
+    hprep = {}
+    pworker = None
+    if welds:
+        nbl = np.array([len(c) for c in cycles], dtype=np.int64)
+        loop_gid_host = (voff[np.repeat(np.arange(K), nbl)] + loop_local).astype(np.int32)
+    if overlap_prep and not prep_at_weld:
+        def _hprep_early():
+            try:
+                torch.cuda.set_device(dev)
+                t_h = time.perf_counter()
+                with torch.cuda.stream(lo):
+                    lg = torch.as_tensor(loop_gid_host).to(dev)
+                    batch.harmonic_prepare(lg, comps=own, rtol=cfg.rtol, cluster=cfg.cluster, stream=lo)
+                hprep["t"] = time.perf_counter() - t_h
+                hprep["gid"] = lg
+            except BaseException as exc:
+                hprep["err"] = exc
+
+        pworker = threading.Thread(target=_hprep_early, name="pgcp-harmonic-prepare")
+        pworker.start()
     steps, plan, perr = [], None, None
     t_plan = time.perf_counter()
     try:
@@ -288,23 +317,27 @@ def parameterize(mesh, cuts=None, mode="free", workers=1, seed=0, mobius_area=Fa
             steps = plan_weld_schedule(part, mode, pairs=cfg.pairs if cfg.schedule == "pairs" else None)
         if welds:
             plan = WeldPlan(cycles, steps, mesh.n_vertices)
-            loop_gid_host = (voff[plan.slot_sub] + loop_local).astype(np.int32)
         timings["plan (overlapped)"] = time.perf_counter() - t_plan
-        if overlap_prep and not prep_at_weld:
-            t_h = time.perf_counter()
-            with torch.cuda.stream(lo):
-                loop_gid = torch.as_tensor(loop_gid_host).to(dev)
-                batch.harmonic_prepare(loop_gid, comps=own, rtol=cfg.rtol, cluster=cfg.cluster, stream=lo)
-            timings["harmonic prepare (overlapped)"] = time.perf_counter() - t_h
     except BaseException as exc:
         perr = exc
     worker.join()
+    # the preparation is joined here, before the weld: letting it run on into
+    # the weld was measured to starve the weld's cluster kernels now and then
+    # (one cfg-2 step in ten: weld 9 -> 63 ms)
+    if pworker is not None:
+        pworker.join()
+        if "err" in hprep and perr is None:
+            perr = hprep["err"]
+        if "t" in hprep:
+            timings["harmonic prepare (overlapped)"] = hprep["t"]
+    sys.setswitchinterval(swi)
     cur.wait_stream(hi)
     cur.wait_stream(lo)
     if "err" in fres:
         raise fres["err"]
     if perr is not None:
         raise perr
+    pworker = None
     z0, fst = fres["out"]
     clk.stop("flatten")
     report.solver = {"flatten_iters": [s["iters"] for s in fst], "flatten": batch.last_solve(0)}
@@ -316,8 +349,7 @@ def parameterize(mesh, cuts=None, mode="free", workers=1, seed=0, mobius_area=Fa
     else:
         # ---- welding on tracked boundary values ---------------------------------
         clk.start()
-        if not overlap_prep or prep_at_weld:
-            loop_gid = torch.as_tensor(loop_gid_host).to(dev)
+        loop_gid = torch.as_tensor(loop_gid_host).to(dev)
         hworker = None
         if prep_at_weld:
             lo.wait_stream(cur)
@@ -336,7 +368,8 @@ def parameterize(mesh, cuts=None, mode="free", workers=1, seed=0, mobius_area=Fa
             hworker.start()
         # with the preparation beside it, the weld runs on the high-priority
         # stream: its cluster launches get the SMs the factorization frees
-        wstream = hi if (hworker is not None and os.environ.get("PGCP_WELD_HI", "1") != "0") else cur
+        wstream = hi if ((hworker is not None or pworker is not None)
+                         and os.environ.get("PGCP_WELD_HI", "1") != "0") else cur
         if wstream is not cur:
             wstream.wait_stream(cur)
         try:
@@ -352,8 +385,9 @@ def parameterize(mesh, cuts=None, mode="free", workers=1, seed=0, mobius_area=Fa
                     out, _ = run_schedule(tv, plan.info, plan.src, plan.wb_off, plan.wb, cfg.hard_tol)
                     report.seam_residuals = [float(x) for x in out[:, 1]]
         except BaseException:
-            if hworker is not None:  # never leave the preparation running on the batch
-                hworker.join()
+            for w in (hworker, pworker):  # never leave the preparation running on the batch
+                if w is not None:
+                    w.join()
             raise
         if wstream is not cur:
             cur.wait_stream(wstream)
@@ -362,12 +396,13 @@ def parameterize(mesh, cuts=None, mode="free", workers=1, seed=0, mobius_area=Fa
             A, B = plan.exterior_candidates
             exterior = B if out[-1, 2] > 0 else A
         clk.stop("weld")
-        if hworker is not None:
-            hworker.join()
-            cur.wait_stream(lo)
-            if "err" in hprep:
-                raise hprep["err"]
-            timings["harmonic prepare (overlapped)"] = hprep["t"]
+        for w in (hworker, pworker):
+            if w is not None:
+                w.join()
+                cur.wait_stream(lo)
+                if "err" in hprep:
+                    raise hprep["err"]
+                timings["harmonic prepare (overlapped)"] = hprep["t"]
 
         if mode == "disk":
             clk.start()
