@@ -1931,7 +1931,7 @@ static int ws_acquire(size_t bytes, cudaStream_t s, int* slot_out, void** p_out)
         for (const WsSlot& w : g_ws)
             if (w.dev == dev) cached += w.bytes;
         PGCP_TRY_CUDA(cudaMemGetInfo(&free_b, &total_b));
-        const bool room = cached + bytes + bytes / 8 <= total_b / 2;
+        const bool room = cached + bytes + bytes * 3 / 10 <= total_b / 2;
         for (int i = 0; i < (int)g_ws.size() && best < 0 && !room; ++i)
             if (g_ws[i].dev == dev && !g_ws[i].busy) best = i;
         if (best < 0) {
@@ -1946,7 +1946,9 @@ static int ws_acquire(size_t bytes, cudaStream_t s, int* slot_out, void** p_out)
             w.p = nullptr;
             w.bytes = 0;
         }
-        const size_t want = std::max<size_t>(bytes + bytes / 8, 1 << 20);
+        // 30 % headroom: the flatten's and the Dirichlet system's buffers are
+        // close in size and are acquired concurrently in either order
+        const size_t want = std::max<size_t>(bytes + bytes * 3 / 10, 1 << 20);
         PGCP_TRY_CUDA(cudaMalloc(&w.p, want));
         w.bytes = want;
         if (getenv("PGCP_DIRECT_TIMING")) {
@@ -2157,7 +2159,8 @@ int factor_level(DirectFactor* D, FacArgs fa, int l, int type, cudaStream_t s) {
     PGCP_TRY(set_smem(k_factor<T>, smem));
     const int nt = schur_tiles(D->lvl_maxu[l]);
     const int maxs = D->lst_maxs[2 * l + type];
-    if (maxs <= FUSED_MAXS) {
+    static const int fused_maxs = env_int("PGCP_DIRECT_FUSED_MAXS", FUSED_MAXS);
+    if (maxs <= fused_maxs) {
         const bool inl = nt <= 1;
         k_factor<T><<<n, DNT, smem, s>>>(fa, inl ? FAC_SCHUR_INLINE : 0);
         PGCP_LAUNCH_CHECK();
