@@ -1,4 +1,7 @@
 // capi.cu -- extern "C" entry points of libpgcp_b200.so (include/pgcp_b200.h).
+#include <algorithm>
+#include <cstdlib>
+
 #include "batch.cuh"
 
 using namespace pgcp;
@@ -18,6 +21,24 @@ void keep_pool(int dev) {
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
         uint64_t thr = ~0ull;
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        // map the pool's working set once (PGCP_POOL_RESERVE_GB, default 8):
+        // growing it later (mapping memory while other threads allocate and
+        // launch) stalls the driver for milliseconds
+        const char* e = getenv("PGCP_POOL_RESERVE_GB");
+        const double gb = e ? atof(e) : 8.0;
+        size_t free_b = 0, total_b = 0;
+        if (gb > 0 && cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
+            const size_t want = std::min<size_t>((size_t)(gb * 1e9), free_b / 4);
+            void* p = nullptr;
+            int cur = 0;
+            cudaGetDevice(&cur);
+            cudaSetDevice(dev);
+            if (cudaMallocAsync(&p, want, 0) == cudaSuccess) {
+                cudaFreeAsync(p, 0);
+                cudaStreamSynchronize(0);
+            }
+            cudaSetDevice(cur);
+        }
     }
     cudaGetLastError();
     done[dev] = true;
