@@ -282,6 +282,59 @@ __global__ void k_nd_roots(int32_t nslot, const int64_t* __restrict__ uoff, int 
     }
 }
 
+// Boundary-last ordering of the DNCP system: every slot's loop unknowns form
+// its root front (eliminated last, complex), the interior gets the nested
+// dissection below it. The interior block of the factor is then the factor
+// of the Dirichlet system L_II (direct_solve_interior).
+__global__ void k_nd_bl_count(int64_t NU, const int32_t* __restrict__ uslot, const int32_t* __restrict__ urow,
+                              const uint8_t* __restrict__ onloop, int32_t* __restrict__ cnt2) {
+    GRID_STRIDE(u, NU) atomicAdd(cnt2 + 2 * uslot[u] + (onloop[urow[u]] ? 0 : 1), 1);
+}
+__global__ void k_nd_bl_roots(int32_t nslot, const int32_t* __restrict__ cnt2, int leafmax, NodeArrays nd) {
+    GRID_STRIDE(j, nslot) {
+        const int32_t nb = cnt2[2 * j], ni = cnt2[2 * j + 1];
+        const int64_t C = nslot + j;
+        nd.parent[j] = -1;                 // the loop's front
+        nd.chA[j] = (int32_t)C;
+        nd.chB[j] = -1;
+        nd.cnt[j] = nb;
+        nd.npiv[j] = nb;
+        nd.leaf[j] = 2;
+        nd.slot[j] = (int32_t)j;
+        nd.parent[C] = (int32_t)j;         // the interior's root region
+        nd.chA[C] = nd.chB[C] = -1;
+        nd.cnt[C] = ni;
+        nd.slot[C] = (int32_t)j;
+        nd.leaf[C] = ni <= leafmax;
+        nd.npiv[C] = ni <= leafmax ? ni : 0;
+    }
+}
+__global__ void k_nd_bl_init_u(int64_t NU, int32_t nslot, const int32_t* __restrict__ uslot,
+                               const int32_t* __restrict__ urow, const uint8_t* __restrict__ onloop,
+                               const int8_t* __restrict__ leaf, int32_t* __restrict__ reg,
+                               int32_t* __restrict__ node_of) {
+    GRID_STRIDE(u, NU) {
+        const int j = uslot[u];
+        if (onloop[urow[u]]) {
+            node_of[u] = j;
+            reg[u] = -1;
+            continue;
+        }
+        const int C = nslot + j;
+        if (leaf[C]) {
+            node_of[u] = C;
+            reg[u] = -1;
+        } else {
+            reg[u] = C;
+            node_of[u] = -1;
+        }
+    }
+}
+__global__ void k_d_rowel(int64_t NU, const int32_t* __restrict__ urow, const int32_t* __restrict__ elim,
+                          int32_t* __restrict__ rowel) {
+    GRID_STRIDE(u, NU) rowel[urow[u]] = elim[u];
+}
+
 __global__ void k_nd_init_u(int64_t NU, const int32_t* __restrict__ uslot, const int8_t* __restrict__ leaf,
                             int32_t* __restrict__ reg, int32_t* __restrict__ node_of) {
     GRID_STRIDE(u, NU) {
@@ -1817,9 +1870,11 @@ __device__ __forceinline__ void wait_flag(const int* flag, int* err) {
 // backward one) and wait for the fronts they depend on (children / parent),
 // whose tickets are smaller and so held by CTAs already running: no level
 // barriers, no per-level launches, real and complex fronts in one launch.
+// skip: fronts with id < skip are not solved (the loops' fronts in the
+// interior-only solve: their x stays 0, set beforehand)
 __global__ void __launch_bounds__(DNT) k_solve_pers(SolArgs a, const int32_t* __restrict__ order, int nn,
                                                     int* __restrict__ done, int* ticket,
-                                                    const int8_t* __restrict__ ntype, int backward) {
+                                                    const int8_t* __restrict__ ntype, int backward, int skip) {
     extern __shared__ __align__(16) unsigned char dsm[];
     __shared__ __align__(16) double2 Lb[SB * SB];
     __shared__ int sq;
@@ -1830,6 +1885,10 @@ __global__ void __launch_bounds__(DNT) k_solve_pers(SolArgs a, const int32_t* __
         __syncthreads();
         if (q >= nn) return;
         const int N = backward ? order[nn - 1 - q] : order[q];
+        if (N < skip) {
+            if (threadIdx.x == 0) st_release_gpu(done + N, 1);
+            continue;
+        }
         if (threadIdx.x == 0) {
             if (backward) {
                 const int P = a.nd.parent[N];
@@ -2031,6 +2090,8 @@ struct DirectFactor {
     DevBuf<double2> X;
     DevBuf<int32_t> err;
     DevBuf<int8_t> ntype;
+    bool boundary_last = false;   // level 0 = the loops' fronts (the interior block factors L_II)
+    DevBuf<int32_t> rowel;        // system row -> elimination index (-1: padding)
     DevBuf<int32_t> order;   // fronts deepest level first (the persistent solves' ticket order)
     DevBuf<int32_t> sync;    // [0] ticket counter, [1 + N] front N done
     // fronts per (level, type): nlist[lst_off[2 l + t], lst_off[2 l + t + 1])
@@ -2309,18 +2370,33 @@ int direct_factor(pgcp_batch* b, const DirectInput& in, DirectFactor** out, cuda
     PGCP_TRY(node_of.alloc(NU, s));
     PGCP_TRY(side.alloc(NU, s));
     PGCP_TRY(grp.alloc(NU, s));
-    k_nd_roots<<<grid_for(nslot, 128), 128, 0, s>>>(nslot, D->uoff.p, leafmax, nd);
-    PGCP_LAUNCH_CHECK();
-    k_nd_init_u<<<grid_for(NU, 256), 256, 0, s>>>(NU, D->uslot.p, D->leaf.p, reg.p, node_of.p);
-    PGCP_LAUNCH_CHECK();
+    D->boundary_last = in.cplx && in.onloop != nullptr;
+    if (D->boundary_last) {
+        DevBuf<int32_t> cnt2;
+        PGCP_TRY(cnt2.alloc(2 * (int64_t)nslot, s));
+        PGCP_TRY(cnt2.zero(s));
+        k_nd_bl_count<<<grid_for(NU, 256), 256, 0, s>>>(NU, D->uslot.p, D->urow.p, in.onloop, cnt2.p);
+        PGCP_LAUNCH_CHECK();
+        k_nd_bl_roots<<<grid_for(nslot, 128), 128, 0, s>>>(nslot, cnt2.p, leafmax, nd);
+        PGCP_LAUNCH_CHECK();
+        k_nd_bl_init_u<<<grid_for(NU, 256), 256, 0, s>>>(NU, nslot, D->uslot.p, D->urow.p, in.onloop, D->leaf.p,
+                                                        reg.p, node_of.p);
+        PGCP_LAUNCH_CHECK();
+    } else {
+        k_nd_roots<<<grid_for(nslot, 128), 128, 0, s>>>(nslot, D->uoff.p, leafmax, nd);
+        PGCP_LAUNCH_CHECK();
+        k_nd_init_u<<<grid_for(NU, 256), 256, 0, s>>>(NU, D->uslot.p, D->leaf.p, reg.p, node_of.p);
+        PGCP_LAUNCH_CHECK();
+    }
     DevBuf<int32_t> scan, ndst;  // ndst: [0..1] live level range, [2] overflow, [4..] per-level ranges
     PGCP_TRY(scan.alloc(ncap + 1, s));
     constexpr int MAXL = 96;
     PGCP_TRY(ndst.alloc(4 + 2 * MAXL, s));
     PGCP_TRY(ndst.zero(s));
+    const int level0 = D->boundary_last ? 1 : 0;  // boundary-last: level 0 = the loops' fronts
     {
-        const int32_t r0[2] = {0, nslot};
-        PGCP_TRY_CUDA(cudaMemcpyAsync(ndst.p, r0, sizeof(r0), cudaMemcpyHostToDevice, s));
+        const int32_t r0[6] = {D->boundary_last ? nslot : 0, D->boundary_last ? 2 * nslot : nslot, 0, 0, 0, nslot};
+        PGCP_TRY_CUDA(cudaMemcpyAsync(ndst.p, r0, sizeof(r0), cudaMemcpyHostToDevice, s));  // [4..5] = level 0
     }
     int32_t* rng = ndst.p;
     int32_t* hist = ndst.p + 4;
@@ -2329,7 +2405,7 @@ int direct_factor(pgcp_batch* b, const DirectInput& in, DirectFactor** out, cuda
     const int rgrid = 4 * 148;
     int nlev = 0;
     const bool nd_detail = env_int("PGCP_DIRECT_TIMING", 0) >= 2;
-    for (int level = 0;; ++level) {
+    for (int level = level0;; ++level) {
         if (level >= MAXL) {
             set_error("direct solver: nested dissection did not terminate");
             return DIRECT_FALLBACK;
@@ -2417,6 +2493,10 @@ int direct_factor(pgcp_batch* b, const DirectInput& in, DirectFactor** out, cuda
         PGCP_TRY(D->elim.alloc(NU, s));
         PGCP_TRY(D->perm.alloc(NU, s));
         k_nd_elim<<<grid_for(NU, 256), 256, 0, s>>>(NU, kout.p, vout.p, gstart.p, D->pfirst.p, D->elim.p, D->perm.p);
+        PGCP_LAUNCH_CHECK();
+        PGCP_TRY(D->rowel.alloc(D->rows, s));
+        PGCP_TRY(D->rowel.fill_bytes(0xff, s));
+        k_d_rowel<<<grid_for(NU, 256), 256, 0, s>>>(NU, D->urow.p, D->elim.p, D->rowel.p);
         PGCP_LAUNCH_CHECK();
     }
     pt.mark("postorder");
@@ -2676,7 +2756,8 @@ int direct_solve(DirectFactor* D, const double2* b_rows, double2* x_rows, cudaSt
         const int grid = std::max(1, std::min(per_sm * sms, D->nnodes));
         for (int bwd = 0; bwd < 2; ++bwd) {
             PGCP_TRY_CUDA(cudaMemsetAsync(D->sync.p + 1, 0, (size_t)(D->nnodes + 1) * sizeof(int), s));
-            k_solve_pers<<<grid, DNT, smem, s>>>(a, D->order.p, D->nnodes, D->sync.p + 2, D->sync.p + 1, D->ntype.p, bwd);
+            k_solve_pers<<<grid, DNT, smem, s>>>(a, D->order.p, D->nnodes, D->sync.p + 2, D->sync.p + 1, D->ntype.p, bwd,
+                                                 0);
             PGCP_LAUNCH_CHECK();
             pt.mark(bwd ? "backward" : "forward");
         }
@@ -2703,6 +2784,109 @@ int direct_solve(DirectFactor* D, const double2* b_rows, double2* x_rows, cudaSt
             set_error("direct solver: substitution dependency wait timed out");
             return PGCP_E_CUDA;
         }
+    }
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    D->solve_ms = ms;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return PGCP_OK;
+}
+
+namespace {
+__global__ void k_h2f_rhs(int64_t rows_h, const int32_t* __restrict__ h2f, const double2* __restrict__ bh,
+                          double2* __restrict__ bf) {
+    GRID_STRIDE(r, rows_h) {
+        const int f = h2f[r];
+        if (f >= 0) bf[f] = bh[r];
+    }
+}
+__global__ void k_zero_roots(int32_t nroot, const int64_t* __restrict__ pfirst, const int32_t* __restrict__ npiv,
+                             double2* __restrict__ X) {
+    const int j = blockIdx.x;
+    if (j >= nroot) return;
+    for (int k = threadIdx.x; k < npiv[j]; k += blockDim.x) X[pfirst[j] + k] = make_double2(0.0, 0.0);
+}
+__global__ void k_f2h_x(int64_t rows_h, const int32_t* __restrict__ h2f, const int32_t* __restrict__ rowel,
+                        const double2* __restrict__ X, double2* __restrict__ xh) {
+    GRID_STRIDE(r, rows_h) {
+        const int f = h2f[r];
+        const int e = f >= 0 ? rowel[f] : -1;
+        xh[r] = e >= 0 ? X[e] : make_double2(0.0, 0.0);
+    }
+}
+}  // namespace
+
+bool direct_is_boundary_last(const DirectFactor* F) { return F && F->boundary_last; }
+
+// The Dirichlet solve L_II x = b with the interior block of a boundary-last
+// DNCP factor (the interior rows of the scaled DNCP system are the scaled
+// Dirichlet system's): forward and backward sweeps over every front but the
+// loops', whose x is held at 0. h2f maps the Dirichlet system's rows to the
+// DNCP system's rows (-1: padding).
+int direct_solve_interior(DirectFactor* D, const int32_t* h2f, int64_t rows_h, const double2* b_h, double2* x_h,
+                          cudaStream_t s) {
+    if (!D->boundary_last) {
+        set_error("direct solver: interior solve needs a boundary-last factor");
+        return PGCP_E_INVALID;
+    }
+    cudaEvent_t e0, e1;
+    PGCP_TRY_CUDA(cudaEventCreate(&e0));
+    PGCP_TRY_CUDA(cudaEventCreate(&e1));
+    PGCP_TRY_CUDA(cudaEventRecord(e0, s));
+    DevBuf<double2> bf;
+    PGCP_TRY(bf.alloc(D->rows, s));
+    PGCP_TRY(bf.zero(s));
+    k_h2f_rhs<<<grid_for(rows_h, 256), 256, 0, s>>>(rows_h, h2f, b_h, bf.p);
+    PGCP_LAUNCH_CHECK();
+    SolArgs a;
+    a.nd = D->na();
+    a.pfirst = D->pfirst.p;
+    a.perm = D->perm.p;
+    a.urow = D->urow.p;
+    a.ucnt = D->ucnt.p;
+    a.ustart = D->ustart.p;
+    a.upool = D->upool.p;
+    a.foff = D->foff.p;
+    a.woff = D->woff.p;
+    a.fpool = D->fpool.p;
+    a.list = nullptr;
+    a.W = D->W.p;
+    a.X = D->X.p;
+    a.b = bf.p;
+    const int L = (int)D->levels.size();
+    int maxf = 0, maxu = 0;
+    for (int l = 0; l < L; ++l) {
+        maxf = std::max(maxf, D->lvl_maxf[l]);
+        maxu = std::max(maxu, D->lvl_maxu[l]);
+    }
+    const size_t smem = (size_t)maxf * sizeof(double2) + (size_t)maxu * 4 + 16;
+    PGCP_TRY(set_smem(k_solve_pers, smem));
+    int per_sm = 1, dev = 0, sms = 148;
+    PGCP_TRY_CUDA(cudaGetDevice(&dev));
+    PGCP_TRY_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    PGCP_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve_pers, DNT, smem));
+    const int grid = std::max(1, std::min(per_sm * sms, D->nnodes));
+    for (int bwd = 0; bwd < 2; ++bwd) {
+        if (bwd) {  // the loops' unknowns are the Dirichlet data: x_B = 0 in the eliminated form
+            k_zero_roots<<<D->nslot, 128, 0, s>>>(D->nslot, D->pfirst.p, D->npiv.p, D->X.p);
+            PGCP_LAUNCH_CHECK();
+        }
+        PGCP_TRY_CUDA(cudaMemsetAsync(D->sync.p + 1, 0, (size_t)(D->nnodes + 1) * sizeof(int), s));
+        k_solve_pers<<<grid, DNT, smem, s>>>(a, D->order.p, D->nnodes, D->sync.p + 2, D->sync.p + 1, D->ntype.p, bwd,
+                                             D->nslot);
+        PGCP_LAUNCH_CHECK();
+    }
+    k_f2h_x<<<grid_for(rows_h, 256), 256, 0, s>>>(rows_h, h2f, D->rowel.p, D->X.p, x_h);
+    PGCP_LAUNCH_CHECK();
+    PGCP_TRY_CUDA(cudaEventRecord(e1, s));
+    PGCP_TRY_CUDA(cudaEventSynchronize(e1));
+    int timeout_flag = 0;
+    PGCP_TRY(d2h_async(&timeout_flag, D->sync.p, sizeof(int), s));
+    PGCP_TRY(d2h_flush(s));
+    if (timeout_flag) {
+        set_error("direct solver: substitution dependency wait timed out");
+        return PGCP_E_CUDA;
     }
     float ms = 0;
     cudaEventElapsedTime(&ms, e0, e1);

@@ -27,6 +27,7 @@ struct DirectInput {
     const int2* cpl = nullptr;
     const double2* cplc = nullptr;
     bool cplx = false;                // complex Hermitian (DNCP coupling) vs real symmetric
+    const uint8_t* onloop = nullptr;  // per row: boundary-loop vertex (DNCP: order the loop last)
 };
 
 struct DirectFactor;
@@ -42,6 +43,11 @@ int direct_factor(pgcp_batch* b, const DirectInput& in, DirectFactor** out, cuda
 // x (rows) = A^-1 b (rows), Jacobi-scaled space; padding rows get 0
 int direct_solve(DirectFactor* F, const double2* b_rows, double2* x_rows, cudaStream_t s);
 void direct_free(DirectFactor* F);
+// boundary-last DNCP factor: its interior block is the Dirichlet system's factor
+bool direct_is_boundary_last(const DirectFactor* F);
+// x_h = L_II^-1 b_h with that interior block (h2f: Dirichlet row -> DNCP row)
+int direct_solve_interior(DirectFactor* F, const int32_t* h2f, int64_t rows_h, const double2* b_h, double2* x_h,
+                          cudaStream_t s);
 // last factorization: [nodes, levels, max front, real FMAs of the factorization,
 // factor ms (ordering + symbolic + numeric), last solve ms, front storage
 // bytes, unknowns, numeric-phase ms]

@@ -47,6 +47,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <memory>
 #include <mutex>
 
 #include "batch.cuh"
@@ -112,7 +113,11 @@ struct SolveSystem {
     // frees of a later rebuild or of pgcp_batch_destroy are ordered after it.
     // direct solver (direct.cu): multifrontal Cholesky instead of PCG
     bool use_direct = false;
-    DirectFactor* direct = nullptr;
+    std::shared_ptr<DirectFactor> direct;  // may be shared: a Dirichlet system borrows the DNCP factor
+    bool borrowed = false;                 // solve with the interior block of the flatten's factor
+    bool lazy_direct = false;              // prepared: factor (or borrow) at solve time
+    DevBuf<int32_t> h2f;                   // borrowed: this system's row -> the DNCP system's row
+    cudaStream_t direct_home = nullptr;    // stream the factor's buffers are freed on
     cudaStream_t home = nullptr;
     bool has_home = false;
     cudaEvent_t use_ev = nullptr;
@@ -129,7 +134,6 @@ struct SolveSystem {
     }
     ~SolveSystem() {
         if (use_ev) cudaEventDestroy(use_ev);
-        direct_free(direct);
     }
 };
 
@@ -2728,6 +2732,70 @@ int build_system(pgcp_batch* b, SolveSystem* S, bool dncp, const int32_t* d_pins
 
 // cluster shape, coarse space (two-level) and the per-shape column encoding:
 // everything of a solve that does not depend on the right-hand side
+// loop vertices among a system's rows (the unknown ones: pins have no row)
+__global__ void k_onloop(int32_t nslot, const int32_t* __restrict__ comps, const int64_t* __restrict__ loop_off,
+                         const int32_t* __restrict__ loop, const int64_t* __restrict__ sv_off,
+                         const int32_t* __restrict__ urow, uint8_t* __restrict__ onloop, int64_t total) {
+    GRID_STRIDE(t, total) {
+        int64_t acc = 0;
+        int j = 0;
+        for (; j < nslot; ++j) {
+            const int c = comps[j];
+            const int64_t nb = loop_off[c + 1] - loop_off[c];
+            if (t < acc + nb) break;
+            acc += nb;
+        }
+        if (j >= nslot) continue;
+        const int c = comps[j];
+        const int v = loop[loop_off[c] + (t - acc)];
+        const int r = urow[sv_off[j] + v];
+        if (r >= 0) onloop[r] = 1;
+    }
+}
+
+// Dirichlet row -> DNCP row of the same compact vertex (-1: padding)
+__global__ void k_h2f(int64_t rows, const int32_t* __restrict__ rowsrc, const int32_t* __restrict__ urow_f,
+                      int32_t* __restrict__ h2f) {
+    GRID_STRIDE(r, rows) {
+        const int e = rowsrc[r];
+        h2f[r] = e >= 0 ? urow_f[e] : -1;
+    }
+}
+
+// PGCP_DIRECT_BLAST=1: factor the DNCP system with every loop last and
+// solve the Dirichlet system with the interior block (no second
+// factorization). Measured on cfg 2: the Dirichlet preparation drops from
+// ~8 ms to 0.5 ms of GPU work, but the loops' 510-wide dense fronts put a
+// long serial chain into both substitution sweeps (flatten 12.5 -> 15.9 ms
+// standalone, step +3 ms), so the default keeps two factorizations.
+bool boundary_last_enabled() {
+    const char* e = getenv("PGCP_DIRECT_BLAST");
+    return e && atoi(e) != 0;
+}
+
+// A Dirichlet system over the same submeshes as the last DNCP solve can use
+// the interior block of that boundary-last factor: no factorization at all.
+int try_borrow(pgcp_batch* b, SolveSystem* S, cudaStream_t s) {
+    SolveSystem* F = static_cast<SolveSystem*>(b->sys[0]);
+    if (!F || F == S || S->dncp || !F->dncp || !F->use_direct || !F->direct || !F->setup_done) return 0;
+    if (!direct_is_boundary_last(F->direct.get()) || F->comps != S->comps) return 0;
+    S->direct = F->direct;
+    S->direct_home = F->direct_home;
+    S->borrowed = true;
+    PGCP_TRY(S->h2f.alloc(S->rows, s));
+    if (F->direct_home && F->direct_home != s) {  // the factor is complete before this stream uses it
+        cudaEvent_t ev;
+        PGCP_TRY_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        PGCP_TRY_CUDA(cudaEventRecord(ev, F->direct_home));
+        PGCP_TRY_CUDA(cudaStreamWaitEvent(s, ev, 0));
+        cudaEventDestroy(ev);
+    }
+    k_h2f<<<grid_for(S->rows, 256), 256, 0, s>>>(S->rows, S->rowsrc.p, F->urow.p, S->h2f.p);
+    PGCP_LAUNCH_CHECK();
+    S->setup_done = true;
+    return 1;
+}
+
 int setup_direct(pgcp_batch* b, SolveSystem* S, cudaStream_t s) {
     DirectInput in;
     in.nslot = S->nslot;
@@ -2745,6 +2813,22 @@ int setup_direct(pgcp_batch* b, SolveSystem* S, cudaStream_t s) {
     in.cpl = S->cpl.p;
     in.cplc = S->cplc.p;
     in.cplx = S->dncp;
+    DevBuf<uint8_t> onloop;
+    if (S->dncp && boundary_last_enabled()) {  // order every loop last: the interior block serves the Dirichlet solve
+        PGCP_TRY(onloop.alloc(S->rows, s));
+        PGCP_TRY(onloop.zero(s));
+        int64_t total = 0;
+        for (int j = 0; j < S->nslot; ++j) {
+            const int c = S->comps[j];
+            total += b->h_loop_off[c + 1] - b->h_loop_off[c];
+        }
+        if (total > 0) {
+            k_onloop<<<grid_for(total, 256), 256, 0, s>>>(S->nslot, S->d_comps.p, b->loop_off.p, b->loop.p,
+                                                        S->sv_off.p, S->urow.p, onloop.p, total);
+            PGCP_LAUNCH_CHECK();
+        }
+        in.onloop = onloop.p;
+    }
     DirectFactor* F = nullptr;
     const int rc = direct_factor(b, in, &F, s);
     if (rc == DIRECT_FALLBACK) {  // a front outgrew the kernels' bounds: plain PCG on the device
@@ -2752,8 +2836,9 @@ int setup_direct(pgcp_batch* b, SolveSystem* S, cudaStream_t s) {
         return PGCP_OK;
     }
     PGCP_TRY(rc);
-    direct_free(S->direct);
-    S->direct = F;
+    S->direct = std::shared_ptr<DirectFactor>(F, direct_free);
+    S->direct_home = s;
+    S->borrowed = false;
     S->setup_done = true;
     return PGCP_OK;
 }
@@ -2761,6 +2846,13 @@ int setup_direct(pgcp_batch* b, SolveSystem* S, cudaStream_t s) {
 int setup_solve(pgcp_batch* b, SolveSystem* S, const pgcp_solve_opts* o, cudaStream_t s) {
     const int32_t nslot = S->nslot;
     if (S->use_direct) {
+        if (!S->dncp && boundary_last_enabled()) {
+            // Dirichlet system: the DNCP factor's interior block when there is one
+            const int got = try_borrow(b, S, s);
+            if (got < 0) return got;
+            if (got) return PGCP_OK;
+            if (S->lazy_direct) return PGCP_OK;  // decide at solve time (the flatten may still be running)
+        }
         PGCP_TRY(setup_direct(b, S, s));
         if (S->use_direct) return PGCP_OK;
     }
@@ -2904,7 +2996,20 @@ int run_solve(pgcp_batch* b, SolveSystem* S, const pgcp_solve_opts* o, double* z
     PGCP_TRY_CUDA(cudaEventCreate(&e1));
     PGCP_TRY_CUDA(cudaEventRecord(e0, s));
     if (S->use_direct) {
-        PGCP_TRY(direct_solve(S->direct, S->b.p, S->x.p, s));
+        if (S->borrowed) {
+            PGCP_TRY(direct_solve_interior(S->direct.get(), S->h2f.p, S->rows, S->b.p, S->x.p, s));
+            // the factor's buffers are freed on the DNCP system's stream: order
+            // that after this solve
+            if (S->direct_home && S->direct_home != s) {
+                cudaEvent_t ev;
+                PGCP_TRY_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+                PGCP_TRY_CUDA(cudaEventRecord(ev, s));
+                PGCP_TRY_CUDA(cudaStreamWaitEvent(S->direct_home, ev, 0));
+                cudaEventDestroy(ev);
+            }
+        } else {
+            PGCP_TRY(direct_solve(S->direct.get(), S->b.p, S->x.p, s));
+        }
         k_fill_i32<<<grid_for(nslot, 128), 128, 0, s>>>(S->iters.p, nslot, 1);
         PGCP_LAUNCH_CHECK();
     } else {
@@ -3073,7 +3178,7 @@ int run_solve(pgcp_batch* b, SolveSystem* S, const pgcp_solve_opts* o, double* z
         t.bnorm = hres[8 * j + 4];
         t.status = PGCP_OK;
         bool finite = std::isfinite(t.true_res) && std::isfinite(t.xnorm);
-        if (S->use_direct && S->direct && direct_slot_status(S->direct)[j]) finite = false;  // pivot <= 0
+        if (S->use_direct && S->direct && direct_slot_status(S->direct.get())[j]) finite = false;  // pivot <= 0
         if (!finite) {
             t.status = PGCP_E_SOLVE;
         } else if (t.relres > rtol && t.iters >= A.maxit) {
@@ -3277,7 +3382,9 @@ int prepare_harmonic(pgcp_batch* b, const int32_t* comps, int32_t ncomp, const i
     }
     auto t0 = std::chrono::steady_clock::now();
     PGCP_TRY(build_system(b, S, false, nullptr, nullptr, S->fixed_gid_copy.p, nullptr, nfixed, s));
+    S->lazy_direct = true;  // the direct solver factors (or borrows the DNCP factor) at solve time
     PGCP_TRY(setup_solve(b, S, o, s));
+    S->lazy_direct = false;
     PGCP_TRY_CUDA(cudaStreamSynchronize(s));
     if (getenv("PGCP_PCG_TIMING"))
         fprintf(stderr, "[pcg timing] harmonic prepare (build + setup) %.2f ms (host, synchronised)\n",
@@ -3550,16 +3657,16 @@ void solve_summary(const pgcp_batch* b, int which, double* out) {
     // storage bytes, [16] tree nodes, [17] tree levels, [18] numeric-phase ms
     if (S->use_direct && S->direct) {
         double d[9];
-        direct_stats(S->direct, d);
-        out[10] = 1;
-        out[11] = d[3];
-        out[12] = d[4];
+        direct_stats(S->direct.get(), d);
+        out[10] = S->borrowed ? 2 : 1;  // 2: the DNCP factor's interior block (no factorization of its own)
+        out[11] = S->borrowed ? 0.0 : d[3];
+        out[12] = S->borrowed ? 0.0 : d[4];
         out[13] = d[5];
         out[14] = d[2];
         out[15] = d[6];
         out[16] = d[0];
         out[17] = d[1];
-        out[18] = d[8];
+        out[18] = S->borrowed ? 0.0 : d[8];
     }
 }
 

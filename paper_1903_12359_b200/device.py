@@ -309,7 +309,8 @@ class DeviceBatch:
         nat.check(nat.lib().pgcp_batch_last_solve(self.h, which, out, 19))
         r = {"kernel_ms": out[0], "iters_sum": out[1], "iters_max": out[2], "bytes": out[3],
              "stored_entries": out[4], "rows": out[5], "cluster": int(out[6]), "submeshes": int(out[7]),
-             "ref_bytes": out[8], "coarse_ms": out[9], "solver": "direct" if out[10] else "pcg"}
+             "ref_bytes": out[8], "coarse_ms": out[9], "solver": "direct" if out[10] else "pcg",
+             "borrowed": out[10] == 2}
         if out[10]:
             r.update({"fmas": out[11], "factor_ms": out[12], "solve_ms": out[13], "max_front": int(out[14]),
                       "front_bytes": out[15], "nodes": int(out[16]), "levels": int(out[17]),

@@ -123,3 +123,14 @@ def test_direct_is_default_and_pcg_selectable(cuda, monkeypatch):
     assert b.last_solve(0)["solver"] == "pcg"
     b.flatten(solver="direct")       # explicit beats the environment
     assert b.last_solve(0)["solver"] == "direct"
+
+
+def test_boundary_last_factor_serves_dirichlet(cuda, monkeypatch):
+    """PGCP_DIRECT_BLAST=1: the DNCP system is factored with every boundary
+    loop last; the Dirichlet solve then runs on the interior block of that
+    factor (no factorization of its own) and still matches SuperLU."""
+    from paper_1903_12359_b200 import generators as gen
+    monkeypatch.setenv("PGCP_DIRECT_BLAST", "1")
+    V, F, cuts = gen.height_field_case(97, 3, seed=4)
+    b, z = _check_vs_oracle(V, F, cuts, 1e-9, 1e-12)
+    assert b.last_solve(1)["borrowed"] and b.last_solve(1)["fmas"] == 0
