@@ -1674,6 +1674,34 @@ struct SolArgs {
 
 constexpr int SB = 32;  // pivots per block of the blocked substitutions
 
+// TMA bulk prefetch of a byte range into L2 (no registers, no completion to
+// wait for): a front's pivot columns, issued as soon as the front is known,
+// so the column loads that follow hit L2 instead of HBM
+__device__ __forceinline__ void l2_prefetch(const void* p, int64_t bytes) {
+    uintptr_t a0 = reinterpret_cast<uintptr_t>(p) & ~(uintptr_t)15;
+    int64_t n = (int64_t)((reinterpret_cast<uintptr_t>(p) + bytes - a0) & ~(uintptr_t)15);  // rounded down
+    while (n > 0) {
+        const uint32_t c = (uint32_t)min(n, (int64_t)(1 << 20));
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"(c) : "memory");
+        a0 += c;
+        n -= c;
+    }
+}
+// the pivot columns of front N: s (2f - s + 1) / 2 entries from its start
+__device__ __forceinline__ void prefetch_panel(const SolArgs& a, int N, bool cplx) {
+    const int s = a.nd.npiv[N], f = s + a.ucnt[N];
+    const int64_t n = (int64_t)s * (2 * f - s + 1) / 2;
+    if (cplx) l2_prefetch(front_ptr<double2>(a.fpool, a.foff[N]), n * (int64_t)sizeof(double2));
+    else l2_prefetch(front_ptr<double>(a.fpool, a.foff[N]), n * (int64_t)sizeof(double));
+}
+// right-hand side into elimination order: X[e] = b[row of e] (the forward
+// step of a front then reads its pivots' entries contiguously)
+__global__ void k_perm_rhs(int64_t NU, const int32_t* __restrict__ perm, const int32_t* __restrict__ urow,
+                           const double2* __restrict__ b, double2* __restrict__ X) {
+    GRID_STRIDE(e, NU) X[e] = b[urow[perm[e]]];
+}
+
+
 // Forward step of front N (CTA-wide): gather the pivots' right-hand side and
 // the children's partial sums (fixed order; L2 loads: written by other CTAs
 // of the same persistent launch), blocked substitution with L_PP (one warp
@@ -1690,7 +1718,7 @@ __device__ void fwd_front(const SolArgs& a, int N, unsigned char* dsm, T* Lb) {
     int32_t* Us = reinterpret_cast<int32_t*>(w + f);
     for (int i = threadIdx.x; i < nu; i += DNT) Us[i] = a.upool[a.ustart[N] + i];
     for (int k = threadIdx.x; k < f; k += DNT)
-        w[k] = k < s ? a.b[a.urow[a.perm[pf + k]]] : make_double2(0.0, 0.0);
+        w[k] = k < s ? a.X[pf + k] : make_double2(0.0, 0.0);  // b in elimination order (k_perm_rhs)
     __syncthreads();
     const int ch[2] = {a.nd.chA[N], a.nd.chB[N]};
     for (int c = 0; c < 2; ++c) {
@@ -1709,11 +1737,14 @@ __device__ void fwd_front(const SolArgs& a, int N, unsigned char* dsm, T* Lb) {
     }
     const T* F = front_ptr<T>(a.fpool, a.foff[N]);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __shared__ int64_t coff[SB];  // pk64(0, k0 + k, f): column starts of the block
     for (int k0 = 0; k0 < s; k0 += SB) {
         const int nb = min(SB, s - k0);
+        if (threadIdx.x < SB) coff[threadIdx.x] = pk64(0, k0 + min((int)threadIdx.x, nb - 1), f);
+        __syncthreads();
         for (int idx = threadIdx.x; idx < SB * SB; idx += DNT) {
             const int i = idx % SB, j = idx / SB;
-            Lb[idx] = (i < nb && j < nb && i >= j) ? F[pk64(k0 + i, k0 + j, f)] : zero_t<T>();
+            Lb[idx] = (i < nb && j < nb && i >= j) ? F[coff[j] + k0 + i] : zero_t<T>();
         }
         __syncthreads();
         if (threadIdx.x < nb) dvi[threadIdx.x] = 1.0 / re(Lb[threadIdx.x + threadIdx.x * SB]);
@@ -1736,10 +1767,17 @@ __device__ void fwd_front(const SolArgs& a, int N, unsigned char* dsm, T* Lb) {
         __syncthreads();
         for (int i = k0 + nb + threadIdx.x; i < f; i += DNT) {
             double2 acc = w[i];
-            for (int k = 0; k < nb; ++k) {
-                const double2 t = vmul(F[pk64(i, k0 + k, f)], w[k0 + k]);
-                acc.x -= t.x;
-                acc.y -= t.y;
+            for (int kc = 0; kc < nb; kc += 16) {  // 16 loads in flight, then the FMAs
+                T l[16];
+#pragma unroll
+                for (int k = 0; k < 16; ++k) l[k] = kc + k < nb ? F[coff[kc + k] + i] : zero_t<T>();
+#pragma unroll
+                for (int k = 0; k < 16; ++k)
+                    if (kc + k < nb) {
+                        const double2 t = vmul(l[k], w[k0 + kc + k]);
+                        acc.x -= t.x;
+                        acc.y -= t.y;
+                    }
             }
             w[i] = acc;
         }
@@ -1772,6 +1810,7 @@ __device__ void bwd_front(const SolArgs& a, int N, unsigned char* dsm, T* Lb) {
     for (int k = warp; k < s; k += DNT / 32) {
         const T* colk = F + pk64(0, k, f) + s;  // column k, rows s..f-1
         double sx = 0.0, sy = 0.0;
+#pragma unroll 4
         for (int q = lane; q < nu; q += 32) {
             const double2 v = vmul_cj(colk[q], xu[q]);
             sx += v.x;
@@ -1812,11 +1851,18 @@ __device__ void bwd_front(const SolArgs& a, int N, unsigned char* dsm, T* Lb) {
         __syncthreads();
         for (int i = threadIdx.x; i < k0; i += DNT) {
             double2 acc = t[i];
-            const T* rowi = F + pk64(0, i, f);  // column i of L: entries L[k][i], k in the block
-            for (int k = 0; k < nb; ++k) {
-                const double2 v = vmul_cj(rowi[k0 + k], t[k0 + k]);
-                acc.x -= v.x;
-                acc.y -= v.y;
+            const T* rowi = F + pk64(0, i, f) + k0;  // column i of L: entries L[k][i], k in the block
+            for (int kc = 0; kc < nb; kc += 16) {  // 16 loads in flight, then the FMAs
+                T l[16];
+#pragma unroll
+                for (int k = 0; k < 16; ++k) l[k] = kc + k < nb ? rowi[kc + k] : zero_t<T>();
+#pragma unroll
+                for (int k = 0; k < 16; ++k)
+                    if (kc + k < nb) {
+                        const double2 v = vmul_cj(l[k], t[k0 + kc + k]);
+                        acc.x -= v.x;
+                        acc.y -= v.y;
+                    }
             }
             t[i] = acc;
         }
@@ -1872,12 +1918,14 @@ __device__ __forceinline__ void wait_flag(const int* flag, int* err) {
 // barriers, no per-level launches, real and complex fronts in one launch.
 // skip: fronts with id < skip are not solved (the loops' fronts in the
 // interior-only solve: their x stays 0, set beforehand)
-__global__ void __launch_bounds__(DNT) k_solve_pers(SolArgs a, const int32_t* __restrict__ order, int nn,
+__global__ void __launch_bounds__(DNT, 6) k_solve_pers(SolArgs a, const int32_t* __restrict__ order, int nn,
                                                     int* __restrict__ done, int* ticket,
-                                                    const int8_t* __restrict__ ntype, int backward, int skip) {
+                                                    const int8_t* __restrict__ ntype, int backward, int skip,
+                                                    unsigned long long* __restrict__ trace) {
     extern __shared__ __align__(16) unsigned char dsm[];
     __shared__ __align__(16) double2 Lb[SB * SB];
     __shared__ int sq;
+    unsigned long long tr0 = 0, tr1 = 0;
     for (;;) {
         if (threadIdx.x == 0) sq = atomicAdd(ticket, 1);
         __syncthreads();
@@ -1890,6 +1938,7 @@ __global__ void __launch_bounds__(DNT) k_solve_pers(SolArgs a, const int32_t* __
             continue;
         }
         if (threadIdx.x == 0) {
+            if (trace) tr0 = gtimer();
             if (backward) {
                 const int P = a.nd.parent[N];
                 if (P >= 0) wait_flag(done + P, ticket - 1);
@@ -1898,6 +1947,8 @@ __global__ void __launch_bounds__(DNT) k_solve_pers(SolArgs a, const int32_t* __
                 if (A >= 0) wait_flag(done + A, ticket - 1);
                 if (B >= 0) wait_flag(done + B, ticket - 1);
             }
+            prefetch_panel(a, N, ntype[N] != 0);
+            if (trace) tr1 = gtimer();
         }
         __syncthreads();
         if (backward) {
@@ -1909,7 +1960,287 @@ __global__ void __launch_bounds__(DNT) k_solve_pers(SolArgs a, const int32_t* __
         }
         __threadfence();
         __syncthreads();
-        if (threadIdx.x == 0) st_release_gpu(done + N, 1);
+        if (threadIdx.x == 0) {
+            st_release_gpu(done + N, 1);
+            if (trace) {
+                trace[3 * N] = tr0;
+                trace[3 * N + 1] = tr1;
+                trace[3 * N + 2] = gtimer();
+            }
+        }
+    }
+}
+
+// ---- warp-per-front substitutions for the small fronts (the deep levels:
+// tens of thousands of fronts with f <= SW_F rows, s <= SW_S pivots). One
+// warp owns a front: no CTA barriers, 4 warps of a CTA on 4 fronts, every
+// resident warp of the GPU on its own front. L columns are read SWC at a
+// time with every load of the chunk in flight before the chain consumes
+// them (one memory round trip per chunk instead of one per pivot).
+constexpr int SW_NS = 4;             // rows per lane (forward)
+constexpr int SW_F = 32 * SW_NS;     // largest front on the warp path
+constexpr int SW_NP = 2;             // pivot columns per lane (backward)
+constexpr int SW_S = 32 * SW_NP;     // most pivots on the warp path
+constexpr int SWC = 4;               // columns per chunk (forward chain)
+constexpr int SWQ = 8;               // update rows per chunk (backward GEMV)
+constexpr int SWK = 8;               // chain steps per chunk (backward)
+
+// Forward step by one warp: lane l holds rows l, l+32, ... of w in registers;
+// column k of L (rows k..f-1, contiguous in the packed front) is one
+// coalesced load per slot; y_k is broadcast from the owner lane.
+template <class T>
+__device__ void fwd_front_w(const SolArgs& a, int N, double2* w, int32_t* Us, int lane) {
+    const int s = a.nd.npiv[N];
+    const int nu = a.ucnt[N];
+    const int f = s + nu;
+    const int64_t pf = a.pfirst[N];
+    const int32_t* U = a.upool + a.ustart[N];
+    for (int i = lane; i < nu; i += 32) Us[i] = U[i];
+    for (int k = lane; k < f; k += 32) w[k] = k < s ? a.X[pf + k] : make_double2(0.0, 0.0);
+    __syncwarp();
+    {   // both children's partial sums: loads of both issued together, then
+        // added in fixed order (A, then B) for bitwise-repeatable results
+        const int A = a.nd.chA[N], B = a.nd.chB[N];
+        const int ua = A >= 0 ? a.ucnt[A] : 0, ub = B >= 0 ? a.ucnt[B] : 0;
+        const int32_t* UA = A >= 0 ? a.upool + a.ustart[A] : nullptr;
+        const int32_t* UB = B >= 0 ? a.upool + a.ustart[B] : nullptr;
+        const double2* WA = A >= 0 ? a.W + a.woff[A] + a.nd.npiv[A] : nullptr;
+        const double2* WB = B >= 0 ? a.W + a.woff[B] + a.nd.npiv[B] : nullptr;
+        const int um = max(ua, ub);
+        for (int i0 = 0; i0 < um; i0 += 32) {
+            const int i = i0 + lane;
+            int pa = -1, pb = -1;
+            double2 va = make_double2(0.0, 0.0), vb = va;
+            if (i < ua) {
+                pa = UA[i];
+                va = __ldcg(WA + i);
+            }
+            if (i < ub) {
+                pb = UB[i];
+                vb = __ldcg(WB + i);
+            }
+            if (pa >= 0) {
+                const int p = front_pos(pa, pf, s, Us, nu);
+                w[p].x += va.x;
+                w[p].y += va.y;
+            }
+            __syncwarp();
+            if (pb >= 0) {
+                const int p = front_pos(pb, pf, s, Us, nu);
+                w[p].x += vb.x;
+                w[p].y += vb.y;
+            }
+            __syncwarp();
+        }
+    }
+    double2 r[SW_NS];
+#pragma unroll
+    for (int j = 0; j < SW_NS; ++j) {
+        const int i = lane + 32 * j;
+        r[j] = i < f ? w[i] : make_double2(0.0, 0.0);
+    }
+    const T* F = front_ptr<T>(a.fpool, a.foff[N]);
+    int64_t col = 0;  // pk64(0, k, f): column k starts at col + k
+    for (int k0 = 0; k0 < s; k0 += SWC) {
+        T l[SWC][SW_NS];
+        int64_t cc = col;
+#pragma unroll
+        for (int c = 0; c < SWC; ++c) {
+            const int k = k0 + c;
+#pragma unroll
+            for (int j = 0; j < SW_NS; ++j) {
+                const int i = lane + 32 * j;
+                l[c][j] = (k < s && i >= k && i < f) ? F[cc + i] : zero_t<T>();
+            }
+            cc += f - k - 1;
+        }
+        col = cc;
+#pragma unroll
+        for (int c = 0; c < SWC; ++c) {
+            const int k = k0 + c;
+            if (k >= s) break;
+            const int jk = k >> 5, lk = k & 31;
+            double2 v = r[0];
+            double d = re(l[c][0]);
+#pragma unroll
+            for (int j = 1; j < SW_NS; ++j)
+                if (j == jk) {
+                    v = r[j];
+                    d = re(l[c][j]);
+                }
+            const double dv = 1.0 / d;
+            double2 y = make_double2(v.x * dv, v.y * dv);
+            y.x = __shfl_sync(FULL, y.x, lk);
+            y.y = __shfl_sync(FULL, y.y, lk);
+#pragma unroll
+            for (int j = 0; j < SW_NS; ++j) {
+                const int i = lane + 32 * j;
+                if (i == k) {
+                    r[j] = y;
+                } else if (i > k && i < f) {
+                    const double2 t = vmul(l[c][j], y);
+                    r[j].x -= t.x;
+                    r[j].y -= t.y;
+                }
+            }
+        }
+    }
+    double2* WN = a.W + a.woff[N];
+#pragma unroll
+    for (int j = 0; j < SW_NS; ++j) {
+        const int i = lane + 32 * j;
+        if (i < f) {
+            WN[i] = r[j];
+            if (i < s) a.X[pf + i] = r[j];
+        }
+    }
+}
+
+// Backward step by one warp: lane l owns pivot columns l, l+32 (x_k and its
+// running right-hand side). The update rows' contribution is a per-lane walk
+// down the lane's own column (no reductions); the chain k = s-1..0 then
+// broadcasts x_k and every lane i < k subtracts conj(L[k][i]) x_k.
+template <class T>
+__device__ void bwd_front_w(const SolArgs& a, int N, double2* xs, int lane) {
+    const int s = a.nd.npiv[N];
+    if (s == 0) return;
+    const int nu = a.ucnt[N];
+    const int f = s + nu;
+    const int64_t pf = a.pfirst[N];
+    const int32_t* U = a.upool + a.ustart[N];
+    for (int i = lane; i < nu; i += 32) xs[i] = __ldcg(a.X + U[i]);
+    __syncwarp();
+    const T* F = front_ptr<T>(a.fpool, a.foff[N]);
+    double2 acc[SW_NP];
+    int64_t ck[SW_NP];
+#pragma unroll
+    for (int j = 0; j < SW_NP; ++j) {
+        const int k = lane + 32 * j;
+        ck[j] = pk64(0, min(k, max(s - 1, 0)), f);
+        acc[j] = k < s ? a.X[pf + k] : make_double2(0.0, 0.0);
+    }
+    double dinv[SW_NP];
+#pragma unroll
+    for (int j = 0; j < SW_NP; ++j) {
+        const int k = lane + 32 * j;
+        dinv[j] = k < s ? 1.0 / re(F[ck[j] + k]) : 0.0;
+    }
+    for (int q0 = 0; q0 < nu; q0 += SWQ) {
+        T l[SWQ][SW_NP];
+#pragma unroll
+        for (int q = 0; q < SWQ; ++q)
+#pragma unroll
+            for (int j = 0; j < SW_NP; ++j)
+                l[q][j] = (q0 + q < nu && lane + 32 * j < s) ? F[ck[j] + s + q0 + q] : zero_t<T>();
+#pragma unroll
+        for (int q = 0; q < SWQ; ++q) {
+            if (q0 + q >= nu) break;
+            const double2 xq = xs[q0 + q];
+#pragma unroll
+            for (int j = 0; j < SW_NP; ++j) {
+                const double2 t = vmul_cj(l[q][j], xq);
+                acc[j].x -= t.x;
+                acc[j].y -= t.y;
+            }
+        }
+    }
+    for (int k1 = s; k1 > 0; k1 -= SWK) {
+        T l[SWK][SW_NP];  // l[c][j] = L[k1-1-c][lane + 32 j]
+#pragma unroll
+        for (int c = 0; c < SWK; ++c)
+#pragma unroll
+            for (int j = 0; j < SW_NP; ++j) {
+                const int k = k1 - 1 - c, i = lane + 32 * j;
+                l[c][j] = (k >= 0 && i < k) ? F[ck[j] + k] : zero_t<T>();
+            }
+#pragma unroll
+        for (int c = 0; c < SWK; ++c) {
+            const int k = k1 - 1 - c;
+            if (k < 0) break;
+            const int jk = k >> 5, lk = k & 31;
+            double2 v = acc[0];
+            double dv = dinv[0];
+#pragma unroll
+            for (int j = 1; j < SW_NP; ++j)
+                if (j == jk) {
+                    v = acc[j];
+                    dv = dinv[j];
+                }
+            double2 x = make_double2(v.x * dv, v.y * dv);
+            x.x = __shfl_sync(FULL, x.x, lk);
+            x.y = __shfl_sync(FULL, x.y, lk);
+#pragma unroll
+            for (int j = 0; j < SW_NP; ++j) {
+                const int i = lane + 32 * j;
+                if (i == k) {
+                    acc[j] = x;
+                } else if (i < k) {
+                    const double2 t = vmul_cj(l[c][j], x);
+                    acc[j].x -= t.x;
+                    acc[j].y -= t.y;
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < SW_NP; ++j) {
+        const int k = lane + 32 * j;
+        if (k < s) a.X[pf + k] = acc[j];
+    }
+}
+
+// persistent warp-per-front sweep over order[0, nn) (forward) or its reverse
+// (backward); the same ticket / done-flag protocol as k_solve_pers, per warp
+template <bool backward, int MINB>
+__global__ void __launch_bounds__(DNT, MINB) k_solve_warp(SolArgs a, const int32_t* __restrict__ order, int nn,
+                                                    int* __restrict__ done, int* ticket,
+                                                    const int8_t* __restrict__ ntype, int skip,
+                                                    unsigned long long* __restrict__ trace) {
+    __shared__ __align__(16) double2 wbuf[DNT / 32][SW_F];
+    __shared__ int32_t ubuf[DNT / 32][SW_F];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (;;) {
+        int q = 0;
+        if (lane == 0) q = atomicAdd(ticket, 1);
+        q = __shfl_sync(FULL, q, 0);
+        if (q >= nn) return;
+        const int N = backward ? order[nn - 1 - q] : order[q];
+        if (N < skip) {
+            if (lane == 0) st_release_gpu(done + N, 1);
+            continue;
+        }
+        unsigned long long tr0 = 0, tr1 = 0;
+        if (lane == 0) {
+            if (trace) tr0 = gtimer();
+            if (backward) {
+                const int P = a.nd.parent[N];
+                if (P >= 0) wait_flag(done + P, ticket - 1);
+            } else {
+                const int A = a.nd.chA[N], B = a.nd.chB[N];
+                if (A >= 0) wait_flag(done + A, ticket - 1);
+                if (B >= 0) wait_flag(done + B, ticket - 1);
+            }
+            prefetch_panel(a, N, ntype[N] != 0);
+            if (trace) tr1 = gtimer();
+        }
+        __syncwarp();
+        if (backward) {
+            if (ntype[N]) bwd_front_w<double2>(a, N, wbuf[warp], lane);
+            else bwd_front_w<double>(a, N, wbuf[warp], lane);
+        } else {
+            if (ntype[N]) fwd_front_w<double2>(a, N, wbuf[warp], ubuf[warp], lane);
+            else fwd_front_w<double>(a, N, wbuf[warp], ubuf[warp], lane);
+        }
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) {
+            st_release_gpu(done + N, 1);
+            if (trace) {
+                trace[3 * N] = tr0;
+                trace[3 * N + 1] = tr1;
+                trace[3 * N + 2] = gtimer();
+            }
+        }
     }
 }
 
@@ -2691,6 +3022,133 @@ int direct_factor(pgcp_batch* b, const DirectInput& in, DirectFactor** out, cuda
     return PGCP_OK;
 }
 
+// The forward and backward sweeps as persistent launches: the deep levels
+// whose fronts fit a warp (f <= SW_F, s <= SW_S: closed under descent, as
+// every level below qualifies too) warp-per-front (k_solve_warp), the rest
+// CTA-per-front (k_solve_pers). Both share the done flags; the ticket
+// counter restarts per launch. zero_roots: x of the roots (< skip) := 0
+// before the backward sweep (the interior-only solve).
+int solve_trace_report(DirectFactor* D, const unsigned long long* tr, int bwd, int grid, int per_sm, size_t smem,
+                       cudaStream_t s);
+__global__ void k_zero_roots(int32_t nroot, const int64_t* __restrict__ pfirst, const int32_t* __restrict__ npiv,
+                             double2* __restrict__ X) {
+    const int j = blockIdx.x;
+    if (j >= nroot) return;
+    for (int k = threadIdx.x; k < npiv[j]; k += blockDim.x) X[pfirst[j] + k] = make_double2(0.0, 0.0);
+}
+int solve_sweeps(DirectFactor* D, const SolArgs& a, int skip, bool zero_roots, cudaStream_t s, PhaseTimer* pt) {
+    const int L = (int)D->levels.size();
+    const int nn = D->nnodes;
+    int lcut = L;
+    if (env_int("PGCP_DIRECT_SOLVE_WARP", 1))
+        for (int l = L - 1; l >= 0; --l) {
+            const int ms = std::max(D->lst_maxs[2 * l], D->lst_maxs[2 * l + 1]);
+            if (D->lvl_maxf[l] > SW_F || ms > SW_S) break;
+            lcut = l;
+        }
+    int nsmall = 0;
+    for (int l = lcut; l < L; ++l) nsmall += D->levels[l].second - D->levels[l].first;
+    const int nbig = nn - nsmall;
+    int maxf = 0, maxu = 0;
+    for (int l = 0; l < lcut; ++l) {
+        maxf = std::max(maxf, D->lvl_maxf[l]);
+        maxu = std::max(maxu, D->lvl_maxu[l]);
+    }
+    const size_t smem = (size_t)maxf * sizeof(double2) + (size_t)maxu * 4 + 16;
+    int dev = 0, sms = 148, per_sm = 1, per_sm_w = 1;
+    PGCP_TRY_CUDA(cudaGetDevice(&dev));
+    PGCP_TRY_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    if (nbig > 0) {
+        PGCP_TRY(set_smem(k_solve_pers, smem));
+        PGCP_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve_pers, DNT, smem));
+    }
+    int per_sm_wb = 1;
+    using WarpSweep = void (*)(SolArgs, const int32_t*, int, int*, int*, const int8_t*, int, unsigned long long*);
+    WarpSweep kw[2] = {k_solve_warp<false, 4>, k_solve_warp<true, 4>};
+    switch (env_int("PGCP_DIRECT_SOLVE_MINB", 4)) {  // register cap (resident CTAs per SM) of the warp sweeps
+        case 6: kw[0] = k_solve_warp<false, 6>; kw[1] = k_solve_warp<true, 6>; break;
+        case 8: kw[0] = k_solve_warp<false, 8>; kw[1] = k_solve_warp<true, 8>; break;
+        default: break;
+    }
+    PGCP_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_w, kw[0], DNT, 0));
+    PGCP_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_wb, kw[1], DNT, 0));
+    const int grid = std::max(1, std::min(per_sm * sms, nbig));
+    const int grid_wf = std::max(1, std::min(per_sm_w * sms, (nsmall + DNT / 32 - 1) / (DNT / 32)));
+    const int grid_wb = std::max(1, std::min(per_sm_wb * sms, (nsmall + DNT / 32 - 1) / (DNT / 32)));
+    const bool trace_on = getenv("PGCP_DIRECT_SOLVE_TRACE") != nullptr;
+    DevBuf<unsigned long long> tr;
+    if (trace_on) PGCP_TRY(tr.alloc(3 * (int64_t)nn, s));
+    int* ticket = D->sync.p + 1;
+    int* done = D->sync.p + 2;
+    k_perm_rhs<<<grid_for(D->NU, 256), 256, 0, s>>>(D->NU, D->perm.p, D->urow.p, a.b, D->X.p);
+    PGCP_LAUNCH_CHECK();
+    for (int bwd = 0; bwd < 2; ++bwd) {
+        if (bwd && zero_roots) {
+            k_zero_roots<<<D->nslot, 128, 0, s>>>(D->nslot, D->pfirst.p, D->npiv.p, D->X.p);
+            PGCP_LAUNCH_CHECK();
+        }
+        PGCP_TRY_CUDA(cudaMemsetAsync(ticket, 0, (size_t)(nn + 1) * sizeof(int), s));
+        for (int part = 0; part < 2; ++part) {
+            const bool warp_part = (part == 0) != (bwd != 0);  // forward: small first; backward: big first
+            if (warp_part ? nsmall == 0 : nbig == 0) continue;
+            if (part == 1) PGCP_TRY_CUDA(cudaMemsetAsync(ticket, 0, sizeof(int), s));
+            if (warp_part)
+                kw[bwd]<<<bwd ? grid_wb : grid_wf, DNT, 0, s>>>(a, D->order.p, nsmall, done, ticket, D->ntype.p, skip,
+                                                              trace_on ? tr.p : nullptr);
+            else
+                k_solve_pers<<<grid, DNT, smem, s>>>(a, D->order.p + nsmall, nbig, done, ticket, D->ntype.p, bwd, skip,
+                                                     trace_on ? tr.p : nullptr);
+            PGCP_LAUNCH_CHECK();
+        }
+        if (pt) pt->mark(bwd ? "backward" : "forward");
+        if (trace_on) {
+            fprintf(stderr, "[solve trace] warp path: levels >= %d (%d fronts, grid %d, %d/SM)\n", lcut, nsmall,
+                    bwd ? grid_wb : grid_wf, bwd ? per_sm_wb : per_sm_w);
+            PGCP_TRY(solve_trace_report(D, tr.p, bwd, grid, per_sm, smem, s));
+        }
+    }
+    return PGCP_OK;
+}
+
+// PGCP_DIRECT_SOLVE_TRACE=1: per-level timeline of one persistent sweep from
+// the per-front globaltimer stamps (ticket drawn, dependencies met, done)
+int solve_trace_report(DirectFactor* D, const unsigned long long* tr, int bwd, int grid, int per_sm,
+                              size_t smem, cudaStream_t s) {
+    const int nn = D->nnodes;
+    std::vector<unsigned long long> h(3 * (size_t)nn);
+    PGCP_TRY_CUDA(cudaMemcpyAsync(h.data(), tr, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    PGCP_TRY_CUDA(cudaStreamSynchronize(s));
+    unsigned long long t0 = ~0ull, tend = 0;
+    for (int N = 0; N < nn; ++N) {
+        t0 = std::min(t0, h[3 * N]);
+        tend = std::max(tend, h[3 * N + 2]);
+    }
+    fprintf(stderr, "[solve trace] %s grid %d (%d/SM, smem %zu B) span %.1f us\n", bwd ? "backward" : "forward", grid,
+            per_sm, smem, 1e-3 * (double)(tend - t0));
+    for (size_t l = 0; l < D->levels.size(); ++l) {
+        const int b = D->levels[l].first, e = D->levels[l].second;
+        double wsum = 0, wmax = 0, ksum = 0, kmax = 0;
+        unsigned long long lo = ~0ull, hi = 0, wl = ~0ull;
+        for (int N = b; N < e; ++N) {
+            const double w = 1e-3 * (double)(h[3 * N + 1] - h[3 * N]), k = 1e-3 * (double)(h[3 * N + 2] - h[3 * N + 1]);
+            wsum += w;
+            ksum += k;
+            wmax = std::max(wmax, w);
+            kmax = std::max(kmax, k);
+            lo = std::min(lo, h[3 * N]);
+            wl = std::min(wl, h[3 * N + 1]);
+            hi = std::max(hi, h[3 * N + 2]);
+        }
+        const int n = e - b;
+        fprintf(stderr,
+                "[solve trace]   L%zu fronts %d  first ticket %.1f  first start %.1f  last done %.1f us  "
+                "work mean %.2f max %.2f  wait mean %.2f max %.2f us\n",
+                l, n, 1e-3 * (double)(lo - t0), 1e-3 * (double)(wl - t0), 1e-3 * (double)(hi - t0), ksum / n, kmax,
+                wsum / n, wmax);
+    }
+    return PGCP_OK;
+}
+
 int direct_solve(DirectFactor* D, const double2* b_rows, double2* x_rows, cudaStream_t s) {
     PGCP_TRY_CUDA(cudaMemsetAsync(x_rows, 0, (size_t)D->rows * sizeof(double2), s));
     if (D->NU == 0) return PGCP_OK;
@@ -2741,27 +3199,11 @@ int direct_solve(DirectFactor* D, const double2* b_rows, double2* x_rows, cudaSt
         return PGCP_OK;
     };
     const char* ep = getenv("PGCP_DIRECT_PERSIST");
-    if (!(ep && atoi(ep) == 0)) {  // one persistent, dependency-driven launch per sweep
-        int maxf = 0, maxu = 0;
-        for (int l = 0; l < L; ++l) {
-            maxf = std::max(maxf, D->lvl_maxf[l]);
-            maxu = std::max(maxu, D->lvl_maxu[l]);
-        }
-        const size_t smem = (size_t)maxf * sizeof(double2) + (size_t)maxu * 4 + 16;
-        PGCP_TRY(set_smem(k_solve_pers, smem));
-        int per_sm = 1, dev = 0, sms = 148;
-        PGCP_TRY_CUDA(cudaGetDevice(&dev));
-        PGCP_TRY_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        PGCP_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve_pers, DNT, smem));
-        const int grid = std::max(1, std::min(per_sm * sms, D->nnodes));
-        for (int bwd = 0; bwd < 2; ++bwd) {
-            PGCP_TRY_CUDA(cudaMemsetAsync(D->sync.p + 1, 0, (size_t)(D->nnodes + 1) * sizeof(int), s));
-            k_solve_pers<<<grid, DNT, smem, s>>>(a, D->order.p, D->nnodes, D->sync.p + 2, D->sync.p + 1, D->ntype.p, bwd,
-                                                 0);
-            PGCP_LAUNCH_CHECK();
-            pt.mark(bwd ? "backward" : "forward");
-        }
+    if (!(ep && atoi(ep) == 0)) {  // persistent, dependency-driven launches
+        PGCP_TRY(solve_sweeps(D, a, 0, false, s, &pt));
     } else {
+        k_perm_rhs<<<grid_for(D->NU, 256), 256, 0, s>>>(D->NU, D->perm.p, D->urow.p, a.b, D->X.p);
+        PGCP_LAUNCH_CHECK();
         for (int l = L - 1; l >= 0; --l) {
             PGCP_TRY(launch(true, l, 0));
             PGCP_TRY(launch(true, l, 1));
@@ -2800,12 +3242,6 @@ __global__ void k_h2f_rhs(int64_t rows_h, const int32_t* __restrict__ h2f, const
         const int f = h2f[r];
         if (f >= 0) bf[f] = bh[r];
     }
-}
-__global__ void k_zero_roots(int32_t nroot, const int64_t* __restrict__ pfirst, const int32_t* __restrict__ npiv,
-                             double2* __restrict__ X) {
-    const int j = blockIdx.x;
-    if (j >= nroot) return;
-    for (int k = threadIdx.x; k < npiv[j]; k += blockDim.x) X[pfirst[j] + k] = make_double2(0.0, 0.0);
 }
 __global__ void k_f2h_x(int64_t rows_h, const int32_t* __restrict__ h2f, const int32_t* __restrict__ rowel,
                         const double2* __restrict__ X, double2* __restrict__ xh) {
@@ -2854,29 +3290,7 @@ int direct_solve_interior(DirectFactor* D, const int32_t* h2f, int64_t rows_h, c
     a.W = D->W.p;
     a.X = D->X.p;
     a.b = bf.p;
-    const int L = (int)D->levels.size();
-    int maxf = 0, maxu = 0;
-    for (int l = 0; l < L; ++l) {
-        maxf = std::max(maxf, D->lvl_maxf[l]);
-        maxu = std::max(maxu, D->lvl_maxu[l]);
-    }
-    const size_t smem = (size_t)maxf * sizeof(double2) + (size_t)maxu * 4 + 16;
-    PGCP_TRY(set_smem(k_solve_pers, smem));
-    int per_sm = 1, dev = 0, sms = 148;
-    PGCP_TRY_CUDA(cudaGetDevice(&dev));
-    PGCP_TRY_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    PGCP_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve_pers, DNT, smem));
-    const int grid = std::max(1, std::min(per_sm * sms, D->nnodes));
-    for (int bwd = 0; bwd < 2; ++bwd) {
-        if (bwd) {  // the loops' unknowns are the Dirichlet data: x_B = 0 in the eliminated form
-            k_zero_roots<<<D->nslot, 128, 0, s>>>(D->nslot, D->pfirst.p, D->npiv.p, D->X.p);
-            PGCP_LAUNCH_CHECK();
-        }
-        PGCP_TRY_CUDA(cudaMemsetAsync(D->sync.p + 1, 0, (size_t)(D->nnodes + 1) * sizeof(int), s));
-        k_solve_pers<<<grid, DNT, smem, s>>>(a, D->order.p, D->nnodes, D->sync.p + 2, D->sync.p + 1, D->ntype.p, bwd,
-                                             D->nslot);
-        PGCP_LAUNCH_CHECK();
-    }
+    PGCP_TRY(solve_sweeps(D, a, D->nslot, true, s, nullptr));
     k_f2h_x<<<grid_for(rows_h, 256), 256, 0, s>>>(rows_h, h2f, D->rowel.p, D->X.p, x_h);
     PGCP_LAUNCH_CHECK();
     PGCP_TRY_CUDA(cudaEventRecord(e1, s));
