@@ -53,6 +53,10 @@ PGCP_API int pgcp_abi_version(void);
 PGCP_API const char* pgcp_last_error(void);
 /* number of kernels this library has launched in the process */
 PGCP_API unsigned long long pgcp_launch_count(void);
+/* diagnostics: the direct solver's workspace cache on the current device --
+ * out[0] slots, out[1] cached bytes, out[2] slot (re)allocations since load,
+ * out[3] host ms spent in them (cudaFree + cudaMalloc) */
+PGCP_API int pgcp_workspace_stats(double* out, int nout);
 
 /* -------------------------------------------------------------------------
  * Batch of disk-type submeshes of one parent mesh, device resident.

@@ -84,6 +84,7 @@ _SIGS = {
     "pgcp_batch_stitch": ([_VP, _VP, ctypes.c_int, _D, _D, _VP, _VP, _VP, _VP, _VP, _VP], ctypes.c_int),
     "pgcp_batch_last_solve": ([_VP, ctypes.c_int, _PD, ctypes.c_int], ctypes.c_int),
     "pgcp_launch_count": ([], ctypes.c_ulonglong),
+    "pgcp_workspace_stats": ([_PD, ctypes.c_int], ctypes.c_int),
     "pgcp_face_layout": ([_VP, _VP, _I64, _VP, _VP], ctypes.c_int),
     "pgcp_beltrami": ([_VP, _VP, _VP, _VP, _I64, _VP, _PI64, _VP], ctypes.c_int),
     "pgcp_corner_angles": ([_VP, ctypes.c_int, _VP, _I64, _VP, _VP, _VP], ctypes.c_int),

@@ -1,4 +1,5 @@
 // common.cu -- errors, device-wide scans, stable counting sort.
+#include <mutex>
 #include <atomic>
 
 #include "common.cuh"
@@ -213,6 +214,19 @@ int stable_counting_sort(const int32_t* keys, int64_t n, int32_t nkeys, int32_t*
 }
 
 namespace {
+// Pinned staging buffers are process-wide and never freed: a host thread
+// takes one on its first read and hands it back to the free list when it
+// exits. (cudaMallocHost / cudaFreeHost per thread cost a page-pinning call
+// and a device-wide synchronisation every time the pipeline's short-lived
+// worker threads came and went: 0.1-0.5 s outliers in the flatten and the
+// Dirichlet preparation.)
+struct PinBuf {
+    unsigned char* buf = nullptr;
+    size_t cap = 0;
+};
+std::mutex g_pin_mu;
+std::vector<PinBuf> g_pin_free;
+
 struct PinStage {
     unsigned char* buf = nullptr;
     size_t cap = 0, used = 0;
@@ -222,7 +236,31 @@ struct PinStage {
     };
     std::vector<Pending> pend;
     ~PinStage() {
-        if (buf) cudaFreeHost(buf);
+        if (!buf) return;
+        std::lock_guard<std::mutex> lock(g_pin_mu);
+        g_pin_free.push_back({buf, cap});
+    }
+    // a buffer of at least `bytes`: the largest free one if it fits, else a new one
+    int take(size_t bytes) {
+        {
+            std::lock_guard<std::mutex> lock(g_pin_mu);
+            if (buf) g_pin_free.push_back({buf, cap});  // too small: back to the list
+            buf = nullptr;
+            cap = 0;
+            int best = -1;
+            for (int i = 0; i < (int)g_pin_free.size(); ++i)
+                if (g_pin_free[i].cap >= bytes && (best < 0 || g_pin_free[i].cap < g_pin_free[best].cap)) best = i;
+            if (best >= 0) {
+                buf = g_pin_free[best].buf;
+                cap = g_pin_free[best].cap;
+                g_pin_free.erase(g_pin_free.begin() + best);
+                return PGCP_OK;
+            }
+        }
+        const size_t want = bytes < (1u << 20) ? (1u << 20) : bytes + bytes / 4;
+        PGCP_TRY_CUDA(cudaMallocHost((void**)&buf, want));
+        cap = want;
+        return PGCP_OK;
     }
 };
 thread_local PinStage g_pin;
@@ -233,14 +271,7 @@ int d2h_async(void* host, const void* dev, size_t bytes, cudaStream_t s) {
     const size_t off = (p.used + 15) & ~(size_t)15;
     if (off + bytes > p.cap) {
         if (!p.pend.empty()) PGCP_TRY(d2h_flush(s));  // queued copies go out first
-        if (bytes > p.cap) {
-            if (p.buf) PGCP_TRY_CUDA(cudaFreeHost(p.buf));
-            p.buf = nullptr;
-            p.cap = 0;
-            const size_t want = bytes < (1u << 20) ? (1u << 20) : bytes + bytes / 4;
-            PGCP_TRY_CUDA(cudaMallocHost((void**)&p.buf, want));
-            p.cap = want;
-        }
+        if (bytes > p.cap) PGCP_TRY(p.take(bytes));
         return d2h_async(host, dev, bytes, s);
     }
     PGCP_TRY_CUDA(cudaMemcpyAsync(p.buf + off, dev, bytes, cudaMemcpyDeviceToHost, s));

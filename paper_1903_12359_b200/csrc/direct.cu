@@ -2305,6 +2305,8 @@ struct WsSlot {
 };
 static std::mutex g_ws_mu;
 static std::vector<WsSlot> g_ws;
+static long long g_ws_grows = 0;  // slot (re)allocations since load
+static double g_ws_grow_ms = 0;   // host time spent in them (cudaFree + cudaMalloc)
 
 static int ws_acquire(size_t bytes, cudaStream_t s, int* slot_out, void** p_out) {
     int dev = 0;
@@ -2330,6 +2332,7 @@ static int ws_acquire(size_t bytes, cudaStream_t s, int* slot_out, void** p_out)
             g_ws[best].dev = dev;
         }
         WsSlot& w = g_ws[best];
+        const auto t_grow = std::chrono::steady_clock::now();
         if (w.p) {
             if (w.ready) PGCP_TRY_CUDA(cudaEventSynchronize(w.ready));
             PGCP_TRY_CUDA(cudaFree(w.p));
@@ -2341,6 +2344,8 @@ static int ws_acquire(size_t bytes, cudaStream_t s, int* slot_out, void** p_out)
         const size_t want = std::max<size_t>(bytes + bytes * 3 / 10, 1 << 20);
         PGCP_TRY_CUDA(cudaMalloc(&w.p, want));
         w.bytes = want;
+        ++g_ws_grows;
+        g_ws_grow_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_grow).count();
         if (getenv("PGCP_DIRECT_TIMING")) {
             size_t cached = 0;
             int nsl = 0;
@@ -3311,3 +3316,24 @@ int direct_solve_interior(DirectFactor* D, const int32_t* h2f, int64_t rows_h, c
 }
 
 }  // namespace pgcp
+
+// diagnostics: the direct solver's workspace cache on the current device
+// (out[0] slots, out[1] cached bytes, out[2] slot (re)allocations since the
+// library was loaded, out[3] host ms spent in them)
+extern "C" PGCP_API int pgcp_workspace_stats(double* out, int nout) {
+    if (!out || nout < 4) {
+        pgcp::set_error("pgcp_workspace_stats: invalid arguments");
+        return PGCP_E_INVALID;
+    }
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(pgcp::g_ws_mu);
+    double slots = 0, bytes = 0;
+    for (const pgcp::WsSlot& w : pgcp::g_ws)
+        if (w.dev == dev) slots += 1, bytes += (double)w.bytes;
+    out[0] = slots;
+    out[1] = bytes;
+    out[2] = (double)pgcp::g_ws_grows;
+    out[3] = pgcp::g_ws_grow_ms;
+    return PGCP_OK;
+}
