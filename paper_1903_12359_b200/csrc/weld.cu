@@ -76,18 +76,21 @@ __device__ __forceinline__ bool cabs_lt(double2 a, double t) {
     return cabs_(a) < t;
 }
 
-// numpy's complex division (Smith's method with a reciprocal)
+// numpy's complex division (Smith's method with a reciprocal). The two
+// orientations are one instruction stream with selects (same operations,
+// same roundings): lanes of a warp that fall on different sides of
+// |Re b| >= |Im b| no longer run both halves one after the other.
 __device__ double2 cdiv(double2 a, double2 b) {
-    double abr = fabs(b.x), abi = fabs(b.y);
-    if (abr >= abi) {
-        if (abr == 0.0 && abi == 0.0) return C(a.x / abr, a.y / abi);
-        double rat = b.y / b.x;
-        double scl = 1.0 / (b.x + b.y * rat);
-        return C((a.x + a.y * rat) * scl, (a.y - a.x * rat) * scl);
-    }
-    double rat = b.x / b.y;
-    double scl = 1.0 / (b.y + b.x * rat);
-    return C((a.x * rat + a.y) * scl, (a.y * rat - a.x) * scl);
+    const double abr = fabs(b.x), abi = fabs(b.y);
+    if (abr == 0.0 && abi == 0.0) return C(a.x / abr, a.y / abi);
+    const bool rb = abr >= abi;
+    const double p = rb ? b.x : b.y, q = rb ? b.y : b.x;  // |p| >= |q|
+    const double u = rb ? a.x : a.y, v = rb ? a.y : a.x;
+    const double rat = q / p;
+    const double scl = 1.0 / fma(q, rat, p);
+    // rb: ((a.x + a.y rat), (a.y - a.x rat)) scl; else ((a.x rat + a.y), (a.y rat - a.x)) scl
+    const double im = fma(-u, rat, v) * scl;
+    return C(fma(v, rat, u) * scl, rb ? im : -im);
 }
 
 // |(x, y)|: sqrt(x^2 + y^2) with one rounding of the sum of squares when both
@@ -120,19 +123,51 @@ __device__ double2 csqrt_(double2 z) {
         double r = sqrt(0.5 * fabs(im));
         return C(r, copysign(r, im));
     }
-    double d = fast_hypot(re, im);
-    double r, s;
-    if (re > 0) {
-        r = sqrt(0.5 * (d + re));
-        s = 0.5 * (im / r);
-    } else {
-        s = sqrt(0.5 * (d - re));
-        r = fabs(0.5 * (im / s));
-    }
-    return C(r, copysign(s, im));
+    // re > 0: r = sqrt((d + re) / 2), s = im / 2r; else s = sqrt((d - re) / 2),
+    // r = |im / 2s| -- one stream with selects (no divergence across lanes)
+    const double d = fast_hypot(re, im);
+    const double big = sqrt(0.5 * (d + fabs(re)));
+    const double small = 0.5 * (im / big);
+    const bool pos = re > 0;
+    return C(pos ? big : fabs(small), copysign(pos ? small : big, im));
 }
 
 __device__ __forceinline__ int rec_side(int flags, int k) { return (int)(int8_t)((flags >> (16 + 8 * k)) & 0xff); }
+
+// principal sqrt of w for Re w != 0, Im w != 0 and moderate magnitudes: the
+// csqrt_ formula with one rsqrt for sqrt((d + |re|) / 2) and the division by
+// it (within a few ulps of csqrt_; one transcendental fewer on the chain)
+__device__ __forceinline__ bool csqrt_fast(double2 w, double2& out) {
+    const double m = fmax(fabs(w.x), fabs(w.y)), n = fmin(fabs(w.x), fabs(w.y));
+    if (!(m < 1e150 && n > 1e-150)) return false;
+    const double d = sqrt(fma(w.x, w.x, w.y * w.y));
+    const double h = 0.5 * (d + fabs(w.x));
+    const double rs = rsqrt(h);
+    const double big = h * rs, small = 0.5 * w.y * rs;
+    out = (w.x > 0) ? C(big, small) : C(fabs(small), copysign(big, w.y));
+    return true;
+}
+
+// the unlabelled Open map sqrt(L^2 - 1), L = pp z / (1 + i qq z) with
+// (pp, qq) = xi / |xi|^2, for finite z and moderate magnitudes. Scaled by
+// |xi|^2: L = Re(xi) z / (|xi|^2 + i Im(xi) z), so the chain needs neither
+// the record's own reciprocal nor Smith's two divisions -- one reciprocal of
+// |den|^2 -- and csqrt_fast. The general path below handles every other
+// case; results agree within a few ulps.
+__device__ __forceinline__ bool open_fast(double2 xi, double2& z) {
+    const double s2 = fma(xi.x, xi.x, xi.y * xi.y);
+    const double dx = fma(-xi.y, z.y, s2), dy = xi.y * z.x;
+    const double nx = xi.x * z.x, ny = xi.x * z.y;
+    const double dm = fmax(fabs(dx), fabs(dy)), nm = fmax(fabs(nx), fabs(ny));
+    if (!(dm > 1e-100 && dm < 1e100 && nm < 1e100 && (nm > 1e-100 || nm == 0.0))) return false;
+    const double inv = 1.0 / fma(dx, dx, dy * dy);
+    const double Lx = fma(nx, dx, ny * dy) * inv, Ly = fma(ny, dx, -nx * dy) * inv;
+    if (!(fmax(fabs(Lx), fabs(Ly)) < 1e60)) return false;
+    double2 r;
+    if (!csqrt_fast(C(fma(Lx, Lx, -fma(Ly, Ly, 1.0)), 2.0 * Lx * Ly), r)) return false;
+    z = r;
+    return true;
+}
 
 // Open record body (welding.py OpenRec.apply) on explicit parameters: the
 // zip loop keeps xi, Re/|xi|^2, Im/|xi|^2 in registers instead of a record
@@ -142,6 +177,7 @@ __device__ __forceinline__ void apply_open(double2 xi, double pp, double qq, int
         s = (int8_t)br;
         return;
     }
+    if (s == 0 && open_fast(xi, z)) return;
     if (s != 0) {
         double t = c_isinf(z) ? INFINITY : z.y;
         double den = 1.0 - qq * t;
@@ -184,22 +220,32 @@ __device__ __forceinline__ void apply_close(double ai, double bi, double c, doub
     }
     if (s != 0) {
         double t = c_isinf(z) ? INFINITY : z.y;
-        double den = c + d * t;
-        double t2 = (den == 0.0) ? INFINITY : t / den;
-        if (isinf(t)) t2 = (d != 0.0) ? 1.0 / d : INFINITY;
+        // t / (c + d t) = t (a - b) / ((a + b) t - 2ab): from the record's two
+        // points directly, so the chain does not wait for c and d
+        const double den2 = fma(ai + bi, t, -2.0 * ai * bi);
+        const bool fast = fabs(t) < 1e100 && fabs(den2) > 1e-100 && fabs(den2) < 1e100 && fabs(ai) < 1e100 &&
+                          fabs(bi) < 1e100 && ai != bi;
+        double t2;
+        if (fast) {
+            t2 = t * (ai - bi) * (1.0 / den2);
+        } else {
+            const double den = c + d * t;
+            t2 = (den == 0.0) ? INFINITY : t / den;
+            if (isinf(t)) t2 = (d != 0.0) ? 1.0 / d : INFINITY;
+        }
         if (!isfinite(t2)) {
             z = cinf();
             return;  // side kept
         }
-        if (fabs(t2) > 1.0) {
-            double mag = (fabs(t2) < 1e100) ? sqrt(fmax(t2 * t2 - 1.0, 0.0)) : fabs(t2);
-            double sg = t2 > 0 ? 1.0 : -1.0;
-            z = C(0.0 * sg, sg * mag);
-            s = t2 > 0 ? UP : DOWN;
-        } else {
-            z = C(sqrt(fmax(1.0 - t2 * t2, 0.0)), 0.0);
-            s = 0;
-        }
+        // |t2| > 1: +-i sqrt(t2^2 - 1) on the axis (side kept by sign); else
+        // sqrt(1 - t2^2) on the real line -- selects, one sqrt
+        const bool off = fabs(t2) > 1.0;
+        const double u = fma(t2, t2, -1.0);
+        const double root = sqrt(off ? fmax(u, 0.0) : fmax(-u, 0.0));
+        const double mag = (off && !(fabs(t2) < 1e100)) ? fabs(t2) : root;
+        const double sg = t2 > 0 ? 1.0 : -1.0;
+        z = off ? C(0.0 * sg, sg * mag) : C(mag, 0.0);
+        s = off ? (int8_t)(t2 > 0 ? UP : DOWN) : (int8_t)0;
         return;
     }
     double2 T;
@@ -218,6 +264,35 @@ __device__ __forceinline__ void apply_close(double ai, double bi, double c, doub
     }
     s = 0;
     return;
+}
+
+__device__ __forceinline__ void close_params(double a, double b, double& c, double& d);
+__device__ __forceinline__ void open_params(double2 xi, double& pp, double& qq);
+
+// apply_open from the record's point alone: (pp, qq) are formed only where
+// the unlabelled fast path does not apply (as apply_close_ab below)
+__device__ __forceinline__ void apply_open_xi(double2 xi, int br, double2& z, int8_t& s) {
+    if (s == 0 && !c_eq(z, xi) && c_fin(z) && open_fast(xi, z)) return;
+    double pp, qq;
+    open_params(xi, pp, qq);
+    apply_open(xi, pp, qq, br, z, s);
+}
+
+// apply_close from the record's two points: c and d are formed only where
+// the labelled fast path does not apply (the wavefront chain's common case
+// needs neither, so their division stays off the chain)
+__device__ __forceinline__ void apply_close_ab(double ai, double bi, double2& z, int8_t& s) {
+    if (s != 0 && !c_isinf(z) && fabs(z.y) < 1e100 && fabs(ai) < 1e100 && fabs(bi) < 1e100 && ai != bi &&
+        !(z.x == 0.0 && (z.y == ai || z.y == bi))) {
+        const double den2 = fma(ai + bi, z.y, -2.0 * ai * bi);
+        if (fabs(den2) > 1e-100 && fabs(den2) < 1e100) {
+            apply_close(ai, bi, 0.0, 0.0, z, s);  // takes the fast branch (same conditions)
+            return;
+        }
+    }
+    double c, d;
+    close_params(ai, bi, c, d);
+    apply_close(ai, bi, c, d, z, s);
 }
 
 // one record on one point (welding.py:251-509)
@@ -504,6 +579,8 @@ struct Phase1Args {
     int* prog;              // per step [2]: records published per log (streamed replay), or nullptr
     int prog_every;         // publish the counters every this many logged steps
     long long* timing;      // optional (PGCP_WELD_TIMING): per step [publish+barrier, build, apply, zip steps] cycles
+    int spin_ns;            // k_phase1w: back-off of the waiting warps between polls (0: busy spin)
+    int timing_detail;      // PGCP_WELD_TIMING=2: per-segment chain split printed by k_phase1w
 };
 
 // Streamed replay (k_replay_stream): phase 1 publishes, per step and log, the
@@ -1071,7 +1148,7 @@ constexpr int WE_TIMEOUT = 19;
 constexpr unsigned long long WAVE_TIMEOUT_NS = 2000000000ull;
 
 struct WaveRec {
-    double x0, x1, x2, x3;  // Open: xi.re, xi.im, pp, qq; Close: a, b, c, d
+    double x0, x1, x2, x3;  // Open: xi.re, xi.im; Close: a, b (the parameters are formed by whoever needs them)
 };
 
 __device__ __forceinline__ int ld_vol_i(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
@@ -1081,10 +1158,11 @@ __device__ __forceinline__ void fence_gpu() { asm volatile("fence.acq_rel.gpu;" 
 
 // wait until *cnt (this CTA's shared memory) reaches need or carries the abort
 // bit; returns the observed value (WAVE_ABORT set on abort / timeout)
-__device__ __forceinline__ int wave_wait(const int* cnt, int need, unsigned long long& t0) {
+__device__ __forceinline__ int wave_wait(const int* cnt, int need, unsigned long long& t0, int spin_ns) {
     int v = ld_vol_i(cnt);
     int spins = 0;
     while ((v & WAVE_COUNT) < need && !(v & WAVE_ABORT)) {
+        if (spin_ns > 0) __nanosleep(spin_ns);
         if (++spins == 256) {
             spins = 0;
             const unsigned long long now = gtimer();
@@ -1261,11 +1339,14 @@ __global__ void __launch_bounds__(PT + 32, 1) k_phase1w(Phase1Args A) {
                     const int j1 = min(k, min((hi - 1) / 2, (wq0 + 31) / 2));
                     const int j0 = j;
                     bool bad = false;
+                    long long dbg[4] = {0, 0, 0, 0};
+                    const bool dbg_on = A.timing && k >= 1000 && A.timing_detail;
                     for (; j <= j1; ++j) {
+                        const long long ta = dbg_on ? clock64() : 0;
                         const int lq = 2 * j - wq0;
                         const double2 xs = C(__shfl_sync(FULL, z.x, lq + side), __shfl_sync(FULL, z.y, lq + side));
                         const int ss = __shfl_sync(FULL, (int)s8, lq + side);
-                        int e = 0;
+                        int e = 0;  // every lane checks its side's point (a_j even, b_j odd lanes)
                         if (ss != 0 || c_isinf(xs)) {
                             e = WE_ZIP_HALF;
                         } else if (!(xs.x > 0)) {
@@ -1273,8 +1354,8 @@ __global__ void __launch_bounds__(PT + 32, 1) k_phase1w(Phase1Args A) {
                         } else if (cabs_lt(xs, 1e-13)) {
                             e = WE_ZIP_COLL;
                         }
-                        const int ea = __shfl_sync(FULL, e, lq), eb = __shfl_sync(FULL, e, lq + 1);
-                        if (ea || eb) {
+                        if (__any_sync(FULL, e != 0)) {
+                            const int ea = __shfl_sync(FULL, e, lq), eb = __shfl_sync(FULL, e, lq + 1);
                             if (lane == 0) {
                                 raise(ea ? ea : eb, j, ea ? 0 : 1);
                                 fence_cluster();
@@ -1283,29 +1364,44 @@ __global__ void __launch_bounds__(PT + 32, 1) k_phase1w(Phase1Args A) {
                             bad = true;
                             break;
                         }
-                        double pp, qq;
-                        open_params(xs, pp, qq);
-                        if (lane == lq || lane == lq + 1) {
-                            WaveRec w;
-                            w.x0 = xs.x;
-                            w.x1 = xs.y;
-                            w.x2 = pp;
-                            w.x3 = qq;
-                            ringO[2 * j + side] = w;
+                        const long long tb = dbg_on ? clock64() : 0;
+                        // record j for the ring ((pp, qq): one reciprocal, off the chain --
+                        // the unlabelled apply below needs only xi). The segment's last
+                        // record is published before its apply (the next warp takes the
+                        // chain from it); the others after, so the fence waits on stores
+                        // that have long completed
+                        const bool last = j == j1;
+                        auto put = [&]() {
+                            if (lane == lq || lane == lq + 1) *reinterpret_cast<double2*>(&ringO[2 * j + side]) = xs;
+                            __syncwarp();
+                            if (lane == lq) {
+                                __threadfence_block();
+                                st_vol_i(&s_cnt[0][rank], j);
+                            }
+                        };
+                        if (last) put();
+                        const long long tc = dbg_on ? clock64() : 0;
+                        if (have && t > j) apply_open_xi(xs, side ? DOWN : UP, z, s8);
+                        if (!last) put();
+                        if (dbg_on) {
+                            const double zz = __shfl_sync(FULL, z.x, (lq + 2) & 31);
+                            const long long td = clock64() + (zz == 12345.678 ? 1 : 0);
+                            dbg[0] += tb - ta;
+                            dbg[1] += tc - tb;
+                            dbg[2] += td - tc;
+                            dbg[3] += 1;
                         }
-                        __syncwarp();
-                        if (lane == lq) {
-                            __threadfence_block();
-                            st_vol_i(&s_cnt[0][rank], j);
-                        }
-                        if (have && t > j) apply_open(xs, pp, qq, side ? DOWN : UP, z, s8);
                     }
+                    if (dbg_on && lane == 0)
+                        printf("[wave dbg] open rank %d warp %d j %d..%d: shfl+params+check %lld, publish %lld, apply+publish %lld cycles/record\n",
+                               rank, (int)(threadIdx.x >> 5), j0, j1, dbg[0] / max(1ll, dbg[3]), dbg[1] / max(1ll, dbg[3]),
+                               dbg[2] / max(1ll, dbg[3]));
                     if (bad) break;
                     // catch-up: my own record and the rest of the segment, in order
                     if (have)
                         for (int jj = max(t, j0); jj <= j1; ++jj) {
-                            const WaveRec w = ringO[2 * jj + side];
-                            apply_open(C(w.x0, w.x1), w.x2, w.x3, side ? DOWN : UP, z, s8);
+                            const double2 xi = *reinterpret_cast<const double2*>(&ringO[2 * jj + side]);
+                            apply_open_xi(xi, side ? DOWN : UP, z, s8);
                         }
                     __syncwarp();
                 } else {
@@ -1313,7 +1409,7 @@ __global__ void __launch_bounds__(PT + 32, 1) k_phase1w(Phase1Args A) {
                     const int r = (2 * j) / chunk;
                     int v = 0;
                     if (lane == 0) {  // one lane acquires; the warp stays converged
-                        v = wave_wait(&s_cnt[0][r], j, t0);
+                        v = wave_wait(&s_cnt[0][r], j, t0, A.spin_ns);
                         if (r == rank) __threadfence_block(); else fence_cluster();
                     }
                     v = __shfl_sync(FULL, v, 0);
@@ -1329,8 +1425,8 @@ __global__ void __launch_bounds__(PT + 32, 1) k_phase1w(Phase1Args A) {
                     const int upto = min(v & WAVE_COUNT, k);
                     for (; j <= upto; ++j) {
                         if (2 * j >= wq0 && 2 * j < wq0 + 32 && 2 * j < hi) break;  // mine to build
-                        const WaveRec w = ringO[2 * j + side];
-                        if (have) apply_open(C(w.x0, w.x1), w.x2, w.x3, side ? DOWN : UP, z, s8);
+                        const double2 xi = *reinterpret_cast<const double2*>(&ringO[2 * j + side]);
+                        if (have) apply_open_xi(xi, side ? DOWN : UP, z, s8);
                     }
                 }
             }
@@ -1340,7 +1436,7 @@ __global__ void __launch_bounds__(PT + 32, 1) k_phase1w(Phase1Args A) {
             for (int jf = jlo; jf <= jhi;) {
                 int v = 0;
                 if (lane == 0) {
-                    v = wave_wait(&s_cnt[0][rank], jf, t0);
+                    v = wave_wait(&s_cnt[0][rank], jf, t0, A.spin_ns);
                     __threadfence_block();
                 }
                 v = __shfl_sync(FULL, v, 0);
@@ -1354,8 +1450,8 @@ __global__ void __launch_bounds__(PT + 32, 1) k_phase1w(Phase1Args A) {
                 const int upto = ab ? jf - 1 : min(v & WAVE_COUNT, jhi);
                 for (int jj = jf + lane; jj <= upto; jj += 32) {
                     const WaveRec wa = ringO[2 * jj], wb = ringO[2 * jj + 1];
-                    log_a[jj] = mk_open_p(C(wa.x0, wa.x1), wa.x2, wa.x3, UP);
-                    log_b[jj] = mk_open_p(C(wb.x0, wb.x1), wb.x2, wb.x3, DOWN);
+                    log_a[jj] = mk_open(C(wa.x0, wa.x1), UP);
+                    log_b[jj] = mk_open(C(wb.x0, wb.x1), DOWN);
                 }
                 fence_gpu();  // the logs before the records leave this CTA (replay progress causality)
                 __syncwarp();
@@ -1434,7 +1530,10 @@ __global__ void __launch_bounds__(PT + 32, 1) k_phase1w(Phase1Args A) {
                     const int jtop = j;
                     const int jbot = max(1, wq0 / 2);
                     bool bad = false;
+                    long long dbg[4] = {0, 0, 0, 0};
+                    const bool dbg_on = A.timing && k >= 1000 && A.timing_detail;
                     for (; j >= jbot; --j) {
+                        const long long ta = dbg_on ? clock64() : 0;
                         const int lq = 2 * j - wq0;
                         const double2 al = C(__shfl_sync(FULL, z.x, lq), __shfl_sync(FULL, z.y, lq));
                         const double2 be = C(__shfl_sync(FULL, z.x, lq + 1), __shfl_sync(FULL, z.y, lq + 1));
@@ -1456,35 +1555,48 @@ __global__ void __launch_bounds__(PT + 32, 1) k_phase1w(Phase1Args A) {
                             bad = true;
                             break;
                         }
-                        double cc, dd;
-                        close_params(al.y, be.y, cc, dd);
-                        if (lane == lq) {
-                            WaveRec w;
-                            w.x0 = al.y;
-                            w.x1 = be.y;
-                            w.x2 = cc;
-                            w.x3 = dd;
-                            ringC[j] = w;
+                        const long long tb = dbg_on ? clock64() : 0;
+                        // record j for the ring (c, d: one division, off the chain --
+                        // the labelled apply below needs only a and b); the segment's
+                        // last record goes out before its apply (see the zip loop)
+                        const bool last = j == jbot;
+                        auto put = [&]() {
+                            if (lane == lq) *reinterpret_cast<double2*>(&ringC[j]) = C(al.y, be.y);
+                            __syncwarp();
+                            if (lane == lq) {
+                                __threadfence_block();
+                                st_vol_i(&s_cnt[1][rank], k - j);
+                            }
+                        };
+                        if (last) put();
+                        const long long tc = dbg_on ? clock64() : 0;
+                        if (have && t < j) apply_close_ab(al.y, be.y, z, s8);
+                        if (!last) put();
+                        if (dbg_on) {
+                            const double zz = __shfl_sync(FULL, z.y, (lq + 30) & 31);
+                            const long long td = clock64() + (zz == 12345.678 ? 1 : 0);
+                            dbg[0] += tb - ta;
+                            dbg[1] += tc - tb;
+                            dbg[2] += td - tc;
+                            dbg[3] += 1;
                         }
-                        __syncwarp();
-                        if (lane == lq) {
-                            __threadfence_block();
-                            st_vol_i(&s_cnt[1][rank], k - j);
-                        }
-                        if (have && t < j) apply_close(al.y, be.y, cc, dd, z, s8);
                     }
+                    if (dbg_on && lane == 0)
+                        printf("[wave dbg] close rank %d warp %d j %d..%d: shfl+params+check %lld, publish %lld, apply+publish %lld cycles/record\n",
+                               rank, (int)(threadIdx.x >> 5), jtop, jbot, dbg[0] / max(1ll, dbg[3]), dbg[1] / max(1ll, dbg[3]),
+                               dbg[2] / max(1ll, dbg[3]));
                     if (bad) break;
                     if (have)
                         for (int jj = min(t, jtop); jj >= jbot; --jj) {
                             const WaveRec w = ringC[jj];
-                            apply_close(w.x0, w.x1, w.x2, w.x3, z, s8);
+                            apply_close_ab(w.x0, w.x1, z, s8);
                         }
                     __syncwarp();
                 } else {
                     const int r = (2 * j) / chunk;
                     int v = 0;
                     if (lane == 0) {
-                        v = wave_wait(&s_cnt[1][r], k - j, t0);
+                        v = wave_wait(&s_cnt[1][r], k - j, t0, A.spin_ns);
                         if (r == rank) __threadfence_block(); else fence_cluster();
                     }
                     v = __shfl_sync(FULL, v, 0);
@@ -1501,7 +1613,7 @@ __global__ void __launch_bounds__(PT + 32, 1) k_phase1w(Phase1Args A) {
                     for (; j >= lowest; --j) {
                         if (2 * j >= wq0 && 2 * j < wq0 + 32 && 2 * j < hi) break;
                         const WaveRec w = ringC[j];
-                        if (have) apply_close(w.x0, w.x1, w.x2, w.x3, z, s8);
+                        if (have) apply_close_ab(w.x0, w.x1, z, s8);
                     }
                 }
             }
@@ -1511,7 +1623,7 @@ __global__ void __launch_bounds__(PT + 32, 1) k_phase1w(Phase1Args A) {
             for (int jf = jtop; jf >= jbot;) {
                 int v = 0;
                 if (lane == 0) {
-                    v = wave_wait(&s_cnt[1][rank], k - jf, t0);
+                    v = wave_wait(&s_cnt[1][rank], k - jf, t0, A.spin_ns);
                     __threadfence_block();
                 }
                 v = __shfl_sync(FULL, v, 0);
@@ -1525,7 +1637,7 @@ __global__ void __launch_bounds__(PT + 32, 1) k_phase1w(Phase1Args A) {
                 const int lowest = ab ? jf + 1 : max(jbot, k - (v & WAVE_COUNT));
                 for (int jj = jf - lane; jj >= lowest; jj -= 32) {
                     const WaveRec w = ringC[jj];
-                    const Rec rc = mk_close_p(w.x0, w.x1, w.x2, w.x3);
+                    const Rec rc = mk_close(w.x0, w.x1);
                     log_a[base_a + (k - 1 - jj)] = rc;
                     log_b[base_b + (k - 1 - jj)] = rc;
                 }
@@ -2355,6 +2467,8 @@ int run_schedule(double2* tv, int32_t nsteps, const int32_t* info, const int32_t
         a.prog = streamed ? d_prog.p + 2 * q0 : nullptr;
         a.prog_every = std::max(1, env_int("PGCP_WELD_PROG_EVERY", 8));
         a.timing = d_wtime.p ? d_wtime.p + 4 * q0 : nullptr;
+        a.spin_ns = env_int("PGCP_WELD_SPIN_NS", 0);
+        a.timing_detail = env_int("PGCP_WELD_TIMING", 0) >= 2;
         int kmax = 0;
         for (int q = q0; q < q1; ++q) kmax = std::max(kmax, sd[q].k);
         const int NP = 2 * (kmax + 3);

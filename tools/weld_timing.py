@@ -1,6 +1,6 @@
 import os, sys
 sys.path.insert(0, os.getcwd())
-os.environ["PGCP_WELD_TIMING"] = "1"
+os.environ.setdefault("PGCP_WELD_TIMING", "1")
 import paper_1903_12359_b200 as pg
 from paper_1903_12359_b200 import generators as gen
 V, F, cuts = gen.height_field_case(1024, 8)
