@@ -6,12 +6,16 @@
 //   SqrtRatio(pts[0], pts[1]); Open(pts[j]) j = 2..k; axis-Mobius(pts[0]);
 //   Close(va[j], vb[j]) j = k-1..1; SquareMobius(va[0]); 3-point Mobius(aux).
 // So a weld runs in two phases:
-//   phase 1  k_phase1c: one thread-block cluster per weld (up to 16 CTAs)
-//            holds the 2(k+3) arc + tracking points in the CTAs' shared
-//            memory; per record step the owners of the next parameter points
-//            publish them into every CTA through DSMEM, one cluster barrier,
-//            then every thread rebuilds the record and applies it to its
-//            points (the records are the serial critical path);
+//   phase 1  one thread-block cluster per weld (up to 16 CTAs) holds the
+//            2(k+3) arc + tracking points in the CTAs' shared memory / registers.
+//            k_phase1w (default, "wavefront"): the record chain runs inside
+//            the warp that holds the next parameter points (shuffles, no
+//            barrier); the other warps and CTAs follow through shared-memory
+//            rings filled by a forwarder warp over DSMEM (see the comment
+//            above k_phase1w). k_phase1c (PGCP_WELD_WAVE=0, the round-1 form):
+//            per record step the owners publish the parameter points into
+//            every CTA through DSMEM, one cluster barrier, then every thread
+//            rebuilds the record. The two are bit-identical;
 //   phase 2  every other tracked point of the two components (non-arc cycle
 //            points and interior seam points: the reference's `apply_log` on
 //            "others", pipeline.py:200-204) replays its side's log
@@ -211,6 +215,24 @@ __device__ __forceinline__ void apply_open(double2 xi, double pp, double qq, int
     return;
 }
 
+// the unlabelled Close map sqrt(T^2 + 1), T = z / (c - i d z), for finite z
+// and moderate magnitudes: one reciprocal of |den|^2 instead of Smith's two
+// divisions, and csqrt_fast (the counterpart of open_fast; every replayed
+// cycle point takes this path once per Close record). The general path in
+// apply_close handles every other case; results agree within a few ulps.
+__device__ __forceinline__ bool close_fast(double c, double d, double2& z) {
+    const double dx = fma(d, z.y, c), dy = -d * z.x;
+    const double dm = fmax(fabs(dx), fabs(dy)), zm = fmax(fabs(z.x), fabs(z.y));
+    if (!(dm > 1e-100 && dm < 1e100 && zm < 1e100 && zm > 1e-100)) return false;
+    const double inv = 1.0 / fma(dx, dx, dy * dy);
+    const double Tx = fma(z.x, dx, z.y * dy) * inv, Ty = fma(z.y, dx, -z.x * dy) * inv;
+    if (!(fmax(fabs(Tx), fabs(Ty)) < 1e60)) return false;
+    double2 r;
+    if (!csqrt_fast(C(fma(Tx, Tx, -fma(Ty, Ty, -1.0)), 2.0 * Tx * Ty), r)) return false;
+    z = r;
+    return true;
+}
+
 // Close record body (welding.py CloseRec.apply) on explicit parameters
 __device__ __forceinline__ void apply_close(double ai, double bi, double c, double d, double2& z, int8_t& s) {
     if (c_eq(z, C(0.0, ai)) || c_eq(z, C(0.0, bi))) {
@@ -248,6 +270,7 @@ __device__ __forceinline__ void apply_close(double ai, double bi, double c, doub
         s = off ? (int8_t)(t2 > 0 ? UP : DOWN) : (int8_t)0;
         return;
     }
+    if (c_fin(z) && close_fast(c, d, z)) return;  // s == 0 here and stays 0
     double2 T;
     if (c_isinf(z)) {
         T = (d != 0.0) ? C(0.0, 1.0 / d) : cinf();
@@ -398,6 +421,38 @@ __device__ __forceinline__ void apply_rec(const Rec& r, double2& z, int8_t& s) {
         }
         default:
             z = C(NAN, NAN);
+    }
+}
+
+// The replay kernels walk a log record by record on one point: the apply is
+// a ~1.4K-cycle dependent chain, and a record load issued only when the
+// previous apply has finished adds its L2 latency to every record. Open and
+// Close records (all but ~5 of a log) use kind, flags and p[0..3] only, so the
+// replays keep the next record's first 40 bytes in flight during the current
+// apply; the other kinds read the whole record when they are applied.
+struct RecHead {
+    int32_t kind, flags;
+    double p0, p1, p2, p3;
+};
+__device__ __forceinline__ RecHead load_head(const Rec* r) {
+    RecHead h;
+    const int2 kf = *reinterpret_cast<const int2*>(r);  // kind, flags (8-byte aligned)
+    h.kind = kf.x;
+    h.flags = kf.y;
+    h.p0 = r->p[0];
+    h.p1 = r->p[1];
+    h.p2 = r->p[2];
+    h.p3 = r->p[3];
+    return h;
+}
+// same operations as apply_rec(*full, z, s)
+__device__ __forceinline__ void apply_head(const RecHead& h, const Rec* full, double2& z, int8_t& s) {
+    if (h.kind == R_OPEN) {
+        apply_open(C(h.p0, h.p1), h.p2, h.p3, (int)(int8_t)(h.flags & 0xff), z, s);
+    } else if (h.kind == R_CLOSE) {
+        apply_close(h.p0, h.p1, h.p2, h.p3, z, s);
+    } else {
+        apply_rec(*full, z, s);
     }
 }
 
@@ -1839,9 +1894,13 @@ __global__ void k_replay_slots(ReplayArgs A) {
         double2 z = A.tv[slot];
         int8_t s = 0;
         double stage = 0;
+        RecHead nxt = {};
+        if (nrec > 0) nxt = load_head(log);
         for (int r = 0; r < nrec; ++r) {
             if (r == sq) stage = c_fin(z) ? cabs_(z) : 0.0;
-            apply_rec(log[r], z, s);  // fields read in place (L1 broadcast), no local copy
+            const RecHead cur = nxt;
+            if (r + 1 < nrec) nxt = load_head(log + r + 1);  // in flight during this apply
+            apply_head(cur, log + r, z, s);
         }
         if (c_nan(z)) atomicExch(A.nan_flag, 1);
         A.tv[slot] = z;
@@ -1894,6 +1953,8 @@ __global__ void k_replay_stream(ReplayArgs A, const int* __restrict__ prog, int*
         int8_t s = 0;
         double stage = 0;
         int avail = 0, sq = 0, v = 0;
+        RecHead nxt = {};
+        bool have_nxt = false;
         for (int r = 0;; ++r) {
             if (r >= avail) {
                 if (v & PROG_DONE) break;
@@ -1903,7 +1964,12 @@ __global__ void k_replay_stream(ReplayArgs A, const int* __restrict__ prog, int*
             }
             if (sq == 0) sq = (int)__ldcg(meta + (sideB ? 15 : 14));  // known before record sq is published
             if (sq > 0 && r == sq) stage = c_fin(z) ? cabs_(z) : 0.0;
-            apply_rec(log[r], z, s);
+            const RecHead cur = have_nxt ? nxt : load_head(log + r);
+            // the next record, if already covered by the counter read (acquire)
+            // above, is loaded now and arrives during this apply
+            have_nxt = r + 1 < avail;
+            if (have_nxt) nxt = load_head(log + r + 1);
+            apply_head(cur, log + r, z, s);
         }
         if (!(v & PROG_DONE)) v = wait_prog(pg, PROG_COUNT, timeout_flag);
         if ((v & PROG_TIMEOUT) || __ldcg(meta + 2) != 0.0) continue;  // failed step: leave values
@@ -2452,10 +2518,18 @@ int run_schedule(double2* tv, int32_t nsteps, const int32_t* info, const int32_t
     PGCP_TRY_CUDA(cudaMemcpyAsync(d_sd.p, sd.data(), nsteps * sizeof(StepDesc), cudaMemcpyHostToDevice, s));
     PGCP_TRY_CUDA(cudaMemcpyAsync(d_src.p, src, src_off[nsteps] * sizeof(int32_t), cudaMemcpyHostToDevice, s));
     PGCP_TRY_CUDA(cudaMemcpyAsync(d_wb.p, wb3.data(), 3 * nwb * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    // PGCP_WELD_TIMING: CUDA events around the setup copies and every level
+    std::vector<cudaEvent_t> lev_ev;
+    if (wtiming) {
+        lev_ev.resize(nlev + 2);
+        for (auto& e : lev_ev) PGCP_TRY_CUDA(cudaEventCreate(&e));
+        PGCP_TRY_CUDA(cudaEventRecord(lev_ev[0], s));
+    }
     int q0 = 0;
     for (int l = 0; l < nlev; ++l) {
         int q1 = q0;
         while (q1 < nsteps && level[order[q1]] == l) ++q1;
+        if (wtiming && l == 0) PGCP_TRY_CUDA(cudaEventRecord(lev_ev[1], s));
         Phase1Args a;
         a.steps = d_sd.p + q0;
         a.src = d_src.p;
@@ -2533,6 +2607,7 @@ int run_schedule(double2* tv, int32_t nsteps, const int32_t* info, const int32_t
             }
         }
         q0 = q1;
+        if (wtiming) PGCP_TRY_CUDA(cudaEventRecord(lev_ev[l + 2], s));
     }
     std::vector<double> meta((size_t)META * nsteps);
     std::vector<unsigned long long> mx(3 * (size_t)nsteps);
@@ -2547,6 +2622,18 @@ int run_schedule(double2* tv, int32_t nsteps, const int32_t* info, const int32_t
     if (recs_host && recs_cap_total >= rec_tot) PGCP_TRY(d2h_async(recs_host, d_recs.p, rec_tot * sizeof(Rec), s));
     PGCP_TRY(d2h_flush(s));
     if (wtiming) {
+        PGCP_TRY_CUDA(cudaEventSynchronize(lev_ev.back()));
+        fprintf(stderr, "[weld timing] device ms:");
+        for (int l = 0; l + 1 < (int)lev_ev.size(); ++l) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, lev_ev[l], lev_ev[l + 1]);
+            if (l == 0)
+                fprintf(stderr, " setup copies %.3f", ms);
+            else
+                fprintf(stderr, " L%d %.3f", l - 1, ms);
+        }
+        fprintf(stderr, "\n");
+        for (auto& e : lev_ev) cudaEventDestroy(e);
         std::vector<long long> wt(4 * (size_t)nsteps);
         PGCP_TRY_CUDA(cudaMemcpy(wt.data(), d_wtime.p, wt.size() * sizeof(long long), cudaMemcpyDeviceToHost));
         for (int q = 0; q < nsteps; ++q) {

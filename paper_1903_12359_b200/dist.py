@@ -223,7 +223,7 @@ def bench_distributed(args, V, F, cuts, pairs, metric, unit, workload):
         if sampler:
             sampler.start()
         l0 = lib.pgcp_launch_count()
-        ms_steps, pcg_ms, pcg_bytes = [], [], []  # pcg_bytes: SURVEY 8(d) algorithmic bytes
+        ms_steps, num_ms, num_fmas = [], [], []  # the direct solver's numeric phase of this rank's flatten
         for _ in range(args.steps):
             flush.zero_()
             dist.barrier()
@@ -236,8 +236,10 @@ def bench_distributed(args, V, F, cuts, pairs, metric, unit, workload):
             torch.cuda.synchronize()
             ms_steps.append(_max_over_ranks(e0.elapsed_time(e1), dev))
             fl = rep.solver["flatten"]
-            pcg_ms.append(fl["kernel_ms"])
-            pcg_bytes.append(fl["ref_bytes"])
+            if fl.get("solver") != "direct":
+                raise RuntimeError("the bench measures the default (direct) solver")
+            num_ms.append(fl["numeric_ms"])
+            num_fmas.append(fl["fmas"])
         dist.barrier()
         torch.cuda.synchronize()
         launches = _sum_over_ranks(lib.pgcp_launch_count() - l0, dev)
@@ -269,15 +271,23 @@ def bench_distributed(args, V, F, cuts, pairs, metric, unit, workload):
                    "d2h_bytes_per_step": int(d2h)}
 
         peak, peak_src = B.measured_peak()
-        kernel_ms = _max_over_ranks(statistics.mean(pcg_ms), dev)
-        bytes_all = _sum_over_ranks(statistics.mean(pcg_bytes), dev)
+        fp64 = B.fp64_probe_tflops()
+        numeric_ms = _max_over_ranks(statistics.mean(num_ms), dev)
+        fmas_all = _sum_over_ranks(statistics.mean(num_fmas), dev)
         if rank == 0:
-            achieved = bytes_all / world / (kernel_ms / 1e3) / 1e9
-            roof = {"bound": "l2", "kernel": "k_pcg2 (flatten, rank-local shard of the 64 subdomains)",
-                    "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                    "traffic": B.ncu_traffic(), "peak_source": peak_src, "kernel_ms": kernel_ms,
-                    "note": "per-GPU average of the flatten launch's algorithmic bytes over the slowest "
-                            "rank's kernel time"}
+            # per-GPU average of the factorization flops over the slowest rank's numeric phase
+            achieved = 2.0 * fmas_all / world / (numeric_ms / 1e3) / 1e12
+            roof = {"bound": "fp64",
+                    "kernel": "multifrontal numeric factorization of each rank's shard of the 64 cfg-2 DNCP "
+                              "systems (bench.py's `roofline` at N = 1)",
+                    "achieved": achieved, "peak": fp64, "unit": "TFLOP/s",
+                    "frac": achieved / fp64 if fp64 else None,
+                    "traffic": B.ncu_summary("r2_direct_ncu_summary.json").get("dram_bytes_per_factorization"),
+                    "peak_source": "measured here: pgcp_fp64_probe on rank 0", "numeric_ms": numeric_ms,
+                    "flops_per_step_all_ranks": 2.0 * fmas_all, "hbm_peak": peak, "hbm_peak_source": peak_src,
+                    "note": "per-GPU average of the factorization flops over the slowest rank's numeric "
+                            "phase; latency-bound small fronts (DESIGN.md section 4b); `traffic` is the "
+                            "single-GPU capture"}
             line = {"metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
                     "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
                     "vs_baseline": None, "dtype": "f64", "data": "synthetic",
