@@ -1116,6 +1116,11 @@ __global__ void __launch_bounds__(DNT, sizeof(T) == 8 ? 8 : 4) k_factor(FacArgs 
 constexpr int PB = 32;
 constexpr int FUSED_MAXS = 48;
 constexpr size_t SM_FRONT_BYTES = 112 * 1024;  // k_factor_sm: two CTAs per SM
+// k_factor_warp CTA: 8 warps share this much dynamic shared memory (real
+// fronts: three CTAs per SM at 80 registers; complex: two at 125)
+constexpr size_t warp_cta_bytes(size_t tsz) { return tsz == 8 ? 75 * 1024 : 112 * 1024; }
+// k_factor_warp fronts split off a list of larger ones: up to 70 wide (real and complex)
+constexpr size_t warp_split_bytes(size_t tsz) { return tsz == 8 ? 20 * 1024 : 40 * 1024; }
 constexpr size_t WARP_FRONT_BYTES = 40 * 1024; // k_factor_warp: per warp (packed lower triangle)  // levels whose fronts all have <= this many pivots stay fused
 
 // phase 0 (one CTA per front): factor the diagonal block in place;
@@ -1471,17 +1476,21 @@ __global__ void __launch_bounds__(DNT) k_factor_sm(FacArgs a) {
 __device__ __forceinline__ int pk(int i, int j, int f) { return j * (2 * f - j - 1) / 2 + i; }
 
 template <class T, int WB>
-__global__ void __launch_bounds__(256) k_factor_warp(FacArgs a, int nfront, int wbytes) {
+__global__ void __launch_bounds__(256) k_factor_warp(FacArgs a, const int32_t* __restrict__ gstart,
+                                                     const int32_t* __restrict__ wsoff) {
     extern __shared__ __align__(16) unsigned char dsm[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int idx = blockIdx.x * (blockDim.x >> 5) + warp;
-    if (idx >= nfront) return;
+    // a.list is the whole node list here; group blockIdx.x holds the list
+    // positions [gstart[g], gstart[g + 1]), one per warp, each with its own
+    // slice of the CTA's shared memory (sized by the front, not by the list)
+    const int idx = gstart[blockIdx.x] + warp;
+    if (idx >= gstart[blockIdx.x + 1]) return;
     const int N = a.list[idx];
     const int s = a.nd.npiv[N];
     const int nu = a.ucnt[N];
     const int f = s + nu;
     const int64_t pf = a.pfirst[N];
-    unsigned char* base = dsm + (size_t)warp * wbytes;
+    unsigned char* base = dsm + wsoff[idx];
     T* S = reinterpret_cast<T*>(base);
     const int np = f * (f + 1) / 2;
     int32_t* Us = reinterpret_cast<int32_t*>(S + np);
@@ -2436,6 +2445,15 @@ struct DirectFactor {
     std::vector<int> lst_maxs;               // per (level, type): largest pivot count
     std::vector<int> lst_maxf;               // ... largest front
     std::vector<int32_t> h_nlist, h_npiv, h_fsz, h_order;  // host copies (uploads stay async)
+    // k_factor_warp groups: every list is sorted by front size (largest
+    // first); the fronts small enough for one warp (from lst_wfirst on) are
+    // packed, in that order, into CTAs of up to 8 fronts whose packed
+    // triangles fill the CTA's shared memory -- so a CTA of leaf-sized fronts
+    // runs 8 warps where a CTA of the list's largest fronts runs 2
+    std::vector<int64_t> lst_wfirst;         // per (level, type): first list position handled by k_factor_warp
+    std::vector<int64_t> grp_off;            // per (level, type): its groups are [grp_off[q], grp_off[q + 1])
+    std::vector<int32_t> h_gstart, h_wsoff;  // group -> first list position (+ end sentinel per list); position -> smem offset
+    DevBuf<int32_t> gstart, wsoff;
     std::vector<int> lvl_maxf, lvl_maxu;
     int ncplx = 0;
     std::vector<int32_t> h_err;
@@ -2506,9 +2524,8 @@ int set_smem(K kern, size_t bytes) {
 
 template <class T>
 int factor_level(DirectFactor* D, FacArgs fa, int l, int type, cudaStream_t s) {
-    const int64_t o0 = D->lst_off[2 * l + type], o1 = D->lst_off[2 * l + type + 1];
-    if (o1 <= o0) return PGCP_OK;
-    const int n = (int)(o1 - o0);
+    const int64_t o0 = D->lst_off[2 * l + type];
+    if (D->lst_off[2 * l + type + 1] <= o0) return PGCP_OK;
     fa.list = D->nlist.p + o0;
     const size_t tsz = sizeof(T);
     const int maxu_child = (l + 1 < (int)D->levels.size()) ? D->lvl_maxu[l + 1] : 0;
@@ -2517,29 +2534,37 @@ int factor_level(DirectFactor* D, FacArgs fa, int l, int type, cudaStream_t s) {
         set_error("direct solver: front update set too large (%d)", D->lvl_maxu[l]);
         return DIRECT_FALLBACK;
     }
-    {   // the smallest fronts: one warp each
-        const int maxf_t = D->lst_maxf[2 * l + type];
-        size_t wb = (size_t)maxf_t * (maxf_t + 1) / 2 * tsz + (size_t)(D->lvl_maxu[l] + maxu_child) * 4 + 16;
-        wb = (wb + 15) & ~(size_t)15;
-        if (wb <= WARP_FRONT_BYTES && !getenv("PGCP_DIRECT_NO_WARP")) {
-            const int wpc = (int)std::max<size_t>(1, std::min<size_t>(8, (96 * 1024) / wb));
-            const int wbk = env_int("PGCP_DIRECT_WB", 8);
-            if (wbk == 4) {
-                PGCP_TRY(set_smem(k_factor_warp<T, 4>, wb * wpc));
-                k_factor_warp<T, 4><<<(n + wpc - 1) / wpc, 32 * wpc, wb * wpc, s>>>(fa, n, (int)wb);
-            } else if (wbk == 8) {
-                PGCP_TRY(set_smem(k_factor_warp<T, 8>, wb * wpc));
-                k_factor_warp<T, 8><<<(n + wpc - 1) / wpc, 32 * wpc, wb * wpc, s>>>(fa, n, (int)wb);
-            } else {
-                PGCP_TRY(set_smem(k_factor_warp<T, 16>, wb * wpc));
-                k_factor_warp<T, 16><<<(n + wpc - 1) / wpc, 32 * wpc, wb * wpc, s>>>(fa, n, (int)wb);
-            }
-            PGCP_LAUNCH_CHECK();
-            return PGCP_OK;
+    // the fronts small enough for one warp each (the tail of the size-sorted
+    // list), grouped into CTAs by packed size (see DirectFactor::grp_off)
+    if (D->grp_off[2 * l + type + 1] > D->grp_off[2 * l + type]) {
+        const int64_t g0 = D->grp_off[2 * l + type], g1 = D->grp_off[2 * l + type + 1];
+        const int ng = (int)(g1 - g0) - 1;  // the list's last entry is its end sentinel
+        FacArgs fw = fa;
+        fw.list = D->nlist.p;
+        const size_t cta = warp_cta_bytes(tsz);
+        const int wbk = env_int("PGCP_DIRECT_WB", 8);
+        if (wbk == 4) {
+            PGCP_TRY(set_smem(k_factor_warp<T, 4>, cta));
+            k_factor_warp<T, 4><<<ng, 256, cta, s>>>(fw, D->gstart.p + g0, D->wsoff.p);
+        } else if (wbk == 8) {
+            PGCP_TRY(set_smem(k_factor_warp<T, 8>, cta));
+            k_factor_warp<T, 8><<<ng, 256, cta, s>>>(fw, D->gstart.p + g0, D->wsoff.p);
+        } else {
+            PGCP_TRY(set_smem(k_factor_warp<T, 16>, cta));
+            k_factor_warp<T, 16><<<ng, 256, cta, s>>>(fw, D->gstart.p + g0, D->wsoff.p);
         }
+        PGCP_LAUNCH_CHECK();
+    }
+    // the larger fronts of the list: [o0, lst_wfirst)
+    const int64_t o1 = D->lst_wfirst[2 * l + type];
+    if (o1 <= o0) return PGCP_OK;
+    const int n = (int)(o1 - o0);
+    int maxf_t = 0, maxs = 0;
+    for (int64_t q = o0; q < o1; ++q) {
+        maxf_t = std::max(maxf_t, D->h_fsz[D->h_nlist[q]]);
+        maxs = std::max(maxs, D->h_npiv[D->h_nlist[q]]);
     }
     {   // fronts that fit in shared memory: the resident kernel
-        const int maxf_t = D->lst_maxf[2 * l + type];
         const size_t sm = (size_t)maxf_t * maxf_t * tsz + (size_t)(D->lvl_maxu[l] + maxu_child) * 4 + 16;
         if (sm <= SM_FRONT_BYTES && !getenv("PGCP_DIRECT_NO_SMEM")) {
             if (env_int("PGCP_DIRECT_SB", 8) == 8) {
@@ -2555,7 +2580,6 @@ int factor_level(DirectFactor* D, FacArgs fa, int l, int type, cudaStream_t s) {
     }
     PGCP_TRY(set_smem(k_factor<T>, smem));
     const int nt = schur_tiles(D->lvl_maxu[l]);
-    const int maxs = D->lst_maxs[2 * l + type];
     static const int fused_maxs = env_int("PGCP_DIRECT_FUSED_MAXS", FUSED_MAXS);
     if (maxs <= fused_maxs) {
         const bool inl = nt <= 1;
@@ -2941,6 +2965,76 @@ int direct_factor(pgcp_batch* b, const DirectInput& in, DirectFactor** out, cuda
         }
     }
     D->lst_off[2 * D->levels.size()] = (int64_t)hl.size();
+    // every list largest front first (ties by node id: deterministic), then
+    // the warp-sized tail of each list packed into k_factor_warp's groups
+    {
+        const size_t nq = 2 * D->levels.size();
+        D->lst_wfirst.assign(nq, 0);
+        D->grp_off.assign(nq + 1, 0);
+        D->h_gstart.clear();
+        D->h_wsoff.assign(std::max<size_t>(hl.size(), 1), 0);
+        const bool no_warp = getenv("PGCP_DIRECT_NO_WARP") != nullptr;
+        for (size_t q = 0; q < nq; ++q) {
+            const int64_t o0 = D->lst_off[q], o1 = D->lst_off[q + 1];
+            {   // stable counting sort by front size, descending (the list is in node order)
+                int fmax = 0;
+                for (int64_t i = o0; i < o1; ++i) fmax = std::max(fmax, hf[hl[i]]);
+                std::vector<int32_t> start(fmax + 2, 0), tmp(hl.begin() + o0, hl.begin() + o1);
+                for (int32_t N : tmp) ++start[fmax - hf[N] + 1];
+                for (int k = 0; k <= fmax; ++k) start[k + 1] += start[k];
+                for (int32_t N : tmp) hl[o0 + start[fmax - hf[N]]++] = N;
+            }
+            const size_t l = q / 2, tsz = (q & 1) ? 16 : 8;
+            const int maxu_child = l + 1 < D->levels.size() ? D->lvl_maxu[l + 1] : 0;
+            // bytes of front N in k_factor_warp: packed triangle, its update
+            // rows and the relative indices of a child's update rows
+            auto wbytes = [&](int32_t N) {
+                const size_t f = (size_t)hf[N], nu = (size_t)(hf[N] - hp[N]);
+                return (f * (f + 1) / 2 * tsz + (nu + (size_t)maxu_child) * 4 + 16 + 15) & ~(size_t)15;
+            };
+            // A list whose largest front fits a warp goes to k_factor_warp whole.
+            // Otherwise the fronts up to warp_split_bytes (f <= 70:
+            // measured 3x faster per front there than a CTA each, while
+            // a lone warp on an 80-100 wide front is slower than a CTA) split
+            // off, if they are most of the list; the few larger ones take a CTA
+            // each. PGCP_DIRECT_WSPLIT=0: no split (a mixed list takes CTAs).
+            static const bool wsplit = env_int("PGCP_DIRECT_WSPLIT", 1) != 0;
+            int64_t w0 = o0;
+            if (no_warp) {
+                w0 = o1;
+            } else if (o1 > o0 && wbytes(hl[o0]) > WARP_FRONT_BYTES) {
+                while (w0 < o1 && wbytes(hl[w0]) > warp_split_bytes(tsz)) ++w0;
+                if (!wsplit || 2 * (o1 - w0) < (o1 - o0)) w0 = o1;
+            }
+            D->lst_wfirst[q] = w0;
+            D->grp_off[q] = (int64_t)D->h_gstart.size();
+            if (w0 < o1) {
+                const size_t cap = warp_cta_bytes(tsz);
+                size_t used = cap + 1;  // forces a new group at the first front
+                int cnt = 0;
+                for (int64_t i = w0; i < o1; ++i) {
+                    const size_t wb = wbytes(hl[i]);
+                    if (cnt == 8 || used + wb > cap) {
+                        D->h_gstart.push_back((int32_t)i);
+                        used = 0;
+                        cnt = 0;
+                    }
+                    D->h_wsoff[i] = (int32_t)used;
+                    used += wb;
+                    ++cnt;
+                }
+                D->h_gstart.push_back((int32_t)o1);  // end sentinel of this list's groups
+            }
+        }
+        D->grp_off[nq] = (int64_t)D->h_gstart.size();
+        PGCP_TRY(D->gstart.alloc(std::max<int64_t>((int64_t)D->h_gstart.size(), 1), s));
+        PGCP_TRY(D->wsoff.alloc((int64_t)D->h_wsoff.size(), s));
+        if (!D->h_gstart.empty())
+            PGCP_TRY_CUDA(cudaMemcpyAsync(D->gstart.p, D->h_gstart.data(), D->h_gstart.size() * sizeof(int32_t),
+                                          cudaMemcpyHostToDevice, s));
+        PGCP_TRY_CUDA(cudaMemcpyAsync(D->wsoff.p, D->h_wsoff.data(), D->h_wsoff.size() * sizeof(int32_t),
+                                      cudaMemcpyHostToDevice, s));
+    }
     D->lst_maxs.assign(2 * D->levels.size(), 0);
     D->lst_maxf.assign(2 * D->levels.size(), 0);
     for (size_t q = 0; q < 2 * D->levels.size(); ++q)
@@ -2975,6 +3069,24 @@ int direct_factor(pgcp_batch* b, const DirectInput& in, DirectFactor** out, cuda
             }
             fprintf(stderr, "[direct levels] L%zu nodes %d max front %d max pivots %d max update %d FMAs %.3g\n", l,
                     D->levels[l].second - D->levels[l].first, D->lvl_maxf[l], maxp, D->lvl_maxu[l], lf);
+            if (env_int("PGCP_DIRECT_TIMING", 0) >= 2) {  // front-size distribution (count and FMA shares)
+                std::vector<std::pair<int, double>> fs;
+                for (int N = D->levels[l].first; N < D->levels[l].second; ++N) {
+                    const double f = hf[N], sp = hp[N], u = f - sp;
+                    fs.push_back({hf[N], (ht[N] ? 4.0 : 1.0) * (sp * sp * sp / 6.0 + u * sp * sp / 2.0 + u * u * sp / 2.0)});
+                }
+                std::sort(fs.begin(), fs.end());
+                const size_t n = fs.size();
+                double acc = 0;
+                fprintf(stderr, "[direct levels]    front size quantiles 10/50/90%%: %d %d %d; FMA share of fronts <=",
+                        fs[n / 10].first, fs[n / 2].first, fs[(9 * n) / 10].first);
+                size_t i = 0;
+                for (int cut : {40, 48, 56, 64, 72, 80}) {
+                    while (i < n && fs[i].first <= cut) acc += fs[i++].second;
+                    fprintf(stderr, " %d: %.2f (%zu)", cut, lf > 0 ? acc / lf : 0.0, i);
+                }
+                fprintf(stderr, "\n");
+            }
         }
     }
     D->front_bytes = 8.0 * (double)ftot;

@@ -3032,9 +3032,13 @@ int run_solve(pgcp_batch* b, SolveSystem* S, const pgcp_solve_opts* o, double* z
                                             b->loop_off.p, b->loop.p, (const double2*)z, S->res.p);
         PGCP_LAUNCH_CHECK();
     }
+    // SURVEY 8(d) byte model of the PCG (entries of the reference's CSR
+    // system per slot): PCG statistics only -- the direct solver's calls skip
+    // the count, its stream synchronisation and the copy
     DevBuf<long long> refnz;
-    PGCP_TRY(refnz.alloc(nslot, s));
-    {
+    std::vector<long long> hrefnz(nslot, 0);
+    if (!S->use_direct) {
+        PGCP_TRY(refnz.alloc(nslot, s));
         DevBuf<int64_t> dnu;
         std::vector<int64_t> hnu(S->h_nu.begin(), S->h_nu.end());
         PGCP_TRY(dnu.alloc(nslot, s));
@@ -3043,16 +3047,18 @@ int run_solve(pgcp_batch* b, SolveSystem* S, const pgcp_solve_opts* o, double* z
                                         S->dncp ? 1 : 0, refnz.p);
         PGCP_LAUNCH_CHECK();
         PGCP_TRY_CUDA(cudaStreamSynchronize(s));  // hnu is a local
+        PGCP_TRY(d2h_async(hrefnz.data(), refnz.p, nslot * sizeof(long long), s));
     }
-    std::vector<long long> hrefnz(nslot);
-    PGCP_TRY_CUDA(cudaMemcpyAsync(hrefnz.data(), refnz.p, nslot * sizeof(long long), cudaMemcpyDeviceToHost, s));
     std::vector<int32_t> hit(nslot);
     std::vector<double> hres(8 * nslot);
     std::vector<int64_t> hptr(S->nslices + 1);
-    PGCP_TRY_CUDA(cudaMemcpyAsync(hptr.data(), S->sl_ptr.p, (S->nslices + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-    PGCP_TRY_CUDA(cudaMemcpyAsync(hit.data(), S->iters.p, nslot * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    PGCP_TRY_CUDA(cudaMemcpyAsync(hres.data(), S->res.p, 8 * nslot * sizeof(double), cudaMemcpyDeviceToHost, s));
-    PGCP_TRY_CUDA(cudaStreamSynchronize(s));
+    // through the pinned staging buffer: a pageable destination would make
+    // the driver stage the copy synchronously and hold the other host
+    // threads' launches meanwhile (concurrency lessons)
+    PGCP_TRY(d2h_async(hptr.data(), S->sl_ptr.p, (S->nslices + 1) * sizeof(int64_t), s));
+    PGCP_TRY(d2h_async(hit.data(), S->iters.p, nslot * sizeof(int32_t), s));
+    PGCP_TRY(d2h_async(hres.data(), S->res.p, 8 * nslot * sizeof(double), s));
+    PGCP_TRY(d2h_flush(s));
     S->h_iters = hit;
     if (S->coarse && !S->force_jacobi) {
         std::lock_guard<std::mutex> lock(g_prev_mu);
@@ -3162,7 +3168,7 @@ int run_solve(pgcp_batch* b, SolveSystem* S, const pgcp_solve_opts* o, double* z
             S->iters_max = std::max<double>(S->iters_max, hit[j]);
             S->bytes_iter_weighted += bytes * hit[j];
             const double rref = S->dncp ? 2.0 * rows : rows;
-            S->ref_bytes_weighted += (12.0 * (double)hrefnz[j] + 4.0 * (rref + 1.0)) * hit[j];
+            if (!S->use_direct) S->ref_bytes_weighted += (12.0 * (double)hrefnz[j] + 4.0 * (rref + 1.0)) * hit[j];
             S->nrows_u += rows;
             S->nnz_off += (double)e;
         }
@@ -3279,8 +3285,8 @@ int solve_flatten(pgcp_batch* b, const int32_t* comps, int32_t ncomp, const int3
     } else {
         if (b->pins.p == nullptr) PGCP_TRY(default_pins(b, s));
         std::vector<int32_t> all(2 * b->K);
-        PGCP_TRY_CUDA(cudaMemcpyAsync(all.data(), b->pins.p, all.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-        PGCP_TRY_CUDA(cudaStreamSynchronize(s));
+        PGCP_TRY(d2h_async(all.data(), b->pins.p, all.size() * sizeof(int32_t), s));  // pinned staging
+        PGCP_TRY(d2h_flush(s));
         for (int j = 0; j < S->nslot; ++j) {
             hp[2 * j] = all[2 * S->comps[j]];
             hp[2 * j + 1] = all[2 * S->comps[j] + 1];
