@@ -2633,12 +2633,43 @@ int factor_level(DirectFactor* D, FacArgs fa, int l, int type, cudaStream_t s) {
 int factor_levels(DirectFactor* D, FacArgs& fa, cudaStream_t s, PhaseTimer& pt) {
     static const char* names[] = {"L0", "L1", "L2", "L3", "L4", "L5", "L6", "L7", "L8", "L9", "L10", "L11",
                                   "L12", "L13", "L14", "L15", "L16", "L17", "L18", "L19", "L20+"};
-    for (int l = (int)D->levels.size() - 1; l >= 0; --l) {
-        PGCP_TRY(factor_level<double>(D, fa, l, 0, s));
-        PGCP_TRY(factor_level<double2>(D, fa, l, 1, s));
+    // The real and the complex fronts of a level are independent lists. On
+    // the upper levels each is a chain of ~10 small dependent launches that
+    // leaves most SMs idle, so the complex list runs on a second stream of
+    // the same priority, forked and joined per level with events
+    // (PGCP_DIRECT_TWO_STREAMS=0: one stream).
+    static const bool two = env_int("PGCP_DIRECT_TWO_STREAMS", 1) != 0;
+    cudaStream_t s2 = nullptr;
+    cudaEvent_t ef = nullptr, ej = nullptr;
+    if (two && D->ncplx > 0 && D->ncplx < D->nnodes) {
+        int prio = 0;
+        PGCP_TRY_CUDA(cudaStreamGetPriority(s, &prio));
+        PGCP_TRY_CUDA(cudaStreamCreateWithPriority(&s2, cudaStreamNonBlocking, prio));
+        PGCP_TRY_CUDA(cudaEventCreateWithFlags(&ef, cudaEventDisableTiming));
+        PGCP_TRY_CUDA(cudaEventCreateWithFlags(&ej, cudaEventDisableTiming));
+    }
+    int rc = PGCP_OK;
+    for (int l = (int)D->levels.size() - 1; l >= 0 && rc == PGCP_OK; --l) {
+        const bool both = s2 && D->lst_off[2 * l + 1] > D->lst_off[2 * l] && D->lst_off[2 * l + 2] > D->lst_off[2 * l + 1];
+        if (both) {
+            if (cudaEventRecord(ef, s) != cudaSuccess || cudaStreamWaitEvent(s2, ef, 0) != cudaSuccess) rc = PGCP_E_CUDA;
+        }
+        if (rc == PGCP_OK) rc = factor_level<double>(D, fa, l, 0, s);
+        if (rc == PGCP_OK) rc = factor_level<double2>(D, fa, l, 1, both ? s2 : s);
+        if (both) {  // joined even after an error: nothing may outlive the aux stream unordered
+            if (cudaEventRecord(ej, s2) != cudaSuccess || cudaStreamWaitEvent(s, ej, 0) != cudaSuccess) {
+                if (rc == PGCP_OK) rc = PGCP_E_CUDA;
+            }
+        }
         pt.mark(names[std::min(l, 20)]);
     }
-    return PGCP_OK;
+    if (s2) {
+        cudaEventDestroy(ef);
+        cudaEventDestroy(ej);
+        cudaStreamDestroy(s2);  // its work is ordered before s by the last join
+    }
+    if (rc == PGCP_E_CUDA && !cudaGetLastError()) set_error("direct solver: stream fork/join failed");
+    return rc;
 }
 
 }  // namespace
