@@ -487,7 +487,9 @@ def _exchange_boundary(shard, plan, loop_gid_host, z0, dev):
 def _fill_foreign_loops(tv, z, own_slots, loop_gid_host, dev):
     """z on the boundary loops of other ranks' submeshes := their welded
     Dirichlet values (what their harmonic solves hold fixed)."""
-    foreign = np.setdiff1d(np.arange(len(loop_gid_host)), own_slots).astype(np.int32)
+    mine = np.zeros(len(loop_gid_host), dtype=bool)
+    mine[own_slots] = True
+    foreign = np.flatnonzero(~mine).astype(np.int32)
     if not len(foreign):
         return
     src = torch.as_tensor(foreign).to(dev)
