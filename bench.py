@@ -54,7 +54,7 @@ WORKLOAD = ("cfg2: 1024x1024 height field (8 Gaussian bumps, seed 0), 8x8 cell-a
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["b200", "reference"], default="b200")
     p.add_argument("--grid", type=int, default=1024, help="vertices per side (1024 = cfg 2)")
