@@ -302,6 +302,23 @@ PGCP_API int pgcp_weld_schedule_run(double* tv, int32_t nsteps, const int32_t* i
                                     const int64_t* wb_off, const int32_t* wb, double hard_tol, double* out,
                                     pgcp_rec* recs, int64_t recs_cap, void* stream);
 
+/* The same in two calls, so that the host-side preparation of a schedule
+ * (levels, launch-order descriptors, write-back lists, device buffers and
+ * their uploads: ~0.4 ms on cfg 2) can run before the tracked values exist --
+ * pipeline.py prepares on the planning thread while the flatten runs.
+ *   prepare  arguments as pgcp_weld_schedule_run; uploads on `stream`; the
+ *            host arrays may be released when it returns; *handle owns the
+ *            device buffers
+ *   execute  runs the prepared schedule on tv, once, on `stream` (ordered after
+ *            the preparing stream by an event); out / recs as above.
+ *            Synchronises.
+ *   free     releases the handle (after execute has returned, or unused). */
+PGCP_API int pgcp_weld_schedule_prepare(int32_t nsteps, const int32_t* info, const int32_t* src, const int64_t* wb_off,
+                                        const int32_t* wb, void* stream, void** handle);
+PGCP_API int pgcp_weld_schedule_execute(void* handle, double* tv, double hard_tol, double* out, pgcp_rec* recs,
+                                        int64_t recs_cap, void* stream);
+PGCP_API void pgcp_weld_schedule_free(void* handle);
+
 /* apply_log: replay nrec host records on device points (in/out) with
  * optional int8 side tags. Synchronises; PGCP_E_WELD on NaN. */
 PGCP_API int pgcp_weld_replay(const pgcp_rec* recs, int32_t nrec, double* pts, int8_t* sides, int64_t npts,

@@ -35,8 +35,11 @@
 // test_welds_match_reference / test_weld_corpus, and the k >= 1000 welds of
 // cfg 2 in tests/test_gpu_cfg2.py), not bit for bit.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstring>
+#include <memory>
+#include <mutex>
 #include <string>
 #include <unordered_map>
 
@@ -1961,8 +1964,12 @@ __global__ void k_replay_stream(ReplayArgs A, const int* __restrict__ prog, int*
                 v = wait_prog(pg, r + 1, timeout_flag);
                 avail = v & PROG_COUNT;
                 if (r >= avail) break;  // finished (or failed / timed out) with fewer records
+                // the index of the SquareMobius record is written before the
+                // counter that covers it is published, so it is enough to look
+                // for it when the counter has moved (a load per record would
+                // put an L2 round trip on every step of the chain)
+                if (sq == 0) sq = (int)__ldcg(meta + (sideB ? 15 : 14));
             }
-            if (sq == 0) sq = (int)__ldcg(meta + (sideB ? 15 : 14));  // known before record sq is published
             if (sq > 0 && r == sq) stage = c_fin(z) ? cabs_(z) : 0.0;
             const RecHead cur = have_nxt ? nxt : load_head(log + r);
             // the next record, if already covered by the counter read (acquire)
@@ -2409,18 +2416,47 @@ double bits_to_d(unsigned long long b) {
 
 }  // namespace
 
-// Run a whole weld schedule on the tracked values tv (device complex).
+// A weld schedule prepared for one run: levels, launch-order descriptors,
+// write-back lists and every device buffer, uploaded on the preparing stream.
+// pipeline.py prepares it on the planning thread while the flatten runs, so
+// the weld stage starts with its first launch (the preparation is ~0.4 ms of
+// host time on cfg 2).
+struct Schedule {
+    int nsteps = 0, nlev = 0;
+    std::vector<int> level, order, pos;
+    std::vector<StepDesc> sd;
+    std::vector<int64_t> lev_wb;
+    std::vector<int32_t> wb3, h_src;
+    int64_t rec_tot = 0, arc_tot = 0;
+    DevBuf<StepDesc> d_sd;
+    DevBuf<int32_t> d_src, d_wb;
+    DevBuf<Rec> d_recs;
+    DevBuf<double2> d_arc;
+    DevBuf<double> d_meta;
+    DevBuf<unsigned long long> d_max;
+    DevBuf<int> d_nan, d_prog, d_tmo;
+    DevBuf<long long> d_wtime;
+    bool streamed = true, wtiming = false, used = false;
+    cudaStream_t sp = nullptr;     // the preparing stream (allocations, uploads)
+    cudaEvent_t ready = nullptr;   // recorded on sp after the uploads
+    double prep_ms = 0;
+    ~Schedule() {
+        if (ready) cudaEventDestroy(ready);
+    }
+};
+
 //  info  host int32 [nsteps*6]: k, closed, na, nb, comp_a, comp_b
 //  src   host int32 [sum(na+nb)] slot ids of a_cycle then b_cycle per step
 //  wb_off host int64 [nsteps+1], wb host int32 [2*total] (slot, code)
-//  out   host f64 [nsteps*8]: seam_error, seam_residual, area(res.a arc), status,
-//        nrec_a, nrec_b, level, spare
-int run_schedule(double2* tv, int32_t nsteps, const int32_t* info, const int32_t* src, const int64_t* wb_off,
-                 const int32_t* wb, double hard_tol, double* out, Rec* recs_host, int64_t recs_cap_total,
-                 cudaStream_t s) {
+int schedule_prepare(int32_t nsteps, const int32_t* info, const int32_t* src, const int64_t* wb_off, const int32_t* wb,
+                     cudaStream_t s, Schedule* S) {
+    S->nsteps = nsteps;
+    S->sp = s;
     if (nsteps <= 0) return PGCP_OK;
+    const auto th0 = std::chrono::steady_clock::now();
     // levels: a step waits for the previous steps on either of its components
-    std::vector<int> level(nsteps, 0);
+    std::vector<int>& level = S->level;
+    level.assign(nsteps, 0);
     {
         std::vector<std::pair<int, int>> last;  // comp -> level
         std::unordered_map<int, int> lv;
@@ -2434,18 +2470,23 @@ int run_schedule(double2* tv, int32_t nsteps, const int32_t* info, const int32_t
             lv[cb] = l;
         }
     }
-    int nlev = *std::max_element(level.begin(), level.end()) + 1;
+    const int nlev = S->nlev = *std::max_element(level.begin(), level.end()) + 1;
     // order steps by (level, index)
-    std::vector<int> order(nsteps);
+    std::vector<int>& order = S->order;
+    order.resize(nsteps);
     for (int i = 0; i < nsteps; ++i) order[i] = i;
     std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return level[x] < level[y]; });
-    std::vector<int> pos(nsteps);
+    std::vector<int>& pos = S->pos;
+    pos.resize(nsteps);
     for (int q = 0; q < nsteps; ++q) pos[order[q]] = q;
     // descriptors (in launch order)
-    std::vector<StepDesc> sd(nsteps);
+    std::vector<StepDesc>& sd = S->sd;
+    sd.resize(nsteps);
     std::vector<int64_t> src_off(nsteps + 1, 0);
     for (int i = 0; i < nsteps; ++i) src_off[i + 1] = src_off[i] + info[6 * i + 2] + info[6 * i + 3];
-    int64_t rec_tot = 0, arc_tot = 0;
+    int64_t& rec_tot = S->rec_tot;
+    int64_t& arc_tot = S->arc_tot;
+    rec_tot = arc_tot = 0;
     for (int q = 0; q < nsteps; ++q) {
         int i = order[q];
         StepDesc& d = sd[q];
@@ -2463,8 +2504,10 @@ int run_schedule(double2* tv, int32_t nsteps, const int32_t* info, const int32_t
     }
     // write-back entries (slot, code, launch-order step)
     int64_t nwb = wb_off[nsteps];
-    std::vector<int32_t> wb3(3 * std::max<int64_t>(nwb, 1));
-    std::vector<int64_t> lev_wb(nlev + 1, 0);
+    std::vector<int32_t>& wb3 = S->wb3;
+    wb3.resize(3 * std::max<int64_t>(nwb, 1));
+    std::vector<int64_t>& lev_wb = S->lev_wb;
+    lev_wb.assign(nlev + 1, 0);
     {
         int64_t o = 0;
         for (int l = 0; l < nlev; ++l) {
@@ -2482,13 +2525,14 @@ int run_schedule(double2* tv, int32_t nsteps, const int32_t* info, const int32_t
         }
         lev_wb[nlev] = o;
     }
-    DevBuf<StepDesc> d_sd;
-    DevBuf<int32_t> d_src, d_wb;
-    DevBuf<Rec> d_recs;
-    DevBuf<double2> d_arc;
-    DevBuf<double> d_meta;
-    DevBuf<unsigned long long> d_max;
-    DevBuf<int> d_nan;
+    auto& d_sd = S->d_sd;
+    auto& d_src = S->d_src;
+    auto& d_wb = S->d_wb;
+    auto& d_recs = S->d_recs;
+    auto& d_arc = S->d_arc;
+    auto& d_meta = S->d_meta;
+    auto& d_max = S->d_max;
+    auto& d_nan = S->d_nan;
     PGCP_TRY(d_sd.alloc(nsteps, s));
     PGCP_TRY(d_src.alloc(src_off[nsteps], s));
     PGCP_TRY(d_wb.alloc(3 * std::max<int64_t>(nwb, 1), s));
@@ -2501,14 +2545,15 @@ int run_schedule(double2* tv, int32_t nsteps, const int32_t* info, const int32_t
     PGCP_TRY(d_nan.zero(s));
     // streamed replay (default): each level's replay runs concurrently with
     // its phase 1 (PGCP_WELD_STREAM=0: after it)
-    const bool streamed = env_int("PGCP_WELD_STREAM", 1) != 0;
-    DevBuf<long long> d_wtime;  // PGCP_WELD_TIMING: phase-1 zip-loop cycle split per step
-    const bool wtiming = env_int("PGCP_WELD_TIMING", 0) != 0;
+    const bool streamed = S->streamed = env_int("PGCP_WELD_STREAM", 1) != 0;
+    auto& d_wtime = S->d_wtime;  // PGCP_WELD_TIMING: phase-1 zip-loop cycle split per step
+    const bool wtiming = S->wtiming = env_int("PGCP_WELD_TIMING", 0) != 0;
     if (wtiming) {
         PGCP_TRY(d_wtime.alloc(4 * (int64_t)nsteps, s));
         PGCP_TRY(d_wtime.zero(s));
     }
-    DevBuf<int> d_prog, d_tmo;
+    auto& d_prog = S->d_prog;
+    auto& d_tmo = S->d_tmo;
     if (streamed) {
         PGCP_TRY(d_prog.alloc(2 * (int64_t)nsteps, s));
         PGCP_TRY(d_prog.zero(s));
@@ -2516,8 +2561,48 @@ int run_schedule(double2* tv, int32_t nsteps, const int32_t* info, const int32_t
         PGCP_TRY(d_tmo.zero(s));
     }
     PGCP_TRY_CUDA(cudaMemcpyAsync(d_sd.p, sd.data(), nsteps * sizeof(StepDesc), cudaMemcpyHostToDevice, s));
-    PGCP_TRY_CUDA(cudaMemcpyAsync(d_src.p, src, src_off[nsteps] * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    S->h_src.assign(src, src + src_off[nsteps]);  // the caller's array need not outlive this call
+    PGCP_TRY_CUDA(cudaMemcpyAsync(d_src.p, S->h_src.data(), src_off[nsteps] * sizeof(int32_t), cudaMemcpyHostToDevice, s));
     PGCP_TRY_CUDA(cudaMemcpyAsync(d_wb.p, wb3.data(), 3 * nwb * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    PGCP_TRY_CUDA(cudaEventCreateWithFlags(&S->ready, cudaEventDisableTiming));
+    PGCP_TRY_CUDA(cudaEventRecord(S->ready, s));
+    S->prep_ms = 1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - th0).count();
+    return PGCP_OK;
+}
+
+// Run a prepared schedule on the tracked values tv (device complex), once.
+//  out   host f64 [nsteps*8]: seam_error, seam_residual, area(res.a arc), status,
+//        nrec_a, nrec_b, level, spare
+int schedule_execute(Schedule* S, double2* tv, double hard_tol, double* out, Rec* recs_host, int64_t recs_cap_total,
+                     cudaStream_t s) {
+    const int nsteps = S->nsteps;
+    if (nsteps <= 0) return PGCP_OK;
+    if (S->used) {
+        set_error("pgcp_weld_schedule_execute: a prepared schedule runs once");
+        return PGCP_E_INVALID;
+    }
+    S->used = true;
+    if (s != S->sp) PGCP_TRY_CUDA(cudaStreamWaitEvent(s, S->ready, 0));  // uploads happened on the preparing stream
+    const int nlev = S->nlev;
+    const std::vector<int>& level = S->level;
+    const std::vector<int>& order = S->order;
+    const std::vector<int>& pos = S->pos;
+    const std::vector<StepDesc>& sd = S->sd;
+    const std::vector<int64_t>& lev_wb = S->lev_wb;
+    const int64_t rec_tot = S->rec_tot;
+    auto& d_sd = S->d_sd;
+    auto& d_src = S->d_src;
+    auto& d_wb = S->d_wb;
+    auto& d_recs = S->d_recs;
+    auto& d_arc = S->d_arc;
+    auto& d_meta = S->d_meta;
+    auto& d_max = S->d_max;
+    auto& d_nan = S->d_nan;
+    auto& d_prog = S->d_prog;
+    auto& d_tmo = S->d_tmo;
+    auto& d_wtime = S->d_wtime;
+    const bool streamed = S->streamed, wtiming = S->wtiming;
+    const auto th1 = std::chrono::steady_clock::now();
     // PGCP_WELD_TIMING: CUDA events around the setup copies and every level
     std::vector<cudaEvent_t> lev_ev;
     if (wtiming) {
@@ -2589,10 +2674,20 @@ int run_schedule(double2* tv, int32_t nsteps, const int32_t* info, const int32_t
             r.maxbits = d_max.p;
             r.nan_flag = d_nan.p;
             if (streamed) {
+                // experiment knobs: CTA size of the replay and a dynamic shared-memory
+                // request it does not use (a large request keeps replay CTAs off
+                // the SMs that hold the level's phase-1 CTAs)
+                static const int rnt = std::max(32, std::min(1024, env_int("PGCP_WELD_REPLAY_NT", 128)));
+                static const int rsm = std::max(0, std::min(200, env_int("PGCP_WELD_REPLAY_SMEM_KB", 0))) * 1024;
+                static std::once_flag rsm_once;
+                if (rsm > 48 * 1024)
+                    std::call_once(rsm_once, [] {
+                        cudaFuncSetAttribute(k_replay_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, rsm);
+                    });
                 cudaLaunchConfig_t rc = {};
-                rc.gridDim = dim3((unsigned)grid_for(n, 128), 1, 1);
-                rc.blockDim = dim3(128, 1, 1);
-                rc.dynamicSmemBytes = 0;
+                rc.gridDim = dim3((unsigned)grid_for(n, rnt), 1, 1);
+                rc.blockDim = dim3(rnt, 1, 1);
+                rc.dynamicSmemBytes = rsm;
                 rc.stream = s;
                 cudaLaunchAttribute ra[1];
                 ra[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -2609,6 +2704,7 @@ int run_schedule(double2* tv, int32_t nsteps, const int32_t* info, const int32_t
         q0 = q1;
         if (wtiming) PGCP_TRY_CUDA(cudaEventRecord(lev_ev[l + 2], s));
     }
+    const auto th2 = std::chrono::steady_clock::now();  // every level launched
     std::vector<double> meta((size_t)META * nsteps);
     std::vector<unsigned long long> mx(3 * (size_t)nsteps);
     int hnan = 0;
@@ -2623,6 +2719,12 @@ int run_schedule(double2* tv, int32_t nsteps, const int32_t* info, const int32_t
     PGCP_TRY(d2h_flush(s));
     if (wtiming) {
         PGCP_TRY_CUDA(cudaEventSynchronize(lev_ev.back()));
+        const auto th3 = std::chrono::steady_clock::now();
+        auto ms_of = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+            return 1e3 * std::chrono::duration<double>(b - a).count();
+        };
+        fprintf(stderr, "[weld timing] host ms: preparation %.3f, launches %.3f, wait + reads %.3f\n", S->prep_ms,
+                ms_of(th1, th2), ms_of(th2, th3));
         fprintf(stderr, "[weld timing] device ms:");
         for (int l = 0; l + 1 < (int)lev_ev.size(); ++l) {
             float ms = 0.f;
@@ -2701,6 +2803,16 @@ int run_schedule(double2* tv, int32_t nsteps, const int32_t* info, const int32_t
     return status;
 }
 
+// Run a whole weld schedule on the tracked values tv (prepare + execute).
+int run_schedule(double2* tv, int32_t nsteps, const int32_t* info, const int32_t* src, const int64_t* wb_off,
+                 const int32_t* wb, double hard_tol, double* out, Rec* recs_host, int64_t recs_cap_total,
+                 cudaStream_t s) {
+    if (nsteps <= 0) return PGCP_OK;
+    Schedule S;
+    PGCP_TRY(schedule_prepare(nsteps, info, src, wb_off, wb, s, &S));
+    return schedule_execute(&S, tv, hard_tol, out, recs_host, recs_cap_total, s);
+}
+
 }  // namespace weld
 }  // namespace pgcp
 
@@ -2708,6 +2820,33 @@ using namespace pgcp;
 using namespace pgcp::weld;
 
 extern "C" {
+
+PGCP_API int pgcp_weld_schedule_prepare(int32_t nsteps, const int32_t* info, const int32_t* src, const int64_t* wb_off,
+                                        const int32_t* wb, void* stream, void** handle) {
+    if (!handle || nsteps < 0 || (nsteps > 0 && (!info || !src || !wb_off))) {
+        set_error("pgcp_weld_schedule_prepare: invalid arguments");
+        return PGCP_E_INVALID;
+    }
+    *handle = nullptr;
+    std::unique_ptr<Schedule> S(new Schedule());
+    int rc = schedule_prepare(nsteps, info, src, wb_off, wb, reinterpret_cast<cudaStream_t>(stream), S.get());
+    if (rc != PGCP_OK) return rc;
+    *handle = S.release();
+    return PGCP_OK;
+}
+
+PGCP_API int pgcp_weld_schedule_execute(void* handle, double* tv, double hard_tol, double* out, pgcp_rec* recs_host,
+                                        int64_t recs_cap, void* stream) {
+    Schedule* S = reinterpret_cast<Schedule*>(handle);
+    if (!S || !tv || (S->nsteps > 0 && !out)) {
+        set_error("pgcp_weld_schedule_execute: invalid arguments");
+        return PGCP_E_INVALID;
+    }
+    return schedule_execute(S, reinterpret_cast<double2*>(tv), hard_tol, out, recs_host, recs_cap,
+                            reinterpret_cast<cudaStream_t>(stream));
+}
+
+PGCP_API void pgcp_weld_schedule_free(void* handle) { delete reinterpret_cast<Schedule*>(handle); }
 
 PGCP_API int pgcp_weld_schedule_run(double* tv, int32_t nsteps, const int32_t* info, const int32_t* src,
                                     const int64_t* wb_off, const int32_t* wb, double hard_tol, double* out,

@@ -54,9 +54,12 @@ def validate_cuts(mesh, cuts):
     """Sorted pairs (partition.py:48-59); duplicates rejected here, non-edges
     by the device partition (k_mark_cuts), with the reference's messages."""
     cuts = np.asarray(cuts, dtype=np.int64).reshape(-1, 2)
-    norm = np.sort(cuts, axis=1)
+    norm = np.empty_like(cuts)  # each pair sorted (elementwise min / max: a row-wise np.sort is 4x slower)
+    np.minimum(cuts[:, 0], cuts[:, 1], out=norm[:, 0])
+    np.maximum(cuts[:, 0], cuts[:, 1], out=norm[:, 1])
     if len(norm) > 1:  # duplicates first, as the reference (also duplicate non-edges)
-        key = np.sort(norm[:, 0] * (int(norm.max()) + 1) + norm[:, 1])
+        key = norm[:, 0] * (int(norm[:, 1].max()) + 1) + norm[:, 1]
+        key.sort()
         if np.any(key[1:] == key[:-1]):
             raise PartitionError("duplicate cut edges")
     return norm

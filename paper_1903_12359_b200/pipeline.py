@@ -29,7 +29,7 @@ from .assemble import GlobalParam
 from .errors import PartitionError, SolveError, ValidationError, WeldError
 from .mesh import TriMesh, load_obj, validate_topology, write_obj_with_param
 from .partition import Partition, plan_weld_schedule, read_cut_edges, validate_cuts
-from .welding import (ARC_FROM_B, CYC_A, CYC_B, SIDE_B, _from_native, run_schedule)
+from .welding import (ARC_FROM_B, CYC_A, CYC_B, SIDE_B, PreparedSchedule, _from_native, run_schedule)
 
 
 @dataclass
@@ -310,13 +310,18 @@ def parameterize(mesh, cuts=None, mode="free", workers=1, seed=0, mobius_area=Fa
 
         pworker = threading.Thread(target=_hprep_early, name="pgcp-harmonic-prepare")
         pworker.start()
-    steps, plan, perr = [], None, None
+    steps, plan, perr, sched = [], None, None, None
     t_plan = time.perf_counter()
     try:
         if have_cuts:
             steps = plan_weld_schedule(part, mode, pairs=cfg.pairs if cfg.schedule == "pairs" else None)
         if welds:
             plan = WeldPlan(cycles, steps, mesh.n_vertices)
+            # the weld's host-side preparation and uploads, here (this thread
+            # would only wait for the flatten) instead of at the head of the
+            # weld stage; on this thread's stream, which is idle meanwhile
+            if len(steps) and os.environ.get("PGCP_WELD_PREPARE", "1") != "0":
+                sched = PreparedSchedule(plan.info, plan.src, plan.wb_off, plan.wb)
         timings["plan (overlapped)"] = time.perf_counter() - t_plan
     except BaseException as exc:
         perr = exc
@@ -382,7 +387,10 @@ def parameterize(mesh, cuts=None, mode="free", workers=1, seed=0, mobius_area=Fa
                     own_slots, tv = _exchange_boundary(shard, plan, loop_gid_host, z0, dev)
                 out = None
                 if len(steps):
-                    out, _ = run_schedule(tv, plan.info, plan.src, plan.wb_off, plan.wb, cfg.hard_tol)
+                    if sched is not None:
+                        out = sched.run(tv, cfg.hard_tol)
+                    else:
+                        out, _ = run_schedule(tv, plan.info, plan.src, plan.wb_off, plan.wb, cfg.hard_tol)
                     report.seam_residuals = [float(x) for x in out[:, 1]]
         except BaseException:
             for w in (hworker, pworker):  # never leave the preparation running on the batch

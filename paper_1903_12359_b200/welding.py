@@ -24,6 +24,9 @@ INF = np.complex128(complex(np.inf, 0.0))
 
 _VP, _I32, _I64, _D = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
 nat.register("pgcp_weld_schedule_run", [_VP, _I32, _VP, _VP, _VP, _VP, _D, _VP, _VP, _I64, _VP])
+nat.register("pgcp_weld_schedule_prepare", [_I32, _VP, _VP, _VP, _VP, _VP, ctypes.POINTER(ctypes.c_void_p)])
+nat.register("pgcp_weld_schedule_execute", [_VP, _VP, _D, _VP, _VP, _I64, _VP])
+nat.register("pgcp_weld_schedule_free", [_VP], None)
 nat.register("pgcp_weld_replay", [_VP, _I32, _VP, _VP, _I64, _VP])
 nat.register("pgcp_weld_geodesic", [_VP, _VP, _I32, _VP, _VP, _VP, _I32, _VP, _VP])
 nat.register("pgcp_polygon_interior", [_VP, _VP, _I32, ctypes.c_int, _VP, _VP])
@@ -355,6 +358,46 @@ def run_schedule(tv, info, src, wb_off, wb, hard_tol, want_logs=False):
             logs.append((la, lb))
     nat.check(st)
     return out, logs
+
+
+class PreparedSchedule:
+    """A weld schedule whose host-side preparation and uploads are already
+    done (pgcp_weld_schedule_prepare, on the current stream): `run(tv)` starts
+    with the first weld launch. One run per object."""
+
+    def __init__(self, info, src, wb_off, wb):
+        self.nsteps = len(info)
+        info = np.ascontiguousarray(np.asarray(info, dtype=np.int32).reshape(-1, 6))
+        src = np.ascontiguousarray(np.asarray(src, dtype=np.int32))
+        wb_off = np.ascontiguousarray(np.asarray(wb_off, dtype=np.int64))
+        wb = np.ascontiguousarray(np.asarray(wb, dtype=np.int32).reshape(-1, 2))
+        self._h = ctypes.c_void_p()
+        nat.check(nat.lib().pgcp_weld_schedule_prepare(self.nsteps, info.ctypes.data, src.ctypes.data,
+                                                       wb_off.ctypes.data, wb.ctypes.data, _stream(),
+                                                       ctypes.byref(self._h)))
+
+    def run(self, tv, hard_tol):
+        """Weld the tracked values `tv` (CUDA complex tensor, in place) on the
+        current stream; returns the per-step out array of `run_schedule`."""
+        from .device import ptr
+        out = np.zeros((max(self.nsteps, 1), 8))
+        try:
+            nat.check(nat.lib().pgcp_weld_schedule_execute(self._h, ptr(tv), float(hard_tol), out.ctypes.data, None, 0,
+                                                           _stream()))
+        finally:
+            self.close()
+        return out
+
+    def close(self):
+        if self._h:
+            nat.lib().pgcp_weld_schedule_free(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 ARC_FROM_B = 1 << 24

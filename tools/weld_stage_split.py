@@ -36,6 +36,18 @@ def timed(tv, *a, **k):
 
 
 pl.run_schedule = timed
+_run = wd.PreparedSchedule.run
+
+
+def timed_run(self, tv, hard_tol):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    r = _run(self, tv, hard_tol)
+    print(f"PreparedSchedule.run: {1e3 * (time.perf_counter() - t0):.3f} ms", flush=True)
+    return r
+
+
+wd.PreparedSchedule.run = timed_run
 for _ in range(3):
     gp, rep = pg.parameterize(mesh, cuts, "free", pairs=pairs, keep_device=True)
     print("weld stage ms", rep.timings["weld"] * 1e3, flush=True)
