@@ -2638,7 +2638,7 @@ int factor_levels(DirectFactor* D, FacArgs& fa, cudaStream_t s, PhaseTimer& pt) 
     // leaves most SMs idle, so the complex list runs on a second stream of
     // the same priority, forked and joined per level with events
     // (PGCP_DIRECT_TWO_STREAMS=0: one stream).
-    static const bool two = env_int("PGCP_DIRECT_TWO_STREAMS", 1) != 0;
+    const bool two = env_int("PGCP_DIRECT_TWO_STREAMS", 1) != 0;
     cudaStream_t s2 = nullptr;
     cudaEvent_t ef = nullptr, ej = nullptr;
     if (two && D->ncplx > 0 && D->ncplx < D->nnodes) {
@@ -3029,7 +3029,7 @@ int direct_factor(pgcp_batch* b, const DirectInput& in, DirectFactor** out, cuda
             // a lone warp on an 80-100 wide front is slower than a CTA) split
             // off, if they are most of the list; the few larger ones take a CTA
             // each. PGCP_DIRECT_WSPLIT=0: no split (a mixed list takes CTAs).
-            static const bool wsplit = env_int("PGCP_DIRECT_WSPLIT", 1) != 0;
+            const bool wsplit = env_int("PGCP_DIRECT_WSPLIT", 1) != 0;
             int64_t w0 = o0;
             if (no_warp) {
                 w0 = o1;

@@ -2674,20 +2674,10 @@ int schedule_execute(Schedule* S, double2* tv, double hard_tol, double* out, Rec
             r.maxbits = d_max.p;
             r.nan_flag = d_nan.p;
             if (streamed) {
-                // experiment knobs: CTA size of the replay and a dynamic shared-memory
-                // request it does not use (a large request keeps replay CTAs off
-                // the SMs that hold the level's phase-1 CTAs)
-                static const int rnt = std::max(32, std::min(1024, env_int("PGCP_WELD_REPLAY_NT", 128)));
-                static const int rsm = std::max(0, std::min(200, env_int("PGCP_WELD_REPLAY_SMEM_KB", 0))) * 1024;
-                static std::once_flag rsm_once;
-                if (rsm > 48 * 1024)
-                    std::call_once(rsm_once, [] {
-                        cudaFuncSetAttribute(k_replay_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, rsm);
-                    });
                 cudaLaunchConfig_t rc = {};
-                rc.gridDim = dim3((unsigned)grid_for(n, rnt), 1, 1);
-                rc.blockDim = dim3(rnt, 1, 1);
-                rc.dynamicSmemBytes = rsm;
+                rc.gridDim = dim3((unsigned)grid_for(n, 128), 1, 1);  // larger CTAs measured slower
+                rc.blockDim = dim3(128, 1, 1);
+                rc.dynamicSmemBytes = 0;
                 rc.stream = s;
                 cudaLaunchAttribute ra[1];
                 ra[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

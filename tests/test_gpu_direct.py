@@ -134,3 +134,34 @@ def test_boundary_last_factor_serves_dirichlet(cuda, monkeypatch):
     V, F, cuts = gen.height_field_case(97, 3, seed=4)
     b, z = _check_vs_oracle(V, F, cuts, 1e-9, 1e-12)
     assert b.last_solve(1)["borrowed"] and b.last_solve(1)["fmas"] == 0
+
+
+@pytest.mark.parametrize("switch", ["PGCP_DIRECT_TWO_STREAMS", "PGCP_DIRECT_WSPLIT", "PGCP_DIRECT_NO_WARP"])
+def test_direct_front_scheduling_is_result_neutral(cuda, monkeypatch, switch):
+    """How the fronts of a level are scheduled -- complex fronts on a second
+    stream, warp-sized fronts split off a list of larger ones and packed into
+    CTAs by size -- does not change a front's arithmetic: the flatten and the
+    Dirichlet solve are bit-identical with each option off (257^2 subdomains:
+    the upper lists mix warp-sized and larger fronts, real and complex)."""
+    from paper_1903_12359_b200 import generators as gen
+    V, F, cuts = gen.height_field_case(513, 2, seed=4)
+    b = _batch(V, F, cuts)
+    voff, loops = _loops(b)
+    gid = np.concatenate([voff[c] + loops[c] for c in range(b.K)]).astype(np.int32)
+
+    def run():
+        z, st = b.flatten(solver="direct")
+        assert all(s["status"] == 0 for s in st)
+        z = z.cpu().numpy()
+        zh, sth = b.harmonic(gid, z[gid], solver="direct")
+        assert all(s["status"] == 0 for s in sth)
+        return z, zh.cpu().numpy()
+
+    z0, h0 = run()
+    monkeypatch.setenv(switch, "1" if switch == "PGCP_DIRECT_NO_WARP" else "0")
+    z1, h1 = run()
+    if switch == "PGCP_DIRECT_NO_WARP":  # another kernel's summation order: agreement, not identity
+        assert np.max(np.abs(z0 - z1)) <= 1e-9 * _diam(z0)
+        assert np.max(np.abs(h0 - h1)) <= 1e-9 * _diam(h0)
+    else:
+        assert np.array_equal(z0, z1) and np.array_equal(h0, h1)

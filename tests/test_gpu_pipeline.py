@@ -208,6 +208,30 @@ def test_wave_weld_equals_barrier_weld(cuda, monkeypatch, case):
     assert r0.seam_residuals == r1.seam_residuals
 
 
+def test_prepared_schedule_equals_single_call(cuda, monkeypatch):
+    """pgcp_weld_schedule_prepare + _execute (the pipeline's default: prepared
+    on the planning thread during the flatten) is the same weld as the single
+    pgcp_weld_schedule_run call, bit for bit, and a prepared schedule refuses a
+    second run."""
+    from paper_1903_12359_b200 import TriMesh, parameterize
+    from paper_1903_12359_b200.welding import PreparedSchedule
+    z = load_golden("qtree4x4")
+    mesh = TriMesh(z["V"], z["F"])
+    kw = {"pairs": case_pairs("qtree4x4")}
+    monkeypatch.setenv("PGCP_WELD_PREPARE", "0")
+    g0, r0 = parameterize(mesh, z["cuts"], str(z["mode"]), **kw)
+    monkeypatch.setenv("PGCP_WELD_PREPARE", "1")
+    g1, r1 = parameterize(mesh, z["cuts"], str(z["mode"]), **kw)
+    assert np.array_equal(np.asarray(g0.coords), np.asarray(g1.coords))
+    assert r0.seam_residuals == r1.seam_residuals
+    # an unused handle is released without a run
+    info = np.array([[2, 0, 3, 3, 0, 1]], dtype=np.int32)
+    ps = PreparedSchedule(info, np.arange(6, dtype=np.int32), np.array([0, 0], dtype=np.int64),
+                          np.zeros((0, 2), dtype=np.int32))
+    ps.close()
+    ps.close()
+
+
 def test_wave_weld_errors(cuda, monkeypatch):
     """Weld failures inside the wavefront loops surface as the same
     WeldError as with the barrier kernel, on every weld size."""
