@@ -249,7 +249,7 @@ __global__ void k_default_pins(int32_t K, const int64_t* __restrict__ loop_off, 
 
 // per submesh E_D - A of a complex embedding (flatten.py:89-110); one block
 // per submesh, fixed-order reduction
-__global__ void k_energy(const int64_t* __restrict__ vert_off, const int64_t* __restrict__ row_ptr,
+__global__ void __launch_bounds__(1024) k_energy(const int64_t* __restrict__ vert_off, const int64_t* __restrict__ row_ptr,
                          const int32_t* __restrict__ col, const double* __restrict__ val,
                          const int64_t* __restrict__ loop_off, const int32_t* __restrict__ loop,
                          const double2* __restrict__ z, double* __restrict__ energy) {
@@ -345,7 +345,7 @@ int conformal_energy(pgcp_batch* b, const double* z, double* energy, cudaStream_
     if (!b->has_laplacian) PGCP_TRY(build_laplacian(b, nullptr, s));
     DevBuf<double> e;
     PGCP_TRY(e.alloc(b->K, s));
-    k_energy<<<b->K, 256, 0, s>>>(b->vert_off.p, b->row_ptr.p, b->col.p, b->val.p, b->loop_off.p, b->loop.p,
+    k_energy<<<b->K, 1024, 0, s>>>(b->vert_off.p, b->row_ptr.p, b->col.p, b->val.p, b->loop_off.p, b->loop.p,
                                   (const double2*)z, e.p);
     PGCP_LAUNCH_CHECK();
     PGCP_TRY_CUDA(cudaMemcpyAsync(energy, e.p, b->K * sizeof(double), cudaMemcpyDeviceToHost, s));

@@ -2015,7 +2015,8 @@ __global__ void k_ref_nnz(const int64_t* __restrict__ sl_off, const int64_t* __r
 
 // true residual of the unscaled system from the scaled arrays:
 //   ||b - H x||^2 = sum D |b^ - H^ y|^2, ||x||^2 = sum |y|^2 / D, ||b||^2 = sum D |b^|^2
-__global__ void k_true_residual(PcgArgs A) {
+// (1024 threads: one CTA per slot, so only nslot SMs work; the warps hide the gather latency)
+__global__ void __launch_bounds__(1024) k_true_residual(PcgArgs A) {
     __shared__ double red[3][32];
     const int slot = blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -2099,7 +2100,7 @@ __global__ void k_scatter(int64_t ne, int32_t nslot, const int32_t* __restrict__
 }
 
 // per slot: shoelace area of the loop, E_D - A, max |z| (flatten.py:176-187)
-__global__ void k_flat_checks(const int32_t* __restrict__ comps, const int64_t* __restrict__ vert_off,
+__global__ void __launch_bounds__(1024) k_flat_checks(const int32_t* __restrict__ comps, const int64_t* __restrict__ vert_off,
                               const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
                               const double* __restrict__ val, const int64_t* __restrict__ loop_off,
                               const int32_t* __restrict__ loop, const double2* __restrict__ z,
@@ -3022,13 +3023,13 @@ int run_solve(pgcp_batch* b, SolveSystem* S, const pgcp_solve_opts* o, double* z
         cudaEventSynchronize(e1);
         t_post = std::chrono::steady_clock::now();
     }
-    k_true_residual<<<nslot, 512, 0, s>>>(A);
+    k_true_residual<<<nslot, 1024, 0, s>>>(A);
     PGCP_LAUNCH_CHECK();
     k_scatter<<<grid_for(S->ne, 256), 256, 0, s>>>(S->ne, nslot, S->d_comps.p, S->sv_off.p, b->vert_off.p, S->urow.p,
                                                  S->fixed_ref.p, S->fv.p, S->x.p, S->Dsq.p, (double2*)z);
     PGCP_LAUNCH_CHECK();
     if (S->dncp) {
-        k_flat_checks<<<nslot, 256, 0, s>>>(S->d_comps.p, b->vert_off.p, b->row_ptr.p, b->col.p, b->val.p,
+        k_flat_checks<<<nslot, 1024, 0, s>>>(S->d_comps.p, b->vert_off.p, b->row_ptr.p, b->col.p, b->val.p,
                                             b->loop_off.p, b->loop.p, (const double2*)z, S->res.p);
         PGCP_LAUNCH_CHECK();
     }
