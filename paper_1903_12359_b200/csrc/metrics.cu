@@ -492,13 +492,17 @@ __global__ void k_hist_bins(const double* __restrict__ x, int64_t n, const doubl
     }
 }
 
-int sum_of(const double* part, int nblocks, double* out, cudaStream_t s) {
-    std::vector<double> h(nblocks);
-    PGCP_TRY_CUDA(cudaMemcpyAsync(h.data(), part, nblocks * sizeof(double), cudaMemcpyDeviceToHost, s));
-    PGCP_TRY_CUDA(cudaStreamSynchronize(s));
-    double t = 0;
-    for (double v : h) t += v;
-    *out = t;
+// host sum of nsums consecutive groups of nblocks block partials (fixed
+// order), read through the pinned staging buffer with one synchronisation
+int sum_of(const double* part, int nblocks, double* out, cudaStream_t s, int nsums = 1) {
+    std::vector<double> h((size_t)nblocks * nsums);
+    PGCP_TRY(d2h_async(h.data(), part, h.size() * sizeof(double), s));
+    PGCP_TRY(d2h_flush(s));
+    for (int q = 0; q < nsums; ++q) {
+        double t = 0;
+        for (int i = 0; i < nblocks; ++i) t += h[(size_t)q * nblocks + i];
+        out[q] = t;
+    }
     return PGCP_OK;
 }
 
@@ -509,6 +513,15 @@ int dsum(int64_t n, Fn fn, DevBuf<double>& part, double* out, cudaStream_t s) {
     k_partial_sum<Fn><<<SUM_BLOCKS, 256, 0, s>>>(n, fn, part.p);
     PGCP_LAUNCH_CHECK();
     return sum_of(part.p, SUM_BLOCKS, out, s);
+}
+// two independent sums, one synchronisation (part holds 2 x SUM_BLOCKS)
+template <class Fa, class Fb>
+int dsum2(int64_t na, Fa fa, int64_t nb, Fb fb, DevBuf<double>& part, double* out2, cudaStream_t s) {
+    k_partial_sum<Fa><<<SUM_BLOCKS, 256, 0, s>>>(na, fa, part.p);
+    PGCP_LAUNCH_CHECK();
+    k_partial_sum<Fb><<<SUM_BLOCKS, 256, 0, s>>>(nb, fb, part.p + SUM_BLOCKS);
+    PGCP_LAUNCH_CHECK();
+    return sum_of(part.p, SUM_BLOCKS, out2, s, 2);
 }
 
 double lerp_np(double a, double b, double t) {
@@ -592,8 +605,8 @@ int select_ranks(const double* x, int64_t n, SelState* hs, Reducer& red, cudaStr
         k_sel_pick<RB><<<NSEL, 256, 0, s>>>(pass, st.p, hist.p, rep.p);
         PGCP_LAUNCH_CHECK();
     }
-    PGCP_TRY_CUDA(cudaMemcpyAsync(hs, st.p, NSEL * sizeof(SelState), cudaMemcpyDeviceToHost, s));
-    PGCP_TRY_CUDA(cudaStreamSynchronize(s));
+    PGCP_TRY(d2h_async(hs, st.p, NSEL * sizeof(SelState), s));  // pinned staging (common.cuh)
+    PGCP_TRY(d2h_flush(s));
     return PGCP_OK;
 }
 
@@ -602,8 +615,7 @@ int select_ranks(const double* x, int64_t n, SelState* hs, Reducer& red, cudaStr
 int summarize_dev(const double* x, int64_t n, double* out4, int64_t* count, DevBuf<double>& part, cudaStream_t s,
                   Reducer& red, double* vmax = nullptr) {
     double cs[2] = {0, 0};  // count, sum
-    PGCP_TRY(dsum(n, Count{x}, part, &cs[0], s));
-    PGCP_TRY(dsum(n, AbsVal{x}, part, &cs[1], s));
+    PGCP_TRY(dsum2(n, Count{x}, n, AbsVal{x}, part, cs, s));
     PGCP_TRY(red.host(cs, 2, PGCP_RED_SUM));
     const double cnt = cs[0], sum = cs[1];
     *count = (int64_t)cnt;
@@ -701,9 +713,9 @@ PGCP_API int pgcp_batch_stitch_ex(pgcp_batch* b, const double* z, int mode, doub
     PGCP_LAUNCH_CHECK();
     unsigned long long h[4];
     int hm = 0;
-    PGCP_TRY_CUDA(cudaMemcpyAsync(h, bits.p, sizeof h, cudaMemcpyDeviceToHost, s));
-    PGCP_TRY_CUDA(cudaMemcpyAsync(&hm, missing.p, sizeof hm, cudaMemcpyDeviceToHost, s));
-    PGCP_TRY_CUDA(cudaStreamSynchronize(s));
+    PGCP_TRY(d2h_async(h, bits.p, sizeof h, s));
+    PGCP_TRY(d2h_async(&hm, missing.p, sizeof hm, s));
+    PGCP_TRY(d2h_flush(s));
     double seam, scale, circ;
     memcpy(&seam, &h[0], 8);
     memcpy(&scale, &h[1], 8);
@@ -795,7 +807,7 @@ PGCP_API int pgcp_area_distortion(const double* V, const int32_t* F, int64_t n, 
     PGCP_TRY(absd.alloc(3 * m, s));
     PGCP_TRY(a_new.alloc(m, s));
     PGCP_TRY(a_ref.alloc(m, s));
-    PGCP_TRY(part.alloc(SUM_BLOCKS, s));
+    PGCP_TRY(part.alloc(2 * SUM_BLOCKS, s));
     k_distortion<<<grid_for(m, 256), 256, 0, s>>>(V, F, m, coords, mode_sphere, nullptr, dc.p, vc.p, absd.p, a_new.p,
                                                   a_ref.p);
     PGCP_LAUNCH_CHECK();
@@ -843,7 +855,7 @@ PGCP_API int pgcp_distortion_ex(const double* V, const int32_t* F, int64_t n, in
     PGCP_TRY(a_new.alloc(m, s));
     PGCP_TRY(a_ref.alloc(m, s));
     PGCP_TRY(aabs.alloc(m, s));
-    PGCP_TRY(part.alloc(SUM_BLOCKS, s));
+    PGCP_TRY(part.alloc(2 * SUM_BLOCKS, s));
     k_distortion<<<grid_for(m, 256), 256, 0, s>>>(V, F, m, coords, mode_sphere, face_mask, d, valid, absd.p, a_new.p,
                                                   a_ref.p);
     PGCP_LAUNCH_CHECK();
@@ -852,8 +864,7 @@ PGCP_API int pgcp_distortion_ex(const double* V, const int32_t* F, int64_t n, in
     double mval = 0;
     PGCP_TRY(summarize_dev(absd.p, 3 * m, ang, &nc, part, s, red, &mval));
     double sa[2] = {0, 0};  // total parametric and original area
-    PGCP_TRY(dsum(m, Plain{a_new.p}, part, &sa[0], s));
-    PGCP_TRY(dsum(m, Plain{a_ref.p}, part, &sa[1], s));
+    PGCP_TRY(dsum2(m, Plain{a_new.p}, m, Plain{a_ref.p}, part, sa, s));
     PGCP_TRY(red.host(sa, 2, PGCP_RED_SUM));
     k_area_logratio<<<grid_for(m, 256), 256, 0, s>>>(m, a_new.p, a_ref.p, sa[0], sa[1], aabs.p);
     PGCP_LAUNCH_CHECK();
@@ -893,8 +904,8 @@ PGCP_API int pgcp_distortion_ex(const double* V, const int32_t* F, int64_t n, in
             k_hist_bins<<<grid_for(3 * m, 256), 256, 0, s>>>(absd.p, 3 * m, de.p, (int)nb, cnt.p);
         PGCP_LAUNCH_CHECK();
         PGCP_TRY(red.dev(cnt.p, nb, PGCP_RED_U64, PGCP_RED_SUM));
-        PGCP_TRY_CUDA(cudaMemcpyAsync(hist, cnt.p, nb * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
-        PGCP_TRY_CUDA(cudaStreamSynchronize(s));
+        PGCP_TRY(d2h_async(hist, cnt.p, nb * sizeof(uint64_t), s));
+        PGCP_TRY(d2h_flush(s));
     }
     summary[14] = (double)red.bytes;
     return PGCP_OK;
