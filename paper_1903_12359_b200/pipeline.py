@@ -266,9 +266,10 @@ def parameterize(mesh, cuts=None, mode="free", workers=1, seed=0, mobius_area=Fa
     overlap_prep = welds and os.environ.get("PGCP_OVERLAP_HPREP", "1") != "0"
     # where the harmonic preparation (the Dirichlet factorization) overlaps:
     # the flatten (default) or, with PGCP_HPREP_AT=weld, the weld (the weld
-    # then runs on the high-priority stream). cfg 2: the weld placement is
-    # ~1.5 ms faster with device-resident inputs but 2-8 ms slower and
-    # erratic end to end (host-array inputs), so the default stays here.
+    # then runs on the high-priority stream). cfg 2, end of round 2: beside the
+    # weld the flatten runs at its standalone 10.7 ms (12.4 with the
+    # preparation beside it), but the weld's latency-bound record chain slows
+    # from 5.4 to 8.8 ms: 25.5 ms per step against 23.5, so the default stays.
     prep_at_weld = overlap_prep and os.environ.get("PGCP_HPREP_AT", "flatten") == "weld"
 
     def _flatten():
