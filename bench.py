@@ -486,7 +486,7 @@ def main():
     num_ms = statistics.mean(x["numeric_ms"] for x in fl)
     fmas = statistics.mean(x["fmas"] for x in fl)
     achieved = 2.0 * fmas / (num_ms / 1e3) / 1e12
-    dncp = ncu_summary("r2_direct_ncu_summary.json")
+    dncp = ncu_summary("r2_direct_ncu_summary_end.json")
     roof = {"bound": "fp64",
             "kernel": "multifrontal numeric factorization of the 64 cfg-2 DNCP systems (k_factor_warp / "
                       "k_factor_sm / k_factor / k_asm_* / k_pdiag / k_pupd / k_schur: 13 dissection levels x "

@@ -282,7 +282,7 @@ def bench_distributed(args, V, F, cuts, pairs, metric, unit, workload):
                               "systems (bench.py's `roofline` at N = 1)",
                     "achieved": achieved, "peak": fp64, "unit": "TFLOP/s",
                     "frac": achieved / fp64 if fp64 else None,
-                    "traffic": B.ncu_summary("r2_direct_ncu_summary.json").get("dram_bytes_per_factorization"),
+                    "traffic": B.ncu_summary("r2_direct_ncu_summary_end.json").get("dram_bytes_per_factorization"),
                     "peak_source": "measured here: pgcp_fp64_probe on rank 0", "numeric_ms": numeric_ms,
                     "flops_per_step_all_ranks": 2.0 * fmas_all, "hbm_peak": peak, "hbm_peak_source": peak_src,
                     "note": "per-GPU average of the factorization flops over the slowest rank's numeric "

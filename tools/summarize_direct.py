@@ -14,7 +14,7 @@ import sys
 
 NUMERIC = ("k_factor", "k_factor_sm", "k_factor_warp", "k_schur", "k_pdiag", "k_pupd", "k_asm_cols", "k_asm_child")
 SETUP = ("k_d_", "k_nd_", "k_sym", "k_eadj", "k_mark_cplx", "k_front_sizes", "k_iota")
-SOLVE = ("k_fwd", "k_bwd", "k_d_scatter")
+SOLVE = ("k_fwd", "k_bwd", "k_d_scatter", "k_solve_pers", "k_solve_warp", "k_perm_rhs")
 
 
 def launches(path):
