@@ -1145,7 +1145,11 @@ __global__ void __launch_bounds__(DNT) k_pdiag(FacArgs a, int k0, int phase) {
     }
     if (phase == 0) {
         __syncthreads();
-        if (threadIdx.x < 32) diag_factor<T, PB>(Ld, nb, &bad);
+        // by the whole CTA in shared memory: the one-warp register form is a
+        // fully unrolled 32 x 32 block (~10K straight-line instructions for
+        // complex fronts, every one a cold instruction fetch): 54-105 us per
+        // level in the launch list against ~15 us this way
+        diag_factor_cta<T, PB, DNT>(Ld, nb, &bad);
         __syncthreads();
         for (int idx = threadIdx.x; idx < PB * PB; idx += DNT) {
             const int i = idx % PB, j = idx / PB;
