@@ -430,6 +430,7 @@ def main():
     sampler.start()
     l0 = lib.pgcp_launch_count()
     total_ms = 0.0
+    step_ms = []
     flat_stats, harm_stats = [], []
     stages = {}
     for _ in range(args.steps):
@@ -441,7 +442,8 @@ def main():
         gp, rep = step_value()
         e1.record(stream)
         torch.cuda.synchronize()
-        total_ms += e0.elapsed_time(e1)
+        step_ms.append(e0.elapsed_time(e1))
+        total_ms += step_ms[-1]
         flat_stats.append(rep.solver["flatten"])
         harm_stats.append(rep.solver.get("harmonic", {}))
         for k, v in rep.timings.items():
@@ -542,6 +544,7 @@ def main():
                        "l2": "flushed before every timed step (256 MiB write)", "parallelism": "1 GPU"},
             "roofline": roof, "roofline_pcg": roof_pcg, "roofline_cfg5": cfg5, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
             "gpu_launches": int(launches),
+            "ms_steps": [round(x, 3) for x in step_ms], "ms_per_step_median": statistics.median(step_ms),
             "stages_ms_per_step": {k: v / args.steps for k, v in stages.items()},
             "quality": {"flips": rep.flips, "angular_mean_deg": rep.distortion["angular_abs"]["mean"],
                         "angular_sd_deg": rep.distortion["angular_abs"]["sd"]}}
