@@ -1116,9 +1116,6 @@ __global__ void __launch_bounds__(DNT, sizeof(T) == 8 ? 8 : 4) k_factor(FacArgs 
 constexpr int PB = 32;
 constexpr int FUSED_MAXS = 48;
 constexpr size_t SM_FRONT_BYTES = 112 * 1024;  // k_factor_sm: two CTAs per SM
-// k_factor_warp CTA: 8 warps share this much dynamic shared memory (real
-// fronts: three CTAs per SM at 80 registers; complex: two at 125)
-constexpr size_t warp_cta_bytes(size_t tsz) { return tsz == 8 ? 75 * 1024 : 112 * 1024; }
 // k_factor_warp fronts split off a list of larger ones: up to 70 wide (real and complex)
 constexpr size_t warp_split_bytes(size_t tsz) { return tsz == 8 ? 20 * 1024 : 40 * 1024; }
 constexpr size_t WARP_FRONT_BYTES = 40 * 1024; // k_factor_warp: per warp (packed lower triangle)  // levels whose fronts all have <= this many pivots stay fused
@@ -2267,6 +2264,15 @@ int env_int(const char* name, int dflt) {
     return e ? atoi(e) : dflt;
 }
 
+// k_factor_warp CTA: up to 8 warps share this much dynamic shared memory (real
+// fronts: three CTAs per SM at 80 registers; complex: two at 125); tunable for sweeps
+inline size_t warp_cta_bytes(size_t tsz) {
+    const int kb = env_int(tsz == 8 ? "PGCP_DIRECT_WCTA_KB" : "PGCP_DIRECT_WCTA_KB_C", tsz == 8 ? 75 : 112);
+    return (size_t)std::max(40, std::min(kb, 220)) * 1024;  // at least one WARP_FRONT_BYTES front
+}
+// warps (= fronts) per k_factor_warp CTA
+inline int warp_cta_warps() { return std::max(1, std::min(8, env_int("PGCP_DIRECT_WCTA_W", 8))); }
+
 // PGCP_DIRECT_TIMING=1: CUDA-event split of the phases (and the host time
 // between the marks), printed to stderr
 struct PhaseTimer {
@@ -2549,13 +2555,13 @@ int factor_level(DirectFactor* D, FacArgs fa, int l, int type, cudaStream_t s) {
         const int wbk = env_int("PGCP_DIRECT_WB", 8);
         if (wbk == 4) {
             PGCP_TRY(set_smem(k_factor_warp<T, 4>, cta));
-            k_factor_warp<T, 4><<<ng, 256, cta, s>>>(fw, D->gstart.p + g0, D->wsoff.p);
+            k_factor_warp<T, 4><<<ng, 32 * warp_cta_warps(), cta, s>>>(fw, D->gstart.p + g0, D->wsoff.p);
         } else if (wbk == 8) {
             PGCP_TRY(set_smem(k_factor_warp<T, 8>, cta));
-            k_factor_warp<T, 8><<<ng, 256, cta, s>>>(fw, D->gstart.p + g0, D->wsoff.p);
+            k_factor_warp<T, 8><<<ng, 32 * warp_cta_warps(), cta, s>>>(fw, D->gstart.p + g0, D->wsoff.p);
         } else {
             PGCP_TRY(set_smem(k_factor_warp<T, 16>, cta));
-            k_factor_warp<T, 16><<<ng, 256, cta, s>>>(fw, D->gstart.p + g0, D->wsoff.p);
+            k_factor_warp<T, 16><<<ng, 32 * warp_cta_warps(), cta, s>>>(fw, D->gstart.p + g0, D->wsoff.p);
         }
         PGCP_LAUNCH_CHECK();
     }
@@ -3045,11 +3051,12 @@ int direct_factor(pgcp_batch* b, const DirectInput& in, DirectFactor** out, cuda
             D->grp_off[q] = (int64_t)D->h_gstart.size();
             if (w0 < o1) {
                 const size_t cap = warp_cta_bytes(tsz);
+                const int maxw = warp_cta_warps();
                 size_t used = cap + 1;  // forces a new group at the first front
                 int cnt = 0;
                 for (int64_t i = w0; i < o1; ++i) {
                     const size_t wb = wbytes(hl[i]);
-                    if (cnt == 8 || used + wb > cap) {
+                    if (cnt == maxw || used + wb > cap) {
                         D->h_gstart.push_back((int32_t)i);
                         used = 0;
                         cnt = 0;
