@@ -174,3 +174,20 @@ def test_cut_file_round_trip(tmp_path):
     p.write_text("1 2 3\n")
     with pytest.raises(PartitionError, match="expected two vertex ids"):
         read_cut_edges(p)
+
+
+def test_validate_cuts_normalises_and_rejects_duplicates():
+    """partition.py:48-59: every pair sorted, order kept, duplicates (in either
+    orientation) rejected with the reference's message; empty input allowed."""
+    from paper_1903_12359_b200.errors import PartitionError
+    from paper_1903_12359_b200.partition import validate_cuts
+    rng = np.random.default_rng(3)
+    a = rng.permutation(5000)[:2000].reshape(-1, 2).astype(np.int64)
+    norm = validate_cuts(None, a)
+    assert np.array_equal(norm, np.sort(a, axis=1))
+    assert norm.dtype == np.int64 and norm.flags.c_contiguous
+    assert validate_cuts(None, np.zeros((0, 2), np.int64)).shape == (0, 2)
+    assert np.array_equal(validate_cuts(None, [[7, 3]]), [[3, 7]])
+    dup = np.vstack([a, a[17][::-1]])
+    with pytest.raises(PartitionError, match="duplicate cut edges"):
+        validate_cuts(None, dup)
