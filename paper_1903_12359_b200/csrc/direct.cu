@@ -982,10 +982,16 @@ __device__ __forceinline__ void diag_factor_cta(T* Ld, int nb, int* bad) {
         __syncthreads();
         for (int i = k + 1 + threadIdx.x; i < nb; i += NTH) Ld[i + k * LDB] = scale(Ld[i + k * LDB], sinv);
         __syncthreads();
-        const int m = nb - k - 1;
-        for (int t = threadIdx.x; t < m * m; t += NTH) {
-            const int j = k + 1 + t / m, i = k + 1 + t % m;
-            if (i >= j) fma_cj(Ld[i + j * LDB], scale(Ld[i + k * LDB], -1.0), Ld[j + k * LDB]);
+        {   // trailing update: lane = row, the warps stride over the columns (no
+            // index divisions, conflict-free rows, broadcast l_jk); each entry
+            // takes the same one multiply-add per k as before
+            static_assert(LDB <= 32, "one lane per row of the block");
+            const int i = k + 1 + (int)(threadIdx.x & 31);
+            if (i < nb) {
+                const T lik = scale(Ld[i + k * LDB], -1.0);
+                for (int j = k + 1 + (int)(threadIdx.x >> 5); j <= i; j += NTH / 32)
+                    fma_cj(Ld[i + j * LDB], lik, Ld[j + k * LDB]);
+            }
         }
         __syncthreads();
     }
